@@ -1,0 +1,102 @@
+"""ctypes binding of libringpipe_b200.so (include/ringpipe_b200.h).
+
+Loading is strict: there is no CPU fallback.  If the library is missing or
+was built for another architecture, importing the product path raises.
+"""
+
+import ctypes
+import os
+
+from .errors import raise_for_status
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libringpipe_b200.so")
+_lib = None
+
+# rp_dtype / rp_math / rp_epilogue (include/ringpipe_b200.h)
+F32, BF16 = 0, 1
+MATH_BF16, MATH_TF32, MATH_TF32X3 = 0, 1, 2
+EPI_STORE, EPI_BIAS_RELU, EPI_BIAS_DROPOUT_RESIDUAL, EPI_LSE_PARTIAL, EPI_CE_GRAD = range(5)
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("math", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
+        ("a_mn_major", ctypes.c_int32),
+        ("b_mn_major", ctypes.c_int32),
+        ("M", ctypes.c_int64),
+        ("N", ctypes.c_int64),
+        ("K", ctypes.c_int64),
+        ("batch", ctypes.c_int64),
+        ("A", ctypes.c_void_p),
+        ("A_lo", ctypes.c_void_p),
+        ("lda", ctypes.c_int64),
+        ("stride_a", ctypes.c_int64),
+        ("B", ctypes.c_void_p),
+        ("B_lo", ctypes.c_void_p),
+        ("ldb", ctypes.c_int64),
+        ("stride_b", ctypes.c_int64),
+        ("C", ctypes.c_void_p),
+        ("ldc", ctypes.c_int64),
+        ("stride_c", ctypes.c_int64),
+        ("epilogue", ctypes.c_int32),
+        ("tile_n", ctypes.c_int32),
+        ("alpha", ctypes.c_float),
+        ("bias", ctypes.c_void_p),
+        ("residual", ctypes.c_void_p),
+        ("ld_residual", ctypes.c_int64),
+        ("stride_residual", ctypes.c_int64),
+        ("drop_enabled", ctypes.c_int32),
+        ("drop_scale", ctypes.c_float),
+        ("drop_seed", ctypes.c_uint64),
+        ("drop_threshold", ctypes.c_uint64),
+        ("drop_pos0", ctypes.c_uint64),
+        ("targets", ctypes.c_void_p),
+        ("lse", ctypes.c_void_p),
+        ("partial", ctypes.c_void_p),
+        ("target_logit", ctypes.c_void_p),
+        ("ce_scale", ctypes.c_float),
+    ]
+
+
+def lib():
+    """The loaded library; raises ImportError when it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(
+                f"{_LIB_PATH} not built; run `python -m paper_1909_06695_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        _lib = ctypes.CDLL(_LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+def _declare(L):
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    L.rp_version.restype = ctypes.c_char_p
+    L.rp_last_error.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+    L.rp_gemm.argtypes = [ctypes.POINTER(GemmArgs), vp]
+    L.rp_gemm_tile_n.argtypes = [i64]
+    L.rp_tf32_split.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp]
+
+
+def last_error():
+    buf = ctypes.create_string_buffer(1024)
+    lib().rp_last_error(buf, 1024)
+    return buf.value.decode(errors="replace")
+
+
+def check(status, what=""):
+    if status != 0:
+        raise_for_status(status, f"{what}: {last_error()}")
+
+
+def exported_symbols():
+    """Names declared in include/ringpipe_b200.h (for the load/export test)."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "ringpipe_b200.h")
+    text = open(hdr).read()
+    return sorted(set(re.findall(r"\b(rp_[a-z0-9_]+)\s*\(", text)))

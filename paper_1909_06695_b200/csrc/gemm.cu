@@ -1,0 +1,530 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+// Replaces the reference's fixed-order fp64 contractions `kernels.mm` /
+// `kernels.bmm` (reference pkg/src/ringpipe/kernels.py:23-48, 68-81) for every
+// dense contraction of the block (layers.py:176-195, 218-247) and the tied head
+// (layers.py:269, 310-321).
+//
+//   C[b](M x N) = epilogue( alpha * A[b](M x K) * B[b](K x N) )
+//
+// A is K-major ([M,K] row-major) or MN-major ([K,M] row-major); B is K-major
+// ([N,K] row-major) or MN-major ([K,N] row-major).  Operands are staged by TMA
+// into 128B-swizzled shared memory, one elected thread issues tcgen05.mma into
+// a double-buffered TMEM accumulator, and four epilogue warps drain TMEM with
+// tcgen05.ld and apply the fused epilogue (bias/ReLU, bias/dropout/residual,
+// logsumexp partials for the tied-vocab cross-entropy, or the softmax-CE
+// gradient dz).  "tf32x3" runs three accumulation passes (hi*hi + hi*lo +
+// lo*hi) over pre-split operands to reach fp32 accuracy on the tf32 pipe.
+#include <algorithm>
+#include <mutex>
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "rp_internal.h"
+
+namespace rp {
+
+template <bool kTf32, int BN_>
+struct GemmCfg {
+  static constexpr int BM = 128;
+  static constexpr int BN = BN_;
+  static constexpr int ELEM = kTf32 ? 4 : 2;
+  static constexpr int BK = 128 / ELEM;     // one 128-byte swizzle row of K
+  static constexpr int UK = kTf32 ? 8 : 16;  // K per tcgen05.mma
+  static constexpr int CHUNK = 128 / ELEM;  // MN elements per 128B chunk (MN-major)
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct GemmParams {
+  int M, N, K, batch;
+  int a_mn, b_mn, passes;
+  int m_tiles, n_tiles, num_tiles, kb_per_pass;
+  int out_bf16, epi;
+  float alpha;
+  void* C;
+  int64_t ldc, stride_c;
+  const float* bias;
+  const void* resid;
+  int64_t ld_resid, stride_resid;
+  uint64_t drop_seed, drop_thr, drop_pos0;
+  float drop_scale;
+  int drop_on;
+  const int64_t* targets;
+  const float* lse;
+  float* partial;
+  float* target_logit;
+  float ce_scale;
+  int vec_ok;
+};
+
+__device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int n0, int b,
+                                            const float (&v)[32]) {
+  const int64_t base = (int64_t)b * p.stride_c + m * p.ldc + n0;
+  if (p.vec_ok && n0 + 32 <= p.N) {
+    if (p.out_bf16) {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.C) + base);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 t = __floats2bfloat162_rn(v[q * 8 + 2 * h], v[q * 8 + 2 * h + 1]);
+          w[h] = *reinterpret_cast<uint32_t*>(&t);
+        }
+        dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    } else {
+      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.C) + base);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (n0 + j < p.N) {
+        if (p.out_bf16)
+          reinterpret_cast<__nv_bfloat16*>(p.C)[base + j] = __float2bfloat16_rn(v[j]);
+        else
+          reinterpret_cast<float*>(p.C)[base + j] = v[j];
+      }
+    }
+  }
+}
+
+template <bool kTf32, int BN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA_lo,
+                const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB_lo,
+                const GemmParams p) {
+  using Cfg = GemmCfg<kTf32, BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tmem_full = empty + Cfg::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    if (p.passes > 1) {
+      tma_prefetch(&mapA_lo);
+      tma_prefetch(&mapB_lo);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mb = tile % p.m_tiles;
+        const int rest = tile / p.m_tiles;
+        const int nb = rest % p.n_tiles;
+        const int b = rest / p.n_tiles;
+        const int m0 = mb * Cfg::BM, n0 = nb * BN;
+        for (int pass = 0; pass < p.passes; ++pass) {
+          const CUtensorMap* ma = (pass == 2) ? &mapA_lo : &mapA;
+          const CUtensorMap* mbm = (pass == 1) ? &mapB_lo : &mapB;
+          for (int kb = 0; kb < p.kb_per_pass; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+            uint8_t* sb = sa + Cfg::A_BYTES;
+            const int k0 = kb * Cfg::BK;
+            if (!p.a_mn) {
+              tma_load_3d(sa, ma, &full[stage], k0, m0, b);
+            } else {
+#pragma unroll
+              for (int c = 0; c < Cfg::BM / Cfg::CHUNK; ++c)
+                tma_load_3d(sa + c * (Cfg::BK * 128), ma, &full[stage], m0 + c * Cfg::CHUNK, k0, b);
+            }
+            if (!p.b_mn) {
+              tma_load_3d(sb, mbm, &full[stage], k0, n0, b);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / Cfg::CHUNK; ++c)
+                tma_load_3d(sb + c * (Cfg::BK * 128), mbm, &full[stage], n0 + c * Cfg::CHUNK, k0, b);
+            }
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread) ----------------
+      const uint32_t idesc = umma_idesc(kTf32, p.a_mn, p.b_mn, Cfg::BM, BN);
+      const uint32_t a_lbo = p.a_mn ? Cfg::BK * 128 : 16;
+      const uint32_t b_lbo = p.b_mn ? Cfg::BK * 128 : 16;
+      const uint32_t a_step = p.a_mn ? Cfg::UK * 128 : 32;
+      const uint32_t b_step = p.b_mn ? Cfg::UK * 128 : 32;
+      // tf32 MN-major tiles are 128B-swizzled with 32B atoms (4 K-rows per atom)
+      const uint32_t a_lay = (kTf32 && p.a_mn) ? 1u : 2u, b_lay = (kTf32 && p.b_mn) ? 1u : 2u;
+      const uint32_t a_sbo = (kTf32 && p.a_mn) ? 512u : 1024u, b_sbo = (kTf32 && p.b_mn) ? 512u : 1024u;
+      uint32_t stage = 0, phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int pass = 0; pass < p.passes; ++pass) {
+          for (int kb = 0; kb < p.kb_per_pass; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint64_t ad = umma_desc(sa + k * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, b_sbo, b_lay);
+              tc_mma<kTf32>(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
+            }
+            tc_commit(&empty[stage]);
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+        tc_commit(&tmem_full[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps ----------------
+    const int e = warp - 4;  // TMEM lane quarter
+    int local = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+      const int mb = tile % p.m_tiles;
+      const int rest = tile / p.m_tiles;
+      const int nb = rest % p.n_tiles;
+      const int b = rest / p.n_tiles;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int64_t m = (int64_t)mb * Cfg::BM + e * 32 + lane;
+      const bool row_ok = m < p.M;
+      const int64_t grow = (int64_t)b * p.M + m;  // row index over the folded batch
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(e * 32) << 16);
+
+      float run_max = -INFINITY, run_sum = 0.f;
+      int64_t tgt = -1;
+      float lse_row = 0.f;
+      if (row_ok && (p.epi == RP_EPI_LSE_PARTIAL || p.epi == RP_EPI_CE_GRAD)) {
+        tgt = p.targets[grow];
+        if (p.epi == RP_EPI_CE_GRAD) lse_row = p.lse[grow];
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int n0 = nb * BN + c * 32;
+        uint32_t r[32];
+        tmem_ld32(t_row + c * 32, r);
+        if (!row_ok || n0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+        switch (p.epi) {
+          case RP_EPI_STORE:
+            store_chunk(p, m, n0, b, v);
+            break;
+          case RP_EPI_BIAS_RELU: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float t = v[j] + ((p.bias && n0 + j < p.N) ? p.bias[n0 + j] : 0.f);
+              v[j] = fmaxf(t, 0.f);
+            }
+            store_chunk(p, m, n0, b, v);
+            break;
+          }
+          case RP_EPI_BIAS_DROPOUT_RESIDUAL: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = n0 + j;
+              if (n < p.N) {
+                float t = v[j] + (p.bias ? p.bias[n] : 0.f);
+                if (p.drop_on) {
+                  const uint64_t pos = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n;
+                  t = dropout_keep(p.drop_seed, pos, p.drop_thr) ? t * p.drop_scale : 0.f;
+                }
+                if (p.resid) {
+                  const int64_t ri = (int64_t)b * p.stride_resid + m * p.ld_resid + n;
+                  t += p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.resid)[ri])
+                                  : reinterpret_cast<const float*>(p.resid)[ri];
+                }
+                v[j] = t;
+              }
+            }
+            store_chunk(p, m, n0, b, v);
+            break;
+          }
+          case RP_EPI_LSE_PARTIAL: {
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < p.N) cmax = fmaxf(cmax, v[j]);
+            const float nmax = fmaxf(run_max, cmax);
+            float s = run_sum * __expf(run_max - nmax);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (n0 + j < p.N) s += __expf(v[j] - nmax);
+            run_max = nmax;
+            run_sum = s;
+            if (tgt >= n0 && tgt < n0 + 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (tgt == n0 + j) p.target_logit[grow] = v[j];
+            }
+            break;
+          }
+          case RP_EPI_CE_GRAD: {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float pr = __expf(v[j] - lse_row);
+              v[j] = (pr - ((tgt == n0 + j) ? 1.f : 0.f)) * p.ce_scale;
+            }
+            store_chunk(p, m, n0, b, v);
+            break;
+          }
+          default:
+            break;
+        }
+      }
+      if (row_ok && p.epi == RP_EPI_LSE_PARTIAL) {
+        float* dst = p.partial + (grow * p.n_tiles + nb) * 2;
+        dst[0] = run_max;
+        dst[1] = run_sum;
+      }
+      tc_fence_before();
+      mbar_arrive(&tmem_empty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 -> (hi, lo) split for the 3-pass tf32 path.  Both halves are rounded to
+// nearest tf32 here, so the tensor core consumes them exactly whatever its own
+// fp32->tf32 conversion does; the residual |x - hi - lo| <= 2^-24 |x| is
+// unbiased (truncating lo instead leaves a bias that grows like sqrt(K)).
+__device__ __forceinline__ float round_tf32(float v) {
+  uint32_t b = __float_as_uint(v);
+  if ((b & 0x7F800000u) == 0x7F800000u) return v;  // inf / nan unchanged
+  b += 0x0FFFu + ((b >> 13) & 1u);
+  return __uint_as_float(b & 0xFFFFE000u);
+}
+
+__global__ void tf32_split_kernel(const float* __restrict__ x, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t rows, int64_t cols, int64_t ld_src,
+                                  int64_t ld_dst) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const float v = x[r * ld_src + c];
+    const float h = round_tf32(v);
+    hi[r * ld_dst + c] = h;
+    lo[r * ld_dst + c] = round_tf32(v - h);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+// rows x inner matrix (inner contiguous), `batch` copies at `bstride` elements.
+int make_map(CUtensorMap* map, const void* ptr, bool tf32, int64_t inner, int64_t rows, int64_t ld,
+             int64_t batch, int64_t bstride, int box_inner, int box_rows, bool mn_major) {
+  auto enc = encoder();
+  if (!enc) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int e = tf32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0)
+    return set_error(RP_ERR_DIMENSION, "GEMM operand base must be 16-byte aligned");
+  if ((ld * e) % 16 != 0) return set_error(RP_ERR_DIMENSION, "GEMM leading dimension must be a multiple of 16 bytes");
+  if (batch <= 1) bstride = ld * std::max<int64_t>(rows, 1);
+  if ((bstride * e) % 16 != 0) return set_error(RP_ERR_DIMENSION, "GEMM batch stride must be a multiple of 16 bytes");
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)std::max<int64_t>(batch, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * e), (cuuint64_t)(bstride * e)};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RP_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool kTf32, int BN>
+int launch(const rp_gemm_args& a, cudaStream_t stream) {
+  using Cfg = GemmCfg<kTf32, BN>;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_kernel<kTf32, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  });
+  CUtensorMap ma, mal, mb, mbl;
+  const int64_t batch = std::max<int64_t>(a.batch, 1);
+  int st;
+  // A: K-major -> inner K, rows M ; MN-major -> inner M, rows K
+  if (!a.a_mn_major)
+    st = make_map(&ma, a.A, kTf32, a.K, a.M, a.lda, batch, a.stride_a, Cfg::BK, Cfg::BM, false);
+  else
+    st = make_map(&ma, a.A, kTf32, a.M, a.K, a.lda, batch, a.stride_a, Cfg::CHUNK, Cfg::BK, true);
+  if (st) return st;
+  if (!a.b_mn_major)
+    st = make_map(&mb, a.B, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, BN, false);
+  else
+    st = make_map(&mb, a.B, kTf32, a.N, a.K, a.ldb, batch, a.stride_b, Cfg::CHUNK, Cfg::BK, true);
+  if (st) return st;
+  int passes = 1;
+  mal = ma;
+  mbl = mb;
+  if (a.math == RP_MATH_TF32X3) {
+    if (!a.A_lo || !a.B_lo) return set_error(RP_ERR_INVALID, "tf32x3 GEMM needs split operands A_lo/B_lo");
+    passes = 3;
+    if (!a.a_mn_major)
+      st = make_map(&mal, a.A_lo, kTf32, a.K, a.M, a.lda, batch, a.stride_a, Cfg::BK, Cfg::BM, false);
+    else
+      st = make_map(&mal, a.A_lo, kTf32, a.M, a.K, a.lda, batch, a.stride_a, Cfg::CHUNK, Cfg::BK, true);
+    if (st) return st;
+    if (!a.b_mn_major)
+      st = make_map(&mbl, a.B_lo, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, BN, false);
+    else
+      st = make_map(&mbl, a.B_lo, kTf32, a.N, a.K, a.ldb, batch, a.stride_b, Cfg::CHUNK, Cfg::BK, true);
+    if (st) return st;
+  }
+  GemmParams p{};
+  p.M = (int)a.M;
+  p.N = (int)a.N;
+  p.K = (int)a.K;
+  p.batch = (int)batch;
+  p.a_mn = a.a_mn_major;
+  p.b_mn = a.b_mn_major;
+  p.passes = passes;
+  p.m_tiles = (int)((a.M + Cfg::BM - 1) / Cfg::BM);
+  p.n_tiles = (int)((a.N + BN - 1) / BN);
+  p.num_tiles = p.m_tiles * p.n_tiles * p.batch;
+  p.kb_per_pass = (int)((a.K + Cfg::BK - 1) / Cfg::BK);
+  p.out_bf16 = a.out_dtype == RP_BF16;
+  p.epi = a.epilogue;
+  p.alpha = a.alpha;
+  p.C = a.C;
+  p.ldc = a.ldc;
+  p.stride_c = a.stride_c;
+  p.bias = a.bias;
+  p.resid = a.residual;
+  p.ld_resid = a.ld_residual;
+  p.stride_resid = a.stride_residual;
+  p.drop_seed = a.drop_seed;
+  p.drop_thr = a.drop_threshold;
+  p.drop_pos0 = a.drop_pos0;
+  p.drop_scale = a.drop_scale;
+  p.drop_on = a.drop_enabled;
+  p.targets = a.targets;
+  p.lse = a.lse;
+  p.partial = a.partial;
+  p.target_logit = a.target_logit;
+  p.ce_scale = a.ce_scale;
+  const int oe = p.out_bf16 ? 2 : 4;
+  p.vec_ok = ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) && ((a.ldc * oe) % 16 == 0) &&
+             ((a.stride_c * oe) % 16 == 0 || batch == 1);
+  if (p.num_tiles == 0) return RP_OK;
+  const int grid = std::min(p.num_tiles, num_sms());
+  gemm_kernel<kTf32, BN><<<grid, 256, Cfg::SMEM_BYTES, stream>>>(ma, mal, mb, mbl, p);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_error(RP_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(err));
+  return RP_OK;
+}
+
+}  // namespace
+
+int gemm_tile_n(int64_t N) { return N > 128 ? 256 : (N > 64 ? 128 : 64); }
+
+int gemm(const rp_gemm_args& a, cudaStream_t stream) {
+  if (a.M < 0 || a.N < 0 || a.K <= 0) return set_error(RP_ERR_DIMENSION, "bad GEMM shape");
+  if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return set_error(RP_ERR_DIMENSION, "GEMM dim too large");
+  const bool tf32 = a.math != RP_MATH_BF16;
+  const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.N);
+  if (tf32) {
+    if (bn == 256) return launch<true, 256>(a, stream);
+    if (bn == 128) return launch<true, 128>(a, stream);
+    return launch<true, 64>(a, stream);
+  }
+  if (bn == 256) return launch<false, 256>(a, stream);
+  if (bn == 128) return launch<false, 128>(a, stream);
+  return launch<false, 64>(a, stream);
+}
+
+int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
+               cudaStream_t stream) {
+  const int64_t n = rows * cols;
+  if (n == 0) return RP_OK;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+  tf32_split_kernel<<<(int)blocks, threads, 0, stream>>>(x, hi, lo, rows, cols, ld_src, ld_dst);
+  return check_launch("tf32_split");
+}
+
+}  // namespace rp
