@@ -50,7 +50,8 @@ typedef enum rp_epilogue {
   RP_EPI_BIAS_RELU = 1,             /* C = relu(alpha*AB + bias)        layers.py:190-191 */
   RP_EPI_BIAS_DROPOUT_RESIDUAL = 2, /* C = resid + (alpha*AB+bias)*mask layers.py:184-187,192-195 */
   RP_EPI_LSE_PARTIAL = 3,           /* per-(row, N-tile) (max, sumexp) + target logit  layers.py:310-316 */
-  RP_EPI_CE_GRAD = 4                /* C = (exp(AB - lse[row]) - onehot) * ce_scale    layers.py:317-319 */
+  RP_EPI_CE_GRAD = 4,               /* C = (exp(AB - lse[row]) - onehot) * ce_scale    layers.py:317-319 */
+  RP_EPI_RELU_GRAD = 5              /* C = alpha*AB * (residual > 0)                   layers.py:221 */
 } rp_epilogue;
 
 /* C[b] = epilogue(alpha * opA(A[b]) * opB(B[b])).
@@ -95,6 +96,74 @@ int rp_gemm(const rp_gemm_args* args, void* stream);
 int rp_gemm_tile_n(int64_t N);
 int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src,
                   int64_t ld_dst, void* stream);
+
+
+/* Device status word bits, OR-ed by kernels (a device int32 owned by the caller);
+ * the host polls it once per step and raises the matching reference exception. */
+#define RP_FLAG_NONFINITE 1 /* NonFiniteError: check_finite, tensor.py:93-96 / optim.py:47-49 */
+#define RP_FLAG_DIMENSION 2 /* DimensionError: token/target range, layers.py:116-117, 292-293 */
+
+/* ---- LayerNorm (layers.py:62-79) ----------------------------------------- */
+/* y = (x-mu)*rstd*g + b over rows of d; saves mean/rstd (fp32). dtype: rp_dtype of x/y;
+ * gain/bias are fp32. */
+int rp_layernorm_fwd(int32_t dtype, const void* x, const float* gain, const float* bias, void* y, float* mean,
+                     float* rstd, int64_t rows, int64_t d, int32_t* flag, void* stream);
+/* dx = LN-backward(dy) + resid_grad (fp32); dx_masked = dx*dropout-mask (dtype) if non-NULL;
+ * writes rp_layernorm_bwd_blocks(rows) partial rows of dgain/dbias. */
+int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
+                     const float* gain, const float* resid_grad, float* dx, void* dx_masked, uint64_t seed,
+                     uint64_t threshold, float scale, int32_t drop_enabled, float* partial_gain,
+                     float* partial_bias, int64_t rows, int64_t d, void* stream);
+int rp_layernorm_bwd_blocks(int64_t rows);
+
+/* ---- deterministic column sums (bias/gain gradients, layers.py:72-73,220,223) ---- */
+int rp_colsum_blocks(int64_t rows);
+int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* partial,
+                      void* stream);
+int rp_colsum_finish(const float* partial, int32_t nblocks, int64_t cols, float* out, void* stream);
+/* out = g * mask(seed, pos0 + r*d + j) (dtype), partial column sums of the masked values
+ * (layers.py:209-220). */
+int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
+                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream);
+
+/* ---- causal single-head attention softmax (layers.py:180-183, 237) ---------- */
+/* rows = B*T rows of length T, row stride ld (>= T) */
+int rp_softmax_causal(int32_t dtype, const float* scores, void* probs, int64_t rows, int64_t T, int64_t ld,
+                      void* stream);
+/* g_s = (g_p - rowsum(g_p*P)) * P * scale */
+int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, void* grad_scores, float scale,
+                   int64_t rows, int64_t T, int64_t ld, void* stream);
+
+/* ---- embedding (layers.py:114-136) ---------------------------------------- */
+int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
+                 int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
+                 int32_t drop_enabled, int32_t* flag, void* stream);
+/* grad_pos [Tmax,d] (fully written); emb[tok] += beta * sum of masked rows (deterministic,
+ * sorted scatter).  work: rp_embed_bwd_workspace(B*T) uint64 words. */
+int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
+                 uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
+                 float* emb_grad, float beta, uint64_t* work, void* stream);
+int64_t rp_embed_bwd_workspace(int64_t n_tokens);
+
+/* ---- tied-head cross-entropy finish (layers.py:287-296, 310-316) ------------ */
+int rp_ce_finish(const float* partial, int32_t ntiles, const float* target_logit, const int64_t* targets,
+                 int64_t vocab, int64_t rows, float* lse, float* loss_rows, float* loss, double* loss64,
+                 int32_t* flag, void* stream);
+
+/* ---- optimizers over flat fp32 master buffers (optim.py:52-126) ------------- */
+/* copy (compute dtype) receives the updated weights: the next snapshot-ring slot. */
+int rp_adam_step(float* w, const float* g, float* m, float* v, void* copy, int32_t copy_dtype, int64_t n, float lr,
+                 float beta1, float beta2, float eps, float bias_corr1, float bias_corr2, int32_t* flag,
+                 void* stream);
+int rp_sgd_step(float* w, const float* g, void* copy, int32_t copy_dtype, int64_t n, float lr, int32_t* flag,
+                void* stream);
+
+/* ---- misc ----------------------------------------------------------------- */
+/* uniform_signed init from the reference stream (tensor.py:72-74), fp64 math, fp32 out */
+int rp_init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, void* stream);
+int rp_cast(const void* in, int32_t in_dtype, void* out, int32_t out_dtype, int64_t n, void* stream);
+/* out (+)= sum x^2 in fp64; part: >= 296 doubles of scratch (engine.py:72-80) */
+int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t accumulate, void* stream);
 
 #ifdef __cplusplus
 }

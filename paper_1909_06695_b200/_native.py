@@ -15,7 +15,8 @@ _lib = None
 # rp_dtype / rp_math / rp_epilogue (include/ringpipe_b200.h)
 F32, BF16 = 0, 1
 MATH_BF16, MATH_TF32, MATH_TF32X3 = 0, 1, 2
-EPI_STORE, EPI_BIAS_RELU, EPI_BIAS_DROPOUT_RESIDUAL, EPI_LSE_PARTIAL, EPI_CE_GRAD = range(5)
+EPI_STORE, EPI_BIAS_RELU, EPI_BIAS_DROPOUT_RESIDUAL, EPI_LSE_PARTIAL, EPI_CE_GRAD, EPI_RELU_GRAD = range(6)
+FLAG_NONFINITE, FLAG_DIMENSION = 1, 2
 
 
 class GemmArgs(ctypes.Structure):
@@ -74,12 +75,38 @@ def lib():
 
 
 def _declare(L):
-    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+    f32, f64 = ctypes.c_float, ctypes.c_double
+    sig = {
+        "rp_last_error": [ctypes.c_char_p, ctypes.c_size_t],
+        "rp_gemm": [ctypes.POINTER(GemmArgs), vp],
+        "rp_gemm_tile_n": [i64],
+        "rp_tf32_split": [vp, vp, vp, i64, i64, i64, i64, vp],
+        "rp_layernorm_fwd": [i32, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp],
+        "rp_layernorm_bwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, u64, u64, f32, i32, vp, vp, i64, i64, vp],
+        "rp_layernorm_bwd_blocks": [i64],
+        "rp_colsum_blocks": [i64],
+        "rp_colsum_partial": [i32, vp, i64, i64, i64, vp, vp],
+        "rp_colsum_finish": [vp, i32, i64, vp, vp],
+        "rp_mask_grad": [i32, vp, vp, i64, i64, u64, u64, u64, f32, i32, vp, vp],
+        "rp_softmax_causal": [i32, vp, vp, i64, i64, i64, vp],
+        "rp_softmax_bwd": [i32, vp, vp, vp, f32, i64, i64, i64, vp],
+        "rp_embed_fwd": [i32, vp, vp, vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp],
+        "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, vp],
+        "rp_embed_bwd_workspace": [i64],
+        "rp_ce_finish": [vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp],
+        "rp_adam_step": [vp, vp, vp, vp, vp, i32, i64, f32, f32, f32, f32, f32, f32, vp, vp],
+        "rp_sgd_step": [vp, vp, vp, i32, i64, f32, vp, vp],
+        "rp_init_uniform": [vp, i64, u64, u64, f64, vp],
+        "rp_cast": [vp, i32, vp, i32, i64, vp],
+        "rp_sq_norm": [vp, i64, vp, vp, i32, vp],
+    }
     L.rp_version.restype = ctypes.c_char_p
-    L.rp_last_error.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
-    L.rp_gemm.argtypes = [ctypes.POINTER(GemmArgs), vp]
-    L.rp_gemm_tile_n.argtypes = [i64]
-    L.rp_tf32_split.argtypes = [vp, vp, vp, i64, i64, i64, i64, vp]
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int32
+    L.rp_embed_bwd_workspace.restype = i64
 
 
 def last_error():

@@ -49,4 +49,77 @@ int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t co
   return rp::tf32_split(x, hi, lo, rows, cols, ld_src, ld_dst, static_cast<cudaStream_t>(stream));
 }
 
+#define RP_S(s) static_cast<cudaStream_t>(s)
+
+int rp_layernorm_fwd(int32_t dtype, const void* x, const float* gain, const float* bias, void* y, float* mean,
+                     float* rstd, int64_t rows, int64_t d, int32_t* flag, void* stream) {
+  return rp::layernorm_fwd(dtype, x, gain, bias, y, mean, rstd, rows, d, flag, RP_S(stream));
+}
+int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
+                     const float* gain, const float* resid_grad, float* dx, void* dx_masked, uint64_t seed,
+                     uint64_t threshold, float scale, int32_t drop_enabled, float* partial_gain,
+                     float* partial_bias, int64_t rows, int64_t d, void* stream) {
+  return rp::layernorm_bwd(dtype, dy, x, mean, rstd, gain, resid_grad, dx, dx_masked, seed, threshold, scale,
+                           drop_enabled, partial_gain, partial_bias, rows, d, RP_S(stream));
+}
+int rp_layernorm_bwd_blocks(int64_t rows) { return rp::ln_bwd_blocks(rows); }
+int rp_colsum_blocks(int64_t rows) { return rp::colsum_blocks(rows); }
+int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* partial,
+                      void* stream) {
+  return rp::colsum_partial(dtype, x, rows, cols, ld, partial, RP_S(stream));
+}
+int rp_colsum_finish(const float* partial, int32_t nblocks, int64_t cols, float* out, void* stream) {
+  return rp::colsum_finish(partial, nblocks, cols, out, RP_S(stream));
+}
+int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
+                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream) {
+  return rp::mask_grad(dtype, g, out, rows, d, seed, pos0, threshold, scale, drop_enabled, partial, RP_S(stream));
+}
+int rp_softmax_causal(int32_t dtype, const float* scores, void* probs, int64_t rows, int64_t T, int64_t ld,
+                      void* stream) {
+  return rp::softmax_causal(dtype, scores, probs, rows, T, ld, RP_S(stream));
+}
+int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, void* grad_scores, float scale,
+                   int64_t rows, int64_t T, int64_t ld, void* stream) {
+  return rp::softmax_bwd(dtype, grad_probs, probs, grad_scores, scale, rows, T, ld, RP_S(stream));
+}
+int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
+                 int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
+                 int32_t drop_enabled, int32_t* flag, void* stream) {
+  return rp::embed_fwd(dtype, tokens, tied, pos, out, B, T, d, vocab, seed, threshold, scale, drop_enabled, flag,
+                       RP_S(stream));
+}
+int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
+                 uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
+                 float* emb_grad, float beta, uint64_t* work, void* stream) {
+  return rp::embed_bwd(grad, tokens, B, T, Tmax, d, seed, threshold, scale, drop_enabled, grad_pos, emb_grad, beta,
+                       work, RP_S(stream));
+}
+int64_t rp_embed_bwd_workspace(int64_t n_tokens) { return rp::embed_bwd_workspace(n_tokens); }
+int rp_ce_finish(const float* partial, int32_t ntiles, const float* target_logit, const int64_t* targets,
+                 int64_t vocab, int64_t rows, float* lse, float* loss_rows, float* loss, double* loss64,
+                 int32_t* flag, void* stream) {
+  return rp::ce_finish(partial, ntiles, target_logit, targets, vocab, rows, lse, loss_rows, loss, loss64, flag,
+                       RP_S(stream));
+}
+int rp_adam_step(float* w, const float* g, float* m, float* v, void* copy, int32_t copy_dtype, int64_t n, float lr,
+                 float beta1, float beta2, float eps, float bias_corr1, float bias_corr2, int32_t* flag,
+                 void* stream) {
+  return rp::adam_step(w, g, m, v, copy, copy_dtype, n, lr, beta1, beta2, eps, bias_corr1, bias_corr2, flag,
+                       RP_S(stream));
+}
+int rp_sgd_step(float* w, const float* g, void* copy, int32_t copy_dtype, int64_t n, float lr, int32_t* flag,
+                void* stream) {
+  return rp::sgd_step(w, g, copy, copy_dtype, n, lr, flag, RP_S(stream));
+}
+int rp_init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, void* stream) {
+  return rp::init_uniform(out, n, seed, pos0, scale, RP_S(stream));
+}
+int rp_cast(const void* in, int32_t in_dtype, void* out, int32_t out_dtype, int64_t n, void* stream) {
+  return rp::cast(in, in_dtype, out, out_dtype, n, RP_S(stream));
+}
+int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t accumulate, void* stream) {
+  return rp::sq_norm(x, n, part, out, accumulate, RP_S(stream));
+}
+
 }  // extern "C"

@@ -1,0 +1,222 @@
+// Token embedding gather/scatter (reference layers.py:114-136) and the
+// cross-entropy finish of the tied head (layers.py:287-296, 310-316).
+//
+// The input-side tied gradient is a scatter-add over token ids
+// (np.add.at, layers.py:135).  It is made deterministic without float
+// atomics: one CTA bitonic-sorts (token, position) keys in shared memory, then
+// one warp per run of equal tokens sums its rows in position order -- the
+// same order np.add.at visits them -- and adds beta * sum into the packet's
+// mixed embedding gradient (engine.py:54-69) whose output-side half the head
+// GEMM already wrote.
+#include <algorithm>
+
+#include "common.cuh"
+#include "rp_internal.h"
+
+namespace rp {
+
+// out[r, :] = (V[tok[r], :] + pos[r % T, :]) * mask(r*d + j)
+template <typename T>
+__global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const T* __restrict__ V, const T* __restrict__ pos,
+                                 T* __restrict__ out, int64_t rows, int Tn, int d, int64_t vocab, uint64_t seed,
+                                 uint64_t thr, float scale, int drop_on, int32_t* flag) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const int64_t id = tok[r];
+  const bool ok = id >= 0 && id < vocab;
+  if (!ok) {
+    if (threadIdx.x == 0 && flag) atomicOr(flag, RP_FLAG_DIMENSION);
+  }
+  const int t = (int)(r % Tn);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float v = (ok ? to_f(V[id * d + j]) : 0.f) + to_f(pos[(int64_t)t * d + j]);
+    if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
+    out[r * d + j] = from_f<T>(v);
+  }
+}
+
+// grad_pos[t, j] = sum_b g[b*T + t, j] * mask ; rows t >= T are zero.
+__global__ void embed_pos_grad_kernel(const float* __restrict__ g, float* __restrict__ gpos, int B, int Tn, int Tmax,
+                                      int d, uint64_t seed, uint64_t thr, float scale, int drop_on) {
+  const int t = blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float s = 0.f;
+    if (t < Tn) {
+      for (int b = 0; b < B; ++b) {
+        const int64_t r = (int64_t)b * Tn + t;
+        float v = g[r * d + j];
+        if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
+        s += v;
+      }
+    }
+    gpos[(int64_t)t * d + j] = s;
+  }
+}
+
+// Single-CTA bitonic sort of (token << 32 | position) keys.
+__global__ void __launch_bounds__(1024) token_sort_kernel(const int64_t* __restrict__ tok, int n, int npow2,
+                                                          uint64_t* __restrict__ sorted) {
+  extern __shared__ uint64_t keys[];
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x)
+    keys[i] = (i < n) ? ((static_cast<uint64_t>(tok[i]) << 32) | static_cast<uint32_t>(i)) : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= npow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const uint64_t a = keys[i], b = keys[ixj];
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sorted[i] = keys[i];
+}
+
+// One warp per sorted index; the warp that starts a run of equal tokens sums
+// the run's rows (in position order) and does emb[tok] += beta * sum.
+__global__ void embed_tied_grad_kernel(const uint64_t* __restrict__ sorted, int n, const float* __restrict__ g, int d,
+                                       uint64_t seed, uint64_t thr, float scale, int drop_on, float beta,
+                                       float* __restrict__ emb) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const uint32_t tokv = static_cast<uint32_t>(sorted[warp] >> 32);
+  if (warp > 0 && static_cast<uint32_t>(sorted[warp - 1] >> 32) == tokv) return;
+  int end = warp + 1;
+  while (end < n && static_cast<uint32_t>(sorted[end] >> 32) == tokv) ++end;
+  constexpr int C = 8;
+  for (int j0 = 0; j0 < d; j0 += 32 * C) {
+    float acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.f;
+    for (int q = warp; q < end; ++q) {
+      const int64_t r = static_cast<uint32_t>(sorted[q] & 0xffffffffu);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int j = j0 + lane + 32 * c;
+        if (j < d) {
+          float v = g[r * d + j];
+          if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
+          acc[c] += v;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int j = j0 + lane + 32 * c;
+      if (j < d) emb[(int64_t)tokv * d + j] += beta * acc[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cross-entropy finish: lse per row from the head GEMM's (max, sumexp)
+// partials, per-row loss lse - z_y, then a fixed-order mean.
+__global__ void ce_rows_kernel(const float* __restrict__ partial, int ntiles, const float* __restrict__ zy,
+                               const int64_t* __restrict__ tgt, int64_t vocab, int64_t rows, float* __restrict__ lse,
+                               float* __restrict__ loss_rows, int32_t* flag) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows) return;
+  const float* p = partial + m * ntiles * 2;
+  float mx = -INFINITY;
+  for (int t = 0; t < ntiles; ++t) mx = fmaxf(mx, p[2 * t]);
+  float s = 0.f;
+  for (int t = 0; t < ntiles; ++t) s += p[2 * t + 1] * __expf(p[2 * t] - mx);
+  const float l = mx + logf(s);
+  lse[m] = l;
+  loss_rows[m] = l - zy[m];
+  const int64_t y = tgt[m];
+  if (flag) {
+    if (y < 0 || y >= vocab) atomicOr(flag, RP_FLAG_DIMENSION);
+    if (!isfinite(l)) atomicOr(flag, RP_FLAG_NONFINITE);
+  }
+}
+
+__global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x, int64_t n, float* __restrict__ out,
+                                                    double* __restrict__ out64) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double mean = n ? red[0] / (double)n : 0.0;
+    if (out) *out = (float)mean;
+    if (out64) *out64 = mean;
+  }
+}
+
+// ---------------------------------------------------------------------------
+#define RP_DT(DT, ...)              \
+  if ((DT) == RP_BF16) {            \
+    using T = __nv_bfloat16;        \
+    __VA_ARGS__;                    \
+  } else {                          \
+    using T = float;                \
+    __VA_ARGS__;                    \
+  }
+
+int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, void* out, int64_t B, int64_t Tn,
+              int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
+              cudaStream_t st) {
+  const int64_t rows = B * Tn;
+  if (rows == 0) return RP_OK;
+  const int threads = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
+  RP_DT(dtype, embed_fwd_kernel<T><<<(unsigned)rows, threads, 0, st>>>(tok, (const T*)V, (const T*)pos, (T*)out,
+                                                                       rows, (int)Tn, (int)d, vocab, seed, thr,
+                                                                       scale, drop_on, flag));
+  return check_launch("embed_fwd");
+}
+
+int64_t embed_bwd_workspace(int64_t n_tokens) { return n_tokens; }  // uint64 words
+
+int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
+              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, uint64_t* work,
+              cudaStream_t st) {
+  const int64_t n = B * Tn;
+  const int threads = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
+  if (gpos) {
+    embed_pos_grad_kernel<<<(unsigned)Tmax, threads, 0, st>>>(g, gpos, (int)B, (int)Tn, (int)Tmax, (int)d, seed, thr,
+                                                              scale, drop_on);
+    if (int e = check_launch("embed_pos_grad")) return e;
+  }
+  if (!emb || n == 0) return RP_OK;
+  int npow2 = 1;
+  while (npow2 < n) npow2 <<= 1;
+  const size_t smem = (size_t)npow2 * sizeof(uint64_t);
+  if (smem > 227 * 1024) return set_error(RP_ERR_DIMENSION, "embed_bwd: %lld tokens exceed the in-CTA sort", (long long)n);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(token_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  token_sort_kernel<<<1, 1024, smem, st>>>(tok, (int)n, npow2, work);
+  if (int e = check_launch("token_sort")) return e;
+  const int64_t warps_per_block = 8;
+  embed_tied_grad_kernel<<<(unsigned)((n + warps_per_block - 1) / warps_per_block), 256, 0, st>>>(
+      work, (int)n, g, (int)d, seed, thr, scale, drop_on, beta, emb);
+  return check_launch("embed_tied_grad");
+}
+
+int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,
+              float* lse, float* loss_rows, float* loss, double* loss64, int32_t* flag, cudaStream_t st) {
+  if (rows == 0) return RP_OK;
+  ce_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(partial, ntiles, zy, tgt, vocab, rows, lse,
+                                                                  loss_rows, flag);
+  if (int e = check_launch("ce_rows")) return e;
+  mean_kernel<<<1, 1024, 0, st>>>(loss_rows, rows, loss, loss64);
+  return check_launch("ce_mean");
+}
+
+}  // namespace rp

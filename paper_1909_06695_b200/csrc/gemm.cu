@@ -308,6 +308,20 @@ __global__ void __launch_bounds__(256, 1)
             }
             break;
           }
+          case RP_EPI_RELU_GRAD: {
+            // out = acc * (aux > 0), aux = the ReLU output h1 (layers.py:221)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (n0 + j < p.N) {
+                const int64_t ri = (int64_t)b * p.stride_resid + m * p.ld_resid + n0 + j;
+                const float a = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.resid)[ri])
+                                           : reinterpret_cast<const float*>(p.resid)[ri];
+                v[j] = a > 0.f ? v[j] : 0.f;
+              }
+            }
+            store_chunk(p, m, n0, b, v);
+            break;
+          }
           case RP_EPI_CE_GRAD: {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {

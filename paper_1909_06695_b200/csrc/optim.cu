@@ -1,0 +1,142 @@
+// Fused optimizer updates over a module's flat parameter buffer
+// (reference optim.py:52-126), device-side weight init with the reference's
+// counter RNG (layers.py:107-112, 149-166, tensor.py:72-74), dtype casts and a
+// deterministic squared-norm reduction (engine.py:72-80).
+//
+// Adam/SGD read the fp32 master weights, gradient and moments once, write
+// weights and moments once, and in the same pass write the compute-dtype copy
+// of the updated weights straight into the next snapshot-ring slot (the
+// reference's separate deep copy, model.py:171-172, disappears).  Any
+// non-finite updated weight raises the NONFINITE status bit (optim.py:47-49).
+#include <algorithm>
+
+#include "common.cuh"
+#include "rp_internal.h"
+
+namespace rp {
+
+template <typename T>
+__global__ void adam_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, T* __restrict__ copy, int64_t n, float lr, float b1, float b2,
+                            float eps, float c1, float c2, int32_t* flag) {
+  bool finite = true;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    float mi = m[i] * b1 + (1.f - b1) * gi;
+    float vi = v[i] * b2 + (1.f - b2) * (gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    const float wi = w[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    w[i] = wi;
+    finite &= isfinite(wi);
+    if (copy) copy[i] = from_f<T>(wi);
+  }
+  if (!finite && flag) atomicOr(flag, RP_FLAG_NONFINITE);
+}
+
+template <typename T>
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, T* __restrict__ copy, int64_t n,
+                           float lr, int32_t* flag) {
+  bool finite = true;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float wi = w[i] - lr * g[i];
+    w[i] = wi;
+    finite &= isfinite(wi);
+    if (copy) copy[i] = from_f<T>(wi);
+  }
+  if (!finite && flag) atomicOr(flag, RP_FLAG_NONFINITE);
+}
+
+// out[i] = ((bits53(seed, pos0 + i) * 2^-53) * 2 - 1) * scale, evaluated in
+// fp64 exactly as the reference's uniform_signed, then rounded to fp32.
+__global__ void init_uniform_kernel(float* __restrict__ out, int64_t n, uint64_t seed, uint64_t pos0, double scale) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = (double)rng_bits53(seed, pos0 + (uint64_t)i) * (1.0 / 9007199254740992.0);
+    out[i] = (float)((u * 2.0 - 1.0) * scale);
+  }
+}
+
+template <typename Tin, typename Tout>
+__global__ void cast_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = from_f<Tout>(to_f(in[i]));
+}
+
+__global__ void sq_norm_partial_kernel(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = x[i];
+    s += t * t;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ part, int n, double* __restrict__ out, int accumulate) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = accumulate ? *out + s : s;
+  }
+}
+
+namespace {
+inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
+}  // namespace
+
+int adam_step(float* w, const float* g, float* m, float* v, void* copy, int copy_dtype, int64_t n, float lr, float b1,
+              float b2, float eps, float c1, float c2, int32_t* flag, cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  if (copy_dtype == RP_BF16)
+    adam_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(w, g, m, v, (__nv_bfloat16*)copy, n, lr, b1, b2, eps, c1,
+                                                             c2, flag);
+  else
+    adam_kernel<float><<<grid_for(n), 256, 0, st>>>(w, g, m, v, (float*)copy, n, lr, b1, b2, eps, c1, c2, flag);
+  return check_launch("adam");
+}
+
+int sgd_step(float* w, const float* g, void* copy, int copy_dtype, int64_t n, float lr, int32_t* flag,
+             cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  if (copy_dtype == RP_BF16)
+    sgd_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(w, g, (__nv_bfloat16*)copy, n, lr, flag);
+  else
+    sgd_kernel<float><<<grid_for(n), 256, 0, st>>>(w, g, (float*)copy, n, lr, flag);
+  return check_launch("sgd");
+}
+
+int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  init_uniform_kernel<<<grid_for(n), 256, 0, st>>>(out, n, seed, pos0, scale);
+  return check_launch("init_uniform");
+}
+
+int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  if (in_dtype == RP_F32 && out_dtype == RP_BF16)
+    cast_kernel<float, __nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const float*)in, (__nv_bfloat16*)out, n);
+  else if (in_dtype == RP_BF16 && out_dtype == RP_F32)
+    cast_kernel<__nv_bfloat16, float><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)in, (float*)out, n);
+  else if (in_dtype == RP_F32 && out_dtype == RP_F32)
+    cast_kernel<float, float><<<grid_for(n), 256, 0, st>>>((const float*)in, (float*)out, n);
+  else
+    cast_kernel<__nv_bfloat16, __nv_bfloat16>
+        <<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, n);
+  return check_launch("cast");
+}
+
+int sq_norm(const float* x, int64_t n, double* part /* >= 296 */, double* out, int accumulate, cudaStream_t st) {
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 296));
+  sq_norm_partial_kernel<<<nb, 256, 0, st>>>(x, n, part);
+  if (int e = check_launch("sq_norm")) return e;
+  sum_partials_kernel<<<1, 32, 0, st>>>(part, nb, out, accumulate);
+  return check_launch("sq_norm_sum");
+}
+
+}  // namespace rp

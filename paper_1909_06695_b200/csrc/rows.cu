@@ -1,0 +1,365 @@
+// Row-wise HBM-bound kernels of the block: LayerNorm forward/backward
+// (reference layers.py:62-79), causal softmax forward/backward
+// (layers.py:180-183, 237), dropout-masked gradients (layers.py:209-216) and
+// deterministic column reductions for the bias / gain / LN-bias gradients
+// (layers.py:72-73, 220, 223).
+//
+// One warp owns one row; a row of d <= 32*NPL elements lives in registers, so
+// every kernel reads its inputs once and writes its outputs once.  Column
+// reductions never use float atomics: each CTA writes a partial row and a
+// second pass sums partials in fixed order, so results are bitwise
+// reproducible for a given shape.
+#include <algorithm>
+
+#include "common.cuh"
+#include "rp_internal.h"
+
+namespace rp {
+
+constexpr int kRowThreads = 256;  // 8 warps
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr float kLnEps = 1e-5f;  // layers.py:25
+
+__device__ __forceinline__ void flag_set(int32_t* flag, int bit) {
+  if (flag) atomicOr(flag, bit);
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm forward: y = (x - mu) * rstd * g + b; saves (mu, rstd).
+template <typename T, int NPL>
+__global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                              const float* __restrict__ b, T* __restrict__ y,
+                                                              float* __restrict__ mean, float* __restrict__ rstd,
+                                                              int64_t rows, int d, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const T* xr = x + row * d;
+  float v[NPL];
+  float s = 0.f;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = (j < d) ? to_f(xr[j]) : 0.f;
+    finite &= isfinite(v[i]);
+    s += v[i];
+  }
+  s = warp_sum(s);
+  const float mu = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    const float c = (j < d) ? v[i] - mu : 0.f;
+    q += c * c;
+  }
+  q = warp_sum(q);
+  const float rs = rsqrtf(q / d + kLnEps);
+  T* yr = y + row * d;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < d) yr[j] = from_f<T>((v[i] - mu) * rs * g[j] + b[j]);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+  if (!__all_sync(0xffffffffu, finite) && lane == 0) flag_set(flag, RP_FLAG_NONFINITE);
+}
+
+// LayerNorm backward (layers.py:70-79) fused with the residual add and the
+// dropout mask of the branch feeding this LN:
+//   dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) + resid_grad
+//   dx_masked = dx * mask(seed, row*d + j)            (optional, dtype T)
+// Per-CTA column partials of dy*xhat (gain) and dy (bias).
+template <typename T, int NPL>
+__global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
+    const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
+    float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+  __shared__ float red_g[kRowWarps][32 * NPL];
+  __shared__ float red_b[kRowWarps][32 * NPL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc_g[NPL], acc_b[NPL], gv[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    acc_g[i] = acc_b[i] = 0.f;
+    const int j = lane + 32 * i;
+    gv[i] = (j < d) ? g[j] : 0.f;
+  }
+  const int64_t stride = (int64_t)gridDim.x * kRowWarps;
+  for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NPL], dyv[NPL];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int j = lane + 32 * i;
+      if (j < d) {
+        xh[i] = (to_f(x[row * d + j]) - mu) * rs;
+        dyv[i] = dy[row * d + j];
+      } else {
+        xh[i] = dyv[i] = 0.f;
+      }
+      const float dxh = dyv[i] * gv[i];
+      s1 += dxh;
+      s2 += dxh * xh[i];
+      acc_g[i] += dyv[i] * xh[i];
+      acc_b[i] += dyv[i];
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const int j = lane + 32 * i;
+      if (j < d) {
+        float o = rs * (dyv[i] * gv[i] - s1 - xh[i] * s2);
+        if (resid_grad) o += resid_grad[row * d + j];
+        dx[row * d + j] = o;
+        if (dx_masked) {
+          float mo = o;
+          if (drop_on) mo = dropout_keep(seed, (uint64_t)row * d + j, thr) ? o * scale : 0.f;
+          dx_masked[row * d + j] = from_f<T>(mo);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    red_g[w][lane + 32 * i] = acc_g[i];
+    red_b[w][lane + 32 * i] = acc_b[i];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += kRowThreads) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRowWarps; ++q) {
+      sg += red_g[q][j];
+      sb += red_b[q][j];
+    }
+    part_g[(int64_t)blockIdx.x * d + j] = sg;
+    part_b[(int64_t)blockIdx.x * d + j] = sb;
+  }
+}
+
+// out[j] = sum_b partial[b, j]  (fixed order), optionally scaled.
+__global__ void colsum_finish_kernel(const float* __restrict__ part, int nblk, int64_t cols, float* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * cols + j];
+  out[j] = s;
+}
+
+// Column partial sums of a [rows, cols] matrix (row-major, ld).
+template <typename T>
+__global__ void colsum_partial_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                      float* __restrict__ part) {
+  const int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) s += to_f(x[r * ld + j]);
+  part[(int64_t)blockIdx.x * cols + j] = s;
+}
+
+// out = g * mask (T) with column partials of the masked fp32 values
+// (the b2 gradient, layers.py:215-220).
+template <typename T>
+__global__ void mask_grad_kernel(const float* __restrict__ g, T* __restrict__ out, int64_t rows, int d,
+                                 uint64_t seed, uint64_t pos0, uint64_t thr, float scale, int drop_on,
+                                 float* __restrict__ part) {
+  const int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    float v = g[r * d + j];
+    if (drop_on) v = dropout_keep(seed, pos0 + (uint64_t)r * d + j, thr) ? v * scale : 0.f;
+    out[r * d + j] = from_f<T>(v);
+    s += v;
+  }
+  if (part) part[(int64_t)blockIdx.x * d + j] = s;
+}
+
+// ---------------------------------------------------------------------------
+// causal softmax over rows of length T (scores already scaled by 1/sqrt(d)).
+template <typename T, int NPL>
+__global__ void __launch_bounds__(kRowThreads) softmax_causal_kernel(const float* __restrict__ s, T* __restrict__ p,
+                                                                      int64_t rows, int Tn, int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int i = (int)(row % Tn);  // query position
+  const float* sr = s + row * ld;
+  float v[NPL];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int j = lane + 32 * q;
+    v[q] = (j <= i) ? sr[j] : -INFINITY;
+    mx = fmaxf(mx, v[q]);
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int j = lane + 32 * q;
+    v[q] = (j <= i) ? __expf(v[q] - mx) : 0.f;
+    sum += v[q];
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  T* pr = p + row * ld;
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int j = lane + 32 * q;
+    if (j < Tn) pr[j] = from_f<T>(v[q] * inv);
+  }
+}
+
+// g_s = (g_p - sum_j g_p*P) * P * scale   (layers.py:237, 1/sqrt(d) folded in)
+template <typename T, int NPL>
+__global__ void __launch_bounds__(kRowThreads) softmax_bwd_kernel(const float* __restrict__ gp, const T* __restrict__ p,
+                                                                   T* __restrict__ gs, float scale, int64_t rows,
+                                                                   int Tn, int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float gv[NPL], pv[NPL];
+  float dot = 0.f;
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int j = lane + 32 * q;
+    gv[q] = (j < Tn) ? gp[row * ld + j] : 0.f;
+    pv[q] = (j < Tn) ? to_f(p[row * ld + j]) : 0.f;
+    dot += gv[q] * pv[q];
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int q = 0; q < NPL; ++q) {
+    const int j = lane + 32 * q;
+    if (j < Tn) gs[row * ld + j] = from_f<T>((gv[q] - dot) * pv[q] * scale);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+namespace {
+
+inline int npl_for(int64_t n) {
+  if (n <= 64) return 2;
+  if (n <= 128) return 4;
+  if (n <= 256) return 8;
+  if (n <= 512) return 16;
+  if (n <= 1024) return 32;
+  if (n <= 2048) return 64;
+  return -1;
+}
+
+inline int row_blocks(int64_t rows) { return (int)((rows + kRowWarps - 1) / kRowWarps); }
+
+}  // namespace
+
+int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 296)); }
+
+#define RP_NPL_DISPATCH(NPL_VAL, ...)                                   \
+  switch (NPL_VAL) {                                                    \
+    case 2: { constexpr int NPL = 2; __VA_ARGS__; break; }              \
+    case 4: { constexpr int NPL = 4; __VA_ARGS__; break; }              \
+    case 8: { constexpr int NPL = 8; __VA_ARGS__; break; }              \
+    case 16: { constexpr int NPL = 16; __VA_ARGS__; break; }            \
+    case 32: { constexpr int NPL = 32; __VA_ARGS__; break; }            \
+    case 64: { constexpr int NPL = 64; __VA_ARGS__; break; }            \
+    default: return set_error(RP_ERR_DIMENSION, "row length too large"); \
+  }
+
+#define RP_NPL_DISPATCH_SMALL(NPL_VAL, ...)                             \
+  switch (NPL_VAL) {                                                    \
+    case 2: { constexpr int NPL = 2; __VA_ARGS__; break; }              \
+    case 4: { constexpr int NPL = 4; __VA_ARGS__; break; }              \
+    case 8: { constexpr int NPL = 8; __VA_ARGS__; break; }              \
+    case 16: { constexpr int NPL = 16; __VA_ARGS__; break; }            \
+    default: return set_error(RP_ERR_DIMENSION, "row length too large"); \
+  }
+
+#define RP_DTYPE_DISPATCH(DT, ...)                     \
+  if ((DT) == RP_BF16) {                               \
+    using T = __nv_bfloat16;                           \
+    __VA_ARGS__;                                       \
+  } else {                                             \
+    using T = float;                                   \
+    __VA_ARGS__;                                       \
+  }
+
+int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
+                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st) {
+  if (rows == 0) return RP_OK;
+  const int npl = npl_for(d);
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, ln_fwd_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
+                                                    (const T*)x, g, b, (T*)y, mean, rstd,
+                                                    rows, (int)d, flag)));
+  return check_launch("layernorm_fwd");
+}
+
+int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
+                  const float* resid_grad, float* dx, void* dx_masked, uint64_t seed, uint64_t thr, float scale,
+                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st) {
+  if (rows == 0) return RP_OK;
+  const int npl = npl_for(d);
+  if (npl > 16) return set_error(RP_ERR_DIMENSION, "layernorm_bwd supports d <= 512 in this build");
+  const int nb = ln_bwd_blocks(rows);
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH_SMALL(npl, ln_bwd_kernel<T, NPL><<<nb, kRowThreads, 0, st>>>(
+                                                    dy, (const T*)x, mean, rstd, g, resid_grad, dx,
+                                                    (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
+                                                    rows, (int)d)));
+  return check_launch("layernorm_bwd");
+}
+
+int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStream_t st) {
+  if (cols == 0) return RP_OK;
+  colsum_finish_kernel<<<(int)((cols + 255) / 256), 256, 0, st>>>(part, nblk, cols, out);
+  return check_launch("colsum_finish");
+}
+
+int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 128)); }
+
+int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st) {
+  if (cols == 0) return RP_OK;
+  dim3 grid(colsum_blocks(rows), (unsigned)((cols + 127) / 128));
+  RP_DTYPE_DISPATCH(dtype, colsum_partial_kernel<T><<<grid, 128, 0, st>>>((const T*)x, rows, cols, ld, part));
+  return check_launch("colsum_partial");
+}
+
+int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
+              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st) {
+  if (d == 0) return RP_OK;
+  dim3 grid(colsum_blocks(rows), (unsigned)((d + 127) / 128));
+  RP_DTYPE_DISPATCH(dtype, mask_grad_kernel<T><<<grid, 128, 0, st>>>(g, (T*)out, rows, (int)d, seed, pos0, thr,
+                                                                     scale, drop_on, part));
+  return check_launch("mask_grad");
+}
+
+int softmax_causal(int dtype, const float* s, void* p, int64_t rows, int64_t Tn, int64_t ld, cudaStream_t st) {
+  if (rows == 0) return RP_OK;
+  const int npl = npl_for(Tn);
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, softmax_causal_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
+                                                    s, (T*)p, rows, (int)Tn, ld)));
+  return check_launch("softmax_causal");
+}
+
+int softmax_bwd(int dtype, const float* gp, const void* p, void* gs, float scale, int64_t rows, int64_t Tn,
+                int64_t ld, cudaStream_t st) {
+  if (rows == 0) return RP_OK;
+  const int npl = npl_for(Tn);
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, softmax_bwd_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
+                                                    gp, (const T*)p, (T*)gs, scale, rows, (int)Tn, ld)));
+  return check_launch("softmax_bwd");
+}
+
+}  // namespace rp

@@ -17,4 +17,35 @@ int gemm_tile_n(int64_t N);
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);
 
+int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
+                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st);
+int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
+                  const float* resid_grad, float* dx, void* dx_masked, uint64_t seed, uint64_t thr, float scale,
+                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st);
+int ln_bwd_blocks(int64_t rows);
+int colsum_blocks(int64_t rows);
+int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st);
+int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStream_t st);
+int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
+              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st);
+int softmax_causal(int dtype, const float* s, void* p, int64_t rows, int64_t Tn, int64_t ld, cudaStream_t st);
+int softmax_bwd(int dtype, const float* gp, const void* p, void* gs, float scale, int64_t rows, int64_t Tn,
+                int64_t ld, cudaStream_t st);
+int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, void* out, int64_t B, int64_t Tn,
+              int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
+              cudaStream_t st);
+int64_t embed_bwd_workspace(int64_t n_tokens);
+int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
+              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, uint64_t* work,
+              cudaStream_t st);
+int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,
+              float* lse, float* loss_rows, float* loss, double* loss64, int32_t* flag, cudaStream_t st);
+int adam_step(float* w, const float* g, float* m, float* v, void* copy, int copy_dtype, int64_t n, float lr, float b1,
+              float b2, float eps, float c1, float c2, int32_t* flag, cudaStream_t st);
+int sgd_step(float* w, const float* g, void* copy, int copy_dtype, int64_t n, float lr, int32_t* flag,
+             cudaStream_t st);
+int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, cudaStream_t st);
+int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st);
+int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
+
 }  // namespace rp

@@ -1,0 +1,458 @@
+"""The Ouroboros delayed-gradient schedule on B200s.
+
+Drop-in for reference engine.py: `BatchSample`, `GradientPacket`,
+`embedding_gradient`, `packet_grad_sq_norm`, `LogicalCostModel`,
+`ScheduleTrace`, `PipelineEngine`, `ConcurrentPipelineEngine`,
+`SequentialRunner`, `sequential_gradients`, `check_one_step_behind`,
+`WorkerFailure`.
+
+Step t (reference engine.py:246-259):
+  1. every module's snapshot ring holds w^t (written by the previous step's
+     fused optimizer, so this is free),
+  2. batch t relays forward through modules 1..K at w^t; module K ends in the
+     fused tied-vocab cross-entropy (no [N, V] logits in HBM),
+  3. module k back-propagates sample t-K+k at w^{t-K+k} from its stored slot
+     and the boundary gradient module k+1 produced at t-1 (zero while
+     t-K+k < 0); modules run K..1 so the output-side tied gradient is in
+     place before the input-side half is scattered onto it,
+  4. the packet's tied gradient is 1/2 Vo(t) + 1/2 Vi(t-K+1) (engine.py:54-69),
+  5. the optimizer applies the packet.
+
+`PipelineEngine` issues everything on the current CUDA stream;
+`ConcurrentPipelineEngine` gives every module its own forward and backward
+streams ordered only by the true dependencies (events), so a module's stale
+backward overlaps the relay (the GPU analogue of the reference's worker
+threads, engine.py:271-406), and its packets are bitwise identical because
+every kernel is deterministic.
+"""
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import DimensionError, NonFiniteError, ScheduleViolation, WorkerFailure  # noqa: F401
+from .model import build_modules
+
+# ---------------------------------------------------------------------------
+# records
+
+
+@dataclass
+class BatchSample:
+    x: object  # token ids [B, T] (numpy or torch)
+    y: object  # next-token targets [B, T]
+    sample_id: int
+
+
+@dataclass
+class GradientPacket:
+    """module_grads: per module {"L{idx}.{name}": fp32 device view};
+    emb_grad: the mixed tied gradient [V, d] (fp32, device).  Views are
+    overwritten by the next step; use `.cpu()` to keep a copy."""
+
+    step: int
+    module_grads: list
+    emb_grad: object
+    sample_ids: list
+    loss: float
+
+    def cpu(self):
+        return GradientPacket(
+            self.step,
+            [{k: v.detach().double().cpu().numpy() for k, v in g.items()} for g in self.module_grads],
+            self.emb_grad.detach().double().cpu().numpy(),
+            list(self.sample_ids),
+            self.loss,
+        )
+
+
+def embedding_gradient(t, K, grad_vo_fresh, grad_vi_stale, convention="half_avg"):
+    """Reference engine.py:54-69 on explicit tensors (host or device)."""
+    if t - K + 1 < 0:
+        if grad_vi_stale is not None:
+            raise ScheduleViolation("stale embedding gradient before step K-1")
+        return grad_vo_fresh * 0
+    if grad_vi_stale is None:
+        raise ScheduleViolation("missing stale embedding gradient")
+    if tuple(grad_vo_fresh.shape) != tuple(grad_vi_stale.shape):
+        raise DimensionError("embedding gradient shape mismatch")
+    if convention == "half_avg":
+        return 0.5 * grad_vo_fresh + 0.5 * grad_vi_stale
+    if convention == "sum":
+        return grad_vo_fresh + grad_vi_stale
+    raise ValueError(f"unknown tied_grad convention {convention!r}")
+
+
+def tied_coefficients(t, K, convention):
+    """(alpha_out, beta_in) of the fused tied gradient; (0, 0) = zero packet."""
+    if convention not in ("half_avg", "sum"):
+        raise ValueError(f"unknown tied_grad convention {convention!r}")
+    if t - K + 1 < 0:
+        return 0.0, 0.0
+    return (0.5, 0.5) if convention == "half_avg" else (1.0, 1.0)
+
+
+def packet_grad_sq_norm(packet):
+    """Squared norm of the packet, accumulated in fp64 on the device in a
+    fixed key order (engine.py:72-80)."""
+    from . import ops
+
+    dev = packet.emb_grad.device
+    part = torch.empty(296, dtype=torch.float64, device=dev)
+    out = torch.zeros((), dtype=torch.float64, device=dev)
+    for grads in packet.module_grads:
+        for key in sorted(grads):
+            g = grads[key]
+            ops.sq_norm(g.contiguous(), part, out, accumulate=True)
+    ops.sq_norm(packet.emb_grad, part, out, accumulate=True)
+    return float(out.item())
+
+
+# ---------------------------------------------------------------------------
+# logical clock + trace (engine.py:83-135), kept for API compatibility
+
+
+@dataclass
+class LogicalCostModel:
+    fwd: list
+    bwd: list
+    relay: float = 0.05
+
+    @classmethod
+    def derived(cls, part, relay=0.05, recompute=True):
+        sizes = [hi - lo for lo, hi in part.groups]
+        factor = 3.0 if recompute else 2.0
+        return cls([float(s) for s in sizes], [factor * s for s in sizes], relay)
+
+    @classmethod
+    def synthetic(cls, K, module_cost=1.0, relay=0.05):
+        return cls([module_cost] * K, [module_cost] * K, relay)
+
+
+class ScheduleTrace:
+    """Occupancy rows {step, module, phase, sample, start, end}; the engines
+    fill start/end from the logical clock, or from CUDA events when
+    `timed=True` (milliseconds since the first recorded step)."""
+
+    def __init__(self):
+        self.rows = []
+
+    def record(self, step, module, phase, sample_id, start, end):
+        self.rows.append({"step": step, "module": module, "phase": phase, "sample": sample_id,
+                          "start": start, "end": end})
+
+    def to_jsonl(self, path):
+        with open(path, "w") as fh:
+            for row in self.rows:
+                fh.write(json.dumps(row) + "\n")
+
+    def backward_rows(self):
+        return [r for r in self.rows if r["phase"] == "backward"]
+
+    def idle_backward_steps(self, module, from_step=0):
+        return [r["step"] for r in self.rows if r["phase"] == "idle" and r["module"] == module
+                and r["step"] >= from_step]
+
+
+def check_one_step_behind(trace, K):
+    for row in trace.backward_rows():
+        if row["step"] != row["sample"] + K - row["module"]:
+            raise ScheduleViolation(
+                f"backward of module {row['module']} for sample {row['sample']} at step {row['step']}")
+    return True
+
+
+# ---------------------------------------------------------------------------
+# executors
+
+
+def _to_device_tokens(a, device):
+    if torch.is_tensor(a):
+        return a.to(device=device, dtype=torch.int64, non_blocking=True)
+    arr = np.ascontiguousarray(np.asarray(a), dtype=np.int64)
+    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+
+
+class PipelineEngine:
+    """Deterministic single-stream executor of the delayed-gradient schedule."""
+
+    def __init__(self, stack, part, dropout_seed, tied_grad="half_avg", stale_weights="snapshot", train=True,
+                 cost_model=None):
+        if tied_grad not in ("half_avg", "sum"):
+            raise ValueError(f"unknown tied_grad convention {tied_grad!r}")
+        if stale_weights not in ("snapshot", "current"):
+            raise ValueError(f"unknown stale_weights mode {stale_weights!r}")
+        self.stack = stack
+        self.part = part
+        self.K = part.k
+        self.modules = build_modules(stack, part, dropout_seed)
+        self.tied_grad = tied_grad
+        self.stale_weights = stale_weights
+        self.train = train
+        self.costs = cost_model or LogicalCostModel.derived(part)
+        self.trace = ScheduleTrace()
+        self.clock = 0.0
+        self.last_step_logical = 0.0
+        self.last_backward_logical = 0.0
+        self.runtime = stack.runtime
+        self.device = stack.runtime.device
+        self.boundary = {}  # k -> fp32 [B*T, d] produced by module k+1 at the previous step
+        self._bpool = {}
+        self.last_loss_device = None
+
+    # -- boundary buffers (ping-pong by step parity) --------------------------
+    def _bbuf(self, k, parity, Nt, d):
+        key = (k, parity)
+        b = self._bpool.get(key)
+        if b is None or b.shape != (Nt, d):
+            b = torch.empty(Nt, d, dtype=torch.float32, device=self.device)
+            self._bpool[key] = b
+        return b
+
+    # -- phases ---------------------------------------------------------------
+    def _relay(self, t, x, y, sample_id):
+        B, T = x.shape
+        cur = x
+        start = self.clock
+        for m in self.modules:
+            nxt = self.modules[m.index] if m.index < self.K else None
+            out = nxt.input_buffer(t, B, T) if nxt is not None else None
+            end = start + self.costs.fwd[m.index - 1]
+            self.trace.record(t, m.index, "forward", sample_id, start, end)
+            cur = m.forward(cur, t, sample_id, y if m.has_projection else None, self.train, out=out)
+            if m.index < self.K:
+                cur = cur.view(B, T, -1)
+            start = end + (self.costs.relay if m.index < self.K else 0.0)
+        return cur, start
+
+    def _backward_one(self, t, k, coef, B, T):
+        m = self.modules[k - 1]
+        s = t - self.K + k
+        if s < 0:
+            m.zero_grads()
+            return None
+        slot = m.pop_slot()
+        if slot.step != s:
+            raise ScheduleViolation(f"module {k} popped slot for step {slot.step}, expected {s}")
+        grad_out = None
+        if not m.has_projection:
+            if k not in self.boundary:
+                raise ScheduleViolation(f"module {k} missing boundary gradient")
+            grad_out = self.boundary[k]
+        g_in = self._bbuf(k - 1, t & 1, B * T, m.d) if k > 1 else None
+        alpha, beta = coef
+        emb = (alpha if m.has_projection else 0.0, beta if m.has_embedding else 0.0, self.stack.tied_store.grad)
+        m.recompute_backward(slot, grad_out, self.stale_weights, self.train, g_in=g_in, emb=emb, live_step=t)
+        return g_in, slot.sample_id
+
+    def _backward_all(self, t, B, T):
+        coef = tied_coefficients(t, self.K, self.tied_grad)
+        if coef == (0.0, 0.0):
+            self.stack.tied_store.grad.zero_()
+        results = {}
+        for k in range(self.K, 0, -1):
+            results[k] = self._backward_one(t, k, coef, B, T)
+        return results
+
+    def _assemble(self, t, results, loss):
+        nb = {}
+        sids = []
+        grads = []
+        for k in range(1, self.K + 1):
+            m = self.modules[k - 1]
+            res = results[k]
+            grads.append(m.grad_views)
+            if res is None:
+                sids.append(None)
+                continue
+            g_in, sid = res
+            sids.append(sid)
+            if k > 1:
+                nb[k - 1] = g_in
+        self.boundary = nb
+        return GradientPacket(t, grads, self.stack.tied_store.grad, sids, loss)
+
+    def _advance_clock(self, t, results, relay_end):
+        longest = 0.0
+        for k in range(1, self.K + 1):
+            res = results[k]
+            if res is None:
+                self.trace.record(t, k, "idle", None, relay_end, relay_end)
+                continue
+            dur = self.costs.bwd[k - 1]
+            self.trace.record(t, k, "backward", res[1], relay_end, relay_end + dur)
+            longest = max(longest, dur)
+        handoff = self.costs.relay if self.K > 1 else 0.0
+        end = relay_end + longest + handoff
+        self.last_step_logical = end - self.clock
+        self.last_backward_logical = longest + handoff
+        self.clock = end
+
+    # -- public -----------------------------------------------------------------
+    def step(self, t, batch, optimizer=None, sync=True):
+        """One schedule step.  Returns (packet, loss); with sync=False the loss
+        stays a 0-d device tensor and the status word is not polled."""
+        if t < 0:
+            raise ValueError("step index must be >= 0")
+        x = _to_device_tokens(batch.x, self.device)
+        y = _to_device_tokens(batch.y, self.device)
+        B, T = x.shape
+        for m in self.modules:
+            m.snapshot(t)
+        loss_dev, relay_end = self._relay(t, x, y, batch.sample_id)
+        results = self._backward_all(t, B, T)
+        packet = self._assemble(t, results, loss_dev)
+        self._advance_clock(t, results, relay_end)
+        if optimizer is not None:
+            optimizer.apply(t, packet, self.modules, self.stack.tied)
+        self.last_loss_device = loss_dev
+        if sync:
+            self.runtime.check(f"step {t}")
+            loss = float(loss_dev.item())
+            packet.loss = loss
+            return packet, loss
+        return packet, loss_dev
+
+    def export_boundary(self):
+        return dict(self.boundary)
+
+    def import_boundary(self, grads):
+        self.boundary = {k: torch.as_tensor(v).to(self.device, torch.float32).reshape(-1, self.modules[0].d)
+                         for k, v in grads.items()}
+
+    def close(self):
+        pass
+
+
+class ConcurrentPipelineEngine(PipelineEngine):
+    """Same schedule with per-module CUDA streams.
+
+    fwd(k,t) waits fwd(k-1,t); bwd(k,t) waits bwd(k+1,t-1) (its boundary) and,
+    for k=K, fwd(K,t); the optimizer waits every fwd/bwd of step t; fwd(k,t+1)
+    waits the optimizer.  Module 1's tied scatter waits module K's Vo GEMM.
+    """
+
+    def __init__(self, *args, timeout=120.0, **kwargs):
+        super().__init__(*args, **kwargs)
+        if self.K < 2:
+            raise ValueError("concurrent execution needs K >= 2")
+        self._timeout = timeout
+        self._fs = [torch.cuda.Stream(device=self.device) for _ in range(self.K)]
+        self._bs = [torch.cuda.Stream(device=self.device) for _ in range(self.K)]
+        self._bwd_done = {}
+
+    def step(self, t, batch, optimizer=None, sync=True):
+        if t < 0:
+            raise ValueError("step index must be >= 0")
+        main = torch.cuda.current_stream(self.device)
+        x = _to_device_tokens(batch.x, self.device)
+        y = _to_device_tokens(batch.y, self.device)
+        B, T = x.shape
+        start_ev = torch.cuda.Event()
+        start_ev.record(main)
+        for m in self.modules:
+            m.snapshot(t)
+        # forward relay on per-module forward streams
+        fwd_done = []
+        cur = x
+        prev = start_ev
+        for m in self.modules:
+            s = self._fs[m.index - 1]
+            s.wait_event(prev)
+            nxt = self.modules[m.index] if m.index < self.K else None
+            with torch.cuda.stream(s):
+                out = nxt.input_buffer(t, B, T) if nxt is not None else None
+                cur = m.forward(cur, t, batch.sample_id, y if m.has_projection else None, self.train, out=out)
+                if m.index < self.K:
+                    cur = cur.view(B, T, -1)
+                ev = torch.cuda.Event()
+                ev.record(s)
+            fwd_done.append(ev)
+            prev = ev
+        loss_dev = cur
+        # stale backwards
+        coef = tied_coefficients(t, self.K, self.tied_grad)
+        results = {}
+        bwd_done = {}
+        vo_ready = None
+        for k in range(self.K, 0, -1):
+            m = self.modules[k - 1]
+            s = self._bs[k - 1]
+            s.wait_event(start_ev)
+            if k == self.K:
+                s.wait_event(fwd_done[k - 1])
+                if coef == (0.0, 0.0):
+                    with torch.cuda.stream(s):
+                        self.stack.tied_store.grad.zero_()
+            if (k + 1) in self._bwd_done:
+                s.wait_event(self._bwd_done[k + 1])
+            if m.has_embedding and vo_ready is not None:
+                s.wait_event(vo_ready)
+            with torch.cuda.stream(s):
+                results[k] = self._backward_one(t, k, coef, B, T)
+                ev = torch.cuda.Event()
+                ev.record(s)
+            bwd_done[k] = ev
+            if k == self.K:
+                vo_ready = ev
+        self._bwd_done = bwd_done
+        for ev in fwd_done + list(bwd_done.values()):
+            main.wait_event(ev)
+        packet = self._assemble(t, results, loss_dev)
+        relay_end = self.clock + sum(self.costs.fwd) + self.costs.relay * (self.K - 1)
+        self._advance_clock(t, results, relay_end)
+        if optimizer is not None:
+            optimizer.apply(t, packet, self.modules, self.stack.tied)
+        done = torch.cuda.Event()
+        done.record(main)
+        for s in self._fs + self._bs:
+            s.wait_event(done)
+        self.last_loss_device = loss_dev
+        if sync:
+            self.runtime.check(f"step {t}")
+            loss = float(loss_dev.item())
+            packet.loss = loss
+            return packet, loss
+        return packet, loss_dev
+
+
+class SequentialRunner(PipelineEngine):
+    """Plain backprop over the whole stack (engine.py:443-491): the K=1
+    baseline, keeping the caller's partition only for packet slicing."""
+
+    def __init__(self, stack, part, dropout_seed, tied_grad="half_avg", train=True, cost_model=None):
+        from .model import partition
+
+        super().__init__(stack, partition(stack.num_layers, 1), dropout_seed, tied_grad, "snapshot", train,
+                         cost_model or LogicalCostModel.derived(part, recompute=False))
+        self.user_part = part
+
+    def step(self, t, batch, optimizer=None, sync=True):
+        packet, loss = super().step(t, batch, optimizer, sync)
+        grads = []
+        allg = packet.module_grads[0]
+        for lo, hi in self.user_part.groups:
+            grads.append({k: v for k, v in allg.items() if lo <= int(k.split(".")[0][1:]) < hi})
+        packet.module_grads = grads
+        packet.sample_ids = [batch.sample_id] * self.user_part.k
+        return packet, loss
+
+
+def sequential_gradients(stack, batch, dropout_seed, step, train=True):
+    """Full backprop at the stack's current weights without touching them:
+    returns (grads by key as host fp64 arrays, grad_vi, grad_vo, loss)."""
+    from .model import build_modules, partition
+
+    part = partition(stack.num_layers, 1)
+    (m,) = build_modules(stack, part, dropout_seed)
+    m.snapshot(step)
+    x = _to_device_tokens(batch.x, stack.runtime.device)
+    y = _to_device_tokens(batch.y, stack.runtime.device)
+    loss = m.forward(x, step, batch.sample_id, y, train)
+    slot = m.pop_slot()
+    _, grads, tied, _ = m.recompute_backward(slot, None, "snapshot", train)
+    stack.runtime.check("sequential_gradients")
+    host = {k: v.double().cpu().numpy() for k, v in grads.items()}
+    return host, tied["Vi"].double().cpu().numpy(), tied["Vo"].double().cpu().numpy(), float(loss.item())

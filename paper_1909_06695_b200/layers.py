@@ -1,0 +1,219 @@
+"""Device forward / hand-derived backward of the three layer kinds.
+
+Same math and op order as the reference layer protocol (reference
+pkg/src/ringpipe/layers.py): token+position embedding with dropout
+(layers.py:114-136), the pre-LN single-head block (layers.py:168-253) and the
+tied projection with its fused softmax cross-entropy head (layers.py:268-322).
+Every op is one call into libringpipe_b200.so: tcgen05 GEMMs with fused
+epilogues for all contractions, row kernels for LayerNorm / softmax /
+dropout-masked gradients, a deterministic sorted scatter for the tied
+embedding gradient.  Activations are stored in the compute dtype (bf16 or
+fp32), every reduction and every gradient flowing along the residual stream
+is fp32.
+
+Dropout streams follow the reference exactly: the layer's seed is
+mix64(dropout_seed, step, global_layer_idx) (model.py:218-219); the
+embedding mask occupies stream positions [0, n); the block's attention mask
+[0, n) and FFN mask [n, 2n) with n = B*T*d (layers.py:184-195, 209-212).
+"""
+
+import math
+
+import torch
+
+from . import _native as N
+from . import ops
+from .rng import keep_threshold
+
+BLOCK_VEC = (("ln1_g", "d"), ("ln1_b", "d"), ("ln2_g", "d"), ("ln2_b", "d"), ("b1", "f"), ("b2", "d"))
+BLOCK_MAT = (("wqkv", ("d", "3d")), ("wo", ("d", "d")), ("w1", ("d", "f")), ("w2", ("f", "d")))
+# reference key order of a block's parameters (layers.py:153-166)
+BLOCK_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2")
+
+
+def _pad8(n):
+    return (n + 7) // 8 * 8
+
+
+class Dropout:
+    """(seed, integer keep threshold, 1/(1-p)) of one layer stream, or None."""
+
+    @staticmethod
+    def make(seed, p, train):
+        if not train or p <= 0.0:
+            return None
+        return (seed, keep_threshold(p), 1.0 / (1.0 - p))
+
+
+class Workspace:
+    """Named scratch buffers reused across calls (one per module and role)."""
+
+    def __init__(self, device):
+        self.device = device
+        self._bufs = {}
+
+    def get(self, name, shape, dtype):
+        shape = tuple(int(s) for s in shape)
+        t = self._bufs.get(name)
+        if t is None or t.dtype != dtype or t.numel() < math.prod(shape):
+            t = torch.empty(math.prod(shape), dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t[: math.prod(shape)].view(shape)
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for t in self._bufs.values())
+
+
+class BlockTape:
+    """Forward intermediates of one block for one stale slot (store-all)."""
+
+    def __init__(self, B, T, d, f, dtype, device):
+        N = B * T
+        Tp = _pad8(T)
+        e = lambda *s: torch.empty(s, dtype=dtype, device=device)  # noqa: E731
+        f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
+        self.a = e(N, d)
+        self.qkv = e(B, T, 3 * d)
+        self.probs_buf = e(B, T, Tp)
+        self.probs = self.probs_buf[:, :, :T]
+        self.ctx = e(B, T, d)
+        self.x1 = e(N, d)
+        self.m = e(N, d)
+        self.h1 = e(N, f)
+        self.mean1, self.rstd1, self.mean2, self.rstd2 = f32(N), f32(N), f32(N), f32(N)
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for t in
+                   (self.a, self.qkv, self.probs_buf, self.ctx, self.x1, self.m, self.h1,
+                    self.mean1, self.rstd1, self.mean2, self.rstd2))
+
+
+# ---------------------------------------------------------------------------
+# embedding (layers.py:114-136)
+
+
+def embed_forward(tied_c, pos_c, tokens, out, vocab, drop, flag):
+    ops.embed_fwd(tokens, tied_c, pos_c, out.view(tokens.shape[0], tokens.shape[1], -1), vocab, drop, flag)
+
+
+def embed_backward(g, tokens, t_max, grad_pos, emb_grad, beta, ws, drop):
+    """grad_pos fully written; emb_grad[tok] += beta * (scatter-sum of masked g)."""
+    n = tokens.numel()
+    work = ws.get("embed_sort", (max(1, n),), torch.int64)
+    ops.embed_bwd(g, tokens, t_max, grad_pos, emb_grad, beta, work, drop)
+
+
+# ---------------------------------------------------------------------------
+# transformer block (layers.py:168-253)
+
+
+def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
+    """x, out: [B*T, d] compute dtype.  W: compute-dtype matrices; vecs: fp32."""
+    d = x.shape[-1]
+    n = B * T * d
+    ops.layernorm_fwd(x, vecs["ln1_g"], vecs["ln1_b"], tape.a, tape.mean1, tape.rstd1, flag)
+    ops.gemm(tape.a, W["wqkv"], b_mn=True, out=tape.qkv.view(B * T, 3 * d))
+    q, k, v = tape.qkv[..., :d], tape.qkv[..., d: 2 * d], tape.qkv[..., 2 * d:]
+    Tp = tape.probs_buf.shape[-1]
+    scores = ws.get("scores", (B, T, Tp), torch.float32)[:, :, :T]
+    ops.gemm(q, k, alpha=1.0 / math.sqrt(d), out=scores)
+    ops.softmax_causal(scores, tape.probs)
+    ops.gemm(tape.probs, v, b_mn=True, out=tape.ctx)
+    d0 = None if drop is None else (drop[0], drop[1], drop[2], 0)
+    ops.gemm(tape.ctx.view(B * T, d), W["wo"], b_mn=True, out=tape.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL,
+             residual=x, dropout=d0)
+    ops.layernorm_fwd(tape.x1, vecs["ln2_g"], vecs["ln2_b"], tape.m, tape.mean2, tape.rstd2, flag)
+    ops.gemm(tape.m, W["w1"], b_mn=True, out=tape.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+    d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
+    ops.gemm(tape.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
+             residual=tape.x1, dropout=d1)
+
+
+def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
+    """g_out, g_x: [B*T, d] fp32 (g_x may alias g_out).  G: fp32 grad views."""
+    d = x.shape[-1]
+    f = tape.h1.shape[-1]
+    Nt = B * T
+    n = Nt * d
+    cdt = x.dtype
+    inv = 1.0 / math.sqrt(d)
+    nbc = ops.colsum_blocks(Nt)
+    part = ws.get("colsum_part", (nbc, max(f, 3 * d)), torch.float32)
+    # feed-forward branch
+    g_h2 = ws.get("g_h2", (Nt, d), cdt)
+    ops.mask_grad(g_out, g_h2, n, drop, part[:, :d])
+    ops.colsum_finish(part[:, :d], nbc, G["b2"])
+    ops.gemm(tape.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
+    g_z1 = ws.get("g_z1", (Nt, f), cdt)
+    ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tape.h1)
+    ops.colsum_partial(g_z1, part[:, :f])
+    ops.colsum_finish(part[:, :f], nbc, G["b1"])
+    ops.gemm(tape.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
+    g_m = ws.get("g_m", (Nt, d), torch.float32)
+    ops.gemm(g_z1, W["w1"], out=g_m)
+    nbl = ops.layernorm_bwd_blocks(Nt)
+    pg = ws.get("ln_pg", (nbl, d), torch.float32)
+    pb = ws.get("ln_pb", (nbl, d), torch.float32)
+    g_x1 = ws.get("g_x1", (Nt, d), torch.float32)
+    g_proj = ws.get("g_proj", (Nt, d), cdt)
+    ops.layernorm_bwd(g_m, tape.x1, tape.mean2, tape.rstd2, vecs["ln2_g"], g_x1, pg, pb, resid_grad=g_out,
+                      dx_masked=g_proj, dropout=drop)
+    ops.colsum_finish(pg, nbl, G["ln2_g"])
+    ops.colsum_finish(pb, nbl, G["ln2_b"])
+    # attention branch
+    ops.gemm(tape.ctx.view(Nt, d), g_proj, a_mn=True, b_mn=True, out=G["wo"])
+    g_ctx = ws.get("g_ctx", (B, T, d), cdt)
+    ops.gemm(g_proj, W["wo"], out=g_ctx.view(Nt, d))
+    Tp = tape.probs_buf.shape[-1]
+    g_p = ws.get("g_p", (B, T, Tp), torch.float32)[:, :, :T]
+    q, k, v = tape.qkv[..., :d], tape.qkv[..., d: 2 * d], tape.qkv[..., 2 * d:]
+    ops.gemm(g_ctx, v, out=g_p)
+    g_qkv = ws.get("g_qkv", (B, T, 3 * d), cdt)
+    ops.gemm(tape.probs, g_ctx, a_mn=True, b_mn=True, out=g_qkv[..., 2 * d:])
+    g_s = ws.get("g_s", (B, T, Tp), cdt)[:, :, :T]
+    ops.softmax_bwd(g_p, tape.probs, g_s, inv)
+    ops.gemm(g_s, k, b_mn=True, out=g_qkv[..., :d])
+    ops.gemm(g_s, q, a_mn=True, b_mn=True, out=g_qkv[..., d: 2 * d])
+    g2 = g_qkv.view(Nt, 3 * d)
+    ops.gemm(tape.a, g2, a_mn=True, b_mn=True, out=G["wqkv"])
+    g_a = ws.get("g_a", (Nt, d), torch.float32)
+    ops.gemm(g2, W["wqkv"], out=g_a)
+    ops.layernorm_bwd(g_a, x, tape.mean1, tape.rstd1, vecs["ln1_g"], g_x, pg, pb, resid_grad=g_x1)
+    ops.colsum_finish(pg, nbl, G["ln1_g"])
+    ops.colsum_finish(pb, nbl, G["ln1_b"])
+
+
+# ---------------------------------------------------------------------------
+# tied head (layers.py:287-322)
+
+
+class HeadState:
+    """Per-slot head intermediates: row logsumexp and the loss."""
+
+    def __init__(self, Nt, device):
+        self.lse = torch.empty(Nt, dtype=torch.float32, device=device)
+        self.loss = torch.empty((), dtype=torch.float32, device=device)
+        self.loss64 = torch.empty((), dtype=torch.float64, device=device)
+
+
+def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
+    """Mean CE of h @ tied^T against targets without materialising logits."""
+    Nt = h.shape[0]
+    bn = ops.gemm_tile_n(vocab)
+    nt = (vocab + bn - 1) // bn
+    partial = ws.get("head_partial", (Nt, nt, 2), torch.float32)
+    zy = ws.get("head_zy", (Nt,), torch.float32)
+    rows_loss = ws.get("head_rows", (Nt,), torch.float32)
+    ops.gemm(h, tied_c, epilogue=N.EPI_LSE_PARTIAL, targets=targets, partial=partial, target_logit=zy)
+    ops.ce_finish(partial, zy, targets, vocab, hs.lse, rows_loss, hs.loss, hs.loss64, flag)
+
+
+def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
+    """g_h = dz @ tied (fp32); vo_out = vo_alpha * dz^T @ h when vo_out is given."""
+    Nt, d = h.shape
+    vp = _pad8(vocab)
+    dz = ws.get("head_dz", (Nt, vp), h.dtype)[:, :vocab]
+    ops.gemm(h, tied_c, epilogue=N.EPI_CE_GRAD, targets=targets, lse=hs.lse, ce_scale=1.0 / Nt, out=dz)
+    ops.gemm(dz, tied_c, b_mn=True, out=g_h)
+    if vo_out is not None:
+        ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha)

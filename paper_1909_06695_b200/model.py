@@ -1,0 +1,596 @@
+"""Layer stack, contiguous ring partition, and device-resident Ouroboros modules.
+
+Drop-in for reference model.py: `build_stack`, `LayerStack`, `partition`,
+`ModulePartition`, `StaleSlot`, `ModuleState`, `build_modules`,
+`PartitionError`, `ScheduleViolation` keep their names and argument meaning.
+
+B200 layout:
+  * every layer owns one flat fp32 master buffer [vectors | matrices] with a
+    same-shaped gradient buffer; the reference-facing `params` / grads dicts
+    are views into it (wq/wk/wv are column blocks of one [d, 3d] wqkv);
+  * the snapshot ring (model.py:175-196) is a ring of compute-dtype copies of
+    that buffer; the optimizer writes the next step's copy directly into the
+    next ring slot, so `snapshot(t)` is free in steady state;
+  * the tied matrix V lives once on the Ouroboros device: fp32 master, fp32
+    gradient (= the packet's mixed embedding gradient) and a compute copy;
+  * stale slots (model.py:162-168) keep every forward intermediate
+    ("store-all"), which the reference proves bitwise equal to its recompute
+    (tests/test_model.py:110-129); `stale_weights="current"` recomputes at
+    the live weights.
+"""
+
+import math
+from collections import deque
+from dataclasses import dataclass
+
+import torch
+
+from . import layers as LY
+from . import ops
+from .errors import DimensionError, PartitionError, ScheduleViolation
+from .rng import mix64
+from .runtime import Runtime
+
+# ---------------------------------------------------------------------------
+# layer descriptors (the reference layer kinds, layers.py:96-280)
+
+
+class EmbeddingLayer:
+    kind = "embedding"
+
+    def __init__(self, vocab_size, model_dim, max_seq_len, dropout_p):
+        self.vocab_size, self.model_dim = vocab_size, model_dim
+        self.max_seq_len, self.dropout_p = max_seq_len, dropout_p
+
+    def specs(self):
+        return [], [("pos", (self.max_seq_len, self.model_dim))]
+
+
+class TransformerBlockLayer:
+    kind = "block"
+
+    def __init__(self, model_dim, ffn_dim, dropout_p):
+        self.model_dim, self.ffn_dim, self.dropout_p = model_dim, ffn_dim, dropout_p
+
+    def specs(self):
+        d, f = self.model_dim, self.ffn_dim
+        dims = {"d": d, "f": f, "3d": 3 * d}
+        vec = [(n, (dims[s],)) for n, s in LY.BLOCK_VEC]
+        mat = [(n, (dims[a], dims[b])) for n, (a, b) in LY.BLOCK_MAT]
+        return vec, mat
+
+
+class OutputProjectionLayer:
+    kind = "projection"
+
+    def __init__(self, vocab_size, model_dim):
+        self.vocab_size, self.model_dim = vocab_size, model_dim
+
+    def specs(self):
+        return [], []
+
+
+# ---------------------------------------------------------------------------
+# device storage
+
+
+def _dtype_of(name):
+    if name in ("bf16", torch.bfloat16):
+        return torch.bfloat16
+    if name in ("fp32", "f32", torch.float32):
+        return torch.float32
+    raise ValueError(f"unknown compute dtype {name!r}")
+
+
+class LayerParams:
+    """fp32 master + gradient + snapshot ring of one layer."""
+
+    def __init__(self, layer, device, cdtype):
+        self.layer, self.device, self.cdtype = layer, device, cdtype
+        vec, mat = layer.specs()
+        self.n_vec = sum(math.prod(s) for _, s in vec)
+        self.n_mat = sum(math.prod(s) for _, s in mat)
+        n = self.n_vec + self.n_mat
+        self.master = torch.zeros(n, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(n, dtype=torch.float32, device=device)
+        self.m = self.v = None
+        self._vec_specs, self._mat_specs = vec, mat
+        self.P = self._carve(self.master, torch.float32, torch.float32)  # internal names
+        self.G = self._carve(self.grad, torch.float32, torch.float32)
+        self.params = self._public(self.P)
+        self.grads = self._public(self.G)
+        self.ring = []
+        self.ring_step = []
+
+    def _carve(self, flat, vec_dt, mat_dt, vec_flat=None, mat_flat=None):
+        out = {}
+        if vec_flat is None:
+            vec_flat, mat_flat = flat[: self.n_vec], flat[self.n_vec:]
+        off = 0
+        for name, shape in self._vec_specs:
+            out[name] = vec_flat[off: off + math.prod(shape)].view(shape)
+            off += math.prod(shape)
+        off = 0
+        for name, shape in self._mat_specs:
+            out[name] = mat_flat[off: off + math.prod(shape)].view(shape)
+            off += math.prod(shape)
+        return out
+
+    def _public(self, D):
+        if self.layer.kind != "block":
+            return dict(D)
+        d = self.layer.model_dim
+        w = D["wqkv"]
+        views = {"wq": w[:, :d], "wk": w[:, d: 2 * d], "wv": w[:, 2 * d:]}
+        return {k: (views[k] if k in views else D[k]) for k in LY.BLOCK_KEYS}
+
+    # -- snapshot ring ----------------------------------------------------
+    def configure_ring(self, capacity):
+        self.ring = []
+        for _ in range(capacity):
+            vec = torch.empty(self.n_vec, dtype=torch.float32, device=self.device)
+            mat = torch.empty(self.n_mat, dtype=self.cdtype, device=self.device)
+            self.ring.append((vec, mat, self._carve(None, None, None, vec, mat)))
+        self.ring_step = [None] * capacity
+
+    def ring_slot(self, step):
+        return step % len(self.ring)
+
+    def ensure(self, step):
+        """Make the ring hold the current master weights for `step`."""
+        i = self.ring_slot(step)
+        if self.ring_step[i] != step:
+            vec, mat, _ = self.ring[i]
+            if self.n_vec:
+                vec.copy_(self.master[: self.n_vec])
+            if self.n_mat:
+                ops.cast(self.master[self.n_vec:], mat)
+            self.ring_step[i] = step
+
+    def weights(self, step):
+        i = self.ring_slot(step)
+        if self.ring_step[i] != step:
+            raise ScheduleViolation(f"snapshot for step {step} not in ring")
+        return self.ring[i][2]
+
+    def copy_targets(self, step):
+        """(vec, mat) buffers the optimizer fills with the weights for `step`."""
+        i = self.ring_slot(step)
+        self.ring_step[i] = step
+        vec, mat, _ = self.ring[i]
+        return vec, mat
+
+    def nbytes(self):
+        return (self.master.numel() * 4 * (2 if self.m is None else 4)
+                + sum(v.numel() * 4 + m.numel() * m.element_size() for v, m, _ in self.ring))
+
+
+class TiedMatrix:
+    """The shared input-embedding / output-projection matrix V on the
+    Ouroboros device (model.py:55-59)."""
+
+    def __init__(self, vocab, d, device, cdtype):
+        self.vocab, self.d, self.device, self.cdtype = vocab, d, device, cdtype
+        self.master = torch.zeros(vocab, d, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(vocab, d, dtype=torch.float32, device=device)
+        self.m = self.v = None
+        self.compute = self.master if cdtype == torch.float32 else torch.empty(vocab, d, dtype=cdtype, device=device)
+
+    def refresh(self):
+        if self.compute is not self.master:
+            ops.cast(self.master, self.compute)
+
+
+class LayerStack:
+    """The unpartitioned model (model.py:36-50): `layers`, `params` (per-layer
+    dicts of fp32 master views; embedding and projection dicts share the one
+    `tied` tensor) and `tied`."""
+
+    def __init__(self, layers, storage, tied, runtime, cdtype):
+        self.layers = layers
+        self.storage = storage
+        self.tied_store = tied
+        self.tied = tied.master
+        self.runtime = runtime
+        self.cdtype = cdtype
+        self.params = []
+        for layer, st in zip(layers, storage):
+            p = dict(st.params)
+            if layer.kind in ("embedding", "projection"):
+                p = {"tied": self.tied, **p}
+            self.params.append(p)
+
+    @property
+    def num_layers(self):
+        return len(self.layers)
+
+
+def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, *, dtype="bf16",
+                device=None):
+    """Same draw order and scales as the reference (model.py:53-60,
+    layers.py:107-112, 149-166): V ~ U(+-1/sqrt(d)) first, then per layer the
+    position table and wq, wk, wv, wo, w1 (1/sqrt(d)) and w2 (1/sqrt(f));
+    gains 1, biases 0.  The stream is evaluated on the device."""
+    if model_dim % 8 or ffn_dim % 8:
+        raise DimensionError("model_dim and ffn_dim must be multiples of 8 (TMA 16-byte rows)")
+    rt = Runtime.get(device)
+    cdt = _dtype_of(dtype)
+    layers = [EmbeddingLayer(vocab_size, model_dim, seq_len, dropout_p)]
+    layers += [TransformerBlockLayer(model_dim, ffn_dim, dropout_p) for _ in range(n_blocks)]
+    layers.append(OutputProjectionLayer(vocab_size, model_dim))
+    storage = [LayerParams(layer, rt.device, cdt) for layer in layers]
+    tied = TiedMatrix(vocab_size, model_dim, rt.device, cdt)
+    with torch.cuda.device(rt.device):
+        _init_params(layers, storage, tied, init_seed)
+        tied.refresh()
+    return LayerStack(layers, storage, tied, rt, cdt)
+
+
+def _init_params(layers, storage, tied, init_seed):
+    seed = mix64(init_seed)
+    pos = 0
+    d = tied.d
+    sd = 1.0 / math.sqrt(d)
+
+    def draw(dst, scale):
+        nonlocal pos
+        if dst.is_contiguous():
+            ops.init_uniform(dst, seed, pos, scale)
+        else:
+            tmp = torch.empty(dst.shape, dtype=torch.float32, device=dst.device)
+            ops.init_uniform(tmp, seed, pos, scale)
+            dst.copy_(tmp)
+        pos += dst.numel()
+
+    draw(tied.master, sd)
+    for layer, st in zip(layers, storage):
+        P = st.params
+        if layer.kind == "embedding":
+            draw(P["pos"], sd)
+        elif layer.kind == "block":
+            P["ln1_g"].fill_(1.0)
+            P["ln2_g"].fill_(1.0)
+            for w in ("wq", "wk", "wv", "wo", "w1"):
+                draw(P[w], sd)
+            draw(P["w2"], 1.0 / math.sqrt(layer.ffn_dim))
+
+
+# ---------------------------------------------------------------------------
+# partition (model.py:63-141) -- pure integer logic
+
+
+@dataclass
+class ModulePartition:
+    k: int
+    groups: list
+    device_of: list
+
+    def __post_init__(self):
+        if len(self.groups) != self.k or len(self.device_of) != self.k:
+            raise PartitionError("group/device lists must have K entries")
+        nxt = 0
+        for lo, hi in self.groups:
+            if lo != nxt or hi <= lo:
+                raise PartitionError("groups must be contiguous, ordered, nonempty")
+            nxt = hi
+        if self.k >= 2 and self.device_of[0] != self.device_of[-1]:
+            raise PartitionError("first and last module must share a device")
+
+    @property
+    def num_devices(self):
+        return len(set(self.device_of))
+
+
+def _balanced(L, K):
+    q, r = divmod(L, K)
+    return [q + (i < r) for i in range(K)]
+
+
+def _minmax(costs, K):
+    """Contiguous split of `costs` into K groups minimising the largest group
+    sum; ties resolved towards the earliest cut (reference DP order)."""
+    L = len(costs)
+    pre = [0.0]
+    for c in costs:
+        pre.append(pre[-1] + float(c))
+    INF = float("inf")
+    best = [[INF] * (L + 1) for _ in range(K + 1)]
+    cut = [[0] * (L + 1) for _ in range(K + 1)]
+    best[0][0] = 0.0
+    for k in range(1, K + 1):
+        for j in range(k, L - (K - k) + 1):
+            for i in range(k - 1, j):
+                if best[k - 1][i] == INF:
+                    continue
+                val = max(best[k - 1][i], pre[j] - pre[i])
+                if val < best[k][j]:
+                    best[k][j], cut[k][j] = val, i
+    sizes, j = [], L
+    for k in range(K, 0, -1):
+        i = cut[k][j]
+        sizes.append(j - i)
+        j = i
+    return sizes[::-1]
+
+
+def partition(L, K, balance="even", costs=None):
+    """K contiguous groups over L layers; modules 1 and K share device 0, so
+    K modules occupy K-1 devices (ring placement, model.py:115-141)."""
+    if not 1 <= K <= L:
+        raise PartitionError(f"need 1 <= K <= L, got K={K}, L={L}")
+    if balance == "even":
+        sizes = _balanced(L, K)
+    elif balance == "by_cost":
+        if costs is None or len(costs) != L:
+            raise PartitionError("by_cost needs one cost per layer")
+        sizes = _minmax(costs, K)
+    else:
+        raise PartitionError(f"unknown balance mode {balance!r}")
+    groups, lo = [], 0
+    for s in sizes:
+        groups.append((lo, lo + s))
+        lo += s
+    device_of = [0] if K == 1 else [0, *range(1, K - 1), 0]
+    return ModulePartition(K, groups, device_of)
+
+
+# ---------------------------------------------------------------------------
+# modules
+
+
+@dataclass
+class StaleSlot:
+    step: int
+    sample_id: int
+    inputs: object
+    targets: object
+    layer_seeds: list
+    arena: object = None
+
+
+class _Arena:
+    """Device storage of one stale slot: module input, every block's tape,
+    tokens (embedding module) / targets + head state (projection module)."""
+
+    def __init__(self, module, B, T):
+        dev, cdt = module.device, module.cdtype
+        d, Nt = module.d, B * T
+        self.B, self.T = B, T
+        self.tokens = torch.empty(B, T, dtype=torch.int64, device=dev) if module.has_embedding else None
+        self.targets = torch.empty(Nt, dtype=torch.int64, device=dev) if module.has_projection else None
+        n_acts = module.n_blocks + (1 if module.has_projection else 0)
+        self.acts = [torch.empty(Nt, d, dtype=cdt, device=dev) for _ in range(n_acts)]
+        self.tapes = [LY.BlockTape(B, T, d, module.f, cdt, dev) for _ in range(module.n_blocks)]
+        self.head = LY.HeadState(Nt, dev) if module.has_projection else None
+
+
+class ModuleState:
+    """One pipeline module (model.py:199-304) resident on one device."""
+
+    def __init__(self, index, k_total, layer_range, layers, params, dropout_seed, *, storage=None, tied=None,
+                 runtime=None, cdtype=torch.bfloat16):
+        self.index, self.k_total, self.layer_range = index, k_total, layer_range
+        self.layers, self.params = layers, params
+        self.storage = storage
+        self.tied = tied
+        self.runtime = runtime
+        self.device = runtime.device
+        self.cdtype = cdtype
+        self.dropout_seed = dropout_seed
+        self.slot_capacity = k_total - index + 1
+        self.slots = deque()
+        self.peak_slot_floats = 0
+        self.peak_slots = 0
+        self.has_embedding = layers[0].kind == "embedding"
+        self.has_projection = layers[-1].kind == "projection"
+        self.block_idx = [i for i, l in enumerate(layers) if l.kind == "block"]
+        self.n_blocks = len(self.block_idx)
+        ref = layers[self.block_idx[0]] if self.block_idx else layers[0]
+        self.d = ref.model_dim
+        self.f = layers[self.block_idx[0]].ffn_dim if self.block_idx else 8
+        self.vocab = tied.vocab if tied is not None else None
+        self.dropout_p = getattr(layers[0], "dropout_p", 0.0) if not self.block_idx else layers[self.block_idx[0]].dropout_p
+        if self.has_embedding:
+            self.dropout_p = layers[0].dropout_p
+        for st in storage:
+            st.configure_ring(self.slot_capacity)
+        self._arenas = [None] * self.slot_capacity
+        self._shape = None
+        self.ws_fwd = LY.Workspace(self.device)
+        self.ws_bwd = LY.Workspace(self.device)
+        start = layer_range[0]
+        self.grad_views = {}
+        for off, st in enumerate(storage):
+            for name, t in st.grads.items():
+                self.grad_views[f"L{start + off}.{name}"] = t
+        self._standalone_tied = None
+        self.last_forward_step = None
+
+    # -- seeds / snapshots -------------------------------------------------
+    def _layer_seed(self, step, offset):
+        return mix64(self.dropout_seed, step, self.layer_range[0] + offset)
+
+    def snapshot(self, step):
+        for st in self.storage:
+            st.ensure(step)
+
+    def _arena(self, step, B, T):
+        if self._shape != (B, T):
+            if self.slots:
+                raise DimensionError("batch shape changed while stale slots are pending")
+            self._arenas = [None] * self.slot_capacity
+            self._shape = (B, T)
+        i = step % self.slot_capacity
+        if self._arenas[i] is None:
+            self._arenas[i] = _Arena(self, B, T)
+        return self._arenas[i]
+
+    def input_buffer(self, step, B, T):
+        """Where the upstream module should write this module's input."""
+        a = self._arena(step, B, T)
+        return a.acts[0] if a.acts else None
+
+    # -- forward -----------------------------------------------------------
+    def forward(self, x, step, sample_id, targets=None, train=True, out=None):
+        """Run the slice at the live weights of `step` and queue a stale slot.
+        Returns the output activations [B*T, d], or for the projection module
+        the mean cross-entropy as a 0-d device tensor."""
+        if self.has_embedding:
+            B, T = x.shape
+        else:
+            B, T = self._shape if x is None else (None, None)
+            if x is not None:
+                Nt = x.numel() // self.d
+                B, T = (x.shape[0], x.shape[1]) if x.dim() == 3 else self._infer_bt(Nt)
+        seeds = [self._layer_seed(step, i) for i in range(len(self.layers))]
+        arena = self._arena(step, B, T)
+        if self.has_embedding:
+            arena.tokens.copy_(x if torch.is_tensor(x) else torch.as_tensor(x), non_blocking=True)
+        elif x is not None and arena.acts and x.data_ptr() != arena.acts[0].data_ptr():
+            arena.acts[0].copy_(x.reshape(B * T, self.d))
+        if self.has_projection:
+            if targets is None:
+                raise ScheduleViolation("projection module slot lacks targets")
+            tt = targets if torch.is_tensor(targets) else torch.as_tensor(targets)
+            arena.targets.copy_(tt.reshape(-1), non_blocking=True)
+        slot = StaleSlot(step, sample_id, arena.acts[0] if arena.acts else arena.tokens, targets, seeds, arena)
+        self.slots.append(slot)
+        if len(self.slots) > self.slot_capacity:
+            self.slots.pop()
+            raise ScheduleViolation(f"module {self.index} slot queue exceeded {self.slot_capacity}")
+        self.peak_slots = max(self.peak_slots, len(self.slots))
+        stored = len(self.slots) * B * T * (1 if self.has_embedding else self.d)
+        self.peak_slot_floats = max(self.peak_slot_floats, stored)
+        self.last_forward_step = step
+        return self._run_forward(step, arena, seeds, train, out, self.ws_fwd)
+
+    def _infer_bt(self, Nt):
+        if self._shape is not None and self._shape[0] * self._shape[1] == Nt:
+            return self._shape
+        raise DimensionError("pass module inputs as [B, T, d] to fix the batch shape")
+
+    def _run_forward(self, wstep, arena, seeds, train, out, ws):
+        B, T = arena.B, arena.T
+        flag = self.runtime.flag
+        nxt = 0  # next act buffer to fill
+        cur = None
+        for off, layer in enumerate(self.layers):
+            st = self.storage[off]
+            p = layer.dropout_p if hasattr(layer, "dropout_p") else 0.0
+            drop = LY.Dropout.make(seeds[off], p, train)
+            if layer.kind == "embedding":
+                dst = arena.acts[0] if arena.acts else out
+                Wv = st.weights(wstep)
+                LY.embed_forward(self.tied.compute, Wv["pos"], arena.tokens, dst, self.vocab, drop, flag)
+                cur = dst
+                nxt = 1
+            elif layer.kind == "block":
+                j = self.block_idx.index(off)
+                x_in = arena.acts[j]
+                last_act = j + 1 >= len(arena.acts)
+                dst = out if last_act else arena.acts[j + 1]
+                if dst is None:
+                    dst = self.ws_fwd.get("module_out", (B * T, self.d), self.cdtype)
+                W = st.weights(wstep)
+                LY.block_forward(W, W, x_in, dst.view(B * T, self.d), arena.tapes[j], B, T, drop, ws, flag)
+                cur = dst
+                nxt = j + 2
+            else:  # projection + fused CE head
+                h = arena.acts[-1]
+                LY.head_forward(h, self.tied.compute, arena.targets, self.vocab, arena.head, ws, flag)
+                return arena.head.loss
+        return cur
+
+    # -- backward ----------------------------------------------------------
+    def pop_slot(self):
+        if not self.slots:
+            raise ScheduleViolation(f"module {self.index} has no pending slot")
+        return self.slots.popleft()
+
+    def recompute_backward(self, slot, grad_out, stale_mode="snapshot", train=True, *, g_in=None, emb=None,
+                           live_step=None):
+        """Delayed backward for one slot (model.py:250-293).
+
+        "snapshot": gradients at the weights the slot's forward used (the
+        ring entry for slot.step), from the stored intermediates.
+        "current": re-run the forward at the live weights, then backprop.
+        `emb=(alpha, beta, grad)` fuses the tied gradient into `grad`
+        (output side alpha*Vo written, input side beta*Vi added); without
+        it the two tied gradients are returned separately like the reference.
+        Returns (g_in, grads, {"Vi", "Vo"}, loss)."""
+        arena = slot.arena
+        B, T = arena.B, arena.T
+        Nt, d = B * T, self.d
+        if stale_mode == "snapshot":
+            wstep = slot.step
+            for st in self.storage:
+                st.weights(wstep)  # raises ScheduleViolation when evicted
+        elif stale_mode == "current":
+            wstep = live_step if live_step is not None else self.last_forward_step
+            self._run_forward(wstep, arena, slot.layer_seeds, train, None, self.ws_bwd)
+        else:
+            raise ValueError(f"unknown stale_weights mode {stale_mode!r}")
+        ws = self.ws_bwd
+        tied_out = {"Vi": None, "Vo": None}
+        if emb is None:
+            emb_alpha, emb_beta = 1.0, 1.0
+            vo_buf = vi_buf = None
+            if self.has_projection:
+                vo_buf = torch.empty(self.vocab, d, dtype=torch.float32, device=self.device)
+            if self.has_embedding:
+                vi_buf = torch.zeros(self.vocab, d, dtype=torch.float32, device=self.device)
+            tied_out = {"Vi": vi_buf, "Vo": vo_buf}
+        else:
+            emb_alpha, emb_beta, emb_grad = emb
+            vo_buf = emb_grad if emb_alpha else None
+            vi_buf = emb_grad if emb_beta else None
+        loss = None
+        g = None
+        if self.has_projection:
+            g = ws.get("g_stream_a", (Nt, d), torch.float32)
+            LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
+                             emb_alpha, ws)
+            loss = arena.head.loss
+        else:
+            if grad_out is None:
+                raise ScheduleViolation(f"module {self.index} missing boundary gradient")
+            g = grad_out.reshape(Nt, d)
+        ping = 0
+        for j in range(self.n_blocks - 1, -1, -1):
+            off = self.block_idx[j]
+            st = self.storage[off]
+            W = st.weights(wstep)
+            drop = LY.Dropout.make(slot.layer_seeds[off], self.layers[off].dropout_p, train)
+            first = j == 0 and not self.has_embedding
+            if first and g_in is not None:
+                g_next = g_in.reshape(Nt, d)
+            else:
+                g_next = ws.get("g_stream_b" if ping == 0 else "g_stream_a", (Nt, d), torch.float32)
+                ping ^= 1
+            LY.block_backward(W, W, arena.acts[j], arena.tapes[j], g, g_next, st.G, B, T, drop, ws)
+            g = g_next
+        if self.has_embedding:
+            st = self.storage[0]
+            drop = LY.Dropout.make(slot.layer_seeds[0], self.layers[0].dropout_p, train)
+            LY.embed_backward(g, arena.tokens, self.layers[0].max_seq_len, st.G["pos"],
+                              vi_buf, emb_beta, ws, drop)
+            return None, self.grad_views, tied_out, loss
+        if g_in is not None:
+            if g.data_ptr() != g_in.data_ptr():
+                g_in.reshape(Nt, d).copy_(g)
+            return g_in, self.grad_views, tied_out, loss
+        return g.clone().view(B, T, d), self.grad_views, tied_out, loss
+
+    def zero_grads(self):
+        for st in self.storage:
+            st.grad.zero_()
+        return self.grad_views
+
+
+def build_modules(stack, part, dropout_seed):
+    modules = []
+    for k, (lo, hi) in enumerate(part.groups, start=1):
+        modules.append(ModuleState(k, part.k, (lo, hi), stack.layers[lo:hi], stack.params[lo:hi], dropout_seed,
+                                   storage=stack.storage[lo:hi], tied=stack.tied_store, runtime=stack.runtime,
+                                   cdtype=stack.cdtype))
+    return modules

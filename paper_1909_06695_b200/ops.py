@@ -44,19 +44,24 @@ def _mat3(t, name):
 
 
 def tf32_split(x):
-    """(hi, lo) with hi = x truncated to tf32, lo = x - hi (both fp32)."""
+    """(hi, lo): x rounded to tf32 and the tf32-rounded remainder (both fp32).
+
+    Outputs keep x's shape but with rows padded to 16 bytes so that TMA can
+    address them whatever the logical width."""
     _require_cuda(x)
     if x.dtype != torch.float32:
         raise DimensionError("tf32_split takes fp32")
-    hi = torch.empty_like(x, memory_format=torch.contiguous_format)
-    lo = torch.empty_like(hi)
-    cols = x.shape[-1]
-    rows = x.numel() // max(cols, 1)
     if x.stride(-1) != 1 or (x.dim() == 3 and x.stride(0) != x.shape[1] * x.stride(1)):
         x = x.contiguous()
+    cols = x.shape[-1]
+    rows = x.numel() // max(cols, 1)
+    ld_dst = (cols + 3) // 4 * 4
+    shape = tuple(x.shape[:-1]) + (ld_dst,)
+    hi = torch.empty(shape, dtype=torch.float32, device=x.device)
+    lo = torch.empty_like(hi)
     ld = x.stride(-2) if x.dim() >= 2 else cols
-    N.check(N.lib().rp_tf32_split(_ptr(x), _ptr(hi), _ptr(lo), rows, cols, ld, cols, _stream()), "tf32_split")
-    return hi, lo
+    N.check(N.lib().rp_tf32_split(_ptr(x), _ptr(hi), _ptr(lo), rows, cols, ld, ld_dst, _stream()), "tf32_split")
+    return hi[..., :cols], lo[..., :cols]
 
 
 def gemm(
@@ -165,3 +170,114 @@ def gemm(
 
 def gemm_tile_n(n):
     return N.lib().rp_gemm_tile_n(n)
+
+
+# ---------------------------------------------------------------------------
+# row kernels
+
+
+def _dtc(t):
+    return _DT[t.dtype]
+
+
+def layernorm_fwd(x, gain, bias, y, mean, rstd, flag=None):
+    rows, d = x.numel() // x.shape[-1], x.shape[-1]
+    N.check(N.lib().rp_layernorm_fwd(_dtc(x), _ptr(x), _ptr(gain), _ptr(bias), _ptr(y), _ptr(mean), _ptr(rstd),
+                                     rows, d, _ptr(flag), _stream()), "layernorm_fwd")
+
+
+def layernorm_bwd_blocks(rows):
+    return N.lib().rp_layernorm_bwd_blocks(rows)
+
+
+def layernorm_bwd(dy, x, mean, rstd, gain, dx, part_g, part_b, resid_grad=None, dx_masked=None, dropout=None):
+    rows, d = x.numel() // x.shape[-1], x.shape[-1]
+    seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    N.check(N.lib().rp_layernorm_bwd(_dtc(x), _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gain),
+                                     _ptr(resid_grad), _ptr(dx), _ptr(dx_masked), seed, thr, scale,
+                                     int(dropout is not None), _ptr(part_g), _ptr(part_b), rows, d, _stream()),
+            "layernorm_bwd")
+
+
+def colsum_blocks(rows):
+    return N.lib().rp_colsum_blocks(rows)
+
+
+def colsum_partial(x, part):
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    N.check(N.lib().rp_colsum_partial(_dtc(x), _ptr(x), rows, cols, x.stride(-2), _ptr(part), _stream()),
+            "colsum_partial")
+
+
+def colsum_finish(part, nblk, out):
+    N.check(N.lib().rp_colsum_finish(_ptr(part), nblk, out.numel(), _ptr(out), _stream()), "colsum_finish")
+
+
+def mask_grad(g, out, pos0, dropout, part):
+    rows, d = g.numel() // g.shape[-1], g.shape[-1]
+    seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    N.check(N.lib().rp_mask_grad(_dtc(out), _ptr(g), _ptr(out), rows, d, seed, pos0, thr, scale,
+                                 int(dropout is not None), _ptr(part), _stream()), "mask_grad")
+
+
+def softmax_causal(scores, probs):
+    """scores fp32 [B,T,>=T] view -> probs [B,T,T] view (row stride from probs)."""
+    B, T = scores.shape[0], scores.shape[1]
+    if scores.stride(1) != probs.stride(1):
+        raise DimensionError("scores/probs row strides differ")
+    N.check(N.lib().rp_softmax_causal(_dtc(probs), _ptr(scores), _ptr(probs), B * T, T, probs.stride(1), _stream()),
+            "softmax_causal")
+
+
+def softmax_bwd(grad_probs, probs, grad_scores, scale):
+    B, T = probs.shape[0], probs.shape[1]
+    N.check(N.lib().rp_softmax_bwd(_dtc(probs), _ptr(grad_probs), _ptr(probs), _ptr(grad_scores), scale, B * T, T,
+                                   probs.stride(1), _stream()), "softmax_bwd")
+
+
+def embed_fwd(tokens, tied, pos, out, vocab, dropout=None, flag=None):
+    B, T = tokens.shape
+    d = tied.shape[1]
+    seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    N.check(N.lib().rp_embed_fwd(_dtc(out), _ptr(tokens), _ptr(tied), _ptr(pos), _ptr(out), B, T, d, vocab, seed,
+                                 thr, scale, int(dropout is not None), _ptr(flag), _stream()), "embed_fwd")
+
+
+def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None):
+    B, T = tokens.shape
+    d = grad.shape[-1]
+    seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, seed, thr, scale,
+                                 int(dropout is not None), _ptr(grad_pos), _ptr(emb_grad), beta, _ptr(work),
+                                 _stream()), "embed_bwd")
+
+
+def ce_finish(partial, target_logit, targets, vocab, lse, loss_rows, loss, loss64=None, flag=None):
+    rows, ntiles = partial.shape[0], partial.shape[1]
+    N.check(N.lib().rp_ce_finish(_ptr(partial), ntiles, _ptr(target_logit), _ptr(targets), vocab, rows, _ptr(lse),
+                                 _ptr(loss_rows), _ptr(loss), _ptr(loss64), _ptr(flag), _stream()), "ce_finish")
+
+
+def adam_step(w, g, m, v, copy, n, lr, b1, b2, eps, c1, c2, flag=None):
+    cd = _dtc(copy) if copy is not None else N.F32
+    N.check(N.lib().rp_adam_step(_ptr(w), _ptr(g), _ptr(m), _ptr(v), _ptr(copy), cd, n, lr, b1, b2, eps, c1, c2,
+                                 _ptr(flag), _stream()), "adam_step")
+
+
+def sgd_step(w, g, copy, n, lr, flag=None):
+    cd = _dtc(copy) if copy is not None else N.F32
+    N.check(N.lib().rp_sgd_step(_ptr(w), _ptr(g), _ptr(copy), cd, n, lr, _ptr(flag), _stream()), "sgd_step")
+
+
+def init_uniform(out, seed, pos0, scale):
+    N.check(N.lib().rp_init_uniform(_ptr(out), out.numel(), seed & ((1 << 64) - 1), pos0, float(scale), _stream()),
+            "init_uniform")
+
+
+def cast(src, dst):
+    N.check(N.lib().rp_cast(_ptr(src), _dtc(src), _ptr(dst), _dtc(dst), src.numel(), _stream()), "cast")
+
+
+def sq_norm(x, part, out, accumulate=False):
+    N.check(N.lib().rp_sq_norm(_ptr(x), x.numel(), _ptr(part), _ptr(out), int(accumulate), _stream()), "sq_norm")

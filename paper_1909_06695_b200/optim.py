@@ -1,0 +1,171 @@
+"""Optimizers applied to delayed-gradient packets, plus LR schedules.
+
+Drop-in for reference optim.py: `LrSchedule`, `SgdOptimizer`,
+`AdamOptimizer`, `make_optimizer` with the same arguments, the same global
+bias-correction clock (optim.py:99-112) and zero-padded early gradients fed
+as literal zeros.  `apply` launches one fused update per layer buffer
+(csrc/optim.cu): fp32 master, moments and gradient are read once, and the
+compute-dtype copy of the new weights is written straight into the module's
+next snapshot-ring slot.
+"""
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+
+
+@dataclass
+class LrSchedule:
+    """fixed | diminishing base/(1+t) | linear warm-up then cosine to zero."""
+
+    base: float
+    mode: str = "fixed"
+    warmup_steps: int = 0
+    total_steps: int = 0
+
+    def __post_init__(self):
+        if self.base <= 0:
+            raise ValueError("base learning rate must be positive")
+        if self.mode not in ("fixed", "diminishing", "warmup-cosine"):
+            raise ValueError(f"unknown schedule mode {self.mode!r}")
+        if self.mode == "warmup-cosine" and self.warmup_steps >= self.total_steps:
+            raise ValueError("warm-up must end before total_steps in cosine mode")
+
+    def at(self, t):
+        if t < 0:
+            raise ValueError("step must be >= 0")
+        if self.mode == "fixed":
+            return self.base
+        if self.mode == "diminishing":
+            return self.base / (1.0 + t)
+        if t < self.warmup_steps:
+            return self.base * (t + 1) / self.warmup_steps
+        x = (t - self.warmup_steps) / (self.total_steps - self.warmup_steps)
+        return self.base * 0.5 * (1.0 + math.cos(math.pi * x))
+
+
+def _targets(module, t):
+    return [st.copy_targets(t + 1) for st in module.storage]
+
+
+class _Base:
+    def _each(self, t, modules, tied, fn):
+        flag = None
+        for m in modules:
+            flag = m.runtime.flag
+            for st, (vec_dst, mat_dst) in zip(m.storage, _targets(m, t)):
+                n = st.master.numel()
+                if n == 0:
+                    continue
+                fn(st, 0, st.n_vec, vec_dst)
+                fn(st, st.n_vec, n, mat_dst)
+        return flag
+
+
+class SgdOptimizer(_Base):
+    name = "sgd"
+
+    def __init__(self, schedule):
+        self.schedule = schedule
+
+    def apply(self, t, packet, modules, tied):
+        lr = self.schedule.at(t)
+        flag = _flag_of(modules)
+
+        def fn(st, lo, hi, dst):
+            if hi > lo:
+                ops.sgd_step(st.master[lo:hi], st.grad[lo:hi], dst, hi - lo, lr, flag)
+
+        self._each(t, modules, tied, fn)
+        if tied is not None:
+            store = _tied_store(modules)
+            copy = None if store.compute is store.master else store.compute
+            ops.sgd_step(store.master, store.grad, copy, store.master.numel(), lr, _flag_of(modules))
+        return lr
+
+    def state_arrays(self):
+        return {}
+
+    def load_state_arrays(self, arrays):
+        if arrays:
+            raise ValueError("sgd carries no optimizer state")
+
+
+class AdamOptimizer(_Base):
+    name = "adam"
+
+    def __init__(self, schedule, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.schedule = schedule
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self._mods = []
+
+    @staticmethod
+    def _moments(obj):
+        if obj.m is None:
+            obj.m = torch.zeros_like(obj.master)
+            obj.v = torch.zeros_like(obj.master)
+        return obj.m, obj.v
+
+    def apply(self, t, packet, modules, tied):
+        lr = self.schedule.at(t)
+        c1 = 1.0 - self.beta1 ** (t + 1)
+        c2 = 1.0 - self.beta2 ** (t + 1)
+        flag = _flag_of(modules)
+        self._mods = modules
+
+        def fn(st, lo, hi, dst):
+            if hi > lo:
+                m, v = self._moments(st)
+                ops.adam_step(st.master[lo:hi], st.grad[lo:hi], m[lo:hi], v[lo:hi], dst, hi - lo, lr, self.beta1,
+                              self.beta2, self.eps, c1, c2, flag)
+
+        self._each(t, modules, tied, fn)
+        if tied is not None:
+            store = _tied_store(modules)
+            m, v = self._moments(store)
+            copy = None if store.compute is store.master else store.compute
+            ops.adam_step(store.master, store.grad, m, v, copy, store.master.numel(), lr, self.beta1, self.beta2,
+                          self.eps, c1, c2, flag)
+        return lr
+
+    def state_arrays(self):
+        """Moments keyed like the reference (optim.py:128-135)."""
+        out = {}
+        for m in self._mods:
+            start = m.layer_range[0]
+            for off, st in enumerate(m.storage):
+                if st.m is None:
+                    continue
+                for name, view in st.params.items():
+                    rel = view.data_ptr() - st.master.data_ptr()
+                    sl = lambda buf: buf.view(-1)[rel // 4: rel // 4 + view.numel()]  # noqa: E731
+                    out[f"adam.m.L{start + off}.{name}"] = sl(st.m)
+                    out[f"adam.v.L{start + off}.{name}"] = sl(st.v)
+        if self._mods:
+            store = _tied_store(self._mods)
+            if store is not None and store.m is not None:
+                out["adam.m.tied"] = store.m
+                out["adam.v.tied"] = store.v
+        return out
+
+
+def _flag_of(modules):
+    return modules[0].runtime.flag if modules else None
+
+
+def _tied_store(modules):
+    for m in modules:
+        if m.tied is not None:
+            return m.tied
+    return None
+
+
+def make_optimizer(kind, schedule, beta1=0.9, beta2=0.999, eps=1e-8):
+    if kind == "sgd":
+        return SgdOptimizer(schedule)
+    if kind == "adam":
+        return AdamOptimizer(schedule, beta1, beta2, eps)
+    raise ValueError(f"unknown optimizer {kind!r}")
