@@ -165,6 +165,63 @@ int rp_cast(const void* in, int32_t in_dtype, void* out, int32_t out_dtype, int6
 /* out (+)= sum x^2 in fp64; part: >= 296 doubles of scratch (engine.py:72-80) */
 int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t accumulate, void* stream);
 
+
+/* ---- layer-level entry points: the reference layer protocol ------------------
+ * TransformerBlockLayer.forward/backward (layers.py:168-253) and the projection
+ * layer + loss_and_head_backward (layers.py:268-322) as single native calls. */
+typedef struct rp_block_desc {
+  int64_t B, T, d, f;
+  int32_t dtype;        /* rp_dtype of activations and matrix weights */
+  int32_t drop_enabled; /* train && p > 0 */
+  uint64_t drop_seed;   /* mix64(dropout_seed, step, layer), model.py:218-219 */
+  uint64_t drop_threshold;
+  float drop_scale;
+} rp_block_desc;
+
+typedef struct rp_block_weights {
+  const void* wqkv; /* [d, 3d] = [wq | wk | wv] (dtype) */
+  const void* wo;   /* [d, d] */
+  const void* w1;   /* [d, f] */
+  const void* w2;   /* [f, d] */
+  const float *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2;
+} rp_block_weights;
+
+/* forward intermediates kept in a stale slot ("store-all"; the reference
+ * recomputes them, model.py:250-268, and proves the two bitwise equal) */
+typedef struct rp_block_tape {
+  void *a, *qkv, *probs, *ctx, *x1, *m, *h1; /* probs: [B, T, pad8(T)] */
+  float *mean1, *rstd1, *mean2, *rstd2;
+} rp_block_tape;
+
+typedef struct rp_block_grads {
+  float *wqkv, *wo, *w1, *w2, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2;
+} rp_block_grads;
+
+int64_t rp_block_workspace_bytes(const rp_block_desc* desc);
+int rp_block_forward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, void* out,
+                     const rp_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                     void* stream);
+/* g_x = dL/dx (fp32) from g_out = dL/dout (fp32); parameter grads (fp32) overwritten */
+int rp_block_backward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, const rp_block_tape* tape,
+                      const float* g_out, float* g_x, const rp_block_grads* grads, void* workspace,
+                      int64_t workspace_bytes, void* stream);
+
+typedef struct rp_head_desc {
+  int64_t rows, d, vocab;
+  int32_t dtype;
+} rp_head_desc;
+
+int64_t rp_head_workspace_bytes(const rp_head_desc* desc);
+/* mean CE of x @ tied^T vs targets without materialising logits; lse kept for backward */
+int rp_head_forward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets, float* lse,
+                    float* loss, double* loss64, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                    void* stream);
+/* g_x = dL/dx (fp32); vo (if non-NULL) = vo_alpha * dL/dtied from the output side
+ * (the fresh half of the mixed tied gradient, engine.py:54-69) */
+int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets,
+                     const float* lse, float* g_x, float* vo, float vo_alpha, void* workspace,
+                     int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,32 @@ class GemmArgs(ctypes.Structure):
     ]
 
 
+class BlockDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("d", ctypes.c_int64), ("f", ctypes.c_int64),
+                ("dtype", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_seed", ctypes.c_uint64),
+                ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float)]
+
+
+class BlockWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("wqkv", "wo", "w1", "w2", "ln1_g", "ln1_b", "ln2_g", "ln2_b",
+                                                 "b1", "b2")]
+
+
+class BlockTape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("a", "qkv", "probs", "ctx", "x1", "m", "h1", "mean1", "rstd1",
+                                                 "mean2", "rstd2")]
+
+
+class BlockGrads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("wqkv", "wo", "w1", "w2", "ln1_g", "ln1_b", "ln2_g", "ln2_b",
+                                                 "b1", "b2")]
+
+
+class HeadDesc(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("d", ctypes.c_int64), ("vocab", ctypes.c_int64),
+                ("dtype", ctypes.c_int32)]
+
+
 def lib():
     """The loaded library; raises ImportError when it is absent."""
     global _lib
@@ -100,6 +126,14 @@ def _declare(L):
         "rp_init_uniform": [vp, i64, u64, u64, f64, vp],
         "rp_cast": [vp, i32, vp, i32, i64, vp],
         "rp_sq_norm": [vp, i64, vp, vp, i32, vp],
+        "rp_block_workspace_bytes": [ctypes.POINTER(BlockDesc)],
+        "rp_block_forward": [ctypes.POINTER(BlockDesc), ctypes.POINTER(BlockWeights), vp, vp,
+                             ctypes.POINTER(BlockTape), vp, i64, vp, vp],
+        "rp_block_backward": [ctypes.POINTER(BlockDesc), ctypes.POINTER(BlockWeights), vp,
+                              ctypes.POINTER(BlockTape), vp, vp, ctypes.POINTER(BlockGrads), vp, i64, vp],
+        "rp_head_workspace_bytes": [ctypes.POINTER(HeadDesc)],
+        "rp_head_forward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
+        "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, vp, i64, vp],
     }
     L.rp_version.restype = ctypes.c_char_p
     for name, args in sig.items():
@@ -107,6 +141,8 @@ def _declare(L):
         fn.argtypes = args
         fn.restype = ctypes.c_int32
     L.rp_embed_bwd_workspace.restype = i64
+    L.rp_block_workspace_bytes.restype = i64
+    L.rp_head_workspace_bytes.restype = i64
 
 
 def last_error():

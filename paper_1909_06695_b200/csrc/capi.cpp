@@ -122,4 +122,27 @@ int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t acc
   return rp::sq_norm(x, n, part, out, accumulate, RP_S(stream));
 }
 
+int64_t rp_block_workspace_bytes(const rp_block_desc* desc) { return rp::block_workspace_bytes(*desc); }
+int rp_block_forward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, void* out,
+                     const rp_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                     void* stream) {
+  return rp::block_forward(*desc, *w, x, out, *tape, workspace, workspace_bytes, flag, RP_S(stream));
+}
+int rp_block_backward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, const rp_block_tape* tape,
+                      const float* g_out, float* g_x, const rp_block_grads* grads, void* workspace,
+                      int64_t workspace_bytes, void* stream) {
+  return rp::block_backward(*desc, *w, x, *tape, g_out, g_x, *grads, workspace, workspace_bytes, RP_S(stream));
+}
+int64_t rp_head_workspace_bytes(const rp_head_desc* desc) { return rp::head_workspace_bytes(*desc); }
+int rp_head_forward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets, float* lse,
+                    float* loss, double* loss64, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                    void* stream) {
+  return rp::head_forward(*desc, x, tied, targets, lse, loss, loss64, workspace, workspace_bytes, flag, RP_S(stream));
+}
+int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets,
+                     const float* lse, float* g_x, float* vo, float vo_alpha, void* workspace,
+                     int64_t workspace_bytes, void* stream) {
+  return rp::head_backward(*desc, x, tied, targets, lse, g_x, vo, vo_alpha, workspace, workspace_bytes, RP_S(stream));
+}
+
 }  // extern "C"

@@ -1,0 +1,343 @@
+// Native layer composition: one C-ABI call runs a whole transformer block
+// forward or backward, or the tied head, issuing its GEMMs and row kernels
+// back-to-back on the caller's stream.  This is the reference's layer
+// protocol seam (`forward(params, x, rng, train)` / `backward(params, tape,
+// grad_out)`, reference layers.py:28-37, 168-253, 299-322) with the Python
+// per-op dispatch removed from the hot loop.
+//
+// Scratch comes from a caller-owned device workspace (rp_*_workspace_bytes);
+// in tf32x3 mode every GEMM operand is split into (hi, lo) halves inside it.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "rp_internal.h"
+
+namespace rp {
+namespace {
+
+inline int64_t pad8(int64_t n) { return (n + 7) / 8 * 8; }
+inline int64_t al256(int64_t n) { return (n + 255) / 256 * 256; }
+inline int esize(int dt) { return dt == RP_BF16 ? 2 : 4; }
+
+struct Bump {
+  char* base;
+  int64_t cap, off = 0;
+  void* take(int64_t bytes) {
+    void* p = base + off;
+    off += al256(bytes);
+    return p;
+  }
+};
+
+// Row-major matrix view (optionally batched).
+struct Mat {
+  const void* p;
+  int64_t rows, cols, ld;
+  int64_t batch = 1, bstride = 0;
+};
+
+inline Mat mat(const void* p, int64_t rows, int64_t cols, int64_t ld) { return Mat{p, rows, cols, ld, 1, 0}; }
+inline Mat bmat(const void* p, int64_t b, int64_t rows, int64_t cols, int64_t ld, int64_t bs) {
+  return Mat{p, rows, cols, ld, b, bs};
+}
+
+struct Ctx {
+  int dtype;  // compute dtype of activations / weights
+  cudaStream_t st;
+  char* split_base = nullptr;  // tf32x3 split scratch
+  int64_t split_cap = 0;
+};
+
+struct Epi {
+  int kind = RP_EPI_STORE;
+  float alpha = 1.f;
+  const float* bias = nullptr;
+  const void* resid = nullptr;
+  int64_t ld_resid = 0, stride_resid = 0;
+  int drop = 0;
+  uint64_t seed = 0, thr = 0, pos0 = 0;
+  float scale = 1.f;
+  const int64_t* targets = nullptr;
+  const float* lse = nullptr;
+  float* partial = nullptr;
+  float* target_logit = nullptr;
+  float ce_scale = 0.f;
+};
+
+int split_into(Ctx& c, Bump& b, const Mat& m, const void** hi, const void** lo, int64_t* ld, int64_t* bs) {
+  const int64_t ldd = (m.cols + 3) / 4 * 4;
+  const int64_t n = m.batch * m.rows * ldd;
+  float* h = static_cast<float*>(b.take(n * 4));
+  float* l = static_cast<float*>(b.take(n * 4));
+  if (b.off > b.cap) return set_error(RP_ERR_INVALID, "tf32x3 split scratch too small");
+  for (int64_t i = 0; i < m.batch; ++i) {
+    const float* src = static_cast<const float*>(m.p) + i * m.bstride;
+    if (int e = tf32_split(src, h + i * m.rows * ldd, l + i * m.rows * ldd, m.rows, m.cols, m.ld, ldd, c.st)) return e;
+  }
+  *hi = h;
+  *lo = l;
+  *ld = ldd;
+  *bs = m.rows * ldd;
+  return RP_OK;
+}
+
+// C = epi(alpha * opA(A) opB(B)).  A: [M,K] (a_mn: stored [K,M]); B: stored [N,K] (b_mn: [K,N]).
+int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, int out_dtype, const Epi& e = Epi()) {
+  rp_gemm_args g;
+  std::memset(&g, 0, sizeof(g));
+  g.math = c.dtype == RP_BF16 ? RP_MATH_BF16 : RP_MATH_TF32X3;
+  g.out_dtype = out_dtype;
+  g.a_mn_major = a_mn;
+  g.b_mn_major = b_mn;
+  g.M = a_mn ? A.cols : A.rows;
+  g.K = a_mn ? A.rows : A.cols;
+  g.N = b_mn ? B.cols : B.rows;
+  g.batch = std::max(A.batch, B.batch);
+  g.A = A.p;
+  g.lda = A.ld;
+  g.stride_a = A.batch > 1 ? A.bstride : 0;
+  g.B = B.p;
+  g.ldb = B.ld;
+  g.stride_b = B.batch > 1 ? B.bstride : 0;
+  Bump sb{c.split_base, c.split_cap};
+  if (g.math == RP_MATH_TF32X3) {
+    int64_t ld, bs;
+    const void *hi, *lo;
+    if (int r = split_into(c, sb, A, &hi, &lo, &ld, &bs)) return r;
+    g.A = hi;
+    g.A_lo = lo;
+    g.lda = ld;
+    g.stride_a = A.batch > 1 ? bs : 0;
+    if (int r = split_into(c, sb, B, &hi, &lo, &ld, &bs)) return r;
+    g.B = hi;
+    g.B_lo = lo;
+    g.ldb = ld;
+    g.stride_b = B.batch > 1 ? bs : 0;
+  }
+  g.C = const_cast<void*>(C.p);
+  g.ldc = C.ld;
+  g.stride_c = C.bstride;
+  g.epilogue = e.kind;
+  g.alpha = e.alpha;
+  g.bias = e.bias;
+  g.residual = e.resid;
+  g.ld_residual = e.ld_resid;
+  g.stride_residual = e.stride_resid;
+  g.drop_enabled = e.drop;
+  g.drop_seed = e.seed;
+  g.drop_threshold = e.thr;
+  g.drop_pos0 = e.pos0;
+  g.drop_scale = e.scale;
+  g.targets = e.targets;
+  g.lse = e.lse;
+  g.partial = e.partial;
+  g.target_logit = e.target_logit;
+  g.ce_scale = e.ce_scale;
+  return gemm(g, c.st);
+}
+
+int64_t split_bytes(int dtype, int64_t max_elems) {
+  // two operands x (hi, lo), rows padded to 4 floats
+  return dtype == RP_BF16 ? 0 : 4 * al256((max_elems + 4096) * 4) + 4096;
+}
+
+#define RP_TRY(x)                 \
+  do {                            \
+    if (int _e = (x)) return _e;  \
+  } while (0)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// block
+
+int64_t block_workspace_bytes(const rp_block_desc& d) {
+  const int64_t N = d.B * d.T, Tp = pad8(d.T), e = esize(d.dtype);
+  const int64_t nbp = std::max<int64_t>(colsum_blocks(N), ln_bwd_blocks(N));
+  int64_t b = 0;
+  b += al256(d.B * d.T * Tp * 4);              // scores / g_p
+  b += al256(d.B * d.T * Tp * e);              // g_s
+  b += al256(N * d.d * e) * 3;                 // g_h2, g_proj, g_ctx
+  b += al256(N * d.f * e);                     // g_z1
+  b += al256(N * 3 * d.d * e);                 // g_qkv
+  b += al256(N * d.d * 4) * 3;                 // g_m, g_x1, g_a
+  b += al256(nbp * std::max(d.f, 3 * d.d) * 4) * 3;  // partials
+  b += split_bytes(d.dtype, std::max({N * d.f, d.B * d.T * Tp, N * 3 * d.d, d.d * d.f}));
+  return b + 4096;
+}
+
+int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void* x, void* out, const rp_block_tape& tp,
+                  void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st) {
+  if (ws_bytes < block_workspace_bytes(d)) return set_error(RP_ERR_INVALID, "block workspace too small");
+  const int64_t B = d.B, T = d.T, D = d.d, F = d.f, N = B * T, Tp = pad8(T);
+  const int dt = d.dtype, e = esize(dt);
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  float* scores = static_cast<float*>(bp.take(B * T * Tp * 4));
+  Ctx c{dt, st};
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  const char* qkv = static_cast<const char*>(tp.qkv);
+  RP_TRY(layernorm_fwd(dt, x, w.ln1_g, w.ln1_b, tp.a, tp.mean1, tp.rstd1, N, D, flag, st));
+  RP_TRY(mm(c, mat(tp.a, N, D, D), false, mat(w.wqkv, D, 3 * D, 3 * D), true, mat(tp.qkv, N, 3 * D, 3 * D), dt));
+  Epi es;
+  es.alpha = 1.f / std::sqrt(static_cast<float>(D));
+  RP_TRY(mm(c, bmat(qkv, B, T, D, 3 * D, T * 3 * D), false, bmat(qkv + D * e, B, T, D, 3 * D, T * 3 * D), false,
+            bmat(scores, B, T, T, Tp, T * Tp), RP_F32, es));
+  RP_TRY(softmax_causal(dt, scores, tp.probs, N, T, Tp, st));
+  RP_TRY(mm(c, bmat(tp.probs, B, T, T, Tp, T * Tp), false, bmat(qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D), true,
+            bmat(tp.ctx, B, T, D, D, T * D), dt));
+  Epi e0;
+  e0.kind = RP_EPI_BIAS_DROPOUT_RESIDUAL;
+  e0.resid = x;
+  e0.ld_resid = D;
+  e0.drop = d.drop_enabled;
+  e0.seed = d.drop_seed;
+  e0.thr = d.drop_threshold;
+  e0.scale = d.drop_scale;
+  e0.pos0 = 0;
+  RP_TRY(mm(c, mat(tp.ctx, N, D, D), false, mat(w.wo, D, D, D), true, mat(tp.x1, N, D, D), dt, e0));
+  RP_TRY(layernorm_fwd(dt, tp.x1, w.ln2_g, w.ln2_b, tp.m, tp.mean2, tp.rstd2, N, D, flag, st));
+  Epi e1;
+  e1.kind = RP_EPI_BIAS_RELU;
+  e1.bias = w.b1;
+  RP_TRY(mm(c, mat(tp.m, N, D, D), false, mat(w.w1, D, F, F), true, mat(tp.h1, N, F, F), dt, e1));
+  Epi e2 = e0;
+  e2.bias = w.b2;
+  e2.resid = tp.x1;
+  e2.pos0 = static_cast<uint64_t>(N * D);
+  RP_TRY(mm(c, mat(tp.h1, N, F, F), false, mat(w.w2, F, D, D), true, mat(out, N, D, D), dt, e2));
+  return RP_OK;
+}
+
+int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void* x, const rp_block_tape& tp,
+                   const float* g_out, float* g_x, const rp_block_grads& G, void* ws, int64_t ws_bytes,
+                   cudaStream_t st) {
+  if (ws_bytes < block_workspace_bytes(d)) return set_error(RP_ERR_INVALID, "block workspace too small");
+  const int64_t B = d.B, T = d.T, D = d.d, F = d.f, N = B * T, Tp = pad8(T);
+  const int dt = d.dtype, e = esize(dt);
+  const int nbc = colsum_blocks(N), nbl = ln_bwd_blocks(N);
+  const int64_t nbp = std::max<int64_t>(nbc, nbl);
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  float* g_p = static_cast<float*>(bp.take(B * T * Tp * 4));
+  void* g_s = bp.take(B * T * Tp * e);
+  void* g_h2 = bp.take(N * D * e);
+  void* g_proj = bp.take(N * D * e);
+  void* g_ctx = bp.take(N * D * e);
+  void* g_z1 = bp.take(N * F * e);
+  char* g_qkv = static_cast<char*>(bp.take(N * 3 * D * e));
+  float* g_m = static_cast<float*>(bp.take(N * D * 4));
+  float* g_x1 = static_cast<float*>(bp.take(N * D * 4));
+  float* g_a = static_cast<float*>(bp.take(N * D * 4));
+  const int64_t pw = std::max(F, 3 * D);
+  float* part = static_cast<float*>(bp.take(nbp * pw * 4));
+  float* pg = static_cast<float*>(bp.take(nbp * pw * 4));
+  float* pb = static_cast<float*>(bp.take(nbp * pw * 4));
+  Ctx c{dt, st};
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  const char* qkv = static_cast<const char*>(tp.qkv);
+  const float inv = 1.f / std::sqrt(static_cast<float>(D));
+  // feed-forward branch (layers.py:209-232)
+  RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(N * D), d.drop_threshold, d.drop_scale,
+                   d.drop_enabled, part, st));
+  RP_TRY(colsum_finish(part, nbc, D, G.b2, st));
+  RP_TRY(mm(c, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32));
+  Epi er;
+  er.kind = RP_EPI_RELU_GRAD;
+  er.resid = tp.h1;
+  er.ld_resid = F;
+  RP_TRY(mm(c, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er));
+  RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, st));
+  RP_TRY(colsum_finish(part, nbc, F, G.b1, st));
+  RP_TRY(mm(c, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32));
+  RP_TRY(mm(c, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32));
+  RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
+                       d.drop_threshold, d.drop_scale, d.drop_enabled, pg, pb, N, D, st));
+  RP_TRY(colsum_finish(pg, nbl, D, G.ln2_g, st));
+  RP_TRY(colsum_finish(pb, nbl, D, G.ln2_b, st));
+  // attention branch (layers.py:234-247)
+  RP_TRY(mm(c, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32));
+  RP_TRY(mm(c, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt));
+  const Mat q = bmat(qkv, B, T, D, 3 * D, T * 3 * D);
+  const Mat k = bmat(qkv + D * e, B, T, D, 3 * D, T * 3 * D);
+  const Mat v = bmat(qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D);
+  const Mat P = bmat(tp.probs, B, T, T, Tp, T * Tp);
+  const Mat gctx = bmat(g_ctx, B, T, D, D, T * D);
+  RP_TRY(mm(c, gctx, false, v, false, bmat(g_p, B, T, T, Tp, T * Tp), RP_F32));
+  RP_TRY(mm(c, P, true, gctx, true, bmat(g_qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D), dt));
+  RP_TRY(softmax_bwd(dt, g_p, tp.probs, g_s, inv, N, T, Tp, st));
+  const Mat gs = bmat(g_s, B, T, T, Tp, T * Tp);
+  RP_TRY(mm(c, gs, false, k, true, bmat(g_qkv, B, T, D, 3 * D, T * 3 * D), dt));
+  RP_TRY(mm(c, gs, true, q, true, bmat(g_qkv + D * e, B, T, D, 3 * D, T * 3 * D), dt));
+  RP_TRY(mm(c, mat(tp.a, N, D, D), true, mat(g_qkv, N, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32));
+  RP_TRY(mm(c, mat(g_qkv, N, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, N, D, D), RP_F32));
+  RP_TRY(layernorm_bwd(dt, g_a, x, tp.mean1, tp.rstd1, w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
+  RP_TRY(colsum_finish(pg, nbl, D, G.ln1_g, st));
+  RP_TRY(colsum_finish(pb, nbl, D, G.ln1_b, st));
+  return RP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tied head
+
+int64_t head_workspace_bytes(const rp_head_desc& h) {
+  const int bn = gemm_tile_n(h.vocab);
+  const int64_t nt = (h.vocab + bn - 1) / bn;
+  const int64_t e = esize(h.dtype);
+  int64_t b = al256(h.rows * nt * 2 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
+  b += split_bytes(h.dtype, std::max(h.rows * pad8(h.vocab), h.vocab * h.d));
+  return b + 4096;
+}
+
+int head_forward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, float* lse,
+                 float* loss, double* loss64, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st) {
+  if (ws_bytes < head_workspace_bytes(h)) return set_error(RP_ERR_INVALID, "head workspace too small");
+  const int bn = gemm_tile_n(h.vocab);
+  const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab;
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  float* partial = static_cast<float*>(bp.take(N * nt * 2 * 4));
+  float* zy = static_cast<float*>(bp.take(N * 4));
+  float* rows = static_cast<float*>(bp.take(N * 4));
+  bp.take(N * pad8(V) * esize(h.dtype));  // dz (backward)
+  Ctx c{h.dtype, st};
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  Epi e;
+  e.kind = RP_EPI_LSE_PARTIAL;
+  e.targets = targets;
+  e.partial = partial;
+  e.target_logit = zy;
+  RP_TRY(mm(c, mat(x, N, D, D), false, mat(tied, V, D, D), false, Mat{nullptr, N, V, 0}, RP_F32, e));
+  return ce_finish(partial, (int)nt, zy, targets, V, N, lse, rows, loss, loss64, flag, st);
+}
+
+int head_backward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, const float* lse,
+                  float* g_x, float* vo, float vo_alpha, void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < head_workspace_bytes(h)) return set_error(RP_ERR_INVALID, "head workspace too small");
+  const int bn = gemm_tile_n(h.vocab);
+  const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab, Vp = pad8(V);
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  bp.take(N * nt * 2 * 4);
+  bp.take(N * 4);
+  bp.take(N * 4);
+  void* dz = bp.take(N * Vp * esize(h.dtype));
+  Ctx c{h.dtype, st};
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  Epi e;
+  e.kind = RP_EPI_CE_GRAD;
+  e.targets = targets;
+  e.lse = lse;
+  e.ce_scale = 1.f / static_cast<float>(N);
+  RP_TRY(mm(c, mat(x, N, D, D), false, mat(tied, V, D, D), false, mat(dz, N, V, Vp), h.dtype, e));
+  RP_TRY(mm(c, mat(dz, N, V, Vp), false, mat(tied, V, D, D), true, mat(g_x, N, D, D), RP_F32));
+  if (vo) {
+    Epi ev;
+    ev.alpha = vo_alpha;
+    RP_TRY(mm(c, mat(dz, N, V, Vp), true, mat(x, N, D, D), true, mat(vo, V, D, D), RP_F32, ev));
+  }
+  return RP_OK;
+}
+
+}  // namespace rp

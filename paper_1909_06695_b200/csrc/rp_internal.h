@@ -48,4 +48,16 @@ int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double sca
 int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st);
 int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
 
+int64_t block_workspace_bytes(const rp_block_desc& d);
+int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void* x, void* out, const rp_block_tape& tp,
+                  void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);
+int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void* x, const rp_block_tape& tp,
+                   const float* g_out, float* g_x, const rp_block_grads& G, void* ws, int64_t ws_bytes,
+                   cudaStream_t st);
+int64_t head_workspace_bytes(const rp_head_desc& h);
+int head_forward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, float* lse,
+                 float* loss, double* loss64, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);
+int head_backward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, const float* lse,
+                  float* g_x, float* vo, float vo_alpha, void* ws, int64_t ws_bytes, cudaStream_t st);
+
 }  // namespace rp

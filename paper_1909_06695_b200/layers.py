@@ -107,7 +107,7 @@ def embed_backward(g, tokens, t_max, grad_pos, emb_grad, beta, ws, drop):
 # transformer block (layers.py:168-253)
 
 
-def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
+def block_forward_ops(W, vecs, x, out, tape, B, T, drop, ws, flag):
     """x, out: [B*T, d] compute dtype.  W: compute-dtype matrices; vecs: fp32."""
     d = x.shape[-1]
     n = B * T * d
@@ -123,13 +123,14 @@ def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
     ops.gemm(tape.ctx.view(B * T, d), W["wo"], b_mn=True, out=tape.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL,
              residual=x, dropout=d0)
     ops.layernorm_fwd(tape.x1, vecs["ln2_g"], vecs["ln2_b"], tape.m, tape.mean2, tape.rstd2, flag)
-    ops.gemm(tape.m, W["w1"], b_mn=True, out=tape.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+    with ops.span("ffn1_gemm"):
+        ops.gemm(tape.m, W["w1"], b_mn=True, out=tape.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
     d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
     ops.gemm(tape.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
              residual=tape.x1, dropout=d1)
 
 
-def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
+def block_backward_ops(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
     """g_out, g_x: [B*T, d] fp32 (g_x may alias g_out).  G: fp32 grad views."""
     d = x.shape[-1]
     f = tape.h1.shape[-1]
@@ -196,7 +197,7 @@ class HeadState:
         self.loss64 = torch.empty((), dtype=torch.float64, device=device)
 
 
-def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
+def head_forward_ops(h, tied_c, targets, vocab, hs, ws, flag):
     """Mean CE of h @ tied^T against targets without materialising logits."""
     Nt = h.shape[0]
     bn = ops.gemm_tile_n(vocab)
@@ -204,16 +205,113 @@ def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
     partial = ws.get("head_partial", (Nt, nt, 2), torch.float32)
     zy = ws.get("head_zy", (Nt,), torch.float32)
     rows_loss = ws.get("head_rows", (Nt,), torch.float32)
-    ops.gemm(h, tied_c, epilogue=N.EPI_LSE_PARTIAL, targets=targets, partial=partial, target_logit=zy)
+    with ops.span("head_gemm"):
+        ops.gemm(h, tied_c, epilogue=N.EPI_LSE_PARTIAL, targets=targets, partial=partial, target_logit=zy)
     ops.ce_finish(partial, zy, targets, vocab, hs.lse, rows_loss, hs.loss, hs.loss64, flag)
 
 
-def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
+def head_backward_ops(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
     """g_h = dz @ tied (fp32); vo_out = vo_alpha * dz^T @ h when vo_out is given."""
     Nt, d = h.shape
     vp = _pad8(vocab)
     dz = ws.get("head_dz", (Nt, vp), h.dtype)[:, :vocab]
-    ops.gemm(h, tied_c, epilogue=N.EPI_CE_GRAD, targets=targets, lse=hs.lse, ce_scale=1.0 / Nt, out=dz)
-    ops.gemm(dz, tied_c, b_mn=True, out=g_h)
+    with ops.span("head_gemm"):
+        ops.gemm(h, tied_c, epilogue=N.EPI_CE_GRAD, targets=targets, lse=hs.lse, ce_scale=1.0 / Nt, out=dz)
+    with ops.span("head_gemm"):
+        ops.gemm(dz, tied_c, b_mn=True, out=g_h)
     if vo_out is not None:
-        ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha)
+        with ops.span("head_gemm"):
+            ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha)
+
+
+# ---------------------------------------------------------------------------
+# native composites (csrc/layers.cpp): one C-ABI call per layer.  The *_ops
+# functions above are the same sequence issued op by op from Python and are
+# kept as a cross-check (tests/test_layers_gpu.py asserts bitwise equality).
+
+import ctypes  # noqa: E402
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _block_desc(x, f, B, T, drop):
+    dsc = N.BlockDesc()
+    dsc.B, dsc.T, dsc.d, dsc.f = B, T, x.shape[-1], f
+    dsc.dtype = N.BF16 if x.dtype == torch.bfloat16 else N.F32
+    if drop is not None:
+        dsc.drop_enabled, dsc.drop_seed, dsc.drop_threshold, dsc.drop_scale = 1, drop[0], drop[1], drop[2]
+    return dsc
+
+
+def _weights(W):
+    w = N.BlockWeights()
+    for n in ("wqkv", "wo", "w1", "w2", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "b1", "b2"):
+        setattr(w, n, W[n].data_ptr())
+    return w
+
+
+def _tape(tp):
+    t = N.BlockTape()
+    t.a, t.qkv, t.probs, t.ctx = _p(tp.a), _p(tp.qkv), _p(tp.probs_buf), _p(tp.ctx)
+    t.x1, t.m, t.h1 = _p(tp.x1), _p(tp.m), _p(tp.h1)
+    t.mean1, t.rstd1, t.mean2, t.rstd2 = _p(tp.mean1), _p(tp.rstd1), _p(tp.mean2), _p(tp.rstd2)
+    return t
+
+
+def _ws_bytes(ws, name, nbytes):
+    buf = ws.get(name, (int(nbytes),), torch.uint8)
+    return buf
+
+
+def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
+    f = tape.h1.shape[-1]
+    dsc = _block_desc(x, f, B, T, drop)
+    nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
+    buf = _ws_bytes(ws, "block_ws", nbytes)
+    ops._count(12)
+    N.check(N.lib().rp_block_forward(ctypes.byref(dsc), ctypes.byref(_weights(W)), _p(x), _p(out),
+                                     ctypes.byref(_tape(tape)), _p(buf), nbytes, _p(flag), ops._stream()),
+            "block_forward")
+
+
+def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
+    f = tape.h1.shape[-1]
+    dsc = _block_desc(x, f, B, T, drop)
+    nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
+    buf = _ws_bytes(ws, "block_ws", nbytes)
+    g = N.BlockGrads()
+    for n in ("wqkv", "wo", "w1", "w2", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "b1", "b2"):
+        setattr(g, n, G[n].data_ptr())
+    ops._count(27)
+    N.check(N.lib().rp_block_backward(ctypes.byref(dsc), ctypes.byref(_weights(W)), _p(x), ctypes.byref(_tape(tape)),
+                                      _p(g_out), _p(g_x), ctypes.byref(g), _p(buf), nbytes, ops._stream()),
+            "block_backward")
+
+
+def _head_desc(h, vocab):
+    hd = N.HeadDesc()
+    hd.rows, hd.d, hd.vocab = h.shape[0], h.shape[1], vocab
+    hd.dtype = N.BF16 if h.dtype == torch.bfloat16 else N.F32
+    return hd
+
+
+def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
+    hd = _head_desc(h, vocab)
+    nbytes = N.lib().rp_head_workspace_bytes(ctypes.byref(hd))
+    buf = _ws_bytes(ws, "head_ws", nbytes)
+    ops._count(3)
+    with ops.span("head_gemm"):
+        N.check(N.lib().rp_head_forward(ctypes.byref(hd), _p(h), _p(tied_c), _p(targets), _p(hs.lse), _p(hs.loss),
+                                        _p(hs.loss64), _p(buf), nbytes, _p(flag), ops._stream()), "head_forward")
+
+
+def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
+    hd = _head_desc(h, vocab)
+    nbytes = N.lib().rp_head_workspace_bytes(ctypes.byref(hd))
+    buf = _ws_bytes(ws, "head_ws", nbytes)
+    ops._count(3 if vo_out is not None else 2)
+    with ops.span("head_gemm_bwd"):
+        N.check(N.lib().rp_head_backward(ctypes.byref(hd), _p(h), _p(tied_c), _p(targets), _p(hs.lse), _p(g_h),
+                                         _p(vo_out), vo_alpha, _p(buf), nbytes, ops._stream()), "head_backward")

@@ -16,6 +16,46 @@ from .errors import DimensionError
 _DT = {torch.float32: N.F32, torch.bfloat16: N.BF16}
 
 
+class Probe:
+    """Optional instrumentation used by bench.py: counts native kernel launches
+    and records CUDA events around tagged GEMMs on the stream they run on."""
+
+    def __init__(self):
+        self.launches = 0
+        self.events = {}  # tag -> list of (start, end)
+
+    def span(self, tag):
+        return _Span(self, tag)
+
+
+class _Span:
+    def __init__(self, probe, tag):
+        self.probe, self.tag = probe, tag
+
+    def __enter__(self):
+        if self.probe is not None:
+            self.s = torch.cuda.Event(enable_timing=True)
+            self.s.record()
+
+    def __exit__(self, *exc):
+        if self.probe is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.probe.events.setdefault(self.tag, []).append((self.s, e))
+
+
+PROBE = None  # set to a Probe() to instrument
+
+
+def _count(n=1):
+    if PROBE is not None:
+        PROBE.launches += n
+
+
+def span(tag):
+    return _Span(PROBE, tag)
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -60,6 +100,7 @@ def tf32_split(x):
     hi = torch.empty(shape, dtype=torch.float32, device=x.device)
     lo = torch.empty_like(hi)
     ld = x.stride(-2) if x.dim() >= 2 else cols
+    _count(1)
     N.check(N.lib().rp_tf32_split(_ptr(x), _ptr(hi), _ptr(lo), rows, cols, ld, ld_dst, _stream()), "tf32_split")
     return hi[..., :cols], lo[..., :cols]
 
@@ -164,6 +205,7 @@ def gemm(
     if target_logit is not None:
         args.target_logit = target_logit.data_ptr()
     args.ce_scale = ce_scale
+    _count(1)
     N.check(N.lib().rp_gemm(ctypes.byref(args), _stream()), "gemm")
     return out
 
@@ -182,6 +224,7 @@ def _dtc(t):
 
 def layernorm_fwd(x, gain, bias, y, mean, rstd, flag=None):
     rows, d = x.numel() // x.shape[-1], x.shape[-1]
+    _count(1)
     N.check(N.lib().rp_layernorm_fwd(_dtc(x), _ptr(x), _ptr(gain), _ptr(bias), _ptr(y), _ptr(mean), _ptr(rstd),
                                      rows, d, _ptr(flag), _stream()), "layernorm_fwd")
 
@@ -193,6 +236,7 @@ def layernorm_bwd_blocks(rows):
 def layernorm_bwd(dy, x, mean, rstd, gain, dx, part_g, part_b, resid_grad=None, dx_masked=None, dropout=None):
     rows, d = x.numel() // x.shape[-1], x.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    _count(1)
     N.check(N.lib().rp_layernorm_bwd(_dtc(x), _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gain),
                                      _ptr(resid_grad), _ptr(dx), _ptr(dx_masked), seed, thr, scale,
                                      int(dropout is not None), _ptr(part_g), _ptr(part_b), rows, d, _stream()),
@@ -206,17 +250,20 @@ def colsum_blocks(rows):
 def colsum_partial(x, part):
     cols = x.shape[-1]
     rows = x.numel() // cols
+    _count(1)
     N.check(N.lib().rp_colsum_partial(_dtc(x), _ptr(x), rows, cols, x.stride(-2), _ptr(part), _stream()),
             "colsum_partial")
 
 
 def colsum_finish(part, nblk, out):
+    _count(1)
     N.check(N.lib().rp_colsum_finish(_ptr(part), nblk, out.numel(), _ptr(out), _stream()), "colsum_finish")
 
 
 def mask_grad(g, out, pos0, dropout, part):
     rows, d = g.numel() // g.shape[-1], g.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    _count(1)
     N.check(N.lib().rp_mask_grad(_dtc(out), _ptr(g), _ptr(out), rows, d, seed, pos0, thr, scale,
                                  int(dropout is not None), _ptr(part), _stream()), "mask_grad")
 
@@ -226,12 +273,14 @@ def softmax_causal(scores, probs):
     B, T = scores.shape[0], scores.shape[1]
     if scores.stride(1) != probs.stride(1):
         raise DimensionError("scores/probs row strides differ")
+    _count(1)
     N.check(N.lib().rp_softmax_causal(_dtc(probs), _ptr(scores), _ptr(probs), B * T, T, probs.stride(1), _stream()),
             "softmax_causal")
 
 
 def softmax_bwd(grad_probs, probs, grad_scores, scale):
     B, T = probs.shape[0], probs.shape[1]
+    _count(1)
     N.check(N.lib().rp_softmax_bwd(_dtc(probs), _ptr(grad_probs), _ptr(probs), _ptr(grad_scores), scale, B * T, T,
                                    probs.stride(1), _stream()), "softmax_bwd")
 
@@ -240,6 +289,7 @@ def embed_fwd(tokens, tied, pos, out, vocab, dropout=None, flag=None):
     B, T = tokens.shape
     d = tied.shape[1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    _count(1)
     N.check(N.lib().rp_embed_fwd(_dtc(out), _ptr(tokens), _ptr(tied), _ptr(pos), _ptr(out), B, T, d, vocab, seed,
                                  thr, scale, int(dropout is not None), _ptr(flag), _stream()), "embed_fwd")
 
@@ -248,6 +298,7 @@ def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None)
     B, T = tokens.shape
     d = grad.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    _count(3)
     N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, seed, thr, scale,
                                  int(dropout is not None), _ptr(grad_pos), _ptr(emb_grad), beta, _ptr(work),
                                  _stream()), "embed_bwd")
@@ -255,29 +306,35 @@ def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None)
 
 def ce_finish(partial, target_logit, targets, vocab, lse, loss_rows, loss, loss64=None, flag=None):
     rows, ntiles = partial.shape[0], partial.shape[1]
+    _count(2)
     N.check(N.lib().rp_ce_finish(_ptr(partial), ntiles, _ptr(target_logit), _ptr(targets), vocab, rows, _ptr(lse),
                                  _ptr(loss_rows), _ptr(loss), _ptr(loss64), _ptr(flag), _stream()), "ce_finish")
 
 
 def adam_step(w, g, m, v, copy, n, lr, b1, b2, eps, c1, c2, flag=None):
     cd = _dtc(copy) if copy is not None else N.F32
+    _count(1)
     N.check(N.lib().rp_adam_step(_ptr(w), _ptr(g), _ptr(m), _ptr(v), _ptr(copy), cd, n, lr, b1, b2, eps, c1, c2,
                                  _ptr(flag), _stream()), "adam_step")
 
 
 def sgd_step(w, g, copy, n, lr, flag=None):
     cd = _dtc(copy) if copy is not None else N.F32
+    _count(1)
     N.check(N.lib().rp_sgd_step(_ptr(w), _ptr(g), _ptr(copy), cd, n, lr, _ptr(flag), _stream()), "sgd_step")
 
 
 def init_uniform(out, seed, pos0, scale):
+    _count(1)
     N.check(N.lib().rp_init_uniform(_ptr(out), out.numel(), seed & ((1 << 64) - 1), pos0, float(scale), _stream()),
             "init_uniform")
 
 
 def cast(src, dst):
+    _count(1)
     N.check(N.lib().rp_cast(_ptr(src), _dtc(src), _ptr(dst), _dtc(dst), src.numel(), _stream()), "cast")
 
 
 def sq_norm(x, part, out, accumulate=False):
+    _count(2)
     N.check(N.lib().rp_sq_norm(_ptr(x), x.numel(), _ptr(part), _ptr(out), int(accumulate), _stream()), "sq_norm")

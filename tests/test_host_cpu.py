@@ -1,0 +1,145 @@
+"""CPU-side checks: the C-ABI library loads and exports every declared
+symbol; host logic (partition, seeds, schedules, tied mixing) matches the
+reference's golden values (tests/test_model.py:19-61, test_optim.py:14-50,
+test_engine.py:77-106)."""
+
+import ctypes
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1909_06695_b200 import _native
+from paper_1909_06695_b200.errors import DimensionError, PartitionError, ScheduleViolation
+from paper_1909_06695_b200.model import partition
+from paper_1909_06695_b200.optim import LrSchedule
+from paper_1909_06695_b200.rng import SeededRng, keep_threshold, mix64
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = _native.lib()
+    names = _native.exported_symbols()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert b"sm_100a" in lib.rp_version()
+
+
+def test_so_is_sm100a():
+    import subprocess
+
+    so = _native._LIB_PATH
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_header_mentions_reference_interfaces():
+    hdr = open(os.path.join(os.path.dirname(GOLD), "..", "include", "ringpipe_b200.h")).read()
+    for cite in ("kernels.py:68-81", "layers.py:62-79", "optim.py:52-126", "engine.py:54-69"):
+        assert cite in hdr
+
+
+def test_gemm_rejects_misaligned_without_gpu_work():
+    # argument validation happens before any launch
+    args = _native.GemmArgs()
+    args.M, args.N, args.K = 8, 8, 0
+    st = _native.lib().rp_gemm(ctypes.byref(args), None)
+    assert st == 1  # RP_ERR_DIMENSION
+    assert "shape" in _native.last_error()
+
+
+class TestPartition:
+    def test_goldens(self):
+        g = np.load(os.path.join(GOLD, "reference_basics.npz"))
+        for L_, K in [(12, 4), (5, 3), (8, 2), (8, 5), (14, 9), (6, 2), (12, 1)]:
+            p = partition(L_, K)
+            assert np.array_equal(np.array(p.groups), g[f"part.{L_}.{K}.groups"])
+            assert p.device_of == list(g[f"part.{L_}.{K}.dev"])
+        assert partition(4, 2, "by_cost", [10.0, 1, 1, 1]).groups == [(0, 1), (1, 4)]
+        costs = [3.0, 1.0, 4.0, 1.0, 5.0, 9.0, 2.0, 6.0]
+        assert np.array_equal(np.array(partition(8, 3, "by_cost", costs).groups), g["part.bycost2.groups"])
+
+    @pytest.mark.parametrize("K", [2, 3, 4, 5])
+    def test_ring(self, K):
+        p = partition(8, K)
+        assert p.num_devices == K - 1 and p.device_of[0] == p.device_of[-1]
+
+    def test_invalid(self):
+        with pytest.raises(PartitionError):
+            partition(4, 5)
+        with pytest.raises(PartitionError):
+            partition(4, 0)
+        with pytest.raises(PartitionError):
+            partition(4, 2, balance="by_cost")
+
+    def test_c2_k9(self):
+        assert [b - a for a, b in partition(14, 9).groups] == [2, 2, 2, 2, 2, 1, 1, 1, 1]
+
+
+def test_rng_and_seeds_match_reference_goldens():
+    assert np.array_equal(SeededRng(1).uniform((3,)),
+                          np.array([0.5665615751722809, 0.7457817572627011, 0.9710027535867962]))
+    g = np.load(os.path.join(GOLD, "reference_basics.npz"))
+    assert np.array_equal(SeededRng(12345, 1000).uniform((5,)), g["rng_mid"])
+    assert mix64(1, 2) != mix64(2, 1)
+    from oracle.rng import hash64
+
+    for parts in [(7,), (99, 7, 3), (2 ** 64 - 1, 5, 0)]:
+        assert mix64(*parts) == hash64(*parts)
+
+
+def test_keep_threshold_is_exact_float_compare():
+    for p in (0.1, 0.2, 0.15, 0.5, 1e-9):
+        thr = keep_threshold(p)
+        for bits in (thr - 1, thr, thr + 1):
+            u = bits * (1.0 / (1 << 53))
+            assert (u >= p) == (bits >= thr)
+
+
+def test_lr_schedule_values():
+    # reference tests/test_optim.py:14-50
+    s = LrSchedule(0.1, "diminishing")
+    assert s.at(0) == 0.1 and abs(s.at(9) - 0.01) < 1e-15
+    w = LrSchedule(1.0, "warmup-cosine", 10, 110)
+    assert w.at(0) == pytest.approx(0.1) and w.at(9) == pytest.approx(1.0)
+    assert w.at(10) == pytest.approx(1.0) and w.at(60) == pytest.approx(0.5) and w.at(110) == pytest.approx(0.0)
+    with pytest.raises(ValueError):
+        LrSchedule(0.0)
+    with pytest.raises(ValueError):
+        LrSchedule(1.0, "warmup-cosine", 10, 10)
+
+
+def test_embedding_gradient_rules():
+    # reference tests/test_engine.py:77-106 on host arrays
+    from paper_1909_06695_b200.engine import embedding_gradient, tied_coefficients
+
+    assert not embedding_gradient(1, 3, np.ones((4, 2)), None).any()
+    G = SeededRng(5).uniform((4, 2))
+    assert not embedding_gradient(5, 3, G, -G).any()
+    assert np.array_equal(embedding_gradient(5, 3, np.full((2, 2), 3.0), np.full((2, 2), 1.0)), np.full((2, 2), 2.0))
+    with pytest.raises(DimensionError):
+        embedding_gradient(5, 2, np.ones((2, 2)), np.ones((3, 2)))
+    with pytest.raises(ScheduleViolation):
+        embedding_gradient(5, 3, np.ones((2, 2)), None)
+    assert tied_coefficients(0, 3, "half_avg") == (0.0, 0.0)
+    assert tied_coefficients(2, 3, "half_avg") == (0.5, 0.5)
+    assert tied_coefficients(2, 3, "sum") == (1.0, 1.0)
+
+
+def test_product_never_imports_oracle():
+    import pathlib
+
+    pkg = pathlib.Path(_native.__file__).parent
+    for py in pkg.rglob("*.py"):
+        assert "oracle" not in py.read_text().replace("oracle/", ""), py
+
+
+def test_flops_per_token_c2():
+    import bench
+
+    c = bench.CONFIGS["c2"]
+    # 356.0 MFLOP forward, 1.068 GFLOP model FLOPs per token
+    assert bench.flops_per_token(c) / 3 == pytest.approx(356.0e6, rel=2e-3)
