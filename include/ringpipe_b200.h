@@ -87,6 +87,7 @@ typedef struct rp_gemm_args {
   float* partial;           /* [batch*M, n_tiles, 2] */
   float* target_logit;      /* [batch*M] */
   float ce_scale;
+  int32_t k_splits; /* > 1: C = [k_splits, M, N] fp32 partials over K ranges (rp_splitk_reduce) */
 } rp_gemm_args;
 
 const char* rp_version(void);
@@ -94,6 +95,8 @@ int rp_last_error(char* buf, size_t len);
 
 int rp_gemm(const rp_gemm_args* args, void* stream);
 int rp_gemm_tile_n(int64_t N);
+/* out[m,n] = sum_s part[s][m,n] in fixed order (deterministic split-K finish) */
+int rp_splitk_reduce(const float* part, int32_t splits, int64_t M, int64_t N, float* out, int64_t ldo, void* stream);
 int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src,
                   int64_t ld_dst, void* stream);
 
@@ -123,6 +126,7 @@ int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, 
 int rp_colsum_finish(const float* partial, int32_t nblocks, int64_t cols, float* out, void* stream);
 /* out = g * mask(seed, pos0 + r*d + j) (dtype), partial column sums of the masked values
  * (layers.py:209-220). */
+int rp_mask_grad_blocks(int64_t rows, int64_t d); /* partial rows rp_mask_grad writes */
 int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
                  uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream);
 
@@ -138,12 +142,13 @@ int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, vo
 int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
                  int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
                  int32_t drop_enabled, int32_t* flag, void* stream);
-/* grad_pos [Tmax,d] (fully written); emb[tok] += beta * sum of masked rows (deterministic,
- * sorted scatter).  work: rp_embed_bwd_workspace(B*T) uint64 words. */
+/* grad_pos [Tmax,d] (fully written); emb[tok] += beta * sum of masked rows (deterministic
+ * sorted, chunked scatter; replaces np.add.at, layers.py:135).
+ * workspace: rp_embed_bwd_workspace_bytes(B*T, d) bytes. */
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
                  uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
-                 float* emb_grad, float beta, uint64_t* work, void* stream);
-int64_t rp_embed_bwd_workspace(int64_t n_tokens);
+                 float* emb_grad, float beta, void* workspace, void* stream);
+int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
 
 /* ---- tied-head cross-entropy finish (layers.py:287-296, 310-316) ------------ */
 int rp_ce_finish(const float* partial, int32_t ntiles, const float* target_logit, const int64_t* targets,

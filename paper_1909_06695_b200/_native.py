@@ -57,6 +57,7 @@ class GemmArgs(ctypes.Structure):
         ("partial", ctypes.c_void_p),
         ("target_logit", ctypes.c_void_p),
         ("ce_scale", ctypes.c_float),
+        ("k_splits", ctypes.c_int32),
     ]
 
 
@@ -107,11 +108,13 @@ def _declare(L):
         "rp_last_error": [ctypes.c_char_p, ctypes.c_size_t],
         "rp_gemm": [ctypes.POINTER(GemmArgs), vp],
         "rp_gemm_tile_n": [i64],
+        "rp_splitk_reduce": [vp, i32, i64, i64, vp, i64, vp],
         "rp_tf32_split": [vp, vp, vp, i64, i64, i64, i64, vp],
         "rp_layernorm_fwd": [i32, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp],
         "rp_layernorm_bwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, u64, u64, f32, i32, vp, vp, i64, i64, vp],
         "rp_layernorm_bwd_blocks": [i64],
         "rp_colsum_blocks": [i64],
+        "rp_mask_grad_blocks": [i64, i64],
         "rp_colsum_partial": [i32, vp, i64, i64, i64, vp, vp],
         "rp_colsum_finish": [vp, i32, i64, vp, vp],
         "rp_mask_grad": [i32, vp, vp, i64, i64, u64, u64, u64, f32, i32, vp, vp],
@@ -119,7 +122,7 @@ def _declare(L):
         "rp_softmax_bwd": [i32, vp, vp, vp, f32, i64, i64, i64, vp],
         "rp_embed_fwd": [i32, vp, vp, vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp],
         "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, vp],
-        "rp_embed_bwd_workspace": [i64],
+        "rp_embed_bwd_workspace_bytes": [i64, i64],
         "rp_ce_finish": [vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp],
         "rp_adam_step": [vp, vp, vp, vp, vp, i32, i64, f32, f32, f32, f32, f32, f32, vp, vp],
         "rp_sgd_step": [vp, vp, vp, i32, i64, f32, vp, vp],
@@ -140,7 +143,7 @@ def _declare(L):
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int32
-    L.rp_embed_bwd_workspace.restype = i64
+    L.rp_embed_bwd_workspace_bytes.restype = i64
     L.rp_block_workspace_bytes.restype = i64
     L.rp_head_workspace_bytes.restype = i64
 

@@ -44,6 +44,10 @@ int rp_gemm(const rp_gemm_args* args, void* stream) {
 
 int rp_gemm_tile_n(int64_t N) { return rp::gemm_tile_n(N); }
 
+int rp_splitk_reduce(const float* part, int32_t splits, int64_t M, int64_t N, float* out, int64_t ldo, void* stream) {
+  return rp::splitk_reduce(part, splits, M, N, out, ldo, static_cast<cudaStream_t>(stream));
+}
+
 int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                   void* stream) {
   return rp::tf32_split(x, hi, lo, rows, cols, ld_src, ld_dst, static_cast<cudaStream_t>(stream));
@@ -64,6 +68,7 @@ int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float*
 }
 int rp_layernorm_bwd_blocks(int64_t rows) { return rp::ln_bwd_blocks(rows); }
 int rp_colsum_blocks(int64_t rows) { return rp::colsum_blocks(rows); }
+int rp_mask_grad_blocks(int64_t rows, int64_t d) { return rp::mask_grad_blocks(rows, d); }
 int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* partial,
                       void* stream) {
   return rp::colsum_partial(dtype, x, rows, cols, ld, partial, RP_S(stream));
@@ -91,11 +96,11 @@ int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const v
 }
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
                  uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
-                 float* emb_grad, float beta, uint64_t* work, void* stream) {
+                 float* emb_grad, float beta, void* work, void* stream) {
   return rp::embed_bwd(grad, tokens, B, T, Tmax, d, seed, threshold, scale, drop_enabled, grad_pos, emb_grad, beta,
                        work, RP_S(stream));
 }
-int64_t rp_embed_bwd_workspace(int64_t n_tokens) { return rp::embed_bwd_workspace(n_tokens); }
+int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) { return rp::embed_bwd_workspace_bytes(n_tokens, d); }
 int rp_ce_finish(const float* partial, int32_t ntiles, const float* target_logit, const int64_t* targets,
                  int64_t vocab, int64_t rows, float* lse, float* loss_rows, float* loss, double* loss64,
                  int32_t* flag, void* stream) {

@@ -4,10 +4,10 @@
 // The input-side tied gradient is a scatter-add over token ids
 // (np.add.at, layers.py:135).  It is made deterministic without float
 // atomics: one CTA bitonic-sorts (token, position) keys in shared memory, then
-// one warp per run of equal tokens sums its rows in position order -- the
-// same order np.add.at visits them -- and adds beta * sum into the packet's
-// mixed embedding gradient (engine.py:54-69) whose output-side half the head
-// GEMM already wrote.
+// runs of equal tokens are summed in position order (chunked, so Zipf-head
+// tokens with hundreds of occurrences do not serialise) and beta * sum is
+// added into the packet's mixed embedding gradient (engine.py:54-69) whose
+// output-side half the head GEMM already wrote.
 #include <algorithm>
 
 #include "common.cuh"
@@ -79,40 +79,62 @@ __global__ void __launch_bounds__(1024) token_sort_kernel(const int64_t* __restr
   for (int i = threadIdx.x; i < n; i += blockDim.x) sorted[i] = keys[i];
 }
 
-// One warp per sorted index; the warp that starts a run of equal tokens sums
-// the run's rows (in position order) and does emb[tok] += beta * sum.
-__global__ void embed_tied_grad_kernel(const uint64_t* __restrict__ sorted, int n, const float* __restrict__ g, int d,
-                                       uint64_t seed, uint64_t thr, float scale, int drop_on, float beta,
-                                       float* __restrict__ emb) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= n) return;
-  const uint32_t tokv = static_cast<uint32_t>(sorted[warp] >> 32);
-  if (warp > 0 && static_cast<uint32_t>(sorted[warp - 1] >> 32) == tokv) return;
-  int end = warp + 1;
-  while (end < n && static_cast<uint32_t>(sorted[end] >> 32) == tokv) ++end;
-  constexpr int C = 8;
-  for (int j0 = 0; j0 < d; j0 += 32 * C) {
-    float acc[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) acc[c] = 0.f;
-    for (int q = warp; q < end; ++q) {
-      const int64_t r = static_cast<uint32_t>(sorted[q] & 0xffffffffu);
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const int j = j0 + lane + 32 * c;
-        if (j < d) {
-          float v = g[r * d + j];
-          if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
-          acc[c] += v;
-        }
+// Deterministic scatter-sum of masked gradient rows into the tied gradient,
+// in two passes so hot (Zipf-head) tokens do not serialise on one warp:
+//  1) chunk c of kChunk sorted positions: per column, sum each run of equal
+//     tokens inside the chunk in position order -> partial[first position];
+//  2) per run start (segment of equal tokens): add the chunk partials of the
+//     segment in chunk order, emb[tok] += beta * total.
+constexpr int kChunk = 32;
+
+__global__ void embed_chunk_partial_kernel(const uint64_t* __restrict__ sorted, int n, const float* __restrict__ g,
+                                           int d, uint64_t seed, uint64_t thr, float scale, int drop_on,
+                                           float* __restrict__ partial) {
+  __shared__ uint32_t tok_s[kChunk];
+  __shared__ uint32_t row_s[kChunk];
+  const int c0 = blockIdx.x * kChunk;
+  const int len = min(kChunk, n - c0);
+  if (threadIdx.x < len) {
+    tok_s[threadIdx.x] = static_cast<uint32_t>(sorted[c0 + threadIdx.x] >> 32);
+    row_s[threadIdx.x] = static_cast<uint32_t>(sorted[c0 + threadIdx.x] & 0xffffffffu);
+  }
+  __syncthreads();
+  for (int j = blockIdx.y * blockDim.x + threadIdx.x; j < d; j += gridDim.y * blockDim.x) {
+    float acc = 0.f;
+    int start = 0;
+    for (int q = 0; q < len; ++q) {
+      const int64_t r = row_s[q];
+      float v = g[r * d + j];
+      if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
+      acc += v;
+      if (q + 1 == len || tok_s[q + 1] != tok_s[q]) {
+        partial[(int64_t)(c0 + start) * d + j] = acc;
+        acc = 0.f;
+        start = q + 1;
       }
     }
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const int j = j0 + lane + 32 * c;
-      if (j < d) emb[(int64_t)tokv * d + j] += beta * acc[c];
+  }
+}
+
+__global__ void embed_segment_kernel(const uint64_t* __restrict__ sorted, int n, const float* __restrict__ partial,
+                                     int d, float beta, float* __restrict__ emb) {
+  const int i = blockIdx.x;
+  const uint32_t tokv = static_cast<uint32_t>(sorted[i] >> 32);
+  if (i > 0 && static_cast<uint32_t>(sorted[i - 1] >> 32) == tokv) return;
+  int end = i + 1;
+  // segment end: first position with a different token (scan chunk starts)
+  while (end < n && static_cast<uint32_t>(sorted[end] >> 32) == tokv) {
+    const int next_chunk = (end / kChunk + 1) * kChunk;
+    if (next_chunk < n && static_cast<uint32_t>(sorted[next_chunk - 1] >> 32) == tokv) {
+      end = next_chunk;
+    } else {
+      ++end;
     }
+  }
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float total = partial[(int64_t)i * d + j];
+    for (int c = (i / kChunk + 1) * kChunk; c < end; c += kChunk) total += partial[(int64_t)c * d + j];
+    emb[(int64_t)tokv * d + j] += beta * total;
   }
 }
 
@@ -179,11 +201,15 @@ int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, voi
   return check_launch("embed_fwd");
 }
 
-int64_t embed_bwd_workspace(int64_t n_tokens) { return n_tokens; }  // uint64 words
+int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) {
+  return ((n_tokens * 8 + 255) / 256) * 256 + n_tokens * d * 4;
+}
 
 int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
-              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, uint64_t* work,
+              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
               cudaStream_t st) {
+  uint64_t* work = static_cast<uint64_t*>(workspace);
+  float* partial = reinterpret_cast<float*>(static_cast<char*>(workspace) + ((B * Tn * 8 + 255) / 256) * 256);
   const int64_t n = B * Tn;
   const int threads = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
   if (gpos) {
@@ -203,10 +229,13 @@ int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t
   }
   token_sort_kernel<<<1, 1024, smem, st>>>(tok, (int)n, npow2, work);
   if (int e = check_launch("token_sort")) return e;
-  const int64_t warps_per_block = 8;
-  embed_tied_grad_kernel<<<(unsigned)((n + warps_per_block - 1) / warps_per_block), 256, 0, st>>>(
-      work, (int)n, g, (int)d, seed, thr, scale, drop_on, beta, emb);
-  return check_launch("embed_tied_grad");
+  const int nchunk = (int)((n + kChunk - 1) / kChunk);
+  const int tpb = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
+  dim3 grid(nchunk, (unsigned)std::max<int64_t>(1, (d + tpb - 1) / tpb));
+  embed_chunk_partial_kernel<<<grid, tpb, 0, st>>>(work, (int)n, g, (int)d, seed, thr, scale, drop_on, partial);
+  if (int e = check_launch("embed_chunk_partial")) return e;
+  embed_segment_kernel<<<(unsigned)n, tpb, 0, st>>>(work, (int)n, partial, (int)d, beta, emb);
+  return check_launch("embed_segment");
 }
 
 int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,

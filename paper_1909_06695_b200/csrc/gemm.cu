@@ -61,6 +61,8 @@ struct GemmParams {
   float* target_logit;
   float ce_scale;
   int vec_ok;
+  int resid_vec;
+  int ksplit;  // > 0: "batch" b covers K range [b*ksplit, (b+1)*ksplit) of one matrix
 };
 
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int n0, int b,
@@ -94,6 +96,45 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int 
           reinterpret_cast<float*>(p.C)[base + j] = v[j];
       }
     }
+  }
+}
+
+// 32 consecutive residual / aux elements of row m (same dtype as C), vectorised
+// when the row chunk is in bounds and 16-byte aligned.
+__device__ __forceinline__ void load_chunk(const GemmParams& p, int64_t m, int n0, int b, float (&r)[32]) {
+  const int64_t base = (int64_t)b * p.stride_resid + m * p.ld_resid + n0;
+  if (p.resid_vec && n0 + 32 <= p.N) {
+    if (p.out_bf16) {
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.resid) + base);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = src[q];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(&w[h]);
+          const float2 f = __bfloat1622float2(t);
+          r[q * 8 + 2 * h] = f.x;
+          r[q * 8 + 2 * h + 1] = f.y;
+        }
+      }
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.resid) + base);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = src[q];
+        r[4 * q] = f.x;
+        r[4 * q + 1] = f.y;
+        r[4 * q + 2] = f.z;
+        r[4 * q + 3] = f.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      r[j] = (n0 + j < p.N) ? (p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.resid)[base + j])
+                                          : reinterpret_cast<const float*>(p.resid)[base + j])
+                            : 0.f;
   }
 }
 
@@ -149,6 +190,8 @@ __global__ void __launch_bounds__(256, 1)
         const int nb = rest % p.n_tiles;
         const int b = rest / p.n_tiles;
         const int m0 = mb * Cfg::BM, n0 = nb * BN;
+        const int kbase = p.ksplit ? b * p.ksplit : 0;
+        const int bc = p.ksplit ? 0 : b;
         for (int pass = 0; pass < p.passes; ++pass) {
           const CUtensorMap* ma = (pass == 2) ? &mapA_lo : &mapA;
           const CUtensorMap* mbm = (pass == 1) ? &mapB_lo : &mapB;
@@ -157,20 +200,20 @@ __global__ void __launch_bounds__(256, 1)
             mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
             uint8_t* sb = sa + Cfg::A_BYTES;
-            const int k0 = kb * Cfg::BK;
+            const int k0 = kbase + kb * Cfg::BK;
             if (!p.a_mn) {
-              tma_load_3d(sa, ma, &full[stage], k0, m0, b);
+              tma_load_3d(sa, ma, &full[stage], k0, m0, bc);
             } else {
 #pragma unroll
               for (int c = 0; c < Cfg::BM / Cfg::CHUNK; ++c)
-                tma_load_3d(sa + c * (Cfg::BK * 128), ma, &full[stage], m0 + c * Cfg::CHUNK, k0, b);
+                tma_load_3d(sa + c * (Cfg::BK * 128), ma, &full[stage], m0 + c * Cfg::CHUNK, k0, bc);
             }
             if (!p.b_mn) {
-              tma_load_3d(sb, mbm, &full[stage], k0, n0, b);
+              tma_load_3d(sb, mbm, &full[stage], k0, n0, bc);
             } else {
 #pragma unroll
               for (int c = 0; c < BN / Cfg::CHUNK; ++c)
-                tma_load_3d(sb + c * (Cfg::BK * 128), mbm, &full[stage], n0 + c * Cfg::CHUNK, k0, b);
+                tma_load_3d(sb + c * (Cfg::BK * 128), mbm, &full[stage], n0 + c * Cfg::CHUNK, k0, bc);
             }
             if (++stage == Cfg::STAGES) {
               stage = 0;
@@ -269,22 +312,20 @@ __global__ void __launch_bounds__(256, 1)
             break;
           }
           case RP_EPI_BIAS_DROPOUT_RESIDUAL: {
+            float r[32];
+            if (p.resid) {
+              load_chunk(p, m, n0, b, r);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) r[j] = 0.f;
+            }
+            const uint64_t pos_row = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = n0 + j;
-              if (n < p.N) {
-                float t = v[j] + (p.bias ? p.bias[n] : 0.f);
-                if (p.drop_on) {
-                  const uint64_t pos = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n;
-                  t = dropout_keep(p.drop_seed, pos, p.drop_thr) ? t * p.drop_scale : 0.f;
-                }
-                if (p.resid) {
-                  const int64_t ri = (int64_t)b * p.stride_resid + m * p.ld_resid + n;
-                  t += p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.resid)[ri])
-                                  : reinterpret_cast<const float*>(p.resid)[ri];
-                }
-                v[j] = t;
-              }
+              float t = v[j] + ((p.bias && n < p.N) ? p.bias[n] : 0.f);
+              if (p.drop_on) t = dropout_keep(p.drop_seed, pos_row + j, p.drop_thr) ? t * p.drop_scale : 0.f;
+              v[j] = t + r[j];
             }
             store_chunk(p, m, n0, b, v);
             break;
@@ -310,15 +351,10 @@ __global__ void __launch_bounds__(256, 1)
           }
           case RP_EPI_RELU_GRAD: {
             // out = acc * (aux > 0), aux = the ReLU output h1 (layers.py:221)
+            float r[32];
+            load_chunk(p, m, n0, b, r);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (n0 + j < p.N) {
-                const int64_t ri = (int64_t)b * p.stride_resid + m * p.ld_resid + n0 + j;
-                const float a = p.out_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.resid)[ri])
-                                           : reinterpret_cast<const float*>(p.resid)[ri];
-                v[j] = a > 0.f ? v[j] : 0.f;
-              }
-            }
+            for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.f ? v[j] : 0.f;
             store_chunk(p, m, n0, b, v);
             break;
           }
@@ -351,6 +387,40 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------------------
+// split-K: out[m, n] = sum_s part[s][m, n] in fixed order (deterministic).
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int64_t M, int64_t N, int64_t sstride,
+                                     float* __restrict__ out, int64_t ldo) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= M * N) return;
+  const int64_t m = i / N, n = i - m * N;
+  if ((N & 3) == 0 && (ldo & 3) == 0) {
+    float4 acc = *reinterpret_cast<const float4*>(part + i);
+    for (int s = 1; s < S; ++s) {
+      const float4 v = *reinterpret_cast<const float4*>(part + s * sstride + i);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    *reinterpret_cast<float4*>(out + m * ldo + n) = acc;
+  } else {
+    for (int64_t e = i; e < min(i + 4, M * N); ++e) {
+      float acc = part[e];
+      for (int s = 1; s < S; ++s) acc += part[s * sstride + e];
+      const int64_t mm = e / N, nn = e - mm * N;
+      out[mm * ldo + nn] = acc;
+    }
+  }
+}
+
+int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, int64_t ldo, cudaStream_t st) {
+  const int64_t n4 = (M * N + 3) / 4;
+  if (n4 == 0) return RP_OK;
+  splitk_reduce_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(part, S, M, N, M * N, out, ldo);
+  return check_launch("splitk_reduce");
 }
 
 // ---------------------------------------------------------------------------
@@ -439,7 +509,11 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
     cudaFuncSetAttribute(gemm_kernel<kTf32, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   });
   CUtensorMap ma, mal, mb, mbl;
-  const int64_t batch = std::max<int64_t>(a.batch, 1);
+  const int ks = a.k_splits > 1 ? a.k_splits : 1;
+  if (ks > 1 && (a.batch > 1 || a.epilogue != RP_EPI_STORE))
+    return set_error(RP_ERR_INVALID, "split-K needs batch 1 and the plain store epilogue");
+  const int64_t kchunk = ks > 1 ? ((a.K + ks - 1) / ks + Cfg::BK - 1) / Cfg::BK * Cfg::BK : a.K;
+  const int64_t batch = ks > 1 ? 1 : std::max<int64_t>(a.batch, 1);
   int st;
   // A: K-major -> inner K, rows M ; MN-major -> inner M, rows K
   if (!a.a_mn_major)
@@ -473,14 +547,15 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.M = (int)a.M;
   p.N = (int)a.N;
   p.K = (int)a.K;
-  p.batch = (int)batch;
+  p.batch = ks > 1 ? ks : (int)batch;
+  p.ksplit = ks > 1 ? (int)kchunk : 0;
   p.a_mn = a.a_mn_major;
   p.b_mn = a.b_mn_major;
   p.passes = passes;
   p.m_tiles = (int)((a.M + Cfg::BM - 1) / Cfg::BM);
   p.n_tiles = (int)((a.N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles * p.batch;
-  p.kb_per_pass = (int)((a.K + Cfg::BK - 1) / Cfg::BK);
+  p.kb_per_pass = (int)((kchunk + Cfg::BK - 1) / Cfg::BK);
   p.out_bf16 = a.out_dtype == RP_BF16;
   p.epi = a.epilogue;
   p.alpha = a.alpha;
@@ -502,8 +577,10 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.target_logit = a.target_logit;
   p.ce_scale = a.ce_scale;
   const int oe = p.out_bf16 ? 2 : 4;
+  p.resid_vec = ((reinterpret_cast<uintptr_t>(a.residual) & 15) == 0) && ((a.ld_residual * oe) % 16 == 0) &&
+                ((a.stride_residual * oe) % 16 == 0 || batch == 1);
   p.vec_ok = ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) && ((a.ldc * oe) % 16 == 0) &&
-             ((a.stride_c * oe) % 16 == 0 || batch == 1);
+             ((a.stride_c * oe) % 16 == 0 || p.batch == 1);
   if (p.num_tiles == 0) return RP_OK;
   const int grid = std::min(p.num_tiles, num_sms());
   gemm_kernel<kTf32, BN><<<grid, 256, Cfg::SMEM_BYTES, stream>>>(ma, mal, mb, mbl, p);

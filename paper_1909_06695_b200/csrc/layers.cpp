@@ -17,6 +17,11 @@ namespace rp {
 namespace {
 
 inline int64_t pad8(int64_t n) { return (n + 7) / 8 * 8; }
+
+#define RP_TRY0(x)                \
+  do {                            \
+    if (int _e = (x)) return _e;  \
+  } while (0)
 inline int64_t al256(int64_t n) { return (n + 255) / 256 * 256; }
 inline int esize(int dt) { return dt == RP_BF16 ? 2 : 4; }
 
@@ -47,7 +52,29 @@ struct Ctx {
   cudaStream_t st;
   char* split_base = nullptr;  // tf32x3 split scratch
   int64_t split_cap = 0;
+  float* splitk = nullptr;  // split-K partials
+  int64_t splitk_cap = 0;   // bytes
 };
+
+// Deterministic split-K for weight-gradient shaped GEMMs (few output tiles,
+// long K): pick S minimising waves(S) * tile_time(K/S) + partial traffic.
+int choose_splits(int64_t M, int64_t N, int64_t K, int bn, int64_t cap_bytes) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  if (tiles >= 148 || K < 1024 || cap_bytes <= 0) return 1;
+  const double R = 1.1e15 / 148.0, BW = 5.5e12;
+  int best = 1;
+  double best_t = 2.0 * 128 * bn * (double)K / R;
+  const int smax = (int)std::min<int64_t>({64, K / 512, cap_bytes / (M * N * 4)});
+  for (int S = 2; S <= smax; ++S) {
+    const double waves = std::ceil((double)(tiles * S) / 148.0);
+    const double t = waves * 2.0 * 128 * bn * ((double)K / S) / R + (double)S * M * N * 8.0 / BW;
+    if (t < best_t * 0.97) {
+      best_t = t;
+      best = S;
+    }
+  }
+  return best;
+}
 
 struct Epi {
   int kind = RP_EPI_STORE;
@@ -118,6 +145,15 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.C = const_cast<void*>(C.p);
   g.ldc = C.ld;
   g.stride_c = C.bstride;
+  int splits = 1;
+  if (out_dtype == RP_F32 && e.kind == RP_EPI_STORE && g.batch == 1 && c.splitk)
+    splits = choose_splits(g.M, g.N, g.K, gemm_tile_n(g.N), c.splitk_cap);
+  if (splits > 1) {
+    g.k_splits = splits;
+    g.C = c.splitk;
+    g.ldc = g.N;
+    g.stride_c = g.M * g.N;
+  }
   g.epilogue = e.kind;
   g.alpha = e.alpha;
   g.bias = e.bias;
@@ -134,7 +170,10 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.partial = e.partial;
   g.target_logit = e.target_logit;
   g.ce_scale = e.ce_scale;
-  return gemm(g, c.st);
+  RP_TRY0(gemm(g, c.st));
+  if (splits > 1) return splitk_reduce(c.splitk, splits, g.M, g.N, static_cast<float*>(const_cast<void*>(C.p)), C.ld,
+                                       c.st);
+  return RP_OK;
 }
 
 int64_t split_bytes(int dtype, int64_t max_elems) {
@@ -152,9 +191,11 @@ int64_t split_bytes(int dtype, int64_t max_elems) {
 // ---------------------------------------------------------------------------
 // block
 
+constexpr int64_t kBlockSplitK = 296LL * 128 * 256 * 4;  // split-K partials of the dW GEMMs
+
 int64_t block_workspace_bytes(const rp_block_desc& d) {
   const int64_t N = d.B * d.T, Tp = pad8(d.T), e = esize(d.dtype);
-  const int64_t nbp = std::max<int64_t>(colsum_blocks(N), ln_bwd_blocks(N));
+  const int64_t nbp = std::max<int64_t>({colsum_blocks(N), ln_bwd_blocks(N), mask_grad_blocks(N, d.d)});
   int64_t b = 0;
   b += al256(d.B * d.T * Tp * 4);              // scores / g_p
   b += al256(d.B * d.T * Tp * e);              // g_s
@@ -163,6 +204,7 @@ int64_t block_workspace_bytes(const rp_block_desc& d) {
   b += al256(N * 3 * d.d * e);                 // g_qkv
   b += al256(N * d.d * 4) * 3;                 // g_m, g_x1, g_a
   b += al256(nbp * std::max(d.f, 3 * d.d) * 4) * 3;  // partials
+  b += al256(kBlockSplitK);
   b += split_bytes(d.dtype, std::max({N * d.f, d.B * d.T * Tp, N * 3 * d.d, d.d * d.f}));
   return b + 4096;
 }
@@ -217,7 +259,7 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   const int64_t B = d.B, T = d.T, D = d.d, F = d.f, N = B * T, Tp = pad8(T);
   const int dt = d.dtype, e = esize(dt);
   const int nbc = colsum_blocks(N), nbl = ln_bwd_blocks(N);
-  const int64_t nbp = std::max<int64_t>(nbc, nbl);
+  const int64_t nbp = std::max<int64_t>({(int64_t)nbc, (int64_t)nbl, (int64_t)mask_grad_blocks(N, D)});
   Bump bp{static_cast<char*>(ws), ws_bytes};
   float* g_p = static_cast<float*>(bp.take(B * T * Tp * 4));
   void* g_s = bp.take(B * T * Tp * e);
@@ -234,6 +276,8 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   float* pg = static_cast<float*>(bp.take(nbp * pw * 4));
   float* pb = static_cast<float*>(bp.take(nbp * pw * 4));
   Ctx c{dt, st};
+  c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
+  c.splitk_cap = kBlockSplitK;
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
   const char* qkv = static_cast<const char*>(tp.qkv);
@@ -241,7 +285,7 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   // feed-forward branch (layers.py:209-232)
   RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(N * D), d.drop_threshold, d.drop_scale,
                    d.drop_enabled, part, st));
-  RP_TRY(colsum_finish(part, nbc, D, G.b2, st));
+  RP_TRY(colsum_finish(part, mask_grad_blocks(N, D), D, G.b2, st));
   RP_TRY(mm(c, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32));
   Epi er;
   er.kind = RP_EPI_RELU_GRAD;
@@ -281,11 +325,14 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
 // ---------------------------------------------------------------------------
 // tied head
 
+constexpr int64_t kHeadSplitK = 16;  // max split-K factor of g_x = dz @ tied
+
 int64_t head_workspace_bytes(const rp_head_desc& h) {
   const int bn = gemm_tile_n(h.vocab);
   const int64_t nt = (h.vocab + bn - 1) / bn;
   const int64_t e = esize(h.dtype);
   int64_t b = al256(h.rows * nt * 2 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
+  b += al256(kHeadSplitK * h.rows * h.d * 4);
   b += split_bytes(h.dtype, std::max(h.rows * pad8(h.vocab), h.vocab * h.d));
   return b + 4096;
 }
@@ -300,6 +347,7 @@ int head_forward(const rp_head_desc& h, const void* x, const void* tied, const i
   float* zy = static_cast<float*>(bp.take(N * 4));
   float* rows = static_cast<float*>(bp.take(N * 4));
   bp.take(N * pad8(V) * esize(h.dtype));  // dz (backward)
+  bp.take(kHeadSplitK * N * D * 4);        // split-K partials (backward)
   Ctx c{h.dtype, st};
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
@@ -323,6 +371,8 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
   bp.take(N * 4);
   void* dz = bp.take(N * Vp * esize(h.dtype));
   Ctx c{h.dtype, st};
+  c.splitk = static_cast<float*>(bp.take(kHeadSplitK * N * D * 4));
+  c.splitk_cap = kHeadSplitK * N * D * 4;
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
   Epi e;

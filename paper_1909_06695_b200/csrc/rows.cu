@@ -24,6 +24,205 @@ __device__ __forceinline__ void flag_set(int32_t* flag, int bit) {
   if (flag) atomicOr(flag, bit);
 }
 
+// 4-wide vector load/store of T as fp32.
+template <typename T> struct V4;
+template <> struct V4<float> {
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[4]) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct V4<__nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float (&v)[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[4]) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Vectorised variants (d % 128 == 0): lane owns 4 consecutive columns per
+// 128-column group, NG groups per row.
+
+template <typename T, int NG>
+__global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restrict__ x, const float* __restrict__ g,
+                                                                 const float* __restrict__ b, T* __restrict__ y,
+                                                                 float* __restrict__ mean, float* __restrict__ rstd,
+                                                                 int64_t rows, int d, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float v[NG][4];
+  float s = 0.f;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    V4<T>::ld(x + row * d + (i * 32 + lane) * 4, v[i]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      finite &= isfinite(v[i][q]);
+      s += v[i][q];
+    }
+  }
+  const float mu = warp_sum(s) / d;
+  float qv = 0.f;
+#pragma unroll
+  for (int i = 0; i < NG; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) qv += (v[i][q] - mu) * (v[i][q] - mu);
+  const float rs = rsqrtf(warp_sum(qv) / d + kLnEps);
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const int j = (i * 32 + lane) * 4;
+    const float4 gg = *reinterpret_cast<const float4*>(g + j);
+    const float4 bb = *reinterpret_cast<const float4*>(b + j);
+    float o[4] = {(v[i][0] - mu) * rs * gg.x + bb.x, (v[i][1] - mu) * rs * gg.y + bb.y,
+                  (v[i][2] - mu) * rs * gg.z + bb.z, (v[i][3] - mu) * rs * gg.w + bb.w};
+    V4<T>::st(y + row * d + j, o);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+  if (!__all_sync(0xffffffffu, finite) && lane == 0) flag_set(flag, RP_FLAG_NONFINITE);
+}
+
+template <typename T, int NG>
+__global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
+    const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
+    float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+  __shared__ float red[kRowWarps][2][128 * NG];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
+    gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
+  }
+  const int64_t stride = (int64_t)gridDim.x * kRowWarps;
+  for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NG][4], dyv[NG][4];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const int j = (i * 32 + lane) * 4;
+      V4<T>::ld(x + row * d + j, xh[i]);
+      V4<float>::ld(dy + row * d + j, dyv[i]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xh[i][q] = (xh[i][q] - mu) * rs;
+        const float t = dyv[i][q] * gv[i][q];
+        s1 += t;
+        s2 += t * xh[i][q];
+        acc_g[i][q] += dyv[i][q] * xh[i][q];
+        acc_b[i][q] += dyv[i][q];
+      }
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const int j = (i * 32 + lane) * 4;
+      float o[4], r[4];
+      if (resid_grad) {
+        V4<float>::ld(resid_grad + row * d + j, r);
+      } else {
+        r[0] = r[1] = r[2] = r[3] = 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + r[q];
+      V4<float>::st(dx + row * d + j, o);
+      if (dx_masked) {
+        if (drop_on) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = dropout_keep(seed, (uint64_t)row * d + j + q, thr) ? o[q] * scale : 0.f;
+        }
+        V4<T>::st(dx_masked + row * d + j, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NG; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[w][0][(i * 32 + lane) * 4 + q] = acc_g[i][q];
+      red[w][1][(i * 32 + lane) * 4 + q] = acc_b[i][q];
+    }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += kRowThreads) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRowWarps; ++q) {
+      sg += red[q][0][j];
+      sb += red[q][1][j];
+    }
+    part_g[(int64_t)blockIdx.x * d + j] = sg;
+    part_b[(int64_t)blockIdx.x * d + j] = sb;
+  }
+}
+
+// out = g * mask (T) with per-CTA column partials of the masked fp32 values.
+template <typename T, int NG>
+__global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* __restrict__ g, T* __restrict__ out,
+                                                                    int64_t rows, int d, uint64_t seed, uint64_t pos0,
+                                                                    uint64_t thr, float scale, int drop_on,
+                                                                    float* __restrict__ part) {
+  __shared__ float red[kRowWarps][128 * NG];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float acc[NG][4];
+#pragma unroll
+  for (int i = 0; i < NG; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * kRowWarps;
+  for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const int j = (i * 32 + lane) * 4;
+      float v[4];
+      V4<float>::ld(g + row * d + j, v);
+      if (drop_on) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          v[q] = dropout_keep(seed, pos0 + (uint64_t)row * d + j + q, thr) ? v[q] * scale : 0.f;
+      }
+      V4<T>::st(out + row * d + j, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] += v[q];
+    }
+  }
+  if (!part) return;
+#pragma unroll
+  for (int i = 0; i < NG; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[w][(i * 32 + lane) * 4 + q] = acc[i][q];
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += kRowThreads) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRowWarps; ++q) s += red[q][j];
+    part[(int64_t)blockIdx.x * d + j] = s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // LayerNorm forward: y = (x - mu) * rstd * g + b; saves (mu, rstd).
 template <typename T, int NPL>
@@ -145,13 +344,24 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
   }
 }
 
-// out[j] = sum_b partial[b, j]  (fixed order), optionally scaled.
-__global__ void colsum_finish_kernel(const float* __restrict__ part, int nblk, int64_t cols, float* __restrict__ out) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= cols) return;
+// out[j] = sum_b partial[b, j]: 32 columns x 32 partial lanes per CTA, each
+// lane sums a fixed strided subset, then lane sums combine in fixed order.
+__global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __restrict__ part, int nblk, int64_t cols,
+                                                             float* __restrict__ out) {
+  __shared__ float red[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + tx;
   float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * cols + j];
-  out[j] = s;
+  if (j < cols)
+    for (int b = ty; b < nblk; b += 32) s += part[(int64_t)b * cols + j];
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < cols) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) t += red[q][tx];
+    out[j] = t;
+  }
 }
 
 // Column partial sums of a [rows, cols] matrix (row-major, ld).
@@ -266,7 +476,7 @@ inline int row_blocks(int64_t rows) { return (int)((rows + kRowWarps - 1) / kRow
 
 }  // namespace
 
-int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 296)); }
+int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 592)); }
 
 #define RP_NPL_DISPATCH(NPL_VAL, ...)                                   \
   switch (NPL_VAL) {                                                    \
@@ -297,9 +507,28 @@ int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
     __VA_ARGS__;                                       \
   }
 
+#define RP_NG_DISPATCH(NGV, ...)                     \
+  switch (NGV) {                                    \
+    case 1: { constexpr int NG = 1; __VA_ARGS__; break; } \
+    case 2: { constexpr int NG = 2; __VA_ARGS__; break; } \
+    case 4: { constexpr int NG = 4; __VA_ARGS__; break; } \
+    default: break;                                 \
+  }
+
+inline int ng_for(int64_t d) {
+  if (d % 128 != 0) return 0;
+  const int64_t ng = d / 128;
+  return (ng == 1 || ng == 2 || ng == 4) ? (int)ng : 0;
+}
+
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
                   int64_t rows, int64_t d, int32_t* flag, cudaStream_t st) {
   if (rows == 0) return RP_OK;
+  if (const int ng = ng_for(d)) {
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, ln_fwd_v4_kernel<T, NG><<<row_blocks(rows), kRowThreads, 0, st>>>(
+                                                    (const T*)x, g, b, (T*)y, mean, rstd, rows, (int)d, flag)));
+    return check_launch("layernorm_fwd");
+  }
   const int npl = npl_for(d);
   RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, ln_fwd_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
                                                     (const T*)x, g, b, (T*)y, mean, rstd,
@@ -311,9 +540,15 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
                   const float* resid_grad, float* dx, void* dx_masked, uint64_t seed, uint64_t thr, float scale,
                   int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st) {
   if (rows == 0) return RP_OK;
+  const int nb = ln_bwd_blocks(rows);
+  if (const int ng = ng_for(d)) {
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, ln_bwd_v4_kernel<T, NG><<<nb, kRowThreads, 0, st>>>(
+                                                    dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,
+                                                    seed, thr, scale, drop_on, part_g, part_b, rows, (int)d)));
+    return check_launch("layernorm_bwd");
+  }
   const int npl = npl_for(d);
   if (npl > 16) return set_error(RP_ERR_DIMENSION, "layernorm_bwd supports d <= 512 in this build");
-  const int nb = ln_bwd_blocks(rows);
   RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH_SMALL(npl, ln_bwd_kernel<T, NPL><<<nb, kRowThreads, 0, st>>>(
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx,
                                                     (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
@@ -323,8 +558,12 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
 
 int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStream_t st) {
   if (cols == 0) return RP_OK;
-  colsum_finish_kernel<<<(int)((cols + 255) / 256), 256, 0, st>>>(part, nblk, cols, out);
+  colsum_finish_kernel<<<(int)((cols + 31) / 32), 1024, 0, st>>>(part, nblk, cols, out);
   return check_launch("colsum_finish");
+}
+
+int mask_grad_blocks(int64_t rows, int64_t d) {
+  return ng_for(d) ? ln_bwd_blocks(rows) : colsum_blocks(rows);
 }
 
 int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 128)); }
@@ -339,6 +578,13 @@ int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t
 int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
               uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st) {
   if (d == 0) return RP_OK;
+  if (const int ng = ng_for(d)) {
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, mask_grad_v4_kernel<T, NG><<<ln_bwd_blocks(rows), kRowThreads, 0, st>>>(
+                                                    g, (T*)out, rows, (int)d, seed, pos0, thr, scale, drop_on, part)));
+    return check_launch("mask_grad");
+  }
+  // scalar fallback writes colsum_blocks(rows) partial rows; callers pass
+  // rp_mask_grad_blocks(rows, d) to the finish
   dim3 grid(colsum_blocks(rows), (unsigned)((d + 127) / 128));
   RP_DTYPE_DISPATCH(dtype, mask_grad_kernel<T><<<grid, 128, 0, st>>>(g, (T*)out, rows, (int)d, seed, pos0, thr,
                                                                      scale, drop_on, part));

@@ -14,6 +14,7 @@ int check_launch(const char* what);
 
 int gemm(const rp_gemm_args& a, cudaStream_t stream);
 int gemm_tile_n(int64_t N);
+int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, int64_t ldo, cudaStream_t st);
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);
 
@@ -24,6 +25,7 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
                   int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st);
 int ln_bwd_blocks(int64_t rows);
 int colsum_blocks(int64_t rows);
+int mask_grad_blocks(int64_t rows, int64_t d);
 int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st);
 int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStream_t st);
 int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
@@ -34,9 +36,9 @@ int softmax_bwd(int dtype, const float* gp, const void* p, void* gs, float scale
 int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, void* out, int64_t B, int64_t Tn,
               int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
               cudaStream_t st);
-int64_t embed_bwd_workspace(int64_t n_tokens);
+int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
 int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
-              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, uint64_t* work,
+              uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
               cudaStream_t st);
 int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,
               float* lse, float* loss_rows, float* loss, double* loss64, int32_t* flag, cudaStream_t st);

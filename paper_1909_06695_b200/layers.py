@@ -99,7 +99,8 @@ def embed_forward(tied_c, pos_c, tokens, out, vocab, drop, flag):
 def embed_backward(g, tokens, t_max, grad_pos, emb_grad, beta, ws, drop):
     """grad_pos fully written; emb_grad[tok] += beta * (scatter-sum of masked g)."""
     n = tokens.numel()
-    work = ws.get("embed_sort", (max(1, n),), torch.int64)
+    nbytes = N.lib().rp_embed_bwd_workspace_bytes(n, g.shape[-1])
+    work = ws.get("embed_ws", (max(256, nbytes),), torch.uint8)
     ops.embed_bwd(g, tokens, t_max, grad_pos, emb_grad, beta, work, drop)
 
 
@@ -139,11 +140,13 @@ def block_backward_ops(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
     cdt = x.dtype
     inv = 1.0 / math.sqrt(d)
     nbc = ops.colsum_blocks(Nt)
-    part = ws.get("colsum_part", (nbc, max(f, 3 * d)), torch.float32)
+    nbm = ops.mask_grad_blocks(Nt, d)
+    part = ws.get("colsum_part", (max(nbc, nbm), max(f, 3 * d)), torch.float32)
     # feed-forward branch
     g_h2 = ws.get("g_h2", (Nt, d), cdt)
-    ops.mask_grad(g_out, g_h2, n, drop, part[:, :d])
-    ops.colsum_finish(part[:, :d], nbc, G["b2"])
+    pm = ws.get("mask_part", (nbm, d), torch.float32)
+    ops.mask_grad(g_out, g_h2, n, drop, pm)
+    ops.colsum_finish(pm, nbm, G["b2"])
     ops.gemm(tape.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
     g_z1 = ws.get("g_z1", (Nt, f), cdt)
     ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tape.h1)

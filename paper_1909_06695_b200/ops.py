@@ -247,6 +247,10 @@ def colsum_blocks(rows):
     return N.lib().rp_colsum_blocks(rows)
 
 
+def mask_grad_blocks(rows, d):
+    return N.lib().rp_mask_grad_blocks(rows, d)
+
+
 def colsum_partial(x, part):
     cols = x.shape[-1]
     rows = x.numel() // cols
@@ -298,7 +302,7 @@ def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None)
     B, T = tokens.shape
     d = grad.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
-    _count(3)
+    _count(4)
     N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, seed, thr, scale,
                                  int(dropout is not None), _ptr(grad_pos), _ptr(emb_grad), beta, _ptr(work),
                                  _stream()), "embed_bwd")
