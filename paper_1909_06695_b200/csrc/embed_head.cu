@@ -141,23 +141,32 @@ __global__ void embed_segment_kernel(const uint64_t* __restrict__ sorted, int n,
 // ---------------------------------------------------------------------------
 // cross-entropy finish: lse per row from the head GEMM's (max, sumexp)
 // partials, per-row loss lse - z_y, then a fixed-order mean.
+// one warp per row: lanes stride over the row's n-tile partials (coalesced)
 __global__ void ce_rows_kernel(const float* __restrict__ partial, int ntiles, const float* __restrict__ zy,
                                const int64_t* __restrict__ tgt, int64_t vocab, int64_t rows, float* __restrict__ lse,
                                float* __restrict__ loss_rows, int32_t* flag) {
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t m = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (m >= rows) return;
-  const float* p = partial + m * ntiles * 2;
+  const float2* p = reinterpret_cast<const float2*>(partial + m * ntiles * 2);
   float mx = -INFINITY;
-  for (int t = 0; t < ntiles; ++t) mx = fmaxf(mx, p[2 * t]);
+  for (int t = lane; t < ntiles; t += 32) mx = fmaxf(mx, p[t].x);
+  mx = warp_max(mx);
   float s = 0.f;
-  for (int t = 0; t < ntiles; ++t) s += p[2 * t + 1] * __expf(p[2 * t] - mx);
-  const float l = mx + logf(s);
-  lse[m] = l;
-  loss_rows[m] = l - zy[m];
-  const int64_t y = tgt[m];
-  if (flag) {
-    if (y < 0 || y >= vocab) atomicOr(flag, RP_FLAG_DIMENSION);
-    if (!isfinite(l)) atomicOr(flag, RP_FLAG_NONFINITE);
+  for (int t = lane; t < ntiles; t += 32) {
+    const float2 v = p[t];
+    s += v.y * __expf(v.x - mx);
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    const float l = mx + logf(s);
+    lse[m] = l;
+    loss_rows[m] = l - zy[m];
+    const int64_t y = tgt[m];
+    if (flag) {
+      if (y < 0 || y >= vocab) atomicOr(flag, RP_FLAG_DIMENSION);
+      if (!isfinite(l)) atomicOr(flag, RP_FLAG_NONFINITE);
+    }
   }
 }
 
@@ -241,8 +250,8 @@ int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t
 int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,
               float* lse, float* loss_rows, float* loss, double* loss64, int32_t* flag, cudaStream_t st) {
   if (rows == 0) return RP_OK;
-  ce_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(partial, ntiles, zy, tgt, vocab, rows, lse,
-                                                                  loss_rows, flag);
+  ce_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(partial, ntiles, zy, tgt, vocab, rows, lse,
+                                                                       loss_rows, flag);
   if (int e = check_launch("ce_rows")) return e;
   mean_kernel<<<1, 1024, 0, st>>>(loss_rows, rows, loss, loss64);
   return check_launch("ce_mean");

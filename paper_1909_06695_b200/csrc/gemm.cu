@@ -16,6 +16,7 @@
 // gradient dz).  "tf32x3" runs three accumulation passes (hi*hi + hi*lo +
 // lo*hi) over pre-split operands to reach fp32 accuracy on the tf32 pipe.
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -38,7 +39,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STAGE_OUT = 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGE_OUT + 1024 + 256 + 2048;
 };
 
 struct GemmParams {
@@ -63,6 +65,8 @@ struct GemmParams {
   int vec_ok;
   int resid_vec;
   int ksplit;  // > 0: "batch" b covers K range [b*ksplit, (b+1)*ksplit) of one matrix
+  int n_fast;  // raster: N tiles fastest
+  int tma_store;  // bf16 C written by TMA bulk stores from a swizzled smem tile
 };
 
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int n0, int b,
@@ -138,15 +142,62 @@ __device__ __forceinline__ void load_chunk(const GemmParams& p, int64_t m, int n
   }
 }
 
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One warp's 32x32 bf16 chunk (lane = row) -> 64B-swizzled smem tile -> one
+// TMA bulk store.  The swizzle (16B chunk k of row r at k ^ ((r>>1)&3)) matches
+// CU_TENSOR_MAP_SWIZZLE_64B and keeps the st.shared at 4 wavefronts.
+__device__ __forceinline__ void emit_tma(const CUtensorMap& mapC, uint8_t* tile, const float (&v)[32], int lane,
+                                         int col0, int row0) {
+  if (lane == 0) tma_store_wait_read();  // previous store of this warp finished reading smem
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t w[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(v[k * 8 + 2 * h], v[k * 8 + 2 * h + 1]);
+      w[h] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    const int off = lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4);
+    *reinterpret_cast<uint4*>(tile + off) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) tma_store_2d(&mapC, tile, col0, row0);
+}
+
+// Tile raster: the dimension with fewer tiles runs fastest, so consecutive
+// CTAs share the operand along the other dimension (L2 reuse instead of a
+// second DRAM stream).  The batch / split-K index is slowest.
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& mb, int& nb, int& b) {
+  if (p.n_fast) {
+    nb = tile % p.n_tiles;
+    const int rest = tile / p.n_tiles;
+    mb = rest % p.m_tiles;
+    b = rest / p.m_tiles;
+  } else {
+    mb = tile % p.m_tiles;
+    const int rest = tile / p.m_tiles;
+    nb = rest % p.n_tiles;
+    b = rest / p.n_tiles;
+  }
+}
+
 template <bool kTf32, int BN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA_lo,
                 const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB_lo,
-                const GemmParams p) {
+                const __grid_constant__ CUtensorMap mapC, const GemmParams p) {
   using Cfg = GemmCfg<kTf32, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* stage_out = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + Cfg::STAGE_OUT);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tmem_full = empty + Cfg::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
@@ -162,6 +213,7 @@ __global__ void __launch_bounds__(256, 1)
       tma_prefetch(&mapA_lo);
       tma_prefetch(&mapB_lo);
     }
+    if (p.tma_store) tma_prefetch(&mapC);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -170,7 +222,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 128);
+      mbar_init(&tmem_empty[a], 256);
     }
     fence_mbar_init();
   }
@@ -185,10 +237,8 @@ __global__ void __launch_bounds__(256, 1)
       // ---------------- TMA producer ----------------
       uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mb = tile % p.m_tiles;
-        const int rest = tile / p.m_tiles;
-        const int nb = rest % p.n_tiles;
-        const int b = rest / p.n_tiles;
+        int mb, nb, b;
+        decode_tile(p, tile, mb, nb, b);
         const int m0 = mb * Cfg::BM, n0 = nb * BN;
         const int kbase = p.ksplit ? b * p.ksplit : 0;
         const int bc = p.ksplit ? 0 : b;
@@ -265,84 +315,131 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue warps ----------------
-    const int e = warp - 4;  // TMEM lane quarter
+    // ---------------- epilogue: 8 warps, two per TMEM lane quarter ----------------
+    // warp w may only touch TMEM lanes 32*(w%4)..+31; the two warps of a quarter
+    // split the tile's columns in halves.
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    constexpr int kHalf = BN / 64;  // 32-column chunks per half
+    float* red = reinterpret_cast<float*>(stage_out + Cfg::STAGE_OUT + 256);  // [2 halves][2][128]
+    uint8_t* my_out = stage_out + (warp - 4) * 2048;                           // 32 rows x 64 B, 64B-swizzled
+    const float kLog2e = 1.4426950408889634f;
     int local = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
-      const int mb = tile % p.m_tiles;
-      const int rest = tile / p.m_tiles;
-      const int nb = rest % p.n_tiles;
-      const int b = rest / p.n_tiles;
+      int mb, nb, b;
+      decode_tile(p, tile, mb, nb, b);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = (int64_t)mb * Cfg::BM + e * 32 + lane;
+      const int64_t m = (int64_t)mb * Cfg::BM + q * 32 + lane;
       const bool row_ok = m < p.M;
       const int64_t grow = (int64_t)b * p.M + m;  // row index over the folded batch
-      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(e * 32) << 16);
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 
       float run_max = -INFINITY, run_sum = 0.f;
       int64_t tgt = -1;
-      float lse_row = 0.f;
+      float lse2 = 0.f;  // lse*log2e - log2(ce_scale)
       if (row_ok && (p.epi == RP_EPI_LSE_PARTIAL || p.epi == RP_EPI_CE_GRAD)) {
         tgt = p.targets[grow];
-        if (p.epi == RP_EPI_CE_GRAD) lse_row = p.lse[grow];
+        if (p.epi == RP_EPI_CE_GRAD) lse2 = p.lse[grow] * kLog2e - __log2f(p.ce_scale);
       }
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int cc = 0; cc < kHalf; ++cc) {
+        const int c = half * kHalf + cc;
         const int n0 = nb * BN + c * 32;
         uint32_t r[32];
         tmem_ld32(t_row + c * 32, r);
-        if (!row_ok || n0 >= p.N) continue;
+        if (n0 >= p.N) continue;  // warp-uniform
+        if (!row_ok) {
+          // rows past M: the TMA store clips them, but the warp must still
+          // take part in the cooperative smem tile
+          if (p.tma_store && p.epi != RP_EPI_LSE_PARTIAL) {
+            float z[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] = 0.f;
+            emit_tma(mapC, my_out, z, lane, n0, (int)((int64_t)b * p.M + (int64_t)mb * Cfg::BM + q * 32));
+          }
+          continue;
+        }
+        const bool full = n0 + 32 <= p.N;
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int trow = (int)((int64_t)b * p.M + (int64_t)mb * Cfg::BM + q * 32);
+#define RP_EMIT()                                            \
+  do {                                                       \
+    if (p.tma_store)                                         \
+      emit_tma(mapC, my_out, v, lane, n0, trow);             \
+    else                                                     \
+      store_chunk(p, m, n0, b, v);                           \
+  } while (0)
         switch (p.epi) {
           case RP_EPI_STORE:
-            store_chunk(p, m, n0, b, v);
+            if (p.alpha != 1.f) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+            }
+            RP_EMIT();
             break;
           case RP_EPI_BIAS_RELU: {
+            if (p.bias && full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float t = v[j] + ((p.bias && n0 + j < p.N) ? p.bias[n0 + j] : 0.f);
-              v[j] = fmaxf(t, 0.f);
+              for (int j = 0; j < 32; ++j) v[j] = fmaxf(fmaf(v[j], p.alpha, p.bias[n0 + j]), 0.f);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                v[j] = fmaxf(v[j] * p.alpha + ((p.bias && n0 + j < p.N) ? p.bias[n0 + j] : 0.f), 0.f);
             }
-            store_chunk(p, m, n0, b, v);
+            RP_EMIT();
             break;
           }
           case RP_EPI_BIAS_DROPOUT_RESIDUAL: {
-            float r[32];
+            float rr[32];
             if (p.resid) {
-              load_chunk(p, m, n0, b, r);
+              load_chunk(p, m, n0, b, rr);
             } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = 0.f;
+              for (int j = 0; j < 32; ++j) rr[j] = 0.f;
             }
             const uint64_t pos_row = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = n0 + j;
-              float t = v[j] + ((p.bias && n < p.N) ? p.bias[n] : 0.f);
+              float t = v[j] * p.alpha + ((p.bias && (full || n < p.N)) ? p.bias[n] : 0.f);
               if (p.drop_on) t = dropout_keep(p.drop_seed, pos_row + j, p.drop_thr) ? t * p.drop_scale : 0.f;
-              v[j] = t + r[j];
+              v[j] = t + rr[j];
             }
-            store_chunk(p, m, n0, b, v);
+            RP_EMIT();
             break;
           }
           case RP_EPI_LSE_PARTIAL: {
             float cmax = -INFINITY;
+            if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (n0 + j < p.N) cmax = fmaxf(cmax, v[j]);
+              for (int j = 0; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < p.N) cmax = fmaxf(cmax, v[j]);
+            }
             const float nmax = fmaxf(run_max, cmax);
-            float s = run_sum * __expf(run_max - nmax);
+            const float nm2 = nmax * kLog2e;
+            float s0 = run_sum * fast_exp2(run_max * kLog2e - nm2), s1 = 0.f;
+            if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (n0 + j < p.N) s += __expf(v[j] - nmax);
+              for (int j = 0; j < 32; j += 2) {
+                s0 += fast_exp2(fmaf(v[j], kLog2e, -nm2));
+                s1 += fast_exp2(fmaf(v[j + 1], kLog2e, -nm2));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < p.N) s0 += fast_exp2(fmaf(v[j], kLog2e, -nm2));
+            }
             run_max = nmax;
-            run_sum = s;
-            if (tgt >= n0 && tgt < n0 + 32) {
+            run_sum = s0 + s1;
+            if ((uint64_t)(tgt - n0) < 32ull) {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (tgt == n0 + j) p.target_logit[grow] = v[j];
@@ -351,36 +448,51 @@ __global__ void __launch_bounds__(256, 1)
           }
           case RP_EPI_RELU_GRAD: {
             // out = acc * (aux > 0), aux = the ReLU output h1 (layers.py:221)
-            float r[32];
-            load_chunk(p, m, n0, b, r);
+            float rr[32];
+            load_chunk(p, m, n0, b, rr);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = r[j] > 0.f ? v[j] : 0.f;
-            store_chunk(p, m, n0, b, v);
+            for (int j = 0; j < 32; ++j) v[j] = rr[j] > 0.f ? v[j] * p.alpha : 0.f;
+            RP_EMIT();
             break;
           }
           case RP_EPI_CE_GRAD: {
+            // dz = softmax * scale - onehot * scale, scale folded into the exponent
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float pr = __expf(v[j] - lse_row);
-              v[j] = (pr - ((tgt == n0 + j) ? 1.f : 0.f)) * p.ce_scale;
+            for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], kLog2e, -lse2));
+            if ((uint64_t)(tgt - n0) < 32ull) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (tgt == n0 + j) v[j] -= p.ce_scale;
             }
-            store_chunk(p, m, n0, b, v);
+            RP_EMIT();
             break;
           }
           default:
             break;
         }
       }
-      if (row_ok && p.epi == RP_EPI_LSE_PARTIAL) {
-        float* dst = p.partial + (grow * p.n_tiles + nb) * 2;
-        dst[0] = run_max;
-        dst[1] = run_sum;
+#undef RP_EMIT
+      if (p.epi == RP_EPI_LSE_PARTIAL) {
+        // combine the two column halves of each row
+        red[(half * 2 + 0) * 128 + q * 32 + lane] = run_max;
+        red[(half * 2 + 1) * 128 + q * 32 + lane] = run_sum;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (half == 0 && row_ok) {
+          const float m1 = red[2 * 128 + q * 32 + lane], s1 = red[3 * 128 + q * 32 + lane];
+          const float M = fmaxf(run_max, m1);
+          const float S = run_sum * fast_exp2((run_max - M) * kLog2e) + s1 * fast_exp2((m1 - M) * kLog2e);
+          float* dst = p.partial + (grow * p.n_tiles + nb) * 2;
+          dst[0] = M;
+          dst[1] = S;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       tc_fence_before();
       mbar_arrive(&tmem_empty[acc]);
     }
   }
 
+  if (warp >= 4 && p.tma_store && lane == 0) tma_store_wait_all();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -543,7 +655,28 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
       st = make_map(&mbl, a.B_lo, kTf32, a.N, a.K, a.ldb, batch, a.stride_b, Cfg::CHUNK, Cfg::BK, true);
     if (st) return st;
   }
+  CUtensorMap mc;
+  std::memset(&mc, 0, sizeof(mc));
+  bool tma_store = false;
+  {
+    auto enc = encoder();
+    const int64_t rows_c = a.M * batch;
+    // folded-batch rows must not spill into the next batch: M % BM == 0 when batched
+    const bool packed_batch = batch == 1 || (a.stride_c == a.M * a.ldc && a.M % Cfg::BM == 0);
+    if (enc && a.out_dtype == RP_BF16 && ks == 1 && a.C && packed_batch &&
+        (reinterpret_cast<uintptr_t>(a.C) & 15) == 0 && (a.ldc * 2) % 16 == 0 && a.N >= 32 &&
+        a.epilogue != RP_EPI_LSE_PARTIAL && rows_c < (1LL << 31)) {
+      cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)rows_c};
+      cuuint64_t strides[1] = {(cuuint64_t)(a.ldc * 2)};
+      cuuint32_t box[2] = {32, 32};
+      cuuint32_t estr[2] = {1, 1};
+      tma_store = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.C, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   GemmParams p{};
+  p.tma_store = tma_store;
   p.M = (int)a.M;
   p.N = (int)a.N;
   p.K = (int)a.K;
@@ -555,6 +688,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.m_tiles = (int)((a.M + Cfg::BM - 1) / Cfg::BM);
   p.n_tiles = (int)((a.N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles * p.batch;
+  p.n_fast = p.n_tiles < p.m_tiles;
   p.kb_per_pass = (int)((kchunk + Cfg::BK - 1) / Cfg::BK);
   p.out_bf16 = a.out_dtype == RP_BF16;
   p.epi = a.epilogue;
@@ -583,7 +717,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
              ((a.stride_c * oe) % 16 == 0 || p.batch == 1);
   if (p.num_tiles == 0) return RP_OK;
   const int grid = std::min(p.num_tiles, num_sms());
-  gemm_kernel<kTf32, BN><<<grid, 256, Cfg::SMEM_BYTES, stream>>>(ma, mal, mb, mbl, p);
+  gemm_kernel<kTf32, BN><<<grid, 384, Cfg::SMEM_BYTES, stream>>>(ma, mal, mb, mbl, mc, p);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(RP_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(err));
   return RP_OK;
