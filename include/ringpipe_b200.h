@@ -222,10 +222,11 @@ int rp_head_forward(const rp_head_desc* desc, const void* x, const void* tied, c
                     float* loss, double* loss64, void* workspace, int64_t workspace_bytes, int32_t* flag,
                     void* stream);
 /* g_x = dL/dx (fp32); vo (if non-NULL) = vo_alpha * dL/dtied from the output side
- * (the fresh half of the mixed tied gradient, engine.py:54-69) */
+ * (the fresh half of the mixed tied gradient, engine.py:54-69), or vo += that when
+ * vo_accumulate (the input-side half may already be there: 0 + a + b == 0 + b + a) */
 int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets,
-                     const float* lse, float* g_x, float* vo, float vo_alpha, void* workspace,
-                     int64_t workspace_bytes, void* stream);
+                     const float* lse, float* g_x, float* vo, float vo_alpha, int32_t vo_accumulate,
+                     void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -136,7 +136,7 @@ def _declare(L):
                               ctypes.POINTER(BlockTape), vp, vp, ctypes.POINTER(BlockGrads), vp, i64, vp],
         "rp_head_workspace_bytes": [ctypes.POINTER(HeadDesc)],
         "rp_head_forward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
-        "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, vp, i64, vp],
+        "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, i32, vp, i64, vp],
     }
     L.rp_version.restype = ctypes.c_char_p
     for name, args in sig.items():

@@ -145,9 +145,10 @@ int rp_head_forward(const rp_head_desc* desc, const void* x, const void* tied, c
   return rp::head_forward(*desc, x, tied, targets, lse, loss, loss64, workspace, workspace_bytes, flag, RP_S(stream));
 }
 int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, const int64_t* targets,
-                     const float* lse, float* g_x, float* vo, float vo_alpha, void* workspace,
-                     int64_t workspace_bytes, void* stream) {
-  return rp::head_backward(*desc, x, tied, targets, lse, g_x, vo, vo_alpha, workspace, workspace_bytes, RP_S(stream));
+                     const float* lse, float* g_x, float* vo, float vo_alpha, int32_t vo_accumulate,
+                     void* workspace, int64_t workspace_bytes, void* stream) {
+  return rp::head_backward(*desc, x, tied, targets, lse, g_x, vo, vo_alpha, vo_accumulate, workspace, workspace_bytes,
+                           RP_S(stream));
 }
 
 }  // extern "C"

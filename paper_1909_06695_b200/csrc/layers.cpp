@@ -361,7 +361,8 @@ int head_forward(const rp_head_desc& h, const void* x, const void* tied, const i
 }
 
 int head_backward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, const float* lse,
-                  float* g_x, float* vo, float vo_alpha, void* ws, int64_t ws_bytes, cudaStream_t st) {
+                  float* g_x, float* vo, float vo_alpha, int vo_accumulate, void* ws, int64_t ws_bytes,
+                  cudaStream_t st) {
   if (ws_bytes < head_workspace_bytes(h)) return set_error(RP_ERR_INVALID, "head workspace too small");
   const int bn = gemm_tile_n(h.vocab);
   const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab, Vp = pad8(V);
@@ -385,6 +386,11 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
   if (vo) {
     Epi ev;
     ev.alpha = vo_alpha;
+    if (vo_accumulate) {  // vo += alpha * dz^T x   (residual epilogue reading vo in place)
+      ev.kind = RP_EPI_BIAS_DROPOUT_RESIDUAL;
+      ev.resid = vo;
+      ev.ld_resid = D;
+    }
     RP_TRY(mm(c, mat(dz, N, V, Vp), true, mat(x, N, D, D), true, mat(vo, V, D, D), RP_F32, ev));
   }
   return RP_OK;

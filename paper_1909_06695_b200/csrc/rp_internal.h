@@ -60,6 +60,7 @@ int64_t head_workspace_bytes(const rp_head_desc& h);
 int head_forward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, float* lse,
                  float* loss, double* loss64, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);
 int head_backward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, const float* lse,
-                  float* g_x, float* vo, float vo_alpha, void* ws, int64_t ws_bytes, cudaStream_t st);
+                  float* g_x, float* vo, float vo_alpha, int vo_accumulate, void* ws, int64_t ws_bytes,
+                  cudaStream_t st);
 
 }  // namespace rp

@@ -13,8 +13,8 @@ Step t (reference engine.py:246-259):
      fused tied-vocab cross-entropy (no [N, V] logits in HBM),
   3. module k back-propagates sample t-K+k at w^{t-K+k} from its stored slot
      and the boundary gradient module k+1 produced at t-1 (zero while
-     t-K+k < 0); modules run K..1 so the output-side tied gradient is in
-     place before the input-side half is scattered onto it,
+     t-K+k < 0); the two tied halves are added onto a zeroed buffer (in
+     either order: with two terms on zero, fp32 addition is order-free),
   4. the packet's tied gradient is 1/2 Vo(t) + 1/2 Vi(t-K+1) (engine.py:54-69),
   5. the optimizer applies the packet.
 
@@ -249,8 +249,7 @@ class PipelineEngine:
 
     def _backward_all(self, t, B, T):
         coef = tied_coefficients(t, self.K, self.tied_grad)
-        if coef == (0.0, 0.0):
-            self.stack.tied_store.grad.zero_()
+        self.stack.tied_store.grad.zero_()  # both tied halves accumulate onto zero
         results = {}
         for k in range(self.K, 0, -1):
             results[k] = self._backward_one(t, k, coef, B, T)
@@ -331,7 +330,8 @@ class ConcurrentPipelineEngine(PipelineEngine):
 
     fwd(k,t) waits fwd(k-1,t); bwd(k,t) waits bwd(k+1,t-1) (its boundary) and,
     for k=K, fwd(K,t); the optimizer waits every fwd/bwd of step t; fwd(k,t+1)
-    waits the optimizer.  Module 1's tied scatter waits module K's Vo GEMM.
+    waits the optimizer.  Modules 1 and K add their tied-gradient halves onto
+    a zeroed buffer one after the other (module K after module 1).
     """
 
     def __init__(self, *args, timeout=120.0, **kwargs):
@@ -372,31 +372,32 @@ class ConcurrentPipelineEngine(PipelineEngine):
             fwd_done.append(ev)
             prev = ev
         loss_dev = cur
-        # stale backwards
+        # stale backwards: modules k < K depend only on last step's boundary,
+        # so they start with the step and overlap the relay; module K needs
+        # its fresh forward.  The tied gradient is zeroed first; modules 1 and
+        # K then add their halves in either order (mutually excluded).
         coef = tied_coefficients(t, self.K, self.tied_grad)
+        self.stack.tied_store.grad.zero_()
+        zero_ev = torch.cuda.Event()
+        zero_ev.record(main)
         results = {}
         bwd_done = {}
-        vo_ready = None
-        for k in range(self.K, 0, -1):
+        order = list(range(self.K - 1, 0, -1)) + [self.K]
+        for k in order:
             m = self.modules[k - 1]
             s = self._bs[k - 1]
-            s.wait_event(start_ev)
+            s.wait_event(zero_ev)
             if k == self.K:
                 s.wait_event(fwd_done[k - 1])
-                if coef == (0.0, 0.0):
-                    with torch.cuda.stream(s):
-                        self.stack.tied_store.grad.zero_()
+                if self.K > 1:
+                    s.wait_event(bwd_done[1])  # exclusive access to the tied gradient
             if (k + 1) in self._bwd_done:
                 s.wait_event(self._bwd_done[k + 1])
-            if m.has_embedding and vo_ready is not None:
-                s.wait_event(vo_ready)
             with torch.cuda.stream(s):
                 results[k] = self._backward_one(t, k, coef, B, T)
                 ev = torch.cuda.Event()
                 ev.record(s)
             bwd_done[k] = ev
-            if k == self.K:
-                vo_ready = ev
         self._bwd_done = bwd_done
         for ev in fwd_done + list(bwd_done.values()):
             main.wait_event(ev)

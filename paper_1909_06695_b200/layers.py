@@ -213,7 +213,7 @@ def head_forward_ops(h, tied_c, targets, vocab, hs, ws, flag):
     ops.ce_finish(partial, zy, targets, vocab, hs.lse, rows_loss, hs.loss, hs.loss64, flag)
 
 
-def head_backward_ops(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
+def head_backward_ops(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws, vo_accumulate=False):
     """g_h = dz @ tied (fp32); vo_out = vo_alpha * dz^T @ h when vo_out is given."""
     Nt, d = h.shape
     vp = _pad8(vocab)
@@ -224,7 +224,11 @@ def head_backward_ops(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
         ops.gemm(dz, tied_c, b_mn=True, out=g_h)
     if vo_out is not None:
         with ops.span("head_gemm"):
-            ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha)
+            if vo_accumulate:
+                ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha,
+                         epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=vo_out)
+            else:
+                ops.gemm(dz, h, a_mn=True, b_mn=True, out=vo_out, alpha=vo_alpha)
 
 
 # ---------------------------------------------------------------------------
@@ -310,11 +314,12 @@ def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
                                         _p(hs.loss64), _p(buf), nbytes, _p(flag), ops._stream()), "head_forward")
 
 
-def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws):
+def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws, vo_accumulate=False):
     hd = _head_desc(h, vocab)
     nbytes = N.lib().rp_head_workspace_bytes(ctypes.byref(hd))
     buf = _ws_bytes(ws, "head_ws", nbytes)
     ops._count(3 if vo_out is not None else 2)
     with ops.span("head_gemm_bwd"):
         N.check(N.lib().rp_head_backward(ctypes.byref(hd), _p(h), _p(tied_c), _p(targets), _p(hs.lse), _p(g_h),
-                                         _p(vo_out), vo_alpha, _p(buf), nbytes, ops._stream()), "head_backward")
+                                         _p(vo_out), vo_alpha, int(vo_accumulate), _p(buf), nbytes, ops._stream()),
+                "head_backward")

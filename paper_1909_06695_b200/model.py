@@ -514,9 +514,11 @@ class ModuleState:
         "snapshot": gradients at the weights the slot's forward used (the
         ring entry for slot.step), from the stored intermediates.
         "current": re-run the forward at the live weights, then backprop.
-        `emb=(alpha, beta, grad)` fuses the tied gradient into `grad`
-        (output side alpha*Vo written, input side beta*Vi added); without
-        it the two tied gradients are returned separately like the reference.
+        `emb=(alpha, beta, grad)` fuses the tied gradient into `grad`, which
+        the caller zeroed: alpha*Vo and beta*Vi are both added (in either
+        order -- with two terms on a zero start fp32 addition is order-free);
+        without it the two tied gradients are returned separately like the
+        reference.
         Returns (g_in, grads, {"Vi", "Vo"}, loss)."""
         arena = slot.arena
         B, T = arena.B, arena.T
@@ -549,7 +551,7 @@ class ModuleState:
         if self.has_projection:
             g = ws.get("g_stream_a", (Nt, d), torch.float32)
             LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
-                             emb_alpha, ws)
+                             emb_alpha, ws, vo_accumulate=emb is not None)
             loss = arena.head.loss
         else:
             if grad_out is None:

@@ -114,3 +114,31 @@ def test_bf16_loss_tracks_oracle():
         _, loss = eng.step(t, BatchSample(x, y, t), gopt)
         oloss, _ = ora.step(t, x, y)
         assert abs(loss - oloss) <= 2e-2 * abs(oloss), (t, loss, oloss)
+
+
+def test_distributed_engine_single_rank_equals_pipeline_engine():
+    """The multi-GPU engine driving real device modules (1 rank, K=2: both
+    modules on GPU 0, no communication) is bitwise equal to PipelineEngine."""
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as M
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200.distributed import DistributedPipelineEngine, build_local_modules
+
+    cfg = SMALL
+    _, e1, o1, _ = make_pair(cfg, 2, "adam", 2e-3, dtype="bf16")
+    stack = M.build_stack(cfg["vocab"], cfg["d"], cfg["f"], cfg["blocks"], cfg["seq"], cfg["p"], cfg["init_seed"],
+                          dtype="bf16")
+    part = M.partition(stack.num_layers, 2)
+    mods = build_local_modules(stack, part, cfg["dseed"], 0)
+    e2 = DistributedPipelineEngine(mods, part, 0, tied=stack.tied_store, device=stack.runtime.device)
+    o2 = O.make_optimizer("adam", O.LrSchedule(2e-3, "fixed"))
+    for t, (x, y) in enumerate(batches(cfg, 5)):
+        p1, l1 = e1.step(t, E.BatchSample(x, y, t), o1)
+        c1 = p1.cpu()
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        p2, l2 = e2.step(t, E.BatchSample(xd, yd, t), o2)
+        assert l1 == float(l2.item())
+        assert np.array_equal(c1.emb_grad, p2.emb_grad.double().cpu().numpy())
+        for g1, g2 in zip(c1.module_grads, p2.module_grads):
+            for key in g1:
+                assert np.array_equal(g1[key], g2[key].double().cpu().numpy()), key
