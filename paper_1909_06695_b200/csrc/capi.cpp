@@ -42,7 +42,7 @@ int rp_gemm(const rp_gemm_args* args, void* stream) {
   return rp::gemm(*args, static_cast<cudaStream_t>(stream));
 }
 
-int rp_gemm_tile_n(int64_t N) { return rp::gemm_tile_n(N); }
+int rp_gemm_tile_n(int64_t M, int64_t N, int64_t batch) { return rp::gemm_tile_n(M, N, batch); }
 
 int rp_splitk_reduce(const float* part, int32_t splits, int64_t M, int64_t N, float* out, int64_t ldo, void* stream) {
   return rp::splitk_reduce(part, splits, M, N, out, ldo, static_cast<cudaStream_t>(stream));

@@ -16,6 +16,7 @@
 // gradient dz).  "tf32x3" runs three accumulation passes (hi*hi + hi*lo +
 // lo*hi) over pre-split operands to reach fp32 accuracy on the tf32 pipe.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -231,6 +232,12 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // alloc, descriptor prefetch) overlapped the previous kernel's tail; wait
+  // for its results before touching global memory, and let the next kernel
+  // start its own prologue as our CTAs retire.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   }
 
-  if (warp >= 4 && p.tma_store && lane == 0) tma_store_wait_all();
+  if (warp >= 4 && p.tma_store && lane == 0) tma_store_wait_read();  // smem may be released
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -600,6 +607,15 @@ int make_map(CUtensorMap* map, const void* ptr, bool tf32, int64_t inner, int64_
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return RP_OK;
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RP_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 int num_sms() {
@@ -717,21 +733,49 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
              ((a.stride_c * oe) % 16 == 0 || p.batch == 1);
   if (p.num_tiles == 0) return RP_OK;
   const int grid = std::min(p.num_tiles, num_sms());
-  gemm_kernel<kTf32, BN><<<grid, 384, Cfg::SMEM_BYTES, stream>>>(ma, mal, mb, mbl, mc, p);
-  cudaError_t err = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_kernel<kTf32, BN>, ma, mal, mb, mbl, mc, p);
+  if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(RP_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(err));
   return RP_OK;
 }
 
 }  // namespace
 
-int gemm_tile_n(int64_t N) { return N > 128 ? 256 : (N > 64 ? 128 : 64); }
+// N tile.  Default: the widest tile (256) whenever N > 128 -- narrower tiles
+// read the A tile from shared memory more often per MMA and measured slower
+// on every block GEMM (tools/prof_block.py: 0.458 vs 0.593 ms per block
+// fwd+bwd).  RP_TILE_N_SPREAD=1 instead narrows N to give every SM two tiles.
+int gemm_tile_n(int64_t M, int64_t N, int64_t batch) {
+  static int spread = -1;
+  if (spread < 0) {
+    const char* e = getenv("RP_TILE_N_SPREAD");
+    spread = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!spread) return N > 128 ? 256 : (N > 64 ? 128 : 64);
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  const int64_t mt = (M + 127) / 128 * std::max<int64_t>(batch, 1);
+  for (int bn : {256, 128}) {
+    if (mt * ((N + bn - 1) / bn) >= 2 * 148) return bn;
+  }
+  return 64;
+}
 
 int gemm(const rp_gemm_args& a, cudaStream_t stream) {
   if (a.M < 0 || a.N < 0 || a.K <= 0) return set_error(RP_ERR_DIMENSION, "bad GEMM shape");
   if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return set_error(RP_ERR_DIMENSION, "GEMM dim too large");
   const bool tf32 = a.math != RP_MATH_BF16;
-  const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.N);
+  const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.M, a.N, a.k_splits > 1 ? a.k_splits : a.batch);
   if (tf32) {
     if (bn == 256) return launch<true, 256>(a, stream);
     if (bn == 128) return launch<true, 128>(a, stream);

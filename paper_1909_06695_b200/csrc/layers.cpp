@@ -147,7 +147,7 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.stride_c = C.bstride;
   int splits = 1;
   if (out_dtype == RP_F32 && e.kind == RP_EPI_STORE && g.batch == 1 && c.splitk)
-    splits = choose_splits(g.M, g.N, g.K, gemm_tile_n(g.N), c.splitk_cap);
+    splits = choose_splits(g.M, g.N, g.K, 256, c.splitk_cap);
   if (splits > 1) {
     g.k_splits = splits;
     g.C = c.splitk;
@@ -328,7 +328,7 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
 constexpr int64_t kHeadSplitK = 16;  // max split-K factor of g_x = dz @ tied
 
 int64_t head_workspace_bytes(const rp_head_desc& h) {
-  const int bn = gemm_tile_n(h.vocab);
+  const int bn = gemm_tile_n(h.rows, h.vocab, 1);
   const int64_t nt = (h.vocab + bn - 1) / bn;
   const int64_t e = esize(h.dtype);
   int64_t b = al256(h.rows * nt * 2 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
@@ -340,7 +340,7 @@ int64_t head_workspace_bytes(const rp_head_desc& h) {
 int head_forward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, float* lse,
                  float* loss, double* loss64, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st) {
   if (ws_bytes < head_workspace_bytes(h)) return set_error(RP_ERR_INVALID, "head workspace too small");
-  const int bn = gemm_tile_n(h.vocab);
+  const int bn = gemm_tile_n(h.rows, h.vocab, 1);
   const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab;
   Bump bp{static_cast<char*>(ws), ws_bytes};
   float* partial = static_cast<float*>(bp.take(N * nt * 2 * 4));
@@ -364,7 +364,7 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
                   float* g_x, float* vo, float vo_alpha, int vo_accumulate, void* ws, int64_t ws_bytes,
                   cudaStream_t st) {
   if (ws_bytes < head_workspace_bytes(h)) return set_error(RP_ERR_INVALID, "head workspace too small");
-  const int bn = gemm_tile_n(h.vocab);
+  const int bn = gemm_tile_n(h.rows, h.vocab, 1);
   const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab, Vp = pad8(V);
   Bump bp{static_cast<char*>(ws), ws_bytes};
   bp.take(N * nt * 2 * 4);

@@ -13,7 +13,7 @@ int set_error(int status, const char* fmt, ...);
 int check_launch(const char* what);
 
 int gemm(const rp_gemm_args& a, cudaStream_t stream);
-int gemm_tile_n(int64_t N);
+int gemm_tile_n(int64_t M, int64_t N, int64_t batch);
 int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, int64_t ldo, cudaStream_t st);
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);

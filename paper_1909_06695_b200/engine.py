@@ -308,7 +308,7 @@ class PipelineEngine:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
         self.last_loss_device = loss_dev
         if sync:
-            self.runtime.check(f"step {t}")
+            self.runtime.check(f"step {t}", self.modules)
             loss = float(loss_dev.item())
             packet.loss = loss
             return packet, loss
@@ -412,11 +412,25 @@ class ConcurrentPipelineEngine(PipelineEngine):
             s.wait_event(done)
         self.last_loss_device = loss_dev
         if sync:
-            self.runtime.check(f"step {t}")
+            try:
+                self.runtime.check(f"step {t}", self.modules)
+            except (NonFiniteError, DimensionError) as exc:
+                # the reference's threaded executor reports worker errors as
+                # WorkerFailure with a per-module diagnostic (engine.py:300-311, 390-396)
+                raise WorkerFailure(self._diagnostic(t, exc)) from exc
             loss = float(loss_dev.item())
             packet.loss = loss
             return packet, loss
         return packet, loss_dev
+
+    def _diagnostic(self, t, exc):
+        lines = [f"concurrent schedule aborted at step {t}", f"{type(exc).__name__}: {exc}"]
+        for row in self.trace.rows[-3 * self.K:]:
+            lines.append(str(row))
+        return "\n".join(lines)
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
 
 
 class SequentialRunner(PipelineEngine):
@@ -454,6 +468,6 @@ def sequential_gradients(stack, batch, dropout_seed, step, train=True):
     loss = m.forward(x, step, batch.sample_id, y, train)
     slot = m.pop_slot()
     _, grads, tied, _ = m.recompute_backward(slot, None, "snapshot", train)
-    stack.runtime.check("sequential_gradients")
+    stack.runtime.check("sequential_gradients", [m])
     host = {k: v.double().cpu().numpy() for k, v in grads.items()}
     return host, tied["Vi"].double().cpu().numpy(), tied["Vo"].double().cpu().numpy(), float(loss.item())

@@ -203,7 +203,7 @@ class HeadState:
 def head_forward_ops(h, tied_c, targets, vocab, hs, ws, flag):
     """Mean CE of h @ tied^T against targets without materialising logits."""
     Nt = h.shape[0]
-    bn = ops.gemm_tile_n(vocab)
+    bn = ops.gemm_tile_n(vocab, Nt)
     nt = (vocab + bn - 1) // bn
     partial = ws.get("head_partial", (Nt, nt, 2), torch.float32)
     zy = ws.get("head_zy", (Nt,), torch.float32)

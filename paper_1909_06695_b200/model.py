@@ -204,6 +204,14 @@ class LayerStack:
     def num_layers(self):
         return len(self.layers)
 
+    def refresh(self):
+        """Re-derive every compute copy from the fp32 masters after the caller
+        edited `params` / `tied` in place (the reference's live arrays have no
+        copies to invalidate)."""
+        for st in self.storage:
+            st.ring_step = [None] * len(st.ring)
+        self.tied_store.refresh()
+
 
 def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, *, dtype="bf16",
                 device=None):
@@ -405,6 +413,8 @@ class ModuleState:
                 self.grad_views[f"L{start + off}.{name}"] = t
         self._standalone_tied = None
         self.last_forward_step = None
+        # per-module device status word (RP_FLAG_*), polled once per step
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     # -- seeds / snapshots -------------------------------------------------
     def _layer_seed(self, step, offset):
@@ -471,7 +481,7 @@ class ModuleState:
 
     def _run_forward(self, wstep, arena, seeds, train, out, ws):
         B, T = arena.B, arena.T
-        flag = self.runtime.flag
+        flag = self.flag
         nxt = 0  # next act buffer to fill
         cur = None
         for off, layer in enumerate(self.layers):

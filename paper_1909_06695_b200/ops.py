@@ -210,8 +210,8 @@ def gemm(
     return out
 
 
-def gemm_tile_n(n):
-    return N.lib().rp_gemm_tile_n(n)
+def gemm_tile_n(n, m=8192, batch=1):
+    return N.lib().rp_gemm_tile_n(m, n, batch)
 
 
 # ---------------------------------------------------------------------------

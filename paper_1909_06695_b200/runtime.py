@@ -41,14 +41,18 @@ class Runtime:
             cls._by_device[device] = rt
         return rt
 
-    def check(self, context="step"):
-        """Synchronously read and clear the status word; raise on errors."""
-        self._host.copy_(self.flag)
-        torch.cuda.current_stream(self.device).synchronize()
-        bits = int(self._host.item())
-        if bits:
-            self.flag.zero_()
-            if bits & N.FLAG_DIMENSION:
-                raise DimensionError(f"token or target id out of range ({context})")
-            if bits & N.FLAG_NONFINITE:
-                raise NonFiniteError(f"non-finite values in {context}")
+    def check(self, context="step", modules=()):
+        """Synchronously read and clear the status words (the optimizer's and
+        each module's); raise the reference exception naming the culprit."""
+        words = [m.flag for m in modules] + [self.flag]
+        host = torch.cat([w.view(1) for w in words]).cpu()
+        bad = [(i, int(b)) for i, b in enumerate(host.tolist()) if b]
+        if not bad:
+            return
+        for w in words:
+            w.zero_()
+        i, bits = bad[0]
+        where = f"module {modules[i].index}" if i < len(modules) else "optimizer update"
+        if bits & N.FLAG_DIMENSION:
+            raise DimensionError(f"token or target id out of range in {where} ({context})")
+        raise NonFiniteError(f"non-finite values in {where} ({context})")

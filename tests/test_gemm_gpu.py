@@ -133,7 +133,7 @@ def test_lse_partial_and_ce_grad(dev, dtype):
     h = _mk((M, d), dt, dev, 15) * 3
     tied = _mk((V, d), dt, dev, 16)
     y = torch.randint(0, V, (M,), device=dev, generator=None)
-    bn = ops.gemm_tile_n(V)
+    bn = ops.gemm_tile_n(V, M)
     nt = (V + bn - 1) // bn
     partial = torch.empty((M, nt, 2), dtype=torch.float32, device=dev)
     zy = torch.empty((M,), dtype=torch.float32, device=dev)
