@@ -88,6 +88,7 @@ typedef struct rp_gemm_args {
   float* target_logit;      /* [batch*M] */
   float ce_scale;
   int32_t k_splits; /* > 1: C = [k_splits, M, N] fp32 partials over K ranges (rp_splitk_reduce) */
+  int32_t max_ctas; /* > 0: cap the persistent grid (SM budget when sharing the GPU with another stream) */
 } rp_gemm_args;
 
 const char* rp_version(void);
@@ -182,6 +183,7 @@ typedef struct rp_block_desc {
   uint64_t drop_seed;   /* mix64(dropout_seed, step, layer), model.py:218-219 */
   uint64_t drop_threshold;
   float drop_scale;
+  int32_t max_ctas; /* SM budget for every GEMM of the layer (0 = whole GPU) */
 } rp_block_desc;
 
 typedef struct rp_block_weights {

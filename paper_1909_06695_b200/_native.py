@@ -58,13 +58,14 @@ class GemmArgs(ctypes.Structure):
         ("target_logit", ctypes.c_void_p),
         ("ce_scale", ctypes.c_float),
         ("k_splits", ctypes.c_int32),
+        ("max_ctas", ctypes.c_int32),
     ]
 
 
 class BlockDesc(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("d", ctypes.c_int64), ("f", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_seed", ctypes.c_uint64),
-                ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float)]
+                ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float), ("max_ctas", ctypes.c_int32)]
 
 
 class BlockWeights(ctypes.Structure):

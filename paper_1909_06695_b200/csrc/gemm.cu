@@ -27,18 +27,21 @@
 
 namespace rp {
 
-template <bool kTf32, int BN_>
+template <bool kTf32, int BN_, int kCta_ = 1>
 struct GemmCfg {
-  static constexpr int BM = 128;
+  static constexpr int kCta = kCta_;       // 2: CTA pair shares one 256-row tile (cta_group::2)
+  static constexpr int BM = 128;           // rows of A / D per CTA
+  static constexpr int BM_TILE = 128 * kCta;
   static constexpr int BN = BN_;
+  static constexpr int B_ROWS = BN / kCta;  // N rows of B staged per CTA
   static constexpr int ELEM = kTf32 ? 4 : 2;
   static constexpr int BK = 128 / ELEM;     // one 128-byte swizzle row of K
   static constexpr int UK = kTf32 ? 8 : 16;  // K per tcgen05.mma
   static constexpr int CHUNK = 128 / ELEM;  // MN elements per 128B chunk (MN-major)
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
   static constexpr int STAGE_OUT = 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGE_OUT + 1024 + 256 + 2048;
@@ -189,12 +192,13 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
   }
 }
 
-template <bool kTf32, int BN>
+template <bool kTf32, int BN, int kCta>
 __global__ void __launch_bounds__(384, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA_lo,
                 const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB_lo,
                 const __grid_constant__ CUtensorMap mapC, const GemmParams p) {
-  using Cfg = GemmCfg<kTf32, BN>;
+  using Cfg = GemmCfg<kTf32, BN, kCta>;
+  static_assert(kCta == 1 || !kTf32, "CTA-pair mode is bf16 only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_out = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // 1024-aligned
@@ -206,6 +210,9 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = kCta == 2 ? cluster_rank() : 0;  // CTA rank within the pair
+  const bool leader = crank == 0;
+  const int tile0 = blockIdx.x / kCta, tstep = gridDim.x / kCta;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapA);
@@ -223,13 +230,21 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 256);
+      // 1 CTA: every epilogue thread arrives; pair: one arrival per epilogue
+      // warp of both CTAs, on the leader's barrier
+      mbar_init(&tmem_empty[a], kCta == 2 ? 16 : 256);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (kCta == 2)
+      tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCta == 2) cluster_sync();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Programmatic dependent launch: everything above (barrier init, TMEM
@@ -243,10 +258,10 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
         int mb, nb, b;
         decode_tile(p, tile, mb, nb, b);
-        const int m0 = mb * Cfg::BM, n0 = nb * BN;
+        const int m0 = mb * Cfg::BM_TILE + crank * Cfg::BM, n0 = nb * BN + crank * Cfg::B_ROWS;
         const int kbase = p.ksplit ? b * p.ksplit : 0;
         const int bc = p.ksplit ? 0 : b;
         for (int pass = 0; pass < p.passes; ++pass) {
@@ -254,23 +269,43 @@ __global__ void __launch_bounds__(384, 1)
           const CUtensorMap* mbm = (pass == 1) ? &mapB_lo : &mapB;
           for (int kb = 0; kb < p.kb_per_pass; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
             uint8_t* sb = sa + Cfg::A_BYTES;
             const int k0 = kbase + kb * Cfg::BK;
-            if (!p.a_mn) {
-              tma_load_3d(sa, ma, &full[stage], k0, m0, bc);
-            } else {
+            if constexpr (kCta == 2) {
+              // both CTAs' bytes complete on the leader's barrier
+              const uint32_t fb = leader_addr(&full[stage]);
+              if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+              if (!p.a_mn) {
+                tma_load_3d_pair(sa, ma, fb, k0, m0, bc);
+              } else {
 #pragma unroll
-              for (int c = 0; c < Cfg::BM / Cfg::CHUNK; ++c)
-                tma_load_3d(sa + c * (Cfg::BK * 128), ma, &full[stage], m0 + c * Cfg::CHUNK, k0, bc);
-            }
-            if (!p.b_mn) {
-              tma_load_3d(sb, mbm, &full[stage], k0, n0, bc);
-            } else {
+                for (int c = 0; c < Cfg::BM / Cfg::CHUNK; ++c)
+                  tma_load_3d_pair(sa + c * (Cfg::BK * 128), ma, fb, m0 + c * Cfg::CHUNK, k0, bc);
+              }
+              if (!p.b_mn) {
+                tma_load_3d_pair(sb, mbm, fb, k0, n0, bc);
+              } else {
 #pragma unroll
-              for (int c = 0; c < BN / Cfg::CHUNK; ++c)
-                tma_load_3d(sb + c * (Cfg::BK * 128), mbm, &full[stage], n0 + c * Cfg::CHUNK, k0, bc);
+                for (int c = 0; c < Cfg::B_ROWS / Cfg::CHUNK; ++c)
+                  tma_load_3d_pair(sb + c * (Cfg::BK * 128), mbm, fb, n0 + c * Cfg::CHUNK, k0, bc);
+              }
+            } else {
+              mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+              if (!p.a_mn) {
+                tma_load_3d(sa, ma, &full[stage], k0, m0, bc);
+              } else {
+#pragma unroll
+                for (int c = 0; c < Cfg::BM / Cfg::CHUNK; ++c)
+                  tma_load_3d(sa + c * (Cfg::BK * 128), ma, &full[stage], m0 + c * Cfg::CHUNK, k0, bc);
+              }
+              if (!p.b_mn) {
+                tma_load_3d(sb, mbm, &full[stage], k0, n0, bc);
+              } else {
+#pragma unroll
+                for (int c = 0; c < BN / Cfg::CHUNK; ++c)
+                  tma_load_3d(sb + c * (Cfg::BK * 128), mbm, &full[stage], n0 + c * Cfg::CHUNK, k0, bc);
+              }
             }
             if (++stage == Cfg::STAGES) {
               stage = 0;
@@ -281,9 +316,9 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread) ----------------
-      const uint32_t idesc = umma_idesc(kTf32, p.a_mn, p.b_mn, Cfg::BM, BN);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (single thread; the pair's leader) ----------------
+      const uint32_t idesc = umma_idesc(kTf32, p.a_mn, p.b_mn, Cfg::BM_TILE, BN);
       const uint32_t a_lbo = p.a_mn ? Cfg::BK * 128 : 16;
       const uint32_t b_lbo = p.b_mn ? Cfg::BK * 128 : 16;
       const uint32_t a_step = p.a_mn ? Cfg::UK * 128 : 32;
@@ -293,7 +328,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t a_sbo = (kTf32 && p.a_mn) ? 512u : 1024u, b_sbo = (kTf32 && p.b_mn) ? 512u : 1024u;
       uint32_t stage = 0, phase = 0;
       int local = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+      for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -309,16 +344,25 @@ __global__ void __launch_bounds__(384, 1)
             for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
               const uint64_t ad = umma_desc(sa + k * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, b_sbo, b_lay);
-              tc_mma<kTf32>(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
+              if constexpr (kCta == 2)
+                tc_mma_pair(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
+              else
+                tc_mma<kTf32>(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
             }
-            tc_commit(&empty[stage]);
+            if constexpr (kCta == 2)
+              tc_commit_pair(&empty[stage]);
+            else
+              tc_commit(&empty[stage]);
             if (++stage == Cfg::STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
         }
-        tc_commit(&tmem_full[acc]);
+        if constexpr (kCta == 2)
+          tc_commit_pair(&tmem_full[acc]);
+        else
+          tc_commit(&tmem_full[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -332,14 +376,15 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* my_out = stage_out + (warp - 4) * 2048;                           // 32 rows x 64 B, 64B-swizzled
     const float kLog2e = 1.4426950408889634f;
     int local = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
       int mb, nb, b;
       decode_tile(p, tile, mb, nb, b);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = (int64_t)mb * Cfg::BM + q * 32 + lane;
+      const int64_t mrow0 = (int64_t)mb * Cfg::BM_TILE + crank * Cfg::BM;  // this CTA's first row
+      const int64_t m = mrow0 + q * 32 + lane;
       const bool row_ok = m < p.M;
       const int64_t grow = (int64_t)b * p.M + m;  // row index over the folded batch
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
@@ -365,7 +410,7 @@ __global__ void __launch_bounds__(384, 1)
             float z[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) z[j] = 0.f;
-            emit_tma(mapC, my_out, z, lane, n0, (int)((int64_t)b * p.M + (int64_t)mb * Cfg::BM + q * 32));
+            emit_tma(mapC, my_out, z, lane, n0, (int)((int64_t)b * p.M + mrow0 + q * 32));
           }
           continue;
         }
@@ -373,7 +418,7 @@ __global__ void __launch_bounds__(384, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int trow = (int)((int64_t)b * p.M + (int64_t)mb * Cfg::BM + q * 32);
+        const int trow = (int)((int64_t)b * p.M + mrow0 + q * 32);
 #define RP_EMIT()                                            \
   do {                                                       \
     if (p.tma_store)                                         \
@@ -495,16 +540,25 @@ __global__ void __launch_bounds__(384, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
+      if constexpr (kCta == 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&tmem_empty[acc]));
+      } else {
+        mbar_arrive(&tmem_empty[acc]);
+      }
     }
   }
 
   if (warp >= 4 && p.tma_store && lane == 0) tma_store_wait_read();  // smem may be released
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCta == 2) cluster_sync();  // the leader's MMAs wrote both CTAs' TMEM
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (kCta == 2)
+      tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -609,6 +663,15 @@ int make_map(CUtensorMap* map, const void* ptr, bool tf32, int64_t inner, int64_
   return RP_OK;
 }
 
+bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RP_2CTA");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -629,12 +692,13 @@ int num_sms() {
   return n;
 }
 
-template <bool kTf32, int BN>
+template <bool kTf32, int BN, int kCta>
 int launch(const rp_gemm_args& a, cudaStream_t stream) {
-  using Cfg = GemmCfg<kTf32, BN>;
+  using Cfg = GemmCfg<kTf32, BN, kCta>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_kernel<kTf32, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_kernel<kTf32, BN, kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM_BYTES);
   });
   CUtensorMap ma, mal, mb, mbl;
   const int ks = a.k_splits > 1 ? a.k_splits : 1;
@@ -650,7 +714,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
     st = make_map(&ma, a.A, kTf32, a.M, a.K, a.lda, batch, a.stride_a, Cfg::CHUNK, Cfg::BK, true);
   if (st) return st;
   if (!a.b_mn_major)
-    st = make_map(&mb, a.B, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, BN, false);
+    st = make_map(&mb, a.B, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, Cfg::B_ROWS, false);
   else
     st = make_map(&mb, a.B, kTf32, a.N, a.K, a.ldb, batch, a.stride_b, Cfg::CHUNK, Cfg::BK, true);
   if (st) return st;
@@ -666,7 +730,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
       st = make_map(&mal, a.A_lo, kTf32, a.M, a.K, a.lda, batch, a.stride_a, Cfg::CHUNK, Cfg::BK, true);
     if (st) return st;
     if (!a.b_mn_major)
-      st = make_map(&mbl, a.B_lo, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, BN, false);
+      st = make_map(&mbl, a.B_lo, kTf32, a.K, a.N, a.ldb, batch, a.stride_b, Cfg::BK, Cfg::B_ROWS, false);
     else
       st = make_map(&mbl, a.B_lo, kTf32, a.N, a.K, a.ldb, batch, a.stride_b, Cfg::CHUNK, Cfg::BK, true);
     if (st) return st;
@@ -701,7 +765,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.a_mn = a.a_mn_major;
   p.b_mn = a.b_mn_major;
   p.passes = passes;
-  p.m_tiles = (int)((a.M + Cfg::BM - 1) / Cfg::BM);
+  p.m_tiles = (int)((a.M + Cfg::BM_TILE - 1) / Cfg::BM_TILE);
   p.n_tiles = (int)((a.N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles * p.batch;
   p.n_fast = p.n_tiles < p.m_tiles;
@@ -732,18 +796,23 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.vec_ok = ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) && ((a.ldc * oe) % 16 == 0) &&
              ((a.stride_c * oe) % 16 == 0 || p.batch == 1);
   if (p.num_tiles == 0) return RP_OK;
-  const int grid = std::min(p.num_tiles, num_sms());
+  int grid = std::min(p.num_tiles * kCta, num_sms() / kCta * kCta);
+  if (a.max_ctas > 0) grid = std::min(grid, std::max(kCta, a.max_ctas / kCta * kCta));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kCta;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_kernel<kTf32, BN>, ma, mal, mb, mbl, mc, p);
+  cfg.numAttrs = kCta > 1 ? 2 : 1;
+  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_kernel<kTf32, BN, kCta>, ma, mal, mb, mbl, mc, p);
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(RP_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(err));
   return RP_OK;
@@ -777,13 +846,19 @@ int gemm(const rp_gemm_args& a, cudaStream_t stream) {
   const bool tf32 = a.math != RP_MATH_BF16;
   const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.M, a.N, a.k_splits > 1 ? a.k_splits : a.batch);
   if (tf32) {
-    if (bn == 256) return launch<true, 256>(a, stream);
-    if (bn == 128) return launch<true, 128>(a, stream);
-    return launch<true, 64>(a, stream);
+    if (bn == 256) return launch<true, 256, 1>(a, stream);
+    if (bn == 128) return launch<true, 128, 1>(a, stream);
+    return launch<true, 64, 1>(a, stream);
   }
-  if (bn == 256) return launch<false, 256>(a, stream);
-  if (bn == 128) return launch<false, 128>(a, stream);
-  return launch<false, 64>(a, stream);
+  // bf16: CTA pairs (cta_group::2, 256-row tiles, half of B staged per CTA)
+  // whenever there are rows for both CTAs of a pair
+  if (bn >= 128 && a.M > 128 && pair_enabled()) {
+    if (bn == 256) return launch<false, 256, 2>(a, stream);
+    return launch<false, 128, 2>(a, stream);
+  }
+  if (bn == 256) return launch<false, 256, 1>(a, stream);
+  if (bn == 128) return launch<false, 128, 1>(a, stream);
+  return launch<false, 64, 1>(a, stream);
 }
 
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,

@@ -50,6 +50,7 @@ inline Mat bmat(const void* p, int64_t b, int64_t rows, int64_t cols, int64_t ld
 struct Ctx {
   int dtype;  // compute dtype of activations / weights
   cudaStream_t st;
+  int max_ctas = 0;
   char* split_base = nullptr;  // tf32x3 split scratch
   int64_t split_cap = 0;
   float* splitk = nullptr;  // split-K partials
@@ -115,6 +116,7 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   std::memset(&g, 0, sizeof(g));
   g.math = c.dtype == RP_BF16 ? RP_MATH_BF16 : RP_MATH_TF32X3;
   g.out_dtype = out_dtype;
+  g.max_ctas = c.max_ctas;
   g.a_mn_major = a_mn;
   g.b_mn_major = b_mn;
   g.M = a_mn ? A.cols : A.rows;
@@ -217,6 +219,7 @@ int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void*
   Bump bp{static_cast<char*>(ws), ws_bytes};
   float* scores = static_cast<float*>(bp.take(B * T * Tp * 4));
   Ctx c{dt, st};
+  c.max_ctas = d.max_ctas;
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
   const char* qkv = static_cast<const char*>(tp.qkv);
@@ -276,6 +279,7 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   float* pg = static_cast<float*>(bp.take(nbp * pw * 4));
   float* pb = static_cast<float*>(bp.take(nbp * pw * 4));
   Ctx c{dt, st};
+  c.max_ctas = d.max_ctas;
   c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
   c.splitk_cap = kBlockSplitK;
   c.split_base = bp.base + bp.off;

@@ -339,8 +339,16 @@ class ConcurrentPipelineEngine(PipelineEngine):
         if self.K < 2:
             raise ValueError("concurrent execution needs K >= 2")
         self._timeout = timeout
-        self._fs = [torch.cuda.Stream(device=self.device) for _ in range(self.K)]
-        self._bs = [torch.cuda.Stream(device=self.device) for _ in range(self.K)]
+        # the relay and module K's backward form the step's critical path:
+        # high-priority streams; stale backwards of modules k < K run beside
+        # them on low-priority streams with a capped SM budget
+        hi, lo = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, 0)
+        self._fs = [torch.cuda.Stream(device=self.device, priority=-1) for _ in range(self.K)]
+        self._bs = [torch.cuda.Stream(device=self.device, priority=(-1 if k == self.K else 0))
+                    for k in range(1, self.K + 1)]
+        import os
+
+        self.side_ctas = int(os.environ.get("RP_SIDE_CTAS", "0"))
         self._bwd_done = {}
 
     def step(self, t, batch, optimizer=None, sync=True):
@@ -393,10 +401,16 @@ class ConcurrentPipelineEngine(PipelineEngine):
                     s.wait_event(bwd_done[1])  # exclusive access to the tied gradient
             if (k + 1) in self._bwd_done:
                 s.wait_event(self._bwd_done[k + 1])
-            with torch.cuda.stream(s):
-                results[k] = self._backward_one(t, k, coef, B, T)
-                ev = torch.cuda.Event()
-                ev.record(s)
+            from . import layers as _LY
+
+            _LY.CTA_BUDGET["value"] = self.side_ctas if k < self.K else 0
+            try:
+                with torch.cuda.stream(s):
+                    results[k] = self._backward_one(t, k, coef, B, T)
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+            finally:
+                _LY.CTA_BUDGET["value"] = 0
             bwd_done[k] = ev
         self._bwd_done = bwd_done
         for ev in fwd_done + list(bwd_done.values()):

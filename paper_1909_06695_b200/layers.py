@@ -243,8 +243,14 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
+# SM budget for the block GEMMs issued from the current thread (0 = whole GPU);
+# the concurrent engine lowers it for work off the critical path.
+CTA_BUDGET = {"value": 0}
+
+
 def _block_desc(x, f, B, T, drop):
     dsc = N.BlockDesc()
+    dsc.max_ctas = CTA_BUDGET["value"]
     dsc.B, dsc.T, dsc.d, dsc.f = B, T, x.shape[-1], f
     dsc.dtype = N.BF16 if x.dtype == torch.bfloat16 else N.F32
     if drop is not None:
