@@ -43,8 +43,9 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
-  static constexpr int STAGE_OUT = 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGE_OUT + 1024 + 256 + 2048;
+  static constexpr int STAGE_OUT = 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles (TMA store)
+  static constexpr int STAGE_IN = 8 * 32 * 64;   // per-warp 32x32 bf16 residual tiles (TMA load); LSE reuses it
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGE_OUT + STAGE_IN + 1024 + 256;
 };
 
 struct GemmParams {
@@ -71,6 +72,7 @@ struct GemmParams {
   int ksplit;  // > 0: "batch" b covers K range [b*ksplit, (b+1)*ksplit) of one matrix
   int n_fast;  // raster: N tiles fastest
   int tma_store;  // bf16 C written by TMA bulk stores from a swizzled smem tile
+  int tma_resid;  // bf16 residual / aux read by TMA bulk loads into a swizzled smem tile
 };
 
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int n0, int b,
@@ -146,6 +148,47 @@ __device__ __forceinline__ void load_chunk(const GemmParams& p, int64_t m, int n
   }
 }
 
+// Raw bf16 bits of 32 consecutive residual / aux elements (4 x 16B), issued
+// one chunk ahead so the load latency hides behind the current chunk's math.
+__device__ __forceinline__ void fetch_raw_bf16(const GemmParams& p, int64_t m, int n0, int b, uint4 (&raw)[4]) {
+  const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.resid) +
+                                                    ((int64_t)b * p.stride_resid + m * p.ld_resid + n0));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) raw[q] = src[q];
+}
+__device__ __forceinline__ void unpack_raw_bf16(const uint4 (&raw)[4], float (&r)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t w[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+      r[q * 8 + 2 * h] = f.x;
+      r[q * 8 + 2 * h + 1] = f.y;
+    }
+  }
+}
+// 32 bias values as 8 broadcast float4 loads (or scalar at the ragged edge)
+__device__ __forceinline__ void load_bias(const GemmParams& p, int n0, bool full, float (&bb)[32]) {
+  if (!p.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bb[j] = 0.f;
+  } else if (full && (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0) {
+    const float4* s = reinterpret_cast<const float4*>(p.bias + n0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 f = s[q];
+      bb[4 * q] = f.x;
+      bb[4 * q + 1] = f.y;
+      bb[4 * q + 2] = f.z;
+      bb[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bb[j] = (n0 + j < p.N) ? p.bias[n0 + j] : 0.f;
+  }
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -196,17 +239,20 @@ template <bool kTf32, int BN, int kCta>
 __global__ void __launch_bounds__(384, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA_lo,
                 const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapB_lo,
-                const __grid_constant__ CUtensorMap mapC, const GemmParams p) {
+                const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapR,
+                const GemmParams p) {
   using Cfg = GemmCfg<kTf32, BN, kCta>;
   static_assert(kCta == 1 || !kTf32, "CTA-pair mode is bf16 only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_out = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + Cfg::STAGE_OUT);
+  uint8_t* stage_in = stage_out + Cfg::STAGE_OUT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_in + Cfg::STAGE_IN);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tmem_full = empty + Cfg::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* in_bar = tmem_empty + 2;  // [8] per epilogue warp: residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_bar + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -222,6 +268,7 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch(&mapB_lo);
     }
     if (p.tma_store) tma_prefetch(&mapC);
+    if (p.tma_resid) tma_prefetch(&mapR);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -234,6 +281,7 @@ __global__ void __launch_bounds__(384, 1)
       // warp of both CTAs, on the leader's barrier
       mbar_init(&tmem_empty[a], kCta == 2 ? 16 : 256);
     }
+    for (int w = 0; w < 8; ++w) mbar_init(&in_bar[w], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -372,8 +420,11 @@ __global__ void __launch_bounds__(384, 1)
     const int q = warp & 3;
     const int half = (warp - 4) >> 2;
     constexpr int kHalf = BN / 64;  // 32-column chunks per half
-    float* red = reinterpret_cast<float*>(stage_out + Cfg::STAGE_OUT + 256);  // [2 halves][2][128]
-    uint8_t* my_out = stage_out + (warp - 4) * 2048;                           // 32 rows x 64 B, 64B-swizzled
+    float* red = reinterpret_cast<float*>(stage_in);       // [2 halves][2][128] (LSE only; no residual there)
+    uint8_t* my_out = stage_out + (warp - 4) * 2048;        // 32 rows x 64 B, 64B-swizzled
+    uint8_t* my_in = stage_in + (warp - 4) * 2048;          // residual / aux tile, same layout
+    uint64_t* my_bar = &in_bar[warp - 4];
+    uint32_t in_phase = 0;
     const float kLog2e = 1.4426950408889634f;
     int local = 0;
     for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
@@ -396,10 +447,53 @@ __global__ void __launch_bounds__(384, 1)
         tgt = p.targets[grow];
         if (p.epi == RP_EPI_CE_GRAD) lse2 = p.lse[grow] * kLog2e - __log2f(p.ce_scale);
       }
+      // residual / aux: TMA bulk-loads one 32x32 tile per warp, one chunk
+      // ahead (coalesced), else per-row loads prefetched one chunk ahead
+      const bool uses_aux = p.epi == RP_EPI_RELU_GRAD || (p.epi == RP_EPI_BIAS_DROPOUT_RESIDUAL && p.resid);
+      const bool tma_aux = uses_aux && p.tma_resid;
+      const bool aux = !tma_aux && uses_aux && p.out_bf16 && p.resid_vec;
+      const int trow0 = (int)((int64_t)b * p.M + mrow0 + q * 32);
+      uint4 nxt[4];
+      bool nxt_ok = false;
+      {
+        const int nf = nb * BN + half * kHalf * 32;
+        if (tma_aux && nf < p.N && lane == 0) {
+          mbar_expect_tx(my_bar, 2048);
+          tma_load_2d(my_in, &mapR, my_bar, nf, trow0);
+        }
+        if (aux && row_ok && nf + 32 <= p.N) {
+          fetch_raw_bf16(p, m, nf, b, nxt);
+          nxt_ok = true;
+        }
+      }
 #pragma unroll 1
       for (int cc = 0; cc < kHalf; ++cc) {
         const int c = half * kHalf + cc;
         const int n0 = nb * BN + c * 32;
+        uint4 cur[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+        bool cur_ok = nxt_ok;
+        nxt_ok = false;
+        if (tma_aux && n0 < p.N) {
+          // tile c landed: copy this lane's row (64B-swizzled) to registers,
+          // then reuse the buffer for tile c+1
+          mbar_wait(my_bar, in_phase);
+          in_phase ^= 1;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            cur[k] = *reinterpret_cast<const uint4*>(my_in + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4));
+          cur_ok = true;
+          __syncwarp();
+          if (lane == 0 && cc + 1 < kHalf && n0 + 32 < p.N) {
+            mbar_expect_tx(my_bar, 2048);
+            tma_load_2d(my_in, &mapR, my_bar, n0 + 32, trow0);
+          }
+        }
+        if (aux && row_ok && cc + 1 < kHalf && n0 + 64 <= p.N) {
+          fetch_raw_bf16(p, m, n0 + 32, b, nxt);
+          nxt_ok = true;
+        }
         uint32_t r[32];
         tmem_ld32(t_row + c * 32, r);
         if (n0 >= p.N) continue;  // warp-uniform
@@ -418,7 +512,7 @@ __global__ void __launch_bounds__(384, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const int trow = (int)((int64_t)b * p.M + mrow0 + q * 32);
+        const int trow = trow0;
 #define RP_EMIT()                                            \
   do {                                                       \
     if (p.tma_store)                                         \
@@ -435,30 +529,28 @@ __global__ void __launch_bounds__(384, 1)
             RP_EMIT();
             break;
           case RP_EPI_BIAS_RELU: {
-            if (p.bias && full) {
+            float bb[32];
+            load_bias(p, n0, full, bb);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = fmaxf(fmaf(v[j], p.alpha, p.bias[n0 + j]), 0.f);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                v[j] = fmaxf(v[j] * p.alpha + ((p.bias && n0 + j < p.N) ? p.bias[n0 + j] : 0.f), 0.f);
-            }
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(fmaf(v[j], p.alpha, bb[j]), 0.f);
             RP_EMIT();
             break;
           }
           case RP_EPI_BIAS_DROPOUT_RESIDUAL: {
-            float rr[32];
-            if (p.resid) {
+            float rr[32], bb[32];
+            if (cur_ok) {
+              unpack_raw_bf16(cur, rr);
+            } else if (p.resid) {
               load_chunk(p, m, n0, b, rr);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) rr[j] = 0.f;
             }
+            load_bias(p, n0, full, bb);
             const uint64_t pos_row = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int n = n0 + j;
-              float t = v[j] * p.alpha + ((p.bias && (full || n < p.N)) ? p.bias[n] : 0.f);
+              float t = fmaf(v[j], p.alpha, bb[j]);
               if (p.drop_on) t = dropout_keep(p.drop_seed, pos_row + j, p.drop_thr) ? t * p.drop_scale : 0.f;
               v[j] = t + rr[j];
             }
@@ -501,7 +593,10 @@ __global__ void __launch_bounds__(384, 1)
           case RP_EPI_RELU_GRAD: {
             // out = acc * (aux > 0), aux = the ReLU output h1 (layers.py:221)
             float rr[32];
-            load_chunk(p, m, n0, b, rr);
+            if (cur_ok)
+              unpack_raw_bf16(cur, rr);
+            else
+              load_chunk(p, m, n0, b, rr);
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = rr[j] > 0.f ? v[j] * p.alpha : 0.f;
             RP_EMIT();
@@ -755,8 +850,29 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
+  CUtensorMap mr;
+  std::memset(&mr, 0, sizeof(mr));
+  bool tma_resid = false;
+  {
+    auto enc = encoder();
+    const int64_t rows_r = a.M * batch;
+    const bool uses = a.residual && (a.epilogue == RP_EPI_RELU_GRAD || a.epilogue == RP_EPI_BIAS_DROPOUT_RESIDUAL);
+    const bool packed = batch == 1 || (a.stride_residual == a.M * a.ld_residual && a.M % Cfg::BM == 0);
+    if (enc && uses && a.out_dtype == RP_BF16 && ks == 1 && packed &&
+        (reinterpret_cast<uintptr_t>(a.residual) & 15) == 0 && (a.ld_residual * 2) % 16 == 0 && a.N >= 32 &&
+        rows_r < (1LL << 31) && !getenv("RP_NO_TMA_RESID")) {
+      cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)rows_r};
+      cuuint64_t strides[1] = {(cuuint64_t)(a.ld_residual * 2)};
+      cuuint32_t box[2] = {32, 32};
+      cuuint32_t estr[2] = {1, 1};
+      tma_resid = enc(&mr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.residual), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   GemmParams p{};
   p.tma_store = tma_store;
+  p.tma_resid = tma_resid;
   p.M = (int)a.M;
   p.N = (int)a.N;
   p.K = (int)a.K;
@@ -812,7 +928,7 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = kCta > 1 ? 2 : 1;
-  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_kernel<kTf32, BN, kCta>, ma, mal, mb, mbl, mc, p);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, gemm_kernel<kTf32, BN, kCta>, ma, mal, mb, mbl, mc, mr, p);
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) return set_error(RP_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(err));
   return RP_OK;

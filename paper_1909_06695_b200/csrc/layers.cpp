@@ -9,7 +9,10 @@
 // in tf32x3 mode every GEMM operand is split into (hi, lo) halves inside it.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
+#include <vector>
 
 #include "rp_internal.h"
 
@@ -188,6 +191,43 @@ int64_t split_bytes(int dtype, int64_t max_elems) {
     if (int _e = (x)) return _e;  \
   } while (0)
 
+// A second stream (per device, per host thread) onto which the block backward
+// forks the independent GEMM of each pair that shares an input; the fork and
+// join are event edges, so the pair overlaps (and CUDA-graph capture works).
+struct SideStream {
+  int device = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+SideStream& side_for(cudaStream_t main) {
+  // one side stream per (device, main stream): concurrent callers on
+  // different streams must not serialise on a shared side stream
+  static thread_local std::vector<std::pair<cudaStream_t, SideStream>> pool;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& e : pool)
+    if (e.first == main && e.second.device == dev) return e.second;
+  SideStream ss;
+  int prio = 0;
+  cudaStreamGetPriority(main, &prio);
+  cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, prio);
+  cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+  ss.device = dev;
+  pool.emplace_back(main, ss);
+  return pool.back().second;
+}
+
+bool fork_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RP_FORK");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -206,7 +246,7 @@ int64_t block_workspace_bytes(const rp_block_desc& d) {
   b += al256(N * 3 * d.d * e);                 // g_qkv
   b += al256(N * d.d * 4) * 3;                 // g_m, g_x1, g_a
   b += al256(nbp * std::max(d.f, 3 * d.d) * 4) * 3;  // partials
-  b += al256(kBlockSplitK);
+  b += al256(kBlockSplitK) * 2;  // main + side stream partials
   b += split_bytes(d.dtype, std::max({N * d.f, d.B * d.T * Tp, N * 3 * d.d, d.d * d.f}));
   return b + 4096;
 }
@@ -282,44 +322,77 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   c.max_ctas = d.max_ctas;
   c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
   c.splitk_cap = kBlockSplitK;
+  float* splitk_side = static_cast<float*>(bp.take(kBlockSplitK));
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
+  // side context for the second GEMM of each independent pair (bf16 only:
+  // the tf32x3 check mode shares one operand-split scratch, so it stays serial)
+  const bool fork = dt == RP_BF16 && fork_enabled();
+  SideStream* ss = fork ? &side_for(st) : nullptr;
+  Ctx cs = c;
+  Ctx cf = c;  // first GEMM of a forked pair
+  if (fork) {
+    cs.st = ss->s;
+    cs.splitk = splitk_side;
+    static int budget = -1;
+    if (budget < 0) {
+      const char* e = getenv("RP_FORK_CTAS");
+      budget = e ? atoi(e) : 0;
+    }
+    if (budget > 0) {
+      cs.max_ctas = budget;
+      cf.max_ctas = 148 - budget;
+    }
+  }
+  auto pair = [&](auto&& first, auto&& second) -> int {
+    if (!fork) {
+      RP_TRY(first(c));
+      return second(c);
+    }
+    if (cudaEventRecord(ss->fork, st) != cudaSuccess || cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "block_backward: fork failed");
+    RP_TRY(second(cs));
+    RP_TRY(first(cf));
+    if (cudaEventRecord(ss->join, ss->s) != cudaSuccess || cudaStreamWaitEvent(st, ss->join, 0) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "block_backward: join failed");
+    return RP_OK;
+  };
   const char* qkv = static_cast<const char*>(tp.qkv);
   const float inv = 1.f / std::sqrt(static_cast<float>(D));
   // feed-forward branch (layers.py:209-232)
   RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(N * D), d.drop_threshold, d.drop_scale,
                    d.drop_enabled, part, st));
   RP_TRY(colsum_finish(part, mask_grad_blocks(N, D), D, G.b2, st));
-  RP_TRY(mm(c, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32));
   Epi er;
   er.kind = RP_EPI_RELU_GRAD;
   er.resid = tp.h1;
   er.ld_resid = F;
-  RP_TRY(mm(c, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er); },
+              [&](Ctx& x) { return mm(x, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32); }));
   RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, st));
   RP_TRY(colsum_finish(part, nbc, F, G.b1, st));
-  RP_TRY(mm(c, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32));
-  RP_TRY(mm(c, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32); },
+              [&](Ctx& x) { return mm(x, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32); }));
   RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
                        d.drop_threshold, d.drop_scale, d.drop_enabled, pg, pb, N, D, st));
   RP_TRY(colsum_finish(pg, nbl, D, G.ln2_g, st));
   RP_TRY(colsum_finish(pb, nbl, D, G.ln2_b, st));
   // attention branch (layers.py:234-247)
-  RP_TRY(mm(c, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32));
-  RP_TRY(mm(c, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt); },
+              [&](Ctx& x) { return mm(x, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32); }));
   const Mat q = bmat(qkv, B, T, D, 3 * D, T * 3 * D);
   const Mat k = bmat(qkv + D * e, B, T, D, 3 * D, T * 3 * D);
   const Mat v = bmat(qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D);
   const Mat P = bmat(tp.probs, B, T, T, Tp, T * Tp);
   const Mat gctx = bmat(g_ctx, B, T, D, D, T * D);
-  RP_TRY(mm(c, gctx, false, v, false, bmat(g_p, B, T, T, Tp, T * Tp), RP_F32));
-  RP_TRY(mm(c, P, true, gctx, true, bmat(g_qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D), dt));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, gctx, false, v, false, bmat(g_p, B, T, T, Tp, T * Tp), RP_F32); },
+              [&](Ctx& x) { return mm(x, P, true, gctx, true, bmat(g_qkv + 2 * D * e, B, T, D, 3 * D, T * 3 * D), dt); }));
   RP_TRY(softmax_bwd(dt, g_p, tp.probs, g_s, inv, N, T, Tp, st));
   const Mat gs = bmat(g_s, B, T, T, Tp, T * Tp);
-  RP_TRY(mm(c, gs, false, k, true, bmat(g_qkv, B, T, D, 3 * D, T * 3 * D), dt));
-  RP_TRY(mm(c, gs, true, q, true, bmat(g_qkv + D * e, B, T, D, 3 * D, T * 3 * D), dt));
-  RP_TRY(mm(c, mat(tp.a, N, D, D), true, mat(g_qkv, N, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32));
-  RP_TRY(mm(c, mat(g_qkv, N, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, N, D, D), RP_F32));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, gs, false, k, true, bmat(g_qkv, B, T, D, 3 * D, T * 3 * D), dt); },
+              [&](Ctx& x) { return mm(x, gs, true, q, true, bmat(g_qkv + D * e, B, T, D, 3 * D, T * 3 * D), dt); }));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_qkv, N, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, N, D, D), RP_F32); },
+              [&](Ctx& x) { return mm(x, mat(tp.a, N, D, D), true, mat(g_qkv, N, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32); }));
   RP_TRY(layernorm_bwd(dt, g_a, x, tp.mean1, tp.rstd1, w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
   RP_TRY(colsum_finish(pg, nbl, D, G.ln1_g, st));
   RP_TRY(colsum_finish(pb, nbl, D, G.ln1_b, st));

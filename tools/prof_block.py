@@ -27,13 +27,38 @@ for _ in range(reps):
     LY.block_forward(W, W, x, out, tape, B, T, drop, ws, None)
     LY.block_backward(W, W, x, tape, g_out, g_x, G, B, T, drop, ws)
 torch.cuda.synchronize()
+import time  # noqa: E402
+
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
+h0 = time.perf_counter()
 for _ in range(10):
     LY.block_forward(W, W, x, out, tape, B, T, drop, ws, None)
     LY.block_backward(W, W, x, tape, g_out, g_x, G, B, T, drop, ws)
+host_ms = (time.perf_counter() - h0) * 1e3 / 10
 e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / 10
+print(f"host issue time per block fwd+bwd: {host_ms:.3f} ms")
+# GPU-only time: replay the same work as a CUDA graph
+gr = torch.cuda.CUDAGraph()
+st = torch.cuda.Stream()
+st.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(st):
+    LY.block_forward(W, W, x, out, tape, B, T, drop, ws, None)
+    LY.block_backward(W, W, x, tape, g_out, g_x, G, B, T, drop, ws)
+    with torch.cuda.graph(gr, stream=st):
+        LY.block_forward(W, W, x, out, tape, B, T, drop, ws, None)
+        LY.block_backward(W, W, x, tape, g_out, g_x, G, B, T, drop, ws)
+torch.cuda.synchronize()
+for _ in range(3):
+    gr.replay()
+torch.cuda.synchronize()
+s.record()
+for _ in range(10):
+    gr.replay()
+e.record()
+torch.cuda.synchronize()
+print(f"graph replay block fwd+bwd {s.elapsed_time(e) / 10:.3f} ms")
 fl = 3 * N * (2 * (4 * d * d + 2 * d * f) + 2 * 2 * d * T)  # fwd+bwd incl. full TxT attention
 print(f"block fwd+bwd {ms:.3f} ms -> {fl / ms / 1e9:.1f} TFLOP/s")
