@@ -352,6 +352,83 @@ def run_ours(args, c):
         dist.destroy_process_group()
 
 
+def run_pipeline(args, c):
+    """--mode ouroboros: the multi-GPU Ouroboros step, K = N + 1 modules on
+    the ring of N GPUs (modules 1 and K on GPU 0), P2P relay + boundary
+    exchange over NCCL.  One global batch flows through the pipeline per
+    step, so tokens/s = B*T / step time ("scaling": "strong")."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as M
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200.distributed import DistributedPipelineEngine, build_local_modules
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K = world + 1
+    B, T = c["batch"], c["seq"]
+    stack = M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], T, c["p"], 1, dtype="bf16")
+    part = M.partition(stack.num_layers, K)
+    mods = build_local_modules(stack, part, 3, rank)
+    eng = DistributedPipelineEngine(mods, part, rank, tied=stack.tied_store if rank == 0 else None,
+                                    device=stack.runtime.device)
+    opt = O.make_optimizer("adam", O.LrSchedule(2.5e-4, "fixed"))
+    rng = np.random.default_rng(1234)
+    batches = [(torch.from_numpy(zipf_tokens(rng, (B, T), c["vocab"])).cuda(),
+                torch.from_numpy(zipf_tokens(rng, (B, T), c["vocab"])).cuda()) for _ in range(4)]
+
+    class _B:
+        def __init__(self, x, y, sid):
+            self.x, self.y, self.sample_id, self.shape = x, y, sid, (B, T)
+
+    def step(t):
+        x, y = batches[t % 4]
+        return eng.step(t, _B(x if rank == 0 else None, y if rank == 0 else None, t), opt)
+
+    t = 0
+    for _ in range(max(3, args.warmup) + K):
+        step(t)
+        t += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        s_ev.record()
+        for _ in range(args.steps):
+            step(t)
+            t += 1
+        e_ev.record()
+        torch.cuda.synchronize()
+    ms = s_ev.elapsed_time(e_ev)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    stack.runtime.check("bench", list(mods.values()))
+    if rank == 0:
+        value = B * T * args.steps / (ms / 1e3)
+        pk, _ = peaks()
+        print(json.dumps({
+            "metric": "train tokens/s (Ouroboros step)", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (Zipf token ids, random-init weights)",
+            "config": {"workload": c["name"], "K_modules": K, "global_batch": B, "seq_len": T, "vocab": c["vocab"],
+                       "placement": "ring (modules 1 and K on GPU 0)", "parallelism": f"ouroboros K={K} over {world} GPUs"},
+            "model_flops_util": flops_per_token(c) * value / (world * pk.get("bf16_tflops_sustained", 1385.6) * 1e12),
+            "clocks": clocks.summary(),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,6 +437,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(CONFIGS))
     ap.add_argument("--engine", default="concurrent", choices=["concurrent", "reference"])
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "ouroboros"],
+                    help="N>1: independent K=2 replicas per GPU (default) or the multi-GPU Ouroboros pipeline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--compare-k1", action="store_true")
     args = ap.parse_args()
@@ -367,6 +446,8 @@ def main():
     c = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, c)
+    elif args.mode == "ouroboros":
+        run_pipeline(args, c)
     else:
         run_ours(args, c)
 

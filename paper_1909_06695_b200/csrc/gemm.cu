@@ -41,9 +41,13 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
+  // 192 KB of operand stages in flight per SM (measured: 5 stages of a CTA
+  // pair starve the long-K head GEMMs more than a second store tile helps)
+  static constexpr int PIPE_BYTES = 196608;
+  static constexpr int STAGES = (PIPE_BYTES / STAGE_BYTES) > 8 ? 8 : (PIPE_BYTES / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
-  static constexpr int STAGE_OUT = 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles (TMA store)
+  static constexpr int OUT_BUFS = 1;  // per-warp TMA-store tiles (2 costs a pipeline stage: measured slower)
+  static constexpr int STAGE_OUT = OUT_BUFS * 8 * 32 * 64;  // per-warp 32x32 bf16 staging tiles (TMA store)
   static constexpr int STAGE_IN = 8 * 32 * 64;   // per-warp 32x32 bf16 residual tiles (TMA load); LSE reuses it
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STAGE_OUT + STAGE_IN + 1024 + 256;
 };
@@ -198,9 +202,16 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // One warp's 32x32 bf16 chunk (lane = row) -> 64B-swizzled smem tile -> one
 // TMA bulk store.  The swizzle (16B chunk k of row r at k ^ ((r>>1)&3)) matches
 // CU_TENSOR_MAP_SWIZZLE_64B and keeps the st.shared at 4 wavefronts.
+template <int kBufs>
 __device__ __forceinline__ void emit_tma(const CUtensorMap& mapC, uint8_t* tile, const float (&v)[32], int lane,
                                          int col0, int row0) {
-  if (lane == 0) tma_store_wait_read();  // previous store of this warp finished reading smem
+  // the store that last used this tile (kBufs emits ago) finished reading smem
+  if (lane == 0) {
+    if constexpr (kBufs == 2)
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else
+      tma_store_wait_read();
+  }
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -421,7 +432,8 @@ __global__ void __launch_bounds__(384, 1)
     const int half = (warp - 4) >> 2;
     constexpr int kHalf = BN / 64;  // 32-column chunks per half
     float* red = reinterpret_cast<float*>(stage_in);       // [2 halves][2][128] (LSE only; no residual there)
-    uint8_t* my_out = stage_out + (warp - 4) * 2048;        // 32 rows x 64 B, 64B-swizzled
+    uint8_t* my_out_base = stage_out + (warp - 4) * 2048 * Cfg::OUT_BUFS;  // 32 rows x 64 B, 64B-swizzled
+    int out_buf = 0;
     uint8_t* my_in = stage_in + (warp - 4) * 2048;          // residual / aux tile, same layout
     uint64_t* my_bar = &in_bar[warp - 4];
     uint32_t in_phase = 0;
@@ -504,7 +516,9 @@ __global__ void __launch_bounds__(384, 1)
             float z[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) z[j] = 0.f;
-            emit_tma(mapC, my_out, z, lane, n0, (int)((int64_t)b * p.M + mrow0 + q * 32));
+            emit_tma<Cfg::OUT_BUFS>(mapC, my_out_base + out_buf * 2048, z, lane, n0,
+                                    (int)((int64_t)b * p.M + mrow0 + q * 32));
+            out_buf ^= (Cfg::OUT_BUFS - 1);
           }
           continue;
         }
@@ -513,12 +527,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         const int trow = trow0;
-#define RP_EMIT()                                            \
-  do {                                                       \
-    if (p.tma_store)                                         \
-      emit_tma(mapC, my_out, v, lane, n0, trow);             \
-    else                                                     \
-      store_chunk(p, m, n0, b, v);                           \
+#define RP_EMIT()                                                                   \
+  do {                                                                              \
+    if (p.tma_store) {                                                              \
+      emit_tma<Cfg::OUT_BUFS>(mapC, my_out_base + out_buf * 2048, v, lane, n0, trow); \
+      out_buf ^= (Cfg::OUT_BUFS - 1);                                               \
+    } else {                                                                        \
+      store_chunk(p, m, n0, b, v);                                                  \
+    }                                                                               \
   } while (0)
         switch (p.epi) {
           case RP_EPI_STORE:
@@ -558,31 +574,28 @@ __global__ void __launch_bounds__(384, 1)
             break;
           }
           case RP_EPI_LSE_PARTIAL: {
-            float cmax = -INFINITY;
+            float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
             if (full) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
+              for (int j = 0; j < 32; ++j) cm[j & 3] = fmaxf(cm[j & 3], v[j]);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (n0 + j < p.N) cmax = fmaxf(cmax, v[j]);
+                if (n0 + j < p.N) cm[j & 3] = fmaxf(cm[j & 3], v[j]);
             }
-            const float nmax = fmaxf(run_max, cmax);
+            const float nmax = fmaxf(run_max, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
             const float nm2 = nmax * kLog2e;
-            float s0 = run_sum * fast_exp2(run_max * kLog2e - nm2), s1 = 0.f;
+            float s[4] = {run_sum * fast_exp2(run_max * kLog2e - nm2), 0.f, 0.f, 0.f};
             if (full) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 2) {
-                s0 += fast_exp2(fmaf(v[j], kLog2e, -nm2));
-                s1 += fast_exp2(fmaf(v[j + 1], kLog2e, -nm2));
-              }
+              for (int j = 0; j < 32; ++j) s[j & 3] += fast_exp2(fmaf(v[j], kLog2e, -nm2));
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (n0 + j < p.N) s0 += fast_exp2(fmaf(v[j], kLog2e, -nm2));
+                if (n0 + j < p.N) s[j & 3] += fast_exp2(fmaf(v[j], kLog2e, -nm2));
             }
             run_max = nmax;
-            run_sum = s0 + s1;
+            run_sum = (s[0] + s[1]) + (s[2] + s[3]);
             if ((uint64_t)(tgt - n0) < 32ull) {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
