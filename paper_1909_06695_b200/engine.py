@@ -420,10 +420,9 @@ class ConcurrentPipelineEngine(PipelineEngine):
         self._advance_clock(t, results, relay_end)
         if optimizer is not None:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
-        done = torch.cuda.Event()
-        done.record(main)
-        for s in self._fs + self._bs:
-            s.wait_event(done)
+        # the next step's side streams order themselves after this step's
+        # optimizer through start_ev / zero_ev (recorded on the main stream),
+        # so no trailing fork is left open (CUDA-graph capture needs joins)
         self.last_loss_device = loss_dev
         if sync:
             try:
