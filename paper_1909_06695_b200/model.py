@@ -342,6 +342,64 @@ def partition(L, K, balance="even", costs=None):
     return ModulePartition(K, groups, device_of)
 
 
+def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
+    """Device seconds of one forward + backward per layer, for the by_cost
+    partition (reference model.py:144-159 times the same thing with the wall
+    clock).  Each layer runs on scratch activations at the batch's shape,
+    after one untimed warm-up, bracketed by CUDA events on the current stream.
+    The stack's gradient buffers are used as scratch (the engines overwrite
+    them every step); weights and snapshot rings are untouched."""
+    rt = stack.runtime
+    dev = rt.device
+    tokens = torch.as_tensor(batch_x).to(device=dev, dtype=torch.int64)
+    B, T = tokens.shape
+    Nt = B * T
+    tied = stack.tied_store
+    d, cdt = tied.d, stack.cdtype
+    ws = LY.Workspace(dev)
+    act = torch.empty(Nt, d, dtype=cdt, device=dev)
+    out = torch.empty_like(act)
+    g_out = torch.ones(Nt, d, dtype=torch.float32, device=dev)
+    g_in = torch.empty_like(g_out)
+    targets = torch.zeros(Nt, dtype=torch.int64, device=dev)
+    tape = head = None
+    costs = []
+    for idx, (layer, st) in enumerate(zip(stack.layers, stack.storage)):
+        mat = torch.empty(st.n_mat, dtype=cdt, device=dev)
+        if st.n_mat:
+            ops.cast(st.master[st.n_vec:], mat)
+        W = st._carve(None, None, None, st.master[: st.n_vec], mat)
+        drop = LY.Dropout.make(mix64(dropout_seed, 0, idx), getattr(layer, "dropout_p", 0.0), True)
+        if layer.kind == "embedding":
+            def run():
+                LY.embed_forward(tied.compute, W["pos"], tokens, act, tied.vocab, drop, rt.flag)
+                LY.embed_backward(g_out, tokens, layer.max_seq_len, st.G["pos"], tied.grad, 1.0, ws, drop)
+        elif layer.kind == "block":
+            if tape is None:
+                tape = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev)
+
+            def run():
+                LY.block_forward(W, W, act, out, tape, B, T, drop, ws, rt.flag)
+                LY.block_backward(W, W, act, tape, g_out, g_in, st.G, B, T, drop, ws)
+        else:
+            if head is None:
+                head = LY.HeadState(Nt, dev)
+
+            def run():
+                LY.head_forward(act, tied.compute, targets, tied.vocab, head, ws, rt.flag)
+                LY.head_backward(act, tied.compute, targets, tied.vocab, head, g_in, tied.grad, 1.0, ws)
+        run()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(repeats):
+            run()
+        end.record()
+        end.synchronize()
+        costs.append(start.elapsed_time(end) / 1e3 / repeats)
+    rt.flag.zero_()
+    return costs
+
+
 # ---------------------------------------------------------------------------
 # modules
 
@@ -479,7 +537,11 @@ class ModuleState:
             return self._shape
         raise DimensionError("pass module inputs as [B, T, d] to fix the batch shape")
 
-    def _run_forward(self, wstep, arena, seeds, train, out, ws):
+    def _run_forward(self, wstep, arena, seeds, train, out, ws, tied_c=None, from_act0=False):
+        """Forward of the slice at ring weights `wstep`.  `tied_c` overrides
+        the embedding table (a snapshot of V); `from_act0` starts at the first
+        block from an embedding output already in arena.acts[0] (checkpoint
+        re-derivation: V is not kept in the snapshot ring)."""
         B, T = arena.B, arena.T
         flag = self.flag
         nxt = 0  # next act buffer to fill
@@ -489,9 +551,15 @@ class ModuleState:
             p = layer.dropout_p if hasattr(layer, "dropout_p") else 0.0
             drop = LY.Dropout.make(seeds[off], p, train)
             if layer.kind == "embedding":
+                if from_act0:
+                    cur, nxt = arena.acts[0], 1
+                    continue
                 dst = arena.acts[0] if arena.acts else out
+                if dst is None:  # re-derivation of an embedding-only slot
+                    dst = self.ws_fwd.get("module_out", (B * T, self.d), self.cdtype)
                 Wv = st.weights(wstep)
-                LY.embed_forward(self.tied.compute, Wv["pos"], arena.tokens, dst, self.vocab, drop, flag)
+                LY.embed_forward(self.tied.compute if tied_c is None else tied_c, Wv["pos"], arena.tokens, dst,
+                                 self.vocab, drop, flag)
                 cur = dst
                 nxt = 1
             elif layer.kind == "block":

@@ -101,6 +101,7 @@ class AdamOptimizer(_Base):
         self.schedule = schedule
         self.beta1, self.beta2, self.eps = beta1, beta2, eps
         self._mods = []
+        self._pending = None
 
     @staticmethod
     def _moments(obj):
@@ -114,7 +115,8 @@ class AdamOptimizer(_Base):
         c1 = 1.0 - self.beta1 ** (t + 1)
         c2 = 1.0 - self.beta2 ** (t + 1)
         flag = _flag_of(modules)
-        self._mods = modules
+        if list(modules) != self._mods:
+            self.bind(modules)
 
         def fn(st, lo, hi, dst):
             if hi > lo:
@@ -131,25 +133,62 @@ class AdamOptimizer(_Base):
                           self.eps, c1, c2, flag)
         return lr
 
-    def state_arrays(self):
-        """Moments keyed like the reference (optim.py:128-135)."""
-        out = {}
+    def bind(self, modules):
+        """Attach the modules whose moments `state_arrays` /
+        `load_state_arrays` address (`apply` binds them too)."""
+        self._mods = list(modules)
+        pending, self._pending = getattr(self, "_pending", None), None
+        if pending:
+            self.load_state_arrays(pending)
+        return self
+
+    def _moment_views(self):
+        """(key, m view, v view) for every live parameter: views into the
+        flat moment buffers with the parameter's own strides (wq/wk/wv are
+        column blocks of the fused wqkv)."""
+        out = []
         for m in self._mods:
             start = m.layer_range[0]
             for off, st in enumerate(m.storage):
-                if st.m is None:
+                if st.master.numel() == 0:
                     continue
+                mb, vb = self._moments(st)
                 for name, view in st.params.items():
-                    rel = view.data_ptr() - st.master.data_ptr()
-                    sl = lambda buf: buf.view(-1)[rel // 4: rel // 4 + view.numel()]  # noqa: E731
-                    out[f"adam.m.L{start + off}.{name}"] = sl(st.m)
-                    out[f"adam.v.L{start + off}.{name}"] = sl(st.v)
-        if self._mods:
-            store = _tied_store(self._mods)
-            if store is not None and store.m is not None:
-                out["adam.m.tied"] = store.m
-                out["adam.v.tied"] = store.v
+                    args = (view.size(), view.stride(), view.storage_offset())
+                    out.append((f"L{start + off}.{name}", mb.as_strided(*args), vb.as_strided(*args)))
+        store = _tied_store(self._mods)
+        if store is not None:
+            mb, vb = self._moments(store)
+            out.append(("tied", mb, vb))
         return out
+
+    def state_arrays(self):
+        """Moments keyed `adam.m.{key}` / `adam.v.{key}` like the reference
+        (optim.py:128-135); device views, not copies."""
+        out = {}
+        for key, mv, vv in self._moment_views():
+            out[f"adam.m.{key}"] = mv
+            out[f"adam.v.{key}"] = vv
+        return out
+
+    def load_state_arrays(self, arrays):
+        """Inverse of `state_arrays` (optim.py:137-146).  Keys the checkpoint
+        lacks restart from zero moments, as the reference's lazily created
+        entries do.  Before the modules are bound the arrays are held until
+        `bind` / the next `apply`."""
+        for name in arrays:
+            if not name.startswith(("adam.m.", "adam.v.")):
+                raise ValueError(f"unexpected optimizer state entry {name!r}")
+        if not self._mods:
+            self._pending = dict(arrays)
+            return
+        for key, mv, vv in self._moment_views():
+            for prefix, dst in (("adam.m.", mv), ("adam.v.", vv)):
+                src = arrays.get(prefix + key)
+                if src is None:
+                    dst.zero_()
+                else:
+                    dst.copy_(torch.as_tensor(src).reshape(dst.shape))
 
 
 def _flag_of(modules):
