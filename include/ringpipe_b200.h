@@ -140,6 +140,34 @@ int rp_softmax_causal(int32_t dtype, const float* scores, void* probs, int64_t r
 int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, void* grad_scores, float scale,
                    int64_t rows, int64_t T, int64_t ld, void* stream);
 
+/* ---- Transformer-XL attention glue (oracle/xl.py) --------
+ * No reference interface exists (the reference has no XL path): these are the
+ * HBM-bound pieces around the tcgen05 GEMMs of relative-position multi-head
+ * attention with segment memory.  xa rows: B*M memory rows, then B*T current
+ * rows; head-major layouts qu/qv [H,B,T,dh], kh/vh [H,B,M+T,dh]. */
+int rp_xl_split_qkv(int32_t dtype, const void* qkv, const float* r_w_bias, const float* r_r_bias, void* qu, void* qv,
+                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream);
+/* dst[h, r, c] = src[r*ld + h*dh + c] */
+int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t dst_dtype, void* dst, int64_t rows,
+                      int32_t H, int32_t dh, void* stream);
+/* dst[r*ld + h*dh + c] = src[h, r, c] */
+int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
+                      int32_t H, int32_t dh, void* stream);
+/* g_qkv (xa row layout, [B*(M+T), 3d]) from fp32 head-major dQu, dQv, dK, dV */
+int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
+                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream);
+/* P = softmax((AC + relshift(BD)) * scale) over keys M-mem_len <= j <= M+i; rows = H*B*T */
+int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
+                      int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream);
+/* dAC = P (dP - <dP,P>) * scale; dBD = the same values un-shifted */
+int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
+                      void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,
+                      void* stream);
+/* per-head column sums of dQu / dQv [H, R, dh] -> d r_w_bias, d r_r_bias [H, dh] (deterministic) */
+int64_t rp_xl_bias_grad_workspace_bytes(int32_t H, int32_t dh);
+int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
+                    int32_t H, int64_t R, int32_t dh, void* stream);
+
 /* ---- embedding (layers.py:114-136) ---------------------------------------- */
 int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
                  int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,

@@ -207,7 +207,7 @@ class OuroborosOracle:
 
     def step(self, t, x, y):
         K = self.K
-        G, dVi, dVo, loss = full_grads(self.V, self.layers, x, y, self.dropout_seed, t, self.p, self.train)
+        G, dVi, dVo, loss = self._full_grads(t, x, y)
         self.pending[t] = (G, dVi)
         module_grads, sample_ids = [], []
         for k in range(1, K + 1):
@@ -239,6 +239,10 @@ class OuroborosOracle:
                     grads[key] = g
             self.opt.update(t, params, grads)
         return loss, packet
+
+    def _full_grads(self, t, x, y):
+        """K=1 backprop of sample t at the current weights w^t."""
+        return full_grads(self.V, self.layers, x, y, self.dropout_seed, t, self.p, self.train)
 
     def _param(self, key):
         idx, name = key.split(".", 1)

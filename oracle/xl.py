@@ -28,6 +28,7 @@ import math
 import numpy as np
 
 from . import layers as L
+from .ouroboros import OuroborosOracle
 from .rng import Stream, hash64
 
 XL_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "wr", "r_w_bias", "r_r_bias", "ln2_g", "ln2_b", "w1", "b1",
@@ -223,3 +224,24 @@ def xl_forward_loss(V, layers, x, y, dropout_seed, step, p, mems, mem_len, H, tr
     for i in range(1, nl - 1):
         h, _ = xl_block_fwd(layers[i], h, mems[i - 1], mem_len, H, hash64(dropout_seed, step, i), p, train)
     return L.head_loss(h, V, y)
+
+
+class XLOuroborosOracle(OuroborosOracle):
+    """The Ouroboros schedule over the XL model (fp64).  Memory is data, not a
+    parameter: the forward of segment t runs at the live weights w^t in both
+    the pipeline and plain backprop, so module k's stale gradient of sample s
+    is the K=1 gradient of segment s given the memory segment s-1 left --
+    exactly what `xl_full_grads` computes at step s."""
+
+    def __init__(self, V, layers, K, dropout_seed, p, H, mem_len, batch, optimizer=None, **kw):
+        super().__init__(V, layers, K, dropout_seed, p, optimizer, **kw)
+        self.H, self.M = H, mem_len
+        d = V.shape[1]
+        self.mems = [np.zeros((batch, mem_len, d)) for _ in range(len(layers) - 2)]
+        self.mem_valid = 0
+
+    def _full_grads(self, t, x, y):
+        G, dVi, dVo, loss, self.mems = xl_full_grads(self.V, self.layers, x, y, self.dropout_seed, t, self.p,
+                                                     self.mems, self.mem_valid, self.H, self.train)
+        self.mem_valid = self.M
+        return G, dVi, dVo, loss

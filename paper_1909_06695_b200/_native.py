@@ -130,6 +130,14 @@ def _declare(L):
         "rp_init_uniform": [vp, i64, u64, u64, f64, vp],
         "rp_cast": [vp, i32, vp, i32, i64, vp],
         "rp_sq_norm": [vp, i64, vp, vp, i32, vp],
+        "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
+        "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, vp],
+        "rp_xl_merge_heads": [i32, vp, i32, vp, i64, i64, i32, i32, vp],
+        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
+        "rp_xl_softmax_fwd": [i32, vp, vp, i64, vp, i64, i64, i64, i64, i64, f32, vp],
+        "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
+        "rp_xl_bias_grad_workspace_bytes": [i32, i32],
+        "rp_xl_bias_grad": [vp, vp, vp, vp, vp, i32, i64, i32, vp],
         "rp_block_workspace_bytes": [ctypes.POINTER(BlockDesc)],
         "rp_block_forward": [ctypes.POINTER(BlockDesc), ctypes.POINTER(BlockWeights), vp, vp,
                              ctypes.POINTER(BlockTape), vp, i64, vp, vp],
@@ -145,6 +153,7 @@ def _declare(L):
         fn.argtypes = args
         fn.restype = ctypes.c_int32
     L.rp_embed_bwd_workspace_bytes.restype = i64
+    L.rp_xl_bias_grad_workspace_bytes.restype = i64
     L.rp_block_workspace_bytes.restype = i64
     L.rp_head_workspace_bytes.restype = i64
 

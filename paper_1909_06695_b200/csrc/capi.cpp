@@ -127,6 +127,38 @@ int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t acc
   return rp::sq_norm(x, n, part, out, accumulate, RP_S(stream));
 }
 
+int rp_xl_split_qkv(int32_t dtype, const void* qkv, const float* r_w_bias, const float* r_r_bias, void* qu, void* qv,
+                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream) {
+  return rp::xl_split_qkv(dtype, qkv, r_w_bias, r_r_bias, qu, qv, kh, vh, B, T, M, H, dh, RP_S(stream));
+}
+int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t dst_dtype, void* dst, int64_t rows,
+                      int32_t H, int32_t dh, void* stream) {
+  return rp::xl_split_heads(src_dtype, src, ld, dst_dtype, dst, rows, H, dh, RP_S(stream));
+}
+int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
+                      int32_t H, int32_t dh, void* stream) {
+  return rp::xl_merge_heads(src_dtype, src, dst_dtype, dst, ld, rows, H, dh, RP_S(stream));
+}
+int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
+                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream) {
+  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream));
+}
+int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
+                      int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream) {
+  return rp::xl_softmax_fwd(dtype, ac, bd, ld_scores, probs, ld_p, rows, T, M, mem_len, scale, RP_S(stream));
+}
+int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
+                      void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,
+                      void* stream) {
+  return rp::xl_softmax_bwd(dtype, grad_p, ld_scores, probs, ld_p, grad_ac, grad_bd, rows, T, M, mem_len, scale,
+                            RP_S(stream));
+}
+int64_t rp_xl_bias_grad_workspace_bytes(int32_t H, int32_t dh) { return rp::xl_bias_grad_workspace_bytes(H, dh); }
+int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
+                    int32_t H, int64_t R, int32_t dh, void* stream) {
+  return rp::xl_bias_grad(g_qu, g_qv, workspace, g_r_w_bias, g_r_r_bias, H, R, dh, RP_S(stream));
+}
+
 int64_t rp_block_workspace_bytes(const rp_block_desc* desc) { return rp::block_workspace_bytes(*desc); }
 int rp_block_forward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, void* out,
                      const rp_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,

@@ -50,6 +50,22 @@ int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double sca
 int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st);
 int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
 
+int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, void* qu, void* qv, void* kh, void* vh,
+                 int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st);
+int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, void* dst, int64_t rows, int H, int dh,
+                   cudaStream_t st);
+int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
+                   cudaStream_t st);
+int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st);
+int xl_softmax_fwd(int dtype, const float* ac, const float* bd, int64_t lds, void* p, int64_t ldp, int64_t rows,
+                   int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st);
+int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64_t ldp, void* gac, void* gbd,
+                   int64_t rows, int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st);
+int64_t xl_bias_grad_workspace_bytes(int H, int dh);
+int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
+                 cudaStream_t st);
+
 int64_t block_workspace_bytes(const rp_block_desc& d);
 int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void* x, void* out, const rp_block_tape& tp,
                   void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);

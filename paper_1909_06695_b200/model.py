@@ -30,6 +30,7 @@ from . import ops
 from .errors import DimensionError, PartitionError, ScheduleViolation
 from .rng import mix64
 from .runtime import Runtime
+from .xl import XLTape, sinusoid, xl_block_backward, xl_block_forward
 
 # ---------------------------------------------------------------------------
 # layer descriptors (the reference layer kinds, layers.py:96-280)
@@ -57,6 +58,31 @@ class TransformerBlockLayer:
         dims = {"d": d, "f": f, "3d": 3 * d}
         vec = [(n, (dims[s],)) for n, s in LY.BLOCK_VEC]
         mat = [(n, (dims[a], dims[b])) for n, (a, b) in LY.BLOCK_MAT]
+        return vec, mat
+
+
+class TransformerXLBlockLayer:
+    """Transformer-XL block: relative-position multi-head attention over
+    [segment memory; segment] in the reference's pre-LN block (xl.py,
+    oracle/xl.py).  `mem_len` <= the segment length."""
+
+    kind = "xl_block"
+    VEC = LY.BLOCK_VEC + (("r_w_bias", ("H", "dh")), ("r_r_bias", ("H", "dh")))
+    MAT = LY.BLOCK_MAT + (("wr", ("d", "d")),)
+    KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "wr", "r_w_bias", "r_r_bias", "ln2_g", "ln2_b", "w1", "b1",
+            "w2", "b2")
+
+    def __init__(self, model_dim, ffn_dim, dropout_p, n_heads, mem_len):
+        if model_dim % n_heads:
+            raise DimensionError("model_dim must be a multiple of n_heads")
+        self.model_dim, self.ffn_dim, self.dropout_p = model_dim, ffn_dim, dropout_p
+        self.n_heads, self.mem_len = n_heads, mem_len
+
+    def specs(self):
+        d, f, H = self.model_dim, self.ffn_dim, self.n_heads
+        dims = {"d": d, "f": f, "3d": 3 * d, "H": H, "dh": d // H}
+        vec = [(n, tuple(dims[x] for x in ((s,) if isinstance(s, str) else s))) for n, s in self.VEC]
+        mat = [(n, (dims[a], dims[b])) for n, (a, b) in self.MAT]
         return vec, mat
 
 
@@ -117,12 +143,13 @@ class LayerParams:
         return out
 
     def _public(self, D):
-        if self.layer.kind != "block":
+        if self.layer.kind not in ("block", "xl_block"):
             return dict(D)
         d = self.layer.model_dim
         w = D["wqkv"]
         views = {"wq": w[:, :d], "wk": w[:, d: 2 * d], "wv": w[:, 2 * d:]}
-        return {k: (views[k] if k in views else D[k]) for k in LY.BLOCK_KEYS}
+        keys = LY.BLOCK_KEYS if self.layer.kind == "block" else self.layer.KEYS
+        return {k: (views[k] if k in views else D[k]) for k in keys}
 
     # -- snapshot ring ----------------------------------------------------
     def configure_ring(self, capacity):
@@ -234,6 +261,27 @@ def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, in
     return LayerStack(layers, storage, tied, rt, cdt)
 
 
+def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, n_heads, mem_len, *,
+                   dtype="bf16", device=None):
+    """The Transformer-XL language model: the reference embedding and tied
+    head around `n_blocks` XL blocks with `mem_len` memory rows each."""
+    if model_dim % 8 or ffn_dim % 8 or (model_dim // n_heads) % 8:
+        raise DimensionError("model_dim, ffn_dim and the head dim must be multiples of 8 (TMA 16-byte rows)")
+    if not 0 <= mem_len <= seq_len:
+        raise DimensionError("mem_len must be in [0, seq_len]")
+    rt = Runtime.get(device)
+    cdt = _dtype_of(dtype)
+    layers = [EmbeddingLayer(vocab_size, model_dim, seq_len, dropout_p)]
+    layers += [TransformerXLBlockLayer(model_dim, ffn_dim, dropout_p, n_heads, mem_len) for _ in range(n_blocks)]
+    layers.append(OutputProjectionLayer(vocab_size, model_dim))
+    storage = [LayerParams(layer, rt.device, cdt) for layer in layers]
+    tied = TiedMatrix(vocab_size, model_dim, rt.device, cdt)
+    with torch.cuda.device(rt.device):
+        _init_params(layers, storage, tied, init_seed)
+        tied.refresh()
+    return LayerStack(layers, storage, tied, rt, cdt)
+
+
 def _init_params(layers, storage, tied, init_seed):
     seed = mix64(init_seed)
     pos = 0
@@ -259,6 +307,12 @@ def _init_params(layers, storage, tied, init_seed):
             P["ln1_g"].fill_(1.0)
             P["ln2_g"].fill_(1.0)
             for w in ("wq", "wk", "wv", "wo", "w1"):
+                draw(P[w], sd)
+            draw(P["w2"], 1.0 / math.sqrt(layer.ffn_dim))
+        elif layer.kind == "xl_block":  # oracle/xl.py init_xl_params order
+            P["ln1_g"].fill_(1.0)
+            P["ln2_g"].fill_(1.0)
+            for w in ("wq", "wk", "wv", "wo", "wr", "r_w_bias", "r_r_bias", "w1"):
                 draw(P[w], sd)
             draw(P["w2"], 1.0 / math.sqrt(layer.ffn_dim))
 
@@ -424,9 +478,19 @@ class _Arena:
         self.B, self.T = B, T
         self.tokens = torch.empty(B, T, dtype=torch.int64, device=dev) if module.has_embedding else None
         self.targets = torch.empty(Nt, dtype=torch.int64, device=dev) if module.has_projection else None
-        n_acts = module.n_blocks + (1 if module.has_projection else 0)
-        self.acts = [torch.empty(Nt, d, dtype=cdt, device=dev) for _ in range(n_acts)]
-        self.tapes = [LY.BlockTape(B, T, d, module.f, cdt, dev) for _ in range(module.n_blocks)]
+        self.tapes = []
+        self.acts = []
+        for off in module.block_idx:
+            layer = module.layers[off]
+            if layer.kind == "xl_block":
+                tp = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev)
+                self.acts.append(tp.x)  # the upstream writes straight into [memory; x]
+            else:
+                tp = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev)
+                self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
+            self.tapes.append(tp)
+        if module.has_projection:
+            self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
         self.head = LY.HeadState(Nt, dev) if module.has_projection else None
 
 
@@ -449,7 +513,12 @@ class ModuleState:
         self.peak_slots = 0
         self.has_embedding = layers[0].kind == "embedding"
         self.has_projection = layers[-1].kind == "projection"
-        self.block_idx = [i for i, l in enumerate(layers) if l.kind == "block"]
+        self.block_idx = [i for i, l in enumerate(layers) if l.kind in ("block", "xl_block")]
+        # Transformer-XL segment memory: per XL block the previous segment's
+        # layer input [B*M, d], and how many of its rows are valid
+        self.mem = {}
+        self.mem_len = 0
+        self._R = {}
         self.n_blocks = len(self.block_idx)
         ref = layers[self.block_idx[0]] if self.block_idx else layers[0]
         self.d = ref.model_dim
@@ -537,15 +606,41 @@ class ModuleState:
             return self._shape
         raise DimensionError("pass module inputs as [B, T, d] to fix the batch shape")
 
-    def _run_forward(self, wstep, arena, seeds, train, out, ws, tied_c=None, from_act0=False):
+    # -- Transformer-XL memory ----------------------------------------------
+    def _sinusoid(self, tp):
+        key = (tp.Kl, self.d, self.cdtype)
+        R = self._R.get(key)
+        if R is None:
+            R = self._R[key] = sinusoid(tp.Kl, self.d, self.cdtype, self.device)
+        return R
+
+    def _load_memory(self, off, tp):
+        """Memory rows of this segment = the previous segment's layer input."""
+        buf = self.mem.get(off)
+        if buf is None or buf.shape[0] != tp.B * tp.M:
+            buf = self.mem[off] = torch.zeros(tp.B * tp.M, self.d, dtype=self.cdtype, device=self.device)
+        tp.mem.copy_(buf)
+        tp.mem_len = self.mem_len
+
+    def _store_memory(self, off, tp):
+        if tp.M:
+            self.mem[off].view(tp.B, tp.M, self.d).copy_(tp.x.view(tp.B, tp.T, self.d)[:, tp.T - tp.M:])
+
+    def reset_memory(self):
+        self.mem_len = 0
+
+    def _run_forward(self, wstep, arena, seeds, train, out, ws, tied_c=None, from_act0=False, live=True):
         """Forward of the slice at ring weights `wstep`.  `tied_c` overrides
         the embedding table (a snapshot of V); `from_act0` starts at the first
         block from an embedding output already in arena.acts[0] (checkpoint
-        re-derivation: V is not kept in the snapshot ring)."""
+        re-derivation: V is not kept in the snapshot ring).  `live` marks the
+        step's own forward, which reads and advances the XL memory; replays
+        (stale_weights="current", re-derivation) reuse the slot's memory."""
         B, T = arena.B, arena.T
         flag = self.flag
         nxt = 0  # next act buffer to fill
         cur = None
+        xl_live = None
         for off, layer in enumerate(self.layers):
             st = self.storage[off]
             p = layer.dropout_p if hasattr(layer, "dropout_p") else 0.0
@@ -562,7 +657,7 @@ class ModuleState:
                                  self.vocab, drop, flag)
                 cur = dst
                 nxt = 1
-            elif layer.kind == "block":
+            elif layer.kind in ("block", "xl_block"):
                 j = self.block_idx.index(off)
                 x_in = arena.acts[j]
                 last_act = j + 1 >= len(arena.acts)
@@ -570,13 +665,24 @@ class ModuleState:
                 if dst is None:
                     dst = self.ws_fwd.get("module_out", (B * T, self.d), self.cdtype)
                 W = st.weights(wstep)
-                LY.block_forward(W, W, x_in, dst.view(B * T, self.d), arena.tapes[j], B, T, drop, ws, flag)
+                if layer.kind == "xl_block":
+                    tp = arena.tapes[j]
+                    if live:
+                        self._load_memory(off, tp)
+                    xl_block_forward(W, W, dst.view(B * T, self.d), tp, self._sinusoid(tp), drop, ws, flag)
+                    if live:
+                        self._store_memory(off, tp)
+                        xl_live = tp.M
+                else:
+                    LY.block_forward(W, W, x_in, dst.view(B * T, self.d), arena.tapes[j], B, T, drop, ws, flag)
                 cur = dst
                 nxt = j + 2
             else:  # projection + fused CE head
                 h = arena.acts[-1]
                 LY.head_forward(h, self.tied.compute, arena.targets, self.vocab, arena.head, ws, flag)
-                return arena.head.loss
+                cur = arena.head.loss
+        if xl_live is not None:
+            self.mem_len = xl_live  # M <= T: one segment fills the memory
         return cur
 
     # -- backward ----------------------------------------------------------
@@ -607,7 +713,7 @@ class ModuleState:
                 st.weights(wstep)  # raises ScheduleViolation when evicted
         elif stale_mode == "current":
             wstep = live_step if live_step is not None else self.last_forward_step
-            self._run_forward(wstep, arena, slot.layer_seeds, train, None, self.ws_bwd)
+            self._run_forward(wstep, arena, slot.layer_seeds, train, None, self.ws_bwd, live=False)
         else:
             raise ValueError(f"unknown stale_weights mode {stale_mode!r}")
         ws = self.ws_bwd
@@ -647,7 +753,11 @@ class ModuleState:
             else:
                 g_next = ws.get("g_stream_b" if ping == 0 else "g_stream_a", (Nt, d), torch.float32)
                 ping ^= 1
-            LY.block_backward(W, W, arena.acts[j], arena.tapes[j], g, g_next, st.G, B, T, drop, ws)
+            if self.layers[off].kind == "xl_block":
+                tp = arena.tapes[j]
+                xl_block_backward(W, W, tp, self._sinusoid(tp), g, g_next, st.G, drop, ws)
+            else:
+                LY.block_backward(W, W, arena.acts[j], arena.tapes[j], g, g_next, st.G, B, T, drop, ws)
             g = g_next
         if self.has_embedding:
             st = self.storage[0]

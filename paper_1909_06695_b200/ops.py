@@ -7,6 +7,7 @@ There is deliberately no CPU path: calling these on CPU tensors raises.
 """
 
 import ctypes
+import math
 
 import torch
 
@@ -287,6 +288,61 @@ def softmax_bwd(grad_probs, probs, grad_scores, scale):
     _count(1)
     N.check(N.lib().rp_softmax_bwd(_dtc(probs), _ptr(grad_probs), _ptr(probs), _ptr(grad_scores), scale, B * T, T,
                                    probs.stride(1), _stream()), "softmax_bwd")
+
+
+# ---------------------------------------------------------------------------
+# Transformer-XL attention glue (csrc/xl.cu)
+
+
+def xl_split_qkv(qkv, u, v, qu, qv, kh, vh, B, T, M, H, dh):
+    _require_cuda(qkv, u, v, qu, qv, kh, vh)
+    _count(1)
+    N.check(N.lib().rp_xl_split_qkv(_dtc(qkv), _ptr(qkv), _ptr(u), _ptr(v), _ptr(qu), _ptr(qv), _ptr(kh), _ptr(vh),
+                                    B, T, M, H, dh, _stream()), "xl_split_qkv")
+
+
+def xl_split_heads(src, dst, H, dh):
+    """src [rows, >= H*dh] (row stride src.stride(0)) -> dst [H, rows, dh]."""
+    rows = src.shape[0]
+    _count(1)
+    N.check(N.lib().rp_xl_split_heads(_dtc(src), _ptr(src), src.stride(0), _dtc(dst), _ptr(dst), rows, H, dh,
+                                      _stream()), "xl_split_heads")
+
+
+def xl_merge_heads(src, dst, H, dh):
+    """src [H, rows, dh] -> dst [rows, H*dh] (row stride dst.stride(0))."""
+    rows = dst.shape[0]
+    _count(1)
+    N.check(N.lib().rp_xl_merge_heads(_dtc(src), _ptr(src), _dtc(dst), _ptr(dst), dst.stride(0), rows, H, dh,
+                                      _stream()), "xl_merge_heads")
+
+
+def xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh):
+    _count(1)
+    N.check(N.lib().rp_xl_merge_grads(_dtc(g_qkv), _ptr(g_qu), _ptr(g_qv), _ptr(g_kh), _ptr(g_vh), _ptr(g_qkv), B, T,
+                                      M, H, dh, _stream()), "xl_merge_grads")
+
+
+def xl_softmax_fwd(ac, bd, probs, T, M, mem_len, scale):
+    """ac, bd fp32 [rows, lds]; probs [rows, ldp]; rows = H*B*T."""
+    _count(1)
+    rows = math.prod(probs.shape[:-1])
+    N.check(N.lib().rp_xl_softmax_fwd(_dtc(probs), _ptr(ac), _ptr(bd), ac.stride(-2), _ptr(probs), probs.stride(-2),
+                                      rows, T, M, mem_len, scale, _stream()), "xl_softmax_fwd")
+
+
+def xl_softmax_bwd(g_p, probs, g_ac, g_bd, T, M, mem_len, scale):
+    _count(1)
+    rows = math.prod(probs.shape[:-1])
+    N.check(N.lib().rp_xl_softmax_bwd(_dtc(probs), _ptr(g_p), g_p.stride(-2), _ptr(probs), probs.stride(-2),
+                                      _ptr(g_ac), _ptr(g_bd), rows, T, M, mem_len, scale, _stream()),
+            "xl_softmax_bwd")
+
+
+def xl_bias_grad(g_qu, g_qv, work, g_u, g_v, H, rows, dh):
+    _count(2)
+    N.check(N.lib().rp_xl_bias_grad(_ptr(g_qu), _ptr(g_qv), _ptr(work), _ptr(g_u), _ptr(g_v), H, rows, dh,
+                                    _stream()), "xl_bias_grad")
 
 
 def embed_fwd(tokens, tied, pos, out, vocab, dropout=None, flag=None):

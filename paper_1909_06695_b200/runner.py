@@ -263,7 +263,7 @@ def load_training_state(path, runtime):
                                                                                     stack.cdtype)
                     else:
                         raise ckpt.CheckpointError(f"slot {j} of module {m.index} lacks V for step {step}")
-                m._run_forward(step, arena, seeds, engine.train, None, m.ws_fwd, **kw)
+                m._run_forward(step, arena, seeds, engine.train, None, m.ws_fwd, live=False, **kw)
                 j += 1
             m.last_forward_step = next_step - 1
         engine.import_boundary({int(n.split(".")[1]): arrays.pop(n) for n in list(arrays)

@@ -1,0 +1,184 @@
+"""Transformer-XL block on the device.
+
+Relative-position multi-head attention with segment-level memory (Dai et al.
+2019; fp64 restatement and its tests: oracle/xl.py) inside the reference's
+pre-LN block (reference layers.py:168-253: LayerNorm, dropout positions, ReLU
+FFN and residuals are unchanged).  There is no reference implementation, so
+parity is pinned through the restatement.
+
+Per slot the block keeps `xa` = [memory rows; current rows] (B*M + B*T rows
+of d): the memory part is the previous segment's layer input (stop-gradient),
+the current part is this segment's layer input, written in place by the
+upstream layer or module.  Every contraction is a tcgen05 GEMM over
+head-major operands; csrc/xl.cu does the head splits, the relative-shift
+softmax and the gradient merges.
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import ops
+from .layers import _pad8
+
+
+def sinusoid(Kl, d, dtype, device):
+    """R [Kl, d]: row p encodes distance Kl-1-p as [sin, cos] (XL's
+    PositionalEmbedding over the descending pos_seq), evaluated in fp64."""
+    dist = np.arange(Kl - 1, -1, -1, dtype=np.float64)
+    inv = 1.0 / (10000.0 ** (np.arange(0, d, 2, dtype=np.float64) / d))
+    ang = dist[:, None] * inv[None, :]
+    R = np.concatenate([np.sin(ang), np.cos(ang)], axis=1)
+    return torch.from_numpy(R).to(device=device, dtype=dtype)
+
+
+class XLTape:
+    """Store-all intermediates of one XL block for one stale slot."""
+
+    def __init__(self, B, T, M, d, f, H, dtype, device):
+        Kl = M + T
+        dh = d // H
+        ldk = _pad8(Kl)
+        e = lambda *s: torch.empty(s, dtype=dtype, device=device)  # noqa: E731
+        f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
+        self.B, self.T, self.M, self.H, self.dh, self.Kl, self.ldk = B, T, M, H, dh, Kl, ldk
+        self.xa = e(B * Kl, d)            # [memory rows; current rows]
+        self.a = e(B * Kl, d)
+        self.mean1, self.rstd1 = f32(B * Kl), f32(B * Kl)
+        self.qkv = e(B * Kl, 3 * d)
+        self.qu, self.qv = e(H, B * T, dh), e(H, B * T, dh)
+        self.kh, self.vh = e(H, B * Kl, dh), e(H, B * Kl, dh)
+        self.rh = e(H, Kl, dh)
+        self.probs_buf = e(H * B, T, ldk)
+        self.probs = self.probs_buf[:, :, :Kl]
+        self.ctx = e(B * T, d)
+        self.x1 = e(B * T, d)
+        self.m = e(B * T, d)
+        self.h1 = e(B * T, f)
+        self.mean2, self.rstd2 = f32(B * T), f32(B * T)
+        self.mem_len = 0
+
+    @property
+    def x(self):
+        """This segment's layer input (the upstream writes it here)."""
+        return self.xa[self.B * self.M:]
+
+    @property
+    def mem(self):
+        return self.xa[: self.B * self.M]
+
+    def nbytes(self):
+        return sum(t.numel() * t.element_size() for t in vars(self).values() if torch.is_tensor(t))
+
+
+def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
+    """tp.xa holds [memory; x]; writes out [B*T, d] and the tape."""
+    B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
+    d = H * dh
+    n = B * T * d
+    cdt = tp.xa.dtype
+    ops.layernorm_fwd(tp.xa, vecs["ln1_g"], vecs["ln1_b"], tp.a, tp.mean1, tp.rstd1, flag)
+    ops.gemm(tp.a, W["wqkv"], b_mn=True, out=tp.qkv)
+    ops.xl_split_qkv(tp.qkv, vecs["r_w_bias"], vecs["r_r_bias"], tp.qu, tp.qv, tp.kh, tp.vh, B, T, M, H, dh)
+    r = ws.get("xl_r", (Kl, d), cdt)
+    ops.gemm(R, W["wr"], b_mn=True, out=r)
+    ops.xl_split_heads(r, tp.rh, H, dh)
+    ac = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
+    bd = ws.get("xl_bd", (H, B * T, tp.ldk), torch.float32)[:, :, :Kl]
+    with ops.span("xl_scores"):
+        ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac)
+        ops.gemm(tp.qv, tp.rh, out=bd)
+    ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
+    ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
+    ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
+    ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
+    d0 = None if drop is None else (drop[0], drop[1], drop[2], 0)
+    ops.gemm(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0)
+    ops.layernorm_fwd(tp.x1, vecs["ln2_g"], vecs["ln2_b"], tp.m, tp.mean2, tp.rstd2, flag)
+    ops.gemm(tp.m, W["w1"], b_mn=True, out=tp.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+    d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
+    ops.gemm(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
+             residual=tp.x1, dropout=d1)
+
+
+def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
+    """g_out, g_x: [B*T, d] fp32.  No gradient flows into the memory rows;
+    their LayerNorm / K / V contributions to the weight gradients do."""
+    B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
+    d = H * dh
+    f = tp.h1.shape[-1]
+    Nt = B * T
+    n = Nt * d
+    cdt = tp.xa.dtype
+    scale = 1.0 / math.sqrt(dh)
+    # feed-forward + LN2 (as the reference block)
+    nbc = ops.colsum_blocks(Nt)
+    nbm = ops.mask_grad_blocks(Nt, d)
+    part = ws.get("colsum_part", (max(nbc, nbm), max(f, 3 * d)), torch.float32)
+    g_h2 = ws.get("g_h2", (Nt, d), cdt)
+    pm = ws.get("mask_part", (nbm, d), torch.float32)
+    ops.mask_grad(g_out, g_h2, n, drop, pm)
+    ops.colsum_finish(pm, nbm, G["b2"])
+    ops.gemm(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
+    g_z1 = ws.get("g_z1", (Nt, f), cdt)
+    ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tp.h1)
+    ops.colsum_partial(g_z1, part[:, :f])
+    ops.colsum_finish(part[:, :f], nbc, G["b1"])
+    ops.gemm(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
+    g_m = ws.get("g_m", (Nt, d), torch.float32)
+    ops.gemm(g_z1, W["w1"], out=g_m)
+    nbl_cur = ops.layernorm_bwd_blocks(Nt)
+    nbl_mem = ops.layernorm_bwd_blocks(B * M) if M else 0
+    pg = ws.get("ln_pg", (nbl_cur + nbl_mem, d), torch.float32)
+    pb = ws.get("ln_pb", (nbl_cur + nbl_mem, d), torch.float32)
+    g_x1 = ws.get("g_x1", (Nt, d), torch.float32)
+    g_proj = ws.get("g_proj", (Nt, d), cdt)
+    ops.layernorm_bwd(g_m, tp.x1, tp.mean2, tp.rstd2, vecs["ln2_g"], g_x1, pg[:nbl_cur], pb[:nbl_cur],
+                      resid_grad=g_out, dx_masked=g_proj, dropout=drop)
+    ops.colsum_finish(pg, nbl_cur, G["ln2_g"])
+    ops.colsum_finish(pb, nbl_cur, G["ln2_b"])
+    # relative-position attention
+    ops.gemm(tp.ctx, g_proj, a_mn=True, b_mn=True, out=G["wo"])
+    g_ctx = ws.get("g_ctx", (Nt, d), cdt)
+    ops.gemm(g_proj, W["wo"], out=g_ctx)
+    g_ctx_h = ws.get("xl_g_ctx_h", (H, Nt, dh), cdt)
+    ops.xl_split_heads(g_ctx, g_ctx_h, H, dh)
+    g3 = g_ctx_h.view(H * B, T, dh)
+    g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
+    ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p)
+    g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
+    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
+    g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
+    g_bd = ws.get("xl_g_bd", (H, Nt, tp.ldk), cdt)
+    ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
+    g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
+    g_qu = ws.get("xl_g_qu", (H, Nt, dh), torch.float32)
+    g_kh = ws.get("xl_g_kh", (H * B, Kl, dh), torch.float32)
+    g_qv = ws.get("xl_g_qv", (H, Nt, dh), torch.float32)
+    g_rh = ws.get("xl_g_rh", (H, Kl, dh), torch.float32)
+    ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
+    ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh)
+    ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
+    ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
+    work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
+    ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
+    g_r = ws.get("xl_g_r", (Kl, d), cdt)
+    ops.xl_merge_heads(g_rh, g_r, H, dh)
+    ops.gemm(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
+    g_qkv = ws.get("xl_g_qkv", (B * Kl, 3 * d), cdt)
+    ops.xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh)
+    ops.gemm(tp.a, g_qkv, a_mn=True, b_mn=True, out=G["wqkv"])
+    g_a = ws.get("xl_g_a", (B * Kl, d), torch.float32)
+    ops.gemm(g_qkv, W["wqkv"], out=g_a)
+    # LN1 over both row blocks: memory rows add to the gain / bias sums only
+    BM = B * M
+    if M:
+        g_mem = ws.get("xl_g_mem", (BM, d), torch.float32)
+        ops.layernorm_bwd(g_a[:BM], tp.xa[:BM], tp.mean1[:BM], tp.rstd1[:BM], vecs["ln1_g"], g_mem,
+                          pg[nbl_cur:], pb[nbl_cur:])
+    ops.layernorm_bwd(g_a[BM:], tp.xa[BM:], tp.mean1[BM:], tp.rstd1[BM:], vecs["ln1_g"], g_x, pg[:nbl_cur],
+                      pb[:nbl_cur], resid_grad=g_x1)
+    ops.colsum_finish(pg, nbl_cur + nbl_mem, G["ln1_g"])
+    ops.colsum_finish(pb, nbl_cur + nbl_mem, G["ln1_b"])
