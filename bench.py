@@ -42,13 +42,35 @@ CONFIGS = {
     "c2": dict(name="12L-d512-T512-WT103shape", vocab=267735, d=512, f=2048, blocks=12, seq=512, batch=16, p=0.1),
     # BASELINE.json configs[0] (the reference's CPU-runnable oracle case)
     "c1": dict(name="4L-d128-V1k", vocab=1000, d=128, f=512, blocks=4, seq=64, batch=16, p=0.1),
+    # BASELINE.json configs[2]: Transformer-XL base, enwik8-shaped byte stream
+    # (heads / memory / batch from the public XL scripts)
+    "c3": dict(name="XL-12L-d512-H8-T512-M512-enwik8shape", vocab=256, d=512, f=2048, blocks=12, seq=512, batch=22,
+               p=0.1, heads=8, mem=512),
+    # BASELINE.json configs[4]: Transformer-XL large, text8-shaped (27 symbols)
+    "c5": dict(name="XL-24L-d1024-H8-T768-M768-text8shape", vocab=27, d=1024, f=3072, blocks=24, seq=768,
+               batch=16, p=0.1, heads=8, mem=768),
 }
 
 
+def make_stack(c, seed, dtype="bf16"):
+    from paper_1909_06695_b200 import model as M
+
+    if c.get("heads"):
+        return M.build_xl_stack(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["p"], seed, c["heads"],
+                                c["mem"], dtype=dtype)
+    return M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["p"], seed, dtype=dtype)
+
+
 def flops_per_token(c):
-    """Model FLOPs per token = 3 * F_fwd, F_fwd = n*(2(4d^2+2df) + 2d(T+1)) + 2dV."""
+    """Model FLOPs per token = 3 * F_fwd:
+    reference block  F_fwd = n*(2(4d^2+2df) + 2d(T+1)) + 2dV,
+    XL block         F_fwd = n*(2(2d^2 + 2d^2(M+T)/T + 2df) + 6d(M+(T+1)/2)) + 2dV."""
     d, f, T, V, n = c["d"], c["f"], c["seq"], c["vocab"], c["blocks"]
-    fwd = n * (2 * (4 * d * d + 2 * d * f) + 2 * d * (T + 1)) + 2 * d * V
+    if c.get("heads"):
+        M = c["mem"]
+        fwd = n * (2 * (2 * d * d + 2 * d * d * (M + T) / T + 2 * d * f) + 6 * d * (M + (T + 1) / 2)) + 2 * d * V
+    else:
+        fwd = n * (2 * (4 * d * d + 2 * d * f) + 2 * d * (T + 1)) + 2 * d * V
     return 3 * fwd
 
 
@@ -122,9 +144,15 @@ def cpu_oracle_steps(c, K, steps, batch=1, budget_s=None):
     """Per-step seconds of the fp64 oracle Ouroboros step at B = `batch`."""
     from oracle import ouroboros as OO
 
-    V, layers = OO.init_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], 1)
     opt = OO.Adam(lambda t: 2.5e-4)
-    ora = OO.OuroborosOracle(V, layers, K, 3, c["p"], opt)
+    if c.get("heads"):
+        from oracle import xl as OX
+
+        V, layers = OX.init_xl_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["heads"], 1)
+        ora = OX.XLOuroborosOracle(V, layers, K, 3, c["p"], c["heads"], c["mem"], batch, opt)
+    else:
+        V, layers = OO.init_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], 1)
+        ora = OO.OuroborosOracle(V, layers, K, 3, c["p"], opt)
     rng = np.random.default_rng(0)
     times = []
     t_start = time.perf_counter()
@@ -204,7 +232,7 @@ def run_ours(args, c):
     K = 2
     B, T = c["batch"], c["seq"]
     tokens = B * T
-    stack = M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], T, c["p"], 1 + rank, dtype="bf16")
+    stack = make_stack(c, 1 + rank)
     part = M.partition(stack.num_layers, K)
     cls = E.ConcurrentPipelineEngine if args.engine == "concurrent" else E.PipelineEngine
     eng = cls(stack, part, dropout_seed=3)
@@ -250,10 +278,19 @@ def run_ours(args, c):
     ms_per_step = ms / args.steps
     value = world * tokens * args.steps / (ms / 1e3)
 
-    head = probe.events.get("head_gemm", []) + probe.events.get("head_gemm_bwd", [])
+    if c.get("heads"):
+        # XL: the attention-score GEMM pair AC = (q+u)k^T, BD = (q+v)r^T over
+        # [memory; segment] keys, 2 launches per span, 2*B*T*(M+T)*d FLOPs each
+        head = probe.events.get("xl_scores", [])
+        n_head_launches = 2 * len(head)
+        head_flops = 2.0 * tokens * (c["mem"] + T) * c["d"]
+        kernel_name = "gemm_kernel<bf16> (XL attention scores AC and BD, 2*B*T*(M+T)*d FLOPs/launch)"
+    else:
+        head = probe.events.get("head_gemm", []) + probe.events.get("head_gemm_bwd", [])
+        n_head_launches = len(probe.events.get("head_gemm", [])) + 3 * len(probe.events.get("head_gemm_bwd", []))
+        head_flops = 2.0 * tokens * c["d"] * c["vocab"]
+        kernel_name = "gemm_kernel<bf16,BN=256> (tied-vocab head, 2*N*d*V FLOPs/launch)"
     head_ms = [s.elapsed_time(e) for s, e in head]
-    n_head_launches = len(probe.events.get("head_gemm", [])) + 3 * len(probe.events.get("head_gemm_bwd", []))
-    head_flops = 2.0 * tokens * c["d"] * c["vocab"]
     pk, pk_kind = peaks()
     # spans: forward = 1 vocab GEMM (+ the tiny CE finish), backward = 3 vocab GEMMs
     avg_head_ms = sum(head_ms) / n_head_launches if head_ms else float("nan")
@@ -262,7 +299,7 @@ def run_ours(args, c):
     launches = probe.launches
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "head_gemm_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not c.get("heads"):
         with open(tpath) as fh:
             traffic = json.load(fh).get("bytes_per_launch")
 
@@ -292,7 +329,7 @@ def run_ours(args, c):
     if args.compare_k1 and world == 1:
         del eng
         torch.cuda.empty_cache()
-        stack1 = M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], T, c["p"], 1, dtype="bf16")
+        stack1 = make_stack(c, 1)
         seq = E.SequentialRunner(stack1, M.partition(stack1.num_layers, 1), dropout_seed=3)
         opt1 = O.make_optimizer("adam", O.LrSchedule(2.5e-4, "fixed"))
         for i in range(3):
@@ -329,6 +366,7 @@ def run_ours(args, c):
         "data": "synthetic (Zipf token ids, random-init weights)",
         "config": {"workload": c["name"], "K_modules": K, "global_batch": B * world, "seq_len": T,
                    "vocab": c["vocab"], "d_model": c["d"], "d_ff": c["f"], "n_blocks": c["blocks"],
+                   **({"n_heads": c["heads"], "mem_len": c["mem"]} if c.get("heads") else {}),
                    "engine": args.engine, "placement": "ring (modules 1 and K on GPU 0)",
                    "parallelism": f"ouroboros K={K} per GPU" + (" (replicas)" if world > 1 else ""),
                    "l2": "working set per step >> 126 MB L2 (no flush needed)"},
@@ -336,7 +374,7 @@ def run_ours(args, c):
                 "d2h_bytes_per_step": 4 + 4},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": achieved / peak_t, "traffic": traffic,
-                     "kernel": "gemm_kernel<bf16,BN=256> (tied-vocab head, 2*N*d*V FLOPs/launch)",
+                     "kernel": kernel_name,
                      "launches_per_step": n_head_launches / max(args.steps, 1), "share_of_step": head_share,
                      "peak_kind": f"{pk_kind} bf16_tflops_sustained"},
         "model_flops_util": flops_per_token(c) * value / (world * peak_t * 1e12),
@@ -373,7 +411,7 @@ def run_pipeline(args, c):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     K = world + 1
     B, T = c["batch"], c["seq"]
-    stack = M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], T, c["p"], 1, dtype="bf16")
+    stack = make_stack(c, 1)
     part = M.partition(stack.num_layers, K)
     mods = build_local_modules(stack, part, 3, rank)
     eng = DistributedPipelineEngine(mods, part, rank, tied=stack.tied_store if rank == 0 else None,

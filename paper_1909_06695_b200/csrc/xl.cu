@@ -34,92 +34,151 @@ __device__ __forceinline__ int64_t key_row(int64_t b, int64_t j, int64_t B, int6
   return j < M ? b * M + j : B * M + b * T + (j - M);
 }
 
+// 8 consecutive elements as fp32 (16 B of bf16 / 32 B of fp32); every head
+// dimension is a multiple of 8, so each vector stays inside one head row and
+// both sides of a head permute are 16-byte aligned and coalesced.
+template <typename T> struct V8;
+template <> struct V8<__nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      w[k] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <> struct V8<float> {
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[8]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+#define XL_GRID_LOOP(e, total) \
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (total); e += (int64_t)gridDim.x * blockDim.x)
+
+// unit e = ((h*B + b)*Kl + j)*C + c8, C = dh/8
 template <typename T>
 __global__ void split_qkv_kernel(const T* __restrict__ qkv, const float* __restrict__ u, const float* __restrict__ v,
                                  T* __restrict__ qu, T* __restrict__ qv, T* __restrict__ kh, T* __restrict__ vh,
-                                 int64_t B, int64_t Tn, int64_t M, int H, int dh) {
-  const int64_t Kl = M + Tn;
-  const int64_t d = (int64_t)H * dh;
-  const int64_t total = (int64_t)H * B * Kl * dh;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % dh);
-    int64_t r = e / dh;
-    const int64_t j = r % Kl;
-    r /= Kl;
-    const int64_t b = r % B;
-    const int h = (int)(r / B);
-    const T* src = qkv + key_row(b, j, B, Tn, M) * 3 * d + (int64_t)h * dh + c;
-    kh[e] = src[d];
-    vh[e] = src[2 * d];
+                                 int B, int Tn, int M, int H, int dh) {
+  const int Kl = M + Tn, C = dh / 8, d = H * dh;
+  const int64_t total = (int64_t)H * B * Kl * C;
+  XL_GRID_LOOP(e, total) {
+    const int c = (int)(e % C) * 8;
+    const int64_t hbj = e / C;
+    const int j = (int)(hbj % Kl);
+    const int hb = (int)(hbj / Kl);
+    const int b = hb % B, h = hb / B;
+    const T* src = qkv + key_row(b, j, B, Tn, M) * 3 * d + h * dh + c;
+    float x[8];
+    V8<T>::ld(src + d, x);
+    V8<T>::st(kh + hbj * dh + c, x);
+    V8<T>::ld(src + 2 * d, x);
+    V8<T>::st(vh + hbj * dh + c, x);
     if (j >= M) {
-      const float q = to_f(src[0]);
-      const int64_t o = (((int64_t)h * B + b) * Tn + (j - M)) * dh + c;
-      qu[o] = from_f<T>(q + u[h * dh + c]);
-      qv[o] = from_f<T>(q + v[h * dh + c]);
+      V8<T>::ld(src, x);
+      float y[8];
+      const float* uu = u + h * dh + c;
+      const float* vv = v + h * dh + c;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[k] = x[k] + uu[k];
+      const int64_t o = ((int64_t)hb * Tn + (j - M)) * dh + c;
+      V8<T>::st(qu + o, y);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[k] = x[k] + vv[k];
+      V8<T>::st(qv + o, y);
     }
   }
 }
 
+// dst[h, r, c] = src[r*ld + h*dh + c]; unit e = (h*rows + r)*C + c8
 template <typename S, typename D>
 __global__ void split_heads_kernel(const S* __restrict__ src, int64_t ld, D* __restrict__ dst, int64_t rows, int H,
                                    int dh) {
-  const int64_t total = rows * H * dh;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % dh);
-    const int64_t r = (e / dh) % rows;
-    const int h = (int)(e / (dh * rows));
-    dst[e] = from_f<D>(to_f(src[r * ld + (int64_t)h * dh + c]));
+  const int C = dh / 8;
+  XL_GRID_LOOP(e, rows * H * C) {
+    const int c = (int)(e % C) * 8;
+    const int64_t hr = e / C;
+    const int64_t r = hr % rows;
+    const int h = (int)(hr / rows);
+    float x[8];
+    V8<S>::ld(src + r * ld + h * dh + c, x);
+    V8<D>::st(dst + hr * dh + c, x);
   }
 }
 
+// dst[r*ld + h*dh + c] = src[h, r, c]; unit e = (r*H + h)*C + c8 (row-major writes)
 template <typename S, typename D>
 __global__ void merge_heads_kernel(const S* __restrict__ src, D* __restrict__ dst, int64_t ld, int64_t rows, int H,
                                    int dh) {
-  const int64_t d = (int64_t)H * dh;
-  const int64_t total = rows * d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / d;
-    const int col = (int)(e % d);
-    const int h = col / dh, c = col % dh;
-    dst[r * ld + col] = from_f<D>(to_f(src[((int64_t)h * rows + r) * dh + c]));
+  const int C = dh / 8;
+  XL_GRID_LOOP(e, rows * H * C) {
+    const int c = (int)(e % C) * 8;
+    const int64_t rh = e / C;
+    const int h = (int)(rh % H);
+    const int64_t r = rh / H;
+    float x[8];
+    V8<S>::ld(src + ((int64_t)h * rows + r) * dh + c, x);
+    V8<D>::st(dst + r * ld + h * dh + c, x);
   }
 }
 
 // g_qkv rows in the xa layout: q columns = dQu + dQv (zero on memory rows),
-// k / v columns from the head-major key gradients.
+// k / v columns from the head-major key gradients.  unit = 8 columns of a row.
 template <typename T>
 __global__ void merge_grads_kernel(const float* __restrict__ gqu, const float* __restrict__ gqv,
                                    const float* __restrict__ gkh, const float* __restrict__ gvh, T* __restrict__ gqkv,
-                                   int64_t B, int64_t Tn, int64_t M, int H, int dh) {
-  const int64_t Kl = M + Tn;
-  const int64_t d = (int64_t)H * dh;
-  const int64_t total = B * Kl * 3 * d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / (3 * d);
-    const int col = (int)(e % (3 * d));
-    const int part = col / (int)d;
-    const int h = (col % (int)d) / dh, c = col % dh;
-    int64_t b, j;
-    if (row < B * M) {
-      b = row / M;
-      j = row % M;
+                                   int B, int Tn, int M, int H, int dh) {
+  const int Kl = M + Tn, d = H * dh, C3 = 3 * d / 8;
+  const int64_t BM = (int64_t)B * M;
+  XL_GRID_LOOP(e, (int64_t)B * Kl * C3) {
+    const int64_t row = e / C3;
+    const int col = (int)(e % C3) * 8;
+    const int part = col / d;
+    const int h = (col % d) / dh, c = col % dh;
+    int b, j;
+    if (row < BM) {
+      b = (int)(row / M);
+      j = (int)(row % M);
     } else {
-      b = (row - B * M) / Tn;
-      j = M + (row - B * M) % Tn;
+      b = (int)((row - BM) / Tn);
+      j = M + (int)((row - BM) % Tn);
     }
-    float g;
+    float g[8];
     if (part == 0) {
       if (j < M) {
-        g = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] = 0.f;
       } else {
         const int64_t o = (((int64_t)h * B + b) * Tn + (j - M)) * dh + c;
-        g = gqu[o] + gqv[o];
+        float g2[8];
+        V8<float>::ld(gqu + o, g);
+        V8<float>::ld(gqv + o, g2);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] += g2[k];
       }
     } else {
       const int64_t o = (((int64_t)h * B + b) * Kl + j) * dh + c;
-      g = part == 1 ? gkh[o] : gvh[o];
+      V8<float>::ld((part == 1 ? gkh : gvh) + o, g);
     }
-    gqkv[e] = from_f<T>(g);
+    V8<T>::st(gqkv + row * 3 * d + col, g);
   }
 }
 
@@ -162,9 +221,36 @@ __global__ void __launch_bounds__(kThreads) softmax_fwd_kernel(const float* __re
   }
 }
 
+// 4-wide row access for the backward softmax
+template <typename T> struct V4x;
+template <> struct V4x<__nv_bfloat16> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float (&v)[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[4]) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+    *reinterpret_cast<uint2*>(p) = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+};
+template <> struct V4x<float> {
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[4]) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
 // dS = P (dP - <dP, P>) * scale; writes dAC = dS and the un-shifted
-// dBD[p] = dS[p - (T-1-i)] (zero where no key maps to p).
-template <typename T, int NPL>
+// dBD[p] = dS[p - (T-1-i)] (zero where no key maps to p).  Lane owns 4
+// consecutive columns per 128-column group (NG groups); dS is staged in
+// shared memory for the shifted write.
+template <typename T, int NG>
 __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __restrict__ gp, int64_t lds,
                                                                 const T* __restrict__ p, int64_t ldp,
                                                                 T* __restrict__ gac, T* __restrict__ gbd,
@@ -174,37 +260,54 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __re
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
   if (row >= rows) return;
-  float* gs_row = sh_gs + warp * (32 * NPL);
+  float* gs_row = sh_gs + warp * (128 * NG);
   const int i = (int)(row % Tn);
   const int lo = M - mem_len, hi = M + i, off = Tn - 1 - i;
   const float* g = gp + row * lds;
   const T* pr = p + row * ldp;
-  float pv[NPL], gv[NPL];
+  float pv[NG][4], gv[NG][4];
   float dot = 0.f;
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int j = lane + 32 * q;
-    const bool ok = j >= lo && j <= hi;
-    pv[q] = ok ? to_f(pr[j]) : 0.f;
-    gv[q] = ok ? g[j] : 0.f;
-    dot += pv[q] * gv[q];
+  for (int q = 0; q < NG; ++q) {
+    const int j0 = 4 * lane + 128 * q;
+    if (j0 < ldp) {
+      V4x<T>::ld(pr + j0, pv[q]);
+      V4x<float>::ld(g + j0, gv[q]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pv[q][k] = gv[q][k] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      if (j < lo || j > hi) pv[q][k] = gv[q][k] = 0.f;
+      dot += pv[q][k] * gv[q][k];
+    }
   }
   dot = warp_sum(dot);
   T* ga = gac + row * ldp;
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int j = lane + 32 * q;
-    const float v = pv[q] * (gv[q] - dot) * scale;
-    gs_row[j] = v;
-    if (j < ldp) ga[j] = from_f<T>(v);
+  for (int q = 0; q < NG; ++q) {
+    const int j0 = 4 * lane + 128 * q;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = pv[q][k] * (gv[q][k] - dot) * scale;
+    *reinterpret_cast<float4*>(gs_row + j0) = make_float4(o[0], o[1], o[2], o[3]);
+    if (j0 < ldp) V4x<T>::st(ga + j0, o);
   }
   __syncwarp();
   T* gb = gbd + row * ldp;
 #pragma unroll
-  for (int q = 0; q < NPL; ++q) {
-    const int pcol = lane + 32 * q;
-    const int j = pcol - off;
-    if (pcol < ldp) gb[pcol] = from_f<T>((j >= 0 && j < 32 * NPL) ? gs_row[j] : 0.f);
+  for (int q = 0; q < NG; ++q) {
+    const int p0 = 4 * lane + 128 * q;
+    if (p0 >= ldp) continue;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = p0 + k - off;
+      o[k] = (j >= 0 && j < 128 * NG) ? gs_row[j] : 0.f;
+    }
+    V4x<T>::st(gb + p0, o);
   }
 }
 
@@ -277,53 +380,66 @@ inline int npl_for(int64_t n) {
     default: return set_error(RP_ERR_DIMENSION, "XL key length too large"); \
   }
 
+inline int blocks8(int64_t units) { return blocks_for(units); }
+
 int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, void* qu, void* qv, void* kh, void* vh,
                  int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st) {
-  const int64_t n = (int64_t)H * B * (M + Tn) * dh;
+  if (dh % 8) return set_error(RP_ERR_DIMENSION, "xl_split_qkv: head dim must be a multiple of 8");
+  const int64_t n = (int64_t)H * B * (M + Tn) * (dh / 8);
   if (n == 0) return RP_OK;
-  XL_DTYPE(dtype, split_qkv_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(
-                      (const T*)qkv, u, v, (T*)qu, (T*)qv, (T*)kh, (T*)vh, B, Tn, M, H, dh));
+  XL_DTYPE(dtype, split_qkv_kernel<T><<<blocks8(n), kThreads, 0, st>>>(
+                      (const T*)qkv, u, v, (T*)qu, (T*)qv, (T*)kh, (T*)vh, (int)B, (int)Tn, (int)M, H, dh));
   return check_launch("xl_split_qkv");
 }
 
+#define XL_PAIR(SD, DD, LAUNCH)                        \
+  if ((SD) == RP_BF16 && (DD) == RP_BF16) {              \
+    using S = __nv_bfloat16;                             \
+    using D = __nv_bfloat16;                             \
+    LAUNCH;                                              \
+  } else if ((SD) == RP_F32 && (DD) == RP_BF16) {        \
+    using S = float;                                     \
+    using D = __nv_bfloat16;                             \
+    LAUNCH;                                              \
+  } else if ((SD) == RP_BF16 && (DD) == RP_F32) {        \
+    using S = __nv_bfloat16;                             \
+    using D = float;                                     \
+    LAUNCH;                                              \
+  } else {                                               \
+    using S = float;                                     \
+    using D = float;                                     \
+    LAUNCH;                                              \
+  }
+
 int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, void* dst, int64_t rows, int H, int dh,
                    cudaStream_t st) {
-  const int64_t n = rows * H * dh;
+  if (dh % 8 || ld % 8) return set_error(RP_ERR_DIMENSION, "xl_split_heads: head dim and ld must be multiples of 8");
+  const int64_t n = rows * H * (dh / 8);
   if (n == 0) return RP_OK;
-  const int g = blocks_for(n);
-  if (src_dtype == RP_BF16 && dst_dtype == RP_BF16)
-    split_heads_kernel<<<g, kThreads, 0, st>>>((const __nv_bfloat16*)src, ld, (__nv_bfloat16*)dst, rows, H, dh);
-  else if (src_dtype == RP_F32 && dst_dtype == RP_BF16)
-    split_heads_kernel<<<g, kThreads, 0, st>>>((const float*)src, ld, (__nv_bfloat16*)dst, rows, H, dh);
-  else if (src_dtype == RP_BF16 && dst_dtype == RP_F32)
-    split_heads_kernel<<<g, kThreads, 0, st>>>((const __nv_bfloat16*)src, ld, (float*)dst, rows, H, dh);
-  else
-    split_heads_kernel<<<g, kThreads, 0, st>>>((const float*)src, ld, (float*)dst, rows, H, dh);
+  const int g = blocks8(n);
+  XL_PAIR(src_dtype, dst_dtype,
+          (split_heads_kernel<S, D><<<g, kThreads, 0, st>>>((const S*)src, ld, (D*)dst, rows, H, dh)));
   return check_launch("xl_split_heads");
 }
 
 int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
                    cudaStream_t st) {
-  const int64_t n = rows * H * dh;
+  if (dh % 8 || ld % 8) return set_error(RP_ERR_DIMENSION, "xl_merge_heads: head dim and ld must be multiples of 8");
+  const int64_t n = rows * H * (dh / 8);
   if (n == 0) return RP_OK;
-  const int g = blocks_for(n);
-  if (src_dtype == RP_BF16 && dst_dtype == RP_BF16)
-    merge_heads_kernel<<<g, kThreads, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst, ld, rows, H, dh);
-  else if (src_dtype == RP_F32 && dst_dtype == RP_BF16)
-    merge_heads_kernel<<<g, kThreads, 0, st>>>((const float*)src, (__nv_bfloat16*)dst, ld, rows, H, dh);
-  else if (src_dtype == RP_BF16 && dst_dtype == RP_F32)
-    merge_heads_kernel<<<g, kThreads, 0, st>>>((const __nv_bfloat16*)src, (float*)dst, ld, rows, H, dh);
-  else
-    merge_heads_kernel<<<g, kThreads, 0, st>>>((const float*)src, (float*)dst, ld, rows, H, dh);
+  const int g = blocks8(n);
+  XL_PAIR(src_dtype, dst_dtype,
+          (merge_heads_kernel<S, D><<<g, kThreads, 0, st>>>((const S*)src, (D*)dst, ld, rows, H, dh)));
   return check_launch("xl_merge_heads");
 }
 
 int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
                    int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st) {
-  const int64_t n = B * (M + Tn) * 3 * (int64_t)H * dh;
+  if (dh % 8) return set_error(RP_ERR_DIMENSION, "xl_merge_grads: head dim must be a multiple of 8");
+  const int64_t n = B * (M + Tn) * 3 * (int64_t)H * dh / 8;
   if (n == 0) return RP_OK;
-  XL_DTYPE(dtype, merge_grads_kernel<T><<<blocks_for(n), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv, B, Tn, M,
-                                                                           H, dh));
+  XL_DTYPE(dtype, merge_grads_kernel<T><<<blocks8(n), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv, (int)B,
+                                                                        (int)Tn, (int)M, H, dh));
   return check_launch("xl_merge_grads");
 }
 
@@ -342,17 +458,35 @@ int xl_softmax_fwd(int dtype, const float* ac, const float* bd, int64_t lds, voi
 int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64_t ldp, void* gac, void* gbd,
                    int64_t rows, int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st) {
   if (rows == 0) return RP_OK;
-  if (mem_len < 0 || mem_len > M || ldp < M + Tn || lds < M + Tn)
+  if (mem_len < 0 || mem_len > M || ldp < M + Tn || lds < M + Tn || ldp % 8 || lds % 4)
     return set_error(RP_ERR_DIMENSION, "xl_softmax_bwd: bad memory length or leading dimension");
-  const int npl = npl_for(ldp);
+  const int need = (int)((ldp + 127) / 128);
+  const int ng = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : need <= 12 ? 12 : need <= 16 ? 16 : -1;
   const int g = (int)((rows + kWarps - 1) / kWarps);
-  XL_DTYPE(dtype, XL_NPL(npl, {
-    const size_t smem = sizeof(float) * kWarps * 32 * NPL;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(softmax_bwd_kernel<T, NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    softmax_bwd_kernel<T, NPL><<<g, kThreads, smem, st>>>(gp, lds, (const T*)p, ldp, (T*)gac, (T*)gbd, rows,
-                                                          (int)Tn, (int)M, (int)mem_len, scale);
-  }));
+#define XL_BWD(NGV)                                                                                   \
+  case NGV: {                                                                                         \
+    constexpr int NG = NGV;                                                                           \
+    const size_t smem = sizeof(float) * kWarps * 128 * NG;                                            \
+    XL_DTYPE(dtype, {                                                                                 \
+      if (smem > 48 * 1024)                                                                           \
+        cudaFuncSetAttribute(softmax_bwd_kernel<T, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)smem);                                                              \
+      softmax_bwd_kernel<T, NG><<<g, kThreads, smem, st>>>(gp, lds, (const T*)p, ldp, (T*)gac, (T*)gbd, \
+                                                           rows, (int)Tn, (int)M, (int)mem_len, scale); \
+    });                                                                                               \
+    break;                                                                                            \
+  }
+  switch (ng) {
+    XL_BWD(1)
+    XL_BWD(2)
+    XL_BWD(4)
+    XL_BWD(8)
+    XL_BWD(12)
+    XL_BWD(16)
+    default:
+      return set_error(RP_ERR_DIMENSION, "xl_softmax_bwd: key length not supported");
+  }
+#undef XL_BWD
   return check_launch("xl_softmax_bwd");
 }
 

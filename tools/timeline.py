@@ -17,7 +17,7 @@ from paper_1909_06695_b200 import optim as O  # noqa: E402
 
 c = bench.CONFIGS[os.environ.get("CFG", "c2")]
 B, T = c["batch"], c["seq"]
-stack = M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], T, c["p"], 1, dtype="bf16")
+stack = bench.make_stack(c, 1)
 cls = E.PipelineEngine if os.environ.get("ENGINE") == "reference" else E.ConcurrentPipelineEngine
 eng = cls(stack, M.partition(stack.num_layers, 2), 3)
 opt = O.make_optimizer("adam", O.LrSchedule(2.5e-4))
@@ -49,7 +49,7 @@ busy += cur_e - cur_s
 span = t1 - t0
 tot = collections.defaultdict(float)
 for s, e, n in iv:
-    tot[n.split("(")[0][:50]] += e - s
+    tot[n.replace("(anonymous namespace)::", "").split("(")[0][:60]] += e - s
 print(json.dumps({"steps": steps, "span_ms": span / 1e3, "ms_per_step": span / 1e3 / steps,
                   "gpu_busy_frac": busy / span, "gaps_over_5us": sum(1 for g in gaps if g > 5),
                   "gap_ms_total": sum(gaps) / 1e3}))
