@@ -37,7 +37,7 @@ import torch
 
 from . import checkpoint as ckpt
 from .config import RunConfig
-from .data import BatchSource, load_corpus
+from .data import BatchSource, SegmentStream, load_corpus
 from .engine import (
     ConcurrentPipelineEngine,
     LogicalCostModel,
@@ -49,7 +49,7 @@ from .engine import (
 )
 from .errors import DimensionError, NonFiniteError
 from .metrics import MetricsRow, MetricsWriter
-from .model import StaleSlot, build_modules, build_stack, measure_layer_costs, partition
+from .model import StaleSlot, build_modules, build_stack, build_xl_stack, measure_layer_costs, partition
 from .optim import make_optimizer
 from .rng import SeededRng, mix64
 
@@ -66,7 +66,7 @@ STRUCTURAL_FIELDS = (
     "ffn_dim", "dropout_p", "k", "mode", "tied_grad", "stale_weights",
     "balance", "optimizer", "lr", "lr_mode", "warmup_steps", "steps",
     "adam_beta1", "adam_beta2", "adam_eps", "seed_init", "seed_data",
-    "seed_dropout",
+    "seed_dropout", "n_heads", "mem_len",
 )
 
 
@@ -94,9 +94,15 @@ def _make_engine(cfg, stack, part, cost_model):
 
 def build_runtime(cfg, synthetic_cost=None, device=None):
     tokens, vocab = load_corpus(cfg.data, cfg.vocab_mode)
-    source = BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data)
-    stack = build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
-                        cfg.seed_init, dtype=cfg.dtype, device=device)
+    if cfg.n_heads:
+        # XL: contiguous segment streams so each row's memory precedes it
+        source = SegmentStream(tokens, cfg.seq_len, cfg.batch_size)
+        stack = build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
+                               cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=cfg.dtype, device=device)
+    else:
+        source = BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data)
+        stack = build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
+                            cfg.seed_init, dtype=cfg.dtype, device=device)
     costs = None
     if cfg.balance == "by_cost":
         costs = measure_layer_costs(stack, source.batch_at(0).x, cfg.seed_dropout)
@@ -166,8 +172,18 @@ def collect_state(runtime, next_step):
                 arrays[pre + "embedded"] = a.acts[0].view(a.B, a.T, d)
             if m.has_projection:
                 arrays[pre + "targets"] = a.targets.view(a.B, a.T)
+            for j2, off in enumerate(m.block_idx):
+                tp = a.tapes[j2]
+                if m.layers[off].kind == "xl_block" and tp.M:
+                    arrays[pre + f"mem.L{m.layer_range[0] + off}"] = tp.mem.view(a.B, tp.M, d)
+                    arrays[pre + "mem_len"] = np.array([tp.mem_len], dtype=np.int64)
             arrays[pre + "meta"] = np.array([slot.step, slot.sample_id], dtype=np.int64)
             arrays[pre + "seeds"] = np.array(slot.layer_seeds, dtype=np.uint64)
+    for m in engine.modules:
+        for off, buf in m.mem.items():
+            arrays[f"m{m.index}.mem.L{m.layer_range[0] + off}"] = buf
+        if m.mem:
+            arrays[f"m{m.index}.mem_len"] = np.array([m.mem_len], dtype=np.int64)
     B, T = runtime.cfg.batch_size, runtime.cfg.seq_len
     for k, g in engine.export_boundary().items():
         arrays[f"boundary.{k}"] = g.view(B, T, d) if g.numel() == B * T * d else g
@@ -197,7 +213,8 @@ def load_training_state(path, runtime):
     sidecar = ckpt.load_sidecar(path)
     saved = sidecar.get("config", {})
     for name in STRUCTURAL_FIELDS:
-        ours, theirs = getattr(runtime.cfg, name), saved.get(name)
+        # fields the reference lacks (n_heads, mem_len) default like ours
+        ours, theirs = getattr(runtime.cfg, name), saved.get(name, getattr(RunConfig(), name))
         if ours != theirs:
             raise ckpt.CheckpointError(f"checkpoint config mismatch on {name!r}: {theirs!r} != {ours!r}")
     stack, engine = runtime.stack, runtime.engine
@@ -246,6 +263,15 @@ def load_training_state(path, runtime):
                     _put(arena.acts[0], inputs.reshape(B * T, d), "inputs")
                 if m.has_projection:
                     _put(arena.targets, targets, "targets")
+                slot_mem_len = arrays.pop(f"{pre}slot{j}.mem_len", None)
+                for j2, off in enumerate(m.block_idx):
+                    tp = arena.tapes[j2]
+                    key = f"{pre}slot{j}.mem.L{m.layer_range[0] + off}"
+                    if m.layers[off].kind == "xl_block" and tp.M:
+                        if key not in arrays:
+                            raise ckpt.CheckpointError(f"checkpoint lacks {key!r}")
+                        _put(tp.mem, arrays.pop(key), key)
+                        tp.mem_len = int(slot_mem_len[0])
                 slot = StaleSlot(step, sample_id, arena.tokens if m.has_embedding else arena.acts[0], targets,
                                  seeds, arena)
                 m.slots.append(slot)
@@ -266,6 +292,15 @@ def load_training_state(path, runtime):
                 m._run_forward(step, arena, seeds, engine.train, None, m.ws_fwd, live=False, **kw)
                 j += 1
             m.last_forward_step = next_step - 1
+            for off in m.block_idx:
+                key = f"{pre}mem.L{m.layer_range[0] + off}"
+                if key in arrays:
+                    src = arrays.pop(key)
+                    m.mem[off] = torch.empty(src.size // d, d, dtype=stack.cdtype,
+                                             device=stack.runtime.device)
+                    _put(m.mem[off], src, key)
+            if f"{pre}mem_len" in arrays:
+                m.mem_len = int(arrays.pop(f"{pre}mem_len")[0])
         engine.import_boundary({int(n.split(".")[1]): arrays.pop(n) for n in list(arrays)
                                 if n.startswith("boundary.")})
         engine.clock = float(sidecar["clock"])
@@ -295,6 +330,9 @@ def train(cfg, progress=None):
     try:
         for t in range(start_step, end_step):
             t0 = time.perf_counter()
+            if getattr(runtime.source, "wraps_at", None) and runtime.source.wraps_at(t):
+                for m in engine.modules:
+                    m.reset_memory()  # the segment streams restart
             try:
                 packet, loss = engine.step(t, runtime.source.batch_at(t), optimizer)
             except (NonFiniteError, WorkerFailure, DimensionError):

@@ -117,3 +117,21 @@ def test_by_cost_partition_from_device_costs(in_gold, tmp_path):
     assert len(costs) == rt.stack.num_layers and all(c > 0 for c in costs)
     groups = rt.part.groups
     assert groups[0][0] == 0 and groups[-1][1] == rt.stack.num_layers and len(groups) == 2
+
+
+@pytest.mark.parametrize("mode", ["ouroboros-ref", "ouroboros-concurrent"])
+def test_xl_train_halt_and_resume_is_bit_exact(in_gold, tmp_path, mode):
+    """Transformer-XL runs carry the segment memory (per module and per
+    pending slot) through the checkpoint."""
+    kw = dict(mode=mode, n_heads=2, mem_len=16, k=3)
+    full = R.train(cfg_for(tmp_path, "full", **kw))
+    R.train(cfg_for(tmp_path, "halt", halt_at=5, **kw))
+    resumed = R.train(cfg_for(tmp_path, "resumed", resume=str(tmp_path / "halt" / "checkpoint.bin"), **kw))
+    a = read_metrics(full["metrics_path"])[5:]
+    b = read_metrics(resumed["metrics_path"])
+    assert [(r.loss, r.grad_sq_norm) for r in a] == [(r.loss, r.grad_sq_norm) for r in b]
+    x = ckpt.load_arrays(full["checkpoint_path"])
+    y = ckpt.load_arrays(resumed["checkpoint_path"])
+    assert any(k.startswith("m1.mem.") for k in x) and sorted(x) == sorted(y)
+    for k in x:
+        np.testing.assert_array_equal(x[k], y[k], err_msg=k)
