@@ -9,7 +9,8 @@ import os
 
 from .errors import raise_for_status
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libringpipe_b200.so")
+_LIB_PATH = os.environ.get("RP_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                           "libringpipe_b200.so")
 _lib = None
 
 # rp_dtype / rp_math / rp_epilogue (include/ringpipe_b200.h)

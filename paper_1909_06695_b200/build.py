@@ -16,6 +16,11 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libringpipe_b200.so")
+# A/B variants for kernel experiments: RP_LIB_OUT=<path> RP_EXTRA_NVCC="-DX=1"
+# (load one with RP_LIB_PATH=<path>); the default build ignores both
+if os.environ.get("RP_LIB_OUT"):
+    LIB = os.path.abspath(os.environ["RP_LIB_OUT"])
+EXTRA = os.environ.get("RP_EXTRA_NVCC", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -41,11 +46,15 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
+def _obj_dir():
+    return os.path.join(OUT_DIR, "obj") if not EXTRA else LIB + ".obj"
+
+
 def _compile(src):
-    obj = os.path.join(OUT_DIR, "obj", os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *CFLAGS, "-c", src, "-o", obj]
+    obj = os.path.join(_obj_dir(), os.path.basename(src) + ".o")
+    cmd = [NVCC, *ARCH, *CFLAGS, *EXTRA, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, *CFLAGS, "-x", "cu", *ARCH, "-c", src, "-o", obj]
+        cmd = [NVCC, *CFLAGS, *EXTRA, "-x", "cu", *ARCH, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
@@ -56,7 +65,7 @@ def build(force=False, verbose=True):
     """Compile and link the extension; returns the library path."""
     if not force and not _stale():
         return LIB
-    os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
+    os.makedirs(_obj_dir(), exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(_compile, srcs))
