@@ -49,7 +49,7 @@ typedef enum rp_epilogue {
   RP_EPI_STORE = 0,                 /* C = alpha*AB                                   */
   RP_EPI_BIAS_RELU = 1,             /* C = relu(alpha*AB + bias)        layers.py:190-191 */
   RP_EPI_BIAS_DROPOUT_RESIDUAL = 2, /* C = resid + (alpha*AB+bias)*mask layers.py:184-187,192-195 */
-  RP_EPI_LSE_PARTIAL = 3,           /* per-(row, N-tile) (max, sumexp) + target logit  layers.py:310-316 */
+  RP_EPI_LSE_PARTIAL = 3,           /* per-(row, N-tile, column half) (max, sumexp) + target logit  layers.py:310-316 */
   RP_EPI_CE_GRAD = 4,               /* C = (exp(AB - lse[row]) - onehot) * ce_scale    layers.py:317-319 */
   RP_EPI_RELU_GRAD = 5              /* C = alpha*AB * (residual > 0)                   layers.py:221 */
 } rp_epilogue;
@@ -84,7 +84,7 @@ typedef struct rp_gemm_args {
   uint64_t drop_pos0;       /* stream position of element (0,0) */
   const int64_t* targets;   /* [batch*M] */
   const float* lse;         /* [batch*M] */
-  float* partial;           /* [batch*M, n_tiles, 2] */
+  float* partial;           /* [batch*M, 2*n_tiles, 2]: (max, sumexp) per N tile and column half */
   float* target_logit;      /* [batch*M] */
   float ce_scale;
   int32_t k_splits; /* > 1: C = [k_splits, M, N] fp32 partials over K ranges (rp_splitk_reduce) */

@@ -408,7 +408,7 @@ int64_t head_workspace_bytes(const rp_head_desc& h) {
   const int bn = gemm_tile_n(h.rows, h.vocab, 1);
   const int64_t nt = (h.vocab + bn - 1) / bn;
   const int64_t e = esize(h.dtype);
-  int64_t b = al256(h.rows * nt * 2 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
+  int64_t b = al256(h.rows * nt * 4 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
   b += al256(kHeadSplitK * h.rows * h.d * 4);
   b += split_bytes(h.dtype, std::max(h.rows * pad8(h.vocab), h.vocab * h.d));
   return b + 4096;
@@ -420,7 +420,7 @@ int head_forward(const rp_head_desc& h, const void* x, const void* tied, const i
   const int bn = gemm_tile_n(h.rows, h.vocab, 1);
   const int64_t nt = (h.vocab + bn - 1) / bn, N = h.rows, D = h.d, V = h.vocab;
   Bump bp{static_cast<char*>(ws), ws_bytes};
-  float* partial = static_cast<float*>(bp.take(N * nt * 2 * 4));
+  float* partial = static_cast<float*>(bp.take(N * nt * 4 * 4));  // (max, sum) per row, tile and column half
   float* zy = static_cast<float*>(bp.take(N * 4));
   float* rows = static_cast<float*>(bp.take(N * 4));
   bp.take(N * pad8(V) * esize(h.dtype));  // dz (backward)
@@ -434,7 +434,7 @@ int head_forward(const rp_head_desc& h, const void* x, const void* tied, const i
   e.partial = partial;
   e.target_logit = zy;
   RP_TRY(mm(c, mat(x, N, D, D), false, mat(tied, V, D, D), false, Mat{nullptr, N, V, 0}, RP_F32, e));
-  return ce_finish(partial, (int)nt, zy, targets, V, N, lse, rows, loss, loss64, flag, st);
+  return ce_finish(partial, (int)(2 * nt), zy, targets, V, N, lse, rows, loss, loss64, flag, st);
 }
 
 int head_backward(const rp_head_desc& h, const void* x, const void* tied, const int64_t* targets, const float* lse,

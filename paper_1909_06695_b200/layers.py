@@ -205,7 +205,7 @@ def head_forward_ops(h, tied_c, targets, vocab, hs, ws, flag):
     Nt = h.shape[0]
     bn = ops.gemm_tile_n(vocab, Nt)
     nt = (vocab + bn - 1) // bn
-    partial = ws.get("head_partial", (Nt, nt, 2), torch.float32)
+    partial = ws.get("head_partial", (Nt, 2 * nt, 2), torch.float32)  # per tile and column half
     zy = ws.get("head_zy", (Nt,), torch.float32)
     rows_loss = ws.get("head_rows", (Nt,), torch.float32)
     with ops.span("head_gemm"):

@@ -135,7 +135,7 @@ def test_lse_partial_and_ce_grad(dev, dtype):
     y = torch.randint(0, V, (M,), device=dev, generator=None)
     bn = ops.gemm_tile_n(V, M)
     nt = (V + bn - 1) // bn
-    partial = torch.empty((M, nt, 2), dtype=torch.float32, device=dev)
+    partial = torch.empty((M, 2 * nt, 2), dtype=torch.float32, device=dev)  # per tile and column half
     zy = torch.empty((M,), dtype=torch.float32, device=dev)
     ops.gemm(h, tied, epilogue=N.EPI_LSE_PARTIAL, targets=y, partial=partial, target_logit=zy)
     mx = partial[..., 0].max(dim=1).values
