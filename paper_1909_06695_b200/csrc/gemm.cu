@@ -462,16 +462,18 @@ __global__ void __launch_bounds__(384, 1)
         tgt = p.targets[grow];
         if (p.epi == RP_EPI_CE_GRAD) lse2 = p.lse[grow] * kLog2e - __log2f(p.ce_scale);
       }
-      // CE-gradient epilogue (bf16): no aux input; the TMEM load of the next
-      // 32-column chunk is in flight while this chunk's exps and bf16 TMA
-      // store run (measured: CE pass 2.22 -> 1.84 ms at C2; the LSE pass did
-      // not gain and keeps the generic loop)
+      // epilogues without an aux input (store, bias+ReLU, CE gradient; bf16
+      // math): the TMEM load of the next 32-column chunk is in flight while
+      // this chunk is processed and stored -- the epilogue is latency-bound
+      // at two warps per SM sub-partition (measured: CE pass 2.24 -> 1.82 ms
+      // at C2; the LSE pass did not gain and keeps the generic loop)
       bool head_fast = false;
 #ifndef RP_HEAD_FAST_OFF
 #define RP_HEAD_FAST_OFF 0
 #endif
       if constexpr (!kTf32 && kHalf % 2 == 0 && !RP_HEAD_FAST_OFF) {
-        if (p.epi == RP_EPI_CE_GRAD && p.tma_store) {
+        const bool no_aux = p.epi == RP_EPI_CE_GRAD || p.epi == RP_EPI_STORE || p.epi == RP_EPI_BIAS_RELU;
+        if (no_aux && (p.tma_store || p.epi != RP_EPI_CE_GRAD)) {
           head_fast = true;
           const int trow = (int)((int64_t)b * p.M + mrow0 + q * 32);
           auto chunk = [&](const uint32_t (&r)[32], int c) {
@@ -481,21 +483,35 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
             const bool full = n0 + 32 <= p.N;
-            {
-              if (row_ok) {
+            if (!row_ok) {
+              if (p.tma_store) {  // rows past M: zeros, clipped by the TMA store
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], kLog2e, -lse2));
-                if ((uint64_t)(tgt - n0) < 32ull) {
-#pragma unroll
-                  for (int j = 0; j < 32; ++j)
-                    if (tgt == n0 + j) v[j] -= p.ce_scale;
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0.f;  // rows past M: clipped by the TMA store
+                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                emit_tma<Cfg::OUT_BUFS>(mapC, my_out_base, v, lane, n0, trow);
               }
-              emit_tma<Cfg::OUT_BUFS>(mapC, my_out_base, v, lane, n0, trow);
+              return;
             }
+            if (p.epi == RP_EPI_CE_GRAD) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], kLog2e, -lse2));
+              if ((uint64_t)(tgt - n0) < 32ull) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (tgt == n0 + j) v[j] -= p.ce_scale;
+              }
+            } else if (p.epi == RP_EPI_BIAS_RELU) {
+              float bb[32];
+              load_bias(p, n0, full, bb);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = fmaxf(fmaf(v[j], p.alpha, bb[j]), 0.f);
+            } else if (p.alpha != 1.f) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
+            }
+            if (p.tma_store)
+              emit_tma<Cfg::OUT_BUFS>(mapC, my_out_base, v, lane, n0, trow);
+            else
+              store_chunk(p, m, n0, b, v);
           };
           const int c0 = half * kHalf;
           uint32_t ra[32], rb[32];
