@@ -246,6 +246,7 @@ int64_t block_workspace_bytes(const rp_block_desc& d) {
   b += al256(N * 3 * d.d * e);                 // g_qkv
   b += al256(N * d.d * 4) * 3;                 // g_m, g_x1, g_a
   b += al256(nbp * std::max(d.f, 3 * d.d) * 4) * 3;  // partials
+  b += al256(nbp * d.d * 4) * 3;                      // b2 / ln2 partials (finished together at the end)
   b += al256(kBlockSplitK) * 2;  // main + side stream partials
   b += split_bytes(d.dtype, std::max({N * d.f, d.B * d.T * Tp, N * 3 * d.d, d.d * d.f}));
   return b + 4096;
@@ -318,6 +319,9 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   float* part = static_cast<float*>(bp.take(nbp * pw * 4));
   float* pg = static_cast<float*>(bp.take(nbp * pw * 4));
   float* pb = static_cast<float*>(bp.take(nbp * pw * 4));
+  float* part_b2 = static_cast<float*>(bp.take(nbp * D * 4));
+  float* pg2 = static_cast<float*>(bp.take(nbp * D * 4));
+  float* pb2 = static_cast<float*>(bp.take(nbp * D * 4));
   Ctx c{dt, st};
   c.max_ctas = d.max_ctas;
   c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
@@ -360,23 +364,25 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   const char* qkv = static_cast<const char*>(tp.qkv);
   const float inv = 1.f / std::sqrt(static_cast<float>(D));
   // feed-forward branch (layers.py:209-232)
+  // The bias / LayerNorm column sums only feed the optimizer: their partials
+  // get separate buffers and one batched finish at the end, off the chain of
+  // dependent kernels that carries g_x.
   RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(N * D), d.drop_threshold, d.drop_scale,
-                   d.drop_enabled, part, st));
-  RP_TRY(colsum_finish(part, mask_grad_blocks(N, D), D, G.b2, st));
+                   d.drop_enabled, part_b2, st));
   Epi er;
   er.kind = RP_EPI_RELU_GRAD;
   er.resid = tp.h1;
   er.ld_resid = F;
   RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er); },
               [&](Ctx& x) { return mm(x, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32); }));
-  RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, st));
-  RP_TRY(colsum_finish(part, nbc, F, G.b1, st));
+  // b1 partial sums ride with dW1 on the side stream (both only read g_z1)
   RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32); },
-              [&](Ctx& x) { return mm(x, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32); }));
+              [&](Ctx& x) {
+                RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, x.st));
+                return mm(x, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32);
+              }));
   RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
-                       d.drop_threshold, d.drop_scale, d.drop_enabled, pg, pb, N, D, st));
-  RP_TRY(colsum_finish(pg, nbl, D, G.ln2_g, st));
-  RP_TRY(colsum_finish(pb, nbl, D, G.ln2_b, st));
+                       d.drop_threshold, d.drop_scale, d.drop_enabled, pg2, pb2, N, D, st));
   // attention branch (layers.py:234-247)
   RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt); },
               [&](Ctx& x) { return mm(x, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32); }));
@@ -394,9 +400,10 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_qkv, N, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, N, D, D), RP_F32); },
               [&](Ctx& x) { return mm(x, mat(tp.a, N, D, D), true, mat(g_qkv, N, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32); }));
   RP_TRY(layernorm_bwd(dt, g_a, x, tp.mean1, tp.rstd1, w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
-  RP_TRY(colsum_finish(pg, nbl, D, G.ln1_g, st));
-  RP_TRY(colsum_finish(pb, nbl, D, G.ln1_b, st));
-  return RP_OK;
+  const ColsumJob jobs[6] = {{part_b2, mask_grad_blocks(N, D), D, G.b2}, {part, nbc, F, G.b1},
+                             {pg2, nbl, D, G.ln2_g}, {pb2, nbl, D, G.ln2_b},
+                             {pg, nbl, D, G.ln1_g}, {pb, nbl, D, G.ln1_b}};
+  return colsum_finish_multi(jobs, 6, st);
 }
 
 // ---------------------------------------------------------------------------

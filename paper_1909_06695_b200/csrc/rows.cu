@@ -364,6 +364,29 @@ __global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __rest
   }
 }
 
+// Several colsum finishes in one launch (same per-column order as
+// colsum_finish_kernel, so results are bitwise identical): CTA x covers 32
+// columns of the job whose column-block range contains x.
+__global__ void __launch_bounds__(1024) colsum_finish_multi_kernel(ColsumJobs jobs) {
+  __shared__ float red[32][33];
+  int jb = 0;
+  while (jb + 1 < jobs.n && (int)blockIdx.x >= jobs.first_block[jb + 1]) ++jb;
+  const ColsumJob& J = jobs.job[jb];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = (int64_t)(blockIdx.x - jobs.first_block[jb]) * 32 + tx;
+  float s = 0.f;
+  if (j < J.cols)
+    for (int b = ty; b < J.nblk; b += 32) s += J.part[(int64_t)b * J.cols + j];
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < J.cols) {
+    float t = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) t += red[q][tx];
+    J.out[j] = t;
+  }
+}
+
 // Column partial sums of a [rows, cols] matrix (row-major, ld).
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
@@ -560,6 +583,21 @@ int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStr
   if (cols == 0) return RP_OK;
   colsum_finish_kernel<<<(int)((cols + 31) / 32), 1024, 0, st>>>(part, nblk, cols, out);
   return check_launch("colsum_finish");
+}
+
+int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st) {
+  if (n < 1 || n > kMaxColsumJobs) return set_error(RP_ERR_INVALID, "colsum_finish_multi: 1..%d jobs", kMaxColsumJobs);
+  ColsumJobs J{};
+  J.n = n;
+  int blocks = 0;
+  for (int i = 0; i < n; ++i) {
+    J.job[i] = jobs[i];
+    J.first_block[i] = blocks;
+    blocks += (int)((jobs[i].cols + 31) / 32);
+  }
+  if (blocks == 0) return RP_OK;
+  colsum_finish_multi_kernel<<<blocks, 1024, 0, st>>>(J);
+  return check_launch("colsum_finish_multi");
 }
 
 int mask_grad_blocks(int64_t rows, int64_t d) {

@@ -28,6 +28,20 @@ int colsum_blocks(int64_t rows);
 int mask_grad_blocks(int64_t rows, int64_t d);
 int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st);
 int colsum_finish(const float* part, int nblk, int64_t cols, float* out, cudaStream_t st);
+struct ColsumJob {
+  const float* part;
+  int nblk;
+  int64_t cols;
+  float* out;
+};
+constexpr int kMaxColsumJobs = 8;
+struct ColsumJobs {
+  ColsumJob job[kMaxColsumJobs];
+  int first_block[kMaxColsumJobs];
+  int n;
+};
+// up to kMaxColsumJobs colsum_finish operations in one launch (bitwise equal)
+int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st);
 int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
               uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st);
 int softmax_causal(int dtype, const float* s, void* p, int64_t rows, int64_t Tn, int64_t ld, cudaStream_t st);
