@@ -24,7 +24,8 @@ def main(path, step_marker="embed_fwd_kernel"):
     us = [float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1.0) for d in data]
     # one full step = launches between two embedding forwards
     starts = [i for i, d in enumerate(data) if step_marker in d["Kernel Name"]]
-    lo, hi = (starts[0], starts[1]) if len(starts) >= 2 else (0, len(data))
+    # the last complete window: steady state (earlier ones include warm-up allocations)
+    lo, hi = (starts[-2], starts[-1]) if len(starts) >= 2 else (0, len(data))
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d, t in zip(data[lo:hi], us[lo:hi]):
         name = d["Kernel Name"].split("(")[0][:60]
