@@ -227,7 +227,7 @@ class PipelineEngine:
             start = end + (self.costs.relay if m.index < self.K else 0.0)
         return cur, start
 
-    def _backward_one(self, t, k, coef, B, T):
+    def _backward_one(self, t, k, coef, B, T, after_head=None):
         m = self.modules[k - 1]
         s = t - self.K + k
         if s < 0:
@@ -244,7 +244,8 @@ class PipelineEngine:
         g_in = self._bbuf(k - 1, t & 1, B * T, m.d) if k > 1 else None
         alpha, beta = coef
         emb = (alpha if m.has_projection else 0.0, beta if m.has_embedding else 0.0, self.stack.tied_store.grad)
-        m.recompute_backward(slot, grad_out, self.stale_weights, self.train, g_in=g_in, emb=emb, live_step=t)
+        m.recompute_backward(slot, grad_out, self.stale_weights, self.train, g_in=g_in, emb=emb, live_step=t,
+                             after_head=after_head)
         return g_in, slot.sample_id
 
     def _backward_all(self, t, B, T):
@@ -350,6 +351,10 @@ class ConcurrentPipelineEngine(PipelineEngine):
 
         self.side_ctas = int(os.environ.get("RP_SIDE_CTAS", "0"))
         self._bwd_done = {}
+        # the tied matrix's optimizer update runs on its own stream as soon as
+        # both gradient halves are in, beside module K's block backwards
+        self._ts = torch.cuda.Stream(device=self.device, priority=0)
+        self.split_optimizer = os.environ.get("RP_SPLIT_OPT", "1") != "0"
 
     def step(self, t, batch, optimizer=None, sync=True):
         if t < 0:
@@ -391,6 +396,11 @@ class ConcurrentPipelineEngine(PipelineEngine):
         results = {}
         bwd_done = {}
         order = list(range(self.K - 1, 0, -1)) + [self.K]
+        split = self.split_optimizer and optimizer is not None and hasattr(optimizer, "apply_module")
+        if split:
+            optimizer.prepare(self.modules)
+        tied_done = None
+        opt_done = []
         for k in order:
             m = self.modules[k - 1]
             s = self._bs[k - 1]
@@ -404,22 +414,42 @@ class ConcurrentPipelineEngine(PipelineEngine):
             from . import layers as _LY
 
             _LY.CTA_BUDGET["value"] = self.side_ctas if k < self.K else 0
+            after_head = None
+            if split and k == self.K:
+                def after_head(s=s):
+                    # both tied halves are in (module K waited for module 1):
+                    # update V beside the remaining block backwards
+                    nonlocal tied_done
+                    head_ev = torch.cuda.Event()
+                    head_ev.record(s)
+                    self._ts.wait_event(head_ev)
+                    with torch.cuda.stream(self._ts):
+                        optimizer.apply_tied(t, self.stack.tied_store, self.runtime.flag)
+                        tied_done = torch.cuda.Event()
+                        tied_done.record(self._ts)
             try:
                 with torch.cuda.stream(s):
-                    results[k] = self._backward_one(t, k, coef, B, T)
-                    ev = torch.cuda.Event()
+                    results[k] = self._backward_one(t, k, coef, B, T, after_head=after_head)
+                    ev = torch.cuda.Event()  # gradients (and the boundary) of module k are in
                     ev.record(s)
+                    if split:
+                        optimizer.apply_module(t, self.modules[k - 1])
+                        done = torch.cuda.Event()
+                        done.record(s)
+                        opt_done.append(done)
             finally:
                 _LY.CTA_BUDGET["value"] = 0
             bwd_done[k] = ev
         self._bwd_done = bwd_done
-        for ev in fwd_done + list(bwd_done.values()):
+        for ev in fwd_done + list(bwd_done.values()) + opt_done + ([tied_done] if tied_done is not None else []):
             main.wait_event(ev)
         packet = self._assemble(t, results, loss_dev)
         relay_end = self.clock + sum(self.costs.fwd) + self.costs.relay * (self.K - 1)
         self._advance_clock(t, results, relay_end)
-        if optimizer is not None:
+        if optimizer is not None and not split:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
+        elif split and tied_done is None:
+            optimizer.apply_tied(t, self.stack.tied_store, self.runtime.flag)
         # the next step's side streams order themselves after this step's
         # optimizer through start_ev / zero_ev (recorded on the main stream),
         # so no trailing fork is left open (CUDA-graph capture needs joins)

@@ -692,7 +692,7 @@ class ModuleState:
         return self.slots.popleft()
 
     def recompute_backward(self, slot, grad_out, stale_mode="snapshot", train=True, *, g_in=None, emb=None,
-                           live_step=None):
+                           live_step=None, after_head=None):
         """Delayed backward for one slot (model.py:250-293).
 
         "snapshot": gradients at the weights the slot's forward used (the
@@ -737,6 +737,8 @@ class ModuleState:
             LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
                              emb_alpha, ws, vo_accumulate=emb is not None)
             loss = arena.head.loss
+            if after_head is not None:
+                after_head()  # the tied gradient's output half is complete
         else:
             if grad_out is None:
                 raise ScheduleViolation(f"module {self.index} missing boundary gradient")

@@ -52,17 +52,35 @@ def _targets(module, t):
 
 
 class _Base:
-    def _each(self, t, modules, tied, fn):
-        flag = None
+    """`apply` = `apply_module` for every module + `apply_tied`.  The split
+    form lets the concurrent executor update a module as soon as its own
+    delayed backward is done, and the tied matrix as soon as both of its
+    gradient halves are in (each parameter is still updated exactly once per
+    step with the packet's gradient)."""
+
+    def apply(self, t, packet, modules, tied):
+        self.prepare(modules)
         for m in modules:
-            flag = m.runtime.flag
-            for st, (vec_dst, mat_dst) in zip(m.storage, _targets(m, t)):
-                n = st.master.numel()
-                if n == 0:
-                    continue
-                fn(st, 0, st.n_vec, vec_dst)
-                fn(st, st.n_vec, n, mat_dst)
-        return flag
+            self.apply_module(t, m)
+        if tied is not None:
+            self.apply_tied(t, _tied_store(modules), modules[0].runtime.flag)
+        return self.schedule.at(t)
+
+    def prepare(self, modules):
+        pass
+
+    def apply_module(self, t, module):
+        flag = module.runtime.flag
+        for st, (vec_dst, mat_dst) in zip(module.storage, _targets(module, t)):
+            n = st.master.numel()
+            if n == 0:
+                continue
+            self._update(t, st, 0, st.n_vec, vec_dst, flag)
+            self._update(t, st, st.n_vec, n, mat_dst, flag)
+
+    def apply_tied(self, t, store, flag):
+        copy = None if store.compute is store.master else store.compute
+        self._update(t, store, 0, store.master.numel(), copy, flag)
 
 
 class SgdOptimizer(_Base):
@@ -71,20 +89,9 @@ class SgdOptimizer(_Base):
     def __init__(self, schedule):
         self.schedule = schedule
 
-    def apply(self, t, packet, modules, tied):
-        lr = self.schedule.at(t)
-        flag = _flag_of(modules)
-
-        def fn(st, lo, hi, dst):
-            if hi > lo:
-                ops.sgd_step(st.master[lo:hi], st.grad[lo:hi], dst, hi - lo, lr, flag)
-
-        self._each(t, modules, tied, fn)
-        if tied is not None:
-            store = _tied_store(modules)
-            copy = None if store.compute is store.master else store.compute
-            ops.sgd_step(store.master, store.grad, copy, store.master.numel(), lr, _flag_of(modules))
-        return lr
+    def _update(self, t, st, lo, hi, dst, flag):
+        if hi > lo:
+            ops.sgd_step(st.master[lo:hi], st.grad[lo:hi], dst, hi - lo, self.schedule.at(t), flag)
 
     def state_arrays(self):
         return {}
@@ -110,28 +117,18 @@ class AdamOptimizer(_Base):
             obj.v = torch.zeros_like(obj.master)
         return obj.m, obj.v
 
-    def apply(self, t, packet, modules, tied):
-        lr = self.schedule.at(t)
-        c1 = 1.0 - self.beta1 ** (t + 1)
-        c2 = 1.0 - self.beta2 ** (t + 1)
-        flag = _flag_of(modules)
+    def prepare(self, modules):
         if list(modules) != self._mods:
             self.bind(modules)
 
-        def fn(st, lo, hi, dst):
-            if hi > lo:
-                m, v = self._moments(st)
-                ops.adam_step(st.master[lo:hi], st.grad[lo:hi], m[lo:hi], v[lo:hi], dst, hi - lo, lr, self.beta1,
-                              self.beta2, self.eps, c1, c2, flag)
-
-        self._each(t, modules, tied, fn)
-        if tied is not None:
-            store = _tied_store(modules)
-            m, v = self._moments(store)
-            copy = None if store.compute is store.master else store.compute
-            ops.adam_step(store.master, store.grad, m, v, copy, store.master.numel(), lr, self.beta1, self.beta2,
-                          self.eps, c1, c2, flag)
-        return lr
+    def _update(self, t, st, lo, hi, dst, flag):
+        if hi > lo:
+            lr = self.schedule.at(t)
+            c1 = 1.0 - self.beta1 ** (t + 1)
+            c2 = 1.0 - self.beta2 ** (t + 1)
+            m, v = self._moments(st)
+            ops.adam_step(st.master[lo:hi], st.grad[lo:hi], m[lo:hi], v[lo:hi], dst, hi - lo, lr, self.beta1,
+                          self.beta2, self.eps, c1, c2, flag)
 
     def bind(self, modules):
         """Attach the modules whose moments `state_arrays` /
