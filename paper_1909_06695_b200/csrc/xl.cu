@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __re
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kWarps + warp;
   if (row >= rows) return;
-  float* gs_row = sh_gs + warp * (128 * NG);
+  // one padding float per 32: the stride-4 lane pattern of both the stores
+  // and the shifted reads then hits 32 distinct banks
+  float* gs_row = sh_gs + warp * (132 * NG);
   const int i = (int)(row % Tn);
   const int lo = M - mem_len, hi = M + i, off = Tn - 1 - i;
   const float* g = gp + row * lds;
@@ -292,7 +294,8 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __re
     float o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) o[k] = pv[q][k] * (gv[q][k] - dot) * scale;
-    *reinterpret_cast<float4*>(gs_row + j0) = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gs_row[j0 + k + ((j0 + k) >> 5)] = o[k];
     if (j0 < ldp) V4x<T>::st(ga + j0, o);
   }
   __syncwarp();
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __re
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = p0 + k - off;
-      o[k] = (j >= 0 && j < 128 * NG) ? gs_row[j] : 0.f;
+      o[k] = (j >= 0 && j < 128 * NG) ? gs_row[j + (j >> 5)] : 0.f;
     }
     V4x<T>::st(gb + p0, o);
   }
@@ -466,7 +469,7 @@ int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64
 #define XL_BWD(NGV)                                                                                   \
   case NGV: {                                                                                         \
     constexpr int NG = NGV;                                                                           \
-    const size_t smem = sizeof(float) * kWarps * 128 * NG;                                            \
+    const size_t smem = sizeof(float) * kWarps * 132 * NG;                                            \
     XL_DTYPE(dtype, {                                                                                 \
       if (smem > 48 * 1024)                                                                           \
         cudaFuncSetAttribute(softmax_bwd_kernel<T, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
