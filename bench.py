@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Ouroboros training throughput on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c3|c5]
+                  [--mode replicas|ouroboros] [--no-cpu] [--no-compare-k1]
 
 A "step" is one Ouroboros training step (reference PipelineEngine.step,
 engine.py:246-259): relay forward of one batch through all K modules, every
@@ -478,7 +479,8 @@ def main():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "ouroboros"],
                     help="N>1: independent K=2 replicas per GPU (default) or the multi-GPU Ouroboros pipeline")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--compare-k1", action="store_true")
+    ap.add_argument("--no-compare-k1", dest="compare_k1", action="store_false",
+                    help="skip the K=1 backprop run that gives speedup_vs_k1 (BASELINE metric, second half)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.config]
