@@ -259,6 +259,65 @@ int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, 
                      const float* lse, float* g_x, float* vo, float vo_alpha, int32_t vo_accumulate,
                      void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---- module-level entry points: ModuleState.forward / recompute_backward -----
+ * (model.py:224-304).  One call runs a module's contiguous layer slice --
+ * optional embedding, n_blocks transformer blocks, optional projection + loss
+ * -- over caller-owned weights (the ring snapshot of the slot's step) and the
+ * slot's device storage.  The host keeps the schedule bookkeeping (rings,
+ * slot queue, boundary hand-off), exactly as the reference keeps it in
+ * ModuleState / PipelineEngine. */
+typedef struct rp_module_desc {
+  int64_t B, T, d, f, vocab;
+  int64_t t_max;            /* rows of the embedding position table */
+  int32_t n_blocks, has_embedding, has_projection;
+  int32_t dtype;            /* rp_dtype of activations / matrix weights */
+  int32_t max_ctas;         /* SM budget of every GEMM (0 = whole GPU) */
+  int32_t drop_enabled;     /* train && p > 0 */
+  uint64_t drop_threshold;  /* ceil(p * 2^53) */
+  float drop_scale;         /* 1 / (1 - p) */
+  const uint64_t* layer_seeds; /* host array, one per layer of the slice: mix64(dropout_seed, step, layer) */
+} rp_module_desc;
+
+typedef struct rp_module_weights {
+  const rp_block_weights* blocks; /* host array [n_blocks] */
+  const void* tied;               /* compute copy of the tied matrix [vocab, d] */
+  const void* pos;                /* embedding position table [t_max, d] (dtype) */
+} rp_module_weights;
+
+/* one stale slot (model.py:162-168): acts[j] = input of block j (acts[0] is
+ * written by the embedding or by the upstream module), acts[n_blocks] = head
+ * input when has_projection */
+typedef struct rp_module_slot {
+  const int64_t* tokens;       /* [B, T] (embedding modules) */
+  const int64_t* targets;      /* [B*T]  (projection modules) */
+  void* const* acts;           /* host array [n_blocks + has_projection] of [B*T, d] (dtype) */
+  const rp_block_tape* tapes;  /* host array [n_blocks] */
+  float* lse;                  /* [B*T] head log-sum-exp (projection) */
+  float* loss;                 /* 0-d mean cross entropy (projection) */
+  double* loss64;
+} rp_module_slot;
+
+typedef struct rp_module_grads {
+  const rp_block_grads* blocks; /* host array [n_blocks], overwritten */
+  float* pos;                   /* embedding position-table gradient, overwritten */
+  float* tied;                  /* tied gradient [vocab, d] (fp32) or NULL */
+  float tied_alpha;             /* output half: tied (+)= alpha * dV_out (skipped when 0) */
+  float tied_beta;              /* input half:  tied  += beta * dV_in   (skipped when 0) */
+  int32_t tied_accumulate;      /* 1: add the output half onto tied; 0: overwrite */
+} rp_module_grads;
+
+int64_t rp_module_workspace_bytes(const rp_module_desc* desc);
+/* forward at the given weights; `out` receives the last block's output when
+ * the module has no projection (the downstream module's input buffer) */
+int rp_module_forward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot, void* out,
+                      void* workspace, int64_t workspace_bytes, int32_t* flag, void* stream);
+/* delayed backward from the slot's stored intermediates; g_out = boundary
+ * gradient dL/d(output) (fp32, NULL for projection modules); g_in (may be
+ * NULL) receives dL/d(input) for non-embedding modules */
+int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot,
+                       const float* g_out, float* g_in, const rp_module_grads* grads, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

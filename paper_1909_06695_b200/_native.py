@@ -89,6 +89,29 @@ class HeadDesc(ctypes.Structure):
                 ("dtype", ctypes.c_int32)]
 
 
+class ModuleDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("d", ctypes.c_int64), ("f", ctypes.c_int64),
+                ("vocab", ctypes.c_int64), ("t_max", ctypes.c_int64), ("n_blocks", ctypes.c_int32),
+                ("has_embedding", ctypes.c_int32), ("has_projection", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("max_ctas", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_threshold", ctypes.c_uint64),
+                ("drop_scale", ctypes.c_float), ("layer_seeds", ctypes.POINTER(ctypes.c_uint64))]
+
+
+class ModuleWeights(ctypes.Structure):
+    _fields_ = [("blocks", ctypes.POINTER(BlockWeights)), ("tied", ctypes.c_void_p), ("pos", ctypes.c_void_p)]
+
+
+class ModuleSlot(ctypes.Structure):
+    _fields_ = [("tokens", ctypes.c_void_p), ("targets", ctypes.c_void_p), ("acts", ctypes.POINTER(ctypes.c_void_p)),
+                ("tapes", ctypes.POINTER(BlockTape)), ("lse", ctypes.c_void_p), ("loss", ctypes.c_void_p),
+                ("loss64", ctypes.c_void_p)]
+
+
+class ModuleGrads(ctypes.Structure):
+    _fields_ = [("blocks", ctypes.POINTER(BlockGrads)), ("pos", ctypes.c_void_p), ("tied", ctypes.c_void_p),
+                ("tied_alpha", ctypes.c_float), ("tied_beta", ctypes.c_float), ("tied_accumulate", ctypes.c_int32)]
+
+
 def lib():
     """The loaded library; raises ImportError when it is absent."""
     global _lib
@@ -139,6 +162,11 @@ def _declare(L):
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],
         "rp_xl_bias_grad": [vp, vp, vp, vp, vp, i32, i64, i32, vp],
+        "rp_module_workspace_bytes": [ctypes.POINTER(ModuleDesc)],
+        "rp_module_forward": [ctypes.POINTER(ModuleDesc), ctypes.POINTER(ModuleWeights), ctypes.POINTER(ModuleSlot),
+                              vp, vp, i64, vp, vp],
+        "rp_module_backward": [ctypes.POINTER(ModuleDesc), ctypes.POINTER(ModuleWeights),
+                               ctypes.POINTER(ModuleSlot), vp, vp, ctypes.POINTER(ModuleGrads), vp, i64, vp],
         "rp_block_workspace_bytes": [ctypes.POINTER(BlockDesc)],
         "rp_block_forward": [ctypes.POINTER(BlockDesc), ctypes.POINTER(BlockWeights), vp, vp,
                              ctypes.POINTER(BlockTape), vp, i64, vp, vp],
@@ -156,6 +184,7 @@ def _declare(L):
     L.rp_embed_bwd_workspace_bytes.restype = i64
     L.rp_xl_bias_grad_workspace_bytes.restype = i64
     L.rp_block_workspace_bytes.restype = i64
+    L.rp_module_workspace_bytes.restype = i64
     L.rp_head_workspace_bytes.restype = i64
 
 

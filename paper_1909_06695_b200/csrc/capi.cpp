@@ -159,6 +159,16 @@ int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, floa
   return rp::xl_bias_grad(g_qu, g_qv, workspace, g_r_w_bias, g_r_r_bias, H, R, dh, RP_S(stream));
 }
 
+int64_t rp_module_workspace_bytes(const rp_module_desc* desc) { return rp::module_workspace_bytes(*desc); }
+int rp_module_forward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot, void* out,
+                      void* workspace, int64_t workspace_bytes, int32_t* flag, void* stream) {
+  return rp::module_forward(*desc, *w, *slot, out, workspace, workspace_bytes, flag, RP_S(stream));
+}
+int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot,
+                       const float* g_out, float* g_in, const rp_module_grads* grads, void* workspace,
+                       int64_t workspace_bytes, void* stream) {
+  return rp::module_backward(*desc, *w, *slot, g_out, g_in, *grads, workspace, workspace_bytes, RP_S(stream));
+}
 int64_t rp_block_workspace_bytes(const rp_block_desc* desc) { return rp::block_workspace_bytes(*desc); }
 int rp_block_forward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, void* out,
                      const rp_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,

@@ -93,4 +93,10 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
                   float* g_x, float* vo, float vo_alpha, int vo_accumulate, void* ws, int64_t ws_bytes,
                   cudaStream_t st);
 
+int64_t module_workspace_bytes(const rp_module_desc& m);
+int module_forward(const rp_module_desc& m, const rp_module_weights& w, const rp_module_slot& s, void* out,
+                   void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);
+int module_backward(const rp_module_desc& m, const rp_module_weights& w, const rp_module_slot& s, const float* g_out,
+                    float* g_in, const rp_module_grads& G, void* ws, int64_t ws_bytes, cudaStream_t st);
+
 }  // namespace rp
