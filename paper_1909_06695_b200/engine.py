@@ -498,13 +498,16 @@ class SequentialRunner(PipelineEngine):
         return packet, loss
 
 
-def sequential_gradients(stack, batch, dropout_seed, step, train=True):
+def sequential_gradients(stack, batch, dropout_seed, step, train=True, module=None):
     """Full backprop at the stack's current weights without touching them:
-    returns (grads by key as host fp64 arrays, grad_vi, grad_vo, loss)."""
+    returns (grads by key as host fp64 arrays, grad_vi, grad_vo, loss).
+    `module`: a K=1 module of `stack` to reuse across calls -- it carries the
+    Transformer-XL segment memory from one segment to the next."""
     from .model import build_modules, partition
 
-    part = partition(stack.num_layers, 1)
-    (m,) = build_modules(stack, part, dropout_seed)
+    if module is None:
+        (module,) = build_modules(stack, partition(stack.num_layers, 1), dropout_seed)
+    m = module
     m.snapshot(step)
     x = _to_device_tokens(batch.x, stack.runtime.device)
     y = _to_device_tokens(batch.y, stack.runtime.device)

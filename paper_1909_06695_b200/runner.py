@@ -379,6 +379,9 @@ def _load_masters(stack, snap):
 
 
 def _twin_stack(cfg, vocab, dtype=None):
+    if cfg.n_heads:
+        return build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
+                              cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=dtype or cfg.dtype)
     return build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p, cfg.seed_init,
                        dtype=dtype or cfg.dtype)
 
@@ -461,7 +464,8 @@ def _k1_bitwise_check(cfg, steps=20):
     """The pipeline engine at K=1 against the sequential runner, bitwise
     (reference runner.py:394-421)."""
     tokens, vocab = load_corpus(cfg.data, cfg.vocab_mode)
-    source = BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data)
+    source = (SegmentStream(tokens, cfg.seq_len, cfg.batch_size) if cfg.n_heads
+              else BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data))
     runs = []
     for sequential in (False, True):
         stack = _twin_stack(cfg, vocab)
@@ -533,12 +537,21 @@ def verify(cfg, steps=50):
 
     twin = _twin_stack(cfg, runtime.vocab_size)
     cache = {}
+    twin_module = None
+    if cfg.n_heads:
+        # XL: the memory of segment s is the layer input of segment s-1 at
+        # w^{s-1}; a persistent K=1 twin replayed in step order carries it
+        (twin_module,) = build_modules(twin, partition(twin.num_layers, 1), cfg.seed_dropout)
 
     def oracle(s):
         if s not in cache:
             _load_masters(twin, snapshots[s])
-            cache[s] = sequential_gradients(twin, batches[s], cfg.seed_dropout, s)
+            cache[s] = sequential_gradients(twin, batches[s], cfg.seed_dropout, s, module=twin_module)
         return cache[s]
+
+    if twin_module is not None:
+        for s in range(steps):
+            oracle(s)
 
     deviations, emb_deviations = [], []
     zero_pad_ok = True

@@ -135,3 +135,11 @@ def test_xl_train_halt_and_resume_is_bit_exact(in_gold, tmp_path, mode):
     assert any(k.startswith("m1.mem.") for k in x) and sorted(x) == sorted(y)
     for k in x:
         np.testing.assert_array_equal(x[k], y[k], err_msg=k)
+
+
+def test_verify_xl_passes_exactly(in_gold, tmp_path):
+    """verify on a Transformer-XL run: the twin K=1 replay carries the segment
+    memory, so every delayed gradient still matches exactly."""
+    report = R.verify(cfg_for(tmp_path, n_heads=2, mem_len=16, k=3), steps=8)
+    assert report["passed"], report
+    assert report["oracle_max_abs"] == 0.0 and report["emb_max_abs"] == 0.0
