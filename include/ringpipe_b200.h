@@ -193,6 +193,14 @@ int rp_adam_step(float* w, const float* g, float* m, float* v, void* copy, int32
 int rp_sgd_step(float* w, const float* g, void* copy, int32_t copy_dtype, int64_t n, float lr, int32_t* flag,
                 void* stream);
 
+/* ---- mixed tied gradient (engine.py:54-69) ---------------------------------
+ * out = 1/2 vo + 1/2 vi (convention 0, "half_avg") or vo + vi (1, "sum");
+ * zeros while t-K+1 < 0 (vi must then be NULL: RP_ERR_SCHEDULE otherwise, and
+ * when it is missing later).  The engines fuse this into the head / embedding
+ * backward epilogues; this is the standalone form of the reference function. */
+int rp_embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, float* out, int64_t n,
+                          int32_t convention, void* stream);
+
 /* ---- misc ----------------------------------------------------------------- */
 /* uniform_signed init from the reference stream (tensor.py:72-74), fp64 math, fp32 out */
 int rp_init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, void* stream);

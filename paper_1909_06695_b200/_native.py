@@ -153,6 +153,7 @@ def _declare(L):
         "rp_sgd_step": [vp, vp, vp, i32, i64, f32, vp, vp],
         "rp_init_uniform": [vp, i64, u64, u64, f64, vp],
         "rp_cast": [vp, i32, vp, i32, i64, vp],
+        "rp_embedding_gradient": [i64, i64, vp, vp, vp, i64, i32, vp],
         "rp_sq_norm": [vp, i64, vp, vp, i32, vp],
         "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
         "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, vp],

@@ -120,6 +120,10 @@ int rp_sgd_step(float* w, const float* g, void* copy, int32_t copy_dtype, int64_
 int rp_init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, void* stream) {
   return rp::init_uniform(out, n, seed, pos0, scale, RP_S(stream));
 }
+int rp_embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, float* out, int64_t n,
+                          int32_t convention, void* stream) {
+  return rp::embedding_gradient(t, K, vo, vi, out, n, convention, RP_S(stream));
+}
 int rp_cast(const void* in, int32_t in_dtype, void* out, int32_t out_dtype, int64_t n, void* stream) {
   return rp::cast(in, in_dtype, out, out_dtype, n, RP_S(stream));
 }

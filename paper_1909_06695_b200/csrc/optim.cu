@@ -86,6 +86,13 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, T
   if (!finite && flag) atomicOr(flag, RP_FLAG_NONFINITE);
 }
 
+// Mixed tied gradient (reference engine.py:54-69): out = a*vo + b*vi.
+__global__ void axpby_kernel(const float* __restrict__ x, float a, const float* __restrict__ y, float b,
+                             float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (x ? a * x[i] : 0.f) + (y ? b * y[i] : 0.f);
+}
+
 // out[i] = ((bits53(seed, pos0 + i) * 2^-53) * 2 - 1) * scale, evaluated in
 // fp64 exactly as the reference's uniform_signed, then rounded to fp32.
 __global__ void init_uniform_kernel(float* __restrict__ out, int64_t n, uint64_t seed, uint64_t pos0, double scale) {
@@ -161,6 +168,18 @@ int sgd_step(float* w, const float* g, void* copy, int copy_dtype, int64_t n, fl
   else
     sgd_kernel<float><<<grid_for(n), 256, 0, st>>>(w, g, (float*)copy, n, lr, flag);
   return check_launch("sgd");
+}
+
+int embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, float* out, int64_t n,
+                       int convention, cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  if (convention != 0 && convention != 1) return set_error(RP_ERR_INVALID, "unknown tied_grad convention");
+  const bool padded = t - K + 1 < 0;  // the input-side half does not exist yet: a zero packet
+  if (padded && vi) return set_error(RP_ERR_SCHEDULE, "stale embedding gradient before step K-1");
+  if (!padded && !vi) return set_error(RP_ERR_SCHEDULE, "missing stale embedding gradient");
+  const float c = padded ? 0.f : (convention == 0 ? 0.5f : 1.f);
+  axpby_kernel<<<grid_for(n), 256, 0, st>>>(padded ? nullptr : vo, c, vi, c, out, n);
+  return check_launch("embedding_gradient");
 }
 
 int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, cudaStream_t st) {

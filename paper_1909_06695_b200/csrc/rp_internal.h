@@ -61,6 +61,8 @@ int adam_step(float* w, const float* g, float* m, float* v, void* copy, int copy
 int sgd_step(float* w, const float* g, void* copy, int copy_dtype, int64_t n, float lr, int32_t* flag,
              cudaStream_t st);
 int init_uniform(float* out, int64_t n, uint64_t seed, uint64_t pos0, double scale, cudaStream_t st);
+int embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, float* out, int64_t n,
+                       int convention, cudaStream_t st);
 int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st);
 int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
 

@@ -69,7 +69,26 @@ class GradientPacket:
 
 
 def embedding_gradient(t, K, grad_vo_fresh, grad_vi_stale, convention="half_avg"):
-    """Reference engine.py:54-69 on explicit tensors (host or device)."""
+    """Reference engine.py:54-69.  fp32 CUDA tensors go through
+    `rp_embedding_gradient`; host arrays (the reference's own argument type)
+    are combined on the host -- the engines never call this, they fuse the
+    two halves into the head / embedding backward."""
+    if convention not in ("half_avg", "sum"):
+        raise ValueError(f"unknown tied_grad convention {convention!r}")
+    if (torch.is_tensor(grad_vo_fresh) and grad_vo_fresh.is_cuda and grad_vo_fresh.dtype == torch.float32
+            and (grad_vi_stale is None or (torch.is_tensor(grad_vi_stale) and grad_vi_stale.dtype == torch.float32))):
+        from . import _native as N
+        from . import ops
+
+        if grad_vi_stale is not None and tuple(grad_vo_fresh.shape) != tuple(grad_vi_stale.shape):
+            raise DimensionError("embedding gradient shape mismatch")
+        vo = grad_vo_fresh.contiguous()
+        vi = None if grad_vi_stale is None else grad_vi_stale.contiguous()
+        out = torch.empty_like(vo)
+        N.check(N.lib().rp_embedding_gradient(t, K, vo.data_ptr(), None if vi is None else vi.data_ptr(),
+                                              out.data_ptr(), vo.numel(), 0 if convention == "half_avg" else 1,
+                                              ops._stream()), "embedding_gradient")
+        return out
     if t - K + 1 < 0:
         if grad_vi_stale is not None:
             raise ScheduleViolation("stale embedding gradient before step K-1")

@@ -98,3 +98,23 @@ def test_module_abi_rejects_xl_and_empty():
     dsc.B, dsc.T, dsc.d = 1, 1, 8
     assert N.lib().rp_module_forward(dsc, None, None, None, None, 0, None, None) != 0
     assert np.isscalar(N.lib().rp_module_workspace_bytes(dsc))
+
+
+def test_embedding_gradient_kernel_matches_reference_rule():
+    """rp_embedding_gradient vs the reference rule (engine.py:54-69)."""
+    from paper_1909_06695_b200.engine import embedding_gradient
+    from paper_1909_06695_b200.errors import ScheduleViolation
+
+    dev = torch.device("cuda")
+    vo = torch.rand(7, 8, device=dev) - 0.5
+    vi = torch.rand(7, 8, device=dev) - 0.5
+    for conv, c in (("half_avg", 0.5), ("sum", 1.0)):
+        got = embedding_gradient(5, 3, vo, vi, conv)
+        assert torch.equal(got, c * vo + c * vi)
+        host = embedding_gradient(5, 3, vo.cpu().numpy(), vi.cpu().numpy(), conv)
+        np.testing.assert_array_equal(got.cpu().numpy(), host)
+    assert not embedding_gradient(0, 3, vo, None).any()
+    with pytest.raises(ScheduleViolation):
+        embedding_gradient(0, 3, vo, vi)
+    with pytest.raises(ScheduleViolation):
+        embedding_gradient(4, 3, vo, None)
