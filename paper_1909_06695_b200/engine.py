@@ -246,7 +246,7 @@ class PipelineEngine:
             start = end + (self.costs.relay if m.index < self.K else 0.0)
         return cur, start
 
-    def _backward_one(self, t, k, coef, B, T, after_head=None):
+    def _backward_one(self, t, k, coef, B, T, after_head=None, before_embedding=None, vo_overwrite=False):
         m = self.modules[k - 1]
         s = t - self.K + k
         if s < 0:
@@ -264,7 +264,7 @@ class PipelineEngine:
         alpha, beta = coef
         emb = (alpha if m.has_projection else 0.0, beta if m.has_embedding else 0.0, self.stack.tied_store.grad)
         m.recompute_backward(slot, grad_out, self.stale_weights, self.train, g_in=g_in, emb=emb, live_step=t,
-                             after_head=after_head)
+                             after_head=after_head, before_embedding=before_embedding, vo_overwrite=vo_overwrite)
         return g_in, slot.sample_id
 
     def _backward_all(self, t, B, T):
@@ -349,9 +349,11 @@ class ConcurrentPipelineEngine(PipelineEngine):
     """Same schedule with per-module CUDA streams.
 
     fwd(k,t) waits fwd(k-1,t); bwd(k,t) waits bwd(k+1,t-1) (its boundary) and,
-    for k=K, fwd(K,t); the optimizer waits every fwd/bwd of step t; fwd(k,t+1)
-    waits the optimizer.  Modules 1 and K add their tied-gradient halves onto
-    a zeroed buffer one after the other (module K after module 1).
+    for k=K, fwd(K,t); module k's optimizer update follows its own backward;
+    fwd(k,t+1) waits every update of step t.  Module K writes the tied
+    gradient's output half and module 1's embedding scatter adds the input
+    half after it (bitwise the reference executor's sum), so module K's
+    backward -- the critical path -- never waits for module 1.
     """
 
     def __init__(self, *args, timeout=120.0, **kwargs):
@@ -404,53 +406,61 @@ class ConcurrentPipelineEngine(PipelineEngine):
             fwd_done.append(ev)
             prev = ev
         loss_dev = cur
-        # stale backwards: modules k < K depend only on last step's boundary,
-        # so they start with the step and overlap the relay; module K needs
-        # its fresh forward.  The tied gradient is zeroed first; modules 1 and
-        # K then add their halves in either order (mutually excluded).
+        # Stale backwards.  Modules k < K depend only on last step's boundary,
+        # so they start with the step and overlap the relay; module K needs its
+        # fresh forward.  Tied gradient: module K *writes* its output half
+        # alpha*dV_out (dense, every row) and module 1 then *adds* beta*dV_in
+        # (a scatter into the touched rows) -- fp32 a + b == b + a, so this is
+        # bitwise the reference executor's 0 + a + b, needs no zero fill, and
+        # module K never waits for module 1: only module 1's final embedding
+        # scatter waits for module K's head backward.
         coef = tied_coefficients(t, self.K, self.tied_grad)
-        self.stack.tied_store.grad.zero_()
+        tied_grad = self.stack.tied_store.grad
+        overwrite = coef[0] != 0.0  # module K's head writes every row
+        if not overwrite:
+            tied_grad.zero_()  # warm-up: a zero packet
         zero_ev = torch.cuda.Event()
         zero_ev.record(main)
         results = {}
         bwd_done = {}
-        order = list(range(self.K - 1, 0, -1)) + [self.K]
         split = self.split_optimizer and optimizer is not None and hasattr(optimizer, "apply_module")
         if split:
             optimizer.prepare(self.modules)
-        tied_done = None
         opt_done = []
-        for k in order:
+        head_ev = [None]
+        tied_ready = [None]
+        from . import layers as _LY
+
+        def after_head(s):
+            ev = torch.cuda.Event()
+            ev.record(s)
+            head_ev[0] = ev
+
+        def before_embedding(s):
+            if overwrite and head_ev[0] is not None:
+                s.wait_event(head_ev[0])
+
+        # issue module K first (its head event gates module 1's scatter)
+        for k in [self.K] + list(range(self.K - 1, 0, -1)):
             m = self.modules[k - 1]
             s = self._bs[k - 1]
             s.wait_event(zero_ev)
             if k == self.K:
                 s.wait_event(fwd_done[k - 1])
-                if self.K > 1:
-                    s.wait_event(bwd_done[1])  # exclusive access to the tied gradient
             if (k + 1) in self._bwd_done:
                 s.wait_event(self._bwd_done[k + 1])
-            from . import layers as _LY
-
             _LY.CTA_BUDGET["value"] = self.side_ctas if k < self.K else 0
-            after_head = None
-            if split and k == self.K:
-                def after_head(s=s):
-                    # both tied halves are in (module K waited for module 1):
-                    # update V beside the remaining block backwards
-                    nonlocal tied_done
-                    head_ev = torch.cuda.Event()
-                    head_ev.record(s)
-                    self._ts.wait_event(head_ev)
-                    with torch.cuda.stream(self._ts):
-                        optimizer.apply_tied(t, self.stack.tied_store, self.runtime.flag)
-                        tied_done = torch.cuda.Event()
-                        tied_done.record(self._ts)
             try:
                 with torch.cuda.stream(s):
-                    results[k] = self._backward_one(t, k, coef, B, T, after_head=after_head)
+                    results[k] = self._backward_one(
+                        t, k, coef, B, T,
+                        after_head=(lambda s=s: after_head(s)) if k == self.K else None,
+                        before_embedding=(lambda s=s: before_embedding(s)) if k == 1 else None,
+                        vo_overwrite=overwrite)
                     ev = torch.cuda.Event()  # gradients (and the boundary) of module k are in
                     ev.record(s)
+                    if k == 1:
+                        tied_ready[0] = ev  # both tied halves are in
                     if split:
                         optimizer.apply_module(t, self.modules[k - 1])
                         done = torch.cuda.Event()
@@ -459,6 +469,16 @@ class ConcurrentPipelineEngine(PipelineEngine):
             finally:
                 _LY.CTA_BUDGET["value"] = 0
             bwd_done[k] = ev
+        tied_done = None
+        if split:
+            # the tied update runs beside whatever backward work is left
+            self._ts.wait_event(tied_ready[0])
+            if head_ev[0] is not None:
+                self._ts.wait_event(head_ev[0])
+            with torch.cuda.stream(self._ts):
+                optimizer.apply_tied(t, self.stack.tied_store, self.runtime.flag)
+                tied_done = torch.cuda.Event()
+                tied_done.record(self._ts)
         self._bwd_done = bwd_done
         for ev in fwd_done + list(bwd_done.values()) + opt_done + ([tied_done] if tied_done is not None else []):
             main.wait_event(ev)
@@ -467,8 +487,6 @@ class ConcurrentPipelineEngine(PipelineEngine):
         self._advance_clock(t, results, relay_end)
         if optimizer is not None and not split:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
-        elif split and tied_done is None:
-            optimizer.apply_tied(t, self.stack.tied_store, self.runtime.flag)
         # the next step's side streams order themselves after this step's
         # optimizer through start_ev / zero_ev (recorded on the main stream),
         # so no trailing fork is left open (CUDA-graph capture needs joins)

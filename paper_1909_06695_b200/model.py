@@ -692,7 +692,7 @@ class ModuleState:
         return self.slots.popleft()
 
     def recompute_backward(self, slot, grad_out, stale_mode="snapshot", train=True, *, g_in=None, emb=None,
-                           live_step=None, after_head=None):
+                           live_step=None, after_head=None, before_embedding=None, vo_overwrite=False):
         """Delayed backward for one slot (model.py:250-293).
 
         "snapshot": gradients at the weights the slot's forward used (the
@@ -735,7 +735,7 @@ class ModuleState:
         if self.has_projection:
             g = ws.get("g_stream_a", (Nt, d), torch.float32)
             LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
-                             emb_alpha, ws, vo_accumulate=emb is not None)
+                             emb_alpha, ws, vo_accumulate=emb is not None and not vo_overwrite)
             loss = arena.head.loss
             if after_head is not None:
                 after_head()  # the tied gradient's output half is complete
@@ -762,6 +762,8 @@ class ModuleState:
                 LY.block_backward(W, W, arena.acts[j], arena.tapes[j], g, g_next, st.G, B, T, drop, ws)
             g = g_next
         if self.has_embedding:
+            if before_embedding is not None:
+                before_embedding()  # e.g. order the tied-gradient scatter after the output half
             st = self.storage[0]
             drop = LY.Dropout.make(slot.layer_seeds[0], self.layers[0].dropout_p, train)
             LY.embed_backward(g, arena.tokens, self.layers[0].max_seq_len, st.G["pos"],
