@@ -118,13 +118,23 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
   const int64_t stride = (int64_t)gridDim.x * kRowWarps;
   for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
     const float mu = mean[row], rs = rstd[row];
-    float xh[NG][4], dyv[NG][4];
+    float xh[NG][4], dyv[NG][4], rv[NG][4];
     float s1 = 0.f, s2 = 0.f;
+    // every load of the row is issued up front (the residual gradient too):
+    // one DRAM round trip per row instead of two
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
       V4<T>::ld(x + row * d + j, xh[i]);
       V4<float>::ld(dy + row * d + j, dyv[i]);
+      if (resid_grad) {
+        V4<float>::ld(resid_grad + row * d + j, rv[i]);
+      } else {
+        rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         xh[i][q] = (xh[i][q] - mu) * rs;
@@ -140,14 +150,9 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
-      float o[4], r[4];
-      if (resid_grad) {
-        V4<float>::ld(resid_grad + row * d + j, r);
-      } else {
-        r[0] = r[1] = r[2] = r[3] = 0.f;
-      }
+      float o[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + r[q];
+      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
       V4<float>::st(dx + row * d + j, o);
       if (dx_masked) {
         if (drop_on) {
