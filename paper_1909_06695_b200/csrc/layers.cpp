@@ -230,6 +230,10 @@ bool fork_enabled() {
 
 }  // namespace
 
+int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes) {
+  return choose_splits(M, N, K, 256, cap_bytes);
+}
+
 // ---------------------------------------------------------------------------
 // block
 

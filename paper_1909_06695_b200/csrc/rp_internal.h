@@ -14,6 +14,8 @@ int check_launch(const char* what);
 
 int gemm(const rp_gemm_args& a, cudaStream_t stream);
 int gemm_tile_n(int64_t M, int64_t N, int64_t batch);
+// split count for a batch-1 fp32 GEMM (layers.cpp choose_splits); 1 = no split
+int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes);
 int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, int64_t ldo, cudaStream_t st);
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);

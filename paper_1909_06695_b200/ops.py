@@ -206,9 +206,36 @@ def gemm(
     if target_logit is not None:
         args.target_logit = target_logit.data_ptr()
     args.ce_scale = ce_scale
+    splits = 1
+    if out is not None and out.dtype == torch.float32 and epilogue == N.EPI_STORE and batch == 1:
+        # deterministic split-K for weight-gradient shapes (few tiles, long K),
+        # the same rule and scratch size as the native composites (layers.cpp)
+        splits = N.lib().rp_gemm_choose_splits(M, Nn, K, SPLITK_CAP)
+    if splits > 1:
+        part = _splitk_scratch(out.device)
+        args.k_splits = splits
+        args.C, args.ldc, args.stride_c = part.data_ptr(), Nn, M * Nn
     _count(1)
     N.check(N.lib().rp_gemm(ctypes.byref(args), _stream()), "gemm")
+    if splits > 1:
+        _count(1)
+        N.check(N.lib().rp_splitk_reduce(_ptr(part), splits, M, Nn, _ptr(out), out.stride(-2), _stream()),
+                "splitk_reduce")
     return out
+
+
+SPLITK_CAP = 296 * 128 * 256 * 4  # bytes of split-K partials (= layers.cpp kBlockSplitK)
+_SPLITK = {}
+
+
+def _splitk_scratch(device):
+    """Split-K partials, one buffer per (device, stream): GEMMs on one stream
+    run in order, so they can share it; streams never do."""
+    key = (device, torch.cuda.current_stream().cuda_stream)
+    buf = _SPLITK.get(key)
+    if buf is None:
+        buf = _SPLITK[key] = torch.empty(SPLITK_CAP // 4, dtype=torch.float32, device=device)
+    return buf
 
 
 def gemm_tile_n(n, m=8192, batch=1):
