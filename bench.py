@@ -286,6 +286,12 @@ def run_ours(args, c):
         n_head_launches = 2 * len(head)
         head_flops = 2.0 * tokens * (c["mem"] + T) * c["d"]
         kernel_name = "gemm_kernel<bf16> (XL attention scores AC and BD, 2*B*T*(M+T)*d FLOPs/launch)"
+        if probe.events.get("xl_attn_fwd"):
+            # fused scores + relative shift + softmax: AC and BD in one launch
+            head = probe.events["xl_attn_fwd"]
+            n_head_launches = len(head)
+            head_flops = 4.0 * tokens * (c["mem"] + T) * c["d"]
+            kernel_name = "xl_attn_fwd_kernel (fused XL scores AC+BD + softmax, 4*B*T*(M+T)*d FLOPs/launch)"
     else:
         head = probe.events.get("head_gemm", []) + probe.events.get("head_gemm_bwd", [])
         n_head_launches = len(probe.events.get("head_gemm", [])) + 3 * len(probe.events.get("head_gemm_bwd", []))

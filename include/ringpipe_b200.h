@@ -161,6 +161,11 @@ int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const
 /* P = softmax((AC + relshift(BD)) * scale) over keys M-mem_len <= j <= M+i; rows = H*B*T */
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream);
+/* Fused relative-position scores + softmax (bf16, dh = 64, tcgen05): P [H*B, T, ld_p] from
+ * qu = q+u, qv = q+v [H*B, T, dh], kh [H*B, M+T, dh], r_h [H, M+T, dh]; the same P as
+ * rp_xl_softmax_fwd over the AC / BD GEMM outputs, without materialising them */
+int rp_xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ld_p, int64_t B,
+                   int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len, float scale, void* stream);
 /* dAC = P (dP - <dP,P>) * scale; dBD = the same values un-shifted */
 int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
                       void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,

@@ -155,6 +155,10 @@ int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t l
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream) {
   return rp::xl_softmax_fwd(dtype, ac, bd, ld_scores, probs, ld_p, rows, T, M, mem_len, scale, RP_S(stream));
 }
+int rp_xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ld_p, int64_t B,
+                   int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len, float scale, void* stream) {
+  return rp::xl_attn_fwd(qu, qv, kh, rh, probs, ld_p, B, T, M, H, dh, (int)mem_len, scale, RP_S(stream));
+}
 int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
                       void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,
                       void* stream) {

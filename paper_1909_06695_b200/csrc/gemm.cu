@@ -1013,6 +1013,11 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
 
 }  // namespace
 
+int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
+                 int64_t bstride, int box_inner, int box_rows) {
+  return make_map(map, ptr, false, inner, rows, ld, batch, bstride, box_inner, box_rows, false);
+}
+
 // N tile.  Default: the widest tile (256) whenever N > 128 -- narrower tiles
 // read the A tile from shared memory more often per MMA and measured slower
 // on every block GEMM (tools/prof_block.py: 0.458 vs 0.593 ms per block

@@ -358,6 +358,22 @@ def xl_softmax_fwd(ac, bd, probs, T, M, mem_len, scale):
                                       rows, T, M, mem_len, scale, _stream()), "xl_softmax_fwd")
 
 
+def xl_attn_fwd(qu, qv, kh, rh, probs, B, T, M, mem_len, scale):
+    """Fused scores + softmax (bf16, dh = 64): qu, qv [H*B*T, dh] head-major,
+    kh [H*B*Kl, dh], rh [H*Kl, dh]; probs [H*B, T, ldp]."""
+    _require_cuda(qu, qv, kh, rh, probs)
+    for t in (qu, qv, kh, rh, probs):
+        if t.dtype != torch.bfloat16:
+            raise DimensionError("xl_attn_fwd takes bf16 tensors")
+    for t in (qu, qv, kh, rh):
+        if not t.is_contiguous():
+            raise DimensionError("xl_attn_fwd operands must be contiguous")
+    H, dh = rh.shape[0], rh.shape[-1]
+    _count(1)
+    N.check(N.lib().rp_xl_attn_fwd(_ptr(qu), _ptr(qv), _ptr(kh), _ptr(rh), _ptr(probs), probs.stride(-2), B, T, M,
+                                   H, dh, mem_len, scale, _stream()), "xl_attn_fwd")
+
+
 def xl_softmax_bwd(g_p, probs, g_ac, g_bd, T, M, mem_len, scale):
     _count(1)
     rows = math.prod(probs.shape[:-1])

@@ -15,6 +15,7 @@ softmax and the gradient merges.
 """
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -73,6 +74,15 @@ class XLTape:
         return sum(t.numel() * t.element_size() for t in vars(self).values() if torch.is_tensor(t))
 
 
+FUSED = os.environ.get("RP_XL_FUSED", "1") != "0"
+
+
+def fused_ok(tp):
+    """The fused attention kernels (csrc/xl_attn.cu) take bf16, head dim 64;
+    other shapes and the fp32 check mode use the GEMM + softmax-kernel path."""
+    return FUSED and tp.xa.dtype == torch.bfloat16 and tp.dh == 64
+
+
 def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     """tp.xa holds [memory; x]; writes out [B*T, d] and the tape."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
@@ -85,12 +95,17 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     r = ws.get("xl_r", (Kl, d), cdt)
     ops.gemm(R, W["wr"], b_mn=True, out=r)
     ops.xl_split_heads(r, tp.rh, H, dh)
-    ac = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
-    bd = ws.get("xl_bd", (H, B * T, tp.ldk), torch.float32)[:, :, :Kl]
-    with ops.span("xl_scores"):
-        ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac)
-        ops.gemm(tp.qv, tp.rh, out=bd)
-    ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
+    if fused_ok(tp):
+        # scores + relative shift + masked softmax in one tcgen05 kernel (csrc/xl_attn.cu)
+        with ops.span("xl_attn_fwd"):
+            ops.xl_attn_fwd(tp.qu, tp.qv, tp.kh, tp.rh, tp.probs_buf, B, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
+    else:
+        ac = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
+        bd = ws.get("xl_bd", (H, B * T, tp.ldk), torch.float32)[:, :, :Kl]
+        with ops.span("xl_scores"):
+            ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac)
+            ops.gemm(tp.qv, tp.rh, out=bd)
+        ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
     ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
     ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
     ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
