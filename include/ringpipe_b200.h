@@ -166,6 +166,12 @@ int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t l
  * rp_xl_softmax_fwd over the AC / BD GEMM outputs, without materialising them */
 int rp_xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ld_p, int64_t B,
                    int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len, float scale, void* stream);
+/* Fused backward of rp_xl_attn_fwd's softmax (bf16, dh = 64, tcgen05): dP = g_ctx_h v^T on the tensor
+ * cores, D_i = <g_ctx_i, ctx_i> from the merged [B*T, H*dh] rows, dAC = P (dP - D) * scale and the
+ * un-shifted dBD, both [H*B, T, ld_p]; replaces the dP GEMM + rp_xl_softmax_bwd */
+int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, void* grad_ac, void* grad_bd, int64_t ld_p,
+                   const void* grad_ctx, const void* ctx, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh,
+                   int64_t mem_len, float scale, void* stream);
 /* dAC = P (dP - <dP,P>) * scale; dBD = the same values un-shifted */
 int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
                       void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,

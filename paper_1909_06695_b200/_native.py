@@ -162,6 +162,7 @@ def _declare(L):
         "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
         "rp_xl_softmax_fwd": [i32, vp, vp, i64, vp, i64, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd": [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, i64, f32, vp],
+        "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],
         "rp_xl_bias_grad": [vp, vp, vp, vp, vp, i32, i64, i32, vp],

@@ -813,7 +813,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 // rows x inner matrix (inner contiguous), `batch` copies at `bstride` elements.
 int make_map(CUtensorMap* map, const void* ptr, bool tf32, int64_t inner, int64_t rows, int64_t ld,
-             int64_t batch, int64_t bstride, int box_inner, int box_rows, bool mn_major) {
+             int64_t batch, int64_t bstride, int box_inner, int box_rows, bool mn_major, bool swizzle = true) {
   auto enc = encoder();
   if (!enc) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int e = tf32 ? 4 : 2;
@@ -828,7 +828,8 @@ int make_map(CUtensorMap* map, const void* ptr, bool tf32, int64_t inner, int64_
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                    const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   !swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                   : (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -1014,8 +1015,8 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
 }  // namespace
 
 int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
-                 int64_t bstride, int box_inner, int box_rows) {
-  return make_map(map, ptr, false, inner, rows, ld, batch, bstride, box_inner, box_rows, false);
+                 int64_t bstride, int box_inner, int box_rows, bool swizzle) {
+  return make_map(map, ptr, false, inner, rows, ld, batch, bstride, box_inner, box_rows, false, swizzle);
 }
 
 // N tile.  Default: the widest tile (256) whenever N > 128 -- narrower tiles

@@ -16,7 +16,7 @@ int check_launch(const char* what);
 int gemm(const rp_gemm_args& a, cudaStream_t stream);
 // 3-d bf16 TMA map (128B swizzle): dims {inner, rows, batch}; OOB reads fill zeros
 int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
-                 int64_t bstride, int box_inner, int box_rows);
+                 int64_t bstride, int box_inner, int box_rows, bool swizzle = true);
 int gemm_tile_n(int64_t M, int64_t N, int64_t batch);
 // split count for a batch-1 fp32 GEMM (layers.cpp choose_splits); 1 = no split
 int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes);
@@ -87,6 +87,9 @@ int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64
 // fused XL scores + softmax (xl_attn.cu): bf16, dh = 64
 int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ldp, int64_t B,
                 int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st);
+int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
+                const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
+                float scale, cudaStream_t st);
 int64_t xl_bias_grad_workspace_bytes(int H, int dh);
 int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
                  cudaStream_t st);

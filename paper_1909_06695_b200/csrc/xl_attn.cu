@@ -269,6 +269,274 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// Backward of the scores + softmax: per (head*batch, 128-query tile), per
+// 128-key tile
+//     dP = g_ctx_h v^T                  128 x 128   (TMEM, double-buffered)
+//     dS = P (dP - D) * scale,  D_i = g_ctx_i . ctx_i  (= sum_j P_ij dP_ij)
+// written as dAC (row-aligned, = dS) and as the un-shifted dBD[i, p] =
+// dS[i, p - (T-1-i)].  dBD is assembled in a 4-chunk shared-memory ring in
+// "band" coordinates (row r of key tile n covers band columns
+// 128 n + 127 - r + [0, 128)); after key tile n every row's band chunk n is
+// complete and one TMA bulk store writes it (128 rows x 128 columns), which
+// replaces the fp32 dP GEMM output and the separate softmax-backward pass
+// of the unfused path.
+constexpr int kThreadsBwd = 384;
+constexpr int kGBytes = kQT * kRowBytes;    // g_ctx tile, 16 KB
+constexpr int kVBytes = kKT * kRowBytes;    // v tile, 16 KB
+constexpr int kRingChunk = kQT * 128 * 2;   // 128 rows x 128 band columns bf16 = 32 KB
+constexpr int kRingChunks = 4;
+constexpr int kSmemBwd = 1024 + kGBytes + kStages * kVBytes + kRingChunks * kRingChunk + 128;
+
+struct BwdParams {
+  const __nv_bfloat16* p;  // P [HB, T, ldp]
+  __nv_bfloat16* gac;      // dAC [HB, T, ldp]
+  __nv_bfloat16* gbd;      // dBD [HB, T, ldp] (for the zero margins)
+  const __nv_bfloat16* gctx;  // merged g_ctx [B*T, d]
+  const __nv_bfloat16* ctx;   // merged ctx [B*T, d]
+  int64_t ldp;
+  int B, T, M, Kl, lo, nqt, H, d;
+  float scale;
+};
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+__device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// zero bf16 [a, b) of a row (16-byte stores where aligned)
+__device__ __forceinline__ void zero_row(__nv_bfloat16* row, int64_t a, int64_t b) {
+  const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+  while (a < b && (a & 7)) row[a++] = z;
+  for (; a + 8 <= b; a += 8) *reinterpret_cast<uint4*>(row + a) = make_uint4(0, 0, 0, 0);
+  for (; a < b; ++a) row[a] = z;
+}
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    xl_attn_bwd_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
+                       const __grid_constant__ CUtensorMap mBD, const BwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sG = smem;
+  uint8_t* stages = smem + kGBytes;
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(stages + kStages * kVBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ring) + kRingChunks * kRingChunk);
+  uint64_t* g_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = bars + 3;
+  uint64_t* acc_full = bars + 5;
+  uint64_t* acc_empty = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hb = blockIdx.x / p.nqt, qt = blockIdx.x % p.nqt;
+  const int h = hb / p.B, b = hb % p.B;
+  const int i0 = qt * kQT;
+  const int imax = min(i0 + kQT, p.T) - 1;
+  const int jt_lo = p.lo / kKT, jt_hi = min(p.M + imax, p.Kl - 1) / kKT;
+  const int nt = jt_hi - jt_lo + 1;
+  const int P0 = p.T - kQT - i0 + jt_lo * kKT;  // band column 0 in dBD coordinates
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mG);
+    tma_prefetch(&mV);
+    tma_prefetch(&mBD);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(g_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kSoftWarps * 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(g_full, kGBytes);
+      tma_load_3d(sG, &mG, g_full, 0, i0, hb);
+      for (int n = 0; n < nt; ++n) {
+        const int s = n & 1;
+        mbar_wait(&kv_empty[s], ((n >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[s], kVBytes);
+        tma_load_3d(stages + s * kVBytes, &mV, &kv_full[s], 0, (jt_lo + n) * kKT, hb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(false, false, false, kQT, kKT);
+      const uint32_t ga = smem_u32(sG);
+      mbar_wait(g_full, 0);
+      for (int n = 0; n < nt; ++n) {
+        const int s = n & 1;
+        mbar_wait(&acc_empty[s], ((n >> 1) & 1) ^ 1);
+        mbar_wait(&kv_full[s], (n >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(stages + s * kVBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(tmem_base + s * kKT, umma_desc(ga + 32 * k, 16, 1024), umma_desc(vb + 32 * k, 16, 1024),
+                        idesc, k > 0);
+        tc_commit(&kv_empty[s]);
+        tc_commit(&acc_full[s]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const int i = i0 + r;
+    const bool row_ok = i < p.T;
+    const int jhi = p.M + i;
+    const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    const int64_t rowoff = ((int64_t)hb * p.T + i) * p.ldp;
+    const __nv_bfloat16* prow = p.p + rowoff;
+    __nv_bfloat16* arow = p.gac + rowoff;
+    __nv_bfloat16* brow = p.gbd + rowoff;
+    __nv_bfloat16* myring = ring + r * 128;  // + chunk * 128*128 + column
+    // D_i = g_ctx_i . ctx_i over this head's 64 columns
+    float D = 0.f;
+    if (row_ok) {
+      const int64_t mo = ((int64_t)b * p.T + i) * p.d + h * 64;
+      const uint4* g4 = reinterpret_cast<const uint4*>(p.gctx + mo);
+      const uint4* c4 = reinterpret_cast<const uint4*>(p.ctx + mo);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 gu = g4[c], cu = c4[c];
+        const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, cw[4] = {cu.x, cu.y, cu.z, cu.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[e]));
+          const float2 cf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cw[e]));
+          D = fmaf(gf.x, cf.x, D);
+          D = fmaf(gf.y, cf.y, D);
+        }
+      }
+      // columns outside the key tiles this query tile sees: dAC = 0, and the
+      // dBD margins outside the stored band chunks
+      if (half == 0) {
+        zero_row(arow, 0, (int64_t)jt_lo * kKT);
+        zero_row(brow, 0, lmin(lmax(P0, 0), p.ldp));
+      } else {
+        zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
+        zero_row(brow, lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp), p.ldp);
+      }
+    }
+    // band columns before this row's first key (chunk 0)
+    const __nv_bfloat16 zb = __float2bfloat16_rn(0.f);
+    if (half == 0)
+      for (int c = 0; c < 127 - r; ++c) myring[c] = zb;
+    for (int n = 0; n < nt; ++n) {
+      const int s = n & 1;
+      const int jt0 = (jt_lo + n) * kKT + 64 * half;
+      uint4 pr[2][4];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          pr[k][c] = (row_ok && jt0 + 32 * k + 8 * c + 8 <= p.ldp) ? reinterpret_cast<const uint4*>(prow + jt0 + 32 * k)[c]
+                                                                   : make_uint4(0, 0, 0, 0);
+      mbar_wait(&acc_full[s], (n >> 1) & 1);
+      tc_fence_after();
+      uint32_t dp[2][32];
+      tmem_ld32(tl + s * kKT + 64 * half, dp[0]);
+      tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[s]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int jb = jt0 + 32 * k;
+        float ds[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t w[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+            const int t = 8 * c + 2 * e;
+            ds[t] = pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale;
+            ds[t + 1] = pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale;
+          }
+        }
+        uint32_t o[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          // P is zero outside the window, but dP there is not: mask explicitly
+          const int j = jb + 2 * t;
+          const float a0 = (j >= p.lo && j <= jhi) ? ds[2 * t] : 0.f;
+          const float a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? ds[2 * t + 1] : 0.f;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+          o[t] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        if (row_ok) {
+          if (jb + 32 <= p.ldp) {
+            uint4* dst = reinterpret_cast<uint4*>(arow + jb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[c] = make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          } else {
+            for (int t = 0; t < 32 && jb + t < p.ldp; ++t)
+              arow[jb + t] = reinterpret_cast<const __nv_bfloat16*>(o)[t];
+          }
+        }
+        // shifted copy into the band ring
+        const int cbase = kKT * n + 127 - r + 64 * half + 32 * k;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int c = cbase + t;
+          myring[((c >> 7) & 3) * (kQT * 128) + (c & 127)] = reinterpret_cast<const __nv_bfloat16*>(o)[t];
+        }
+      }
+      if (n == nt - 1 && half == 1) {
+        // band columns after this row's last key (chunk nt)
+        const int c1 = kKT * (nt + 1);
+        for (int c = kKT * n + 255 - r; c < c1; ++c) myring[((c >> 7) & 3) * (kQT * 128) + (c & 127)] = zb;
+      }
+      fence_proxy_async_smem();
+      named_sync(1, kSoftWarps * 32);
+      // band chunk n (and after the last key tile, chunk n + 1) is complete
+      // for every row.  Chunks starting at p >= 0 go out as one TMA bulk
+      // store; the few starting left of p = 0 (short rows: T - 1 - i0 < 127)
+      // are copied by the threads (TMA store boxes need p >= 0).  Chunk m is
+      // rewritten by key tile m + 3, after two more barriers: the elected
+      // thread's wait for all but the newest store covers that.
+      for (int m = n; m <= (n == nt - 1 ? n + 1 : n); ++m) {
+        const int c0 = P0 + kKT * m;
+        const __nv_bfloat16* chunk = ring + (m & 3) * (kQT * 128);
+        if (c0 >= 0) {
+          if (warp == 4 && lane == 0) tma_store_3d(&mBD, chunk, c0, i0, hb);
+        } else {
+          const int tid = threadIdx.x - 128, rr = tid >> 1, cc0 = (tid & 1) * 64;
+          if (i0 + rr < p.T) {
+            __nv_bfloat16* dst = p.gbd + ((int64_t)hb * p.T + i0 + rr) * p.ldp;
+            for (int cc = cc0; cc < cc0 + 64; ++cc) {
+              const int64_t pp = (int64_t)c0 + cc;
+              if (pp >= 0 && pp < p.ldp) dst[pp] = chunk[rr * 128 + cc];
+            }
+          }
+        }
+      }
+      if (warp == 4 && lane == 0) bulk_wait_read_1();
+    }
+    if (warp == 4 && lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 256);
+}
+
 }  // namespace
 
 int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ldp, int64_t B,
@@ -302,6 +570,47 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   if (grid <= 0) return RP_OK;
   xl_attn_fwd_kernel<<<(unsigned)grid, kThreadsFwd, kSmemFwd, st>>>(mqu, mqv, mk, mr, p);
   return check_launch("xl_attn_fwd");
+}
+
+
+int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
+                const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
+                float scale, cudaStream_t st) {
+  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: head dim must be 64 (got %d)", dh);
+  const int64_t Kl = M + Tn, HB = (int64_t)H * B;
+  if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: ldp must be >= M+T and a multiple of 8");
+  if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: mem_len out of range");
+  for (const void* q : {probs, (const void*)gac, (const void*)gbd, gctx, ctx})
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: unaligned operand");
+  CUtensorMap mg, mv, mbd;
+  RP_TRY0(tma_map_bf16(&mg, gctx_h, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
+  RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 128, kQT, false));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(xl_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBwd);
+    attr = true;
+  }
+  BwdParams p;
+  p.p = static_cast<const __nv_bfloat16*>(probs);
+  p.gac = static_cast<__nv_bfloat16*>(gac);
+  p.gbd = static_cast<__nv_bfloat16*>(gbd);
+  p.gctx = static_cast<const __nv_bfloat16*>(gctx);
+  p.ctx = static_cast<const __nv_bfloat16*>(ctx);
+  p.ldp = ldp;
+  p.B = (int)B;
+  p.T = (int)Tn;
+  p.M = (int)M;
+  p.Kl = (int)Kl;
+  p.lo = (int)(M - mem_len);
+  p.nqt = (int)((Tn + kQT - 1) / kQT);
+  p.H = H;
+  p.d = H * dh;
+  p.scale = scale;
+  const int64_t grid = HB * p.nqt;
+  if (grid <= 0) return RP_OK;
+  xl_attn_bwd_kernel<<<(unsigned)grid, kThreadsBwd, kSmemBwd, st>>>(mg, mv, mbd, p);
+  return check_launch("xl_attn_bwd");
 }
 
 }  // namespace rp

@@ -374,6 +374,26 @@ def xl_attn_fwd(qu, qv, kh, rh, probs, B, T, M, mem_len, scale):
                                    H, dh, mem_len, scale, _stream()), "xl_attn_fwd")
 
 
+def xl_attn_bwd(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx, B, T, M, mem_len, scale):
+    """Fused softmax backward (bf16, dh = 64): g_ctx_h [H*B*T, dh] head-major,
+    vh [H*B*Kl, dh], probs / g_ac / g_bd [H*B, T, ldp]; g_ctx, ctx merged
+    [B*T, H*dh] rows (D_i = <g_ctx_i, ctx_i>)."""
+    _require_cuda(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx)
+    for t in (g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx):
+        if t.dtype != torch.bfloat16:
+            raise DimensionError("xl_attn_bwd takes bf16 tensors")
+    for t in (g_ctx_h, vh, g_ctx, ctx):
+        if not t.is_contiguous():
+            raise DimensionError("xl_attn_bwd operands must be contiguous")
+    ldp = probs.stride(-2)
+    if g_ac.stride(-2) != ldp or g_bd.stride(-2) != ldp:
+        raise DimensionError("xl_attn_bwd: P, dAC and dBD must share the row pitch")
+    H, dh = g_ctx.shape[-1] // vh.shape[-1], vh.shape[-1]
+    _count(1)
+    N.check(N.lib().rp_xl_attn_bwd(_ptr(g_ctx_h), _ptr(vh), _ptr(probs), _ptr(g_ac), _ptr(g_bd), ldp, _ptr(g_ctx),
+                                   _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_bwd")
+
+
 def xl_softmax_bwd(g_p, probs, g_ac, g_bd, T, M, mem_len, scale):
     _count(1)
     rows = math.prod(probs.shape[:-1])

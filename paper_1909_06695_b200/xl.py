@@ -161,13 +161,18 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g_ctx_h = ws.get("xl_g_ctx_h", (H, Nt, dh), cdt)
     ops.xl_split_heads(g_ctx, g_ctx_h, H, dh)
     g3 = g_ctx_h.view(H * B, T, dh)
-    g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
-    ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p)
-    g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
-    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
     g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
     g_bd = ws.get("xl_g_bd", (H, Nt, tp.ldk), cdt)
-    ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
+    if fused_ok(tp):
+        # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
+        with ops.span("xl_attn_bwd"):
+            ops.xl_attn_bwd(g_ctx_h, tp.vh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, B, T, M, tp.mem_len, scale)
+    else:
+        g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
+        ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p)
+        ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
+    g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
+    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
     g_qu = ws.get("xl_g_qu", (H, Nt, dh), torch.float32)
     g_kh = ws.get("xl_g_kh", (H * B, Kl, dh), torch.float32)

@@ -155,3 +155,53 @@ def test_fused_block_tracks_unfused_and_restatement(H, T, M, mem_len, monkeypatc
     for k, want in RG.items():
         ea, eb = rel(a[k], want), rel(b[k], want)
         assert ea <= max(1.25 * eb, 3e-2), (k, ea, eb)
+
+
+def ref_bwd(probs, g3, vh, gctx, ctx, B, T, M, mem_len, scale, H, dh):
+    """fp32 dAC and un-shifted dBD from the same bf16 inputs, D from <g_ctx, ctx>."""
+    HB, Kl = H * B, M + T
+    P = probs[:, :, :Kl].float()
+    dP = g3.float().view(HB, T, dh) @ vh.float().view(HB, Kl, dh).transpose(1, 2)
+    D = (gctx.float() * ctx.float()).view(B, T, H, dh).sum(-1).permute(2, 0, 1).reshape(HB, T, 1)
+    dS = P * (dP - D) * scale
+    i = torch.arange(T, device=P.device)[:, None]
+    j = torch.arange(Kl, device=P.device)[None, :]
+    dS = dS.masked_fill(~((j >= M - mem_len) & (j <= M + i)), 0.0)
+    jj = (j - (T - 1 - i)).expand(T, Kl)  # key index j for every (i, p)
+    dBD = torch.gather(dS, 2, jj.clamp(0, Kl - 1).unsqueeze(0).expand(HB, T, Kl))
+    dBD = dBD.masked_fill(((jj < 0) | (jj >= Kl)).unsqueeze(0), 0.0)
+    return dS, dBD
+
+
+@pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 3, 200, 72, 50), (2, 1, 64, 0, 0),
+                                             (1, 2, 256, 256, 100), (2, 8, 512, 512, 512)])
+def test_fused_softmax_backward_matches_fp32(B, H, T, M, mem_len):
+    from paper_1909_06695_b200 import ops
+
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(7 * T + M)
+    dh, Kl = 64, M + T
+    ldp = _pad8(Kl)
+    mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
+    qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
+    kh, rh, vh = mk(H, B * Kl, dh), mk(H, Kl, dh), mk(H, B * Kl, dh)
+    scale = 1.0 / math.sqrt(dh)
+    probs = torch.empty(H * B, T, ldp, device=dev, dtype=torch.bfloat16)
+    ops.xl_attn_fwd(qu, qv, kh, rh, probs, B, T, M, mem_len, scale)
+    g3 = mk(H, B * T, dh)
+    gctx = g3.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    # ctx = P v (bf16-rounded, as the forward's merged tape row)
+    ctx_h = (probs[:, :, :Kl].float() @ vh.float().view(H * B, Kl, dh)).to(torch.bfloat16)
+    ctx = ctx_h.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    gac = torch.full((H * B, T, ldp), float("nan"), device=dev, dtype=torch.bfloat16)
+    gbd = torch.full((H, B * T, ldp), float("nan"), device=dev, dtype=torch.bfloat16)
+    ops.xl_attn_bwd(g3, vh, probs, gac, gbd, gctx, ctx, B, T, M, mem_len, scale)
+    torch.cuda.synchronize()
+    want_ac, want_bd = ref_bwd(probs, g3, vh, gctx, ctx, B, T, M, mem_len, scale, H, dh)
+    assert torch.isfinite(gac.float()).all() and torch.isfinite(gbd.float()).all()
+    assert rel(gac[:, :, :Kl].float().cpu(), want_ac.cpu()) <= 4e-3
+    assert rel(gbd.view(H * B, T, ldp)[:, :, :Kl].float().cpu(), want_bd.cpu()) <= 4e-3
+    assert (gac[:, :, Kl:] == 0).all() and (gbd[:, :, Kl:] == 0).all()
+    # dBD is a permutation of dAC's row entries (plus zeros)
+    assert torch.equal(gac.float().sum(-1), gbd.view(H * B, T, ldp).float().sum(-1)) or \
+        rel(gac.float().sum(-1).cpu(), gbd.view(H * B, T, ldp).float().sum(-1).cpu()) <= 1e-5
