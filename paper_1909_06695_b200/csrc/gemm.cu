@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(384, 1)
   using Cfg = GemmCfg<kTf32, BN, kCta>;
   static_assert(kCta == 1 || !kTf32, "CTA-pair mode is bf16 only");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* stage_out = smem + Cfg::STAGES * Cfg::STAGE_BYTES;  // 1024-aligned
   uint8_t* stage_in = stage_out + Cfg::STAGE_OUT;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_in + Cfg::STAGE_IN);

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
                        const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
                        const FwdParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sQu = smem;
   uint8_t* sQv = smem + kQBytes;
   uint8_t* stages = smem + 2 * kQBytes;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     xl_attn_bwd_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
                        const __grid_constant__ CUtensorMap mBD, const BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sG = smem;
   uint8_t* stages = smem + kGBytes;
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(stages + kStages * kVBytes);
