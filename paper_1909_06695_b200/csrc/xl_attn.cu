@@ -20,6 +20,7 @@
 // thread), warp 2 TMEM allocator, warps 4..11 softmax (warp w owns TMEM lane
 // quarter w % 4 and half of each key tile's columns).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "rp_internal.h"
@@ -35,20 +36,25 @@ namespace rp {
 namespace {
 
 constexpr int kQT = 128;                  // query rows per CTA
-constexpr int kKT = 128;                  // keys per step
-constexpr int kBand = 256;                // relative-encoding rows per step
+constexpr int kKT = 128;                  // keys per backward step
 constexpr int kRowBytes = 128;            // dh = 64 bf16
 constexpr int kQBytes = kQT * kRowBytes;  // 16 KB
-constexpr int kKBytes = kKT * kRowBytes;  // 16 KB
-constexpr int kRBytes = kBand * kRowBytes;  // 32 KB
-constexpr int kStageBytes = kKBytes + kRBytes;
 constexpr int kStages = 2;
+constexpr int kSoftWarps = 8;
+// forward: 64 keys per step, so two steps' accumulators (AC 64 + band 192
+// columns each) fit TMEM and the MMA of step n+1 overlaps the softmax of n
+constexpr int kFKT = 64;                  // keys per forward step
+constexpr int kFBand = kFKT + 128;        // relative-encoding rows per forward step (covers 127 + 64 distances)
+constexpr int kFKBytes = kFKT * kRowBytes;     // 8 KB
+constexpr int kFRBytes = kFBand * kRowBytes;   // 24 KB
+constexpr int kFStageBytes = kFKBytes + kFRBytes;
+constexpr int kFStages = 3;
+constexpr int kFBuf = 256;                // TMEM columns per accumulator buffer
 constexpr int kRing = 66;                 // floats per staged band row: 2 chunks of 32, stride == 2 (mod 32)
 constexpr int kRingWarp = 32 * kRing;
-constexpr int kSoftWarps = 8;
 constexpr int kThreadsFwd = 384;
 constexpr int kTmemCols = 512;
-constexpr int kSmemFwd = 1024 /*align*/ + 2 * kQBytes + kStages * kStageBytes + kSoftWarps * kRingWarp * 4 +
+constexpr int kSmemFwd = 1024 /*align*/ + 2 * kQBytes + kFStages * kFStageBytes + kSoftWarps * kRingWarp * 4 +
                          2 * kQT * 2 * 4 /*stats*/ + 128 /*barriers*/;
 
 struct FwdParams {
@@ -56,6 +62,7 @@ struct FwdParams {
   int64_t ldp;
   int B, T, M, Kl, lo, nqt;
   float c2;  // scale * log2(e)
+  int dbg;   // diagnostics (RP_XL_DBG): 1 = softmax warps only wait/arrive, 2 = no MMAs
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -85,22 +92,22 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   uint8_t* sQu = smem;
   uint8_t* sQv = smem + kQBytes;
   uint8_t* stages = smem + 2 * kQBytes;
-  float* ring = reinterpret_cast<float*>(stages + kStages * kStageBytes);
+  float* ring = reinterpret_cast<float*>(stages + kFStages * kFStageBytes);
   float* stats = ring + kSoftWarps * kRingWarp;  // [half][row][max, sum]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stats + 2 * kQT * 2);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_empty = bars + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* kv_full = bars + 1;   // [kFStages]
+  uint64_t* kv_empty = bars + 4;  // [kFStages]
+  uint64_t* s_full = bars + 7;    // [2]
+  uint64_t* s_empty = bars + 9;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hb = blockIdx.x / p.nqt, qt = blockIdx.x % p.nqt;
   const int h = hb / p.B;
   const int i0 = qt * kQT;
   const int imax = min(i0 + kQT, p.T) - 1;
-  const int jt_lo = p.lo / kKT, jt_hi = min(p.M + imax, p.Kl - 1) / kKT;
+  const int jt_lo = p.lo / kFKT, jt_hi = min(p.M + imax, p.Kl - 1) / kFKT;
   const int per_pass = jt_hi - jt_lo + 1;
   const int nsteps = 2 * per_pass;
 
@@ -112,12 +119,14 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kFStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_empty, kSoftWarps * 32);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], kSoftWarps * 32);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -133,43 +142,56 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
       mbar_expect_tx(q_full, 2 * kQBytes);
       tma_load_3d(sQu, &mQu, q_full, 0, i0, hb);
       tma_load_3d(sQv, &mQv, q_full, 0, i0, hb);
+      int s = 0;
+      uint32_t ph = 0;
       for (int n = 0; n < nsteps; ++n) {
-        const int s = n & 1;
-        mbar_wait(&kv_empty[s], ((n >> 1) & 1) ^ 1);
-        const int j0 = (jt_lo + n % per_pass) * kKT;
-        uint8_t* sk = stages + s * kStageBytes;
-        mbar_expect_tx(&kv_full[s], kStageBytes);
+        mbar_wait(&kv_empty[s], ph ^ 1);
+        const int j0 = (jt_lo + n % per_pass) * kFKT;
+        uint8_t* sk = stages + s * kFStageBytes;
+        mbar_expect_tx(&kv_full[s], kFStageBytes);
         tma_load_3d(sk, &mK, &kv_full[s], 0, j0, hb);
-        tma_load_3d(sk + kKBytes, &mR, &kv_full[s], 0, p.T - kQT - i0 + j0, h);
+        tma_load_3d(sk + kFKBytes, &mR, &kv_full[s], 0, p.T - kQT - i0 + j0, h);
+        if (++s == kFStages) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      const uint32_t id_ac = umma_idesc(false, false, false, kQT, kKT);
-      const uint32_t id_bd = umma_idesc(false, false, false, kQT, kBand);
+      const uint32_t id_ac = umma_idesc(false, false, false, kQT, kFKT);
+      const uint32_t id_bd = umma_idesc(false, false, false, kQT, kFBand);
       const uint32_t qa = smem_u32(sQu), qb = smem_u32(sQv);
       mbar_wait(q_full, 0);
+      int s = 0;
+      uint32_t ph = 0;
       for (int n = 0; n < nsteps; ++n) {
-        const int s = n & 1;
-        mbar_wait(&kv_full[s], (n >> 1) & 1);
-        if (n > 0) mbar_wait(s_empty, (n - 1) & 1);
+        const int buf = n & 1;
+        mbar_wait(&s_empty[buf], ((n >> 1) & 1) ^ 1);
+        mbar_wait(&kv_full[s], ph);
         tc_fence_after();
-        const uint32_t kb = smem_u32(stages + s * kStageBytes), rb = kb + kKBytes;
+        const uint32_t kb = smem_u32(stages + s * kFStageBytes), rb = kb + kFKBytes;
+        const uint32_t d = tmem_base + buf * kFBuf;
+        if (!(p.dbg & 2)) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc_mma<false>(tmem_base, umma_desc(qa + 32 * k, 16, 1024), umma_desc(kb + 32 * k, 16, 1024), id_ac,
-                        k > 0);
+          for (int k = 0; k < 4; ++k)
+            tc_mma<false>(d, umma_desc(qa + 32 * k, 16, 1024), umma_desc(kb + 32 * k, 16, 1024), id_ac, k > 0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc_mma<false>(tmem_base + kKT, umma_desc(qb + 32 * k, 16, 1024), umma_desc(rb + 32 * k, 16, 1024), id_bd,
-                        k > 0);
+          for (int k = 0; k < 4; ++k)
+            tc_mma<false>(d + kFKT, umma_desc(qb + 32 * k, 16, 1024), umma_desc(rb + 32 * k, 16, 1024), id_bd,
+                          k > 0);
+        }
         tc_commit(&kv_empty[s]);
-        tc_commit(s_full);
+        tc_commit(&s_full[buf]);
+        if (++s == kFStages) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax: row r = 32 q + lane, key columns [64 half, +64) ----------------
+    // ---------------- softmax: row r = 32 q + lane, key columns [32 half, +32) of each step ----------------
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int r = 32 * q + lane;
     const int i = i0 + r;
@@ -177,7 +199,10 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
     const int jhi = p.M + i;
     float* myring = ring + (warp - 4) * kRingWarp + lane * kRing;
     const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
-    const int cb0 = 96 - 32 * q + 64 * half;  // first band column this warp stages
+    // band column of key jj for row r is 127 - r + jj: this warp's 32 keys
+    // need band columns [cb0, cb0 + 63)
+    const int cb0 = 96 - 32 * q + 32 * half;
+    const int off = 31 - lane;
     __nv_bfloat16* prow = p.p + ((int64_t)hb * p.T + i) * p.ldp;
     float m = -INFINITY, l = 0.f, inv = 0.f;
     for (int n = 0; n < nsteps; ++n) {
@@ -195,69 +220,78 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
         // columns of key tiles no query of this tile can see
         if (row_ok) {
           const uint4 z = make_uint4(0, 0, 0, 0);
-          const int64_t a0 = half ? (int64_t)(jt_hi + 1) * kKT : 0;
-          const int64_t a1 = half ? p.ldp : (int64_t)jt_lo * kKT;
+          const int64_t a0 = half ? (int64_t)(jt_hi + 1) * kFKT : 0;
+          const int64_t a1 = half ? p.ldp : (int64_t)jt_lo * kFKT;
           for (int64_t c = a0; c < a1; c += 8) *reinterpret_cast<uint4*>(prow + c) = z;
         }
       }
-      const int j0 = (jt_lo + n % per_pass) * kKT + 64 * half;
-      mbar_wait(s_full, n & 1);
+      const int buf = n & 1;
+      const int jb = (jt_lo + n % per_pass) * kFKT + 32 * half;
+      mbar_wait(&s_full[buf], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tl + kKT + cb0, v);
-      stage_band(myring, 0, v);
-      tmem_ld32(tl + kKT + cb0 + 32, v);
-      stage_band(myring, 1, v);
+      if (p.dbg & 1) {
+        tc_fence_before();
+        mbar_arrive(&s_empty[buf]);
+        continue;
+      }
+      const uint32_t tb = tl + buf * kFBuf;
+      uint32_t v0[32], v1[32], a[32];
+      tmem_ld32_async(tb + kFKT + cb0, v0);
+      tmem_ld32_async(tb + kFKT + cb0 + 32, v1);
+      tmem_ld32_async(tb + 32 * half, a);
+      tmem_wait_ld(v0);
+      tmem_wait_ld(v1);
+      tmem_wait_ld(a);
+      tc_fence_before();
+      mbar_arrive(&s_empty[buf]);  // this step's TMEM buffer is free for step n + 2
+      stage_band(myring, 0, v0);
+      stage_band(myring, 1, v1);
       __syncwarp();
-#pragma unroll 1
-      for (int k = 0; k < 2; ++k) {
-        uint32_t a[32];
-        tmem_ld32(tl + 64 * half + 32 * k, a);
-        if (k == 1) {
-          tc_fence_before();
-          mbar_arrive(s_empty);  // every TMEM read of this step is done
+      float s[32];
+      float cm = -INFINITY;
+      if (jb >= p.lo && jb + 31 <= p.M + i0 + 32 * q) {
+        // every key of this chunk is visible to every row of the warp
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          s[t] = (__uint_as_float(a[t]) + myring[off + t]) * p.c2;
+          cm = fmaxf(cm, s[t]);
         }
-        const int jb = j0 + 32 * k;
-        const int off = 31 + 32 * k - lane;
-        float s[32];
-        float cm = -INFINITY;
+      } else {
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int j = jb + t;
-          const float bd = myring[(off + t) & 63];
-          const float x = (__uint_as_float(a[t]) + bd) * p.c2;
+          const float x = (__uint_as_float(a[t]) + myring[off + t]) * p.c2;
           s[t] = (j >= p.lo && j <= jhi) ? x : -INFINITY;
           cm = fmaxf(cm, s[t]);
         }
-        if (k == 0) {
-          __syncwarp();  // slot 0 (band chunk 0) fully read
-          tmem_ld32(tl + kKT + cb0 + 64, v);
-          stage_band(myring, 0, v);
-          __syncwarp();
-        }
-        if (!pass2) {
-          const float mn = fmaxf(m, cm);
-          if (mn != -INFINITY) {
-            float acc = 0.f;
+      }
+      __syncwarp();  // ring reads done before the next step's staging
+      if (!pass2) {
+        const float mn = fmaxf(m, cm);
+        if (mn != -INFINITY) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int t = 0; t < 32; ++t) acc += ex2(s[t] - mn);
-            l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + acc;
-            m = mn;
-          }
-        } else if (row_ok) {
-          uint32_t w[16];
+          for (int t = 0; t < 32; ++t) acc[t & 3] += ex2(s[t] - mn);
+          l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          m = mn;
+        }
+      } else if (row_ok) {
+        uint32_t w[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2(s[2 * t] - m) * inv, ex2(s[2 * t + 1] - m) * inv);
+          w[t] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        if (jb + 32 <= p.ldp) {
+          uint4* dst = reinterpret_cast<uint4*>(prow + jb);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        } else {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2(s[2 * t] - m) * inv, ex2(s[2 * t + 1] - m) * inv);
-            w[t] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          if (jb + 32 <= p.ldp) {
-            uint4* dst = reinterpret_cast<uint4*>(prow + jb);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-          } else {
-            const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(w);
-            for (int t = 0; t < 32 && jb + t < p.ldp; ++t) prow[jb + t] = wb[t];
+            const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[t]);
+            if (jb + 2 * t < p.ldp) prow[jb + 2 * t] = b2.x;
+            if (jb + 2 * t + 1 < p.ldp) prow[jb + 2 * t + 1] = b2.y;
           }
         }
       }
@@ -493,11 +527,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         }
         // shifted copy into the band ring
         const int cbase = kKT * n + 127 - r + 64 * half + 32 * k;
+        // the 32-run crosses at most one chunk boundary, at t = split
+        const int split = 128 - (cbase & 127);
+        const int o0 = ((cbase >> 7) & 3) * (kQT * 128) + (cbase & 127);
+        const int o1 = (((cbase >> 7) + 1) & 3) * (kQT * 128) - split;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int c = cbase + t;
-          myring[((c >> 7) & 3) * (kQT * 128) + (c & 127)] = reinterpret_cast<const __nv_bfloat16*>(o)[t];
-        }
+        for (int t = 0; t < 32; ++t)
+          myring[(t < split ? o0 : o1) + t] = reinterpret_cast<const __nv_bfloat16*>(o)[t];
       }
       if (n == nt - 1 && half == 1) {
         // band columns after this row's last key (chunk nt)
@@ -549,8 +585,8 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   CUtensorMap mqu, mqv, mk, mr;
   RP_TRY0(tma_map_bf16(&mqu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
   RP_TRY0(tma_map_bf16(&mqv, qv, dh, Tn, dh, HB, Tn * dh, 64, kQT));
-  RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
-  RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kBand));
+  RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kFKT));
+  RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(xl_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFwd);
@@ -566,6 +602,8 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   p.lo = (int)(M - mem_len);
   p.nqt = (int)((Tn + kQT - 1) / kQT);
   p.c2 = scale * 1.4426950408889634f;
+  static const int dbg = getenv("RP_XL_DBG") ? atoi(getenv("RP_XL_DBG")) : 0;
+  p.dbg = dbg;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   xl_attn_fwd_kernel<<<(unsigned)grid, kThreadsFwd, kSmemFwd, st>>>(mqu, mqv, mk, mr, p);
