@@ -284,8 +284,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
     float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
-  __shared__ float red_g[kRowWarps][32 * NPL];
-  __shared__ float red_b[kRowWarps][32 * NPL];
+  __shared__ float red[kRowWarps][2][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float acc_g[NPL], acc_b[NPL], gv[NPL];
 #pragma unroll
@@ -331,21 +330,22 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
       }
     }
   }
+  // per-CTA column partials, 32 columns at a time (static shared memory stays
+  // at 2 KB for any d; the warp summation order is fixed)
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
-    red_g[w][lane + 32 * i] = acc_g[i];
-    red_b[w][lane + 32 * i] = acc_b[i];
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < d; j += kRowThreads) {
-    float sg = 0.f, sb = 0.f;
+    if (32 * i >= d) break;
+    if (i) __syncthreads();
+    red[w][0][lane] = acc_g[i];
+    red[w][1][lane] = acc_b[i];
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int which = threadIdx.x >> 5, c = threadIdx.x & 31, j = 32 * i + c;
+      float sacc = 0.f;
 #pragma unroll
-    for (int q = 0; q < kRowWarps; ++q) {
-      sg += red_g[q][j];
-      sb += red_b[q][j];
+      for (int q = 0; q < kRowWarps; ++q) sacc += red[q][which][c];
+      if (j < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + j] = sacc;
     }
-    part_g[(int64_t)blockIdx.x * d + j] = sg;
-    part_b[(int64_t)blockIdx.x * d + j] = sb;
   }
 }
 
@@ -517,15 +517,6 @@ int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
     default: return set_error(RP_ERR_DIMENSION, "row length too large"); \
   }
 
-#define RP_NPL_DISPATCH_SMALL(NPL_VAL, ...)                             \
-  switch (NPL_VAL) {                                                    \
-    case 2: { constexpr int NPL = 2; __VA_ARGS__; break; }              \
-    case 4: { constexpr int NPL = 4; __VA_ARGS__; break; }              \
-    case 8: { constexpr int NPL = 8; __VA_ARGS__; break; }              \
-    case 16: { constexpr int NPL = 16; __VA_ARGS__; break; }            \
-    default: return set_error(RP_ERR_DIMENSION, "row length too large"); \
-  }
-
 #define RP_DTYPE_DISPATCH(DT, ...)                     \
   if ((DT) == RP_BF16) {                               \
     using T = __nv_bfloat16;                           \
@@ -576,8 +567,7 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
     return check_launch("layernorm_bwd");
   }
   const int npl = npl_for(d);
-  if (npl > 16) return set_error(RP_ERR_DIMENSION, "layernorm_bwd supports d <= 512 in this build");
-  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH_SMALL(npl, ln_bwd_kernel<T, NPL><<<nb, kRowThreads, 0, st>>>(
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, ln_bwd_kernel<T, NPL><<<nb, kRowThreads, 0, st>>>(
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx,
                                                     (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
                                                     rows, (int)d)));
