@@ -1,7 +1,7 @@
 """Per-launch summary of an `ncu --set full` report (run here, on the CPU side):
 duration, DRAM bytes read / written, tensor-pipe and SM/DRAM throughput.
 
-  python tools/ncu_summary.py REPORT.ncu-rep [--labels a,b,...] [--json OUT.json] [--source NOTE]
+  python tools/ncu_summary.py REPORT.ncu-rep [--labels "a;b;..."] [--json OUT.json] [--source NOTE]
 
 With --json, also writes the head-GEMM traffic file bench.py reads
 (bytes_per_launch = mean DRAM read + write over the launches)."""
@@ -18,7 +18,7 @@ METRICS = {
     "tensor_pipe_active_pct": ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 1.0),
     "tensor_mem_active_pct": ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 1.0),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
-    "dram_throughput_pct": ("dram__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
+    "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
 }
 UNIT = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
         "Gbyte": 1e9}
@@ -54,7 +54,7 @@ def main():
     ap.add_argument("--source", default="")
     a = ap.parse_args()
     res = load(a.report)
-    labels = a.labels.split(",") if a.labels else []
+    labels = a.labels.split(";") if a.labels else []
     for i, d in enumerate(res):
         if i < len(labels):
             d["launch"] = labels[i]
