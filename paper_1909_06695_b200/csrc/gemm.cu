@@ -471,6 +471,9 @@ __global__ void __launch_bounds__(384, 1)
 #ifndef RP_HEAD_FAST_OFF
 #define RP_HEAD_FAST_OFF 0
 #endif
+#ifndef RP_LSE_FAST_OFF
+#define RP_LSE_FAST_OFF 0
+#endif
       if constexpr (!kTf32 && kHalf % 2 == 0 && !RP_HEAD_FAST_OFF) {
         const bool no_aux = p.epi == RP_EPI_CE_GRAD || p.epi == RP_EPI_STORE || p.epi == RP_EPI_BIAS_RELU;
         if (no_aux && (p.tma_store || p.epi != RP_EPI_CE_GRAD)) {
@@ -524,6 +527,51 @@ __global__ void __launch_bounds__(384, 1)
             tmem_wait_ld(rb);
             if (cc + 2 < kHalf) tmem_ld32_async(t_row + (c0 + cc + 2) * 32, ra);
             chunk(rb, c0 + cc + 1);
+            if (cc + 2 < kHalf) tmem_wait_ld(ra);
+          }
+        } else if (p.epi == RP_EPI_LSE_PARTIAL && !RP_LSE_FAST_OFF) {
+          // online log-sum-exp over this half's columns, next TMEM chunk in
+          // flight; no per-chunk epilogue dispatch.  Same operation order as
+          // the generic loop (bitwise equal): columns past N enter as -inf.
+          head_fast = true;
+          auto lse_chunk = [&](const uint32_t (&r)[32], int c) {
+            const int n0 = nb * BN + c * 32;
+            if (n0 >= p.N || !row_ok) return;
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            if (n0 + 32 > p.N) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j >= p.N) v[j] = -INFINITY;
+            }
+            float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cm[j & 3] = fmaxf(cm[j & 3], v[j]);
+            const float nmax = fmaxf(run_max, fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])));
+            const float nm2 = nmax * kLog2e;
+            float s[4] = {run_sum * fast_exp2(run_max * kLog2e - nm2), 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s[j & 3] += fast_exp2(fmaf(v[j], kLog2e, -nm2));
+            run_max = nmax;
+            run_sum = (s[0] + s[1]) + (s[2] + s[3]);
+            if ((uint64_t)(tgt - n0) < 32ull) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (tgt == n0 + j) p.target_logit[grow] = v[j];
+            }
+          };
+          const int c0 = half * kHalf;
+          uint32_t ra[32], rb[32];
+          tmem_ld32_async(t_row + c0 * 32, ra);
+          tmem_wait_ld(ra);
+#pragma unroll 1
+          for (int cc = 0; cc < kHalf; cc += 2) {
+            tmem_ld32_async(t_row + (c0 + cc + 1) * 32, rb);
+            lse_chunk(ra, c0 + cc);
+            tmem_wait_ld(rb);
+            if (cc + 2 < kHalf) tmem_ld32_async(t_row + (c0 + cc + 2) * 32, ra);
+            lse_chunk(rb, c0 + cc + 1);
             if (cc + 2 < kHalf) tmem_wait_ld(ra);
           }
         }

@@ -31,3 +31,11 @@ e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / 5
 print(f"head fwd+bwd {ms:.3f} ms  -> {4 * 2 * N * d * V / ms / 1e9:.1f} TFLOP/s over 4 GEMMs, loss {hs.loss.item():.4f}")
+f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+f0.record()
+for _ in range(5):
+    LY.head_forward(h, tied, y, V, hs, ws, None)
+f1.record()
+torch.cuda.synchronize()
+print(f"head fwd (LSE pass + CE finish) {f0.elapsed_time(f1) / 5:.3f} ms")
+
