@@ -205,3 +205,42 @@ def test_fused_softmax_backward_matches_fp32(B, H, T, M, mem_len):
     # dBD is a permutation of dAC's row entries (plus zeros)
     assert torch.equal(gac.float().sum(-1), gbd.view(H * B, T, ldp).float().sum(-1)) or \
         rel(gac.float().sum(-1).cpu(), gbd.view(H * B, T, ldp).float().sum(-1).cpu()) <= 1e-5
+
+
+def test_fused_xl_engine_tracks_restatement():
+    """Ouroboros K=2 over segment streams with memory, bf16, head dim 64 (the
+    fused kernels run in every block): loss within the bf16 production
+    tolerance of the fp64 restatement, and the multi-stream executor stays
+    bitwise equal to the single-stream one."""
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200 import xl as XD
+    from paper_1909_06695_b200.data import SegmentStream
+    from oracle import ouroboros as OO
+
+    vocab, d, f, blocks, T, M, H, B, p = 64, 128, 256, 2, 16, 16, 2, 2, 0.1
+    lr = 2e-3
+
+    def make(concurrent):
+        stack = MD.build_xl_stack(vocab, d, f, blocks, T, p, 5, H, M, dtype="bf16")
+        eng = (E.ConcurrentPipelineEngine if concurrent else E.PipelineEngine)(stack, MD.partition(stack.num_layers, 2), 9)
+        return stack, eng, O.make_optimizer("adam", O.LrSchedule(lr, "fixed"))
+
+    s1, e1, o1 = make(False)
+    s2, e2, o2 = make(True)
+    V, layers = X.init_xl_params(vocab, d, f, blocks, T, H, 5)
+    ora = X.XLOuroborosOracle(V, layers, 2, 9, p, H, M, B, OO.Adam(lambda t: lr))
+    toks = (Stream(2).uniform((B * 8 * T + 4,)) * vocab).astype(np.int64)
+    src = SegmentStream(toks, T, B)
+    assert XD.FUSED
+    for t in range(6):
+        b = src.batch_at(t)
+        p1, l1 = e1.step(t, b, o1)
+        c1 = p1.cpu()
+        p2, l2 = e2.step(t, b, o2)
+        c2 = p2.cpu()
+        assert l1 == l2
+        assert np.array_equal(c1.emb_grad, c2.emb_grad)
+        oloss, _ = ora.step(t, b.x, b.y)
+        assert abs(l1 - oloss) <= 2e-2 * abs(oloss), (t, l1, oloss)
