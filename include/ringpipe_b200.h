@@ -128,6 +128,9 @@ int rp_colsum_blocks(int64_t rows);
 int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* partial,
                       void* stream);
 int rp_colsum_finish(const float* partial, int32_t nblocks, int64_t cols, float* out, void* stream);
+/* up to 8 rp_colsum_finish jobs in one launch (bitwise equal to separate calls) */
+int rp_colsum_finish_multi(const float* const* partials, const int32_t* nblocks, const int64_t* cols, float* const* outs,
+                           int32_t n, void* stream);
 /* out = g * mask(seed, pos0 + r*d + j) (dtype), partial column sums of the masked values
  * (layers.py:209-220). */
 int rp_mask_grad_blocks(int64_t rows, int64_t d); /* partial rows rp_mask_grad writes */

@@ -143,6 +143,7 @@ def _declare(L):
         "rp_mask_grad_blocks": [i64, i64],
         "rp_colsum_partial": [i32, vp, i64, i64, i64, vp, vp],
         "rp_colsum_finish": [vp, i32, i64, vp, vp],
+        "rp_colsum_finish_multi": [vp, vp, vp, vp, i32, vp],
         "rp_mask_grad": [i32, vp, vp, i64, i64, u64, u64, u64, f32, i32, vp, vp],
         "rp_softmax_causal": [i32, vp, vp, i64, i64, i64, vp],
         "rp_softmax_bwd": [i32, vp, vp, vp, f32, i64, i64, i64, vp],

@@ -80,6 +80,14 @@ int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, 
 int rp_colsum_finish(const float* partial, int32_t nblocks, int64_t cols, float* out, void* stream) {
   return rp::colsum_finish(partial, nblocks, cols, out, RP_S(stream));
 }
+int rp_colsum_finish_multi(const float* const* partials, const int32_t* nblocks, const int64_t* cols, float* const* outs,
+                           int32_t n, void* stream) {
+  if (n < 1 || n > rp::kMaxColsumJobs)
+    return rp::set_error(RP_ERR_INVALID, "colsum_finish_multi: 1..%d jobs", rp::kMaxColsumJobs);
+  rp::ColsumJob jobs[rp::kMaxColsumJobs];
+  for (int i = 0; i < n; ++i) jobs[i] = rp::ColsumJob{partials[i], nblocks[i], cols[i], outs[i]};
+  return rp::colsum_finish_multi(jobs, n, RP_S(stream));
+}
 int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
                  uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream) {
   return rp::mask_grad(dtype, g, out, rows, d, seed, pos0, threshold, scale, drop_enabled, partial, RP_S(stream));

@@ -287,6 +287,17 @@ def colsum_partial(x, part):
             "colsum_partial")
 
 
+def colsum_finish_multi(jobs):
+    """jobs: up to 8 (part, nblk, out) triples finished in one launch."""
+    n = len(jobs)
+    parts = (ctypes.c_void_p * n)(*[j[0].data_ptr() for j in jobs])
+    nblk = (ctypes.c_int32 * n)(*[j[1] for j in jobs])
+    cols = (ctypes.c_int64 * n)(*[j[2].numel() for j in jobs])
+    outs = (ctypes.c_void_p * n)(*[j[2].data_ptr() for j in jobs])
+    _count(1)
+    N.check(N.lib().rp_colsum_finish_multi(parts, nblk, cols, outs, n, _stream()), "colsum_finish_multi")
+
+
 def colsum_finish(part, nblk, out):
     _count(1)
     N.check(N.lib().rp_colsum_finish(_ptr(part), nblk, out.numel(), _ptr(out), _stream()), "colsum_finish")

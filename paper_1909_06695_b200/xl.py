@@ -135,12 +135,10 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g_h2 = ws.get("g_h2", (Nt, d), cdt)
     pm = ws.get("mask_part", (nbm, d), torch.float32)
     ops.mask_grad(g_out, g_h2, n, drop, pm)
-    ops.colsum_finish(pm, nbm, G["b2"])
     ops.gemm(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
     g_z1 = ws.get("g_z1", (Nt, f), cdt)
     ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tp.h1)
     ops.colsum_partial(g_z1, part[:, :f])
-    ops.colsum_finish(part[:, :f], nbc, G["b1"])
     ops.gemm(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
     g_m = ws.get("g_m", (Nt, d), torch.float32)
     ops.gemm(g_z1, W["w1"], out=g_m)
@@ -150,10 +148,10 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     pb = ws.get("ln_pb", (nbl_cur + nbl_mem, d), torch.float32)
     g_x1 = ws.get("g_x1", (Nt, d), torch.float32)
     g_proj = ws.get("g_proj", (Nt, d), cdt)
-    ops.layernorm_bwd(g_m, tp.x1, tp.mean2, tp.rstd2, vecs["ln2_g"], g_x1, pg[:nbl_cur], pb[:nbl_cur],
+    pg2 = ws.get("ln2_pg", (nbl_cur, d), torch.float32)
+    pb2 = ws.get("ln2_pb", (nbl_cur, d), torch.float32)
+    ops.layernorm_bwd(g_m, tp.x1, tp.mean2, tp.rstd2, vecs["ln2_g"], g_x1, pg2, pb2,
                       resid_grad=g_out, dx_masked=g_proj, dropout=drop)
-    ops.colsum_finish(pg, nbl_cur, G["ln2_g"])
-    ops.colsum_finish(pb, nbl_cur, G["ln2_b"])
     # relative-position attention
     ops.gemm(tp.ctx, g_proj, a_mn=True, b_mn=True, out=G["wo"])
     g_ctx = ws.get("g_ctx", (Nt, d), cdt)
@@ -200,5 +198,7 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
                           pg[nbl_cur:], pb[nbl_cur:])
     ops.layernorm_bwd(g_a[BM:], tp.xa[BM:], tp.mean1[BM:], tp.rstd1[BM:], vecs["ln1_g"], g_x, pg[:nbl_cur],
                       pb[:nbl_cur], resid_grad=g_x1)
-    ops.colsum_finish(pg, nbl_cur + nbl_mem, G["ln1_g"])
-    ops.colsum_finish(pb, nbl_cur + nbl_mem, G["ln1_b"])
+    # every bias / gain column sum of the block finished in one launch
+    ops.colsum_finish_multi([(pm, nbm, G["b2"]), (part[:, :f], nbc, G["b1"]), (pg2, nbl_cur, G["ln2_g"]),
+                             (pb2, nbl_cur, G["ln2_b"]), (pg, nbl_cur + nbl_mem, G["ln1_g"]),
+                             (pb, nbl_cur + nbl_mem, G["ln1_b"])])
