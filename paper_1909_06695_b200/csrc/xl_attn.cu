@@ -615,6 +615,8 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
                 const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
                 float scale, cudaStream_t st) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: head dim must be 64 (got %d)", dh);
+  // dBD chunks are TMA-stored at column T - 128 - i0 + 128 n: 16-byte aligned only for T % 8 == 0
+  if (Tn % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: T must be a multiple of 8 (got %lld)", (long long)Tn);
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
   if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: ldp must be >= M+T and a multiple of 8");
   if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: mem_len out of range");

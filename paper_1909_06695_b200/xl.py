@@ -83,6 +83,12 @@ def fused_ok(tp):
     return FUSED and tp.xa.dtype == torch.bfloat16 and tp.dh == 64
 
 
+def fused_bwd_ok(tp):
+    """The fused backward TMA-stores dBD chunks at column offsets T - 128 - i0
+    + 128 n, which must be 16-byte aligned: T % 8 == 0."""
+    return fused_ok(tp) and tp.T % 8 == 0
+
+
 def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     """tp.xa holds [memory; x]; writes out [B*T, d] and the tape."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
@@ -161,7 +167,7 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g3 = g_ctx_h.view(H * B, T, dh)
     g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
     g_bd = ws.get("xl_g_bd", (H, Nt, tp.ldk), cdt)
-    if fused_ok(tp):
+    if fused_bwd_ok(tp):
         # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
         with ops.span("xl_attn_bwd"):
             ops.xl_attn_bwd(g_ctx_h, tp.vh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, B, T, M, tp.mem_len, scale)

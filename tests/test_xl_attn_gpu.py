@@ -51,7 +51,7 @@ def ref_probs(qu, qv, kh, rh, B, T, M, mem_len, scale):
 
 
 @pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 3, 200, 72, 50), (2, 1, 64, 0, 0),
-                                             (1, 2, 256, 256, 100), (2, 8, 512, 512, 512)])
+                                             (1, 2, 256, 256, 100), (2, 8, 512, 512, 512), (1, 2, 100, 28, 28)])
 def test_fused_scores_softmax_matches_fp32(B, H, T, M, mem_len):
     from paper_1909_06695_b200 import ops
 
@@ -141,7 +141,7 @@ def _block(H, T, M, mem_len, fused, monkeypatch):
     return res, (P, x, mem, gout)
 
 
-@pytest.mark.parametrize("H,T,M,mem_len", [(2, 128, 128, 128), (2, 192, 64, 40)])
+@pytest.mark.parametrize("H,T,M,mem_len", [(2, 128, 128, 128), (2, 192, 64, 40), (2, 100, 36, 36)])
 def test_fused_block_tracks_unfused_and_restatement(H, T, M, mem_len, monkeypatch):
     a, (P, x, mem, gout) = _block(H, T, M, mem_len, True, monkeypatch)
     b, _ = _block(H, T, M, mem_len, False, monkeypatch)
@@ -244,3 +244,18 @@ def test_fused_xl_engine_tracks_restatement():
         assert np.array_equal(c1.emb_grad, c2.emb_grad)
         oloss, _ = ora.step(t, b.x, b.y)
         assert abs(l1 - oloss) <= 2e-2 * abs(oloss), (t, l1, oloss)
+
+
+def test_fused_backward_rejects_unaligned_segment_length():
+    """T % 8 != 0 would put dBD chunk stores off 16-byte alignment: the C ABI
+    refuses (DimensionError) and the block falls back to the unfused backward."""
+    from paper_1909_06695_b200 import ops
+    from paper_1909_06695_b200.errors import DimensionError
+
+    B, H, T, M, dh = 1, 1, 100, 28, 64
+    Kl, dev = M + T, "cuda"
+    ldp = _pad8(Kl)
+    z = lambda *s: torch.zeros(*s, device=dev, dtype=torch.bfloat16)  # noqa: E731
+    with pytest.raises(DimensionError):
+        ops.xl_attn_bwd(z(H, B * T, dh), z(H, B * Kl, dh), z(H * B, T, ldp), z(H * B, T, ldp), z(H, B * T, ldp),
+                        z(B * T, H * dh), z(B * T, H * dh), B, T, M, M, dh ** -0.5)
