@@ -181,6 +181,18 @@ int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, con
                       void* stream);
 /* per-head column sums of dQu / dQv [H, R, dh] -> d r_w_bias, d r_r_bias [H, dh] (deterministic) */
 int64_t rp_xl_bias_grad_workspace_bytes(int32_t H, int32_t dh);
+
+/* ---- adaptive tied softmax head (oracle/adaptive.py; BASELINE configs[3]) ----
+ * The contractions run on rp_gemm (RP_EPI_LSE_PARTIAL / RP_EPI_CE_GRAD); these move rows.
+ * rows_copy: dst[r, :cols] = src[r, :cols]; with aug, dst[r, cols] = val ? val[r] : val_const;
+ *            zeros up to ld_dst (builds [h | 1] and [V_head ; W_c | b_c]).
+ * rows_gather: dst[r] = src[idx[r]].  rows_scatter_add (fp32): dst[idx[r]] += src[r], rows unique. */
+int rp_rows_copy(int32_t src_dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, const float* val,
+                 float val_const, int32_t aug, int32_t dst_dtype, void* dst, int64_t ld_dst, void* stream);
+int rp_rows_gather(int32_t dtype, const void* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols,
+                   void* dst, int64_t ld_dst, void* stream);
+int rp_rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols, float* dst,
+                        int64_t ld_dst, void* stream);
 int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
                     int32_t H, int64_t R, int32_t dh, void* stream);
 

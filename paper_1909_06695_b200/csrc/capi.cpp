@@ -179,6 +179,18 @@ int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, con
   return rp::xl_softmax_bwd(dtype, grad_p, ld_scores, probs, ld_p, grad_ac, grad_bd, rows, T, M, mem_len, scale,
                             RP_S(stream));
 }
+int rp_rows_copy(int32_t src_dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, const float* val,
+                 float val_const, int32_t aug, int32_t dst_dtype, void* dst, int64_t ld_dst, void* stream) {
+  return rp::rows_copy(src_dtype, src, ld_src, rows, cols, val, val_const, aug, dst_dtype, dst, ld_dst, RP_S(stream));
+}
+int rp_rows_gather(int32_t dtype, const void* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols,
+                   void* dst, int64_t ld_dst, void* stream) {
+  return rp::rows_gather(dtype, src, ld_src, idx, n, cols, dst, ld_dst, RP_S(stream));
+}
+int rp_rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols, float* dst,
+                        int64_t ld_dst, void* stream) {
+  return rp::rows_scatter_add(src, ld_src, idx, n, cols, dst, ld_dst, RP_S(stream));
+}
 int64_t rp_xl_bias_grad_workspace_bytes(int32_t H, int32_t dh) { return rp::xl_bias_grad_workspace_bytes(H, dh); }
 int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
                     int32_t H, int64_t R, int32_t dh, void* stream) {

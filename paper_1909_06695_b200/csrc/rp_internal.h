@@ -90,6 +90,13 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
 int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
                 const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
                 float scale, cudaStream_t st);
+// adaptive softmax row movers (adaptive.cu)
+int rows_copy(int src_dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, const float* val,
+              float val_const, int aug, int dst_dtype, void* dst, int64_t ld_dst, cudaStream_t st);
+int rows_gather(int dtype, const void* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols, void* dst,
+                int64_t ld_dst, cudaStream_t st);
+int rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols, float* dst,
+                     int64_t ld_dst, cudaStream_t st);
 int64_t xl_bias_grad_workspace_bytes(int H, int dh);
 int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
                  cudaStream_t st);

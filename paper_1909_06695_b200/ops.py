@@ -405,6 +405,32 @@ def xl_attn_bwd(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx, B, T, M, mem_len, sc
                                    _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_bwd")
 
 
+def rows_copy(src, dst, cols=None, val=None, val_const=0.0, aug=False):
+    """dst[r, :cols] = src[r, :cols]; with aug, dst[r, cols] = val[r] (or val_const); zeros to dst's width."""
+    _require_cuda(src, dst)
+    rows = dst.shape[0]
+    cols = src.shape[-1] if cols is None else cols
+    if src.shape[0] != rows:
+        raise DimensionError("rows_copy: row counts differ")
+    _count(1)
+    N.check(N.lib().rp_rows_copy(_dtc(src), _ptr(src), src.stride(0), rows, cols, _ptr(val), val_const, int(aug),
+                                 _dtc(dst), _ptr(dst), dst.stride(0), _stream()), "rows_copy")
+
+
+def rows_gather(src, idx, dst):
+    _require_cuda(src, idx, dst)
+    _count(1)
+    N.check(N.lib().rp_rows_gather(_dtc(src), _ptr(src), src.stride(0), _ptr(idx), idx.numel(), src.shape[-1],
+                                   _ptr(dst), dst.stride(0), _stream()), "rows_gather")
+
+
+def rows_scatter_add(src, idx, dst):
+    _require_cuda(src, idx, dst)
+    _count(1)
+    N.check(N.lib().rp_rows_scatter_add(_ptr(src), src.stride(0), _ptr(idx), idx.numel(), src.shape[-1], _ptr(dst),
+                                        dst.stride(0), _stream()), "rows_scatter_add")
+
+
 def xl_softmax_bwd(g_p, probs, g_ac, g_bd, T, M, mem_len, scale):
     _count(1)
     rows = math.prod(probs.shape[:-1])

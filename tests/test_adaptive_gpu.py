@@ -1,0 +1,70 @@
+"""Adaptive tied softmax head on the device (paper_1909_06695_b200/adaptive.py)
+against the fp64 restatement (oracle/adaptive.py; parity unpinned at the
+reference, which has no adaptive softmax).  fp32 check mode (3-pass tf32
+GEMMs): loss rel <= 1e-5, every gradient rel-L2 <= 1e-4.  bf16 production:
+loss rel <= 1e-2, gradients rel-L2 <= 3e-2 (inputs rounded to bf16 first).
+Covers several tails, an empty tail cluster and a cutoff at the vocabulary end."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import adaptive as A  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
+
+
+def _case(N, d, vocab, cutoffs, seed, empty=None):
+    r = np.random.default_rng(seed)
+    h = r.normal(size=(N, d)) * 0.5
+    V = r.normal(size=(vocab, d)) * 0.3
+    n = len(A.clusters(cutoffs, vocab))
+    Wc = r.normal(size=(n, d)) * 0.3
+    bc = r.normal(size=n) * 0.2
+    # Zipf-like ids: the head is common, the tails rarer
+    y = np.minimum((r.pareto(1.2, size=N) * cutoffs[0] / 4).astype(np.int64), vocab - 1)
+    if empty is not None:
+        lo, hi = A.clusters(cutoffs, vocab)[empty]
+        y[(y >= lo) & (y < hi)] = 0
+    y[0] = vocab - 1
+    return h, V, Wc, bc, y
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("N,d,vocab,cutoffs,empty", [(256, 64, 1000, [200, 500, 800], None),
+                                                     (300, 128, 2048, [512, 1024], 0),
+                                                     (128, 64, 600, [100], None)])
+def test_adaptive_head_matches_restatement(dtype, N, d, vocab, cutoffs, empty):
+    from paper_1909_06695_b200.adaptive import AdaptiveHead
+
+    h, V, Wc, bc, y = _case(N, d, vocab, cutoffs, seed=N + d, empty=empty)
+    cdt = torch.float32 if dtype == "fp32" else torch.bfloat16
+    dev = "cuda"
+    hd = torch.from_numpy(h).to(dev, cdt)
+    Vd = torch.from_numpy(V).to(dev, cdt)
+    Wm = torch.from_numpy(Wc).float().to(dev)
+    bm = torch.from_numpy(bc).float().to(dev)
+    head = AdaptiveHead(vocab, d, cutoffs, dev, cdt)
+    loss = head.forward(hd, Vd, Wm, bm, y)
+    g_h = torch.empty(N, d, device=dev)
+    g_V = torch.full((vocab, d), float("nan"), device=dev)
+    g_W = torch.empty_like(Wm)
+    g_b = torch.empty_like(bm)
+    head.backward(g_h, g_V, g_W, g_b)
+    torch.cuda.synchronize()
+    # reference on the inputs the device saw (bf16-rounded for bf16)
+    hr, Vr = hd.double().cpu().numpy(), Vd.double().cpu().numpy()
+    Wr = Wm.double().cpu().numpy() if dtype == "fp32" else Wm.bfloat16().double().cpu().numpy()
+    br = bm.double().cpu().numpy() if dtype == "fp32" else bm.bfloat16().double().cpu().numpy()
+    rl, rgh, rgV, rgW, rgb = A.adaptive_loss_grad(hr, Vr, Wr, br, y, cutoffs)
+    tl, tg = (1e-5, 1e-4) if dtype == "fp32" else (1e-2, 3e-2)
+    assert abs(float(loss) - rl) <= tl * abs(rl), (float(loss), rl)
+    assert torch.isfinite(g_V).all()
+    for got, want, name in ((g_h, rgh, "h"), (g_V, rgV, "V"), (g_W, rgW, "Wc"), (g_b, rgb, "bc")):
+        assert rel(got.double().cpu().numpy(), want) <= tg, (name, rel(got.double().cpu().numpy(), want))
