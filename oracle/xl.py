@@ -27,6 +27,7 @@ import math
 
 import numpy as np
 
+from . import adaptive as A
 from . import layers as L
 from .ouroboros import OuroborosOracle
 from .rng import Stream, hash64
@@ -172,10 +173,12 @@ def xl_block_bwd(P, c, gout):
 # the XL language model: reference embedding + XL blocks + tied head
 
 
-def init_xl_params(vocab, d, f, n_blocks, seq_len, H, init_seed):
+def init_xl_params(vocab, d, f, n_blocks, seq_len, H, init_seed, cutoffs=None):
     """Draw order: V, the embedding's position table, then per block wq, wk,
     wv, wo, wr (+-1/sqrt d), r_w_bias, r_r_bias (+-1/sqrt d), w1 (+-1/sqrt d),
-    w2 (+-1/sqrt f); LayerNorm gains 1, biases 0."""
+    w2 (+-1/sqrt f); LayerNorm gains 1, biases 0.  With adaptive-softmax
+    cutoffs the projection layer last draws its cluster weights (+-1/sqrt d);
+    cluster biases 0."""
     rs = Stream(hash64(init_seed))
     sd, sf = 1.0 / math.sqrt(d), 1.0 / math.sqrt(f)
     V = rs.uniform_signed((vocab, d), sd)
@@ -192,11 +195,27 @@ def init_xl_params(vocab, d, f, n_blocks, seq_len, H, init_seed):
         P["w2"] = rs.uniform_signed((f, d), sf)
         P["b2"] = np.zeros(d)
         layers.append(P)
-    layers.append({})
+    proj = {}
+    if cutoffs:
+        n = len(A.clusters(cutoffs, vocab))
+        proj = {"cluster_weight": rs.uniform_signed((n, d), sd), "cluster_bias": np.zeros(n)}
+    layers.append(proj)
     return V, layers
 
 
-def xl_full_grads(V, layers, x, y, dropout_seed, step, p, mems, mem_len, H, train=True):
+def _head(h, V, y, P, cutoffs):
+    """(loss, g_h, dVo, projection grads): the tied head, or the adaptive
+    tied softmax (oracle/adaptive.py) when the projection has cluster params."""
+    if not cutoffs:
+        loss, g, dVo = L.head_loss_grad(h, V, y)
+        return loss, g, dVo, {}
+    d = h.shape[-1]
+    loss, g, dVo, gW, gb = A.adaptive_loss_grad(h.reshape(-1, d), V, P["cluster_weight"], P["cluster_bias"],
+                                                np.asarray(y).reshape(-1), cutoffs)
+    return loss, g.reshape(h.shape), dVo, {"cluster_weight": gW, "cluster_bias": gb}
+
+
+def xl_full_grads(V, layers, x, y, dropout_seed, step, p, mems, mem_len, H, train=True, cutoffs=None):
     """K=1 backprop of one segment.  mems: per block [B, M, d] (layer inputs
     of the previous segment).  Returns (grads, dVi, dVo, loss, new_mems)."""
     nl = len(layers)
@@ -207,8 +226,8 @@ def xl_full_grads(V, layers, x, y, dropout_seed, step, p, mems, mem_len, H, trai
         new_mems.append(h[:, h.shape[1] - M:].copy())
         h, c = xl_block_fwd(layers[i], h, mems[i - 1], mem_len, H, hash64(dropout_seed, step, i), p, train)
         caches.append(c)
-    loss, g, dVo = L.head_loss_grad(h, V, y)
-    G = {}
+    loss, g, dVo, Gp = _head(h, V, y, layers[-1], cutoffs)
+    G = {f"L{nl - 1}.{n}": a for n, a in Gp.items()}
     for i in range(nl - 2, 0, -1):
         g, Gi = xl_block_bwd(layers[i], caches[i - 1], g)
         for n, a in Gi.items():
@@ -233,15 +252,16 @@ class XLOuroborosOracle(OuroborosOracle):
     is the K=1 gradient of segment s given the memory segment s-1 left --
     exactly what `xl_full_grads` computes at step s."""
 
-    def __init__(self, V, layers, K, dropout_seed, p, H, mem_len, batch, optimizer=None, **kw):
+    def __init__(self, V, layers, K, dropout_seed, p, H, mem_len, batch, optimizer=None, cutoffs=None, **kw):
         super().__init__(V, layers, K, dropout_seed, p, optimizer, **kw)
         self.H, self.M = H, mem_len
+        self.cutoffs = cutoffs
         d = V.shape[1]
         self.mems = [np.zeros((batch, mem_len, d)) for _ in range(len(layers) - 2)]
         self.mem_valid = 0
 
     def _full_grads(self, t, x, y):
         G, dVi, dVo, loss, self.mems = xl_full_grads(self.V, self.layers, x, y, self.dropout_seed, t, self.p,
-                                                     self.mems, self.mem_valid, self.H, self.train)
+                                                     self.mems, self.mem_valid, self.H, self.train, self.cutoffs)
         self.mem_valid = self.M
         return G, dVi, dVo, loss

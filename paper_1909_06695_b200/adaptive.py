@@ -37,8 +37,8 @@ class AdaptiveHead:
     def __init__(self, vocab, d, cutoffs, device, dtype=torch.bfloat16):
         if not cutoffs or cutoffs[0] <= 0 or any(b <= a for a, b in zip(cutoffs, cutoffs[1:])) or cutoffs[-1] > vocab:
             raise DimensionError(f"adaptive softmax: bad cutoffs {cutoffs} for vocab {vocab}")
-        if d % 8:
-            raise DimensionError("adaptive softmax: d must be a multiple of 8 (TMA row pitch)")
+        if d % 8 or cutoffs[0] % 8:
+            raise DimensionError("adaptive softmax: d and the head size c_0 must be multiples of 8 (TMA 16-byte rows)")
         self.vocab, self.d, self.cutoffs, self.device, self.dtype = vocab, d, list(cutoffs), device, dtype
         self.tails = clusters(cutoffs, vocab)
         self.n = len(self.tails)
@@ -113,9 +113,10 @@ class AdaptiveHead:
         self.N = Nr
         return total
 
-    def backward(self, g_h, g_tied, g_wc, g_bc):
-        """g_h [N, d] fp32 (written), g_tied [V, d] fp32 (written: the output
-        half of the tied gradient), g_wc [n, d], g_bc [n] fp32 (written)."""
+    def backward(self, g_h, g_tied, g_wc, g_bc, alpha=1.0, accumulate=False):
+        """g_h [N, d] fp32 (written), g_tied [V, d] fp32: alpha x the output
+        half of the tied gradient, written or (accumulate) added; g_wc [n, d],
+        g_bc [n] fp32 (written).  g_tied may be None (no tied gradient)."""
         Nr, d, cdt = self.N, self.d, self.dtype
         scale = 1.0 / Nr
         dz = self._buf("dz_h", (Nr, _pad8(self.vh)), cdt)[:, : self.vh]
@@ -124,16 +125,26 @@ class AdaptiveHead:
         g_aug = self._buf("gh_aug", (Nr, self.da), torch.float32)
         ops.gemm(dz, self.w_aug, b_mn=True, out=g_aug)
         ops.rows_copy(g_aug, g_h, cols=d)
-        gw = self._buf("gw_aug", (self.vh, self.da), torch.float32)
-        ops.gemm(dz, self.h_aug, a_mn=True, b_mn=True, out=gw)
-        ops.rows_copy(gw[: self.c0], g_tied[: self.c0], cols=d)
+        def tied_out(a, b, rows_out):
+            # rows_out (+)= alpha * a^T b  (the head GEMM's fused residual add accumulates)
+            if accumulate:
+                ops.gemm(a, b, a_mn=True, b_mn=True, out=rows_out, alpha=alpha, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL,
+                         residual=rows_out)
+            else:
+                ops.gemm(a, b, a_mn=True, b_mn=True, out=rows_out, alpha=alpha)
+
+        if g_tied is not None:
+            tied_out(dz[:, : self.c0], self.h, g_tied[: self.c0])
         if self.n:
-            ops.rows_copy(gw[self.c0:], g_wc, cols=d)
-            ops.rows_copy(gw[self.c0:, d:], g_bc.view(self.n, 1), cols=1)
+            gw = self._buf("gw_aug", (self.n, self.da), torch.float32)
+            ops.gemm(dz[:, self.c0:], self.h_aug, a_mn=True, b_mn=True, out=gw)
+            ops.rows_copy(gw, g_wc, cols=d)
+            ops.rows_copy(gw[:, d:], g_bc.view(self.n, 1), cols=1)
         for k, (lo, hi) in enumerate(self.tails):
             st = self.tail_state[k]
             if st is None:
-                g_tied[lo:hi].zero_()
+                if g_tied is not None and not accumulate:
+                    g_tied[lo:hi].zero_()
                 continue
             idx, yk, hk, lse_k = st
             nk = idx.numel()
@@ -142,4 +153,5 @@ class AdaptiveHead:
             ghk = self._buf(f"gh{k}", (nk, d), torch.float32)
             ops.gemm(dzk, self.tied_c[lo:hi], b_mn=True, out=ghk)
             ops.rows_scatter_add(ghk, idx, g_h)
-            ops.gemm(dzk, hk, a_mn=True, b_mn=True, out=g_tied[lo:hi])
+            if g_tied is not None:
+                tied_out(dzk, hk, g_tied[lo:hi])

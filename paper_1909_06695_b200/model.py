@@ -25,6 +25,7 @@ from dataclasses import dataclass
 
 import torch
 
+from .adaptive import AdaptiveHead, clusters
 from . import layers as LY
 from . import ops
 from .errors import DimensionError, PartitionError, ScheduleViolation
@@ -89,11 +90,17 @@ class TransformerXLBlockLayer:
 class OutputProjectionLayer:
     kind = "projection"
 
-    def __init__(self, vocab_size, model_dim):
+    def __init__(self, vocab_size, model_dim, cutoffs=None):
+        """cutoffs: adaptive tied softmax (adaptive.py, oracle/adaptive.py):
+        the projection then owns one weight row and bias per tail cluster."""
         self.vocab_size, self.model_dim = vocab_size, model_dim
+        self.cutoffs = list(cutoffs) if cutoffs else None
+        self.n_clusters = len(clusters(self.cutoffs, vocab_size)) if self.cutoffs else 0
 
     def specs(self):
-        return [], []
+        if not self.n_clusters:
+            return [], []
+        return [("cluster_bias", (self.n_clusters,))], [("cluster_weight", (self.n_clusters, self.model_dim))]
 
 
 # ---------------------------------------------------------------------------
@@ -262,7 +269,7 @@ def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, in
 
 
 def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, n_heads, mem_len, *,
-                   dtype="bf16", device=None):
+                   dtype="bf16", device=None, cutoffs=None):
     """The Transformer-XL language model: the reference embedding and tied
     head around `n_blocks` XL blocks with `mem_len` memory rows each."""
     if model_dim % 8 or ffn_dim % 8 or (model_dim // n_heads) % 8:
@@ -273,7 +280,7 @@ def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p,
     cdt = _dtype_of(dtype)
     layers = [EmbeddingLayer(vocab_size, model_dim, seq_len, dropout_p)]
     layers += [TransformerXLBlockLayer(model_dim, ffn_dim, dropout_p, n_heads, mem_len) for _ in range(n_blocks)]
-    layers.append(OutputProjectionLayer(vocab_size, model_dim))
+    layers.append(OutputProjectionLayer(vocab_size, model_dim, cutoffs))
     storage = [LayerParams(layer, rt.device, cdt) for layer in layers]
     tied = TiedMatrix(vocab_size, model_dim, rt.device, cdt)
     with torch.cuda.device(rt.device):
@@ -315,6 +322,8 @@ def _init_params(layers, storage, tied, init_seed):
             for w in ("wq", "wk", "wv", "wo", "wr", "r_w_bias", "r_r_bias", "w1"):
                 draw(P[w], sd)
             draw(P["w2"], 1.0 / math.sqrt(layer.ffn_dim))
+        elif layer.kind == "projection" and layer.n_clusters:  # oracle/xl.py init_xl_params
+            draw(P["cluster_weight"], sd)
 
 
 # ---------------------------------------------------------------------------
@@ -492,6 +501,10 @@ class _Arena:
         if module.has_projection:
             self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
         self.head = LY.HeadState(Nt, dev) if module.has_projection else None
+        last = module.layers[-1]
+        self.adaptive = (AdaptiveHead(last.vocab_size, d, last.cutoffs, dev, cdt)
+                         if module.has_projection and last.n_clusters else None)
+        self.targets_host = None  # the adaptive head buckets rows by cluster from the host targets
 
 
 class ModuleState:
@@ -590,6 +603,7 @@ class ModuleState:
                 raise ScheduleViolation("projection module slot lacks targets")
             tt = targets if torch.is_tensor(targets) else torch.as_tensor(targets)
             arena.targets.copy_(tt.reshape(-1), non_blocking=True)
+            arena.targets_host = targets
         slot = StaleSlot(step, sample_id, arena.acts[0] if arena.acts else arena.tokens, targets, seeds, arena)
         self.slots.append(slot)
         if len(self.slots) > self.slot_capacity:
@@ -679,7 +693,13 @@ class ModuleState:
                 nxt = j + 2
             else:  # projection + fused CE head
                 h = arena.acts[-1]
-                LY.head_forward(h, self.tied.compute, arena.targets, self.vocab, arena.head, ws, flag)
+                if arena.adaptive is not None:
+                    P = st.weights(wstep)
+                    loss = arena.adaptive.forward(h, self.tied.compute, P["cluster_weight"], P["cluster_bias"],
+                                                  arena.targets_host, flag)
+                    arena.head.loss.copy_(loss)
+                else:
+                    LY.head_forward(h, self.tied.compute, arena.targets, self.vocab, arena.head, ws, flag)
                 cur = arena.head.loss
         if xl_live is not None:
             self.mem_len = xl_live  # M <= T: one segment fills the memory
@@ -734,8 +754,13 @@ class ModuleState:
         g = None
         if self.has_projection:
             g = ws.get("g_stream_a", (Nt, d), torch.float32)
-            LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
-                             emb_alpha, ws, vo_accumulate=emb is not None and not vo_overwrite)
+            if arena.adaptive is not None:
+                Gp = self.storage[-1].G
+                arena.adaptive.backward(g, vo_buf, Gp["cluster_weight"], Gp["cluster_bias"], alpha=emb_alpha,
+                                        accumulate=emb is not None and not vo_overwrite)
+            else:
+                LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
+                                 emb_alpha, ws, vo_accumulate=emb is not None and not vo_overwrite)
             loss = arena.head.loss
             if after_head is not None:
                 after_head()  # the tied gradient's output half is complete

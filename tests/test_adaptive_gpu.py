@@ -39,7 +39,7 @@ def _case(N, d, vocab, cutoffs, seed, empty=None):
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("N,d,vocab,cutoffs,empty", [(256, 64, 1000, [200, 500, 800], None),
                                                      (300, 128, 2048, [512, 1024], 0),
-                                                     (128, 64, 600, [100], None)])
+                                                     (128, 64, 600, [96], None)])
 def test_adaptive_head_matches_restatement(dtype, N, d, vocab, cutoffs, empty):
     from paper_1909_06695_b200.adaptive import AdaptiveHead
 
@@ -68,3 +68,45 @@ def test_adaptive_head_matches_restatement(dtype, N, d, vocab, cutoffs, empty):
     assert torch.isfinite(g_V).all()
     for got, want, name in ((g_h, rgh, "h"), (g_V, rgV, "V"), (g_W, rgW, "Wc"), (g_b, rgb, "bc")):
         assert rel(got.double().cpu().numpy(), want) <= tg, (name, rel(got.double().cpu().numpy(), want))
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_xl_ouroboros_with_adaptive_head_matches_restatement(K):
+    """Transformer-XL Ouroboros steps with the adaptive tied softmax as the
+    projection (fp32 check mode) against the fp64 restatement: loss rel <=
+    2e-5, every packet tensor (incl. the cluster weights / biases and the mixed
+    tied gradient) rel-L2 <= 2e-4."""
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200.data import SegmentStream
+    from oracle import ouroboros as OO
+    from oracle import xl as X
+    from oracle.rng import Stream
+
+    vocab, d, f, blocks, T, M, H, B, p, cut = 64, 32, 64, 2, 8, 8, 4, 2, 0.1, [16, 40]
+    lr = 2e-3
+    stack = MD.build_xl_stack(vocab, d, f, blocks, T, p, 5, H, M, dtype="fp32", cutoffs=cut)
+    eng = E.PipelineEngine(stack, MD.partition(stack.num_layers, K), 9)
+    gopt = O.make_optimizer("adam", O.LrSchedule(lr, "fixed"))
+    V, layers = X.init_xl_params(vocab, d, f, blocks, T, H, 5, cutoffs=cut)
+    ora = X.XLOuroborosOracle(V, layers, K, 9, p, H, M, B, OO.Adam(lambda t: lr), cutoffs=cut)
+    for k, want in layers[-1].items():
+        assert rel(stack.params[-1][k].double().cpu().numpy(), want) <= 1e-7, k
+    toks = (Stream(2).uniform((B * 8 * T + 4,)) * vocab).astype(np.int64)
+    src = SegmentStream(toks, T, B)
+    for t in range(5):
+        b = src.batch_at(t)
+        packet, loss = eng.step(t, b, gopt)
+        got = packet.cpu()
+        oloss, opk = ora.step(t, b.x, b.y)
+        assert abs(loss - oloss) <= 2e-5 * abs(oloss), (t, loss, oloss)
+        for k in range(K):
+            for key, want in opk["module_grads"][k].items():
+                g = got.module_grads[k][key]
+                if not np.any(want):
+                    assert not np.any(g), (t, k, key)
+                else:
+                    assert rel(g, want) <= 2e-4, (t, k, key, rel(g, want))
+        if np.any(opk["emb_grad"]):
+            assert rel(got.emb_grad, opk["emb_grad"]) <= 2e-4
