@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Ouroboros training throughput on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c3|c5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c3|c4|c5]
                   [--mode replicas|ouroboros] [--no-cpu] [--no-compare-k1]
 
 A "step" is one Ouroboros training step (reference PipelineEngine.step,
@@ -48,6 +48,12 @@ CONFIGS = {
     # (heads / memory / batch from the public XL scripts)
     "c3": dict(name="XL-12L-d512-H8-T512-M512-enwik8shape", vocab=256, d=512, f=2048, blocks=12, seq=512, batch=22,
                p=0.1, heads=8, mem=512),
+    # BASELINE.json configs[3]: Transformer-XL with the adaptive tied softmax over a
+    # WikiText-103-shaped vocabulary (cutoffs 20k / 40k / 200k, public XL scripts).
+    # The published d 410 / 10 heads x 41 break the 16-byte TMA row pitch; the
+    # nearest runnable shape is d 400 = 10 heads x 40, d_ff 2104 (= 2100 rounded to 8)
+    "c4": dict(name="XL-16L-d400(410)-H10x40-T150-M150-adaptive-WT103shape", vocab=267735, d=400, f=2104, blocks=16,
+               seq=150, batch=60, p=0.1, heads=10, mem=150, cutoffs=[20000, 40000, 200000]),
     # BASELINE.json configs[4]: Transformer-XL large, text8-shaped (27 symbols)
     "c5": dict(name="XL-24L-d1024-H8-T768-M768-text8shape", vocab=27, d=1024, f=3072, blocks=24, seq=768,
                batch=16, p=0.1, heads=8, mem=768),
@@ -59,7 +65,7 @@ def make_stack(c, seed, dtype="bf16"):
 
     if c.get("heads"):
         return M.build_xl_stack(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["p"], seed, c["heads"],
-                                c["mem"], dtype=dtype)
+                                c["mem"], dtype=dtype, cutoffs=c.get("cutoffs"))
     return M.build_stack(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["p"], seed, dtype=dtype)
 
 
@@ -68,9 +74,17 @@ def flops_per_token(c):
     reference block  F_fwd = n*(2(4d^2+2df) + 2d(T+1)) + 2dV,
     XL block         F_fwd = n*(2(2d^2 + 2d^2(M+T)/T + 2df) + 6d(M+(T+1)/2)) + 2dV."""
     d, f, T, V, n = c["d"], c["f"], c["seq"], c["vocab"], c["blocks"]
+    head = 2 * d * V
+    if c.get("cutoffs"):
+        # adaptive head: the head cluster for every token, a tail cluster's
+        # width for the (Zipf) share of tokens that fall in it
+        cut = list(c["cutoffs"]) + [V]
+        w = 1.0 / np.arange(1, V + 1, dtype=np.float64)
+        w /= w.sum()
+        head = 2 * d * (cut[0] + len(cut) - 1) + sum(2 * d * (hi - lo) * w[lo:hi].sum() for lo, hi in zip(cut, cut[1:]))
     if c.get("heads"):
         M = c["mem"]
-        fwd = n * (2 * (2 * d * d + 2 * d * d * (M + T) / T + 2 * d * f) + 6 * d * (M + (T + 1) / 2)) + 2 * d * V
+        fwd = n * (2 * (2 * d * d + 2 * d * d * (M + T) / T + 2 * d * f) + 6 * d * (M + (T + 1) / 2)) + head
     else:
         fwd = n * (2 * (4 * d * d + 2 * d * f) + 2 * d * (T + 1)) + 2 * d * V
     return 3 * fwd
@@ -150,8 +164,9 @@ def cpu_oracle_steps(c, K, steps, batch=1, budget_s=None):
     if c.get("heads"):
         from oracle import xl as OX
 
-        V, layers = OX.init_xl_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["heads"], 1)
-        ora = OX.XLOuroborosOracle(V, layers, K, 3, c["p"], c["heads"], c["mem"], batch, opt)
+        V, layers = OX.init_xl_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["heads"], 1,
+                                      cutoffs=c.get("cutoffs"))
+        ora = OX.XLOuroborosOracle(V, layers, K, 3, c["p"], c["heads"], c["mem"], batch, opt, cutoffs=c.get("cutoffs"))
     else:
         V, layers = OO.init_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], 1)
         ora = OO.OuroborosOracle(V, layers, K, 3, c["p"], opt)

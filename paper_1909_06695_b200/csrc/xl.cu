@@ -497,7 +497,7 @@ int64_t xl_bias_grad_workspace_bytes(int H, int dh) { return (int64_t)2 * H * kB
 
 int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
                  cudaStream_t st) {
-  if (dh > kThreads || kThreads % dh) return set_error(RP_ERR_DIMENSION, "xl_bias_grad: head dim must divide 256");
+  if (dh > kThreads) return set_error(RP_ERR_DIMENSION, "xl_bias_grad: head dim must be <= 256");
   bias_partial_kernel<<<dim3(kBiasChunks, H, 2), kThreads, 0, st>>>(gqu, gqv, part, H, R, dh);
   bias_finish_kernel<<<(2 * H * dh + kThreads - 1) / kThreads, kThreads, 0, st>>>(part, gu, gv, H, dh);
   return check_launch("xl_bias_grad");

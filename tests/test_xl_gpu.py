@@ -31,13 +31,14 @@ def host(t):
     return t.detach().double().cpu().numpy()
 
 
-@pytest.mark.parametrize("T,M,mem_len,H", [(8, 8, 8, 4), (8, 8, 0, 4), (12, 6, 6, 2), (8, 8, 5, 1)])
-def test_xl_block_matches_restatement(T, M, mem_len, H):
+@pytest.mark.parametrize("T,M,mem_len,H,d", [(8, 8, 8, 4, 32), (8, 8, 0, 4, 32), (12, 6, 6, 2, 32), (8, 8, 5, 1, 32),
+                                             (10, 6, 6, 2, 80)])
+def test_xl_block_matches_restatement(T, M, mem_len, H, d):
     from paper_1909_06695_b200 import layers as LY
     from paper_1909_06695_b200 import model as MD
     from paper_1909_06695_b200 import xl as XD
 
-    B, d, f = 2, 32, 48
+    B, f = 2, 48
     stack = MD.build_xl_stack(40, d, f, 1, T, 0.2, 3, H, M, dtype="fp32")
     st = stack.storage[1]
     W = st._carve(None, None, None, st.master[: st.n_vec], st.master[st.n_vec:])
