@@ -66,7 +66,7 @@ STRUCTURAL_FIELDS = (
     "ffn_dim", "dropout_p", "k", "mode", "tied_grad", "stale_weights",
     "balance", "optimizer", "lr", "lr_mode", "warmup_steps", "steps",
     "adam_beta1", "adam_beta2", "adam_eps", "seed_init", "seed_data",
-    "seed_dropout", "n_heads", "mem_len",
+    "seed_dropout", "n_heads", "mem_len", "adaptive_cutoffs",
 )
 
 
@@ -98,7 +98,8 @@ def build_runtime(cfg, synthetic_cost=None, device=None):
         # XL: contiguous segment streams so each row's memory precedes it
         source = SegmentStream(tokens, cfg.seq_len, cfg.batch_size)
         stack = build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
-                               cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=cfg.dtype, device=device)
+                               cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=cfg.dtype, device=device,
+                               cutoffs=cfg.cutoffs)
     else:
         source = BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data)
         stack = build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
@@ -381,7 +382,7 @@ def _load_masters(stack, snap):
 def _twin_stack(cfg, vocab, dtype=None):
     if cfg.n_heads:
         return build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
-                              cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=dtype or cfg.dtype)
+                              cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=dtype or cfg.dtype, cutoffs=cfg.cutoffs)
     return build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p, cfg.seed_init,
                        dtype=dtype or cfg.dtype)
 

@@ -137,6 +137,24 @@ def test_xl_train_halt_and_resume_is_bit_exact(in_gold, tmp_path, mode):
         np.testing.assert_array_equal(x[k], y[k], err_msg=k)
 
 
+def test_xl_adaptive_train_resume_and_verify(in_gold, tmp_path):
+    """A Transformer-XL run with the adaptive tied softmax through the
+    harness: halt + resume bit-exact (cluster weights in the checkpoint) and
+    verify's delayed gradients equal K=1 backprop exactly."""
+    kw = dict(mode="ouroboros-concurrent", n_heads=2, mem_len=16, k=3, adaptive_cutoffs="16,40")
+    full = R.train(cfg_for(tmp_path, "full", **kw))
+    R.train(cfg_for(tmp_path, "halt", halt_at=4, **kw))
+    resumed = R.train(cfg_for(tmp_path, "resumed", resume=str(tmp_path / "halt" / "checkpoint.bin"), **kw))
+    a = read_metrics(full["metrics_path"])[4:]
+    b = read_metrics(resumed["metrics_path"])
+    assert [(r.loss, r.grad_sq_norm) for r in a] == [(r.loss, r.grad_sq_norm) for r in b]
+    x = ckpt.load_arrays(full["checkpoint_path"])
+    assert any(k.endswith("cluster_weight") for k in x)
+    report = R.verify(cfg_for(tmp_path, "verify", **kw), steps=6)
+    assert report["passed"], report
+    assert report["oracle_max_abs"] == 0.0
+
+
 def test_verify_xl_passes_exactly(in_gold, tmp_path):
     """verify on a Transformer-XL run: the twin K=1 replay carries the segment
     memory, so every delayed gradient still matches exactly."""
