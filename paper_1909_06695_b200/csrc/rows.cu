@@ -9,6 +9,8 @@
 // reductions never use float atomics: each CTA writes a partial row and a
 // second pass sums partials in fixed order, so results are bitwise
 // reproducible for a given shape.
+#include <cstdlib>
+#include <utility>
 #include <algorithm>
 
 #include "common.cuh"
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restr
                                                                  const float* __restrict__ b, T* __restrict__ y,
                                                                  float* __restrict__ mean, float* __restrict__ rstd,
                                                                  int64_t rows, int d, int32_t* flag) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
     float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ float red[kRowWarps][2][128 * NG];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* 
                                                                     int64_t rows, int d, uint64_t seed, uint64_t pos0,
                                                                     uint64_t thr, float scale, int drop_on,
                                                                     float* __restrict__ part) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ float red[kRowWarps][128 * NG];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float acc[NG][4];
@@ -373,6 +378,7 @@ __global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __rest
 // colsum_finish_kernel, so results are bitwise identical): CTA x covers 32
 // columns of the job whose column-block range contains x.
 __global__ void __launch_bounds__(1024) colsum_finish_multi_kernel(ColsumJobs jobs) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ float red[32][33];
   int jb = 0;
   while (jb + 1 < jobs.n && (int)blockIdx.x >= jobs.first_block[jb + 1]) ++jb;
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(1024) colsum_finish_multi_kernel(ColsumJobs jo
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
                                       float* __restrict__ part) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= cols) return;
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
@@ -430,6 +437,7 @@ __global__ void mask_grad_kernel(const float* __restrict__ g, T* __restrict__ ou
 template <typename T, int NPL>
 __global__ void __launch_bounds__(kRowThreads) softmax_causal_kernel(const float* __restrict__ s, T* __restrict__ p,
                                                                       int64_t rows, int Tn, int64_t ld) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -466,6 +474,7 @@ template <typename T, int NPL>
 __global__ void __launch_bounds__(kRowThreads) softmax_bwd_kernel(const float* __restrict__ gp, const T* __restrict__ p,
                                                                    T* __restrict__ gs, float scale, int64_t rows,
                                                                    int Tn, int64_t ld) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -498,6 +507,34 @@ inline int npl_for(int64_t n) {
   if (n <= 1024) return 32;
   if (n <= 2048) return 64;
   return -1;
+}
+
+// Programmatic dependent launch for the row kernels: a launch may begin
+// while the previous kernel on the stream drains; every kernel below waits
+// (griddepcontrol.wait) before touching global memory.  RP_ROW_PDL=0 turns
+// it off (A/B).
+inline bool row_pdl() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RP_ROW_PDL");
+    const char* g = getenv("RP_NO_PDL");
+    on = ((e && e[0] == '0') || (g && g[0] == '1')) ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = row_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline int row_blocks(int64_t rows) { return (int)((rows + kRowWarps - 1) / kRowWarps); }
@@ -544,7 +581,7 @@ int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void
                   int64_t rows, int64_t d, int32_t* flag, cudaStream_t st) {
   if (rows == 0) return RP_OK;
   if (const int ng = ng_for(d)) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, ln_fwd_v4_kernel<T, NG><<<row_blocks(rows), kRowThreads, 0, st>>>(
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_fwd_v4_kernel<T, NG>, row_blocks(rows), kRowThreads, 0, st, 
                                                     (const T*)x, g, b, (T*)y, mean, rstd, rows, (int)d, flag)));
     return check_launch("layernorm_fwd");
   }
@@ -561,7 +598,7 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
   if (rows == 0) return RP_OK;
   const int nb = ln_bwd_blocks(rows);
   if (const int ng = ng_for(d)) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, ln_bwd_v4_kernel<T, NG><<<nb, kRowThreads, 0, st>>>(
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st, 
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,
                                                     seed, thr, scale, drop_on, part_g, part_b, rows, (int)d)));
     return check_launch("layernorm_bwd");
@@ -591,7 +628,7 @@ int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st) {
     blocks += (int)((jobs[i].cols + 31) / 32);
   }
   if (blocks == 0) return RP_OK;
-  colsum_finish_multi_kernel<<<blocks, 1024, 0, st>>>(J);
+  launch_pdl(colsum_finish_multi_kernel, blocks, 1024, 0, st, J);
   return check_launch("colsum_finish_multi");
 }
 
@@ -604,7 +641,7 @@ int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
 int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st) {
   if (cols == 0) return RP_OK;
   dim3 grid(colsum_blocks(rows), (unsigned)((cols + 127) / 128));
-  RP_DTYPE_DISPATCH(dtype, colsum_partial_kernel<T><<<grid, 128, 0, st>>>((const T*)x, rows, cols, ld, part));
+  RP_DTYPE_DISPATCH(dtype, launch_pdl(colsum_partial_kernel<T>, grid, 128, 0, st, (const T*)x, rows, cols, ld, part));
   return check_launch("colsum_partial");
 }
 
@@ -612,7 +649,7 @@ int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uin
               uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st) {
   if (d == 0) return RP_OK;
   if (const int ng = ng_for(d)) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, mask_grad_v4_kernel<T, NG><<<ln_bwd_blocks(rows), kRowThreads, 0, st>>>(
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(mask_grad_v4_kernel<T, NG>, ln_bwd_blocks(rows), kRowThreads, 0, st, 
                                                     g, (T*)out, rows, (int)d, seed, pos0, thr, scale, drop_on, part)));
     return check_launch("mask_grad");
   }
@@ -627,7 +664,7 @@ int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uin
 int softmax_causal(int dtype, const float* s, void* p, int64_t rows, int64_t Tn, int64_t ld, cudaStream_t st) {
   if (rows == 0) return RP_OK;
   const int npl = npl_for(Tn);
-  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, softmax_causal_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, launch_pdl(softmax_causal_kernel<T, NPL>, row_blocks(rows), kRowThreads, 0, st, 
                                                     s, (T*)p, rows, (int)Tn, ld)));
   return check_launch("softmax_causal");
 }
@@ -636,7 +673,7 @@ int softmax_bwd(int dtype, const float* gp, const void* p, void* gs, float scale
                 int64_t ld, cudaStream_t st) {
   if (rows == 0) return RP_OK;
   const int npl = npl_for(Tn);
-  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, softmax_bwd_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
+  RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, launch_pdl(softmax_bwd_kernel<T, NPL>, row_blocks(rows), kRowThreads, 0, st, 
                                                     gp, (const T*)p, (T*)gs, scale, rows, (int)Tn, ld)));
   return check_launch("softmax_bwd");
 }
