@@ -109,20 +109,34 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
     float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  __shared__ float red[kRowWarps][2][128 * NG];
+  // wide rows (NG > 4, d >= 1024): the gain and the residual gradient are
+  // read where they are used instead of living in registers
+  constexpr bool kLean = NG > 4;
+  __shared__ float red[kRowWarps][2][128];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
+  float acc_g[NG][4], acc_b[NG][4], gv[kLean ? 1 : NG][4];
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
-    gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+    if constexpr (!kLean) {
+      const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
+      gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
   }
+  auto gain = [&](int i, float (&o)[4]) {
+    if constexpr (kLean) {
+      const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
+      o[0] = gg.x; o[1] = gg.y; o[2] = gg.z; o[3] = gg.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = gv[kLean ? 0 : i][q];
+    }
+  };
   const int64_t stride = (int64_t)gridDim.x * kRowWarps;
   for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
     const float mu = mean[row], rs = rstd[row];
-    float xh[NG][4], dyv[NG][4], rv[NG][4];
+    float xh[NG][4], dyv[NG][4], rv[kLean ? 1 : NG][4];
     float s1 = 0.f, s2 = 0.f;
     // every load of the row is issued up front (the residual gradient too):
     // one DRAM round trip per row instead of two
@@ -131,18 +145,22 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
       const int j = (i * 32 + lane) * 4;
       V4<T>::ld(x + row * d + j, xh[i]);
       V4<float>::ld(dy + row * d + j, dyv[i]);
-      if (resid_grad) {
-        V4<float>::ld(resid_grad + row * d + j, rv[i]);
-      } else {
-        rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+      if constexpr (!kLean) {
+        if (resid_grad) {
+          V4<float>::ld(resid_grad + row * d + j, rv[i]);
+        } else {
+          rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+        }
       }
     }
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
+      float gq[4];
+      gain(i, gq);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         xh[i][q] = (xh[i][q] - mu) * rs;
-        const float t = dyv[i][q] * gv[i][q];
+        const float t = dyv[i][q] * gq[q];
         s1 += t;
         s2 += t * xh[i][q];
         acc_g[i][q] += dyv[i][q] * xh[i][q];
@@ -154,9 +172,21 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
+      float gq[4], r4[4];
+      gain(i, gq);
+      if constexpr (kLean) {
+        if (resid_grad) {
+          V4<float>::ld(resid_grad + row * d + j, r4);
+        } else {
+          r4[0] = r4[1] = r4[2] = r4[3] = 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r4[q] = rv[kLean ? 0 : i][q];
+      }
       float o[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
+      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gq[q] - s1 - xh[i][q] * s2) + r4[q];
       V4<float>::st(dx + row * d + j, o);
       if (dx_masked) {
         if (drop_on) {
@@ -168,23 +198,21 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
       }
     }
   }
+  // per-CTA column partials, one 128-column group at a time (warp order fixed)
 #pragma unroll
-  for (int i = 0; i < NG; ++i)
+  for (int i = 0; i < NG; ++i) {
+    if (i) __syncthreads();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      red[w][0][(i * 32 + lane) * 4 + q] = acc_g[i][q];
-      red[w][1][(i * 32 + lane) * 4 + q] = acc_b[i][q];
+      red[w][0][lane * 4 + q] = acc_g[i][q];
+      red[w][1][lane * 4 + q] = acc_b[i][q];
     }
-  __syncthreads();
-  for (int j = threadIdx.x; j < d; j += kRowThreads) {
-    float sg = 0.f, sb = 0.f;
+    __syncthreads();
+    const int which = threadIdx.x >> 7, c = threadIdx.x & 127;
+    float sacc = 0.f;
 #pragma unroll
-    for (int q = 0; q < kRowWarps; ++q) {
-      sg += red[q][0][j];
-      sb += red[q][1][j];
-    }
-    part_g[(int64_t)blockIdx.x * d + j] = sg;
-    part_b[(int64_t)blockIdx.x * d + j] = sb;
+    for (int q = 0; q < kRowWarps; ++q) sacc += red[q][which][c];
+    (which ? part_b : part_g)[(int64_t)blockIdx.x * d + i * 128 + c] = sacc;
   }
 }
 
@@ -568,13 +596,14 @@ int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
     case 1: { constexpr int NG = 1; __VA_ARGS__; break; } \
     case 2: { constexpr int NG = 2; __VA_ARGS__; break; } \
     case 4: { constexpr int NG = 4; __VA_ARGS__; break; } \
+    case 8: { constexpr int NG = 8; __VA_ARGS__; break; } \
     default: break;                                 \
   }
 
 inline int ng_for(int64_t d) {
   if (d % 128 != 0) return 0;
   const int64_t ng = d / 128;
-  return (ng == 1 || ng == 2 || ng == 4) ? (int)ng : 0;
+  return (ng == 1 || ng == 2 || ng == 4 || ng == 8) ? (int)ng : 0;
 }
 
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
