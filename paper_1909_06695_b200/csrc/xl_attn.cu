@@ -37,25 +37,32 @@ namespace {
 
 constexpr int kQT = 128;                  // query rows per CTA
 constexpr int kKT = 128;                  // keys per backward step
-constexpr int kRowBytes = 128;            // dh = 64 bf16
-constexpr int kQBytes = kQT * kRowBytes;  // 16 KB
+constexpr int kRowBytes = 128;            // one 128B-swizzle atom: 64 bf16 of the head dim
 constexpr int kStages = 2;
 constexpr int kSoftWarps = 8;
 // forward: 64 keys per step, so two steps' accumulators (AC 64 + band 192
 // columns each) fit TMEM and the MMA of step n+1 overlaps the softmax of n
 constexpr int kFKT = 64;                  // keys per forward step
 constexpr int kFBand = kFKT + 128;        // relative-encoding rows per forward step (covers 127 + 64 distances)
-constexpr int kFKBytes = kFKT * kRowBytes;     // 8 KB
-constexpr int kFRBytes = kFBand * kRowBytes;   // 24 KB
-constexpr int kFStageBytes = kFKBytes + kFRBytes;
-constexpr int kFStages = 3;
+// NA = head dim / 64 atoms: a tile of R rows is NA [R x 64] swizzle atoms
+template <int NA>
+struct FwdCfg {
+  static constexpr int QBytes = kQT * kRowBytes * NA;
+  static constexpr int KBytes = kFKT * kRowBytes * NA;
+  static constexpr int RBytes = kFBand * kRowBytes * NA;
+  static constexpr int StageBytes = KBytes + RBytes;
+  static constexpr int Stages = NA == 1 ? 3 : 1;  // dh 128: one stage keeps Q + ring in smem
+};
 constexpr int kFBuf = 256;                // TMEM columns per accumulator buffer
 constexpr int kRing = 66;                 // floats per staged band row: 2 chunks of 32, stride == 2 (mod 32)
 constexpr int kRingWarp = 32 * kRing;
 constexpr int kThreadsFwd = 384;
 constexpr int kTmemCols = 512;
-constexpr int kSmemFwd = 1024 /*align*/ + 2 * kQBytes + kFStages * kFStageBytes + kSoftWarps * kRingWarp * 4 +
-                         2 * kQT * 2 * 4 /*stats*/ + 128 /*barriers*/;
+template <int NA>
+constexpr int smem_fwd() {
+  return 1024 /*align*/ + 2 * FwdCfg<NA>::QBytes + FwdCfg<NA>::Stages * FwdCfg<NA>::StageBytes +
+         kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 128 /*barriers*/;
+}
 
 struct FwdParams {
   __nv_bfloat16* p;
@@ -83,6 +90,20 @@ __device__ __forceinline__ void stage_band(float* ring_row, int slot, const uint
   for (int t = 0; t < 16; ++t) dst[t] = make_float2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
 }
 
+// TMA-load NA swizzle atoms of a [rows x 64 NA] tile (atom a at + a * rows * 128 B)
+template <int NA>
+__device__ __forceinline__ void tma_atoms(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int rows, int r0,
+                                          int b) {
+#pragma unroll
+  for (int a = 0; a < NA; ++a) tma_load_3d(dst + a * rows * kRowBytes, map, bar, 64 * a, r0, b);
+}
+// K-major SW128 descriptor of k-step k (16 elements) of an NA-atom tile of `rows` rows
+template <int NA>
+__device__ __forceinline__ uint64_t atom_desc(uint32_t base, int rows, int k) {
+  return umma_desc(base + (k >> 2) * rows * kRowBytes + 32 * (k & 3), 16, 1024);
+}
+
+template <int NA>
 __global__ void __launch_bounds__(kThreadsFwd, 1)
     xl_attn_fwd_kernel(const __grid_constant__ CUtensorMap mQu, const __grid_constant__ CUtensorMap mQv,
                        const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
@@ -90,9 +111,10 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sQu = smem;
-  uint8_t* sQv = smem + kQBytes;
-  uint8_t* stages = smem + 2 * kQBytes;
-  float* ring = reinterpret_cast<float*>(stages + kFStages * kFStageBytes);
+  using C = FwdCfg<NA>;
+  uint8_t* sQv = smem + C::QBytes;
+  uint8_t* stages = smem + 2 * C::QBytes;
+  float* ring = reinterpret_cast<float*>(stages + C::Stages * C::StageBytes);
   float* stats = ring + kSoftWarps * kRingWarp;  // [half][row][max, sum]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stats + 2 * kQT * 2);
   uint64_t* q_full = bars;
@@ -119,7 +141,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < kFStages; ++s) {
+    for (int s = 0; s < C::Stages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
@@ -139,19 +161,19 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_expect_tx(q_full, 2 * kQBytes);
-      tma_load_3d(sQu, &mQu, q_full, 0, i0, hb);
-      tma_load_3d(sQv, &mQv, q_full, 0, i0, hb);
+      mbar_expect_tx(q_full, 2 * C::QBytes);
+      tma_atoms<NA>(sQu, &mQu, q_full, kQT, i0, hb);
+      tma_atoms<NA>(sQv, &mQv, q_full, kQT, i0, hb);
       int s = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nsteps; ++n) {
         mbar_wait(&kv_empty[s], ph ^ 1);
         const int j0 = (jt_lo + n % per_pass) * kFKT;
-        uint8_t* sk = stages + s * kFStageBytes;
-        mbar_expect_tx(&kv_full[s], kFStageBytes);
-        tma_load_3d(sk, &mK, &kv_full[s], 0, j0, hb);
-        tma_load_3d(sk + kFKBytes, &mR, &kv_full[s], 0, p.T - kQT - i0 + j0, h);
-        if (++s == kFStages) {
+        uint8_t* sk = stages + s * C::StageBytes;
+        mbar_expect_tx(&kv_full[s], C::StageBytes);
+        tma_atoms<NA>(sk, &mK, &kv_full[s], kFKT, j0, hb);
+        tma_atoms<NA>(sk + C::KBytes, &mR, &kv_full[s], kFBand, p.T - kQT - i0 + j0, h);
+        if (++s == C::Stages) {
           s = 0;
           ph ^= 1;
         }
@@ -171,20 +193,19 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
         mbar_wait(&s_empty[buf], ((n >> 1) & 1) ^ 1);
         mbar_wait(&kv_full[s], ph);
         tc_fence_after();
-        const uint32_t kb = smem_u32(stages + s * kFStageBytes), rb = kb + kFKBytes;
+        const uint32_t kb = smem_u32(stages + s * C::StageBytes), rb = kb + C::KBytes;
         const uint32_t d = tmem_base + buf * kFBuf;
         if (!(p.dbg & 2)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc_mma<false>(d, umma_desc(qa + 32 * k, 16, 1024), umma_desc(kb + 32 * k, 16, 1024), id_ac, k > 0);
+          for (int k = 0; k < 4 * NA; ++k)
+            tc_mma<false>(d, atom_desc<NA>(qa, kQT, k), atom_desc<NA>(kb, kFKT, k), id_ac, k > 0);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc_mma<false>(d + kFKT, umma_desc(qb + 32 * k, 16, 1024), umma_desc(rb + 32 * k, 16, 1024), id_bd,
-                          k > 0);
+          for (int k = 0; k < 4 * NA; ++k)
+            tc_mma<false>(d + kFKT, atom_desc<NA>(qb, kQT, k), atom_desc<NA>(rb, kFBand, k), id_bd, k > 0);
         }
         tc_commit(&kv_empty[s]);
         tc_commit(&s_full[buf]);
-        if (++s == kFStages) {
+        if (++s == C::Stages) {
           s = 0;
           ph ^= 1;
         }
@@ -316,11 +337,17 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
 // replaces the fp32 dP GEMM output and the separate softmax-backward pass
 // of the unfused path.
 constexpr int kThreadsBwd = 384;
-constexpr int kGBytes = kQT * kRowBytes;    // g_ctx tile, 16 KB
-constexpr int kVBytes = kKT * kRowBytes;    // v tile, 16 KB
+template <int NA>
+struct BwdCfg {
+  static constexpr int GBytes = kQT * kRowBytes * NA;  // g_ctx tile
+  static constexpr int VBytes = kKT * kRowBytes * NA;  // v tile
+};
 constexpr int kRingChunk = kQT * 128 * 2;   // 128 rows x 128 band columns bf16 = 32 KB
 constexpr int kRingChunks = 4;
-constexpr int kSmemBwd = 1024 + kGBytes + kStages * kVBytes + kRingChunks * kRingChunk + 128;
+template <int NA>
+constexpr int smem_bwd() {
+  return 1024 + BwdCfg<NA>::GBytes + kStages * BwdCfg<NA>::VBytes + kRingChunks * kRingChunk + 128;
+}
 
 struct BwdParams {
   const __nv_bfloat16* p;  // P [HB, T, ldp]
@@ -353,12 +380,14 @@ __device__ __forceinline__ void zero_row(__nv_bfloat16* row, int64_t a, int64_t 
   for (; a < b; ++a) row[a] = z;
 }
 
+template <int NA>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     xl_attn_bwd_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
                        const __grid_constant__ CUtensorMap mBD, const BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sG = smem;
+  constexpr int kGBytes = BwdCfg<NA>::GBytes, kVBytes = BwdCfg<NA>::VBytes;
   uint8_t* stages = smem + kGBytes;
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(stages + kStages * kVBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ring) + kRingChunks * kRingChunk);
@@ -402,12 +431,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_expect_tx(g_full, kGBytes);
-      tma_load_3d(sG, &mG, g_full, 0, i0, hb);
+      tma_atoms<NA>(sG, &mG, g_full, kQT, i0, hb);
       for (int n = 0; n < nt; ++n) {
         const int s = n & 1;
         mbar_wait(&kv_empty[s], ((n >> 1) & 1) ^ 1);
         mbar_expect_tx(&kv_full[s], kVBytes);
-        tma_load_3d(stages + s * kVBytes, &mV, &kv_full[s], 0, (jt_lo + n) * kKT, hb);
+        tma_atoms<NA>(stages + s * kVBytes, &mV, &kv_full[s], kKT, (jt_lo + n) * kKT, hb);
       }
     }
   } else if (warp == 1) {
@@ -422,9 +451,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tc_fence_after();
         const uint32_t vb = smem_u32(stages + s * kVBytes);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc_mma<false>(tmem_base + s * kKT, umma_desc(ga + 32 * k, 16, 1024), umma_desc(vb + 32 * k, 16, 1024),
-                        idesc, k > 0);
+        for (int k = 0; k < 4 * NA; ++k)
+          tc_mma<false>(tmem_base + s * kKT, atom_desc<NA>(ga, kQT, k), atom_desc<NA>(vb, kKT, k), idesc, k > 0);
         tc_commit(&kv_empty[s]);
         tc_commit(&acc_full[s]);
       }
@@ -444,11 +472,11 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     // D_i = g_ctx_i . ctx_i over this head's 64 columns
     float D = 0.f;
     if (row_ok) {
-      const int64_t mo = ((int64_t)b * p.T + i) * p.d + h * 64;
+      const int64_t mo = ((int64_t)b * p.T + i) * p.d + h * (64 * NA);
       const uint4* g4 = reinterpret_cast<const uint4*>(p.gctx + mo);
       const uint4* c4 = reinterpret_cast<const uint4*>(p.ctx + mo);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 8 * NA; ++c) {
         const uint4 gu = g4[c], cu = c4[c];
         const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, cw[4] = {cu.x, cu.y, cu.z, cu.w};
 #pragma unroll
@@ -577,7 +605,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 
 int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ldp, int64_t B,
                 int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st) {
-  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd: head dim must be 64 (got %d)", dh);
+  if (dh != 64 && dh != 128) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd: head dim must be 64 or 128 (got %d)", dh);
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
   if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd: ldp must be >= M+T and a multiple of 8");
   if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd: mem_len out of range");
@@ -589,7 +617,8 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(xl_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFwd);
+    cudaFuncSetAttribute(xl_attn_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fwd<1>());
+    cudaFuncSetAttribute(xl_attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fwd<2>());
     attr = true;
   }
   FwdParams p;
@@ -606,7 +635,10 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   p.dbg = dbg;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
-  xl_attn_fwd_kernel<<<(unsigned)grid, kThreadsFwd, kSmemFwd, st>>>(mqu, mqv, mk, mr, p);
+  if (dh == 64)
+    xl_attn_fwd_kernel<1><<<(unsigned)grid, kThreadsFwd, smem_fwd<1>(), st>>>(mqu, mqv, mk, mr, p);
+  else
+    xl_attn_fwd_kernel<2><<<(unsigned)grid, kThreadsFwd, smem_fwd<2>(), st>>>(mqu, mqv, mk, mr, p);
   return check_launch("xl_attn_fwd");
 }
 
@@ -614,7 +646,7 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
 int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
                 const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
                 float scale, cudaStream_t st) {
-  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: head dim must be 64 (got %d)", dh);
+  if (dh != 64 && dh != 128) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: head dim must be 64 or 128 (got %d)", dh);
   // dBD chunks are TMA-stored at column T - 128 - i0 + 128 n: 16-byte aligned only for T % 8 == 0
   if (Tn % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd: T must be a multiple of 8 (got %lld)", (long long)Tn);
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
@@ -628,7 +660,8 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 128, kQT, false));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(xl_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBwd);
+    cudaFuncSetAttribute(xl_attn_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bwd<1>());
+    cudaFuncSetAttribute(xl_attn_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bwd<2>());
     attr = true;
   }
   BwdParams p;
@@ -649,7 +682,10 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   p.scale = scale;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
-  xl_attn_bwd_kernel<<<(unsigned)grid, kThreadsBwd, kSmemBwd, st>>>(mg, mv, mbd, p);
+  if (dh == 64)
+    xl_attn_bwd_kernel<1><<<(unsigned)grid, kThreadsBwd, smem_bwd<1>(), st>>>(mg, mv, mbd, p);
+  else
+    xl_attn_bwd_kernel<2><<<(unsigned)grid, kThreadsBwd, smem_bwd<2>(), st>>>(mg, mv, mbd, p);
   return check_launch("xl_attn_bwd");
 }
 

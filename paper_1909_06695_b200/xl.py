@@ -78,9 +78,9 @@ FUSED = os.environ.get("RP_XL_FUSED", "1") != "0"
 
 
 def fused_ok(tp):
-    """The fused attention kernels (csrc/xl_attn.cu) take bf16, head dim 64;
+    """The fused attention kernels (csrc/xl_attn.cu) take bf16, head dim 64 or 128;
     other shapes and the fp32 check mode use the GEMM + softmax-kernel path."""
-    return FUSED and tp.xa.dtype == torch.bfloat16 and tp.dh == 64
+    return FUSED and tp.xa.dtype == torch.bfloat16 and tp.dh in (64, 128)
 
 
 def fused_bwd_ok(tp):

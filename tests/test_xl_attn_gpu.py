@@ -50,14 +50,15 @@ def ref_probs(qu, qv, kh, rh, B, T, M, mem_len, scale):
     return torch.softmax(s, dim=-1), valid
 
 
+@pytest.mark.parametrize("dh", [64, 128])
 @pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 3, 200, 72, 50), (2, 1, 64, 0, 0),
                                              (1, 2, 256, 256, 100), (2, 8, 512, 512, 512), (1, 2, 100, 28, 28)])
-def test_fused_scores_softmax_matches_fp32(B, H, T, M, mem_len):
+def test_fused_scores_softmax_matches_fp32(B, H, T, M, mem_len, dh):
     from paper_1909_06695_b200 import ops
 
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(T + M)
-    dh, Kl = 64, M + T
+    Kl = M + T
     ldp = _pad8(Kl)
     mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
     qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
@@ -102,13 +103,13 @@ def test_fused_equals_unfused_softmax_path():
     assert rel(p1.float().cpu(), p2.float().cpu()) <= 4e-3
 
 
-def _block(H, T, M, mem_len, fused, monkeypatch):
+def _block(H, T, M, mem_len, fused, monkeypatch, dh=64):
     from paper_1909_06695_b200 import layers as LY
     from paper_1909_06695_b200 import model as MD
     from paper_1909_06695_b200 import xl as XD
 
     monkeypatch.setattr(XD, "FUSED", fused)
-    B, d, f = 2, 64 * H, 128
+    B, d, f = 2, dh * H, 128
     stack = MD.build_xl_stack(40, d, f, 1, T, 0.1, 3, H, M, dtype="bf16")
     st = stack.storage[1]
     from paper_1909_06695_b200 import ops
@@ -141,10 +142,11 @@ def _block(H, T, M, mem_len, fused, monkeypatch):
     return res, (P, x, mem, gout)
 
 
-@pytest.mark.parametrize("H,T,M,mem_len", [(2, 128, 128, 128), (2, 192, 64, 40), (2, 100, 36, 36)])
-def test_fused_block_tracks_unfused_and_restatement(H, T, M, mem_len, monkeypatch):
-    a, (P, x, mem, gout) = _block(H, T, M, mem_len, True, monkeypatch)
-    b, _ = _block(H, T, M, mem_len, False, monkeypatch)
+@pytest.mark.parametrize("H,T,M,mem_len,dh", [(2, 128, 128, 128, 64), (2, 192, 64, 40, 64), (2, 100, 36, 36, 64),
+                                              (2, 128, 128, 100, 128)])
+def test_fused_block_tracks_unfused_and_restatement(H, T, M, mem_len, dh, monkeypatch):
+    a, (P, x, mem, gout) = _block(H, T, M, mem_len, True, monkeypatch, dh)
+    b, _ = _block(H, T, M, mem_len, False, monkeypatch, dh)
     for k in b:
         assert rel(a[k], b[k]) <= 1e-2, (k, rel(a[k], b[k]))
     # against fp64: no worse than the unfused bf16 path (bf16 rounding of the
@@ -173,14 +175,15 @@ def ref_bwd(probs, g3, vh, gctx, ctx, B, T, M, mem_len, scale, H, dh):
     return dS, dBD
 
 
+@pytest.mark.parametrize("dh", [64, 128])
 @pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 3, 200, 72, 50), (2, 1, 64, 0, 0),
                                              (1, 2, 256, 256, 100), (2, 8, 512, 512, 512)])
-def test_fused_softmax_backward_matches_fp32(B, H, T, M, mem_len):
+def test_fused_softmax_backward_matches_fp32(B, H, T, M, mem_len, dh):
     from paper_1909_06695_b200 import ops
 
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(7 * T + M)
-    dh, Kl = 64, M + T
+    Kl = M + T
     ldp = _pad8(Kl)
     mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
     qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
