@@ -72,7 +72,11 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restr
   bool finite = true;
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    V4<T>::ld(x + row * d + (i * 32 + lane) * 4, v[i]);
+    if ((i * 32 + lane) * 4 < d) {
+      V4<T>::ld(x + row * d + (i * 32 + lane) * 4, v[i]);
+    } else {
+      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       finite &= isfinite(v[i][q]);
@@ -83,12 +87,15 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restr
   float qv = 0.f;
 #pragma unroll
   for (int i = 0; i < NG; ++i)
+    if ((i * 32 + lane) * 4 < d) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) qv += (v[i][q] - mu) * (v[i][q] - mu);
+      for (int q = 0; q < 4; ++q) qv += (v[i][q] - mu) * (v[i][q] - mu);
+    }
   const float rs = rsqrtf(warp_sum(qv) / d + kLnEps);
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
     const int j = (i * 32 + lane) * 4;
+    if (j >= d) continue;
     const float4 gg = *reinterpret_cast<const float4*>(g + j);
     const float4 bb = *reinterpret_cast<const float4*>(b + j);
     float o[4] = {(v[i][0] - mu) * rs * gg.x + bb.x, (v[i][1] - mu) * rs * gg.y + bb.y,
@@ -118,7 +125,8 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
     if constexpr (!kLean) {
-      const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
+      const float4 gg = (i * 32 + lane) * 4 < d ? *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
       gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
     }
 #pragma unroll
@@ -126,7 +134,8 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
   }
   auto gain = [&](int i, float (&o)[4]) {
     if constexpr (kLean) {
-      const float4 gg = *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4);
+      const float4 gg = (i * 32 + lane) * 4 < d ? *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
       o[0] = gg.x; o[1] = gg.y; o[2] = gg.z; o[3] = gg.w;
     } else {
 #pragma unroll
@@ -143,6 +152,12 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
+      if (j >= d) {  // ragged width (d % 128 != 0): columns past d contribute nothing
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xh[i][q] = dyv[i][q] = 0.f;
+        if constexpr (!kLean) rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+        continue;
+      }
       V4<T>::ld(x + row * d + j, xh[i]);
       V4<float>::ld(dy + row * d + j, dyv[i]);
       if constexpr (!kLean) {
@@ -172,6 +187,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
+      if (j >= d) continue;
       float gq[4], r4[4];
       gain(i, gq);
       if constexpr (kLean) {
@@ -212,7 +228,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
     float sacc = 0.f;
 #pragma unroll
     for (int q = 0; q < kRowWarps; ++q) sacc += red[q][which][c];
-    (which ? part_b : part_g)[(int64_t)blockIdx.x * d + i * 128 + c] = sacc;
+    if (i * 128 + c < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + i * 128 + c] = sacc;
   }
 }
 
@@ -235,6 +251,7 @@ __global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* 
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = (i * 32 + lane) * 4;
+      if (j >= d) continue;
       float v[4];
       V4<float>::ld(g + row * d + j, v);
       if (drop_on) {
@@ -600,10 +617,12 @@ int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
     default: break;                                 \
   }
 
+// 128-column groups per row for the vector kernels: any d % 4 == 0 up to
+// 1024 (a ragged last group is masked); 0 = use the scalar kernels
 inline int ng_for(int64_t d) {
-  if (d % 128 != 0) return 0;
-  const int64_t ng = d / 128;
-  return (ng == 1 || ng == 2 || ng == 4 || ng == 8) ? (int)ng : 0;
+  if (d % 4 != 0 || d <= 0 || d > 1024) return 0;
+  const int64_t ng = (d + 127) / 128;
+  return ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
 }
 
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
