@@ -1062,6 +1062,22 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
 
 }  // namespace
 
+int tma_map_bf16_store32(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch) {
+  auto enc = encoder();
+  if (!enc) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * 2) % 16 != 0)
+    return set_error(RP_ERR_DIMENSION, "store map: 16-byte aligned rows required");
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)std::max<int64_t>(batch, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(ld * 2 * rows)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(RP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RP_OK;
+}
+
 int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
                  int64_t bstride, int box_inner, int box_rows, bool swizzle) {
   return make_map(map, ptr, false, inner, rows, ld, batch, bstride, box_inner, box_rows, false, swizzle);

@@ -17,6 +17,8 @@ int gemm(const rp_gemm_args& a, cudaStream_t stream);
 // 3-d bf16 TMA map (128B swizzle): dims {inner, rows, batch}; OOB reads fill zeros
 int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch,
                  int64_t bstride, int box_inner, int box_rows, bool swizzle = true);
+// 3-d bf16 map {inner, rows, batch} for 32 x 32 TMA store tiles staged with the 64B swizzle
+int tma_map_bf16_store32(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch);
 int gemm_tile_n(int64_t M, int64_t N, int64_t batch);
 // split count for a batch-1 fp32 GEMM (layers.cpp choose_splits); 1 = no split
 int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes);

@@ -58,10 +58,11 @@ constexpr int kRing = 66;                 // floats per staged band row: 2 chunk
 constexpr int kRingWarp = 32 * kRing;
 constexpr int kThreadsFwd = 384;
 constexpr int kTmemCols = 512;
+constexpr int kPStage = 32 * 64;  // per softmax warp: 32 rows x 32 bf16 of P, 64B-swizzled (TMA store)
 template <int NA>
 constexpr int smem_fwd() {
   return 1024 /*align*/ + 2 * FwdCfg<NA>::QBytes + FwdCfg<NA>::Stages * FwdCfg<NA>::StageBytes +
-         kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 128 /*barriers*/;
+         kSoftWarps * kPStage + kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 128 /*barriers*/;
 }
 
 struct FwdParams {
@@ -90,6 +91,14 @@ __device__ __forceinline__ void stage_band(float* ring_row, int slot, const uint
   for (int t = 0; t < 16; ++t) dst[t] = make_float2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
 }
 
+__device__ __forceinline__ void tma_store_3d_p(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // TMA-load NA swizzle atoms of a [rows x 64 NA] tile (atom a at + a * rows * 128 B)
 template <int NA>
 __device__ __forceinline__ void tma_atoms(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int rows, int r0,
@@ -107,14 +116,15 @@ template <int NA>
 __global__ void __launch_bounds__(kThreadsFwd, 1)
     xl_attn_fwd_kernel(const __grid_constant__ CUtensorMap mQu, const __grid_constant__ CUtensorMap mQv,
                        const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
-                       const FwdParams p) {
+                       const __grid_constant__ CUtensorMap mP, const FwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sQu = smem;
   using C = FwdCfg<NA>;
   uint8_t* sQv = smem + C::QBytes;
   uint8_t* stages = smem + 2 * C::QBytes;
-  float* ring = reinterpret_cast<float*>(stages + C::Stages * C::StageBytes);
+  uint8_t* pstage = stages + C::Stages * C::StageBytes;  // 1024-aligned
+  float* ring = reinterpret_cast<float*>(pstage + kSoftWarps * kPStage);
   float* stats = ring + kSoftWarps * kRingWarp;  // [half][row][max, sum]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stats + 2 * kQT * 2);
   uint64_t* q_full = bars;
@@ -296,28 +306,30 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
           l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
           m = mn;
         }
-      } else if (row_ok) {
+      } else {
+        // the warp's 32 rows x 32 columns of P: staged 64B-swizzled, one TMA
+        // bulk store (rows past T and columns past ldp are clipped by the map)
         uint32_t w[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
           __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2(s[2 * t] - m) * inv, ex2(s[2 * t + 1] - m) * inv);
-          w[t] = *reinterpret_cast<uint32_t*>(&b2);
+          w[t] = row_ok ? *reinterpret_cast<uint32_t*>(&b2) : 0u;
         }
-        if (jb + 32 <= p.ldp) {
-          uint4* dst = reinterpret_cast<uint4*>(prow + jb);
+        uint8_t* tile = pstage + (warp - 4) * kPStage;
+        if (lane == 0) tma_store_wait_read();  // the previous chunk's store has read the tile
+        __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) dst[c] = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&w[t]);
-            if (jb + 2 * t < p.ldp) prow[jb + 2 * t] = b2.x;
-            if (jb + 2 * t + 1 < p.ldp) prow[jb + 2 * t + 1] = b2.y;
-          }
-        }
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(tile + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        // (a box starting past the tensor's end is skipped, not issued)
+        if (lane == 0 && jb < p.ldp && i0 + 32 * q < p.T) tma_store_3d_p(&mP, tile, jb, i0 + 32 * q, hb);
       }
     }
   }
+  if (warp >= 4 && lane == 0) tma_store_wait_all();  // P tiles written before the CTA retires
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -615,6 +627,8 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   RP_TRY0(tma_map_bf16(&mqv, qv, dh, Tn, dh, HB, Tn * dh, 64, kQT));
   RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kFKT));
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
+  CUtensorMap mp;
+  RP_TRY0(tma_map_bf16_store32(&mp, probs, ldp, Tn, ldp, HB));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(xl_attn_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fwd<1>());
@@ -636,9 +650,9 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   if (dh == 64)
-    xl_attn_fwd_kernel<1><<<(unsigned)grid, kThreadsFwd, smem_fwd<1>(), st>>>(mqu, mqv, mk, mr, p);
+    xl_attn_fwd_kernel<1><<<(unsigned)grid, kThreadsFwd, smem_fwd<1>(), st>>>(mqu, mqv, mk, mr, mp, p);
   else
-    xl_attn_fwd_kernel<2><<<(unsigned)grid, kThreadsFwd, smem_fwd<2>(), st>>>(mqu, mqv, mk, mr, p);
+    xl_attn_fwd_kernel<2><<<(unsigned)grid, kThreadsFwd, smem_fwd<2>(), st>>>(mqu, mqv, mk, mr, mp, p);
   return check_launch("xl_attn_fwd");
 }
 
