@@ -358,7 +358,9 @@ constexpr int kRingChunk = kQT * 128 * 2;   // 128 rows x 128 band columns bf16 
 constexpr int kRingChunks = 4;
 template <int NA>
 constexpr int smem_bwd() {
-  return 1024 + BwdCfg<NA>::GBytes + kStages * BwdCfg<NA>::VBytes + kRingChunks * kRingChunk + 128;
+  // dh 64: dAC leaves through per-warp TMA store tiles too (dh 128 has no smem to spare: per-row stores)
+  return 1024 + BwdCfg<NA>::GBytes + kStages * BwdCfg<NA>::VBytes + kRingChunks * kRingChunk +
+         (NA == 1 ? kSoftWarps * kPStage : 0) + 128;
 }
 
 struct BwdParams {
@@ -395,14 +397,16 @@ __device__ __forceinline__ void zero_row(__nv_bfloat16* row, int64_t a, int64_t 
 template <int NA>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     xl_attn_bwd_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
-                       const __grid_constant__ CUtensorMap mBD, const BwdParams p) {
+                       const __grid_constant__ CUtensorMap mBD, const __grid_constant__ CUtensorMap mAC,
+                       const BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t* sG = smem;
   constexpr int kGBytes = BwdCfg<NA>::GBytes, kVBytes = BwdCfg<NA>::VBytes;
   uint8_t* stages = smem + kGBytes;
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(stages + kStages * kVBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ring) + kRingChunks * kRingChunk);
+  uint8_t* astage = reinterpret_cast<uint8_t*>(ring) + kRingChunks * kRingChunk;  // dAC store tiles (NA == 1)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(astage + (NA == 1 ? kSoftWarps * kPStage : 0));
   uint64_t* g_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = bars + 3;
@@ -555,7 +559,19 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
           o[t] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        if (row_ok) {
+        if constexpr (NA == 1) {
+          // the warp's 32 x 32 dAC chunk: 64B-swizzled tile, one TMA bulk store
+          uint8_t* tile = astage + (warp - 4) * kPStage;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(tile + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                row_ok ? make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]) : make_uint4(0, 0, 0, 0);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && jb < p.ldp && i0 + 32 * q < p.T) tma_store_3d_p(&mAC, tile, jb, i0 + 32 * q, hb);
+        } else if (row_ok) {
           if (jb + 32 <= p.ldp) {
             uint4* dst = reinterpret_cast<uint4*>(arow + jb);
 #pragma unroll
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
       if (warp == 4 && lane == 0) bulk_wait_read_1();
     }
-    if (warp == 4 && lane == 0) tma_store_wait_all();
+    if (lane == 0) tma_store_wait_all();  // dAC tiles (and, warp 4, the dBD chunks) written
   }
   tc_fence_before();
   __syncthreads();
@@ -672,6 +688,8 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   RP_TRY0(tma_map_bf16(&mg, gctx_h, dh, Tn, dh, HB, Tn * dh, 64, kQT));
   RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
   RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 128, kQT, false));
+  CUtensorMap mac;
+  RP_TRY0(tma_map_bf16_store32(&mac, gac, ldp, Tn, ldp, HB));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(xl_attn_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bwd<1>());
@@ -697,9 +715,9 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   if (dh == 64)
-    xl_attn_bwd_kernel<1><<<(unsigned)grid, kThreadsBwd, smem_bwd<1>(), st>>>(mg, mv, mbd, p);
+    xl_attn_bwd_kernel<1><<<(unsigned)grid, kThreadsBwd, smem_bwd<1>(), st>>>(mg, mv, mbd, mac, p);
   else
-    xl_attn_bwd_kernel<2><<<(unsigned)grid, kThreadsBwd, smem_bwd<2>(), st>>>(mg, mv, mbd, p);
+    xl_attn_bwd_kernel<2><<<(unsigned)grid, kThreadsBwd, smem_bwd<2>(), st>>>(mg, mv, mbd, mac, p);
   return check_launch("xl_attn_bwd");
 }
 
