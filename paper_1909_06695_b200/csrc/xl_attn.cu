@@ -69,6 +69,7 @@ struct FwdParams {
   __nv_bfloat16* p;
   int64_t ldp;
   int B, T, M, Kl, lo, nqt;
+  int heavy_first;  // CTA order: last (widest causal window) query tiles first
   float c2;  // scale * log2(e)
   int dbg;   // diagnostics (RP_XL_DBG): 1 = softmax warps only wait/arrive, 2 = no MMAs
 };
@@ -77,6 +78,21 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// CTA -> (head*batch, query tile).  Query tile qt sees keys up to M + 128 qt + 127,
+// so the last tiles carry the most key tiles; heavy-first issues every
+// head's last tile before any first tile (longest work first shortens the
+// tail of the ~4.8 waves at C3).
+__device__ __forceinline__ void cta_tile(int nqt, int heavy_first, int& hb, int& qt) {
+  if (heavy_first) {
+    const int nhb = gridDim.x / nqt;
+    qt = nqt - 1 - (int)blockIdx.x / nhb;
+    hb = (int)blockIdx.x % nhb;
+  } else {
+    hb = (int)blockIdx.x / nqt;
+    qt = (int)blockIdx.x % nqt;
+  }
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -135,7 +151,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hb = blockIdx.x / p.nqt, qt = blockIdx.x % p.nqt;
+  int hb, qt;
+  cta_tile(p.nqt, p.heavy_first, hb, qt);
   const int h = hb / p.B;
   const int i0 = qt * kQT;
   const int imax = min(i0 + kQT, p.T) - 1;
@@ -371,6 +388,7 @@ struct BwdParams {
   const __nv_bfloat16* ctx;   // merged ctx [B*T, d]
   int64_t ldp;
   int B, T, M, Kl, lo, nqt, H, d;
+  int heavy_first;
   float scale;
 };
 
@@ -415,7 +433,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hb = blockIdx.x / p.nqt, qt = blockIdx.x % p.nqt;
+  int hb, qt;
+  cta_tile(p.nqt, p.heavy_first, hb, qt);
   const int h = hb / p.B, b = hb % p.B;
   const int i0 = qt * kQT;
   const int imax = min(i0 + kQT, p.T) - 1;
@@ -631,6 +650,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 
 }  // namespace
 
+// RP_XL_ORDER=0 restores the (head*batch)-major CTA order (A/B switch)
+static int xl_heavy_first() {
+  static const int v = getenv("RP_XL_ORDER") ? atoi(getenv("RP_XL_ORDER")) : 1;
+  return v;
+}
+
 int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ldp, int64_t B,
                 int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st) {
   if (dh != 64 && dh != 128) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd: head dim must be 64 or 128 (got %d)", dh);
@@ -660,6 +685,7 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   p.Kl = (int)Kl;
   p.lo = (int)(M - mem_len);
   p.nqt = (int)((Tn + kQT - 1) / kQT);
+  p.heavy_first = xl_heavy_first();
   p.c2 = scale * 1.4426950408889634f;
   static const int dbg = getenv("RP_XL_DBG") ? atoi(getenv("RP_XL_DBG")) : 0;
   p.dbg = dbg;
@@ -709,6 +735,7 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   p.Kl = (int)Kl;
   p.lo = (int)(M - mem_len);
   p.nqt = (int)((Tn + kQT - 1) / kQT);
+  p.heavy_first = xl_heavy_first();
   p.H = H;
   p.d = H * dh;
   p.scale = scale;
