@@ -232,6 +232,118 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
   }
 }
 
+// Wide rows (512 < d <= 1024): a PAIR of warps owns one row, each warp 512
+// columns (4 groups, gain and residual gradient in registers as in the NG <= 4
+// kernel).  The one-warp-per-row NG = 8 kernel needs ~175 registers, so one
+// CTA (8 warps) fits an SM and the row loads of too few warps are in flight;
+// the pair kernel keeps ~128 and runs two CTAs per SM.  The row sums s1, s2
+// combine the two halves through shared memory (part 0 + part 1, the same
+// order in both warps); column partials are summed over the CTA's four
+// same-part warps in warp order.
+template <typename T>
+__global__ void __launch_bounds__(kRowThreads) ln_bwd_pair_kernel(
+    const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
+    float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int NG = 4;
+  __shared__ float red[kRowWarps][2][128];
+  __shared__ float xs[2][kRowWarps][2];  // [iteration parity][warp][s1, s2]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int part = w & 1, pair = w >> 1;
+  const int c0 = part * 512;
+  float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const int j = c0 + (i * 32 + lane) * 4;
+    const float4 gg = j < d ? *reinterpret_cast<const float4*>(g + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
+  }
+  const int64_t stride = (int64_t)gridDim.x * (kRowWarps / 2);
+  int it = 0;
+  for (int64_t row = (int64_t)blockIdx.x * (kRowWarps / 2) + pair; row < rows; row += stride, ++it) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NG][4], dyv[NG][4], rv[NG][4];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const int j = c0 + (i * 32 + lane) * 4;
+      if (j >= d) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xh[i][q] = dyv[i][q] = rv[i][q] = 0.f;
+        continue;
+      }
+      V4<T>::ld(x + row * d + j, xh[i]);
+      V4<float>::ld(dy + row * d + j, dyv[i]);
+      if (resid_grad) {
+        V4<float>::ld(resid_grad + row * d + j, rv[i]);
+      } else {
+        rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        xh[i][q] = (xh[i][q] - mu) * rs;
+        const float t = dyv[i][q] * gv[i][q];
+        s1 += t;
+        s2 += t * xh[i][q];
+        acc_g[i][q] += dyv[i][q] * xh[i][q];
+        acc_b[i][q] += dyv[i][q];
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      xs[it & 1][w][0] = s1;
+      xs[it & 1][w][1] = s2;
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    s1 = (xs[it & 1][2 * pair][0] + xs[it & 1][2 * pair + 1][0]) / d;
+    s2 = (xs[it & 1][2 * pair][1] + xs[it & 1][2 * pair + 1][1]) / d;
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const int j = c0 + (i * 32 + lane) * 4;
+      if (j >= d) continue;
+      float o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
+      V4<float>::st(dx + row * d + j, o);
+      if (dx_masked) {
+        if (drop_on) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = dropout_keep(seed, (uint64_t)row * d + j + q, thr) ? o[q] * scale : 0.f;
+        }
+        V4<T>::st(dx_masked + row * d + j, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[w][0][lane * 4 + q] = acc_g[i][q];
+      red[w][1][lane * 4 + q] = acc_b[i][q];
+    }
+    __syncthreads();
+    const int which = threadIdx.x >> 7, c = threadIdx.x & 127;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      float sacc = 0.f;
+#pragma unroll
+      for (int q = 0; q < kRowWarps / 2; ++q) sacc += red[2 * q + pp][which][c];
+      const int col = pp * 512 + i * 128 + c;
+      if (col < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + col] = sacc;
+    }
+  }
+}
+
 // out = g * mask (T) with per-CTA column partials of the masked fp32 values.
 template <typename T, int NG>
 __global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* __restrict__ g, T* __restrict__ out,
@@ -645,8 +757,15 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
                   int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st) {
   if (rows == 0) return RP_OK;
   const int nb = ln_bwd_blocks(rows);
+  static const bool pair_ok = !getenv("RP_LN_PAIR") || atoi(getenv("RP_LN_PAIR")) != 0;
+  if (ng_for(d) == 8 && pair_ok) {
+    RP_DTYPE_DISPATCH(dtype, launch_pdl(ln_bwd_pair_kernel<T>, nb, kRowThreads, 0, st, dy, (const T*)x, mean, rstd,
+                                        g, resid_grad, dx, (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
+                                        rows, (int)d));
+    return check_launch("layernorm_bwd");
+  }
   if (const int ng = ng_for(d)) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st, 
+    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st,
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,
                                                     seed, thr, scale, drop_on, part_g, part_b, rows, (int)d)));
     return check_launch("layernorm_bwd");
