@@ -232,27 +232,26 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
   }
 }
 
-// Wide rows (512 < d <= 1024): a PAIR of warps owns one row, each warp 512
-// columns (4 groups, gain and residual gradient in registers as in the NG <= 4
-// kernel).  The one-warp-per-row NG = 8 kernel needs ~175 registers, so one
-// CTA (8 warps) fits an SM and the row loads of too few warps are in flight;
-// the pair kernel keeps ~128 and runs two CTAs per SM.  The row sums s1, s2
-// combine the two halves through shared memory (part 0 + part 1, the same
-// order in both warps); column partials are summed over the CTA's four
-// same-part warps in warp order.
-template <typename T>
-__global__ void __launch_bounds__(kRowThreads) ln_bwd_pair_kernel(
+// Split rows: P warps own one row, each NG 128-column groups (gain and
+// residual gradient in registers).  The one-warp-per-row kernel at d 1024
+// needs ~175 registers, so one CTA (8 warps) fits an SM and too few row loads
+// are in flight; NG 4 keeps 128 registers (two CTAs per SM), NG 2 ~80 (three).
+// The row sums s1, s2 combine the P parts through shared memory (part order,
+// the same in every warp of the row); column partials are summed over the
+// CTA's same-part warps in warp order.
+template <typename T, int NG, int P>
+__global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
     const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
     float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  constexpr int NG = 4;
+  constexpr int kRows = kRowWarps / P;  // rows per CTA iteration
   __shared__ float red[kRowWarps][2][128];
   __shared__ float xs[2][kRowWarps][2];  // [iteration parity][warp][s1, s2]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int part = w & 1, pair = w >> 1;
-  const int c0 = part * 512;
+  const int part = w % P, pair = w / P;
+  const int c0 = part * NG * 128;
   float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
@@ -262,9 +261,9 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_pair_kernel(
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
   }
-  const int64_t stride = (int64_t)gridDim.x * (kRowWarps / 2);
+  const int64_t stride = (int64_t)gridDim.x * kRows;
   int it = 0;
-  for (int64_t row = (int64_t)blockIdx.x * (kRowWarps / 2) + pair; row < rows; row += stride, ++it) {
+  for (int64_t row = (int64_t)blockIdx.x * kRows + pair; row < rows; row += stride, ++it) {
     const float mu = mean[row], rs = rstd[row];
     float xh[NG][4], dyv[NG][4], rv[NG][4];
     float s1 = 0.f, s2 = 0.f;
@@ -302,9 +301,16 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_pair_kernel(
       xs[it & 1][w][0] = s1;
       xs[it & 1][w][1] = s2;
     }
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-    s1 = (xs[it & 1][2 * pair][0] + xs[it & 1][2 * pair + 1][0]) / d;
-    s2 = (xs[it & 1][2 * pair][1] + xs[it & 1][2 * pair + 1][1]) / d;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(32 * P) : "memory");
+    s1 = 0.f;
+    s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {  // part order, identical in every warp of the row
+      s1 += xs[it & 1][P * pair + k][0];
+      s2 += xs[it & 1][P * pair + k][1];
+    }
+    s1 /= d;
+    s2 /= d;
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       const int j = c0 + (i * 32 + lane) * 4;
@@ -334,11 +340,11 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_pair_kernel(
     __syncthreads();
     const int which = threadIdx.x >> 7, c = threadIdx.x & 127;
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < P; ++pp) {
       float sacc = 0.f;
 #pragma unroll
-      for (int q = 0; q < kRowWarps / 2; ++q) sacc += red[2 * q + pp][which][c];
-      const int col = pp * 512 + i * 128 + c;
+      for (int q = 0; q < kRows; ++q) sacc += red[P * q + pp][which][c];
+      const int col = (pp * NG + i) * 128 + c;
       if (col < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + col] = sacc;
     }
   }
@@ -757,13 +763,23 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
                   int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st) {
   if (rows == 0) return RP_OK;
   const int nb = ln_bwd_blocks(rows);
-  static const bool pair_ok = !getenv("RP_LN_PAIR") || atoi(getenv("RP_LN_PAIR")) != 0;
-  if (ng_for(d) == 8 && pair_ok) {
-    RP_DTYPE_DISPATCH(dtype, launch_pdl(ln_bwd_pair_kernel<T>, nb, kRowThreads, 0, st, dy, (const T*)x, mean, rstd,
-                                        g, resid_grad, dx, (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
-                                        rows, (int)d));
-    return check_launch("layernorm_bwd");
-  }
+  // warps per row for d > 256 (RP_LN_SPLIT: 1 = one warp per row).  Measured
+  // (tools/ln_bwd_bench.py): d 1024 two warps 106 -> 64 us (four: 70);
+  // d 512 four warps 57 -> 47 us at 22528 rows, 29 -> 23 us at 8192; d 400 27 -> 23 us
+  static const int split_env = getenv("RP_LN_SPLIT") ? atoi(getenv("RP_LN_SPLIT")) : -1;
+  const int ngd = ng_for(d);
+  int split = split_env >= 0 ? split_env : (ngd == 8 ? 2 : ngd == 4 ? 4 : 1);
+  if (ngd < 4) split = 1;
+#define RP_LN_SPLIT_LAUNCH(NGV, PV)                                                                              \
+  RP_DTYPE_DISPATCH(dtype, launch_pdl(ln_bwd_split_kernel<T, NGV, PV>, nb, kRowThreads, 0, st, dy, (const T*)x, mean, \
+                                      rstd, g, resid_grad, dx, (T*)dx_masked, seed, thr, scale, drop_on, part_g,     \
+                                      part_b, rows, (int)d));                                                        \
+  return check_launch("layernorm_bwd")
+  if (ngd == 8 && split == 2) { RP_LN_SPLIT_LAUNCH(4, 2); }
+  if (ngd == 8 && split == 4) { RP_LN_SPLIT_LAUNCH(2, 4); }
+  if (ngd == 4 && split == 2) { RP_LN_SPLIT_LAUNCH(2, 2); }
+  if (ngd == 4 && split == 4) { RP_LN_SPLIT_LAUNCH(1, 4); }
+#undef RP_LN_SPLIT_LAUNCH
   if (const int ng = ng_for(d)) {
     RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st,
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,

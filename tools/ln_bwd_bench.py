@@ -1,6 +1,6 @@
 """LayerNorm backward at the C5 shape (Transformer-XL large: 12288 rows of
 d 1024; residual gradient in, fp32 dx + dropout-masked bf16 dx out), CUDA-event
-timed.  RP_LN_PAIR=0 selects the one-warp-per-row kernel for an A/B."""
+timed.  RP_LN_SPLIT=1/2/4 sets the warps per row for an A/B."""
 import os
 import sys
 
@@ -45,4 +45,4 @@ for _ in range(20):
 ts.sort()
 us = ts[len(ts) // 2] * 1e3
 nbytes = rows * d * (4 + 2 + 4 + 4 + 2)  # dy, x, resid in; dx, dx_masked out
-print(f"ln_bwd rows {rows} d {d} pair={os.environ.get('RP_LN_PAIR', '1')}: {us:.1f} us  {nbytes / us / 1e3:.0f} GB/s")
+print(f"ln_bwd rows {rows} d {d} split={os.environ.get('RP_LN_SPLIT', 'default')}: {us:.1f} us  {nbytes / us / 1e3:.0f} GB/s")
