@@ -276,14 +276,16 @@ def run_ours(args, c):
     barrier()
     torch.cuda.synchronize()
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        s_ev.record()
-        for _ in range(args.steps):
-            x, y = dev[t % nb]
-            eng.step(t, E.BatchSample(x, y, t), opt, sync=False)
-            t += 1
-        e_ev.record()
-        torch.cuda.synchronize()
+    # clocks are sampled over the device-timed region AND the e2e windows
+    # below (the device region alone is ~0.1 s: one nvidia-smi sample)
+    clocks = ClockSampler(local).__enter__()
+    s_ev.record()
+    for _ in range(args.steps):
+        x, y = dev[t % nb]
+        eng.step(t, E.BatchSample(x, y, t), opt, sync=False)
+        t += 1
+    e_ev.record()
+    torch.cuda.synchronize()
     barrier()
     ops.PROBE = None
     ms = s_ev.elapsed_time(e_ev)
@@ -356,6 +358,7 @@ def run_ours(args, c):
         windows = sorted(e2e_window() for _ in range(3))
     finally:
         gc.enable()
+        clocks.__exit__(None, None, None)
     ms2 = windows[1]
     e2e = world * tokens * args.steps / (ms2 / 1e3)
 
