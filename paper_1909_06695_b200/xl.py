@@ -75,6 +75,11 @@ class XLTape:
 
 
 FUSED = os.environ.get("RP_XL_FUSED", "1") != "0"
+# N tile of the unfused score / dP GEMMs (N = M + T keys, K = head dim <= 64:
+# one k-block per tile, so the fp32 output epilogue dominates and 128-wide
+# tiles waste less of it than the default 256 -- C4 shape, tools/xl_score_tiles.py:
+# AC 117 -> 86 us, BD 75 -> 58 us, bitwise equal); 0 = the library default
+SCORE_TILE = int(os.environ.get("RP_XL_SCORE_TILE", "128"))
 
 
 def fused_ok(tp):
@@ -109,8 +114,8 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
         ac = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
         bd = ws.get("xl_bd", (H, B * T, tp.ldk), torch.float32)[:, :, :Kl]
         with ops.span("xl_scores"):
-            ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac)
-            ops.gemm(tp.qv, tp.rh, out=bd)
+            ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac, tile_n=SCORE_TILE)
+            ops.gemm(tp.qv, tp.rh, out=bd, tile_n=SCORE_TILE)
         ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
     ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
     ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
@@ -173,7 +178,7 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
             ops.xl_attn_bwd(g_ctx_h, tp.vh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, B, T, M, tp.mem_len, scale)
     else:
         g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
-        ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p)
+        ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p, tile_n=SCORE_TILE)
         ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
     g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
     ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
