@@ -40,3 +40,16 @@ for tile in (0, 64, 128, 256):
         ref_ac, ref_bd = ac.clone(), bd.clone()
     same = bool(torch.equal(ac, ref_ac) and torch.equal(bd, ref_bd))
     print(f"tile {tile:3d}: AC {a:6.1f} us  BD {b:6.1f} us  bitwise-equal to default: {same}")
+
+# P-reading GEMMs of the fused path: ctx_h = P v (C3: dh 64, C5: dh 128)
+for (Bq, Hq, Tq, Mq, dq) in ((22, 8, 512, 512, 64), (16, 8, 768, 768, 128)):
+    Klq = Mq + Tq
+    P = mk(Hq * Bq, Tq, Klq)
+    vq = mk(Hq * Bq, Klq, dq)
+    o = torch.empty(Hq * Bq, Tq, dq, device="cuda", dtype=torch.bfloat16)
+    ref = None
+    for tile in (0, 64, 128, 256):
+        us = t(lambda: ops.gemm(P, vq, b_mn=True, out=o, tile_n=tile))
+        if ref is None:
+            ref = o.clone()
+        print(f"PV dh {dq} tile {tile:3d}: {us:6.1f} us  bitwise-equal: {bool(torch.equal(o, ref))}")
