@@ -41,6 +41,13 @@ __device__ __forceinline__ bool dropout_keep(uint64_t seed, uint64_t pos, uint64
   return rng_bits53(seed, pos) >= thr;
 }
 
+// The splitmix64 input of position pos is z = seed + (pos + 1) * GOLDEN, so
+// runs of consecutive positions step z by GOLDEN (mod 2^64): loops over a
+// run form z once and add the constant j * GOLDEN, saving the 64-bit
+// multiply per element (bitwise the same bits as dropout_keep).
+__device__ __forceinline__ uint64_t dropout_z(uint64_t seed, uint64_t pos) { return seed + (pos + 1ull) * kGolden; }
+__device__ __forceinline__ bool dropout_keep_z(uint64_t z, uint64_t thr) { return (mix_u64(z) >> 11) >= thr; }
+
 // ---------------------------------------------------------------------------
 // type helpers
 template <typename T> struct Io;

@@ -682,10 +682,11 @@ __global__ void __launch_bounds__(384, 1)
             }
             load_bias(p, n0, full, bb);
             const uint64_t pos_row = p.drop_pos0 + (uint64_t)grow * (uint64_t)p.N + (uint64_t)n0;
+            const uint64_t z0 = dropout_z(p.drop_seed, pos_row);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               float t = fmaf(v[j], p.alpha, bb[j]);
-              if (p.drop_on) t = dropout_keep(p.drop_seed, pos_row + j, p.drop_thr) ? t * p.drop_scale : 0.f;
+              if (p.drop_on) t = dropout_keep_z(z0 + (uint64_t)j * kGolden, p.drop_thr) ? t * p.drop_scale : 0.f;
               v[j] = t + rr[j];
             }
             RP_EMIT();

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
         if (drop_on) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            o[q] = dropout_keep(seed, (uint64_t)row * d + j + q, thr) ? o[q] * scale : 0.f;
+            o[q] = dropout_keep_z(dropout_z(seed, (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? o[q] * scale : 0.f;
         }
         V4<T>::st(dx_masked + row * d + j, o);
       }
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
         if (drop_on) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            o[q] = dropout_keep(seed, (uint64_t)row * d + j + q, thr) ? o[q] * scale : 0.f;
+            o[q] = dropout_keep_z(dropout_z(seed, (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? o[q] * scale : 0.f;
         }
         V4<T>::st(dx_masked + row * d + j, o);
       }
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* 
       if (drop_on) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          v[q] = dropout_keep(seed, pos0 + (uint64_t)row * d + j + q, thr) ? v[q] * scale : 0.f;
+          v[q] = dropout_keep_z(dropout_z(seed, pos0 + (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? v[q] * scale : 0.f;
       }
       V4<T>::st(out + row * d + j, v);
 #pragma unroll
