@@ -53,30 +53,56 @@ __global__ void embed_pos_grad_kernel(const float* __restrict__ g, float* __rest
   }
 }
 
-// Single-CTA bitonic sort of (token << 32 | position) keys.
-__global__ void __launch_bounds__(1024) token_sort_kernel(const int64_t* __restrict__ tok, int n, int npow2,
-                                                          uint64_t* __restrict__ sorted) {
-  extern __shared__ uint64_t keys[];
-  for (int i = threadIdx.x; i < npow2; i += blockDim.x)
-    keys[i] = (i < n) ? ((static_cast<uint64_t>(tok[i]) << 32) | static_cast<uint32_t>(i)) : ~0ull;
+// Sort of (token << 32 | position) keys, in two launches spread over the
+// SMs (the keys are unique, so any correct sort gives the same order):
+//  1) each CTA bitonic-sorts one chunk of kSortChunk keys in shared memory
+//     (padding ~0 sorts last and is never below a real key);
+//  2) each key's global rank = its index in its own chunk + the number of
+//     keys below it in every other chunk (binary search), and it is stored
+//     at that rank.
+constexpr int kSortChunk = 1024;
+
+__global__ void __launch_bounds__(kSortChunk) token_chunk_sort_kernel(const int64_t* __restrict__ tok, int n,
+                                                                      uint64_t* __restrict__ chunks) {
+  __shared__ uint64_t keys[kSortChunk];
+  const int i = threadIdx.x, gi = blockIdx.x * kSortChunk + i;
+  keys[i] = (gi < n) ? ((static_cast<uint64_t>(tok[gi]) << 32) | static_cast<uint32_t>(gi)) : ~0ull;
   __syncthreads();
-  for (int k = 2; k <= npow2; k <<= 1) {
+  for (int k = 2; k <= kSortChunk; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const uint64_t a = keys[i], b = keys[ixj];
-          if ((a > b) == up) {
-            keys[i] = b;
-            keys[ixj] = a;
-          }
+      const int ixj = i ^ j;
+      if (ixj > i) {
+        const bool up = (i & k) == 0;
+        const uint64_t a = keys[i], b = keys[ixj];
+        if ((a > b) == up) {
+          keys[i] = b;
+          keys[ixj] = a;
         }
       }
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sorted[i] = keys[i];
+  chunks[gi] = keys[i];
+}
+
+__global__ void token_rank_kernel(const uint64_t* __restrict__ chunks, int n, int nchunk,
+                                  uint64_t* __restrict__ sorted) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= n) return;  // chunk-sorted padding sits at indices >= n
+  const uint64_t key = chunks[gi];
+  const int mine = gi / kSortChunk;
+  int rank = gi - mine * kSortChunk;
+  for (int c = 0; c < nchunk; ++c) {
+    if (c == mine) continue;
+    const uint64_t* ch = chunks + (int64_t)c * kSortChunk;
+    int lo = 0, hi = kSortChunk;  // first index with ch[idx] >= key
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (ch[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    rank += lo;
+  }
+  sorted[rank] = key;
 }
 
 // Deterministic scatter-sum of masked gradient rows into the tied gradient,
@@ -210,8 +236,11 @@ int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, voi
   return check_launch("embed_fwd");
 }
 
+// [sorted keys, padded to 256 B][row partials n*d fp32; the chunk-sorted keys
+// of the token sort live here first (consumed before the partials are written)]
 int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) {
-  return ((n_tokens * 8 + 255) / 256) * 256 + n_tokens * d * 4;
+  const int64_t chunks = (n_tokens + kSortChunk - 1) / kSortChunk * kSortChunk * 8;
+  return ((n_tokens * 8 + 255) / 256) * 256 + std::max<int64_t>(n_tokens * d * 4, chunks);
 }
 
 int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
@@ -227,17 +256,13 @@ int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t
     if (int e = check_launch("embed_pos_grad")) return e;
   }
   if (!emb || n == 0) return RP_OK;
-  int npow2 = 1;
-  while (npow2 < n) npow2 <<= 1;
-  const size_t smem = (size_t)npow2 * sizeof(uint64_t);
-  if (smem > 227 * 1024) return set_error(RP_ERR_DIMENSION, "embed_bwd: %lld tokens exceed the in-CTA sort", (long long)n);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(token_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  token_sort_kernel<<<1, 1024, smem, st>>>(tok, (int)n, npow2, work);
-  if (int e = check_launch("token_sort")) return e;
+  if (n > INT32_MAX) return set_error(RP_ERR_DIMENSION, "embed_bwd: %lld tokens", (long long)n);
+  const int nsort = (int)((n + kSortChunk - 1) / kSortChunk);
+  uint64_t* chunks = reinterpret_cast<uint64_t*>(partial);
+  token_chunk_sort_kernel<<<(unsigned)nsort, kSortChunk, 0, st>>>(tok, (int)n, chunks);
+  if (int e = check_launch("token_chunk_sort")) return e;
+  token_rank_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(chunks, (int)n, nsort, work);
+  if (int e = check_launch("token_rank")) return e;
   const int nchunk = (int)((n + kChunk - 1) / kChunk);
   const int tpb = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
   dim3 grid(nchunk, (unsigned)std::max<int64_t>(1, (d + tpb - 1) / tpb));
