@@ -38,7 +38,9 @@ typedef enum rp_status {
   RP_ERR_INVALID = 7 /* ValueError */
 } rp_status;
 
-typedef enum rp_dtype { RP_F32 = 0, RP_BF16 = 1 } rp_dtype;
+/* compute dtypes (RP_F32, RP_BF16); the integer / f64 tags appear only in
+ * state entries (rp_state_entry) */
+typedef enum rp_dtype { RP_F32 = 0, RP_BF16 = 1, RP_I64 = 2, RP_U64 = 3, RP_F64 = 4 } rp_dtype;
 
 /* Contraction arithmetic.  BF16: bf16 operands, fp32 accumulate (production).
  * TF32X3: fp32 operands split hi/lo, three tf32 passes, fp32 accumulate
@@ -201,10 +203,12 @@ int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const v
                  int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
                  int32_t drop_enabled, int32_t* flag, void* stream);
 /* grad_pos [Tmax,d] (fully written); emb[tok] += beta * sum of masked rows (deterministic
- * sorted, chunked scatter; replaces np.add.at, layers.py:135).
+ * sorted, chunked scatter; replaces np.add.at, layers.py:135).  Ids outside [0, vocab)
+ * are skipped (rp_embed_fwd already raised RP_FLAG_DIMENSION for them; the reference
+ * raises DimensionError, layers.py:116-117).
  * workspace: rp_embed_bwd_workspace_bytes(B*T, d) bytes. */
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
-                 uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
+                 int64_t vocab, uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
                  float* emb_grad, float beta, void* workspace, void* stream);
 int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
 
@@ -353,6 +357,53 @@ int rp_module_forward(const rp_module_desc* desc, const rp_module_weights* w, co
 int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot,
                        const float* g_out, float* g_in, const rp_module_grads* grads, void* workspace,
                        int64_t workspace_bytes, void* stream);
+
+/* ---- distributed context and point-to-point transfers ---------
+ * The reference's module threads hand activations and boundary gradients over
+ * by reference (engine.py:246-265, 313-373; ring placement model.py:137-140);
+ * across GPUs these are NCCL send/recv over NVLink between the ranks of one
+ * node.  NCCL is loaded at run time: RP_NCCL_LIB, else libnccl.so.2.
+ * Every rank calls rp_ctx_create with the same 128-byte id (rank 0 draws it
+ * with rp_nccl_unique_id and shares it out of band).  Transfers are
+ * asynchronous on `stream`; ordering per peer pair follows issue order, so
+ * every rank issues its relay hops in the global order k = 1..K-1 and its
+ * boundary hops in the order k = K..2 (paper_1909_06695_b200/distributed.py).
+ * A send and a receive that must progress together (including a transfer to
+ * the same rank) go between rp_group_start / rp_group_end. */
+typedef struct rp_ctx rp_ctx;
+int rp_nccl_unique_id(void* id128);
+int rp_ctx_create(int32_t device, const void* nccl_unique_id, int32_t rank, int32_t nranks, rp_ctx** out);
+int rp_ctx_destroy(rp_ctx* ctx);
+int rp_ctx_rank(const rp_ctx* ctx);
+int rp_ctx_nranks(const rp_ctx* ctx);
+/* activation relay module k -> k+1 / boundary gradient k -> k-1 (engine.py:224, 239-245) */
+int rp_send(rp_ctx* ctx, const void* buf, int64_t bytes, int32_t peer, void* stream);
+int rp_recv(rp_ctx* ctx, void* buf, int64_t bytes, int32_t peer, void* stream);
+int rp_group_start(void);
+int rp_group_end(void);
+
+/* ---- state export / import (checkpoint of the device state) ------------------
+ * The reference checkpoints weights, optimizer moments, snapshot rings, pending
+ * slots and boundary gradients under fixed names (runner.py:111-226) in the
+ * RPCK container (checkpoint.py:1-70).  A C host describes the buffers it
+ * owns (device or host) and exports them into / imports them from that
+ * container in memory; fp32 / bf16 widen to f8 exactly, so an export ->
+ * import round trip is bit-exact, and the Python host's and the reference's
+ * loaders read the result. */
+typedef struct rp_state_entry {
+  const char* name;   /* entry name, e.g. "stack.L3.wq", "m2.ring.7.L3.w1", "boundary.1" */
+  void* ptr;          /* the buffer (contiguous) */
+  int32_t dtype;      /* rp_dtype */
+  int32_t on_host;    /* 1: ptr is host memory; 0: device memory */
+  int32_t ndim;       /* <= 4 */
+  int64_t shape[4];
+} rp_state_entry;
+/* bytes of the container holding `entries` (-1 on a malformed entry) */
+int64_t rp_state_bytes(const rp_state_entry* entries, int32_t n);
+/* device/host buffers -> container in host memory `blob` (synchronous on stream) */
+int rp_export_state(const rp_state_entry* entries, int32_t n, void* blob, int64_t blob_bytes, void* stream);
+/* container -> the named buffers (by name; element counts must match) */
+int rp_import_state(const rp_state_entry* entries, int32_t n, const void* blob, int64_t blob_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -126,6 +126,13 @@ def lib():
     return _lib
 
 
+class StateEntry(ctypes.Structure):
+    """rp_state_entry (include/ringpipe_b200.h)."""
+
+    _fields_ = [("name", ctypes.c_char_p), ("ptr", ctypes.c_void_p), ("dtype", ctypes.c_int32),
+                ("on_host", ctypes.c_int32), ("ndim", ctypes.c_int32), ("shape", ctypes.c_int64 * 4)]
+
+
 def _declare(L):
     vp, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
     f32, f64 = ctypes.c_float, ctypes.c_double
@@ -148,7 +155,7 @@ def _declare(L):
         "rp_softmax_causal": [i32, vp, vp, i64, i64, i64, vp],
         "rp_softmax_bwd": [i32, vp, vp, vp, f32, i64, i64, i64, vp],
         "rp_embed_fwd": [i32, vp, vp, vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp],
-        "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, vp],
+        "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, vp],
         "rp_embed_bwd_workspace_bytes": [i64, i64],
         "rp_ce_finish": [vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp],
         "rp_adam_step": [vp, vp, vp, vp, vp, i32, i64, f32, f32, f32, f32, f32, f32, vp, vp],
@@ -183,6 +190,18 @@ def _declare(L):
         "rp_head_workspace_bytes": [ctypes.POINTER(HeadDesc)],
         "rp_head_forward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
         "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, i32, vp, i64, vp],
+        "rp_nccl_unique_id": [vp],
+        "rp_ctx_create": [i32, vp, i32, i32, ctypes.POINTER(vp)],
+        "rp_ctx_destroy": [vp],
+        "rp_ctx_rank": [vp],
+        "rp_ctx_nranks": [vp],
+        "rp_send": [vp, vp, i64, i32, vp],
+        "rp_recv": [vp, vp, i64, i32, vp],
+        "rp_group_start": [],
+        "rp_group_end": [],
+        "rp_state_bytes": [ctypes.POINTER(StateEntry), i32],
+        "rp_export_state": [ctypes.POINTER(StateEntry), i32, vp, i64, vp],
+        "rp_import_state": [ctypes.POINTER(StateEntry), i32, vp, i64, vp],
     }
     L.rp_version.restype = ctypes.c_char_p
     for name, args in sig.items():
@@ -194,6 +213,7 @@ def _declare(L):
     L.rp_block_workspace_bytes.restype = i64
     L.rp_module_workspace_bytes.restype = i64
     L.rp_head_workspace_bytes.restype = i64
+    L.rp_state_bytes.restype = i64
 
 
 def last_error():

@@ -107,9 +107,9 @@ int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const v
                        RP_S(stream));
 }
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
-                 uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
+                 int64_t vocab, uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
                  float* emb_grad, float beta, void* work, void* stream) {
-  return rp::embed_bwd(grad, tokens, B, T, Tmax, d, seed, threshold, scale, drop_enabled, grad_pos, emb_grad, beta,
+  return rp::embed_bwd(grad, tokens, B, T, Tmax, d, vocab, seed, threshold, scale, drop_enabled, grad_pos, emb_grad, beta,
                        work, RP_S(stream));
 }
 int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) { return rp::embed_bwd_workspace_bytes(n_tokens, d); }

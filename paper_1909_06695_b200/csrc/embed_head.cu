@@ -62,11 +62,22 @@ __global__ void embed_pos_grad_kernel(const float* __restrict__ g, float* __rest
 //     at that rank.
 constexpr int kSortChunk = 1024;
 
+// Ids outside [0, vocab) (the forward raised RP_FLAG_DIMENSION for them) get
+// the sentinel token kBadTok: they sort after every valid id and the
+// scatter skips them, so a bad id never addresses the tied gradient.
+constexpr uint32_t kBadTok = 0xffffffffu;
+
 __global__ void __launch_bounds__(kSortChunk) token_chunk_sort_kernel(const int64_t* __restrict__ tok, int n,
-                                                                      uint64_t* __restrict__ chunks) {
+                                                                      int64_t vocab, uint64_t* __restrict__ chunks) {
   __shared__ uint64_t keys[kSortChunk];
   const int i = threadIdx.x, gi = blockIdx.x * kSortChunk + i;
-  keys[i] = (gi < n) ? ((static_cast<uint64_t>(tok[gi]) << 32) | static_cast<uint32_t>(gi)) : ~0ull;
+  uint64_t key = ~0ull;
+  if (gi < n) {
+    const int64_t id = tok[gi];
+    const uint32_t tv = (id >= 0 && id < vocab) ? static_cast<uint32_t>(id) : kBadTok;
+    key = (static_cast<uint64_t>(tv) << 32) | static_cast<uint32_t>(gi);
+  }
+  keys[i] = key;
   __syncthreads();
   for (int k = 2; k <= kSortChunk; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -146,7 +157,7 @@ __global__ void embed_segment_kernel(const uint64_t* __restrict__ sorted, int n,
                                      int d, float beta, float* __restrict__ emb) {
   const int i = blockIdx.x;
   const uint32_t tokv = static_cast<uint32_t>(sorted[i] >> 32);
-  if (i > 0 && static_cast<uint32_t>(sorted[i - 1] >> 32) == tokv) return;
+  if (tokv == kBadTok || (i > 0 && static_cast<uint32_t>(sorted[i - 1] >> 32) == tokv)) return;
   int end = i + 1;
   // segment end: first position with a different token (scan chunk starts)
   while (end < n && static_cast<uint32_t>(sorted[end] >> 32) == tokv) {
@@ -243,7 +254,8 @@ int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) {
   return ((n_tokens * 8 + 255) / 256) * 256 + std::max<int64_t>(n_tokens * d * 4, chunks);
 }
 
-int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
+int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, int64_t vocab,
+              uint64_t seed,
               uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
               cudaStream_t st) {
   uint64_t* work = static_cast<uint64_t*>(workspace);
@@ -257,9 +269,10 @@ int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t
   }
   if (!emb || n == 0) return RP_OK;
   if (n > INT32_MAX) return set_error(RP_ERR_DIMENSION, "embed_bwd: %lld tokens", (long long)n);
+  if (vocab <= 0 || vocab >= (int64_t)kBadTok) return set_error(RP_ERR_DIMENSION, "embed_bwd: vocab %lld", (long long)vocab);
   const int nsort = (int)((n + kSortChunk - 1) / kSortChunk);
   uint64_t* chunks = reinterpret_cast<uint64_t*>(partial);
-  token_chunk_sort_kernel<<<(unsigned)nsort, kSortChunk, 0, st>>>(tok, (int)n, chunks);
+  token_chunk_sort_kernel<<<(unsigned)nsort, kSortChunk, 0, st>>>(tok, (int)n, vocab, chunks);
   if (int e = check_launch("token_chunk_sort")) return e;
   token_rank_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(chunks, (int)n, nsort, work);
   if (int e = check_launch("token_rank")) return e;

@@ -421,7 +421,7 @@ int64_t head_workspace_bytes(const rp_head_desc& h) {
   const int64_t e = esize(h.dtype);
   int64_t b = al256(h.rows * nt * 4 * 4) + al256(h.rows * 4) * 2 + al256(h.rows * pad8(h.vocab) * e);
   b += al256(kHeadSplitK * h.rows * h.d * 4);
-  b += split_bytes(h.dtype, std::max(h.rows * pad8(h.vocab), h.vocab * h.d));
+  b += split_bytes(h.dtype, std::max({h.rows * pad8(h.vocab), h.vocab * h.d, h.rows * h.d}));
   return b + 4096;
 }
 

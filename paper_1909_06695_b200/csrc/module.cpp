@@ -116,7 +116,7 @@ int module_backward(const rp_module_desc& m, const rp_module_weights& w, const r
   if (m.has_embedding) {
     const uint64_t seed = m.drop_enabled ? m.layer_seeds[0] : 0;
     float* vi = (G.tied && G.tied_beta != 0.f) ? G.tied : nullptr;
-    return embed_bwd(g, s.tokens, m.B, m.T, m.t_max, m.d, seed, m.drop_threshold, m.drop_scale, m.drop_enabled,
+    return embed_bwd(g, s.tokens, m.B, m.T, m.t_max, m.d, m.vocab, seed, m.drop_threshold, m.drop_scale, m.drop_enabled,
                      G.pos, vi, G.tied_beta, ws, st);
   }
   if (g_in && g != g_in) {

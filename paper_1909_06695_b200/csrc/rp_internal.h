@@ -59,7 +59,8 @@ int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, voi
               int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
               cudaStream_t st);
 int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
-int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, uint64_t seed,
+int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, int64_t vocab,
+              uint64_t seed,
               uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
               cudaStream_t st);
 int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,

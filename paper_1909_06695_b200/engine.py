@@ -187,10 +187,16 @@ def check_one_step_behind(trace, K):
 # executors
 
 
-def _to_device_tokens(a, device):
-    if torch.is_tensor(a):
+def _to_device_tokens(a, device, vocab=None, what="token"):
+    """Host batches are range-checked before anything launches, so a bad id
+    raises DimensionError before any update, like the reference's forward
+    (layers.py:116-117, 299-305); device batches are checked by the kernels
+    (RP_FLAG_DIMENSION, polled at step granularity)."""
+    if torch.is_tensor(a) and a.is_cuda:
         return a.to(device=device, dtype=torch.int64, non_blocking=True)
-    arr = np.ascontiguousarray(np.asarray(a), dtype=np.int64)
+    arr = np.ascontiguousarray(a.numpy() if torch.is_tensor(a) else np.asarray(a), dtype=np.int64)
+    if vocab is not None and arr.size and (arr.min() < 0 or arr.max() >= vocab):
+        raise DimensionError(f"{what} id out of range [0, {vocab})")
     return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
 
 
@@ -315,8 +321,9 @@ class PipelineEngine:
         stays a 0-d device tensor and the status word is not polled."""
         if t < 0:
             raise ValueError("step index must be >= 0")
-        x = _to_device_tokens(batch.x, self.device)
-        y = _to_device_tokens(batch.y, self.device)
+        V = self.stack.tied_store.vocab
+        x = _to_device_tokens(batch.x, self.device, V, "token")
+        y = _to_device_tokens(batch.y, self.device, V, "target")
         B, T = x.shape
         for m in self.modules:
             m.snapshot(t)
@@ -381,8 +388,9 @@ class ConcurrentPipelineEngine(PipelineEngine):
         if t < 0:
             raise ValueError("step index must be >= 0")
         main = torch.cuda.current_stream(self.device)
-        x = _to_device_tokens(batch.x, self.device)
-        y = _to_device_tokens(batch.y, self.device)
+        V = self.stack.tied_store.vocab
+        x = _to_device_tokens(batch.x, self.device, V, "token")
+        y = _to_device_tokens(batch.y, self.device, V, "target")
         B, T = x.shape
         start_ev = torch.cuda.Event()
         start_ev.record(main)
@@ -535,7 +543,52 @@ class SequentialRunner(PipelineEngine):
         return packet, loss
 
 
-def sequential_gradients(stack, batch, dropout_seed, step, train=True, module=None):
+def sequential_gradients(layers, params_list, batch, dropout_seed, step, train=True):
+    """Reference engine.py:409-440: full-network backprop at explicit weights,
+    the verification oracle.  `layers` is a stack's `.layers` list (or the
+    stack), `params_list` one dict of arrays per layer -- the live
+    `stack.params`, or a snapshot of them (numpy or torch, any dtype; the
+    embedding and projection dicts carry "tied").  The weights are loaded
+    into the stack's twin (`LayerStack.twin`), so the live weights are not
+    touched.  Returns (grads keyed "L{idx}.{name}" as host fp64 arrays,
+    grad_vi, grad_vo, loss, logits); `logits` [B, T, V] is an fp32 device
+    tensor (the training path never materialises it; at V = 267,735 it is
+    N * V * 4 bytes)."""
+    from .model import stack_of
+
+    stack = stack_of(layers)
+    if len(params_list) != stack.num_layers:
+        raise DimensionError(f"params_list has {len(params_list)} entries for {stack.num_layers} layers")
+    if stack.layers[-1].kind != "projection":
+        raise ValueError("stack must end with the output projection")
+    twin = stack.twin()
+    with torch.no_grad():
+        for idx, params in enumerate(params_list):
+            for name, arr in params.items():
+                dst = twin.tied if name == "tied" else twin.params[idx][name]
+                src = torch.as_tensor(np.asarray(arr) if not torch.is_tensor(arr) else arr)
+                if tuple(src.shape) != tuple(dst.shape):
+                    raise DimensionError(f"L{idx}.{name}: shape {tuple(src.shape)} != {tuple(dst.shape)}")
+                dst.copy_(src)
+    twin.refresh()
+    mod = getattr(twin, "_seq_module", None)
+    if mod is None:
+        from .model import build_modules, partition
+
+        (mod,) = build_modules(twin, partition(twin.num_layers, 1), dropout_seed)
+        twin._seq_module = mod
+    mod.dropout_seed = dropout_seed
+    grads, gvi, gvo, loss = stack_gradients(twin, batch, dropout_seed, step, train, module=mod)
+    # logits of the final hidden state (layers.py:268-273), on demand
+    from . import ops
+
+    h = mod._last_hidden
+    B, T = h[1]
+    logits = ops.gemm(h[0], twin.tied_store.compute, out_dtype=torch.float32).view(B, T, -1)
+    return grads, gvi, gvo, loss, logits
+
+
+def stack_gradients(stack, batch, dropout_seed, step, train=True, module=None):
     """Full backprop at the stack's current weights without touching them:
     returns (grads by key as host fp64 arrays, grad_vi, grad_vo, loss).
     `module`: a K=1 module of `stack` to reuse across calls -- it carries the
@@ -546,10 +599,12 @@ def sequential_gradients(stack, batch, dropout_seed, step, train=True, module=No
         (module,) = build_modules(stack, partition(stack.num_layers, 1), dropout_seed)
     m = module
     m.snapshot(step)
-    x = _to_device_tokens(batch.x, stack.runtime.device)
-    y = _to_device_tokens(batch.y, stack.runtime.device)
+    V = stack.tied_store.vocab
+    x = _to_device_tokens(batch.x, stack.runtime.device, V, "token")
+    y = _to_device_tokens(batch.y, stack.runtime.device, V, "target")
     loss = m.forward(x, step, batch.sample_id, y, train)
     slot = m.pop_slot()
+    m._last_hidden = (slot.arena.acts[-1], (slot.arena.B, slot.arena.T))
     _, grads, tied, _ = m.recompute_backward(slot, None, "snapshot", train)
     stack.runtime.check("sequential_gradients", [m])
     host = {k: v.double().cpu().numpy() for k, v in grads.items()}

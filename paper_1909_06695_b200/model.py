@@ -20,6 +20,7 @@ B200 layout:
 """
 
 import math
+import weakref
 from collections import deque
 from dataclasses import dataclass
 
@@ -220,8 +221,10 @@ class LayerStack:
     dicts of fp32 master views; embedding and projection dicts share the one
     `tied` tensor) and `tied`."""
 
-    def __init__(self, layers, storage, tied, runtime, cdtype):
+    def __init__(self, layers, storage, tied, runtime, cdtype, register=True):
         self.layers = layers
+        if register:
+            _STACKS[id(layers)] = weakref.ref(self)
         self.storage = storage
         self.tied_store = tied
         self.tied = tied.master
@@ -238,6 +241,18 @@ class LayerStack:
     def num_layers(self):
         return len(self.layers)
 
+    def twin(self):
+        """A second stack of the same layers on the same device (zero weights,
+        own storage), cached: the scratch model `engine.sequential_gradients`
+        evaluates explicit weights on without touching the live ones."""
+        tw = getattr(self, "_twin", None)
+        if tw is None:
+            dev = self.runtime.device
+            storage = [LayerParams(layer, dev, self.cdtype) for layer in self.layers]
+            tied = TiedMatrix(self.tied_store.vocab, self.tied_store.d, dev, self.cdtype)
+            tw = self._twin = LayerStack(self.layers, storage, tied, self.runtime, self.cdtype, register=False)
+        return tw
+
     def refresh(self):
         """Re-derive every compute copy from the fp32 masters after the caller
         edited `params` / `tied` in place (the reference's live arrays have no
@@ -245,6 +260,20 @@ class LayerStack:
         for st in self.storage:
             st.ring_step = [None] * len(st.ring)
         self.tied_store.refresh()
+
+
+_STACKS = {}  # id(stack.layers) -> weakref(stack): `layers` lists name their stack
+
+
+def stack_of(layers):
+    """The LayerStack a `layers` list (or the stack itself) belongs to."""
+    if isinstance(layers, LayerStack):
+        return layers
+    ref = _STACKS.get(id(layers))
+    st = ref() if ref is not None else None
+    if st is None or st.layers is not layers:
+        raise ValueError("layers must be the .layers list of a stack built by build_stack / build_xl_stack")
+    return st
 
 
 def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, *, dtype="bf16",

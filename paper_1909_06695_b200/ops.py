@@ -24,14 +24,21 @@ class Probe:
     def __init__(self):
         self.launches = 0
         self.events = {}  # tag -> list of (start, end)
+        self.flops = {}  # tag -> list of algorithmic FLOPs per span (tagged GEMMs)
 
-    def span(self, tag):
-        return _Span(self, tag)
+    def span(self, tag, flops=None):
+        return _Span(self, tag, flops)
+
+    def achieved(self, tag):
+        """(total FLOPs, total ms, spans) of the tagged GEMM spans (synchronize first)."""
+        ev = self.events.get(tag, [])
+        fl = self.flops.get(tag, [])
+        return float(sum(fl)), float(sum(s.elapsed_time(e) for s, e in ev)), len(ev)
 
 
 class _Span:
-    def __init__(self, probe, tag):
-        self.probe, self.tag = probe, tag
+    def __init__(self, probe, tag, flops=None):
+        self.probe, self.tag, self.flops_ = probe, tag, flops
 
     def __enter__(self):
         if self.probe is not None:
@@ -43,6 +50,8 @@ class _Span:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
             self.probe.events.setdefault(self.tag, []).append((self.s, e))
+            if self.flops_ is not None:
+                self.probe.flops.setdefault(self.tag, []).append(self.flops_)
 
 
 PROBE = None  # set to a Probe() to instrument
@@ -53,8 +62,8 @@ def _count(n=1):
         PROBE.launches += n
 
 
-def span(tag):
-    return _Span(PROBE, tag)
+def span(tag, flops=None):
+    return _Span(PROBE, tag, flops)
 
 
 def _stream():
@@ -128,13 +137,16 @@ def gemm(
     a_lo=None,
     b_lo=None,
     tile_n=0,
+    probe=None,
 ):
     """C = epilogue(alpha * opA(a) @ opB(b)) on the tcgen05 GEMM.
 
     a: [M,K] (a_mn=False) or [K,M] (a_mn=True), optionally with a leading
     batch dim.  b: [N,K] (b_mn=False, "B transposed") or [K,N] (b_mn=True).
     bf16 operands run on kind::f16; fp32 operands run the 3-pass tf32 path
-    unless math=MATH_TF32.
+    unless math=MATH_TF32.  probe: a Probe tag -- with ops.PROBE set, the
+    launch (and its split-K reduce) is bracketed by CUDA events and counted
+    as 2*M*N*K*batch algorithmic FLOPs.
     """
     _require_cuda(a, b)
     if a.dtype != b.dtype or a.dtype not in _DT:
@@ -215,12 +227,13 @@ def gemm(
         part = _splitk_scratch(out.device)
         args.k_splits = splits
         args.C, args.ldc, args.stride_c = part.data_ptr(), Nn, M * Nn
-    _count(1)
-    N.check(N.lib().rp_gemm(ctypes.byref(args), _stream()), "gemm")
-    if splits > 1:
+    with _Span(PROBE if probe else None, probe, 2.0 * M * Nn * K * batch):
         _count(1)
-        N.check(N.lib().rp_splitk_reduce(_ptr(part), splits, M, Nn, _ptr(out), out.stride(-2), _stream()),
-                "splitk_reduce")
+        N.check(N.lib().rp_gemm(ctypes.byref(args), _stream()), "gemm")
+        if splits > 1:
+            _count(1)
+            N.check(N.lib().rp_splitk_reduce(_ptr(part), splits, M, Nn, _ptr(out), out.stride(-2), _stream()),
+                    "splitk_reduce")
     return out
 
 
@@ -458,8 +471,10 @@ def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None)
     B, T = tokens.shape
     d = grad.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
+    # ids outside [0, vocab) are skipped by the scatter (the forward flagged them)
+    vocab = emb_grad.shape[0] if emb_grad is not None else 1
     _count(4)
-    N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, seed, thr, scale,
+    N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, vocab, seed, thr, scale,
                                  int(dropout is not None), _ptr(grad_pos), _ptr(emb_grad), beta, _ptr(work),
                                  _stream()), "embed_bwd")
 

@@ -46,6 +46,7 @@ from .engine import (
     WorkerFailure,
     packet_grad_sq_norm,
     sequential_gradients,
+    stack_gradients,
 )
 from .errors import DimensionError, NonFiniteError
 from .metrics import MetricsRow, MetricsWriter
@@ -218,7 +219,17 @@ def load_training_state(path, runtime):
         ours, theirs = getattr(runtime.cfg, name), saved.get(name, getattr(RunConfig(), name))
         if ours != theirs:
             raise ckpt.CheckpointError(f"checkpoint config mismatch on {name!r}: {theirs!r} != {ours!r}")
-    stack, engine = runtime.stack, runtime.engine
+    return restore_state(runtime.stack, runtime.engine, runtime.optimizer, arrays, int(sidecar["next_step"]),
+                         float(sidecar["clock"]))
+
+
+def restore_state(stack, engine, optimizer, arrays, next_step, clock=0.0):
+    """The in-memory half of `load_training_state`: named arrays (our or the
+    reference's checkpoint entry names) -> weights, moments, rings, pending
+    slots (re-derived on the device) and boundary gradients.  Also the entry
+    point of the teacher-forced parity test, which feeds it the fp64 oracle's
+    state every step.  `arrays` is consumed."""
+    arrays = dict(arrays)
     with torch.no_grad():
         for name, view in _layer_entries(stack):
             if name not in arrays:
@@ -226,9 +237,13 @@ def load_training_state(path, runtime):
             _put(view, arrays.pop(name), name)
         stack.refresh()  # compute copies of V; ring entries are reloaded below
         optim = {n[len("optim."):]: arrays.pop(n) for n in list(arrays) if n.startswith("optim.")}
-        runtime.optimizer.load_state_arrays(optim)
-        next_step = int(sidecar["next_step"])
+        optimizer.load_state_arrays(optim)
         d = stack.tied_store.d
+        # the rings hold exactly the snapshots the state names: forget every
+        # other entry (a later step's entry would shadow the restored masters)
+        for m in engine.modules:
+            for st in m.storage:
+                st.ring_step = [None] * len(st.ring_step)
         ref_tied = {}
         for m in engine.modules:
             pre = f"m{m.index}."
@@ -304,7 +319,7 @@ def load_training_state(path, runtime):
                 m.mem_len = int(arrays.pop(f"{pre}mem_len")[0])
         engine.import_boundary({int(n.split(".")[1]): arrays.pop(n) for n in list(arrays)
                                 if n.startswith("boundary.")})
-        engine.clock = float(sidecar["clock"])
+        engine.clock = clock
     torch.cuda.synchronize(stack.runtime.device)
     stack.runtime.check("load_training_state", engine.modules)
     return next_step
@@ -405,7 +420,7 @@ def finite_difference_check(seed=123, coords_per_param=3, h_rel=FD_H_REL):
     rng = SeededRng(mix64(seed, 1))
     x = (rng.uniform((2, 4)) * 7).astype(np.int64)
     y = (rng.uniform((2, 4)) * 7).astype(np.int64)
-    grads, g_vi, g_vo, _ = sequential_gradients(stack, BatchSample(x, y, 0), 5, 0)
+    grads, g_vi, g_vo, _ = stack_gradients(stack, BatchSample(x, y, 0), 5, 0)
     dev = stack.runtime.device
     xd, yd = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
     checks = [("tied", stack.tied, g_vi + g_vo)]
@@ -547,7 +562,7 @@ def verify(cfg, steps=50):
     def oracle(s):
         if s not in cache:
             _load_masters(twin, snapshots[s])
-            cache[s] = sequential_gradients(twin, batches[s], cfg.seed_dropout, s, module=twin_module)
+            cache[s] = stack_gradients(twin, batches[s], cfg.seed_dropout, s, module=twin_module)
         return cache[s]
 
     if twin_module is not None:

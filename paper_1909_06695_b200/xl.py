@@ -74,6 +74,12 @@ class XLTape:
         return sum(t.numel() * t.element_size() for t in vars(self).values() if torch.is_tensor(t))
 
 
+def _bg(*a, **k):
+    """The block's dense contractions (QKV / R / out-projection / FFN and their
+    gradients): one tagged GEMM family for bench.py's roofline."""
+    return ops.gemm(*a, probe="block_gemm", **k)
+
+
 FUSED = os.environ.get("RP_XL_FUSED", "1") != "0"
 # N tile of the unfused score / dP GEMMs (N = M + T keys, K = head dim <= 64:
 # one k-block per tile, so the fp32 output epilogue dominates and 128-wide
@@ -101,10 +107,10 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     n = B * T * d
     cdt = tp.xa.dtype
     ops.layernorm_fwd(tp.xa, vecs["ln1_g"], vecs["ln1_b"], tp.a, tp.mean1, tp.rstd1, flag)
-    ops.gemm(tp.a, W["wqkv"], b_mn=True, out=tp.qkv)
+    _bg(tp.a, W["wqkv"], b_mn=True, out=tp.qkv)
     ops.xl_split_qkv(tp.qkv, vecs["r_w_bias"], vecs["r_r_bias"], tp.qu, tp.qv, tp.kh, tp.vh, B, T, M, H, dh)
     r = ws.get("xl_r", (Kl, d), cdt)
-    ops.gemm(R, W["wr"], b_mn=True, out=r)
+    _bg(R, W["wr"], b_mn=True, out=r)
     ops.xl_split_heads(r, tp.rh, H, dh)
     if fused_ok(tp):
         # scores + relative shift + masked softmax in one tcgen05 kernel (csrc/xl_attn.cu)
@@ -121,11 +127,11 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
     ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
     d0 = None if drop is None else (drop[0], drop[1], drop[2], 0)
-    ops.gemm(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0)
+    _bg(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0)
     ops.layernorm_fwd(tp.x1, vecs["ln2_g"], vecs["ln2_b"], tp.m, tp.mean2, tp.rstd2, flag)
-    ops.gemm(tp.m, W["w1"], b_mn=True, out=tp.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+    _bg(tp.m, W["w1"], b_mn=True, out=tp.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
     d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
-    ops.gemm(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
+    _bg(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
              residual=tp.x1, dropout=d1)
 
 
@@ -146,13 +152,13 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g_h2 = ws.get("g_h2", (Nt, d), cdt)
     pm = ws.get("mask_part", (nbm, d), torch.float32)
     ops.mask_grad(g_out, g_h2, n, drop, pm)
-    ops.gemm(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
+    _bg(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
     g_z1 = ws.get("g_z1", (Nt, f), cdt)
-    ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tp.h1)
+    _bg(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tp.h1)
     ops.colsum_partial(g_z1, part[:, :f])
-    ops.gemm(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
+    _bg(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
     g_m = ws.get("g_m", (Nt, d), torch.float32)
-    ops.gemm(g_z1, W["w1"], out=g_m)
+    _bg(g_z1, W["w1"], out=g_m)
     nbl_cur = ops.layernorm_bwd_blocks(Nt)
     nbl_mem = ops.layernorm_bwd_blocks(B * M) if M else 0
     pg = ws.get("ln_pg", (nbl_cur + nbl_mem, d), torch.float32)
@@ -164,9 +170,9 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     ops.layernorm_bwd(g_m, tp.x1, tp.mean2, tp.rstd2, vecs["ln2_g"], g_x1, pg2, pb2,
                       resid_grad=g_out, dx_masked=g_proj, dropout=drop)
     # relative-position attention
-    ops.gemm(tp.ctx, g_proj, a_mn=True, b_mn=True, out=G["wo"])
+    _bg(tp.ctx, g_proj, a_mn=True, b_mn=True, out=G["wo"])
     g_ctx = ws.get("g_ctx", (Nt, d), cdt)
-    ops.gemm(g_proj, W["wo"], out=g_ctx)
+    _bg(g_proj, W["wo"], out=g_ctx)
     g_ctx_h = ws.get("xl_g_ctx_h", (H, Nt, dh), cdt)
     ops.xl_split_heads(g_ctx, g_ctx_h, H, dh)
     g3 = g_ctx_h.view(H * B, T, dh)
@@ -195,12 +201,12 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
     g_r = ws.get("xl_g_r", (Kl, d), cdt)
     ops.xl_merge_heads(g_rh, g_r, H, dh)
-    ops.gemm(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
+    _bg(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
     g_qkv = ws.get("xl_g_qkv", (B * Kl, 3 * d), cdt)
     ops.xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh)
-    ops.gemm(tp.a, g_qkv, a_mn=True, b_mn=True, out=G["wqkv"])
+    _bg(tp.a, g_qkv, a_mn=True, b_mn=True, out=G["wqkv"])
     g_a = ws.get("xl_g_a", (B * Kl, d), torch.float32)
-    ops.gemm(g_qkv, W["wqkv"], out=g_a)
+    _bg(g_qkv, W["wqkv"], out=g_a)
     # LN1 over both row blocks: memory rows add to the gain / bias sums only
     BM = B * M
     if M:

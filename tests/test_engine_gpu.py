@@ -137,7 +137,7 @@ def test_distributed_engine_single_rank_equals_pipeline_engine():
         c1 = p1.cpu()
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         p2, l2 = e2.step(t, E.BatchSample(xd, yd, t), o2)
-        assert l1 == float(l2.item())
+        assert l1 == float(l2)
         assert np.array_equal(c1.emb_grad, p2.emb_grad.double().cpu().numpy())
         for g1, g2 in zip(c1.module_grads, p2.module_grads):
             for key in g1:
