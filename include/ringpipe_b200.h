@@ -177,6 +177,13 @@ int rp_xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* r
 int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, void* grad_ac, void* grad_bd, int64_t ld_p,
                    const void* grad_ctx, const void* ctx, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh,
                    int64_t mem_len, float scale, void* stream);
+/* rp_xl_attn_bwd plus the query gradients on the tensor cores (dh = 64, T % 128 == 0):
+ * grad_qu = dAC kh and grad_qv = dBD r_h, fp32 [H*B*T, dh] -- the two head-dim-wide GEMMs
+ * over the dAC / dBD matrices are folded into the kernel (dS stays in shared memory) */
+int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
+                      void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,
+                      float* grad_qv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
+                      float scale, void* stream);
 /* dAC = P (dP - <dP,P>) * scale; dBD = the same values un-shifted */
 int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
                       void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,

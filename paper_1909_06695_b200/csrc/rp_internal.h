@@ -93,6 +93,11 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
 int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
                 const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
                 float scale, cudaStream_t st);
+// fused backward with the query gradients on the tensor cores (dh = 64, T % 128 == 0):
+// also gqu = dAC K, gqv = dBD R as fp32 [H*B*T, 64]
+int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
+                   void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
+                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st);
 // adaptive softmax row movers (adaptive.cu)
 int rows_copy(int src_dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, const float* val,
               float val_const, int aug, int dst_dtype, void* dst, int64_t ld_dst, cudaStream_t st);

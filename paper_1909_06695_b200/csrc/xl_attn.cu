@@ -648,6 +648,346 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 2) tmem_dealloc(tmem_base, 256);
 }
 
+// ---------------------------------------------------------------------------
+// Backward with the query gradients fused (head dim 64, T % 128 == 0): the
+// kernel above, plus per key tile n
+//     dQu += dS_n K_n                   128 x 64    (TMEM cols 256..319)
+//     dQv += dBDband_c R_c  (c = n)     128 x 64    (TMEM cols 320..383)
+// on the tensor cores.  dS_n is written once into a 128B-swizzled [128 x 128]
+// shared tile -- the A operand of dQu and the source of the dAC TMA stores --
+// and, shifted, into a 3-chunk ring in band coordinates whose chunk n (complete
+// after key tile n) is the A operand of dQv against the 128 relative-encoding
+// rows it covers and the source of the dBD TMA stores.  This removes the two
+// head-dim-wide GEMMs dQu = dAC K and dQv = dBD R that re-read the 185 MB
+// dAC / dBD matrices per block at the C3 shape.
+constexpr int kRing3 = 3;
+constexpr int kChunkBytes = 128 * 128 * 2;  // 128 rows x 128 band columns, two SW128 atoms
+// P tiles arrive by TMA (two 128B-swizzled 64-key atoms) one tile ahead of
+// the softmax warps: the per-thread P row loads of xl_attn_bwd_kernel were
+// the kernel's dominant stall (ncu: long-scoreboard on the bf16 unpack)
+constexpr int kDqSmem = 1024 + 16384 /*G*/ + 16384 /*V*/ + 16384 /*K*/ + 16384 /*R*/ + kChunkBytes /*P*/ +
+                        kRing3 * kChunkBytes + kChunkBytes /*dS tile*/ + 256 /*barriers*/;
+
+// byte offset of (row r, column c) in a [128 x 128] bf16 tile of two 128B-swizzled 64-column atoms
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
+  return (uint32_t)((c >> 6) * (128 * 128) + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + ((c & 7) << 1));
+}
+
+struct DqParams {
+  BwdParams b;
+  float* gqu;  // [H*B*T, 64] fp32 (rows hb*T + i)
+  float* gqv;
+};
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    xl_attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
+                          const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
+                          const __grid_constant__ CUtensorMap mBD, const __grid_constant__ CUtensorMap mAC,
+                          const __grid_constant__ CUtensorMap mP, const DqParams dq) {
+  const BwdParams& p = dq.b;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
+  uint8_t* sG = smem;
+  uint8_t* sV = smem + 16384;
+  uint8_t* sK = smem + 2 * 16384;
+  uint8_t* sR = smem + 3 * 16384;
+  uint8_t* sP = smem + 4 * 16384;
+  uint8_t* ring = sP + kChunkBytes;
+  uint8_t* sA = ring + kRing3 * kChunkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kChunkBytes);
+  uint64_t* g_full = bars;
+  uint64_t* v_full = bars + 1;
+  uint64_t* v_empty = bars + 2;
+  uint64_t* p_full = bars + 3;
+  uint64_t* p_empty = bars + 4;
+  uint64_t* acc_full = bars + 5;   // [2]
+  uint64_t* acc_empty = bars + 7;  // [2]
+  uint64_t* kr_full = bars + 9;
+  uint64_t* kr_empty = bars + 10;
+  uint64_t* ds_ready = bars + 11;
+  uint64_t* a_free = bars + 12;
+  uint64_t* ring_free = bars + 13;  // [3]
+  uint64_t* dq_full = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int hb, qt;
+  cta_tile(p.nqt, p.heavy_first, hb, qt);
+  const int h = hb / p.B, b = hb % p.B;
+  const int i0 = qt * kQT;
+  const int imax = min(i0 + kQT, p.T) - 1;
+  const int jt_lo = p.lo / kKT, jt_hi = min(p.M + imax, p.Kl - 1) / kKT;
+  const int nt = jt_hi - jt_lo + 1;
+  const int P0 = p.T - kQT - i0 + jt_lo * kKT;  // band column 0 in dBD / R-row coordinates (>= 0: T % 128 == 0)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mG);
+    tma_prefetch(&mV);
+    tma_prefetch(&mK);
+    tma_prefetch(&mR);
+    tma_prefetch(&mBD);
+    tma_prefetch(&mAC);
+    tma_prefetch(&mP);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(g_full, 1);
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(p_full, 1);
+    mbar_init(p_empty, kSoftWarps * 32);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kSoftWarps * 32);
+    }
+    mbar_init(kr_full, 1);
+    mbar_init(kr_empty, 1);
+    mbar_init(ds_ready, 1);
+    mbar_init(a_free, 1);
+    for (int c = 0; c < kRing3; ++c) mbar_init(&ring_free[c], 1);
+    mbar_init(dq_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t t_dqu = tmem_base + 256, t_dqv = tmem_base + 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_expect_tx(g_full, 16384);
+      tma_atoms<1>(sG, &mG, g_full, kQT, i0, hb);
+      for (int n = 0; n <= nt; ++n) {
+        if (n < nt) {
+          mbar_wait(v_empty, (n & 1) ^ 1);
+          mbar_expect_tx(v_full, 16384);
+          tma_atoms<1>(sV, &mV, v_full, kKT, (jt_lo + n) * kKT, hb);
+          mbar_wait(p_empty, (n & 1) ^ 1);
+          mbar_expect_tx(p_full, kChunkBytes);
+          tma_load_3d(sP, &mP, p_full, (jt_lo + n) * kKT, i0, hb);
+          tma_load_3d(sP + 128 * 128, &mP, p_full, (jt_lo + n) * kKT + 64, i0, hb);
+        }
+        // K tile n (MN-major B of dQu) and relative-encoding rows of band chunk n
+        // (MN-major B of dQv); after the last tile only the rows of chunk nt
+        mbar_wait(kr_empty, (n & 1) ^ 1);
+        mbar_expect_tx(kr_full, n < nt ? 32768 : 16384);
+        if (n < nt) tma_load_3d(sK, &mK, kr_full, 0, (jt_lo + n) * kKT, hb);
+        tma_load_3d(sR, &mR, kr_full, 0, P0 + kKT * n, h);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
+      const uint32_t id_dq = umma_idesc(false, false, true, kQT, 64);
+      const uint32_t ga = smem_u32(sG), ka = smem_u32(sK), ra = smem_u32(sR), aa = smem_u32(sA);
+      const uint32_t rg = smem_u32(ring);
+      mbar_wait(g_full, 0);
+      auto issue_dq = [&](int n) {
+        mbar_wait(ds_ready, n & 1);
+        mbar_wait(kr_full, n & 1);
+        tc_fence_after();
+        const uint32_t ch = rg + (uint32_t)((n % kRing3) * kChunkBytes);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma<false>(t_dqu, atom_desc<1>(aa, kQT, k), umma_desc(ka + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
+        tc_commit(a_free);
+        tc_commit(&ring_free[n % kRing3]);
+        tc_commit(kr_empty);
+      };
+      for (int n = 0; n < nt; ++n) {
+        const int s = n & 1;
+        mbar_wait(&acc_empty[s], ((n >> 1) & 1) ^ 1);
+        mbar_wait(v_full, n & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(sV);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vb, kKT, k), id_dp, k > 0);
+        tc_commit(v_empty);
+        tc_commit(&acc_full[s]);
+        if (n >= 1) issue_dq(n - 1);
+      }
+      issue_dq(nt - 1);
+      // band chunk nt (the columns right of the last key tile) is complete with tile nt-1
+      mbar_wait(kr_full, nt & 1);
+      tc_fence_after();
+      const uint32_t ch = rg + (uint32_t)((nt % kRing3) * kChunkBytes);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, 1u);
+      tc_commit(dq_full);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const int i = i0 + r;
+    const int jhi = p.M + i;
+    const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    const int64_t rowoff = ((int64_t)hb * p.T + i) * p.ldp;
+    const __nv_bfloat16* prow = p.p + rowoff;
+    __nv_bfloat16* arow = p.gac + rowoff;
+    __nv_bfloat16* brow = p.gbd + rowoff;
+    // D_i = g_ctx_i . ctx_i over this head's 64 columns
+    float D = 0.f;
+    {
+      const int64_t mo = ((int64_t)b * p.T + i) * p.d + h * 64;
+      const uint4* g4 = reinterpret_cast<const uint4*>(p.gctx + mo);
+      const uint4* c4 = reinterpret_cast<const uint4*>(p.ctx + mo);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 gu = g4[c], cu = c4[c];
+        const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, cw[4] = {cu.x, cu.y, cu.z, cu.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[e]));
+          const float2 cf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cw[e]));
+          D = fmaf(gf.x, cf.x, D);
+          D = fmaf(gf.y, cf.y, D);
+        }
+      }
+      // columns outside the key tiles this query tile sees: dAC = 0, and the
+      // dBD margins outside the stored band chunks
+      if (half == 0) {
+        zero_row(arow, 0, (int64_t)jt_lo * kKT);
+        zero_row(brow, 0, lmin(lmax(P0, 0), p.ldp));
+      } else {
+        zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
+        zero_row(brow, lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp), p.ldp);
+      }
+    }
+    auto ring_at = [&](int bc) -> __nv_bfloat16* {  // band column bc of row r
+      return reinterpret_cast<__nv_bfloat16*>(ring + (bc >> 7) % kRing3 * kChunkBytes + sw128_off(r, bc & 127));
+    };
+    const __nv_bfloat16 zb = __float2bfloat16_rn(0.f);
+    // band columns before this row's first key (chunk 0)
+    if (half == 0)
+      for (int c = 0; c < 127 - r; ++c) *ring_at(c) = zb;
+    for (int n = 0; n < nt; ++n) {
+      const int s = n & 1;
+      const int jt0 = (jt_lo + n) * kKT + 64 * half;
+      // this row's 64 P values of the tile from the swizzled smem tile (zero past ldp: TMA fill)
+      uint4 pr[2][4];
+      mbar_wait(p_full, n & 1);
+      {
+        const uint8_t* prow_s = sP + half * (128 * 128) + r * 128;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            pr[k][c] = *reinterpret_cast<const uint4*>(prow_s + (((4 * k + c) ^ (r & 7)) << 4));
+      }
+      mbar_arrive(p_empty);
+      mbar_wait(&acc_full[s], (n >> 1) & 1);
+      tc_fence_after();
+      uint32_t dp[2][32];
+      tmem_ld32(tl + s * kKT + 64 * half, dp[0]);
+      tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[s]);
+      // the dS tile is free once the previous tile's dQu MMA and this warp's
+      // dAC store from it are done; the upper band chunk of this tile is
+      // reused from tile n - 2, whose dQv MMA must be done (its TMA store was
+      // retired before barrier n - 1)
+      if (n >= 1) mbar_wait(a_free, (n - 1) & 1);
+      if (n >= 2) mbar_wait(&ring_free[(n + 1) % kRing3], ((n - 2) / kRing3) & 1);
+      if (lane == 0) tma_store_wait_read();
+      __syncwarp();
+      const int rsw = r & 7;
+      uint8_t* arow_s = sA + half * (128 * 128) + r * 128;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int jb = jt0 + 32 * k;
+        uint32_t o[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t w[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+            const int t = 8 * c + 2 * e;
+            const int j = jb + t;
+            // P is zero outside the window, but dP there is not: mask explicitly
+            const float a0 = (j >= p.lo && j <= jhi) ? pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale : 0.f;
+            const float a1 =
+                (j + 1 >= p.lo && j + 1 <= jhi) ? pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale : 0.f;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+            o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+        }
+        // dS row segment into the swizzled tile (16-byte chunks 4k .. 4k+3 of this half's atom)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(arow_s + (((4 * k + c) ^ rsw) << 4)) =
+              make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+        // shifted copy into the band ring: the 32-run crosses at most one
+        // 64-column atom boundary -- two segments of constant (chunk, atom)
+        const int cb = kKT * n + 127 - r + 64 * half + 32 * k;
+        const int split = 64 - (cb & 63);
+        uint8_t* seg0 = ring + ((cb >> 7) % kRing3) * kChunkBytes + ((cb >> 6) & 1) * (128 * 128) + r * 128;
+        const int c1 = cb + split;
+        uint8_t* seg1 = ring + ((c1 >> 7) % kRing3) * kChunkBytes + ((c1 >> 6) & 1) * (128 * 128) + r * 128;
+        const int e0 = cb & 63;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const uint32_t w = o[t >> 1];
+          const unsigned short hv = (unsigned short)((t & 1) ? (w >> 16) : (w & 0xffffu));
+          const bool lo = t < split;
+          const int e = lo ? e0 + t : t - split;
+          *reinterpret_cast<unsigned short*>((lo ? seg0 : seg1) + ((((e >> 3) ^ rsw) << 4) | ((e & 7) << 1))) = hv;
+        }
+      }
+      if (n == nt - 1 && half == 1) {
+        // band columns after this row's last key (chunk nt)
+        for (int c = kKT * n + 255 - r; c < kKT * (nt + 1); ++c) *ring_at(c) = zb;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      // this warp's 32 x 64 dAC block straight from the swizzled dS tile
+      if (lane == 0 && jt0 < p.ldp) tma_store_3d(&mAC, sA + half * (128 * 128) + 32 * q * 128, jt0, i0 + 32 * q, hb);
+      // earlier dBD chunk stores have read the ring (all but the newest bulk
+      // group: this tile's dAC store, which nobody waits for here)
+      if (warp == 4 && lane == 0) bulk_wait_read_1();
+      named_sync(1, kSoftWarps * 32);
+      if (warp == 4 && lane == 0) {
+        mbar_arrive(ds_ready);
+        for (int m = n; m <= (n == nt - 1 ? n + 1 : n); ++m) {
+          const uint8_t* ch = ring + (m % kRing3) * kChunkBytes;
+          const int c0 = P0 + kKT * m;
+          if (c0 < p.ldp) tma_store_3d(&mBD, ch, c0, i0, hb);
+          if (c0 + 64 < p.ldp) tma_store_3d(&mBD, ch + 128 * 128, c0 + 64, i0, hb);
+        }
+      }
+    }
+    // ---- dQu / dQv epilogue: rows of this lane quarter, columns [32 half, +32)
+    mbar_wait(dq_full, 0);
+    tc_fence_after();
+    uint32_t v[32];
+    const int64_t orow = ((int64_t)hb * p.T + i) * 64 + 32 * half;
+    tmem_ld32(tl + 256 + 32 * half, v);
+    float4* du = reinterpret_cast<float4*>(dq.gqu + orow);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      du[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
+                          __uint_as_float(v[4 * c + 3]));
+    tmem_ld32(tl + 320 + 32 * half, v);
+    float4* dv = reinterpret_cast<float4*>(dq.gqv + orow);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      dv[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
+                          __uint_as_float(v[4 * c + 3]));
+    if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
 }  // namespace
 
 // RP_XL_ORDER=0 restores the (head*batch)-major CTA order (A/B switch)
@@ -746,6 +1086,57 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   else
     xl_attn_bwd_kernel<2><<<(unsigned)grid, kThreadsBwd, smem_bwd<2>(), st>>>(mg, mv, mbd, mac, p);
   return check_launch("xl_attn_bwd");
+}
+
+int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
+                   void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
+                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st) {
+  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: head dim must be 64 (got %d)", dh);
+  if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: T must be a multiple of 128");
+  const int64_t Kl = M + Tn, HB = (int64_t)H * B;
+  if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: ldp must be >= M+T, multiple of 8");
+  if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: mem_len out of range");
+  for (const void* q : {probs, (const void*)gac, (const void*)gbd, gctx, ctx, (const void*)gqu, (const void*)gqv})
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned operand");
+  CUtensorMap mg, mv, mk, mr, mbd, mac, mp;
+  RP_TRY0(tma_map_bf16(&mp, probs, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mg, gctx_h, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
+  RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
+  RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kKT));
+  RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mac, gac, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(xl_attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
+    attr_dev = dev;
+  }
+  DqParams q{};
+  BwdParams& p = q.b;
+  p.p = static_cast<const __nv_bfloat16*>(probs);
+  p.gac = static_cast<__nv_bfloat16*>(gac);
+  p.gbd = static_cast<__nv_bfloat16*>(gbd);
+  p.gctx = static_cast<const __nv_bfloat16*>(gctx);
+  p.ctx = static_cast<const __nv_bfloat16*>(ctx);
+  p.ldp = ldp;
+  p.B = (int)B;
+  p.T = (int)Tn;
+  p.M = (int)M;
+  p.Kl = (int)Kl;
+  p.lo = (int)(M - mem_len);
+  p.nqt = (int)(Tn / kQT);
+  p.heavy_first = xl_heavy_first();
+  p.H = H;
+  p.d = H * dh;
+  p.scale = scale;
+  q.gqu = gqu;
+  q.gqv = gqv;
+  const int64_t grid = HB * p.nqt;
+  if (grid <= 0) return RP_OK;
+  xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);
+  return check_launch("xl_attn_bwd_dq");
 }
 
 }  // namespace rp

@@ -151,9 +151,11 @@ class LogicalCostModel:
 
 
 class ScheduleTrace:
-    """Occupancy rows {step, module, phase, sample, start, end}; the engines
-    fill start/end from the logical clock, or from CUDA events when
-    `timed=True` (milliseconds since the first recorded step)."""
+    """Occupancy rows {step, module, phase, sample, start, end}.  `engine.trace`
+    carries the reference's logical clock (engine.py:104-135); with
+    `timed=True` the engines also fill `engine.device_trace` from CUDA events
+    recorded on each module's stream around its forward and delayed backward
+    (milliseconds since the first timed step's start)."""
 
     def __init__(self):
         self.rows = []
@@ -200,11 +202,46 @@ def _to_device_tokens(a, device, vocab=None, what="token"):
     return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
 
 
+class _DeviceClock:
+    """CUDA-event timing of (step, module, phase) spans for ScheduleTrace:
+    events are recorded on the stream the work runs on and resolved to
+    milliseconds (relative to the first span's origin event) once they have
+    completed, so timing never adds a host synchronisation to the step."""
+
+    def __init__(self, device):
+        self.device = device
+        self.origin = None
+        self.pending = []  # (step, module, phase, sample, start_ev, end_ev)
+
+    def begin(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if self.origin is None:
+            self.origin = ev
+        return ev
+
+    def end(self, step, module, phase, sample, start_ev):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.pending.append((step, module, phase, sample, start_ev, ev))
+
+    def flush(self, trace, wait=False):
+        keep = []
+        for row in self.pending:
+            if not wait and not row[5].query():
+                keep.append(row)
+                continue
+            row[5].synchronize()
+            trace.record(row[0], row[1], row[2], row[3], self.origin.elapsed_time(row[4]),
+                         self.origin.elapsed_time(row[5]))
+        self.pending = keep
+
+
 class PipelineEngine:
     """Deterministic single-stream executor of the delayed-gradient schedule."""
 
     def __init__(self, stack, part, dropout_seed, tied_grad="half_avg", stale_weights="snapshot", train=True,
-                 cost_model=None):
+                 cost_model=None, timed=False):
         if tied_grad not in ("half_avg", "sum"):
             raise ValueError(f"unknown tied_grad convention {tied_grad!r}")
         if stale_weights not in ("snapshot", "current"):
@@ -218,6 +255,8 @@ class PipelineEngine:
         self.train = train
         self.costs = cost_model or LogicalCostModel.derived(part)
         self.trace = ScheduleTrace()
+        self.device_trace = ScheduleTrace()
+        self._dclock = _DeviceClock(stack.runtime.device) if timed else None
         self.clock = 0.0
         self.last_step_logical = 0.0
         self.last_backward_logical = 0.0
@@ -246,7 +285,10 @@ class PipelineEngine:
             out = nxt.input_buffer(t, B, T) if nxt is not None else None
             end = start + self.costs.fwd[m.index - 1]
             self.trace.record(t, m.index, "forward", sample_id, start, end)
+            ev = self._dclock.begin() if self._dclock else None
             cur = m.forward(cur, t, sample_id, y if m.has_projection else None, self.train, out=out)
+            if ev is not None:
+                self._dclock.end(t, m.index, "forward", sample_id, ev)
             if m.index < self.K:
                 cur = cur.view(B, T, -1)
             start = end + (self.costs.relay if m.index < self.K else 0.0)
@@ -269,8 +311,11 @@ class PipelineEngine:
         g_in = self._bbuf(k - 1, t & 1, B * T, m.d) if k > 1 else None
         alpha, beta = coef
         emb = (alpha if m.has_projection else 0.0, beta if m.has_embedding else 0.0, self.stack.tied_store.grad)
+        ev = self._dclock.begin() if self._dclock else None
         m.recompute_backward(slot, grad_out, self.stale_weights, self.train, g_in=g_in, emb=emb, live_step=t,
                              after_head=after_head, before_embedding=before_embedding, vo_overwrite=vo_overwrite)
+        if ev is not None:
+            self._dclock.end(t, k, "backward", slot.sample_id, ev)
         return g_in, slot.sample_id
 
     def _backward_all(self, t, B, T):
@@ -334,12 +379,20 @@ class PipelineEngine:
         if optimizer is not None:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
         self.last_loss_device = loss_dev
+        if self._dclock:
+            self._dclock.flush(self.device_trace)
         if sync:
             self.runtime.check(f"step {t}", self.modules)
             loss = float(loss_dev.item())
             packet.loss = loss
             return packet, loss
         return packet, loss_dev
+
+    def flush_device_trace(self):
+        """Resolve every recorded span (waits for the device)."""
+        if self._dclock:
+            self._dclock.flush(self.device_trace, wait=True)
+        return self.device_trace
 
     def export_boundary(self):
         return dict(self.boundary)
@@ -406,7 +459,10 @@ class ConcurrentPipelineEngine(PipelineEngine):
             nxt = self.modules[m.index] if m.index < self.K else None
             with torch.cuda.stream(s):
                 out = nxt.input_buffer(t, B, T) if nxt is not None else None
+                tev = self._dclock.begin() if self._dclock else None
                 cur = m.forward(cur, t, batch.sample_id, y if m.has_projection else None, self.train, out=out)
+                if tev is not None:
+                    self._dclock.end(t, m.index, "forward", batch.sample_id, tev)
                 if m.index < self.K:
                     cur = cur.view(B, T, -1)
                 ev = torch.cuda.Event()
@@ -495,6 +551,8 @@ class ConcurrentPipelineEngine(PipelineEngine):
         self._advance_clock(t, results, relay_end)
         if optimizer is not None and not split:
             optimizer.apply(t, packet, self.modules, self.stack.tied)
+        if self._dclock:
+            self._dclock.flush(self.device_trace)
         # the next step's side streams order themselves after this step's
         # optimizer through start_ev / zero_ev (recorded on the main stream),
         # so no trailing fork is left open (CUDA-graph capture needs joins)
@@ -525,11 +583,11 @@ class SequentialRunner(PipelineEngine):
     """Plain backprop over the whole stack (engine.py:443-491): the K=1
     baseline, keeping the caller's partition only for packet slicing."""
 
-    def __init__(self, stack, part, dropout_seed, tied_grad="half_avg", train=True, cost_model=None):
+    def __init__(self, stack, part, dropout_seed, tied_grad="half_avg", train=True, cost_model=None, timed=False):
         from .model import partition
 
         super().__init__(stack, partition(stack.num_layers, 1), dropout_seed, tied_grad, "snapshot", train,
-                         cost_model or LogicalCostModel.derived(part, recompute=False))
+                         cost_model or LogicalCostModel.derived(part, recompute=False), timed=timed)
         self.user_part = part
 
     def step(self, t, batch, optimizer=None, sync=True):

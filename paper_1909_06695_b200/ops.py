@@ -418,6 +418,29 @@ def xl_attn_bwd(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx, B, T, M, mem_len, sc
                                    _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_bwd")
 
 
+def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale):
+    """xl_attn_bwd plus the query gradients on the tensor cores (dh = 64,
+    T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh]."""
+    _require_cuda(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv)
+    for t in (g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx):
+        if t.dtype != torch.bfloat16:
+            raise DimensionError("xl_attn_bwd_dq takes bf16 operands")
+    for t in (g_qu, g_qv):
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise DimensionError("xl_attn_bwd_dq writes contiguous fp32 query gradients")
+    for t in (g_ctx_h, vh, kh, rh, g_ctx, ctx):
+        if not t.is_contiguous():
+            raise DimensionError("xl_attn_bwd_dq operands must be contiguous")
+    ldp = probs.stride(-2)
+    if g_ac.stride(-2) != ldp or g_bd.stride(-2) != ldp:
+        raise DimensionError("xl_attn_bwd_dq: P, dAC and dBD must share the row pitch")
+    H, dh = g_ctx.shape[-1] // vh.shape[-1], vh.shape[-1]
+    _count(1)
+    N.check(N.lib().rp_xl_attn_bwd_dq(_ptr(g_ctx_h), _ptr(vh), _ptr(kh), _ptr(rh), _ptr(probs), _ptr(g_ac),
+                                      _ptr(g_bd), ldp, _ptr(g_ctx), _ptr(ctx), _ptr(g_qu), _ptr(g_qv), B, T, M, H, dh,
+                                      mem_len, scale, _stream()), "xl_attn_bwd_dq")
+
+
 def rows_copy(src, dst, cols=None, val=None, val_const=0.0, aug=False):
     """dst[r, :cols] = src[r, :cols]; with aug, dst[r, cols] = val[r] (or val_const); zeros to dst's width."""
     _require_cuda(src, dst)

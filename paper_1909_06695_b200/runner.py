@@ -83,7 +83,8 @@ class Runtime:
 
 
 def _make_engine(cfg, stack, part, cost_model):
-    common = dict(dropout_seed=cfg.seed_dropout, tied_grad=cfg.tied_grad, cost_model=cost_model)
+    common = dict(dropout_seed=cfg.seed_dropout, tied_grad=cfg.tied_grad, cost_model=cost_model,
+                  timed=bool(getattr(cfg, "timed_trace", False)))
     if cfg.mode == "sequential":
         return SequentialRunner(stack, part, **common)
     if cfg.mode == "ouroboros-ref":
@@ -370,6 +371,8 @@ def train(cfg, progress=None):
     finally:
         writer.close()
         engine.trace.to_jsonl(paths["trace"])
+        if getattr(cfg, "timed_trace", False):
+            engine.flush_device_trace().to_jsonl(os.path.join(cfg.out_dir, "trace_device.jsonl"))
         engine.close()
     return {
         "mode": cfg.mode, "k": runtime.part.k, "steps_run": steps_run, "start_step": start_step,

@@ -100,6 +100,15 @@ def fused_bwd_ok(tp):
     return fused_ok(tp) and tp.T % 8 == 0
 
 
+FUSED_DQ = os.environ.get("RP_XL_FUSED_DQ", "1") != "0"
+
+
+def fused_dq_ok(tp):
+    """The backward with the query-gradient MMAs folded in (xl_attn_bwd_dq):
+    head dim 64 and whole 128-query tiles."""
+    return FUSED_DQ and fused_bwd_ok(tp) and tp.dh == 64 and tp.T % 128 == 0
+
+
 def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
     """tp.xa holds [memory; x]; writes out [B*T, d] and the tape."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
@@ -178,7 +187,16 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g3 = g_ctx_h.view(H * B, T, dh)
     g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
     g_bd = ws.get("xl_g_bd", (H, Nt, tp.ldk), cdt)
-    if fused_bwd_ok(tp):
+    g_qu = ws.get("xl_g_qu", (H, Nt, dh), torch.float32)
+    g_qv = ws.get("xl_g_qv", (H, Nt, dh), torch.float32)
+    dq_done = False
+    if fused_dq_ok(tp):
+        # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu)
+        with ops.span("xl_attn_bwd"):
+            ops.xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, g_qu, g_qv, B,
+                               T, M, tp.mem_len, scale)
+        dq_done = True
+    elif fused_bwd_ok(tp):
         # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
         with ops.span("xl_attn_bwd"):
             ops.xl_attn_bwd(g_ctx_h, tp.vh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, B, T, M, tp.mem_len, scale)
@@ -189,13 +207,13 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
     g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
     ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
-    g_qu = ws.get("xl_g_qu", (H, Nt, dh), torch.float32)
     g_kh = ws.get("xl_g_kh", (H * B, Kl, dh), torch.float32)
-    g_qv = ws.get("xl_g_qv", (H, Nt, dh), torch.float32)
     g_rh = ws.get("xl_g_rh", (H, Kl, dh), torch.float32)
-    ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
+    if not dq_done:
+        ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
     ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh)
-    ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
+    if not dq_done:
+        ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
     work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
     ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)

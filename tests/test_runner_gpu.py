@@ -161,3 +161,31 @@ def test_verify_xl_passes_exactly(in_gold, tmp_path):
     report = R.verify(cfg_for(tmp_path, n_heads=2, mem_len=16, k=3), steps=8)
     assert report["passed"], report
     assert report["oracle_max_abs"] == 0.0 and report["emb_max_abs"] == 0.0
+
+
+def test_timed_trace_rows_follow_the_device(tmp_path):
+    """with timed_trace the engine writes trace_device.jsonl, one
+    row per (step, module, phase) timed by CUDA events on the module's own
+    stream: forwards of a step are ordered along the relay, every span has
+    positive length, and the logical trace is unchanged."""
+    import json
+
+    from paper_1909_06695_b200.config import RunConfig
+    from paper_1909_06695_b200.runner import train
+
+    data = tmp_path / "corpus.txt"
+    data.write_text("the quick brown fox jumps over the lazy dog " * 200)
+    cfg = RunConfig(data=str(data), seq_len=16, batch_size=4, n_blocks=4, model_dim=32, ffn_dim=64, k=3,
+                    mode="ouroboros-concurrent", steps=6, warmup_steps=1, dtype="fp32", out_dir=str(tmp_path / "o"),
+                    timed_trace=True)
+    train(cfg)
+    rows = [json.loads(line) for line in open(tmp_path / "o" / "trace_device.jsonl")]
+    logical = [json.loads(line) for line in open(tmp_path / "o" / "trace.jsonl")]
+    assert len(rows) == 6 * 3 + sum(1 for r in logical if r["phase"] == "backward")
+    for r in rows:
+        assert r["end"] > r["start"] >= 0.0
+    for t in range(6):
+        fwd = sorted((r for r in rows if r["step"] == t and r["phase"] == "forward"), key=lambda r: r["module"])
+        assert [r["module"] for r in fwd] == [1, 2, 3]
+        for a, b in zip(fwd, fwd[1:]):
+            assert b["start"] >= a["end"] - 1e-3  # the relay: module k+1 starts after module k

@@ -262,3 +262,42 @@ def test_fused_backward_rejects_unaligned_segment_length():
     with pytest.raises(DimensionError):
         ops.xl_attn_bwd(z(H, B * T, dh), z(H, B * Kl, dh), z(H * B, T, ldp), z(H * B, T, ldp), z(H, B * T, ldp),
                         z(B * T, H * dh), z(B * T, H * dh), B, T, M, M, dh ** -0.5)
+
+
+@pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 2, 256, 256, 100), (2, 1, 128, 0, 0),
+                                             (1, 3, 384, 128, 60), (2, 8, 512, 512, 512)])
+def test_fused_dq_backward_equals_fused_backward_plus_gemms(B, H, T, M, mem_len):
+    """xl_attn_bwd_dq: dAC / dBD bitwise equal to xl_attn_bwd's, and the
+    in-kernel query gradients dQu = dAC k, dQv = dBD r (tcgen05, dS kept in
+    shared memory) against fp32 torch products of the same bf16 matrices
+    (exact bf16 products, fp32 sums: rel-L2 <= 1e-5)."""
+    from paper_1909_06695_b200 import ops
+
+    dev, dh = "cuda", 64
+    g = torch.Generator(device=dev).manual_seed(11 * T + M + mem_len)
+    Kl = M + T
+    ldp = _pad8(Kl)
+    mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
+    qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
+    kh, rh, vh = mk(H, B * Kl, dh), mk(H, Kl, dh), mk(H, B * Kl, dh)
+    scale = 1.0 / math.sqrt(dh)
+    probs = torch.empty(H * B, T, ldp, device=dev, dtype=torch.bfloat16)
+    ops.xl_attn_fwd(qu, qv, kh, rh, probs, B, T, M, mem_len, scale)
+    g3 = mk(H, B * T, dh)
+    gctx = g3.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    ctx_h = (probs[:, :, :Kl].float() @ vh.float().view(H * B, Kl, dh)).to(torch.bfloat16)
+    ctx = ctx_h.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    nan = lambda *s: torch.full(s, float("nan"), device=dev, dtype=torch.bfloat16)  # noqa: E731
+    gac1, gbd1 = nan(H * B, T, ldp), nan(H, B * T, ldp)
+    gac2, gbd2 = nan(H * B, T, ldp), nan(H, B * T, ldp)
+    gqu = torch.full((H, B * T, dh), float("nan"), device=dev)
+    gqv = torch.full((H, B * T, dh), float("nan"), device=dev)
+    ops.xl_attn_bwd(g3, vh, probs, gac1, gbd1, gctx, ctx, B, T, M, mem_len, scale)
+    ops.xl_attn_bwd_dq(g3, vh, kh, rh, probs, gac2, gbd2, gctx, ctx, gqu, gqv, B, T, M, mem_len, scale)
+    torch.cuda.synchronize()
+    assert torch.equal(gac1, gac2)
+    assert torch.equal(gbd1, gbd2)
+    want_qu = gac2[:, :, :Kl].float() @ kh.view(H * B, Kl, dh).float()
+    want_qv = gbd2.view(H, B * T, ldp)[:, :, :Kl].float() @ rh.float()
+    assert rel(gqu.view(H * B, T, dh).cpu(), want_qu.cpu()) <= 1e-5
+    assert rel(gqv.cpu(), want_qv.cpu()) <= 1e-5
