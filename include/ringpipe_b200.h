@@ -259,6 +259,12 @@ typedef struct rp_block_desc {
   uint64_t drop_threshold;
   float drop_scale;
   int32_t max_ctas; /* SM budget for every GEMM of the layer (0 = whole GPU) */
+  /* Rows (B*T) of the whole batch when this call is one row block of it (the
+   * micro-batched relay, paper_1909_06695_b200/distributed.py); 0 = B*T.  The
+   * second dropout mask then starts at drop_rows_total*d (layers.py:209-212);
+   * the block's own row offset r0 is folded into drop_seed by the caller:
+   * seed + r0*d*0x9E3779B97F4A7C15 addresses positions r0*d + i (tensor.py:41-48). */
+  int64_t drop_rows_total;
 } rp_block_desc;
 
 typedef struct rp_block_weights {
@@ -292,6 +298,9 @@ int rp_block_backward(const rp_block_desc* desc, const rp_block_weights* w, cons
 typedef struct rp_head_desc {
   int64_t rows, d, vocab;
   int32_t dtype;
+  /* rows of the whole batch when this call is one row block of it: the
+   * cross-entropy gradient is scaled by 1/rows_total (layers.py:319); 0 = rows */
+  int64_t rows_total;
 } rp_head_desc;
 
 int64_t rp_head_workspace_bytes(const rp_head_desc* desc);
@@ -364,6 +373,10 @@ int rp_module_forward(const rp_module_desc* desc, const rp_module_weights* w, co
 int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot,
                        const float* g_out, float* g_in, const rp_module_grads* grads, void* workspace,
                        int64_t workspace_bytes, void* stream);
+
+/* y += alpha * x over n fp32 elements (weight-gradient accumulation over the
+ * row blocks of a micro-batched slot, in a fixed order) */
+int rp_axpy(float* y, const float* x, float alpha, int64_t n, void* stream);
 
 /* ---- distributed context and point-to-point transfers ---------
  * The reference's module threads hand activations and boundary gradients over

@@ -54,13 +54,15 @@ def _rows(x):
 # embedding: layers.py:114-136
 
 
-def embed_fwd(V, pos, tokens, seed, p, train):
+def embed_fwd(V, pos, tokens, seed, p, train, pos0=0):
+    """pos0: first dropout position (a row block of a larger batch starts at
+    its first row * d; the whole batch draws [0, N*d), layers.py:124)."""
     tokens = np.asarray(tokens)
     if tokens.size and tokens.max() >= V.shape[0]:
         raise ShapeError("token id out of vocabulary range")
     T = tokens.shape[-1]
     h = V[tokens] + pos[:T]
-    mask = dropout_scale_mask(seed, 0, h.shape, p) if train else None
+    mask = dropout_scale_mask(seed, pos0, h.shape, p) if train else None
     if mask is not None:
         h = h * mask
     return h, (tokens, mask)
@@ -84,9 +86,13 @@ def embed_bwd(g, cache, vocab, pos_shape):
 BLOCK_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2")
 
 
-def block_fwd(P, x, seed, p, train):
+def block_fwd(P, x, seed, p, train, pos0=0, n_total=None):
+    """pos0 / n_total: a row block of a larger batch -- mask0 draws
+    [pos0, pos0 + n), mask1 [n_total + pos0, ...) with n_total = N*d of the
+    whole batch (layers.py:184-195)."""
     B, T, d = x.shape
     n = B * T * d
+    n1 = n if n_total is None else n_total
     a, c1 = ln_fwd(x, P["ln1_g"], P["ln1_b"])
     ar = _rows(a)
     q = (ar @ P["wq"]).reshape(B, T, d)
@@ -100,7 +106,7 @@ def block_fwd(P, x, seed, p, train):
     probs = e / e.sum(axis=-1, keepdims=True)
     ctx = probs @ v
     proj = (_rows(ctx) @ P["wo"]).reshape(B, T, d)
-    m0 = dropout_scale_mask(seed, 0, (B, T, d), p) if train else None
+    m0 = dropout_scale_mask(seed, pos0, (B, T, d), p) if train else None
     if m0 is not None:
         proj = proj * m0
     x1 = x + proj
@@ -108,7 +114,7 @@ def block_fwd(P, x, seed, p, train):
     z1 = _rows(m) @ P["w1"] + P["b1"]
     h1 = np.maximum(z1, 0.0)
     h2 = (h1 @ P["w2"] + P["b2"]).reshape(B, T, d)
-    m1 = dropout_scale_mask(seed, n, (B, T, d), p) if train else None
+    m1 = dropout_scale_mask(seed, n1 + pos0, (B, T, d), p) if train else None
     if m1 is not None:
         h2 = h2 * m1
     out = x1 + h2

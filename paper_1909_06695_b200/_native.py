@@ -66,7 +66,8 @@ class GemmArgs(ctypes.Structure):
 class BlockDesc(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("d", ctypes.c_int64), ("f", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_seed", ctypes.c_uint64),
-                ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float), ("max_ctas", ctypes.c_int32)]
+                ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float), ("max_ctas", ctypes.c_int32),
+                ("drop_rows_total", ctypes.c_int64)]
 
 
 class BlockWeights(ctypes.Structure):
@@ -86,7 +87,7 @@ class BlockGrads(ctypes.Structure):
 
 class HeadDesc(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("d", ctypes.c_int64), ("vocab", ctypes.c_int64),
-                ("dtype", ctypes.c_int32)]
+                ("dtype", ctypes.c_int32), ("rows_total", ctypes.c_int64)]
 
 
 class ModuleDesc(ctypes.Structure):
@@ -191,6 +192,7 @@ def _declare(L):
         "rp_head_workspace_bytes": [ctypes.POINTER(HeadDesc)],
         "rp_head_forward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
         "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, i32, vp, i64, vp],
+        "rp_axpy": [vp, vp, f32, i64, vp],
         "rp_nccl_unique_id": [vp],
         "rp_ctx_create": [i32, vp, i32, i32, ctypes.POINTER(vp)],
         "rp_ctx_destroy": [vp],

@@ -295,7 +295,7 @@ int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void*
   Epi e2 = e0;
   e2.bias = w.b2;
   e2.resid = tp.x1;
-  e2.pos0 = static_cast<uint64_t>(N * D);
+  e2.pos0 = static_cast<uint64_t>((d.drop_rows_total > 0 ? d.drop_rows_total : N) * D);
   RP_TRY(mm(c, mat(tp.h1, N, F, F), false, mat(w.w2, F, D, D), true, mat(out, N, D, D), dt, e2));
   return RP_OK;
 }
@@ -371,7 +371,9 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
   // The bias / LayerNorm column sums only feed the optimizer: their partials
   // get separate buffers and one batched finish at the end, off the chain of
   // dependent kernels that carries g_x.
-  RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(N * D), d.drop_threshold, d.drop_scale,
+  RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed,
+                   static_cast<uint64_t>((d.drop_rows_total > 0 ? d.drop_rows_total : N) * D), d.drop_threshold,
+                   d.drop_scale,
                    d.drop_enabled, part_b2, st));
   Epi er;
   er.kind = RP_EPI_RELU_GRAD;
@@ -468,7 +470,7 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
   e.kind = RP_EPI_CE_GRAD;
   e.targets = targets;
   e.lse = lse;
-  e.ce_scale = 1.f / static_cast<float>(N);
+  e.ce_scale = 1.f / static_cast<float>(h.rows_total > 0 ? h.rows_total : N);
   RP_TRY(mm(c, mat(x, N, D, D), false, mat(tied, V, D, D), false, mat(dz, N, V, Vp), h.dtype, e));
   RP_TRY(mm(c, mat(dz, N, V, Vp), false, mat(tied, V, D, D), true, mat(g_x, N, D, D), RP_F32));
   if (vo) {

@@ -32,7 +32,7 @@ rp_block_desc block_desc(const rp_module_desc& m, int layer) {
   return d;
 }
 
-rp_head_desc head_desc(const rp_module_desc& m) { return rp_head_desc{m.B * m.T, m.d, m.vocab, m.dtype}; }
+rp_head_desc head_desc(const rp_module_desc& m) { return rp_head_desc{m.B * m.T, m.d, m.vocab, m.dtype, 0}; }
 
 int64_t layer_ws_bytes(const rp_module_desc& m) {
   int64_t b = 256;

@@ -170,6 +170,35 @@ int sgd_step(float* w, const float* g, void* copy, int copy_dtype, int64_t n, fl
   return check_launch("sgd");
 }
 
+// y += alpha * x (float4 where aligned): accumulation of a micro-batched
+// slot's per-row-block weight gradients, in row-block order
+__global__ void axpy_kernel(float* __restrict__ y, const float* __restrict__ x, float alpha, int64_t n, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const int64_t n4 = n / 4;
+    for (int64_t q = i; q < n4; q += stride) {
+      float4 a = reinterpret_cast<float4*>(y)[q];
+      const float4 b = reinterpret_cast<const float4*>(x)[q];
+      a.x = fmaf(alpha, b.x, a.x);
+      a.y = fmaf(alpha, b.y, a.y);
+      a.z = fmaf(alpha, b.z, a.z);
+      a.w = fmaf(alpha, b.w, a.w);
+      reinterpret_cast<float4*>(y)[q] = a;
+    }
+    for (int64_t q = n4 * 4 + i; q < n; q += stride) y[q] = fmaf(alpha, x[q], y[q]);
+  } else {
+    for (; i < n; i += stride) y[i] = fmaf(alpha, x[i], y[i]);
+  }
+}
+
+int axpy(float* y, const float* x, float alpha, int64_t n, cudaStream_t st) {
+  if (n == 0) return RP_OK;
+  const int vec = ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  axpy_kernel<<<grid_for(vec ? (n + 3) / 4 : n), 256, 0, st>>>(y, x, alpha, n, vec);
+  return check_launch("axpy");
+}
+
 int embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, float* out, int64_t n,
                        int convention, cudaStream_t st) {
   if (n == 0) return RP_OK;

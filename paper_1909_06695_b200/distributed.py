@@ -216,9 +216,11 @@ class DistributedPipelineEngine:
         comm = self._comm["relay"]
         out_loss = None
         fwd_done = {}
-        mb = B // self.micro
-        for j in range(self.micro):
-            rows = (j * mb, (j + 1) * mb) if self.micro > 1 else None
+        m_ = self.micro
+        mb = B // m_
+        for j in range(m_):
+            micro = (j, m_) if m_ > 1 else None
+            kw_mb = {"micro": micro, "batch_shape": (B, T)} if micro else {}
             prev_ev = start_ev
             for k in range(1, self.K + 1):
                 if not self.owns(k):
@@ -227,11 +229,9 @@ class DistributedPipelineEngine:
                 self._micro_ok(m, B)
                 fs = self._fs[k]
                 S.wait(fs, start_ev)
-                cur = x
+                cur = x[j * mb:(j + 1) * mb] if (k == 1 and micro) else x
                 if k > 1:
-                    buf = m.input_buffer(t, B, T)
-                    if rows is not None:
-                        buf = buf[rows[0] * T:rows[1] * T]
+                    buf = m.input_buffer(t, B, T, micro=micro) if micro else m.input_buffer(t, B, T)
                     if not self.owns(k - 1):
                         S.wait(comm, start_ev)
                         with S.ctx(comm):
@@ -243,20 +243,13 @@ class DistributedPipelineEngine:
                 nxt_local = k < self.K and self.owns(k + 1)
                 out = None
                 if nxt_local:
-                    out = self.mods[k + 1].input_buffer(t, B, T)
-                    if rows is not None:
-                        out = out[rows[0] * T:rows[1] * T]
+                    nm = self.mods[k + 1]
+                    out = nm.input_buffer(t, B, T, micro=micro) if micro else nm.input_buffer(t, B, T)
+                yin = y if m.has_projection else None
+                if yin is not None and micro:
+                    yin = yin[j * mb:(j + 1) * mb]
                 with S.ctx(fs):
-                    kw = {"out": out}
-                    if rows is not None:
-                        kw["rows"] = rows
-                    xin = cur
-                    if k == 1 and rows is not None:
-                        xin = x[rows[0]:rows[1]]
-                    yin = y if m.has_projection else None
-                    if yin is not None and rows is not None:
-                        yin = yin[rows[0]:rows[1]]
-                    res = m.forward(xin, t, sid, yin, self.train, **kw)
+                    res = m.forward(cur, t, sid, yin, self.train, out=out, **kw_mb)
                 ev = S.record(fs)
                 prev_ev = ev
                 fwd_done[k] = ev

@@ -35,6 +35,10 @@ def _pad8(n):
     return (n + 7) // 8 * 8
 
 
+_GOLDEN = 0x9E3779B97F4A7C15
+_MASK64 = (1 << 64) - 1
+
+
 class Dropout:
     """(seed, integer keep threshold, 1/(1-p)) of one layer stream, or None."""
 
@@ -43,6 +47,17 @@ class Dropout:
         if not train or p <= 0.0:
             return None
         return (seed, keep_threshold(p), 1.0 / (1.0 - p))
+
+    @staticmethod
+    def shift(drop, positions):
+        """The same stream `positions` further on: the mask draws
+        splitmix64(seed + (pos + 1) * GOLDEN) (reference tensor.py:41-48,
+        63-70), so position pos + k of `seed` is position pos of
+        seed + k * GOLDEN (mod 2^64).  A row block starting at token row r0 of
+        a [B, T, d] batch uses shift(drop, r0 * d)."""
+        if drop is None or not positions:
+            return drop
+        return ((drop[0] + positions * _GOLDEN) & _MASK64,) + tuple(drop[1:])
 
 
 class Workspace:
@@ -248,8 +263,9 @@ def _p(t):
 CTA_BUDGET = {"value": 0}
 
 
-def _block_desc(x, f, B, T, drop):
+def _block_desc(x, f, B, T, drop, rows_total=0):
     dsc = N.BlockDesc()
+    dsc.drop_rows_total = rows_total or 0
     dsc.max_ctas = CTA_BUDGET["value"]
     dsc.B, dsc.T, dsc.d, dsc.f = B, T, x.shape[-1], f
     dsc.dtype = N.BF16 if x.dtype == torch.bfloat16 else N.F32
@@ -278,9 +294,11 @@ def _ws_bytes(ws, name, nbytes):
     return buf
 
 
-def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
+def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag, rows_total=0):
+    """rows_total: token rows of the whole batch when this is one row block of
+    it (micro-batched relay; the caller shifts `drop` to the block's rows)."""
     f = tape.h1.shape[-1]
-    dsc = _block_desc(x, f, B, T, drop)
+    dsc = _block_desc(x, f, B, T, drop, rows_total)
     nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
     buf = _ws_bytes(ws, "block_ws", nbytes)
     ops._count(12)
@@ -289,9 +307,9 @@ def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag):
             "block_forward")
 
 
-def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
+def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws, rows_total=0):
     f = tape.h1.shape[-1]
-    dsc = _block_desc(x, f, B, T, drop)
+    dsc = _block_desc(x, f, B, T, drop, rows_total)
     nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
     buf = _ws_bytes(ws, "block_ws", nbytes)
     g = N.BlockGrads()
@@ -303,9 +321,10 @@ def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
             "block_backward")
 
 
-def _head_desc(h, vocab):
+def _head_desc(h, vocab, rows_total=0):
     hd = N.HeadDesc()
     hd.rows, hd.d, hd.vocab = h.shape[0], h.shape[1], vocab
+    hd.rows_total = rows_total or 0
     hd.dtype = N.BF16 if h.dtype == torch.bfloat16 else N.F32
     return hd
 
@@ -320,8 +339,10 @@ def head_forward(h, tied_c, targets, vocab, hs, ws, flag):
                                         _p(hs.loss64), _p(buf), nbytes, _p(flag), ops._stream()), "head_forward")
 
 
-def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws, vo_accumulate=False):
-    hd = _head_desc(h, vocab)
+def head_backward(h, tied_c, targets, vocab, hs, g_h, vo_out, vo_alpha, ws, vo_accumulate=False, rows_total=0):
+    """rows_total: rows of the whole batch when h is one row block of it (the
+    cross-entropy gradient is 1/rows_total, layers.py:319)."""
+    hd = _head_desc(h, vocab, rows_total)
     nbytes = N.lib().rp_head_workspace_bytes(ctypes.byref(hd))
     buf = _ws_bytes(ws, "head_ws", nbytes)
     ops._count(3 if vo_out is not None else 2)

@@ -537,7 +537,17 @@ class _Arena:
 
 
 class ModuleState:
-    """One pipeline module (model.py:199-304) resident on one device."""
+    """One pipeline module (model.py:199-304) resident on one device.
+
+    Micro-batched relay (distributed.py): `forward(..., micro=(j, m),
+    batch_shape=(B, T))` runs row block j of m of the batch; the slot keeps one
+    arena per row block (B/m rows each) and the delayed backward runs them in
+    order j = 0..m-1, summing their weight gradients in that order.  Dropout
+    positions stay the flat [B, T, d] indices of the whole batch (the stream is
+    shifted to the block's first row), the loss normaliser stays B*T, so the
+    result is the whole-batch step up to fp32 summation order."""
+
+    supports_micro = True
 
     def __init__(self, index, k_total, layer_range, layers, params, dropout_seed, *, storage=None, tied=None,
                  runtime=None, cdtype=torch.bfloat16):
@@ -573,6 +583,8 @@ class ModuleState:
             st.configure_ring(self.slot_capacity)
         self._arenas = [None] * self.slot_capacity
         self._shape = None
+        self._parts = 1
+        self._loss_total = None
         self.ws_fwd = LY.Workspace(self.device)
         self.ws_bwd = LY.Workspace(self.device)
         start = layer_range[0]
@@ -593,27 +605,40 @@ class ModuleState:
         for st in self.storage:
             st.ensure(step)
 
-    def _arena(self, step, B, T):
-        if self._shape != (B, T):
+    def _arena(self, step, B, T, parts=1, part=None):
+        """The slot storage of `step`: one _Arena, or with parts > 1 the list
+        of row-block arenas (B / parts rows each); `part` picks one."""
+        if self._shape != (B, T) or self._parts != parts:
             if self.slots:
                 raise DimensionError("batch shape changed while stale slots are pending")
+            if B % parts:
+                raise DimensionError(f"batch of {B} rows does not split into {parts} row blocks")
             self._arenas = [None] * self.slot_capacity
             self._shape = (B, T)
+            self._parts = parts
         i = step % self.slot_capacity
         if self._arenas[i] is None:
-            self._arenas[i] = _Arena(self, B, T)
-        return self._arenas[i]
+            self._arenas[i] = (_Arena(self, B, T) if parts == 1 else
+                               [_Arena(self, B // parts, T) for _ in range(parts)])
+        a = self._arenas[i]
+        return a if part is None or parts == 1 else a[part]
 
-    def input_buffer(self, step, B, T):
-        """Where the upstream module should write this module's input."""
-        a = self._arena(step, B, T)
+    def input_buffer(self, step, B, T, micro=None):
+        """Where the upstream module should write this module's input (of row
+        block j when micro = (j, m))."""
+        j, m = micro if micro is not None else (None, 1)
+        a = self._arena(step, B, T, m, j)
         return a.acts[0] if a.acts else None
 
     # -- forward -----------------------------------------------------------
-    def forward(self, x, step, sample_id, targets=None, train=True, out=None):
+    def forward(self, x, step, sample_id, targets=None, train=True, out=None, micro=None, batch_shape=None):
         """Run the slice at the live weights of `step` and queue a stale slot.
         Returns the output activations [B*T, d], or for the projection module
-        the mean cross-entropy as a 0-d device tensor."""
+        the mean cross-entropy as a 0-d device tensor.  micro = (j, m) with
+        batch_shape = (B, T): row block j of m (see the class docstring); the
+        projection module returns the whole batch's loss after the last block."""
+        if micro is not None and micro[1] > 1:
+            return self._forward_block(x, step, sample_id, targets, train, out, micro, batch_shape)
         if self.has_embedding:
             B, T = x.shape
         else:
@@ -644,6 +669,54 @@ class ModuleState:
         self.last_forward_step = step
         return self._run_forward(step, arena, seeds, train, out, self.ws_fwd)
 
+    def _forward_block(self, x, step, sample_id, targets, train, out, micro, batch_shape):
+        j, m = micro
+        if batch_shape is None:
+            raise DimensionError("a micro-batched forward needs batch_shape=(B, T)")
+        B, T = batch_shape
+        if self.layers[-1].kind == "projection" and self.layers[-1].n_clusters:
+            raise DimensionError("the adaptive head does not run micro-batched")
+        mb = B // m
+        seeds = [self._layer_seed(step, i) for i in range(len(self.layers))]
+        parts = self._arena(step, B, T, m)
+        arena = parts[j]
+        if j == 0:
+            slot = StaleSlot(step, sample_id, None, targets, seeds, parts)
+            self.slots.append(slot)
+            if len(self.slots) > self.slot_capacity:
+                self.slots.pop()
+                raise ScheduleViolation(f"module {self.index} slot queue exceeded {self.slot_capacity}")
+            self.peak_slots = max(self.peak_slots, len(self.slots))
+            stored = len(self.slots) * B * T * (1 if self.has_embedding else self.d)
+            self.peak_slot_floats = max(self.peak_slot_floats, stored)
+        elif not self.slots or self.slots[-1].step != step or self.slots[-1].arena is not parts:
+            raise ScheduleViolation(f"module {self.index}: row block {j} of step {step} before block 0")
+        if self.has_embedding:
+            arena.tokens.copy_(x if torch.is_tensor(x) else torch.as_tensor(x), non_blocking=True)
+        elif x is not None and arena.acts and x.data_ptr() != arena.acts[0].data_ptr():
+            arena.acts[0].copy_(x.reshape(mb * T, self.d))
+        if self.has_projection:
+            if targets is None:
+                raise ScheduleViolation("projection module slot lacks targets")
+            tt = targets if torch.is_tensor(targets) else torch.as_tensor(targets)
+            arena.targets.copy_(tt.reshape(-1), non_blocking=True)
+        self.last_forward_step = step
+        res = self._run_forward(step, arena, seeds, train, out, self.ws_fwd, part=(j, m))
+        if self.has_projection:
+            return self._combined_loss(parts) if j == m - 1 else res
+        return res
+
+    def _combined_loss(self, parts):
+        """Mean cross-entropy of the whole batch from its row blocks' means
+        (equal block sizes), in block order."""
+        if self._loss_total is None:
+            self._loss_total = torch.zeros((), dtype=torch.float32, device=self.device)
+        self._loss_total.copy_(parts[0].head.loss)
+        for a in parts[1:]:
+            self._loss_total.add_(a.head.loss)
+        self._loss_total.div_(len(parts))
+        return self._loss_total
+
     def _infer_bt(self, Nt):
         if self._shape is not None and self._shape[0] * self._shape[1] == Nt:
             return self._shape
@@ -657,22 +730,28 @@ class ModuleState:
             R = self._R[key] = sinusoid(tp.Kl, self.d, self.cdtype, self.device)
         return R
 
-    def _load_memory(self, off, tp):
-        """Memory rows of this segment = the previous segment's layer input."""
+    def _load_memory(self, off, tp, part=(0, 1)):
+        """Memory rows of this segment = the previous segment's layer input
+        (rows of row block j of m)."""
+        j, m = part
+        rows = tp.B * tp.M * m
         buf = self.mem.get(off)
-        if buf is None or buf.shape[0] != tp.B * tp.M:
-            buf = self.mem[off] = torch.zeros(tp.B * tp.M, self.d, dtype=self.cdtype, device=self.device)
-        tp.mem.copy_(buf)
+        if buf is None or buf.shape[0] != rows:
+            buf = self.mem[off] = torch.zeros(rows, self.d, dtype=self.cdtype, device=self.device)
+        tp.mem.copy_(buf[j * tp.B * tp.M:(j + 1) * tp.B * tp.M])
         tp.mem_len = self.mem_len
 
-    def _store_memory(self, off, tp):
+    def _store_memory(self, off, tp, part=(0, 1)):
         if tp.M:
-            self.mem[off].view(tp.B, tp.M, self.d).copy_(tp.x.view(tp.B, tp.T, self.d)[:, tp.T - tp.M:])
+            j = part[0]
+            dst = self.mem[off][j * tp.B * tp.M:(j + 1) * tp.B * tp.M]
+            dst.view(tp.B, tp.M, self.d).copy_(tp.x.view(tp.B, tp.T, self.d)[:, tp.T - tp.M:])
 
     def reset_memory(self):
         self.mem_len = 0
 
-    def _run_forward(self, wstep, arena, seeds, train, out, ws, tied_c=None, from_act0=False, live=True):
+    def _run_forward(self, wstep, arena, seeds, train, out, ws, tied_c=None, from_act0=False, live=True,
+                     part=(0, 1)):
         """Forward of the slice at ring weights `wstep`.  `tied_c` overrides
         the embedding table (a snapshot of V); `from_act0` starts at the first
         block from an embedding output already in arena.acts[0] (checkpoint
@@ -684,10 +763,12 @@ class ModuleState:
         nxt = 0  # next act buffer to fill
         cur = None
         xl_live = None
+        j, m = part
+        rows_total = B * T * m if m > 1 else 0  # token rows of the whole batch (row block j of m)
         for off, layer in enumerate(self.layers):
             st = self.storage[off]
             p = layer.dropout_p if hasattr(layer, "dropout_p") else 0.0
-            drop = LY.Dropout.make(seeds[off], p, train)
+            drop = LY.Dropout.shift(LY.Dropout.make(seeds[off], p, train), j * B * T * self.d)
             if layer.kind == "embedding":
                 if from_act0:
                     cur, nxt = arena.acts[0], 1
@@ -701,25 +782,27 @@ class ModuleState:
                 cur = dst
                 nxt = 1
             elif layer.kind in ("block", "xl_block"):
-                j = self.block_idx.index(off)
-                x_in = arena.acts[j]
-                last_act = j + 1 >= len(arena.acts)
-                dst = out if last_act else arena.acts[j + 1]
+                jb = self.block_idx.index(off)
+                x_in = arena.acts[jb]
+                last_act = jb + 1 >= len(arena.acts)
+                dst = out if last_act else arena.acts[jb + 1]
                 if dst is None:
                     dst = self.ws_fwd.get("module_out", (B * T, self.d), self.cdtype)
                 W = st.weights(wstep)
                 if layer.kind == "xl_block":
-                    tp = arena.tapes[j]
+                    tp = arena.tapes[jb]
                     if live:
-                        self._load_memory(off, tp)
-                    xl_block_forward(W, W, dst.view(B * T, self.d), tp, self._sinusoid(tp), drop, ws, flag)
+                        self._load_memory(off, tp, part)
+                    xl_block_forward(W, W, dst.view(B * T, self.d), tp, self._sinusoid(tp), drop, ws, flag,
+                                     rows_total=rows_total)
                     if live:
-                        self._store_memory(off, tp)
+                        self._store_memory(off, tp, part)
                         xl_live = tp.M
                 else:
-                    LY.block_forward(W, W, x_in, dst.view(B * T, self.d), arena.tapes[j], B, T, drop, ws, flag)
+                    LY.block_forward(W, W, x_in, dst.view(B * T, self.d), arena.tapes[jb], B, T, drop, ws, flag,
+                                     rows_total=rows_total)
                 cur = dst
-                nxt = j + 2
+                nxt = jb + 2
             else:  # projection + fused CE head
                 h = arena.acts[-1]
                 if arena.adaptive is not None:
@@ -730,8 +813,8 @@ class ModuleState:
                 else:
                     LY.head_forward(h, self.tied.compute, arena.targets, self.vocab, arena.head, ws, flag)
                 cur = arena.head.loss
-        if xl_live is not None:
-            self.mem_len = xl_live  # M <= T: one segment fills the memory
+        if xl_live is not None and j == m - 1:
+            self.mem_len = xl_live  # M <= T: one segment fills the memory (after its last row block)
         return cur
 
     # -- backward ----------------------------------------------------------
@@ -753,6 +836,9 @@ class ModuleState:
         without it the two tied gradients are returned separately like the
         reference.
         Returns (g_in, grads, {"Vi", "Vo"}, loss)."""
+        if isinstance(slot.arena, list):
+            return self._backward_blocks(slot, grad_out, stale_mode, train, g_in, emb, live_step, after_head,
+                                         before_embedding, vo_overwrite)
         arena = slot.arena
         B, T = arena.B, arena.T
         Nt, d = B * T, self.d
@@ -833,6 +919,107 @@ class ModuleState:
         for st in self.storage:
             st.grad.zero_()
         return self.grad_views
+
+    def _scratch_grads(self, st):
+        """A second gradient buffer of the layer (row blocks j > 0 write here,
+        then it is added onto st.grad)."""
+        if getattr(st, "_gscratch", None) is None or st._gscratch.numel() != st.grad.numel():
+            st._gscratch = torch.empty_like(st.grad)
+            st._Gscratch = st._carve(st._gscratch, torch.float32, torch.float32)
+        return st._Gscratch
+
+    def _backward_blocks(self, slot, grad_out, stale_mode, train, g_in, emb, live_step, after_head,
+                         before_embedding, vo_overwrite):
+        """Delayed backward of a micro-batched slot: row blocks j = 0..m-1 in
+        order; block 0 writes every weight gradient, later blocks add theirs
+        (rp_axpy) -- a fixed summation order, so concurrent == serial stays
+        bitwise.  The tied gradient's output half accumulates over the blocks'
+        head backwards (cross-entropy scale 1/(B*T) of the whole batch), the
+        input half over their embedding scatters."""
+        parts = slot.arena
+        m = len(parts)
+        Bm, T = parts[0].B, parts[0].T
+        Nm, d = Bm * T, self.d
+        rows_total = Nm * m
+        if g_in is None and not self.has_embedding:
+            g_in = torch.empty(rows_total, d, dtype=torch.float32, device=self.device)
+        if stale_mode == "snapshot":
+            wstep = slot.step
+            for st in self.storage:
+                st.weights(wstep)
+        elif stale_mode == "current":
+            wstep = live_step if live_step is not None else self.last_forward_step
+            for j, a in enumerate(parts):
+                self._run_forward(wstep, a, slot.layer_seeds, train, None, self.ws_bwd, live=False, part=(j, m))
+        else:
+            raise ValueError(f"unknown stale_weights mode {stale_mode!r}")
+        ws = self.ws_bwd
+        tied_out = {"Vi": None, "Vo": None}
+        if emb is None:
+            emb_alpha, emb_beta = 1.0, 1.0
+            vo_buf = torch.empty(self.vocab, d, dtype=torch.float32, device=self.device) \
+                if self.has_projection else None
+            vi_buf = torch.zeros(self.vocab, d, dtype=torch.float32, device=self.device) \
+                if self.has_embedding else None
+            tied_out = {"Vi": vi_buf, "Vo": vo_buf}
+        else:
+            emb_alpha, emb_beta, emb_grad = emb
+            vo_buf = emb_grad if emb_alpha else None
+            vi_buf = emb_grad if emb_beta else None
+        for j, arena in enumerate(parts):
+            r0, r1 = j * Nm, (j + 1) * Nm
+            if self.has_projection:
+                g = ws.get("g_stream_a", (Nm, d), torch.float32)
+                LY.head_backward(arena.acts[-1], self.tied.compute, arena.targets, self.vocab, arena.head, g, vo_buf,
+                                 emb_alpha, ws, vo_accumulate=(emb is not None and not vo_overwrite) or j > 0,
+                                 rows_total=rows_total)
+                if after_head is not None and j == m - 1:
+                    after_head()
+            else:
+                if grad_out is None:
+                    raise ScheduleViolation(f"module {self.index} missing boundary gradient")
+                g = grad_out.reshape(rows_total, d)[r0:r1]
+            ping = 0
+            for jb in range(self.n_blocks - 1, -1, -1):
+                off = self.block_idx[jb]
+                st = self.storage[off]
+                W = st.weights(wstep)
+                G = st.G if j == 0 else self._scratch_grads(st)
+                drop = LY.Dropout.shift(LY.Dropout.make(slot.layer_seeds[off], self.layers[off].dropout_p, train),
+                                        r0 * d)
+                first = jb == 0 and not self.has_embedding
+                if first and g_in is not None:
+                    g_next = g_in.reshape(rows_total, d)[r0:r1]
+                else:
+                    g_next = ws.get("g_stream_b" if ping == 0 else "g_stream_a", (Nm, d), torch.float32)
+                    ping ^= 1
+                if self.layers[off].kind == "xl_block":
+                    tp = arena.tapes[jb]
+                    xl_block_backward(W, W, tp, self._sinusoid(tp), g, g_next, G, drop, ws, rows_total=rows_total)
+                else:
+                    LY.block_backward(W, W, arena.acts[jb], arena.tapes[jb], g, g_next, G, Bm, T, drop, ws,
+                                      rows_total=rows_total)
+                if j > 0:
+                    ops.axpy(st.grad, st._gscratch)
+                g = g_next
+            if self.has_embedding:
+                if before_embedding is not None and j == 0:
+                    before_embedding()
+                st = self.storage[0]
+                G = st.G if j == 0 else self._scratch_grads(st)
+                drop = LY.Dropout.shift(LY.Dropout.make(slot.layer_seeds[0], self.layers[0].dropout_p, train),
+                                        r0 * d)
+                LY.embed_backward(g, arena.tokens, self.layers[0].max_seq_len, G["pos"], vi_buf, emb_beta, ws, drop)
+                if j > 0:
+                    ops.axpy(st.grad, st._gscratch)
+            elif g_in is not None:
+                dst = g_in.reshape(rows_total, d)[r0:r1]
+                if g.data_ptr() != dst.data_ptr():
+                    dst.copy_(g)
+        loss = self._combined_loss(parts) if self.has_projection else None
+        if self.has_embedding:
+            return None, self.grad_views, tied_out, loss
+        return g_in, self.grad_views, tied_out, loss
 
 
 def build_modules(stack, part, dropout_seed):

@@ -441,6 +441,15 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
                                       mem_len, scale, _stream()), "xl_attn_bwd_dq")
 
 
+def axpy(y, x, alpha=1.0):
+    """y += alpha * x (fp32, same element count)."""
+    _require_cuda(y, x)
+    if y.dtype != torch.float32 or x.dtype != torch.float32 or y.numel() != x.numel():
+        raise DimensionError("axpy takes two fp32 tensors of one size")
+    _count(1)
+    N.check(N.lib().rp_axpy(_ptr(y), _ptr(x), alpha, y.numel(), _stream()), "axpy")
+
+
 def rows_copy(src, dst, cols=None, val=None, val_const=0.0, aug=False):
     """dst[r, :cols] = src[r, :cols]; with aug, dst[r, cols] = val[r] (or val_const); zeros to dst's width."""
     _require_cuda(src, dst)

@@ -109,11 +109,14 @@ def fused_dq_ok(tp):
     return FUSED_DQ and fused_bwd_ok(tp) and tp.dh == 64 and tp.T % 128 == 0
 
 
-def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
-    """tp.xa holds [memory; x]; writes out [B*T, d] and the tape."""
+def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
+    """tp.xa holds [memory; x]; writes out [B*T, d] and the tape.  rows_total:
+    token rows of the whole batch when this is one row block of it (the
+    second dropout mask starts at rows_total * d; `drop` is already shifted
+    to the block's first row)."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
     d = H * dh
-    n = B * T * d
+    n = (rows_total or B * T) * d
     cdt = tp.xa.dtype
     ops.layernorm_fwd(tp.xa, vecs["ln1_g"], vecs["ln1_b"], tp.a, tp.mean1, tp.rstd1, flag)
     _bg(tp.a, W["wqkv"], b_mn=True, out=tp.qkv)
@@ -144,14 +147,14 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag):
              residual=tp.x1, dropout=d1)
 
 
-def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws):
+def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     """g_out, g_x: [B*T, d] fp32.  No gradient flows into the memory rows;
     their LayerNorm / K / V contributions to the weight gradients do."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
     d = H * dh
     f = tp.h1.shape[-1]
     Nt = B * T
-    n = Nt * d
+    n = (rows_total or Nt) * d
     cdt = tp.xa.dtype
     scale = 1.0 / math.sqrt(dh)
     # feed-forward + LN2 (as the reference block)

@@ -34,6 +34,8 @@ class TiedStore:
 
 
 class CpuModule:
+    supports_micro = True
+
     def __init__(self, index, K, lo, hi, layers, dropout_seed, p, tied, d):
         self.index, self.K, self.lo, self.hi = index, K, lo, hi
         self.params = layers  # list of dicts of numpy arrays (live, shared with the optimizer)
@@ -60,26 +62,56 @@ class CpuModule:
             if len(self.ring) > self.cap:
                 del self.ring[s]
 
-    def input_buffer(self, t, B, T):
-        buf = torch.empty(B * T, self.d, dtype=torch.float64)
+    def input_buffer(self, t, B, T, micro=None):
+        rows = B * T if micro is None else B // micro[1] * T
+        buf = torch.empty(rows, self.d, dtype=torch.float64)
         self._inputs[t] = buf
         return buf
 
-    def _run(self, params, V, x, seeds, train):
+    def _run(self, params, V, x, seeds, train, pos0=0, n_total=None):
         caches = []
         h = x
         for off, kind in enumerate(self.kinds):
             P = params[off]
             if kind == "embedding":
-                h, c = OL.embed_fwd(V, P["pos"], h, seeds[off], self.p, train)
+                h, c = OL.embed_fwd(V, P["pos"], h, seeds[off], self.p, train, pos0=pos0)
             elif kind == "block":
-                h, c = OL.block_fwd(P, h, seeds[off], self.p, train)
+                h, c = OL.block_fwd(P, h, seeds[off], self.p, train, pos0=pos0, n_total=n_total)
             else:
                 c = None
             caches.append(c)
         return h, caches
 
-    def forward(self, x, step, sample_id, targets=None, train=True, out=None):
+    def _forward_block(self, x, step, sample_id, targets, train, out, micro, batch_shape):
+        """Row block j of m (the micro-batched relay): the block's rows of the
+        whole-batch forward -- dropout positions offset by its first row."""
+        j, m = micro
+        B, T = batch_shape
+        mb = B // m
+        seeds = [hash64(self.dropout_seed, step, self.lo + off) for off in range(len(self.kinds))]
+        xin = np.asarray(x) if self.has_embedding else x.numpy().reshape(mb, T, -1).copy()
+        tg = None if targets is None else np.asarray(targets)
+        if j == 0:
+            self.slots.append(Slot(step, sample_id, [xin], [tg], seeds))
+            if len(self.slots) > self.cap:
+                raise RuntimeError("slot overflow")
+        else:
+            self.slots[-1].inputs.append(xin)
+            self.slots[-1].targets.append(tg)
+        V = self.tied.master.numpy() if self.tied is not None else None
+        h, _ = self._run(self.params, V, xin, seeds, train, pos0=j * mb * T * self.d, n_total=B * T * self.d)
+        if self.has_projection:
+            self._block_losses = ([] if j == 0 else self._block_losses) + [OL.head_loss(h, V, tg)]
+            return torch.tensor(float(np.mean(self._block_losses)), dtype=torch.float64)
+        res = torch.from_numpy(np.ascontiguousarray(h.reshape(-1, h.shape[-1])))
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
+
+    def forward(self, x, step, sample_id, targets=None, train=True, out=None, micro=None, batch_shape=None):
+        if micro is not None and micro[1] > 1:
+            return self._forward_block(x, step, sample_id, targets, train, out, micro, batch_shape)
         seeds = [hash64(self.dropout_seed, step, self.lo + off) for off in range(len(self.kinds))]
         if self.has_embedding:
             xin = np.asarray(x)
@@ -107,8 +139,48 @@ class CpuModule:
             g.zero_()
         return self.grads
 
+    def _backward_blocks(self, slot, grad_out, train, g_in, emb):
+        """Row blocks in order; block 0 writes the weight gradients, later
+        blocks add theirs (the device's fixed order)."""
+        params, V = self.ring[slot.step]
+        m = len(slot.inputs)
+        mb, T = slot.inputs[0].shape[0], slot.inputs[0].shape[1]
+        B = mb * m
+        loss = []
+        for j in range(m):
+            r0 = j * mb * T
+            h, caches = self._run(params, V, slot.inputs[j], slot.seeds, train, pos0=r0 * self.d,
+                                  n_total=B * T * self.d)
+            if self.has_projection:
+                lj, g, dvo = OL.head_loss_grad(h, V, slot.targets[j])
+                g, dvo = g / m, dvo / m  # the whole batch's 1/(B*T) normaliser
+                loss.append(lj)
+                if emb is not None and emb[0]:
+                    emb[2].add_(torch.from_numpy(emb[0] * dvo))
+            else:
+                g = grad_out.numpy().reshape(B, T, self.d)[j * mb:(j + 1) * mb]
+            for off in range(len(self.kinds) - 1, -1, -1):
+                kind = self.kinds[off]
+                if kind == "block":
+                    g, G = OL.block_bwd(params[off], caches[off], g)
+                    for n, a in G.items():
+                        dst = self.grads[f"L{self.lo + off}.{n}"]
+                        dst.copy_(torch.from_numpy(a)) if j == 0 else dst.add_(torch.from_numpy(a))
+                elif kind == "embedding":
+                    dvi, gpos = OL.embed_bwd(g, caches[off], V.shape[0], params[off]["pos"].shape)
+                    dst = self.grads[f"L{self.lo + off}.pos"]
+                    dst.copy_(torch.from_numpy(gpos)) if j == 0 else dst.add_(torch.from_numpy(gpos))
+                    if emb is not None and emb[1]:
+                        emb[2].add_(torch.from_numpy(emb[1] * dvi))
+                    g = None
+            if g is not None and g_in is not None:
+                g_in[j * mb * T:(j + 1) * mb * T].copy_(torch.from_numpy(np.ascontiguousarray(g.reshape(-1, self.d))))
+        return g_in, self.grads, {}, (float(np.mean(loss)) if loss else None)
+
     def recompute_backward(self, slot, grad_out, stale_mode="snapshot", train=True, *, g_in=None, emb=None,
                            live_step=None):
+        if isinstance(slot.inputs, list):
+            return self._backward_blocks(slot, grad_out, train, g_in, emb)
         params, V = self.ring[slot.step]
         h, caches = self._run(params, V, slot.inputs, slot.seeds, train)
         B, T = (slot.inputs.shape[0], slot.inputs.shape[1])

@@ -1,10 +1,15 @@
-"""world_size-2 gloo run of DistributedPipelineEngine (the multi-GPU schedule:
-ring placement, P2P relay of activations, boundary-gradient exchange one step
-later, tied gradient on rank 0) against the single-process oracle.
+"""gloo runs of DistributedPipelineEngine (the multi-GPU schedule: ring
+placement, P2P relay of activations on one process group, boundary-gradient
+exchange one step later on another, tied gradient on rank 0) against the
+single-process oracle.
 
-K = 3 modules on 2 ranks: modules 1 and 3 on rank 0, module 2 on rank 1
-(reference model.py:137-140).  Module compute is the fp64 oracle layer math
-(tests/cpu_modules.py), so packets must match the oracle to ~1e-12."""
+world size 2 -> K = 3 modules (1 and 3 on rank 0, 2 on rank 1); world size 3
+-> K = 4 (1 and 4 on rank 0); reference model.py:137-140.  Each with the
+whole-batch relay and the micro-batched relay (the batch streams through the
+ring as m row blocks; dropout positions and the loss normaliser stay those of
+the whole batch, weight gradients sum over the blocks in a fixed order).
+Module compute is the fp64 oracle layer math (tests/cpu_modules.py), so
+packets must match the oracle to ~1e-12."""
 
 import os
 import socket
@@ -19,7 +24,7 @@ import torch.multiprocessing as mp
 from oracle import ouroboros as OO
 from oracle.rng import Stream
 
-CFG = dict(vocab=11, d=8, f=12, blocks=4, seq=5, batch=3, p=0.15, init_seed=4, dseed=6, data_seed=2)
+CFG = dict(vocab=11, d=8, f=12, blocks=4, seq=5, batch=4, p=0.15, init_seed=4, dseed=6, data_seed=2)
 STEPS = 6
 LR = 0.05
 
@@ -47,7 +52,7 @@ class _Batch:
         self.x, self.y, self.sample_id, self.shape = x, y, sid, shape
 
 
-def _worker(rank, world, port, K, outdir):
+def _worker(rank, world, port, K, outdir, micro=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -63,7 +68,8 @@ def _worker(rank, world, port, K, outdir):
             if part.device_of[k - 1] == rank:
                 mods[k] = CpuModule(k, K, lo, hi, layers[lo:hi], CFG["dseed"], CFG["p"],
                                     tied if (lo == 0 or hi == len(layers)) else None, CFG["d"])
-        eng = DistributedPipelineEngine(mods, part, rank, tied=tied, d_model=CFG["d"], grad_dtype=torch.float64)
+        eng = DistributedPipelineEngine(mods, part, rank, tied=tied, d_model=CFG["d"], grad_dtype=torch.float64,
+                                        micro_batches=micro)
         opt = CpuSgd(LR)
         rec = {}
         for t, (x, y) in enumerate(_batches()):
@@ -82,26 +88,28 @@ def _worker(rank, world, port, K, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("K", [3])
-def test_two_rank_ring_matches_oracle(K):
+@pytest.mark.parametrize("world,micro", [(2, 1), (2, 2), (3, 1), (3, 4)])
+def test_ring_matches_oracle(world, micro):
+    K = world + 1
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(2, _free_port(), K, d), nprocs=2, join=True)
-        r0 = dict(np.load(os.path.join(d, "rank0.npz")))
-        r1 = dict(np.load(os.path.join(d, "rank1.npz")))
+        mp.spawn(_worker, args=(world, _free_port(), K, d, micro), nprocs=world, join=True)
+        recs = [dict(np.load(os.path.join(d, f"rank{r}.npz"))) for r in range(world)]
+    r0 = recs[0]
     V, layers = OO.init_params(CFG["vocab"], CFG["d"], CFG["f"], CFG["blocks"], CFG["seq"], CFG["init_seed"])
     ora = OO.OuroborosOracle(V, layers, K, CFG["dseed"], CFG["p"], OO.Sgd(lambda t: LR))
     for t, (x, y) in enumerate(_batches()):
         loss, pk = ora.step(t, x, y)
         assert abs(r0[f"loss.{t}"] - loss) <= 1e-12 * abs(loss)
         for k, mg in enumerate(pk["module_grads"], start=1):
-            rec = r0 if k in (1, K) else r1
+            rec = r0 if k in (1, K) else recs[k - 1]
             for key, ref in mg.items():
                 np.testing.assert_allclose(rec[f"g.{t}.{key}"], ref, rtol=1e-10, atol=1e-13)
         np.testing.assert_allclose(r0[f"emb.{t}"], pk["emb_grad"], rtol=1e-10, atol=1e-13)
-        # rank 0 reports modules (1, K), rank 1 module 2
+        # rank 0 reports modules (1, K), rank r module r + 1
         sids = pk["sample_ids"]
         assert list(r0[f"sid.{t}"]) == [-1 if s is None else s for s in (sids[0], sids[-1])]
-        assert list(r1[f"sid.{t}"]) == [-1 if s is None else s for s in sids[1:-1]]
+        for r in range(1, world):
+            assert list(recs[r][f"sid.{t}"]) == [-1 if sids[r] is None else sids[r]]
 
 
 def test_hop_order_is_global():

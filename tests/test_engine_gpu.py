@@ -142,3 +142,86 @@ def test_distributed_engine_single_rank_equals_pipeline_engine():
         for g1, g2 in zip(c1.module_grads, p2.module_grads):
             for key in g1:
                 assert np.array_equal(g1[key], g2[key].double().cpu().numpy()), key
+
+
+@pytest.mark.parametrize("micro", [2, 4])
+def test_micro_batched_relay_matches_oracle(micro):
+    """The micro-batched relay (distributed.py) on real device
+    modules: the batch streams through the modules as `micro` row blocks at
+    the same weights; dropout positions and the 1/(B*T) normaliser stay the
+    whole batch's, so in the fp32 check mode every step matches the fp64
+    oracle like the whole-batch engine does (loss rel <= 2e-5, packets rel-L2
+    <= 2e-4), and the weight gradients sum over the row blocks in a fixed
+    order (a re-run is bitwise identical)."""
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as M
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200.distributed import DistributedPipelineEngine, build_local_modules
+
+    cfg = dict(SMALL, batch=8)
+    runs = []
+    for _ in range(2):
+        _, _, _, ora = make_pair(cfg, 2, "adam", 2e-3)
+        stack = M.build_stack(cfg["vocab"], cfg["d"], cfg["f"], cfg["blocks"], cfg["seq"], cfg["p"],
+                              cfg["init_seed"], dtype="fp32")
+        part = M.partition(stack.num_layers, 2)
+        mods = build_local_modules(stack, part, cfg["dseed"], 0)
+        eng = DistributedPipelineEngine(mods, part, 0, tied=stack.tied_store, device=stack.runtime.device,
+                                        micro_batches=micro)
+        opt = O.make_optimizer("adam", O.LrSchedule(2e-3, "fixed"))
+        rec = []
+        for t, (x, y) in enumerate(batches(cfg, 5)):
+            packet, loss = eng.step(t, E.BatchSample(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), t),
+                                    opt)
+            got = packet.cpu()
+            oloss, opk = ora.step(t, x, y)
+            assert abs(loss - oloss) <= 2e-5 * abs(oloss), (t, loss, oloss)
+            for k in range(2):
+                for key, want in opk["module_grads"][k].items():
+                    g = got.module_grads[k][key]
+                    if not np.any(want):
+                        assert not np.any(g), (t, k, key)
+                    else:
+                        assert rel(g, want) <= 2e-4, (t, k, key, rel(g, want))
+            if np.any(opk["emb_grad"]):
+                assert rel(got.emb_grad, opk["emb_grad"]) <= 2e-4
+            rec.append((loss, got.emb_grad.copy()))
+        runs.append(rec)
+    for (l1, e1), (l2, e2) in zip(*runs):
+        assert l1 == l2 and np.array_equal(e1, e2)
+
+
+def test_micro_batched_xl_relay_matches_restatement():
+    """The same with Transformer-XL blocks: each row block carries its rows of
+    the segment memory."""
+    from oracle import xl as X
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as M
+    from paper_1909_06695_b200 import optim as O
+    from paper_1909_06695_b200.data import SegmentStream
+    from paper_1909_06695_b200.distributed import DistributedPipelineEngine, build_local_modules
+
+    c = dict(vocab=64, d=32, f=64, blocks=2, seq=8, mem=8, heads=4, batch=4, p=0.1, init_seed=5, dseed=9)
+    stack = M.build_xl_stack(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["p"], c["init_seed"], c["heads"],
+                             c["mem"], dtype="fp32")
+    part = M.partition(stack.num_layers, 2)
+    mods = build_local_modules(stack, part, c["dseed"], 0)
+    eng = DistributedPipelineEngine(mods, part, 0, tied=stack.tied_store, device=stack.runtime.device,
+                                    micro_batches=2)
+    opt = O.make_optimizer("adam", O.LrSchedule(2e-3, "fixed"))
+    V, layers = X.init_xl_params(c["vocab"], c["d"], c["f"], c["blocks"], c["seq"], c["heads"], c["init_seed"])
+    ora = X.XLOuroborosOracle(V, layers, 2, c["dseed"], c["p"], c["heads"], c["mem"], c["batch"],
+                              OO.Adam(lambda t: 2e-3))
+    toks = (Stream(2).uniform((c["batch"] * 7 * c["seq"] + 4,)) * c["vocab"]).astype(np.int64)
+    src = SegmentStream(toks, c["seq"], c["batch"])
+    for t in range(6):
+        b = src.batch_at(t)
+        packet, loss = eng.step(t, E.BatchSample(torch.as_tensor(b.x).cuda(), torch.as_tensor(b.y).cuda(), t), opt)
+        got = packet.cpu()
+        oloss, opk = ora.step(t, b.x, b.y)
+        assert abs(loss - oloss) <= 2e-5 * abs(oloss), (t, loss, oloss)
+        for k in range(2):
+            for key, want in opk["module_grads"][k].items():
+                g = got.module_grads[k][key]
+                if np.any(want):
+                    assert rel(g, want) <= 2e-4, (t, k, key, rel(g, want))
