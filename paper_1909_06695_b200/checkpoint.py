@@ -1,7 +1,13 @@
 """RPCK checkpoint container: named arrays plus a JSON sidecar.
 
-Byte-compatible with the reference container (checkpoint.py:1-70) so runs
-move between the two implementations:
+Byte-compatible with the reference container (checkpoint.py:1-70).  The
+reference's checkpoints load here (runner.load_training_state re-derives the
+pending slots from the reference's ring, including its snapshots of V).  The
+other direction is one-way by design: this package keeps no snapshots of the
+tied matrix (module 1's slots carry their embedding output instead, entry
+`m1.slot{j}.embedded`), so its checkpoints lack the reference's
+`m{k}.ring.{s}.L{i}.tied` entries and the reference loader, which requires
+them (reference runner.py:186-195), cannot read them.  The container layout:
 
     "RPCK" | u32 version=1 | u32 count |
     count x ( u16 name_len | name utf-8 | u8 dtype tag | u8 ndim |

@@ -904,24 +904,25 @@ bool pdl_enabled() {
 }
 
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = n[dev & 63];
+  if (c == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    c = v > 0 ? v : 148;
   }
-  return n;
+  return c;
 }
 
 template <bool kTf32, int BN, int kCta>
 int launch(const rp_gemm_args& a, cudaStream_t stream) {
   using Cfg = GemmCfg<kTf32, BN, kCta>;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done))
     cudaFuncSetAttribute(gemm_kernel<kTf32, BN, kCta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM_BYTES);
-  });
   CUtensorMap ma, mal, mb, mbl;
   const int ks = a.k_splits > 1 ? a.k_splits : 1;
   if (ks > 1 && (a.batch > 1 || a.epilogue != RP_EPI_STORE))
@@ -1089,10 +1090,25 @@ int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows,
 // on every block GEMM (tools/prof_block.py: 0.458 vs 0.593 ms per block
 // fwd+bwd).  RP_TILE_N_SPREAD=1 instead narrows N to give every SM two tiles.
 int gemm_tile_n(int64_t M, int64_t N, int64_t batch) {
-  static int spread = -1;
+  static int spread = -1, waves = -1;
   if (spread < 0) {
     const char* e = getenv("RP_TILE_N_SPREAD");
     spread = (e && e[0] == '1') ? 1 : 0;
+    const char* w = getenv("RP_TILE_WAVES");
+    waves = (w && w[0] == '1') ? 1 : 0;
+  }
+  if (!spread && waves && N > 256 && N <= 1024 && M > 128 && pair_enabled()) {
+    // RP_TILE_WAVES=1 (A/B switch, off by default): pick the 128-wide tile
+    // when the 256-wide tiling leaves most of its last wave of CTA pairs idle
+    // (a 128-wide tile modelled at half the work and ~15% lower efficiency),
+    // e.g. the N = 512 block GEMMs at 11,264 rows (C3: 88 tiles on 74 pairs).
+    // Measured slower on the C3 step (14.05 vs 13.75 ms): the narrow tiles
+    // lose more than the model's 15%.
+    const int64_t pairs = std::max<int64_t>(1, num_sms() / 2);
+    const int64_t mt = (M + 255) / 256 * std::max<int64_t>(batch, 1);
+    const int64_t w256 = (mt * ((N + 255) / 256) + pairs - 1) / pairs;
+    const int64_t w128 = (mt * ((N + 127) / 128) + pairs - 1) / pairs;
+    return (w128 * 128 * 115 < w256 * 256 * 100) ? 128 : 256;
   }
   if (!spread) return N > 128 ? 256 : (N > 64 ? 128 : 64);
   if (N <= 64) return 64;

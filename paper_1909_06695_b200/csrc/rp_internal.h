@@ -6,7 +6,23 @@
 
 #include "../../include/ringpipe_b200.h"
 
+#include <mutex>
+
 namespace rp {
+
+// Function attributes (e.g. the dynamic shared-memory opt-in) are per device:
+// returns true the first time a call site asks on the current device.  `done`
+// is a per-call-site bitmask of devices (a static at the call site).
+inline bool first_on_device(uint64_t& done) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done & bit) return false;
+  done |= bit;
+  return true;
+}
 
 // Records a formatted error message (thread-local) and returns `status`.
 int set_error(int status, const char* fmt, ...);

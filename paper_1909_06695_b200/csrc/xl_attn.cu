@@ -1010,11 +1010,10 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
   CUtensorMap mp;
   RP_TRY0(tma_map_bf16_store32(&mp, probs, ldp, Tn, ldp, HB));
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done)) {
     cudaFuncSetAttribute(xl_attn_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fwd<1>());
     cudaFuncSetAttribute(xl_attn_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fwd<2>());
-    attr = true;
   }
   FwdParams p;
   p.p = static_cast<__nv_bfloat16*>(probs);
@@ -1056,11 +1055,10 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 128, kQT, false));
   CUtensorMap mac;
   RP_TRY0(tma_map_bf16_store32(&mac, gac, ldp, Tn, ldp, HB));
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done)) {
     cudaFuncSetAttribute(xl_attn_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bwd<1>());
     cudaFuncSetAttribute(xl_attn_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bwd<2>());
-    attr = true;
   }
   BwdParams p;
   p.p = static_cast<const __nv_bfloat16*>(probs);
@@ -1106,13 +1104,9 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kKT));
   RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
   RP_TRY0(tma_map_bf16(&mac, gac, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
-  static int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done))
     cudaFuncSetAttribute(xl_attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
-    attr_dev = dev;
-  }
   DqParams q{};
   BwdParams& p = q.b;
   p.p = static_cast<const __nv_bfloat16*>(probs);

@@ -454,7 +454,8 @@ def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
     g_out = torch.ones(Nt, d, dtype=torch.float32, device=dev)
     g_in = torch.empty_like(g_out)
     targets = torch.zeros(Nt, dtype=torch.int64, device=dev)
-    tape = head = None
+    tape = head = xtape = adaptive = R = ytgt = None
+    act.zero_()
     costs = []
     for idx, (layer, st) in enumerate(zip(stack.layers, stack.storage)):
         mat = torch.empty(st.n_mat, dtype=cdt, device=dev)
@@ -473,6 +474,32 @@ def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
             def run():
                 LY.block_forward(W, W, act, out, tape, B, T, drop, ws, rt.flag)
                 LY.block_backward(W, W, act, tape, g_out, g_in, st.G, B, T, drop, ws)
+        elif layer.kind == "xl_block":
+            # a full memory (the steady state): attention over M + T keys
+            if xtape is None:
+                xtape = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev)
+                xtape.xa.zero_()
+                xtape.mem_len = layer.mem_len
+                R = sinusoid(xtape.Kl, d, cdt, dev)
+
+            def run():
+                xl_block_forward(W, W, out, xtape, R, drop, ws, rt.flag)
+                xl_block_backward(W, W, xtape, R, g_out, g_in, st.G, drop, ws)
+        elif layer.n_clusters:
+            # adaptive tied softmax: the head cluster for every row, each tail
+            # for the rows whose (Zipf-distributed, model.py:144-159 has no
+            # targets either) synthetic target falls in it
+            if adaptive is None:
+                adaptive = AdaptiveHead(layer.vocab_size, d, layer.cutoffs, dev, cdt)
+                w = 1.0 / torch.arange(1, layer.vocab_size + 1, dtype=torch.float64)
+                ytgt = torch.multinomial(w / w.sum(), Nt, replacement=True,
+                                         generator=torch.Generator().manual_seed(0)).numpy()
+            P, Gp = W, st.G
+
+            def run():
+                adaptive.forward(act, tied.compute, P["cluster_weight"], P["cluster_bias"], ytgt, rt.flag)
+                adaptive.backward(g_in, tied.grad, Gp["cluster_weight"], Gp["cluster_bias"], alpha=1.0,
+                                  accumulate=False)
         else:
             if head is None:
                 head = LY.HeadState(Nt, dev)

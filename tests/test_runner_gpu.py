@@ -189,3 +189,19 @@ def test_timed_trace_rows_follow_the_device(tmp_path):
         assert [r["module"] for r in fwd] == [1, 2, 3]
         for a, b in zip(fwd, fwd[1:]):
             assert b["start"] >= a["end"] - 1e-3  # the relay: module k+1 starts after module k
+
+
+def test_checkpoint_compatibility_is_one_way(in_gold, tmp_path):
+    """ADVICE r1 (checkpoint.py docstring): our checkpoints carry module 1's
+    embedding outputs (m1.slot{j}.embedded) instead of snapshots of the tied
+    matrix, so the reference's `m{k}.ring.{s}.L{i}.tied` entries -- which the
+    reference loader pops for every ring parameter (reference runner.py:186-195)
+    -- are absent; the reference's own checkpoint has them and loads here
+    (test_resume_from_reference_checkpoint)."""
+    R.train(cfg_for(tmp_path, "halt", halt_at=5))
+    ours = ckpt.load_arrays(str(tmp_path / "halt" / "checkpoint.bin"))
+    ring = [n for n in ours if ".ring." in n]
+    assert ring and not any(n.endswith(".tied") for n in ring)
+    assert any(n.startswith("m1.slot") and n.endswith(".embedded") for n in ours)
+    theirs = ckpt.load_arrays(os.path.join(GOLD, "halt6.bin"))
+    assert any(".ring." in n and n.endswith(".tied") for n in theirs)

@@ -140,3 +140,20 @@ def test_xl_concurrent_bitwise_equals_reference_executor_and_bf16_tracks():
         assert np.array_equal(c1.emb_grad, c2.emb_grad)
         oloss, _ = ora.step(t, b.x, b.y)
         assert abs(l1 - oloss) <= 2e-2 * abs(oloss)
+
+
+def test_by_cost_times_xl_blocks_and_the_adaptive_head():
+    """measure_layer_costs times Transformer-XL blocks as XL blocks
+    (attention over a full memory) and the adaptive head as the adaptive head,
+    so by_cost partitions of the XL configs balance real costs."""
+    from paper_1909_06695_b200 import model as MD
+
+    stack = MD.build_xl_stack(2000, 64, 128, 4, 32, 0.1, 3, 4, 32, dtype="bf16", cutoffs=[104, 504])
+    x = (Stream(1).uniform((4, 32)) * 2000).astype(np.int64)
+    costs = MD.measure_layer_costs(stack, x, dropout_seed=3)
+    assert len(costs) == stack.num_layers and all(c > 0 for c in costs)
+    blocks = costs[1:-1]
+    # the four XL blocks are the same work: within 2x of each other
+    assert max(blocks) <= 2.0 * min(blocks)
+    part = MD.partition(stack.num_layers, 3, "by_cost", costs)
+    assert sum(hi - lo for lo, hi in part.groups) == stack.num_layers
