@@ -649,6 +649,310 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Forward with P.V folded in (head dim 64): xl_attn_fwd_kernel<1>, plus per
+// pass-2 key step the normalised P tile written once into a 128B-swizzled
+// [128 x 64] shared tile -- the A operand of
+//     O += P V_step                       128 x 64   (TMEM cols 256..319)
+// and the source of P's TMA store -- so the head-dim-wide P.V GEMM over the
+// stored P (and the head merge of its output) disappear; O is written
+// straight into the merged ctx rows.  Pass 2 keeps one score buffer (TMEM
+// cols 0..255) so O fits beside it.
+constexpr int kFwdPvSmem = 1024 + 2 * 16384 /*Qu, Qv*/ + 3 * 32768 /*K + R band stages*/ + 8192 /*V*/ +
+                           16384 /*P tile*/ + kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 256;
+
+struct FwdPvParams {
+  FwdParams f;
+  __nv_bfloat16* ctx;  // merged [B*T, H*64]
+  int d;
+};
+
+__global__ void __launch_bounds__(kThreadsFwd, 1)
+    xl_attn_fwd_pv_kernel(const __grid_constant__ CUtensorMap mQu, const __grid_constant__ CUtensorMap mQv,
+                          const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
+                          const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mP,
+                          const FwdPvParams pp) {
+  const FwdParams& p = pp.f;
+  using C = FwdCfg<1>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
+  uint8_t* sQu = smem;
+  uint8_t* sQv = smem + C::QBytes;
+  uint8_t* stages = smem + 2 * C::QBytes;
+  uint8_t* sV = stages + 3 * C::StageBytes;  // 1024-aligned
+  uint8_t* sP = sV + 8192;
+  float* ring = reinterpret_cast<float*>(sP + 16384);
+  float* stats = ring + kSoftWarps * kRingWarp;  // [half][row][max, sum]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stats + 2 * kQT * 2);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [3]
+  uint64_t* kv_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;    // [2]
+  uint64_t* s_empty = bars + 9;   // [2]
+  uint64_t* v_full = bars + 11;
+  uint64_t* v_empty = bars + 12;
+  uint64_t* p_full = bars + 13;
+  uint64_t* p_free = bars + 14;
+  uint64_t* o_full = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int hb, qt;
+  cta_tile(p.nqt, p.heavy_first, hb, qt);
+  const int h = hb / p.B, b = hb % p.B;
+  const int i0 = qt * kQT;
+  const int imax = min(i0 + kQT, p.T) - 1;
+  const int jt_lo = p.lo / kFKT, jt_hi = min(p.M + imax, p.Kl - 1) / kFKT;
+  const int per_pass = jt_hi - jt_lo + 1;
+  const int nsteps = 2 * per_pass;
+  // buffer of step n: pass 1 alternates 0 / 1, pass 2 always 0.  Use index
+  // of that buffer (its mbarrier phase = use & 1):
+  auto buf_of = [&](int n) { return n < per_pass ? (n & 1) : 0; };
+  auto use_of = [&](int n) {
+    if (n < per_pass) return n >> 1;
+    return (per_pass + 1) / 2 + (n - per_pass);  // pass 1 used buffer 0 ceil(per_pass / 2) times
+  };
+  // the last pass-1 use of buffer 1 (its TMEM columns hold O in pass 2)
+  const int last_b1 = per_pass >= 2 ? ((per_pass - 2) | 1) : -1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQu);
+    tma_prefetch(&mQv);
+    tma_prefetch(&mK);
+    tma_prefetch(&mR);
+    tma_prefetch(&mV);
+    tma_prefetch(&mP);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int bb = 0; bb < 2; ++bb) {
+      mbar_init(&s_full[bb], 1);
+      mbar_init(&s_empty[bb], kSoftWarps * 32);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(p_full, kSoftWarps * 32);
+    mbar_init(p_free, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t t_o = tmem_base + 256;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_expect_tx(q_full, 2 * C::QBytes);
+      tma_atoms<1>(sQu, &mQu, q_full, kQT, i0, hb);
+      tma_atoms<1>(sQv, &mQv, q_full, kQT, i0, hb);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int n = 0; n < nsteps; ++n) {
+        mbar_wait(&kv_empty[s], ph ^ 1);
+        const int j0 = (jt_lo + n % per_pass) * kFKT;
+        uint8_t* sk = stages + s * C::StageBytes;
+        mbar_expect_tx(&kv_full[s], C::StageBytes);
+        tma_atoms<1>(sk, &mK, &kv_full[s], kFKT, j0, hb);
+        tma_atoms<1>(sk + C::KBytes, &mR, &kv_full[s], kFBand, p.T - kQT - i0 + j0, h);
+        if (++s == 3) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (n >= per_pass) {
+          const int u = n - per_pass;  // V of pass-2 step u, MN-major B of O += P V
+          mbar_wait(v_empty, (u & 1) ^ 1);
+          mbar_expect_tx(v_full, 8192);
+          tma_load_3d(sV, &mV, v_full, 0, j0, hb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t id_ac = umma_idesc(false, false, false, kQT, kFKT);
+      const uint32_t id_bd = umma_idesc(false, false, false, kQT, kFBand);
+      const uint32_t id_pv = umma_idesc(false, false, true, kQT, 64);
+      const uint32_t qa = smem_u32(sQu), qb = smem_u32(sQv), pa = smem_u32(sP), va = smem_u32(sV);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int u) {
+        mbar_wait(p_full, u & 1);
+        mbar_wait(v_full, u & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(t_o, umma_desc(pa + 32 * k, 16, 1024), umma_desc(va + k * 2048, 8192, 1024), id_pv,
+                        (u | k) != 0);
+        tc_commit(p_free);
+        tc_commit(v_empty);
+      };
+      int s = 0;
+      uint32_t ph = 0;
+      for (int n = 0; n < nsteps; ++n) {
+        const int buf = buf_of(n);
+        mbar_wait(&s_empty[buf], (use_of(n) & 1) ^ 1);
+        mbar_wait(&kv_full[s], ph);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(stages + s * C::StageBytes), rb = kb + C::KBytes;
+        const uint32_t d = tmem_base + buf * kFBuf;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(d, atom_desc<1>(qa, kQT, k), atom_desc<1>(kb, kFKT, k), id_ac, k > 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(d + kFKT, atom_desc<1>(qb, kQT, k), atom_desc<1>(rb, kFBand, k), id_bd, k > 0);
+        tc_commit(&kv_empty[s]);
+        tc_commit(&s_full[buf]);
+        if (++s == 3) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (n == per_pass && last_b1 >= 0) {
+          // O's columns were pass-1 buffer 1: drained by the softmax warps?
+          mbar_wait(&s_empty[1], use_of(last_b1) & 1);
+        }
+        if (n > per_pass) issue_pv(n - per_pass - 1);
+      }
+      issue_pv(per_pass - 1);
+      tc_commit(o_full);
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax: row r = 32 q + lane, key columns [32 half, +32) of each step ----------------
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const int i = i0 + r;
+    const bool row_ok = i < p.T;
+    const int jhi = p.M + i;
+    float* myring = ring + (warp - 4) * kRingWarp + lane * kRing;
+    const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    const int cb0 = 96 - 32 * q + 32 * half;
+    const int off = 31 - lane;
+    __nv_bfloat16* prow = p.p + ((int64_t)hb * p.T + i) * p.ldp;
+    uint8_t* prow_s = sP + r * 128;
+    const int rsw = r & 7;
+    float m = -INFINITY, l = 0.f, inv = 0.f;
+    for (int n = 0; n < nsteps; ++n) {
+      const bool pass2 = n >= per_pass;
+      if (n == per_pass) {
+        stats[(half * kQT + r) * 2] = m;
+        stats[(half * kQT + r) * 2 + 1] = l;
+        named_sync(1, kSoftWarps * 32);
+        const float mo = stats[((1 - half) * kQT + r) * 2], lo_ = stats[((1 - half) * kQT + r) * 2 + 1];
+        const float mm = fmaxf(m, mo);
+        const float ll = (m == -INFINITY ? 0.f : l * ex2(m - mm)) + (mo == -INFINITY ? 0.f : lo_ * ex2(mo - mm));
+        m = mm;
+        inv = ll > 0.f ? 1.f / ll : 0.f;
+        if (row_ok) {
+          const uint4 z = make_uint4(0, 0, 0, 0);
+          const int64_t a0 = half ? (int64_t)(jt_hi + 1) * kFKT : 0;
+          const int64_t a1 = half ? p.ldp : (int64_t)jt_lo * kFKT;
+          for (int64_t c = a0; c < a1; c += 8) *reinterpret_cast<uint4*>(prow + c) = z;
+        }
+      }
+      const int buf = buf_of(n);
+      const int jb = (jt_lo + n % per_pass) * kFKT + 32 * half;
+      mbar_wait(&s_full[buf], use_of(n) & 1);
+      tc_fence_after();
+      const uint32_t tb = tl + buf * kFBuf;
+      uint32_t v0[32], v1[32], a[32];
+      tmem_ld32_async(tb + kFKT + cb0, v0);
+      tmem_ld32_async(tb + kFKT + cb0 + 32, v1);
+      tmem_ld32_async(tb + 32 * half, a);
+      tmem_wait_ld(v0);
+      tmem_wait_ld(v1);
+      tmem_wait_ld(a);
+      tc_fence_before();
+      mbar_arrive(&s_empty[buf]);
+      stage_band(myring, 0, v0);
+      stage_band(myring, 1, v1);
+      __syncwarp();
+      float sv[32];
+      float cm = -INFINITY;
+      if (jb >= p.lo && jb + 31 <= p.M + i0 + 32 * q) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          sv[t] = (__uint_as_float(a[t]) + myring[off + t]) * p.c2;
+          cm = fmaxf(cm, sv[t]);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int j = jb + t;
+          const float x = (__uint_as_float(a[t]) + myring[off + t]) * p.c2;
+          sv[t] = (j >= p.lo && j <= jhi) ? x : -INFINITY;
+          cm = fmaxf(cm, sv[t]);
+        }
+      }
+      __syncwarp();
+      if (!pass2) {
+        const float mn = fmaxf(m, cm);
+        if (mn != -INFINITY) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int t = 0; t < 32; ++t) acc[t & 3] += ex2(sv[t] - mn);
+          l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          m = mn;
+        }
+      } else {
+        const int u = n - per_pass;
+        uint32_t w[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2(sv[2 * t] - m) * inv, ex2(sv[2 * t + 1] - m) * inv);
+          w[t] = row_ok ? *reinterpret_cast<uint32_t*>(&b2) : 0u;
+        }
+        // the P tile is free once O += P V of the previous step and this
+        // quarter's TMA store of it have read it
+        if (u >= 1) mbar_wait(p_free, (u - 1) & 1);
+        if (half == 0 && lane == 0) tma_store_wait_read();
+        named_sync(2 + q, 64);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(prow_s + (((4 * half + c) ^ rsw) << 4)) =
+              make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+        fence_proxy_async_smem();
+        mbar_arrive(p_full);
+        named_sync(2 + q, 64);
+        // this quarter's 32 rows x 64 keys of P (the map clips rows past T and columns past ldp)
+        const int j0 = jb - 32 * half;
+        if (half == 0 && lane == 0 && j0 < p.ldp && i0 + 32 * q < p.T)
+          tma_store_3d_p(&mP, sP + 32 * q * 128, j0, i0 + 32 * q, hb);
+      }
+    }
+    // ---- O = P V: rows of this lane quarter, head columns [32 half, +32) -> merged ctx
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    uint32_t o[32];
+    tmem_ld32(tl + 256 + 32 * half, o);
+    if (row_ok) {
+      uint4* dst = reinterpret_cast<uint4*>(pp.ctx + ((int64_t)b * p.T + i) * pp.d + h * 64 + 32 * half);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ww[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2 * e]), __uint_as_float(o[8 * c + 2 * e + 1]));
+          ww[e] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        dst[c] = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+      }
+    }
+    if (half == 0 && lane == 0) tma_store_wait_all();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+// ---------------------------------------------------------------------------
 // Backward with the query gradients fused (head dim 64, T % 128 == 0): the
 // kernel above, plus per key tile n
 //     dQu += dS_n K_n                   128 x 64    (TMEM cols 256..319)
@@ -1131,6 +1435,46 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   if (grid <= 0) return RP_OK;
   xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);
   return check_launch("xl_attn_bwd_dq");
+}
+
+int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,
+                   int64_t ldp, void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale,
+                   cudaStream_t st) {
+  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: head dim must be 64 (got %d)", dh);
+  const int64_t Kl = M + Tn, HB = (int64_t)H * B;
+  if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: ldp must be >= M+T, multiple of 8");
+  if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: mem_len out of range");
+  if (((reinterpret_cast<uintptr_t>(probs) | reinterpret_cast<uintptr_t>(ctx)) & 15) != 0)
+    return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: unaligned operand");
+  CUtensorMap mqu, mqv, mk, mr, mv, mp;
+  RP_TRY0(tma_map_bf16(&mqu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mqv, qv, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kFKT));
+  RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
+  RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kFKT));
+  RP_TRY0(tma_map_bf16(&mp, probs, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done))
+    cudaFuncSetAttribute(xl_attn_fwd_pv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdPvSmem);
+  FwdPvParams pp{};
+  FwdParams& p = pp.f;
+  p.p = static_cast<__nv_bfloat16*>(probs);
+  p.ldp = ldp;
+  p.B = (int)B;
+  p.T = (int)Tn;
+  p.M = (int)M;
+  p.Kl = (int)Kl;
+  p.lo = (int)(M - mem_len);
+  p.nqt = (int)((Tn + kQT - 1) / kQT);
+  p.heavy_first = xl_heavy_first();
+  p.c2 = scale * 1.4426950408889634f;
+  p.dbg = 0;
+  pp.ctx = static_cast<__nv_bfloat16*>(ctx);
+  pp.d = H * dh;
+  const int64_t grid = HB * p.nqt;
+  if (grid <= 0) return RP_OK;
+  xl_attn_fwd_pv_kernel<<<(unsigned)grid, kThreadsFwd, kFwdPvSmem, st>>>(mqu, mqv, mk, mr, mv, mp, pp);
+  return check_launch("xl_attn_fwd_pv");
 }
 
 }  // namespace rp

@@ -418,6 +418,23 @@ def xl_attn_bwd(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx, B, T, M, mem_len, sc
                                    _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_bwd")
 
 
+def xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ctx, B, T, M, mem_len, scale):
+    """xl_attn_fwd plus ctx = P v (dh = 64): qu / qv [H*B*T, dh], kh / vh
+    [H*B*(M+T), dh], rh [H, M+T, dh] head-major; probs [H*B, T, ldp]; ctx the
+    merged [B*T, H*dh] rows."""
+    _require_cuda(qu, qv, kh, vh, rh, probs, ctx)
+    for t in (qu, qv, kh, vh, rh, probs, ctx):
+        if t.dtype != torch.bfloat16:
+            raise DimensionError("xl_attn_fwd_pv takes bf16 tensors")
+    for t in (qu, qv, kh, vh, rh, ctx):
+        if not t.is_contiguous():
+            raise DimensionError("xl_attn_fwd_pv operands must be contiguous")
+    H, dh = rh.shape[0], rh.shape[-1]
+    _count(1)
+    N.check(N.lib().rp_xl_attn_fwd_pv(_ptr(qu), _ptr(qv), _ptr(kh), _ptr(vh), _ptr(rh), _ptr(probs), probs.stride(-2),
+                                      _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_fwd_pv")
+
+
 def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale):
     """xl_attn_bwd plus the query gradients on the tensor cores (dh = 64,
     T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh]."""

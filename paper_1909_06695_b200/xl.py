@@ -81,6 +81,9 @@ def _bg(*a, **k):
 
 
 FUSED = os.environ.get("RP_XL_FUSED", "1") != "0"
+# N tile of the dropout + residual epilogue GEMMs (out-projection, FFN out):
+# 0 = the library default (A/B switch)
+DROP_TILE = int(os.environ.get("RP_DROP_TILE", "0"))
 # N tile of the unfused score / dP GEMMs (N = M + T keys, K = head dim <= 64:
 # one k-block per tile, so the fp32 output epilogue dominates and 128-wide
 # tiles waste less of it than the default 256 -- C4 shape, tools/xl_score_tiles.py:
@@ -101,6 +104,12 @@ def fused_bwd_ok(tp):
 
 
 FUSED_DQ = os.environ.get("RP_XL_FUSED_DQ", "1") != "0"
+FUSED_PV = os.environ.get("RP_XL_FUSED_PV", "1") != "0"
+
+
+def fused_pv_ok(tp):
+    """The forward with P.V folded in (xl_attn_fwd_pv): head dim 64."""
+    return FUSED_PV and fused_ok(tp) and tp.dh == 64
 
 
 def fused_dq_ok(tp):
@@ -124,7 +133,14 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
     r = ws.get("xl_r", (Kl, d), cdt)
     _bg(R, W["wr"], b_mn=True, out=r)
     ops.xl_split_heads(r, tp.rh, H, dh)
-    if fused_ok(tp):
+    pv_done = False
+    if fused_pv_ok(tp):
+        # scores + relative shift + masked softmax + P.V in one tcgen05 kernel (csrc/xl_attn.cu)
+        with ops.span("xl_attn_fwd"):
+            ops.xl_attn_fwd_pv(tp.qu, tp.qv, tp.kh, tp.vh, tp.rh, tp.probs_buf, tp.ctx, B, T, M, tp.mem_len,
+                               1.0 / math.sqrt(dh))
+        pv_done = True
+    elif fused_ok(tp):
         # scores + relative shift + masked softmax in one tcgen05 kernel (csrc/xl_attn.cu)
         with ops.span("xl_attn_fwd"):
             ops.xl_attn_fwd(tp.qu, tp.qv, tp.kh, tp.rh, tp.probs_buf, B, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
@@ -135,15 +151,17 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
             ops.gemm(tp.qu.view(H * B, T, dh), tp.kh.view(H * B, Kl, dh), out=ac, tile_n=SCORE_TILE)
             ops.gemm(tp.qv, tp.rh, out=bd, tile_n=SCORE_TILE)
         ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
-    ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
-    ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
-    ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
+    if not pv_done:
+        ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
+        ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
+        ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
     d0 = None if drop is None else (drop[0], drop[1], drop[2], 0)
-    _bg(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0)
+    _bg(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0,
+        tile_n=DROP_TILE)
     ops.layernorm_fwd(tp.x1, vecs["ln2_g"], vecs["ln2_b"], tp.m, tp.mean2, tp.rstd2, flag)
     _bg(tp.m, W["w1"], b_mn=True, out=tp.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
     d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
-    _bg(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
+    _bg(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"], tile_n=DROP_TILE,
              residual=tp.x1, dropout=d1)
 
 

@@ -301,3 +301,33 @@ def test_fused_dq_backward_equals_fused_backward_plus_gemms(B, H, T, M, mem_len)
     want_qv = gbd2.view(H, B * T, ldp)[:, :, :Kl].float() @ rh.float()
     assert rel(gqu.view(H * B, T, dh).cpu(), want_qu.cpu()) <= 1e-5
     assert rel(gqv.cpu(), want_qv.cpu()) <= 1e-5
+
+
+@pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 3, 200, 72, 50), (2, 1, 64, 0, 0),
+                                             (1, 2, 256, 256, 100), (2, 8, 512, 512, 512), (1, 2, 100, 28, 28)])
+def test_fused_pv_forward_equals_fused_forward_plus_gemm(B, H, T, M, mem_len):
+    """xl_attn_fwd_pv: P bitwise equal to xl_attn_fwd's, and ctx = P v from the
+    in-kernel tcgen05 MMA (P tile kept in shared memory) against fp32 torch
+    products of the same bf16 P and v, merged to [B*T, H*dh] rows
+    (exact bf16 products, fp32 sums, one bf16 rounding: rel-L2 <= 4e-3)."""
+    from paper_1909_06695_b200 import ops
+
+    dev, dh = "cuda", 64
+    g = torch.Generator(device=dev).manual_seed(3 * T + M + mem_len)
+    Kl = M + T
+    ldp = _pad8(Kl)
+    mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
+    qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
+    kh, rh, vh = mk(H, B * Kl, dh), mk(H, Kl, dh), mk(H, B * Kl, dh)
+    scale = 1.0 / math.sqrt(dh)
+    p1 = torch.full((H * B, T, ldp), float("nan"), device=dev, dtype=torch.bfloat16)
+    p2 = torch.full((H * B, T, ldp), float("nan"), device=dev, dtype=torch.bfloat16)
+    ctx = torch.full((B * T, H * dh), float("nan"), device=dev, dtype=torch.bfloat16)
+    ops.xl_attn_fwd(qu, qv, kh, rh, p1, B, T, M, mem_len, scale)
+    ops.xl_attn_fwd_pv(qu, qv, kh, vh, rh, p2, ctx, B, T, M, mem_len, scale)
+    torch.cuda.synchronize()
+    assert torch.equal(p1, p2)
+    want_h = p2[:, :, :Kl].float() @ vh.view(H * B, Kl, dh).float()  # [HB, T, dh]
+    want = want_h.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh)
+    assert torch.isfinite(ctx.float()).all()
+    assert rel(ctx.float().cpu(), want.cpu()) <= 4e-3
