@@ -53,7 +53,8 @@ typedef enum rp_epilogue {
   RP_EPI_BIAS_DROPOUT_RESIDUAL = 2, /* C = resid + (alpha*AB+bias)*mask layers.py:184-187,192-195 */
   RP_EPI_LSE_PARTIAL = 3,           /* per-(row, N-tile, column half) (max, sumexp) + target logit  layers.py:310-316 */
   RP_EPI_CE_GRAD = 4,               /* C = (exp(AB - lse[row]) - onehot) * ce_scale    layers.py:317-319 */
-  RP_EPI_RELU_GRAD = 5              /* C = alpha*AB * (residual > 0)                   layers.py:221 */
+  RP_EPI_RELU_GRAD = 5,             /* C = alpha*AB * (residual > 0)                   layers.py:221 */
+  RP_EPI_GELU_GRAD = 6              /* C = alpha*AB * gelu'(residual), residual = the pre-activation z1 */
 } rp_epilogue;
 
 /* C[b] = epilogue(alpha * opA(A[b]) * opB(B[b])).
@@ -271,6 +272,9 @@ typedef struct rp_block_desc {
    * the block's own row offset r0 is folded into drop_seed by the caller:
    * seed + r0*d*0x9E3779B97F4A7C15 addresses positions r0*d + i (tensor.py:41-48). */
   int64_t drop_rows_total;
+  /* FFN activation: 0 = ReLU (the reference, layers.py:191), 1 = GELU (exact
+   * erf form, a production option): the tape then also keeps z1 */
+  int32_t activation;
 } rp_block_desc;
 
 typedef struct rp_block_weights {
@@ -286,6 +290,7 @@ typedef struct rp_block_weights {
 typedef struct rp_block_tape {
   void *a, *qkv, *probs, *ctx, *x1, *m, *h1; /* probs: [B, T, pad8(T)] */
   float *mean1, *rstd1, *mean2, *rstd2;
+  void* z1; /* [B*T, f] FFN pre-activation (GELU only; NULL for ReLU) */
 } rp_block_tape;
 
 typedef struct rp_block_grads {
@@ -338,6 +343,7 @@ typedef struct rp_module_desc {
   uint64_t drop_threshold;  /* ceil(p * 2^53) */
   float drop_scale;         /* 1 / (1 - p) */
   const uint64_t* layer_seeds; /* host array, one per layer of the slice: mix64(dropout_seed, step, layer) */
+  int32_t activation;       /* FFN activation of every block: 0 = ReLU, 1 = GELU (rp_block_desc) */
 } rp_module_desc;
 
 typedef struct rp_module_weights {
@@ -379,6 +385,11 @@ int rp_module_forward(const rp_module_desc* desc, const rp_module_weights* w, co
 int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, const rp_module_slot* slot,
                        const float* g_out, float* g_in, const rp_module_grads* grads, void* workspace,
                        int64_t workspace_bytes, void* stream);
+
+/* GELU (exact erf form): y = 0.5 z (1 + erf(z / sqrt 2)) over n elements of
+ * `dtype`, vectorised (the FFN activation option; its gradient is the GEMM
+ * epilogue RP_EPI_GELU_GRAD) */
+int rp_gelu_fwd(int32_t dtype, const void* z, void* y, int64_t n, void* stream);
 
 /* y += alpha * x over n fp32 elements (weight-gradient accumulation over the
  * row blocks of a micro-batched slot, in a fixed order) */

@@ -16,6 +16,7 @@ mask1 [n, 2n) with n = B*T*d (layers.py:184-195, 209-212).
 import math
 
 import numpy as np
+from scipy.special import erf as _erf
 
 from .rng import dropout_scale_mask
 
@@ -86,10 +87,20 @@ def embed_bwd(g, cache, vocab, pos_shape):
 BLOCK_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2")
 
 
-def block_fwd(P, x, seed, p, train, pos0=0, n_total=None):
+def gelu(z):
+    """Exact GELU 0.5 z (1 + erf(z / sqrt 2)) -- the FFN activation option
+    of the device path (the reference FFN is ReLU, layers.py:191)."""
+    return 0.5 * z * (1.0 + _erf(z / math.sqrt(2.0)))
+
+
+def gelu_grad(z):
+    return 0.5 * (1.0 + _erf(z / math.sqrt(2.0))) + z * np.exp(-0.5 * z * z) / math.sqrt(2.0 * math.pi)
+
+
+def block_fwd(P, x, seed, p, train, pos0=0, n_total=None, act="relu"):
     """pos0 / n_total: a row block of a larger batch -- mask0 draws
     [pos0, pos0 + n), mask1 [n_total + pos0, ...) with n_total = N*d of the
-    whole batch (layers.py:184-195)."""
+    whole batch (layers.py:184-195).  act: "relu" (the reference) or "gelu"."""
     B, T, d = x.shape
     n = B * T * d
     n1 = n if n_total is None else n_total
@@ -112,13 +123,14 @@ def block_fwd(P, x, seed, p, train, pos0=0, n_total=None):
     x1 = x + proj
     m, c2 = ln_fwd(x1, P["ln2_g"], P["ln2_b"])
     z1 = _rows(m) @ P["w1"] + P["b1"]
-    h1 = np.maximum(z1, 0.0)
+    h1 = gelu(z1) if act == "gelu" else np.maximum(z1, 0.0)
     h2 = (h1 @ P["w2"] + P["b2"]).reshape(B, T, d)
     m1 = dropout_scale_mask(seed, n1 + pos0, (B, T, d), p) if train else None
     if m1 is not None:
         h2 = h2 * m1
     out = x1 + h2
-    cache = dict(x=x, a=a, q=q, k=k, v=v, probs=probs, ctx=ctx, m=m, z1=z1, h1=h1, c1=c1, c2=c2, m0=m0, m1=m1)
+    cache = dict(x=x, a=a, q=q, k=k, v=v, probs=probs, ctx=ctx, m=m, z1=z1, h1=h1, c1=c1, c2=c2, m0=m0, m1=m1,
+                 act=act)
     return out, cache
 
 
@@ -129,7 +141,7 @@ def block_bwd(P, c, gout):
     gh2r = _rows(gh2)
     G["w2"] = c["h1"].T @ gh2r
     G["b2"] = gh2r.sum(axis=0)
-    gz1 = (gh2r @ P["w2"].T) * (c["z1"] > 0.0)
+    gz1 = (gh2r @ P["w2"].T) * (gelu_grad(c["z1"]) if c.get("act") == "gelu" else (c["z1"] > 0.0))
     G["w1"] = _rows(c["m"]).T @ gz1
     G["b1"] = gz1.sum(axis=0)
     gm = (gz1 @ P["w1"].T).reshape(B, T, d)

@@ -84,7 +84,7 @@ def rel_shift_back(gbd, T):
     return out
 
 
-def xl_block_fwd(P, x, mem, mem_len, H, seed, p, train):
+def xl_block_fwd(P, x, mem, mem_len, H, seed, p, train, act="relu"):
     B, T, d = x.shape
     M = mem.shape[1]
     dh = d // H
@@ -115,14 +115,14 @@ def xl_block_fwd(P, x, mem, mem_len, H, seed, p, train):
     x1 = x + proj
     m, c2 = L.ln_fwd(x1, P["ln2_g"], P["ln2_b"])
     z1 = m @ P["w1"] + P["b1"]
-    h1 = np.maximum(z1, 0.0)
+    h1 = L.gelu(z1) if act == "gelu" else np.maximum(z1, 0.0)
     h2 = h1 @ P["w2"] + P["b2"]
     m1 = L.dropout_scale_mask(seed, n, (B, T, d), p) if train else None
     if m1 is not None:
         h2 = h2 * m1
     out = x1 + h2
     cache = dict(M=M, H=H, R=R, a=a, qu=qu, qv=qv, kh=kh, vh=vh, rh=rh, probs=probs, ctx=ctx, m=m, z1=z1, h1=h1,
-                 c1=c1, c2=c2, m0=m0, m1=m1)
+                 c1=c1, c2=c2, m0=m0, m1=m1, act=act)
     return out, cache
 
 
@@ -135,7 +135,7 @@ def xl_block_bwd(P, c, gout):
     gh2 = gout * c["m1"] if c["m1"] is not None else gout
     G["w2"] = np.einsum("btf,btd->fd", c["h1"], gh2)
     G["b2"] = gh2.sum(axis=(0, 1))
-    gz1 = (gh2 @ P["w2"].T) * (c["z1"] > 0.0)
+    gz1 = (gh2 @ P["w2"].T) * (L.gelu_grad(c["z1"]) if c.get("act") == "gelu" else (c["z1"] > 0.0))
     G["w1"] = np.einsum("btd,btf->df", c["m"], gz1)
     G["b1"] = gz1.sum(axis=(0, 1))
     gm = gz1 @ P["w1"].T

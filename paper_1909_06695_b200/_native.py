@@ -16,7 +16,8 @@ _lib = None
 # rp_dtype / rp_math / rp_epilogue (include/ringpipe_b200.h)
 F32, BF16 = 0, 1
 MATH_BF16, MATH_TF32, MATH_TF32X3 = 0, 1, 2
-EPI_STORE, EPI_BIAS_RELU, EPI_BIAS_DROPOUT_RESIDUAL, EPI_LSE_PARTIAL, EPI_CE_GRAD, EPI_RELU_GRAD = range(6)
+EPI_STORE, EPI_BIAS_RELU, EPI_BIAS_DROPOUT_RESIDUAL, EPI_LSE_PARTIAL, EPI_CE_GRAD, EPI_RELU_GRAD, EPI_GELU_GRAD = range(7)
+ACT_RELU, ACT_GELU = 0, 1
 FLAG_NONFINITE, FLAG_DIMENSION = 1, 2
 
 
@@ -67,7 +68,7 @@ class BlockDesc(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("d", ctypes.c_int64), ("f", ctypes.c_int64),
                 ("dtype", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_seed", ctypes.c_uint64),
                 ("drop_threshold", ctypes.c_uint64), ("drop_scale", ctypes.c_float), ("max_ctas", ctypes.c_int32),
-                ("drop_rows_total", ctypes.c_int64)]
+                ("drop_rows_total", ctypes.c_int64), ("activation", ctypes.c_int32)]
 
 
 class BlockWeights(ctypes.Structure):
@@ -77,7 +78,7 @@ class BlockWeights(ctypes.Structure):
 
 class BlockTape(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("a", "qkv", "probs", "ctx", "x1", "m", "h1", "mean1", "rstd1",
-                                                 "mean2", "rstd2")]
+                                                 "mean2", "rstd2", "z1")]
 
 
 class BlockGrads(ctypes.Structure):
@@ -95,7 +96,8 @@ class ModuleDesc(ctypes.Structure):
                 ("vocab", ctypes.c_int64), ("t_max", ctypes.c_int64), ("n_blocks", ctypes.c_int32),
                 ("has_embedding", ctypes.c_int32), ("has_projection", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_threshold", ctypes.c_uint64),
-                ("drop_scale", ctypes.c_float), ("layer_seeds", ctypes.POINTER(ctypes.c_uint64))]
+                ("drop_scale", ctypes.c_float), ("layer_seeds", ctypes.POINTER(ctypes.c_uint64)),
+                ("activation", ctypes.c_int32)]
 
 
 class ModuleWeights(ctypes.Structure):
@@ -194,6 +196,7 @@ def _declare(L):
         "rp_head_forward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, vp, i64, vp, vp],
         "rp_head_backward": [ctypes.POINTER(HeadDesc), vp, vp, vp, vp, vp, vp, f32, i32, vp, i64, vp],
         "rp_axpy": [vp, vp, f32, i64, vp],
+        "rp_gelu_fwd": [i32, vp, vp, i64, vp],
         "rp_nccl_unique_id": [vp],
         "rp_ctx_create": [i32, vp, i32, i32, ctypes.POINTER(vp)],
         "rp_ctx_destroy": [vp],

@@ -136,6 +136,9 @@ int rp_embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi
                           int32_t convention, void* stream) {
   return rp::embedding_gradient(t, K, vo, vi, out, n, convention, RP_S(stream));
 }
+int rp_gelu_fwd(int32_t dtype, const void* z, void* y, int64_t n, void* stream) {
+  return rp::gelu_fwd(dtype, z, y, n, RP_S(stream));
+}
 int rp_axpy(float* y, const float* x, float alpha, int64_t n, void* stream) {
   return rp::axpy(y, x, alpha, n, RP_S(stream));
 }

@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(384, 1)
       if (!head_fast) {
       // residual / aux: TMA bulk-loads one 32x32 tile per warp, one chunk
       // ahead (coalesced), else per-row loads prefetched one chunk ahead
-      const bool uses_aux = p.epi == RP_EPI_RELU_GRAD || (p.epi == RP_EPI_BIAS_DROPOUT_RESIDUAL && p.resid);
+      const bool uses_aux = p.epi == RP_EPI_RELU_GRAD || p.epi == RP_EPI_GELU_GRAD ||
+                            (p.epi == RP_EPI_BIAS_DROPOUT_RESIDUAL && p.resid);
       const bool tma_aux = uses_aux && p.tma_resid;
       const bool aux = !tma_aux && uses_aux && p.out_bf16 && p.resid_vec;
       const int trow0 = (int)((int64_t)b * p.M + mrow0 + q * 32);
@@ -731,6 +732,23 @@ __global__ void __launch_bounds__(384, 1)
               load_chunk(p, m, n0, b, rr);
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = rr[j] > 0.f ? v[j] * p.alpha : 0.f;
+            RP_EMIT();
+            break;
+          }
+          case RP_EPI_GELU_GRAD: {
+            // out = acc * gelu'(z1), gelu'(z) = Phi(z) + z phi(z), aux = the pre-activation z1
+            float rr[32];
+            if (cur_ok)
+              unpack_raw_bf16(cur, rr);
+            else
+              load_chunk(p, m, n0, b, rr);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float z = rr[j];
+              const float cdf = 0.5f * (1.f + erff(z * 0.70710678118654752f));
+              const float pdf = 0.39894228040143268f * __expf(-0.5f * z * z);
+              v[j] = v[j] * p.alpha * fmaf(z, pdf, cdf);
+            }
             RP_EMIT();
             break;
           }
@@ -984,7 +1002,8 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   {
     auto enc = encoder();
     const int64_t rows_r = a.M * batch;
-    const bool uses = a.residual && (a.epilogue == RP_EPI_RELU_GRAD || a.epilogue == RP_EPI_BIAS_DROPOUT_RESIDUAL);
+    const bool uses = a.residual && (a.epilogue == RP_EPI_RELU_GRAD || a.epilogue == RP_EPI_GELU_GRAD ||
+                                     a.epilogue == RP_EPI_BIAS_DROPOUT_RESIDUAL);
     const bool packed = batch == 1 || (a.stride_residual == a.M * a.ld_residual && a.M % Cfg::BM == 0);
     if (enc && uses && a.out_dtype == RP_BF16 && ks == 1 && packed &&
         (reinterpret_cast<uintptr_t>(a.residual) & 15) == 0 && (a.ld_residual * 2) % 16 == 0 && a.N >= 32 &&

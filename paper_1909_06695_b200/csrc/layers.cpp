@@ -289,9 +289,17 @@ int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void*
   RP_TRY(mm(c, mat(tp.ctx, N, D, D), false, mat(w.wo, D, D, D), true, mat(tp.x1, N, D, D), dt, e0));
   RP_TRY(layernorm_fwd(dt, tp.x1, w.ln2_g, w.ln2_b, tp.m, tp.mean2, tp.rstd2, N, D, flag, st));
   Epi e1;
-  e1.kind = RP_EPI_BIAS_RELU;
   e1.bias = w.b1;
-  RP_TRY(mm(c, mat(tp.m, N, D, D), false, mat(w.w1, D, F, F), true, mat(tp.h1, N, F, F), dt, e1));
+  if (d.activation == 1) {
+    // GELU: z1 = m w1 + b1 kept for the backward, h1 = gelu(z1) by the vector kernel
+    if (!tp.z1) return set_error(RP_ERR_INVALID, "block_forward: GELU needs tape.z1");
+    e1.kind = RP_EPI_BIAS_DROPOUT_RESIDUAL;  // bias only: no residual, no dropout
+    RP_TRY(mm(c, mat(tp.m, N, D, D), false, mat(w.w1, D, F, F), true, mat(tp.z1, N, F, F), dt, e1));
+    RP_TRY(gelu_fwd(dt, tp.z1, tp.h1, N * F, st));
+  } else {
+    e1.kind = RP_EPI_BIAS_RELU;
+    RP_TRY(mm(c, mat(tp.m, N, D, D), false, mat(w.w1, D, F, F), true, mat(tp.h1, N, F, F), dt, e1));
+  }
   Epi e2 = e0;
   e2.bias = w.b2;
   e2.resid = tp.x1;
@@ -376,9 +384,10 @@ int block_backward(const rp_block_desc& d, const rp_block_weights& w, const void
                    d.drop_scale,
                    d.drop_enabled, part_b2, st));
   Epi er;
-  er.kind = RP_EPI_RELU_GRAD;
-  er.resid = tp.h1;
+  er.kind = d.activation == 1 ? RP_EPI_GELU_GRAD : RP_EPI_RELU_GRAD;
+  er.resid = d.activation == 1 ? tp.z1 : tp.h1;
   er.ld_resid = F;
+  if (d.activation == 1 && !tp.z1) return set_error(RP_ERR_INVALID, "block_backward: GELU needs tape.z1");
   RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er); },
               [&](Ctx& x) { return mm(x, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32); }));
   // b1 partial sums ride with dW1 on the side stream (both only read g_z1)

@@ -29,6 +29,7 @@ rp_block_desc block_desc(const rp_module_desc& m, int layer) {
   d.drop_seed = m.drop_enabled ? m.layer_seeds[layer] : 0;
   d.drop_threshold = m.drop_threshold;
   d.drop_scale = m.drop_scale;
+  d.activation = m.activation;
   return d;
 }
 

@@ -90,6 +90,7 @@ int embedding_gradient(int64_t t, int64_t K, const float* vo, const float* vi, f
                        int convention, cudaStream_t st);
 int cast(const void* in, int in_dtype, void* out, int out_dtype, int64_t n, cudaStream_t st);
 int axpy(float* y, const float* x, float alpha, int64_t n, cudaStream_t st);
+int gelu_fwd(int dtype, const void* z, void* y, int64_t n, cudaStream_t st);
 int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
 
 int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, void* qu, void* qv, void* kh, void* vh,

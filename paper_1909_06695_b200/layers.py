@@ -82,9 +82,10 @@ class Workspace:
 class BlockTape:
     """Forward intermediates of one block for one stale slot (store-all)."""
 
-    def __init__(self, B, T, d, f, dtype, device):
+    def __init__(self, B, T, d, f, dtype, device, activation="relu"):
         N = B * T
         Tp = _pad8(T)
+        self.activation = activation
         e = lambda *s: torch.empty(s, dtype=dtype, device=device)  # noqa: E731
         f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
         self.a = e(N, d)
@@ -95,12 +96,36 @@ class BlockTape:
         self.x1 = e(N, d)
         self.m = e(N, d)
         self.h1 = e(N, f)
+        self.z1 = e(N, f) if activation == "gelu" else None  # the GELU pre-activation (its gradient needs it)
         self.mean1, self.rstd1, self.mean2, self.rstd2 = f32(N), f32(N), f32(N), f32(N)
 
     def nbytes(self):
         return sum(t.numel() * t.element_size() for t in
-                   (self.a, self.qkv, self.probs_buf, self.ctx, self.x1, self.m, self.h1,
-                    self.mean1, self.rstd1, self.mean2, self.rstd2))
+                   (self.a, self.qkv, self.probs_buf, self.ctx, self.x1, self.m, self.h1, self.z1,
+                    self.mean1, self.rstd1, self.mean2, self.rstd2) if t is not None)
+
+
+ACTIVATIONS = ("relu", "gelu")
+
+
+def ffn_up(W, vecs, m, tape, probe=None):
+    """h1 = act(m w1 + b1) into tape.h1: ReLU fused in the GEMM epilogue
+    (reference layers.py:190-191); GELU as z1 = m w1 + b1 (kept for the
+    backward) and the vector GELU kernel."""
+    if getattr(tape, "activation", "relu") == "gelu":
+        ops.gemm(m, W["w1"], b_mn=True, out=tape.z1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b1"],
+                 probe=probe)
+        ops.gelu(tape.z1, tape.h1)
+    else:
+        ops.gemm(m, W["w1"], b_mn=True, out=tape.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"], probe=probe)
+
+
+def ffn_act_grad(g_h2, W, tape, g_z1, probe=None):
+    """g_z1 = (g_h2 w2^T) * act'(z1) (reference layers.py:221 for ReLU)."""
+    if getattr(tape, "activation", "relu") == "gelu":
+        ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_GELU_GRAD, residual=tape.z1, probe=probe)
+    else:
+        ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tape.h1, probe=probe)
 
 
 # ---------------------------------------------------------------------------
@@ -140,7 +165,7 @@ def block_forward_ops(W, vecs, x, out, tape, B, T, drop, ws, flag):
              residual=x, dropout=d0)
     ops.layernorm_fwd(tape.x1, vecs["ln2_g"], vecs["ln2_b"], tape.m, tape.mean2, tape.rstd2, flag)
     with ops.span("ffn1_gemm"):
-        ops.gemm(tape.m, W["w1"], b_mn=True, out=tape.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+        ffn_up(W, vecs, tape.m, tape)
     d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
     ops.gemm(tape.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"],
              residual=tape.x1, dropout=d1)
@@ -164,7 +189,7 @@ def block_backward_ops(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws):
     ops.colsum_finish(pm, nbm, G["b2"])
     ops.gemm(tape.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
     g_z1 = ws.get("g_z1", (Nt, f), cdt)
-    ops.gemm(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tape.h1)
+    ffn_act_grad(g_h2, W, tape, g_z1)
     ops.colsum_partial(g_z1, part[:, :f])
     ops.colsum_finish(part[:, :f], nbc, G["b1"])
     ops.gemm(tape.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
@@ -263,9 +288,10 @@ def _p(t):
 CTA_BUDGET = {"value": 0}
 
 
-def _block_desc(x, f, B, T, drop, rows_total=0):
+def _block_desc(x, f, B, T, drop, rows_total=0, activation="relu"):
     dsc = N.BlockDesc()
     dsc.drop_rows_total = rows_total or 0
+    dsc.activation = N.ACT_GELU if activation == "gelu" else N.ACT_RELU
     dsc.max_ctas = CTA_BUDGET["value"]
     dsc.B, dsc.T, dsc.d, dsc.f = B, T, x.shape[-1], f
     dsc.dtype = N.BF16 if x.dtype == torch.bfloat16 else N.F32
@@ -285,6 +311,7 @@ def _tape(tp):
     t = N.BlockTape()
     t.a, t.qkv, t.probs, t.ctx = _p(tp.a), _p(tp.qkv), _p(tp.probs_buf), _p(tp.ctx)
     t.x1, t.m, t.h1 = _p(tp.x1), _p(tp.m), _p(tp.h1)
+    t.z1 = _p(getattr(tp, "z1", None))
     t.mean1, t.rstd1, t.mean2, t.rstd2 = _p(tp.mean1), _p(tp.rstd1), _p(tp.mean2), _p(tp.rstd2)
     return t
 
@@ -298,10 +325,10 @@ def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag, rows_total=0):
     """rows_total: token rows of the whole batch when this is one row block of
     it (micro-batched relay; the caller shifts `drop` to the block's rows)."""
     f = tape.h1.shape[-1]
-    dsc = _block_desc(x, f, B, T, drop, rows_total)
+    dsc = _block_desc(x, f, B, T, drop, rows_total, getattr(tape, "activation", "relu"))
     nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
     buf = _ws_bytes(ws, "block_ws", nbytes)
-    ops._count(12)
+    ops._count(13 if getattr(tape, "activation", "relu") == "gelu" else 12)
     N.check(N.lib().rp_block_forward(ctypes.byref(dsc), ctypes.byref(_weights(W)), _p(x), _p(out),
                                      ctypes.byref(_tape(tape)), _p(buf), nbytes, _p(flag), ops._stream()),
             "block_forward")
@@ -309,7 +336,7 @@ def block_forward(W, vecs, x, out, tape, B, T, drop, ws, flag, rows_total=0):
 
 def block_backward(W, vecs, x, tape, g_out, g_x, G, B, T, drop, ws, rows_total=0):
     f = tape.h1.shape[-1]
-    dsc = _block_desc(x, f, B, T, drop, rows_total)
+    dsc = _block_desc(x, f, B, T, drop, rows_total, getattr(tape, "activation", "relu"))
     nbytes = N.lib().rp_block_workspace_bytes(ctypes.byref(dsc))
     buf = _ws_bytes(ws, "block_ws", nbytes)
     g = N.BlockGrads()

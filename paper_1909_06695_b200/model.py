@@ -52,8 +52,13 @@ class EmbeddingLayer:
 class TransformerBlockLayer:
     kind = "block"
 
-    def __init__(self, model_dim, ffn_dim, dropout_p):
+    def __init__(self, model_dim, ffn_dim, dropout_p, activation="relu"):
+        """activation: the FFN nonlinearity -- "relu" (the reference,
+        layers.py:191) or "gelu" (exact erf form, a production option)."""
+        if activation not in LY.ACTIVATIONS:
+            raise ValueError(f"unknown activation {activation!r}")
         self.model_dim, self.ffn_dim, self.dropout_p = model_dim, ffn_dim, dropout_p
+        self.activation = activation
 
     def specs(self):
         d, f = self.model_dim, self.ffn_dim
@@ -74,11 +79,14 @@ class TransformerXLBlockLayer:
     KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "wr", "r_w_bias", "r_r_bias", "ln2_g", "ln2_b", "w1", "b1",
             "w2", "b2")
 
-    def __init__(self, model_dim, ffn_dim, dropout_p, n_heads, mem_len):
+    def __init__(self, model_dim, ffn_dim, dropout_p, n_heads, mem_len, activation="relu"):
         if model_dim % n_heads:
             raise DimensionError("model_dim must be a multiple of n_heads")
+        if activation not in LY.ACTIVATIONS:
+            raise ValueError(f"unknown activation {activation!r}")
         self.model_dim, self.ffn_dim, self.dropout_p = model_dim, ffn_dim, dropout_p
         self.n_heads, self.mem_len = n_heads, mem_len
+        self.activation = activation
 
     def specs(self):
         d, f, H = self.model_dim, self.ffn_dim, self.n_heads
@@ -277,7 +285,7 @@ def stack_of(layers):
 
 
 def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, *, dtype="bf16",
-                device=None):
+                device=None, activation="relu"):
     """Same draw order and scales as the reference (model.py:53-60,
     layers.py:107-112, 149-166): V ~ U(+-1/sqrt(d)) first, then per layer the
     position table and wq, wk, wv, wo, w1 (1/sqrt(d)) and w2 (1/sqrt(f));
@@ -287,7 +295,7 @@ def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, in
     rt = Runtime.get(device)
     cdt = _dtype_of(dtype)
     layers = [EmbeddingLayer(vocab_size, model_dim, seq_len, dropout_p)]
-    layers += [TransformerBlockLayer(model_dim, ffn_dim, dropout_p) for _ in range(n_blocks)]
+    layers += [TransformerBlockLayer(model_dim, ffn_dim, dropout_p, activation) for _ in range(n_blocks)]
     layers.append(OutputProjectionLayer(vocab_size, model_dim))
     storage = [LayerParams(layer, rt.device, cdt) for layer in layers]
     tied = TiedMatrix(vocab_size, model_dim, rt.device, cdt)
@@ -298,7 +306,7 @@ def build_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, in
 
 
 def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p, init_seed, n_heads, mem_len, *,
-                   dtype="bf16", device=None, cutoffs=None):
+                   dtype="bf16", device=None, cutoffs=None, activation="relu"):
     """The Transformer-XL language model: the reference embedding and tied
     head around `n_blocks` XL blocks with `mem_len` memory rows each."""
     if model_dim % 8 or ffn_dim % 8 or (model_dim // n_heads) % 8:
@@ -308,7 +316,8 @@ def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p,
     rt = Runtime.get(device)
     cdt = _dtype_of(dtype)
     layers = [EmbeddingLayer(vocab_size, model_dim, seq_len, dropout_p)]
-    layers += [TransformerXLBlockLayer(model_dim, ffn_dim, dropout_p, n_heads, mem_len) for _ in range(n_blocks)]
+    layers += [TransformerXLBlockLayer(model_dim, ffn_dim, dropout_p, n_heads, mem_len, activation)
+               for _ in range(n_blocks)]
     layers.append(OutputProjectionLayer(vocab_size, model_dim, cutoffs))
     storage = [LayerParams(layer, rt.device, cdt) for layer in layers]
     tied = TiedMatrix(vocab_size, model_dim, rt.device, cdt)
@@ -469,7 +478,7 @@ def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
                 LY.embed_backward(g_out, tokens, layer.max_seq_len, st.G["pos"], tied.grad, 1.0, ws, drop)
         elif layer.kind == "block":
             if tape is None:
-                tape = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev)
+                tape = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev, layer.activation)
 
             def run():
                 LY.block_forward(W, W, act, out, tape, B, T, drop, ws, rt.flag)
@@ -477,7 +486,7 @@ def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
         elif layer.kind == "xl_block":
             # a full memory (the steady state): attention over M + T keys
             if xtape is None:
-                xtape = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev)
+                xtape = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev, layer.activation)
                 xtape.xa.zero_()
                 xtape.mem_len = layer.mem_len
                 R = sinusoid(xtape.Kl, d, cdt, dev)
@@ -548,10 +557,10 @@ class _Arena:
         for off in module.block_idx:
             layer = module.layers[off]
             if layer.kind == "xl_block":
-                tp = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev)
+                tp = XLTape(B, T, layer.mem_len, d, layer.ffn_dim, layer.n_heads, cdt, dev, layer.activation)
                 self.acts.append(tp.x)  # the upstream writes straight into [memory; x]
             else:
-                tp = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev)
+                tp = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev, layer.activation)
                 self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
             self.tapes.append(tp)
         if module.has_projection:

@@ -36,6 +36,10 @@ def describe(module, B, T, seeds, train, max_ctas=0):
     dsc.has_embedding, dsc.has_projection = int(module.has_embedding), int(module.has_projection)
     dsc.dtype = N.BF16 if module.cdtype == torch.bfloat16 else N.F32
     dsc.max_ctas = max_ctas
+    acts = {module.layers[off].activation for off in module.block_idx}
+    if len(acts) > 1:
+        raise ValueError("the module-level C ABI takes one FFN activation per module")
+    dsc.activation = N.ACT_GELU if acts == {"gelu"} else N.ACT_RELU
     p = module.dropout_p
     if train and p > 0.0:
         dsc.drop_enabled, dsc.drop_threshold, dsc.drop_scale = 1, keep_threshold(p), 1.0 / (1.0 - p)

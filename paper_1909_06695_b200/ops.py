@@ -458,6 +458,15 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
                                       mem_len, scale, _stream()), "xl_attn_bwd_dq")
 
 
+def gelu(z, y):
+    """y = GELU(z) = 0.5 z (1 + erf(z / sqrt 2)) (same dtype and size)."""
+    _require_cuda(z, y)
+    if z.dtype != y.dtype or z.numel() != y.numel() or not (z.is_contiguous() and y.is_contiguous()):
+        raise DimensionError("gelu takes two contiguous tensors of one dtype and size")
+    _count(1)
+    N.check(N.lib().rp_gelu_fwd(_dtc(z), _ptr(z), _ptr(y), z.numel(), _stream()), "gelu")
+
+
 def axpy(y, x, alpha=1.0):
     """y += alpha * x (fp32, same element count)."""
     _require_cuda(y, x)

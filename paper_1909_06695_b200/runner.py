@@ -67,7 +67,7 @@ STRUCTURAL_FIELDS = (
     "ffn_dim", "dropout_p", "k", "mode", "tied_grad", "stale_weights",
     "balance", "optimizer", "lr", "lr_mode", "warmup_steps", "steps",
     "adam_beta1", "adam_beta2", "adam_eps", "seed_init", "seed_data",
-    "seed_dropout", "n_heads", "mem_len", "adaptive_cutoffs",
+    "seed_dropout", "n_heads", "mem_len", "adaptive_cutoffs", "activation",
 )
 
 
@@ -101,11 +101,11 @@ def build_runtime(cfg, synthetic_cost=None, device=None):
         source = SegmentStream(tokens, cfg.seq_len, cfg.batch_size)
         stack = build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
                                cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=cfg.dtype, device=device,
-                               cutoffs=cfg.cutoffs)
+                               cutoffs=cfg.cutoffs, activation=cfg.activation)
     else:
         source = BatchSource(tokens, cfg.seq_len, cfg.batch_size, cfg.seed_data)
         stack = build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
-                            cfg.seed_init, dtype=cfg.dtype, device=device)
+                            cfg.seed_init, dtype=cfg.dtype, device=device, activation=cfg.activation)
     costs = None
     if cfg.balance == "by_cost":
         costs = measure_layer_costs(stack, source.batch_at(0).x, cfg.seed_dropout)
@@ -400,9 +400,10 @@ def _load_masters(stack, snap):
 def _twin_stack(cfg, vocab, dtype=None):
     if cfg.n_heads:
         return build_xl_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p,
-                              cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=dtype or cfg.dtype, cutoffs=cfg.cutoffs)
+                              cfg.seed_init, cfg.n_heads, cfg.mem_len, dtype=dtype or cfg.dtype, cutoffs=cfg.cutoffs,
+                              activation=cfg.activation)
     return build_stack(vocab, cfg.model_dim, cfg.ffn_dim, cfg.n_blocks, cfg.seq_len, cfg.dropout_p, cfg.seed_init,
-                       dtype=dtype or cfg.dtype)
+                       dtype=dtype or cfg.dtype, activation=cfg.activation)
 
 
 def _sequential_loss(stack, x, y, dropout_seed, step):

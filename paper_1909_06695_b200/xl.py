@@ -22,6 +22,7 @@ import torch
 
 from . import _native as N
 from . import ops
+from . import layers as LY
 from .layers import _pad8
 
 
@@ -38,8 +39,9 @@ def sinusoid(Kl, d, dtype, device):
 class XLTape:
     """Store-all intermediates of one XL block for one stale slot."""
 
-    def __init__(self, B, T, M, d, f, H, dtype, device):
+    def __init__(self, B, T, M, d, f, H, dtype, device, activation="relu"):
         Kl = M + T
+        self.activation = activation
         dh = d // H
         ldk = _pad8(Kl)
         e = lambda *s: torch.empty(s, dtype=dtype, device=device)  # noqa: E731
@@ -58,6 +60,7 @@ class XLTape:
         self.x1 = e(B * T, d)
         self.m = e(B * T, d)
         self.h1 = e(B * T, f)
+        self.z1 = e(B * T, f) if activation == "gelu" else None
         self.mean2, self.rstd2 = f32(B * T), f32(B * T)
         self.mem_len = 0
 
@@ -159,7 +162,7 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
     _bg(tp.ctx, W["wo"], b_mn=True, out=tp.x1, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, residual=tp.x, dropout=d0,
         tile_n=DROP_TILE)
     ops.layernorm_fwd(tp.x1, vecs["ln2_g"], vecs["ln2_b"], tp.m, tp.mean2, tp.rstd2, flag)
-    _bg(tp.m, W["w1"], b_mn=True, out=tp.h1, epilogue=N.EPI_BIAS_RELU, bias=vecs["b1"])
+    LY.ffn_up(W, vecs, tp.m, tp, probe="block_gemm")
     d1 = None if drop is None else (drop[0], drop[1], drop[2], n)
     _bg(tp.h1, W["w2"], b_mn=True, out=out, epilogue=N.EPI_BIAS_DROPOUT_RESIDUAL, bias=vecs["b2"], tile_n=DROP_TILE,
              residual=tp.x1, dropout=d1)
@@ -184,7 +187,7 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     ops.mask_grad(g_out, g_h2, n, drop, pm)
     _bg(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
     g_z1 = ws.get("g_z1", (Nt, f), cdt)
-    _bg(g_h2, W["w2"], out=g_z1, epilogue=N.EPI_RELU_GRAD, residual=tp.h1)
+    LY.ffn_act_grad(g_h2, W, tp, g_z1, probe="block_gemm")
     ops.colsum_partial(g_z1, part[:, :f])
     _bg(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
     g_m = ws.get("g_m", (Nt, d), torch.float32)

@@ -113,3 +113,56 @@ def test_native_head_equals_ops_and_oracle(dtype):
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
     assert rel(res[0][1].double().cpu().numpy(), rgh[0]) < (1e-2 if dtype == "bf16" else 2e-5)
     assert rel(res[0][2].double().cpu().numpy(), 0.5 * rgv) < (1e-2 if dtype == "bf16" else 2e-5)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_gelu_block_native_equals_ops_and_oracle(dtype):
+    """The GELU FFN option (north_star's memory-bound GELU kernel + the
+    GELU-gradient GEMM epilogue): the native composite is bitwise the op
+    sequence, and both match the fp64 block with the exact erf GELU
+    (fp32: <= 2e-6 forward, <= 2e-5 gradients; bf16 <= 1e-2 / 3e-2)."""
+    LY, W, x, (W64, V64, x64), B, T, d, f, cdt = _setup(dtype, B=2, T=20, d=32, f=64, seed=5)
+    seed, p = 7654321, 0.15
+    drop = LY.Dropout.make(seed, p, True)
+    outs = []
+    for fwd, bwd in ((LY.block_forward, LY.block_backward), (LY.block_forward_ops, LY.block_backward_ops)):
+        ws = LY.Workspace(x.device)
+        tape = LY.BlockTape(B, T, d, f, cdt, x.device, activation="gelu")
+        out = torch.empty_like(x)
+        fwd(W, W, x, out, tape, B, T, drop, ws, None)
+        g_out = torch.linspace(-1, 1, x.numel(), device=x.device).view_as(x).float()
+        g_x = torch.empty_like(g_out)
+        G = {k: torch.empty(v.shape, dtype=torch.float32, device=x.device) for k, v in W.items()}
+        bwd(W, W, x, tape, g_out, g_x, G, B, T, drop, ws)
+        torch.cuda.synchronize()
+        outs.append((out.clone(), g_x.clone(), {k: v.clone() for k, v in G.items()}, g_out))
+    a, b = outs
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for k in a[2]:
+        assert torch.equal(a[2][k], b[2][k]), k
+    P = {k: v.numpy() for k, v in V64.items()}
+    w = W64["wqkv"].to(cdt).double().numpy()
+    P.update(wq=w[:, :d], wk=w[:, d:2 * d], wv=w[:, 2 * d:], wo=W64["wo"].to(cdt).double().numpy(),
+             w1=W64["w1"].to(cdt).double().numpy(), w2=W64["w2"].to(cdt).double().numpy())
+    xo = x.double().cpu().numpy().reshape(B, T, d)
+    ro, c = OL.block_fwd(P, xo, seed, p, True, act="gelu")
+    rgx, RG = OL.block_bwd(P, c, a[3].double().cpu().numpy().reshape(B, T, d))
+    rel = lambda u, v: np.linalg.norm(u - v) / max(np.linalg.norm(v), 1e-30)  # noqa: E731
+    tf, tg = (2e-6, 2e-5) if dtype == "fp32" else (1e-2, 3e-2)
+    assert rel(a[0].double().cpu().numpy().reshape(B, T, d), ro) < tf
+    assert rel(a[1].double().cpu().numpy().reshape(B, T, d), rgx) < tg
+    for name in ("wo", "w1", "w2", "b1", "b2", "ln1_g", "ln1_b", "ln2_g", "ln2_b"):
+        assert rel(a[2][name].double().cpu().numpy(), RG[name]) < tg, name
+
+
+def test_gelu_kernel_matches_torch():
+    from paper_1909_06695_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(2)
+    for dt, n, tol in ((torch.bfloat16, 3 * 4096 + 5, 8e-3), (torch.float32, 10001, 1e-6)):
+        z = (torch.randn(n, device="cuda", generator=g) * 3).to(dt)
+        y = torch.empty_like(z)
+        ops.gelu(z, y)
+        want = torch.nn.functional.gelu(z.double())
+        err = float((y.double() - want).abs().max() / want.abs().max())
+        assert err <= tol, (dt, err)

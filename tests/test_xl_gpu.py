@@ -157,3 +157,48 @@ def test_by_cost_times_xl_blocks_and_the_adaptive_head():
     assert max(blocks) <= 2.0 * min(blocks)
     part = MD.partition(stack.num_layers, 3, "by_cost", costs)
     assert sum(hi - lo for lo, hi in part.groups) == stack.num_layers
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_xl_block_gelu_matches_restatement(dtype):
+    """XL block with the GELU FFN option vs the fp64 restatement."""
+    from paper_1909_06695_b200 import layers as LY
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import xl as XD
+
+    B, T, M, H, d, f = 2, 128, 128, 2, 128, 256
+    stack = MD.build_xl_stack(40, d, f, 1, T, 0.2, 3, H, M, dtype=dtype, activation="gelu")
+    st = stack.storage[1]
+    st.configure_ring(1)
+    st.ensure(0)
+    W = st.weights(0)
+    P = {k: host(v) for k, v in st._public(W).items()}
+    rs = Stream(17)
+    x = rs.uniform_signed((B, T, d), 1.0)
+    mem = rs.uniform_signed((B, M, d), 1.0)
+    gout = rs.uniform_signed((B, T, d), 1.0)
+    cdt = stack.cdtype
+    x = torch.from_numpy(x).to(cdt).double().numpy()
+    mem = torch.from_numpy(mem).to(cdt).double().numpy()
+    dev = stack.runtime.device
+    tp = XD.XLTape(B, T, M, d, f, H, cdt, dev, activation="gelu")
+    tp.mem.copy_(torch.from_numpy(mem.reshape(B * M, d)))
+    tp.x.copy_(torch.from_numpy(x.reshape(B * T, d)))
+    tp.mem_len = M
+    R = XD.sinusoid(M + T, d, cdt, dev)
+    ws = LY.Workspace(dev)
+    drop = LY.Dropout.make(1234, 0.2, True)
+    out = torch.empty(B * T, d, device=dev, dtype=cdt)
+    XD.xl_block_forward(W, W, out, tp, R, drop, ws, stack.runtime.flag)
+    g = torch.from_numpy(gout.reshape(B * T, d)).float().to(dev)
+    gx = torch.empty_like(g)
+    XD.xl_block_backward(W, W, tp, R, g, gx, st.G, drop, ws)
+    torch.cuda.synchronize()
+    ref, cache = X.xl_block_fwd(P, x, mem, M, H, 1234, 0.2, True, act="gelu")
+    rgx, RG = X.xl_block_bwd(P, cache, gout)
+    tf, tg = (2e-5, 1e-4) if dtype == "fp32" else (1e-2, 3e-2)
+    assert rel(host(out).reshape(B, T, d), ref) <= tf
+    assert rel(host(gx).reshape(B, T, d), rgx) <= tg
+    grads = {k: host(v) for k, v in st.grads.items()}
+    for k, want in RG.items():
+        assert rel(grads[k], want) <= tg, (k, rel(grads[k], want))
