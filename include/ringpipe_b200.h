@@ -333,6 +333,48 @@ int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, 
  * slot's device storage.  The host keeps the schedule bookkeeping (rings,
  * slot queue, boundary hand-off), exactly as the reference keeps it in
  * ModuleState / PipelineEngine. */
+/* ---- Transformer-XL block composite (paper_1909_06695_b200/xl.py; restated in
+ * oracle/xl.py -- the reference has no XL path): relative-position multi-head
+ * attention over [memory; segment] inside the reference's pre-LN block, the
+ * same kernels in the same order as the Python host loop (bitwise equal).
+ * The host fills tape.xa = [memory rows; current rows] before the forward
+ * (the memory is the previous segment's layer input, stop-gradient). */
+#define RP_XL_FUSED_FWD 1 /* rp_xl_attn_fwd (bf16, dh 64 / 128) */
+#define RP_XL_FUSED_BWD 2 /* rp_xl_attn_bwd (bf16, dh 64 / 128, T % 8 == 0) */
+#define RP_XL_FUSED_PV 4  /* rp_xl_attn_fwd_pv (bf16, dh 64) */
+#define RP_XL_FUSED_DQ 8  /* rp_xl_attn_bwd_dq (bf16, dh 64, T % 128 == 0) */
+typedef struct rp_xl_block_desc {
+  int64_t B, T, M, d, f;
+  int32_t H, dtype;
+  int32_t drop_enabled, activation, max_ctas;
+  int32_t mem_len;    /* valid memory rows (M - mem_len leading keys are masked) */
+  uint64_t drop_seed, drop_threshold;
+  float drop_scale;
+  int64_t drop_rows_total;
+  int64_t ldk;        /* row pitch of the probabilities: pad8(M + T) */
+  int32_t fused;      /* RP_XL_FUSED_* (0: the unfused GEMM + softmax path, also the fp32 check mode) */
+  int32_t score_tile; /* N tile of the unfused score GEMMs (0: default) */
+} rp_xl_block_desc;
+typedef struct rp_xl_block_weights {
+  const void *wqkv, *wo, *w1, *w2, *wr; /* matrices (dtype); wr [d, d] projects the sinusoid R */
+  const float *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2, *r_w_bias, *r_r_bias; /* u, v: [H, dh] */
+} rp_xl_block_weights;
+typedef struct rp_xl_block_tape {
+  void *xa, *a, *qkv, *qu, *qv, *kh, *vh, *rh, *probs, *ctx, *x1, *m, *h1, *z1;
+  float *mean1, *rstd1, *mean2, *rstd2;
+} rp_xl_block_tape;
+typedef struct rp_xl_block_grads {
+  float *wqkv, *wo, *w1, *w2, *wr, *ln1_g, *ln1_b, *ln2_g, *ln2_b, *b1, *b2, *r_w_bias, *r_r_bias;
+} rp_xl_block_grads;
+int64_t rp_xl_block_workspace_bytes(const rp_xl_block_desc* desc);
+/* R: the sinusoid relative encodings [M+T, d] (dtype); out: [B*T, d] */
+int rp_xl_block_forward(const rp_xl_block_desc* desc, const rp_xl_block_weights* w, const void* R, void* out,
+                        const rp_xl_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                        void* stream);
+int rp_xl_block_backward(const rp_xl_block_desc* desc, const rp_xl_block_weights* w, const void* R,
+                         const rp_xl_block_tape* tape, const float* g_out, float* g_x, const rp_xl_block_grads* grads,
+                         void* workspace, int64_t workspace_bytes, void* stream);
+
 typedef struct rp_module_desc {
   int64_t B, T, d, f, vocab;
   int64_t t_max;            /* rows of the embedding position table */
@@ -344,12 +386,21 @@ typedef struct rp_module_desc {
   float drop_scale;         /* 1 / (1 - p) */
   const uint64_t* layer_seeds; /* host array, one per layer of the slice: mix64(dropout_seed, step, layer) */
   int32_t activation;       /* FFN activation of every block: 0 = ReLU, 1 = GELU (rp_block_desc) */
+  /* Transformer-XL modules (n_heads > 0): every block is an XL block with M
+   * memory rows, mem_len of them valid; xl_fused / score_tile as in
+   * rp_xl_block_desc.  The host keeps the memory: it writes each block's
+   * memory rows into its tape's xa before the forward. */
+  int32_t n_heads, mem_len;
+  int64_t M;
+  int32_t xl_fused, score_tile;
 } rp_module_desc;
 
 typedef struct rp_module_weights {
   const rp_block_weights* blocks; /* host array [n_blocks] */
   const void* tied;               /* compute copy of the tied matrix [vocab, d] */
   const void* pos;                /* embedding position table [t_max, d] (dtype) */
+  const rp_xl_block_weights* xl_blocks; /* host array [n_blocks] (XL modules) */
+  const void* R;                  /* sinusoid relative encodings [M+T, d] (XL modules) */
 } rp_module_weights;
 
 /* one stale slot (model.py:162-168): acts[j] = input of block j (acts[0] is
@@ -363,6 +414,7 @@ typedef struct rp_module_slot {
   float* lse;                  /* [B*T] head log-sum-exp (projection) */
   float* loss;                 /* 0-d mean cross entropy (projection) */
   double* loss64;
+  const rp_xl_block_tape* xl_tapes; /* host array [n_blocks] (XL modules; acts[j] = the current rows of xa) */
 } rp_module_slot;
 
 typedef struct rp_module_grads {
@@ -372,6 +424,7 @@ typedef struct rp_module_grads {
   float tied_alpha;             /* output half: tied (+)= alpha * dV_out (skipped when 0) */
   float tied_beta;              /* input half:  tied  += beta * dV_in   (skipped when 0) */
   int32_t tied_accumulate;      /* 1: add the output half onto tied; 0: overwrite */
+  const rp_xl_block_grads* xl_blocks; /* host array [n_blocks] (XL modules) */
 } rp_module_grads;
 
 int64_t rp_module_workspace_bytes(const rp_module_desc* desc);

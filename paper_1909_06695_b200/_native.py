@@ -97,22 +97,58 @@ class ModuleDesc(ctypes.Structure):
                 ("has_embedding", ctypes.c_int32), ("has_projection", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("max_ctas", ctypes.c_int32), ("drop_enabled", ctypes.c_int32), ("drop_threshold", ctypes.c_uint64),
                 ("drop_scale", ctypes.c_float), ("layer_seeds", ctypes.POINTER(ctypes.c_uint64)),
-                ("activation", ctypes.c_int32)]
+                ("activation", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("mem_len", ctypes.c_int32),
+                ("M", ctypes.c_int64), ("xl_fused", ctypes.c_int32), ("score_tile", ctypes.c_int32)]
+
+
+XL_FUSED_FWD, XL_FUSED_BWD, XL_FUSED_PV, XL_FUSED_DQ = 1, 2, 4, 8
+
+
+class XlBlockDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("M", ctypes.c_int64), ("d", ctypes.c_int64),
+                ("f", ctypes.c_int64), ("H", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("drop_enabled", ctypes.c_int32), ("activation", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
+                ("mem_len", ctypes.c_int32), ("drop_seed", ctypes.c_uint64), ("drop_threshold", ctypes.c_uint64),
+                ("drop_scale", ctypes.c_float), ("drop_rows_total", ctypes.c_int64), ("ldk", ctypes.c_int64),
+                ("fused", ctypes.c_int32), ("score_tile", ctypes.c_int32)]
+
+
+XL_W_MATS = ("wqkv", "wo", "w1", "w2", "wr")
+XL_W_VECS = ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "b1", "b2", "r_w_bias", "r_r_bias")
+
+
+class XlBlockWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in XL_W_MATS + XL_W_VECS]
+
+
+XL_TAPE = ("xa", "a", "qkv", "qu", "qv", "kh", "vh", "rh", "probs", "ctx", "x1", "m", "h1", "z1", "mean1", "rstd1",
+           "mean2", "rstd2")
+
+
+class XlBlockTape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in XL_TAPE]
+
+
+class XlBlockGrads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("wqkv", "wo", "w1", "w2", "wr", "ln1_g", "ln1_b", "ln2_g", "ln2_b",
+                                                 "b1", "b2", "r_w_bias", "r_r_bias")]
 
 
 class ModuleWeights(ctypes.Structure):
-    _fields_ = [("blocks", ctypes.POINTER(BlockWeights)), ("tied", ctypes.c_void_p), ("pos", ctypes.c_void_p)]
+    _fields_ = [("blocks", ctypes.POINTER(BlockWeights)), ("tied", ctypes.c_void_p), ("pos", ctypes.c_void_p),
+                ("xl_blocks", ctypes.POINTER(XlBlockWeights)), ("R", ctypes.c_void_p)]
 
 
 class ModuleSlot(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_void_p), ("targets", ctypes.c_void_p), ("acts", ctypes.POINTER(ctypes.c_void_p)),
                 ("tapes", ctypes.POINTER(BlockTape)), ("lse", ctypes.c_void_p), ("loss", ctypes.c_void_p),
-                ("loss64", ctypes.c_void_p)]
+                ("loss64", ctypes.c_void_p), ("xl_tapes", ctypes.POINTER(XlBlockTape))]
 
 
 class ModuleGrads(ctypes.Structure):
     _fields_ = [("blocks", ctypes.POINTER(BlockGrads)), ("pos", ctypes.c_void_p), ("tied", ctypes.c_void_p),
-                ("tied_alpha", ctypes.c_float), ("tied_beta", ctypes.c_float), ("tied_accumulate", ctypes.c_int32)]
+                ("tied_alpha", ctypes.c_float), ("tied_beta", ctypes.c_float), ("tied_accumulate", ctypes.c_int32),
+                ("xl_blocks", ctypes.POINTER(XlBlockGrads))]
 
 
 def lib():
@@ -187,6 +223,11 @@ def _declare(L):
                               vp, vp, i64, vp, vp],
         "rp_module_backward": [ctypes.POINTER(ModuleDesc), ctypes.POINTER(ModuleWeights),
                                ctypes.POINTER(ModuleSlot), vp, vp, ctypes.POINTER(ModuleGrads), vp, i64, vp],
+        "rp_xl_block_workspace_bytes": [ctypes.POINTER(XlBlockDesc)],
+        "rp_xl_block_forward": [ctypes.POINTER(XlBlockDesc), ctypes.POINTER(XlBlockWeights), vp, vp,
+                                ctypes.POINTER(XlBlockTape), vp, i64, vp, vp],
+        "rp_xl_block_backward": [ctypes.POINTER(XlBlockDesc), ctypes.POINTER(XlBlockWeights), vp,
+                                 ctypes.POINTER(XlBlockTape), vp, vp, ctypes.POINTER(XlBlockGrads), vp, i64, vp],
         "rp_block_workspace_bytes": [ctypes.POINTER(BlockDesc)],
         "rp_block_forward": [ctypes.POINTER(BlockDesc), ctypes.POINTER(BlockWeights), vp, vp,
                              ctypes.POINTER(BlockTape), vp, i64, vp, vp],
@@ -218,6 +259,7 @@ def _declare(L):
     L.rp_embed_bwd_workspace_bytes.restype = i64
     L.rp_xl_bias_grad_workspace_bytes.restype = i64
     L.rp_block_workspace_bytes.restype = i64
+    L.rp_xl_block_workspace_bytes.restype = i64
     L.rp_module_workspace_bytes.restype = i64
     L.rp_head_workspace_bytes.restype = i64
     L.rp_state_bytes.restype = i64

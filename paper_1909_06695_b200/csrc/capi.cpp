@@ -225,6 +225,17 @@ int rp_module_backward(const rp_module_desc* desc, const rp_module_weights* w, c
                        int64_t workspace_bytes, void* stream) {
   return rp::module_backward(*desc, *w, *slot, g_out, g_in, *grads, workspace, workspace_bytes, RP_S(stream));
 }
+int64_t rp_xl_block_workspace_bytes(const rp_xl_block_desc* desc) { return rp::xl_block_workspace_bytes(*desc); }
+int rp_xl_block_forward(const rp_xl_block_desc* desc, const rp_xl_block_weights* w, const void* R, void* out,
+                        const rp_xl_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,
+                        void* stream) {
+  return rp::xl_block_forward(*desc, *w, R, out, *tape, workspace, workspace_bytes, flag, RP_S(stream));
+}
+int rp_xl_block_backward(const rp_xl_block_desc* desc, const rp_xl_block_weights* w, const void* R,
+                         const rp_xl_block_tape* tape, const float* g_out, float* g_x, const rp_xl_block_grads* grads,
+                         void* workspace, int64_t workspace_bytes, void* stream) {
+  return rp::xl_block_backward(*desc, *w, R, *tape, g_out, g_x, *grads, workspace, workspace_bytes, RP_S(stream));
+}
 int64_t rp_block_workspace_bytes(const rp_block_desc* desc) { return rp::block_workspace_bytes(*desc); }
 int rp_block_forward(const rp_block_desc* desc, const rp_block_weights* w, const void* x, void* out,
                      const rp_block_tape* tape, void* workspace, int64_t workspace_bytes, int32_t* flag,

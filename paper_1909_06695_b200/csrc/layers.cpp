@@ -94,6 +94,7 @@ struct Epi {
   float* partial = nullptr;
   float* target_logit = nullptr;
   float ce_scale = 0.f;
+  int tile_n = 0;  // N tile override (0: the library default)
 };
 
 int split_into(Ctx& c, Bump& b, const Mat& m, const void** hi, const void** lo, int64_t* ld, int64_t* bs) {
@@ -175,6 +176,7 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.partial = e.partial;
   g.target_logit = e.target_logit;
   g.ce_scale = e.ce_scale;
+  g.tile_n = e.tile_n;
   RP_TRY0(gemm(g, c.st));
   if (splits > 1) return splitk_reduce(c.splitk, splits, g.M, g.N, static_cast<float*>(const_cast<void*>(C.p)), C.ld,
                                        c.st);
@@ -493,6 +495,262 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
     RP_TRY(mm(c, mat(dz, N, V, Vp), true, mat(x, N, D, D), true, mat(vo, V, D, D), RP_F32, ev));
   }
   return RP_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Transformer-XL block (the same op sequence as paper_1909_06695_b200/xl.py,
+// so results are bitwise identical; the restatement is oracle/xl.py)
+
+namespace {
+
+struct XlDims {
+  int64_t B, T, M, Kl, D, F, H, dh, N, HB, ldk;
+};
+
+XlDims xl_dims(const rp_xl_block_desc& d) {
+  XlDims x;
+  x.B = d.B;
+  x.T = d.T;
+  x.M = d.M;
+  x.Kl = d.M + d.T;
+  x.D = d.d;
+  x.F = d.f;
+  x.H = d.H;
+  x.dh = d.d / d.H;
+  x.N = d.B * d.T;
+  x.HB = d.H * d.B;
+  x.ldk = d.ldk;
+  return x;
+}
+
+int check_xl(const rp_xl_block_desc& d) {
+  if (d.H <= 0 || d.d % d.H || d.B <= 0 || d.T <= 0 || d.M < 0 || d.mem_len < 0 || d.mem_len > d.M)
+    return set_error(RP_ERR_DIMENSION, "xl_block: bad shape");
+  if (d.ldk < d.M + d.T || d.ldk % 8) return set_error(RP_ERR_DIMENSION, "xl_block: ldk must be pad8(M+T)");
+  if (d.dtype != RP_BF16 && (d.fused & 15)) return set_error(RP_ERR_INVALID, "xl_block: fused kernels are bf16 only");
+  return RP_OK;
+}
+
+}  // namespace
+
+int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
+  const XlDims x = xl_dims(d);
+  const int64_t e = esize(d.dtype);
+  const int64_t nbc = colsum_blocks(x.N), nbm = mask_grad_blocks(x.N, x.D);
+  const int64_t nbl = ln_bwd_blocks(x.N) + (x.M ? ln_bwd_blocks(x.B * x.M) : 0);
+  int64_t b = 0;
+  // forward: r, ctx_h, ac, bd (unfused scores)
+  const int64_t fwd = al256(x.Kl * x.D * e) + al256(x.HB * x.T * x.dh * e) + 2 * al256(x.HB * x.T * x.ldk * 4);
+  // backward
+  int64_t bwd = al256(std::max(nbc, nbm) * std::max(x.F, 3 * x.D) * 4) + al256(nbm * x.D * 4);
+  bwd += al256(x.N * x.D * e) * 3;          // g_h2, g_proj, g_ctx
+  bwd += al256(x.N * x.F * e);              // g_z1
+  bwd += al256(x.N * x.D * 4) * 2;          // g_m, g_x1
+  bwd += al256(nbl * x.D * 4) * 2 + al256(ln_bwd_blocks(x.N) * x.D * 4) * 2;  // LN partials
+  bwd += al256(x.H * x.N * x.dh * e);       // g_ctx_h
+  bwd += 2 * al256(x.HB * x.T * x.ldk * e); // g_ac, g_bd
+  bwd += al256(x.HB * x.T * x.ldk * 4);     // g_p (unfused)
+  bwd += 2 * al256(x.H * x.N * x.dh * 4);   // g_qu, g_qv
+  bwd += 2 * al256(x.HB * x.Kl * x.dh * 4) + al256(x.H * x.Kl * x.dh * 4);  // g_vh, g_kh, g_rh
+  bwd += al256(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh));
+  bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
+  bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
+  bwd += al256(kBlockSplitK);
+  b = std::max(fwd, bwd);
+  b += split_bytes(d.dtype, std::max({x.HB * x.T * x.ldk, x.B * x.Kl * 3 * x.D, x.N * x.F, x.D * x.F}));
+  return b + 4096;
+}
+
+int xl_block_forward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, const void* R, void* out,
+                     const rp_xl_block_tape& tp, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st) {
+  RP_TRY(check_xl(d));
+  if (ws_bytes < xl_block_workspace_bytes(d)) return set_error(RP_ERR_INVALID, "xl_block workspace too small");
+  const XlDims x = xl_dims(d);
+  const int dt = d.dtype, e = esize(dt);
+  const float scale = 1.f / std::sqrt(static_cast<float>(x.dh));
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  void* r = bp.take(x.Kl * x.D * e);
+  void* ctx_h = bp.take(x.HB * x.T * x.dh * e);
+  float* ac = static_cast<float*>(bp.take(x.HB * x.T * x.ldk * 4));
+  float* bd = static_cast<float*>(bp.take(x.HB * x.T * x.ldk * 4));
+  Ctx c{dt, st};
+  c.max_ctas = d.max_ctas;
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  const int64_t BK = x.B * x.Kl;
+  RP_TRY(layernorm_fwd(dt, tp.xa, w.ln1_g, w.ln1_b, tp.a, tp.mean1, tp.rstd1, BK, x.D, flag, st));
+  RP_TRY(mm(c, mat(tp.a, BK, x.D, x.D), false, mat(w.wqkv, x.D, 3 * x.D, 3 * x.D), true,
+            mat(tp.qkv, BK, 3 * x.D, 3 * x.D), dt));
+  RP_TRY(xl_split_qkv(dt, tp.qkv, w.r_w_bias, w.r_r_bias, tp.qu, tp.qv, tp.kh, tp.vh, x.B, x.T, x.M, (int)x.H,
+                      (int)x.dh, st));
+  RP_TRY(mm(c, mat(R, x.Kl, x.D, x.D), false, mat(w.wr, x.D, x.D, x.D), true, mat(r, x.Kl, x.D, x.D), dt));
+  RP_TRY(xl_split_heads(dt, r, x.D, dt, tp.rh, x.Kl, (int)x.H, (int)x.dh, st));
+  bool pv_done = false;
+  if (d.fused & RP_XL_FUSED_PV) {
+    RP_TRY(xl_attn_fwd_pv(tp.qu, tp.qv, tp.kh, tp.vh, tp.rh, tp.probs, x.ldk, tp.ctx, x.B, x.T, x.M, (int)x.H,
+                          (int)x.dh, d.mem_len, scale, st));
+    pv_done = true;
+  } else if (d.fused & RP_XL_FUSED_FWD) {
+    RP_TRY(xl_attn_fwd(tp.qu, tp.qv, tp.kh, tp.rh, tp.probs, x.ldk, x.B, x.T, x.M, (int)x.H, (int)x.dh, d.mem_len,
+                       scale, st));
+  } else {
+    Epi es;
+    es.tile_n = d.score_tile;
+    RP_TRY(mm(c, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), false, bmat(tp.kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh),
+              false, bmat(ac, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), RP_F32, es));
+    RP_TRY(mm(c, bmat(tp.qv, x.H, x.N, x.dh, x.dh, x.N * x.dh), false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh),
+              false, bmat(bd, x.H, x.N, x.Kl, x.ldk, x.N * x.ldk), RP_F32, es));
+    RP_TRY(xl_softmax_fwd(dt, ac, bd, x.ldk, tp.probs, x.ldk, x.HB * x.T, x.T, x.M, d.mem_len, scale, st));
+  }
+  if (!pv_done) {
+    RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), false,
+              bmat(tp.vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), true, bmat(ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh),
+              dt));
+    RP_TRY(xl_merge_heads(dt, ctx_h, dt, tp.ctx, x.D, x.N, (int)x.H, (int)x.dh, st));
+  }
+  const int64_t n = (d.drop_rows_total > 0 ? d.drop_rows_total : x.N) * x.D;
+  const void* xcur = static_cast<const char*>(tp.xa) + x.B * x.M * x.D * e;
+  Epi e0;
+  e0.kind = RP_EPI_BIAS_DROPOUT_RESIDUAL;
+  e0.resid = xcur;
+  e0.ld_resid = x.D;
+  e0.drop = d.drop_enabled;
+  e0.seed = d.drop_seed;
+  e0.thr = d.drop_threshold;
+  e0.scale = d.drop_scale;
+  e0.pos0 = 0;
+  RP_TRY(mm(c, mat(tp.ctx, x.N, x.D, x.D), false, mat(w.wo, x.D, x.D, x.D), true, mat(tp.x1, x.N, x.D, x.D), dt, e0));
+  RP_TRY(layernorm_fwd(dt, tp.x1, w.ln2_g, w.ln2_b, tp.m, tp.mean2, tp.rstd2, x.N, x.D, flag, st));
+  Epi e1;
+  e1.bias = w.b1;
+  if (d.activation == 1) {
+    if (!tp.z1) return set_error(RP_ERR_INVALID, "xl_block_forward: GELU needs tape.z1");
+    e1.kind = RP_EPI_BIAS_DROPOUT_RESIDUAL;
+    RP_TRY(mm(c, mat(tp.m, x.N, x.D, x.D), false, mat(w.w1, x.D, x.F, x.F), true, mat(tp.z1, x.N, x.F, x.F), dt, e1));
+    RP_TRY(gelu_fwd(dt, tp.z1, tp.h1, x.N * x.F, st));
+  } else {
+    e1.kind = RP_EPI_BIAS_RELU;
+    RP_TRY(mm(c, mat(tp.m, x.N, x.D, x.D), false, mat(w.w1, x.D, x.F, x.F), true, mat(tp.h1, x.N, x.F, x.F), dt, e1));
+  }
+  Epi e2 = e0;
+  e2.bias = w.b2;
+  e2.resid = tp.x1;
+  e2.pos0 = static_cast<uint64_t>(n);
+  return mm(c, mat(tp.h1, x.N, x.F, x.F), false, mat(w.w2, x.F, x.D, x.D), true, mat(out, x.N, x.D, x.D), dt, e2);
+}
+
+int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, const void* R,
+                      const rp_xl_block_tape& tp, const float* g_out, float* g_x, const rp_xl_block_grads& G,
+                      void* ws, int64_t ws_bytes, cudaStream_t st) {
+  RP_TRY(check_xl(d));
+  if (ws_bytes < xl_block_workspace_bytes(d)) return set_error(RP_ERR_INVALID, "xl_block workspace too small");
+  const XlDims x = xl_dims(d);
+  const int dt = d.dtype, e = esize(dt);
+  const float scale = 1.f / std::sqrt(static_cast<float>(x.dh));
+  const int64_t N = x.N, D = x.D, F = x.F, BM = x.B * x.M, BK = x.B * x.Kl;
+  const int64_t n = (d.drop_rows_total > 0 ? d.drop_rows_total : N) * D;
+  const int nbc = colsum_blocks(N), nbm = mask_grad_blocks(N, D);
+  const int nbl_cur = ln_bwd_blocks(N), nbl_mem = x.M ? ln_bwd_blocks(BM) : 0;
+  Bump bp{static_cast<char*>(ws), ws_bytes};
+  float* part = static_cast<float*>(bp.take((int64_t)std::max(nbc, nbm) * std::max(F, 3 * D) * 4));
+  float* pm = static_cast<float*>(bp.take((int64_t)nbm * D * 4));
+  void* g_h2 = bp.take(N * D * e);
+  void* g_proj = bp.take(N * D * e);
+  void* g_ctx = bp.take(N * D * e);
+  void* g_z1 = bp.take(N * F * e);
+  float* g_m = static_cast<float*>(bp.take(N * D * 4));
+  float* g_x1 = static_cast<float*>(bp.take(N * D * 4));
+  float* pg = static_cast<float*>(bp.take((int64_t)(nbl_cur + nbl_mem) * D * 4));
+  float* pb = static_cast<float*>(bp.take((int64_t)(nbl_cur + nbl_mem) * D * 4));
+  float* pg2 = static_cast<float*>(bp.take((int64_t)nbl_cur * D * 4));
+  float* pb2 = static_cast<float*>(bp.take((int64_t)nbl_cur * D * 4));
+  void* g_ctx_h = bp.take(x.H * N * x.dh * e);
+  void* g_ac = bp.take(x.HB * x.T * x.ldk * e);
+  void* g_bd = bp.take(x.HB * x.T * x.ldk * e);
+  float* g_p = static_cast<float*>(bp.take(x.HB * x.T * x.ldk * 4));
+  float* g_qu = static_cast<float*>(bp.take(x.H * N * x.dh * 4));
+  float* g_qv = static_cast<float*>(bp.take(x.H * N * x.dh * 4));
+  float* g_vh = static_cast<float*>(bp.take(x.HB * x.Kl * x.dh * 4));
+  float* g_kh = static_cast<float*>(bp.take(x.HB * x.Kl * x.dh * 4));
+  float* g_rh = static_cast<float*>(bp.take(x.H * x.Kl * x.dh * 4));
+  float* bias_ws = static_cast<float*>(bp.take(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh)));
+  void* g_r = bp.take(x.Kl * D * e);
+  void* g_qkv = bp.take(BK * 3 * D * e);
+  float* g_a = static_cast<float*>(bp.take(BK * D * 4));
+  float* g_mem = static_cast<float*>(bp.take(BM * D * 4 + 4));
+  Ctx c{dt, st};
+  c.max_ctas = d.max_ctas;
+  c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
+  c.splitk_cap = kBlockSplitK;
+  c.split_base = bp.base + bp.off;
+  c.split_cap = ws_bytes - bp.off;
+  const int64_t ld_part = std::max(F, 3 * D);
+  // feed-forward + LN2 (as the reference block)
+  RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(n), d.drop_threshold, d.drop_scale,
+                   d.drop_enabled, pm, st));
+  RP_TRY(mm(c, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32));
+  Epi er;
+  er.kind = d.activation == 1 ? RP_EPI_GELU_GRAD : RP_EPI_RELU_GRAD;
+  er.resid = d.activation == 1 ? tp.z1 : tp.h1;
+  er.ld_resid = F;
+  RP_TRY(mm(c, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er));
+  RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, st));
+  (void)ld_part;
+  RP_TRY(mm(c, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32));
+  RP_TRY(mm(c, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32));
+  RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
+                       d.drop_threshold, d.drop_scale, d.drop_enabled, pg2, pb2, N, D, st));
+  // relative-position attention
+  RP_TRY(mm(c, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32));
+  RP_TRY(mm(c, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt));
+  RP_TRY(xl_split_heads(dt, g_ctx, D, dt, g_ctx_h, N, (int)x.H, (int)x.dh, st));
+  bool dq_done = false;
+  if (d.fused & RP_XL_FUSED_DQ) {
+    RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, g_qu, g_qv, x.B,
+                          x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st));
+    dq_done = true;
+  } else if (d.fused & RP_XL_FUSED_BWD) {
+    RP_TRY(xl_attn_bwd(g_ctx_h, tp.vh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, x.B, x.T, x.M, (int)x.H, (int)x.dh,
+                       d.mem_len, scale, st));
+  } else {
+    Epi es;
+    es.tile_n = d.score_tile;
+    RP_TRY(mm(c, bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh), false,
+              bmat(tp.vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), false, bmat(g_p, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk),
+              RP_F32, es));
+    RP_TRY(xl_softmax_bwd(dt, g_p, x.ldk, tp.probs, x.ldk, g_ac, g_bd, x.HB * x.T, x.T, x.M, d.mem_len, scale, st));
+  }
+  RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true, bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh),
+            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+  const Mat gac = bmat(g_ac, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk);
+  const Mat gbd = bmat(g_bd, x.H, N, x.Kl, x.ldk, N * x.ldk);
+  if (!dq_done)
+    RP_TRY(mm(c, gac, false, bmat(tp.kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
+              bmat(g_qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), RP_F32));
+  RP_TRY(mm(c, gac, true, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true,
+            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+  if (!dq_done)
+    RP_TRY(mm(c, gbd, false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
+              bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));
+  RP_TRY(mm(c, gbd, true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh), true, bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh),
+            RP_F32));
+  RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
+  RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
+  RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
+  RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));
+  RP_TRY(mm(c, mat(tp.a, BK, D, D), true, mat(g_qkv, BK, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32));
+  RP_TRY(mm(c, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32));
+  // LN1 over both row blocks: memory rows add to the gain / bias sums only
+  if (x.M)
+    RP_TRY(layernorm_bwd(dt, g_a, tp.xa, tp.mean1, tp.rstd1, w.ln1_g, nullptr, g_mem, nullptr, 0, 0, 1.f, 0,
+                         pg + (int64_t)nbl_cur * D, pb + (int64_t)nbl_cur * D, BM, D, st));
+  RP_TRY(layernorm_bwd(dt, g_a + BM * D, static_cast<const char*>(tp.xa) + BM * D * e, tp.mean1 + BM, tp.rstd1 + BM,
+                       w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
+  const ColsumJob jobs[6] = {{pm, nbm, D, G.b2}, {part, nbc, F, G.b1}, {pg2, nbl_cur, D, G.ln2_g},
+                             {pb2, nbl_cur, D, G.ln2_b}, {pg, nbl_cur + nbl_mem, D, G.ln1_g},
+                             {pb, nbl_cur + nbl_mem, D, G.ln1_b}};
+  return colsum_finish_multi(jobs, 6, st);
 }
 
 }  // namespace rp

@@ -33,11 +33,34 @@ rp_block_desc block_desc(const rp_module_desc& m, int layer) {
   return d;
 }
 
+rp_xl_block_desc xl_desc(const rp_module_desc& m, int layer) {
+  rp_xl_block_desc d{};
+  d.B = m.B;
+  d.T = m.T;
+  d.M = m.M;
+  d.d = m.d;
+  d.f = m.f;
+  d.H = m.n_heads;
+  d.dtype = m.dtype;
+  d.drop_enabled = m.drop_enabled;
+  d.activation = m.activation;
+  d.max_ctas = m.max_ctas;
+  d.mem_len = m.mem_len;
+  d.drop_seed = m.drop_enabled ? m.layer_seeds[layer] : 0;
+  d.drop_threshold = m.drop_threshold;
+  d.drop_scale = m.drop_scale;
+  d.ldk = (m.M + m.T + 7) / 8 * 8;
+  d.fused = m.xl_fused;
+  d.score_tile = m.score_tile;
+  return d;
+}
+
 rp_head_desc head_desc(const rp_module_desc& m) { return rp_head_desc{m.B * m.T, m.d, m.vocab, m.dtype, 0}; }
 
 int64_t layer_ws_bytes(const rp_module_desc& m) {
   int64_t b = 256;
-  if (m.n_blocks > 0) b = std::max(b, block_workspace_bytes(block_desc(m, 0)));
+  if (m.n_blocks > 0)
+    b = std::max(b, m.n_heads > 0 ? xl_block_workspace_bytes(xl_desc(m, 0)) : block_workspace_bytes(block_desc(m, 0)));
   if (m.has_projection) b = std::max(b, head_workspace_bytes(head_desc(m)));
   if (m.has_embedding) b = std::max(b, embed_bwd_workspace_bytes(m.B * m.T, m.d));
   return al256(b);
@@ -49,6 +72,8 @@ int check_desc(const rp_module_desc& m) {
   if (m.n_blocks == 0 && !m.has_embedding && !m.has_projection)
     return set_error(RP_ERR_INVALID, "module: empty layer slice");
   if (m.drop_enabled && !m.layer_seeds) return set_error(RP_ERR_INVALID, "module: dropout needs layer_seeds");
+  if (m.n_heads < 0 || (m.n_heads > 0 && (m.d % m.n_heads || m.M < 0 || m.mem_len < 0 || m.mem_len > m.M)))
+    return set_error(RP_ERR_DIMENSION, "module: bad Transformer-XL shape");
   return RP_OK;
 }
 
@@ -75,7 +100,12 @@ int module_forward(const rp_module_desc& m, const rp_module_weights& w, const rp
   for (int j = 0; j < m.n_blocks; ++j) {
     void* dst = j + 1 < n_acts ? s.acts[j + 1] : out;
     if (!dst) return set_error(RP_ERR_INVALID, "module_forward: no output buffer for the last block");
-    RP_TRY(block_forward(block_desc(m, layer + j), w.blocks[j], s.acts[j], dst, s.tapes[j], ws, lws, flag, st));
+    if (m.n_heads > 0) {
+      if (!w.xl_blocks || !s.xl_tapes || !w.R) return set_error(RP_ERR_INVALID, "module_forward: XL module lacks XL blocks");
+      RP_TRY(xl_block_forward(xl_desc(m, layer + j), w.xl_blocks[j], w.R, dst, s.xl_tapes[j], ws, lws, flag, st));
+    } else {
+      RP_TRY(block_forward(block_desc(m, layer + j), w.blocks[j], s.acts[j], dst, s.tapes[j], ws, lws, flag, st));
+    }
   }
   if (m.has_projection)
     RP_TRY(head_forward(head_desc(m), s.acts[m.n_blocks], w.tied, s.targets, s.lse, s.loss, s.loss64, ws, lws, flag,
@@ -110,8 +140,15 @@ int module_backward(const rp_module_desc& m, const rp_module_weights& w, const r
       g_next = gbuf[ping];
       ping ^= 1;
     }
-    RP_TRY(block_backward(block_desc(m, first_block_layer + j), w.blocks[j], s.acts[j], s.tapes[j], g, g_next,
-                          G.blocks[j], ws, lws, st));
+    if (m.n_heads > 0) {
+      if (!w.xl_blocks || !s.xl_tapes || !G.xl_blocks || !w.R)
+        return set_error(RP_ERR_INVALID, "module_backward: XL module lacks XL blocks");
+      RP_TRY(xl_block_backward(xl_desc(m, first_block_layer + j), w.xl_blocks[j], w.R, s.xl_tapes[j], g, g_next,
+                               G.xl_blocks[j], ws, lws, st));
+    } else {
+      RP_TRY(block_backward(block_desc(m, first_block_layer + j), w.blocks[j], s.acts[j], s.tapes[j], g, g_next,
+                            G.blocks[j], ws, lws, st));
+    }
     g = g_next;
   }
   if (m.has_embedding) {

@@ -144,6 +144,13 @@ int head_backward(const rp_head_desc& h, const void* x, const void* tied, const 
                   float* g_x, float* vo, float vo_alpha, int vo_accumulate, void* ws, int64_t ws_bytes,
                   cudaStream_t st);
 
+int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d);
+int xl_block_forward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, const void* R, void* out,
+                     const rp_xl_block_tape& tp, void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);
+int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, const void* R,
+                      const rp_xl_block_tape& tp, const float* g_out, float* g_x, const rp_xl_block_grads& G,
+                      void* ws, int64_t ws_bytes, cudaStream_t st);
+
 int64_t module_workspace_bytes(const rp_module_desc& m);
 int module_forward(const rp_module_desc& m, const rp_module_weights& w, const rp_module_slot& s, void* out,
                    void* ws, int64_t ws_bytes, int32_t* flag, cudaStream_t st);

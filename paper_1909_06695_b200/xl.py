@@ -261,3 +261,93 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     ops.colsum_finish_multi([(pm, nbm, G["b2"]), (part[:, :f], nbc, G["b1"]), (pg2, nbl_cur, G["ln2_g"]),
                              (pb2, nbl_cur, G["ln2_b"]), (pg, nbl_cur + nbl_mem, G["ln1_g"]),
                              (pb, nbl_cur + nbl_mem, G["ln1_b"])])
+
+
+# ---------------------------------------------------------------------------
+# the same block through the C ABI (rp_xl_block_forward / _backward,
+# csrc/layers.cpp): one call per block for a non-Python host, bitwise equal
+# to the op-by-op path above (tests/test_module_abi_gpu.py)
+
+
+def fused_flags(tp):
+    """The RP_XL_FUSED_* kernels this process's switches select for the tape."""
+    f = 0
+    if fused_pv_ok(tp):
+        f |= N.XL_FUSED_PV
+    elif fused_ok(tp):
+        f |= N.XL_FUSED_FWD
+    if fused_dq_ok(tp):
+        f |= N.XL_FUSED_DQ
+    elif fused_bwd_ok(tp):
+        f |= N.XL_FUSED_BWD
+    return f
+
+
+def xl_desc(tp, drop, rows_total=0, max_ctas=0):
+    from .rng import keep_threshold  # noqa: F401
+
+    d = N.XlBlockDesc()
+    d.B, d.T, d.M, d.d, d.f = tp.B, tp.T, tp.M, tp.H * tp.dh, tp.h1.shape[-1]
+    d.H, d.dtype = tp.H, N.BF16 if tp.xa.dtype == torch.bfloat16 else N.F32
+    d.activation = N.ACT_GELU if getattr(tp, "activation", "relu") == "gelu" else N.ACT_RELU
+    d.max_ctas, d.mem_len = max_ctas, tp.mem_len
+    if drop is not None:
+        d.drop_enabled, d.drop_seed, d.drop_threshold, d.drop_scale = 1, drop[0], drop[1], drop[2]
+    d.drop_rows_total = rows_total or 0
+    d.ldk = tp.ldk
+    d.fused = fused_flags(tp)
+    d.score_tile = SCORE_TILE
+    return d
+
+
+def xl_weights(W):
+    w = N.XlBlockWeights()
+    for n in N.XL_W_MATS + N.XL_W_VECS:
+        setattr(w, n, W[n].data_ptr())
+    return w
+
+
+def xl_tape(tp):
+    t = N.XlBlockTape()
+    for n in N.XL_TAPE:
+        v = tp.probs_buf if n == "probs" else getattr(tp, n, None)
+        setattr(t, n, None if v is None else v.data_ptr())
+    return t
+
+
+def xl_grads(G):
+    g = N.XlBlockGrads()
+    for n in ("wqkv", "wo", "w1", "w2", "wr", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "b1", "b2", "r_w_bias", "r_r_bias"):
+        setattr(g, n, G[n].data_ptr())
+    return g
+
+
+def _native_ws(ws, d):
+    import ctypes
+
+    nbytes = N.lib().rp_xl_block_workspace_bytes(ctypes.byref(d))
+    return ws.get("xl_native_ws", (max(256, nbytes),), torch.uint8), nbytes
+
+
+def xl_block_forward_native(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
+    import ctypes
+
+    d = xl_desc(tp, drop, rows_total)
+    buf, nbytes = _native_ws(ws, d)
+    ops._count(1)
+    N.check(N.lib().rp_xl_block_forward(ctypes.byref(d), ctypes.byref(xl_weights(W)), R.data_ptr(), out.data_ptr(),
+                                        ctypes.byref(xl_tape(tp)), buf.data_ptr(), nbytes,
+                                        None if flag is None else flag.data_ptr(), ops._stream()), "xl_block_forward")
+
+
+def xl_block_backward_native(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
+    import ctypes
+
+    d = xl_desc(tp, drop, rows_total)
+    buf, nbytes = _native_ws(ws, d)
+    ops._count(1)
+    N.check(N.lib().rp_xl_block_backward(ctypes.byref(d), ctypes.byref(xl_weights(W)), R.data_ptr(),
+                                         ctypes.byref(xl_tape(tp)), g_out.data_ptr(), g_x.data_ptr(),
+                                         ctypes.byref(xl_grads(G)), buf.data_ptr(), nbytes, ops._stream()),
+            "xl_block_backward")
+

@@ -85,15 +85,12 @@ def test_module_abi_bitwise_equals_host_loop(dtype):
             assert torch.equal(ia, ib), m.index
 
 
-def test_module_abi_rejects_xl_and_empty():
+def test_module_abi_rejects_bad_descriptors():
     from paper_1909_06695_b200 import _native as N
-    from paper_1909_06695_b200 import model as M
-    from paper_1909_06695_b200 import module_abi as MA
 
-    stack = M.build_xl_stack(VOCAB, D, F, 2, T, 0.1, 5, 2, 8, dtype="fp32")
-    (m,) = M.build_modules(stack, M.partition(stack.num_layers, 1), dropout_seed=9)
-    with pytest.raises(ValueError):
-        MA.describe(m, B, T, [0] * 4, True)
+    dsc = N.ModuleDesc()
+    dsc.B, dsc.T, dsc.d, dsc.n_heads, dsc.M, dsc.mem_len = 1, 1, 8, 3, 4, 0  # heads do not divide d
+    assert N.lib().rp_module_forward(dsc, None, None, None, None, 0, None, None) != 0
     dsc = N.ModuleDesc()
     dsc.B, dsc.T, dsc.d = 1, 1, 8
     assert N.lib().rp_module_forward(dsc, None, None, None, None, 0, None, None) != 0
@@ -118,3 +115,123 @@ def test_embedding_gradient_kernel_matches_reference_rule():
         embedding_gradient(0, 3, vo, vi)
     with pytest.raises(ScheduleViolation):
         embedding_gradient(4, 3, vo, None)
+
+
+def _xl_tape_tensors(tp):
+    out = []
+    for n in ("xa", "a", "qkv", "qu", "qv", "kh", "vh", "rh", "probs_buf", "ctx", "x1", "m", "h1", "z1", "mean1",
+              "rstd1", "mean2", "rstd2"):
+        v = getattr(tp, n, None)
+        if v is not None:
+            out.append(v.clone())
+    return out
+
+
+@pytest.mark.parametrize("dtype,act", [("fp32", "relu"), ("bf16", "relu"), ("bf16", "gelu")])
+def test_xl_block_abi_bitwise_equals_host_loop(dtype, act):
+    """rp_xl_block_forward / _backward (one C call per Transformer-XL block)
+    against the op-by-op host path of xl.py: bitwise equal outputs, tapes and
+    gradients -- bf16 at head dim 64 and T % 128 == 0 runs the fused
+    forward-with-P.V and backward-with-dQ kernels, fp32 the GEMM + softmax path."""
+    from paper_1909_06695_b200 import layers as LY
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import xl as XD
+
+    B_, T_, M_, H, d, f = 2, 128, 128, 2, 128, 256
+    stack = MD.build_xl_stack(64, d, f, 1, T_, 0.1, 3, H, M_, dtype=dtype, activation=act)
+    st = stack.storage[1]
+    st.configure_ring(1)
+    st.ensure(0)
+    W = st.weights(0)
+    dev = stack.runtime.device
+    cdt = stack.cdtype
+    g = torch.Generator(device=dev).manual_seed(5)
+    xa = ((torch.rand(B_ * (M_ + T_), d, device=dev, generator=g) * 2 - 1)).to(cdt)
+    g_out = torch.rand(B_ * T_, d, device=dev, generator=g) - 0.5
+    R = XD.sinusoid(M_ + T_, d, cdt, dev)
+    drop = LY.Dropout.make(4321, 0.1, True)
+    res = []
+    for native in (False, True):
+        tp = XD.XLTape(B_, T_, M_, d, f, H, cdt, dev, act)
+        tp.xa.copy_(xa)
+        tp.mem_len = M_ - 20
+        ws = LY.Workspace(dev)
+        out = torch.empty(B_ * T_, d, dtype=cdt, device=dev)
+        gx = torch.empty(B_ * T_, d, device=dev)
+        st.grad.zero_()
+        if native:
+            XD.xl_block_forward_native(W, W, out, tp, R, drop, ws, stack.runtime.flag)
+            XD.xl_block_backward_native(W, W, tp, R, g_out, gx, st.G, drop, ws)
+        else:
+            XD.xl_block_forward(W, W, out, tp, R, drop, ws, stack.runtime.flag)
+            XD.xl_block_backward(W, W, tp, R, g_out, gx, st.G, drop, ws)
+        torch.cuda.synchronize()
+        res.append((out.clone(), gx.clone(), st.grad.clone(), _xl_tape_tensors(tp)))
+    a, b = res
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    for u, v in zip(a[3], b[3]):
+        assert torch.equal(u, v)
+    if dtype == "bf16":
+        assert XD.fused_flags(tp) == 12  # the P.V-fused forward and the dQ-fused backward ran
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_xl_module_abi_bitwise_equals_host_loop(dtype):
+    """rp_module_forward / rp_module_backward over Transformer-XL modules
+    (memory loaded / stored by the host around the call) against the per-layer
+    host loop: bitwise equal losses, activations, tapes, memory and gradients."""
+    from paper_1909_06695_b200 import layers as LY
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import module_abi as MA
+    from paper_1909_06695_b200.model import StaleSlot, _Arena
+
+    V, d, f, nb, T_, M_, H, B_ = 64, 128, 256, 3, 128, 128, 2, 2
+    runs = []
+    for path in range(2):
+        stack = MD.build_xl_stack(V, d, f, nb, T_, 0.1, 5, H, M_, dtype=dtype)
+        mods = MD.build_modules(stack, MD.partition(stack.num_layers, 2), dropout_seed=9)
+        dev = stack.runtime.device
+        g = torch.Generator(device=dev).manual_seed(3)
+        rec = []
+        for step in range(2):  # the second step sees the first one's memory
+            tokens = torch.randint(0, V, (B_, T_), device=dev, generator=g)
+            targets = torch.randint(0, V, (B_ * T_,), device=dev, generator=g)
+            x_next = None
+            for m in mods:
+                m.snapshot(step)
+                seeds = [m._layer_seed(step, i) for i in range(len(m.layers))]
+                a = _Arena(m, B_, T_)
+                if m.has_embedding:
+                    a.tokens.copy_(tokens)
+                else:
+                    a.acts[0].copy_(x_next)
+                if m.has_projection:
+                    a.targets.copy_(targets)
+                out = None if m.has_projection else torch.empty(B_ * T_, d, dtype=stack.cdtype, device=dev)
+                ws = LY.Workspace(dev)
+                if path == 0:
+                    r = m._run_forward(step, a, seeds, True, out, ws, live=True)
+                else:
+                    r = MA.forward(m, a, step, seeds, True, out, ws, live=True)
+                x_next = out
+                rec += [r.clone()] + [t.clone() for t in a.acts] + [t.clone() for tp in a.tapes
+                                                                   for t in _xl_tape_tensors(tp)]
+                rec += [v.clone() for v in m.mem.values()]
+                g_out = None if m.has_projection else torch.linspace(-1, 1, B_ * T_ * d, device=dev).view(-1, d)
+                g_in = None if m.has_embedding else torch.empty(B_ * T_, d, device=dev)
+                tied = torch.zeros(V, d, device=dev)
+                m.zero_grads()
+                if path == 0:
+                    m.recompute_backward(StaleSlot(step, step, None, None, seeds, a), g_out, "snapshot", True,
+                                         g_in=g_in, emb=(0.5, 0.5, tied))
+                else:
+                    MA.backward(m, a, step, seeds, True, g_out, g_in, tied, 0.5 if m.has_projection else 0.0,
+                                0.5 if m.has_embedding else 0.0, True, ws)
+                rec += [v.clone() for v in m.grad_views.values()] + [tied.clone()]
+                if g_in is not None:
+                    rec.append(g_in.clone())
+        torch.cuda.synchronize()
+        runs.append(rec)
+    assert len(runs[0]) == len(runs[1])
+    for i, (u, v) in enumerate(zip(*runs)):
+        assert torch.equal(u, v), i
