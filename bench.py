@@ -342,7 +342,10 @@ class _Job:
         self.E = E
         self.B, self.T = c["batch"], c["seq"]
         self.world, self.rank = world, rank
-        self.pipeline = world > 1 and args.mode == "pipeline"
+        # --engine distributed at N = 1 runs the multi-GPU engine itself (K = 2
+        # on one rank, no transfers): the pipeline code path of this bench on a
+        # single GPU (its micro-batched relay included)
+        self.pipeline = (world > 1 and args.mode == "pipeline") or args.engine == "distributed"
         self.K = world + 1 if self.pipeline else 2
         B, T = self.B, self.T
         stack = make_stack(c, 1 if self.pipeline else 1 + rank, dtype)
@@ -566,6 +569,7 @@ def run_ours(args, c):
                        "seq_len": T, "vocab": c["vocab"], "d_model": c["d"], "d_ff": c["f"], "n_blocks": c["blocks"],
                        **({"n_heads": c["heads"], "mem_len": c["mem"]} if c.get("heads") else {}),
                        "placement": "ring (modules 1 and K on GPU 0)",
+                       "engine": "DistributedPipelineEngine" if pipeline else "ConcurrentPipelineEngine",
                        "parallelism": (f"ouroboros pipeline K={K} over {world} GPUs"
                                        + (f", {args.micro} micro-batches" if args.micro > 1 else "")
                                        if pipeline else
@@ -599,8 +603,15 @@ def main():
     ap.add_argument("--config", default="c3", choices=list(CONFIGS))
     ap.add_argument("--mode", default="pipeline", choices=["pipeline", "replicas"],
                     help="N>1: the Ouroboros pipeline K=N+1 (default) or independent K=2 replicas per GPU")
+    # Default 1: on one B200 a C3 step with 2 micro-batches through the same
+    # engine measured 21.4 vs 13.6 ms -- at 11 x 512 rows the N = 512 block
+    # GEMMs fill 0.6 waves of CTA pairs, so halving the rows nearly doubles
+    # their time per token; the micro-batched relay pays off only when the
+    # pipeline bubble it removes exceeds that (many GPUs, large batches)
     ap.add_argument("--micro", type=int, default=int(os.environ.get("RP_MICRO", "1")),
                     help="micro-batches per relay in the multi-GPU pipeline")
+    ap.add_argument("--engine", default="auto", choices=["auto", "distributed"],
+                    help="distributed: the multi-GPU engine even at N = 1 (K = 2 on one rank)")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--no-fp32", dest="fp32", action="store_false", help="skip the fp32 check-mode line")
     ap.add_argument("--no-compare-k1", dest="compare_k1", action="store_false",
