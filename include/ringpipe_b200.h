@@ -92,6 +92,12 @@ typedef struct rp_gemm_args {
   float ce_scale;
   int32_t k_splits; /* > 1: C = [k_splits, M, N] fp32 partials over K ranges (rp_splitk_reduce) */
   int32_t max_ctas; /* > 0: cap the persistent grid (SM budget when sharing the GPU with another stream) */
+  /* Banded A (causal / memory-window attention matrices): k_lo_sign = +1 means
+   * row m of op(A) is zero for k < m + k_lo_off, so each output tile starts its
+   * K loop at the first k-block any of its rows needs (adding the skipped
+   * zeros would not change one bit of the fp32 sums); 0 = dense. */
+  int32_t k_lo_sign;
+  int64_t k_lo_off;
 } rp_gemm_args;
 
 const char* rp_version(void);

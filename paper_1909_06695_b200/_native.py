@@ -61,6 +61,8 @@ class GemmArgs(ctypes.Structure):
         ("ce_scale", ctypes.c_float),
         ("k_splits", ctypes.c_int32),
         ("max_ctas", ctypes.c_int32),
+        ("k_lo_sign", ctypes.c_int32),
+        ("k_lo_off", ctypes.c_int64),
     ]
 
 

@@ -77,7 +77,19 @@ struct GemmParams {
   int n_fast;  // raster: N tiles fastest
   int tma_store;  // bf16 C written by TMA bulk stores from a swizzled smem tile
   int tma_resid;  // bf16 residual / aux read by TMA bulk loads into a swizzled smem tile
+  int k_lo_sign;  // banded A: row m is zero for k < m + k_lo_off (sign +1); 0 = dense
+  int k_lo_off;
 };
+
+// First k-block of a tile's K loop: a banded A skips the leading all-zero
+// k-blocks of the tile's first row (the same range for producer and MMA)
+template <int BM_TILE, int BK>
+__device__ __forceinline__ int tile_kb_lo(const GemmParams& p, int mb) {
+  if (p.k_lo_sign <= 0) return 0;
+  const int k = mb * BM_TILE + p.k_lo_off;
+  const int kb = k > 0 ? k / BK : 0;
+  return kb < p.kb_per_pass ? kb : p.kb_per_pass - 1;
+}
 
 __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int n0, int b,
                                             const float (&v)[32]) {
@@ -327,10 +339,11 @@ __global__ void __launch_bounds__(384, 1)
         const int m0 = mb * Cfg::BM_TILE + crank * Cfg::BM, n0 = nb * BN + crank * Cfg::B_ROWS;
         const int kbase = p.ksplit ? b * p.ksplit : 0;
         const int bc = p.ksplit ? 0 : b;
+        const int kb_lo = tile_kb_lo<Cfg::BM_TILE, Cfg::BK>(p, mb);
         for (int pass = 0; pass < p.passes; ++pass) {
           const CUtensorMap* ma = (pass == 2) ? &mapA_lo : &mapA;
           const CUtensorMap* mbm = (pass == 1) ? &mapB_lo : &mapB;
-          for (int kb = 0; kb < p.kb_per_pass; ++kb) {
+          for (int kb = kb_lo; kb < p.kb_per_pass; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
             uint8_t* sb = sa + Cfg::A_BYTES;
@@ -397,8 +410,11 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        int mb_, nb_, b_;
+        decode_tile(p, tile, mb_, nb_, b_);
+        const int kb_lo = tile_kb_lo<Cfg::BM_TILE, Cfg::BK>(p, mb_);
         for (int pass = 0; pass < p.passes; ++pass) {
-          for (int kb = 0; kb < p.kb_per_pass; ++kb) {
+          for (int kb = kb_lo; kb < p.kb_per_pass; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
@@ -408,9 +424,9 @@ __global__ void __launch_bounds__(384, 1)
               const uint64_t ad = umma_desc(sa + k * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t bd = umma_desc(sb + k * b_step, b_lbo, b_sbo, b_lay);
               if constexpr (kCta == 2)
-                tc_mma_pair(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
+                tc_mma_pair(d_tmem, ad, bd, idesc, (pass | (kb - kb_lo) | k) != 0 ? 1u : 0u);
               else
-                tc_mma<kTf32>(d_tmem, ad, bd, idesc, (pass | kb | k) != 0 ? 1u : 0u);
+                tc_mma<kTf32>(d_tmem, ad, bd, idesc, (pass | (kb - kb_lo) | k) != 0 ? 1u : 0u);
             }
             if constexpr (kCta == 2)
               tc_commit_pair(&empty[stage]);
@@ -1020,6 +1036,10 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   GemmParams p{};
   p.tma_store = tma_store;
   p.tma_resid = tma_resid;
+  if (a.k_lo_sign > 0 && (ks > 1 || a.k_lo_off < INT32_MIN / 2 || a.k_lo_off > INT32_MAX / 2))
+    return set_error(RP_ERR_INVALID, "banded A: no split-K, |k_lo_off| < 2^30");
+  p.k_lo_sign = a.k_lo_sign > 0 ? 1 : 0;
+  p.k_lo_off = (int)a.k_lo_off;
   p.M = (int)a.M;
   p.N = (int)a.N;
   p.K = (int)a.K;

@@ -138,6 +138,7 @@ def gemm(
     b_lo=None,
     tile_n=0,
     probe=None,
+    k_lo_off=None,
 ):
     """C = epilogue(alpha * opA(a) @ opB(b)) on the tcgen05 GEMM.
 
@@ -146,7 +147,8 @@ def gemm(
     bf16 operands run on kind::f16; fp32 operands run the 3-pass tf32 path
     unless math=MATH_TF32.  probe: a Probe tag -- with ops.PROBE set, the
     launch (and its split-K reduce) is bracketed by CUDA events and counted
-    as 2*M*N*K*batch algorithmic FLOPs.
+    as 2*M*N*K*batch algorithmic FLOPs.  k_lo_off: op(A) is banded -- row m
+    is zero for k < m + k_lo_off -- and tiles skip those k-blocks.
     """
     _require_cuda(a, b)
     if a.dtype != b.dtype or a.dtype not in _DT:
@@ -199,6 +201,8 @@ def gemm(
         args.out_dtype = N.F32
     args.epilogue = epilogue
     args.tile_n = tile_n
+    if k_lo_off is not None:
+        args.k_lo_sign, args.k_lo_off = 1, int(k_lo_off)
     args.alpha = alpha
     if bias is not None:
         args.bias = bias.data_ptr()
@@ -219,7 +223,7 @@ def gemm(
         args.target_logit = target_logit.data_ptr()
     args.ce_scale = ce_scale
     splits = 1
-    if out is not None and out.dtype == torch.float32 and epilogue == N.EPI_STORE and batch == 1:
+    if out is not None and out.dtype == torch.float32 and epilogue == N.EPI_STORE and batch == 1 and k_lo_off is None:
         # deterministic split-K for weight-gradient shapes (few tiles, long K),
         # the same rule and scratch size as the native composites (layers.cpp)
         splits = N.lib().rp_gemm_choose_splits(M, Nn, K, SPLITK_CAP)

@@ -108,6 +108,7 @@ def fused_bwd_ok(tp):
 
 FUSED_DQ = os.environ.get("RP_XL_FUSED_DQ", "1") != "0"
 FUSED_PV = os.environ.get("RP_XL_FUSED_PV", "1") != "0"
+BANDED = os.environ.get("RP_XL_BANDED", "1") != "0"
 
 
 def fused_pv_ok(tp):
@@ -229,13 +230,16 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
         ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p, tile_n=SCORE_TILE)
         ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
     g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
-    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh)
+    # P^T and dAC^T are banded: key j sees queries i >= j - M (causal window),
+    # so each key tile starts its K loop (over queries) at its first live block
+    band = -M if BANDED else None
+    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
     g_kh = ws.get("xl_g_kh", (H * B, Kl, dh), torch.float32)
     g_rh = ws.get("xl_g_rh", (H, Kl, dh), torch.float32)
     if not dq_done:
         ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
-    ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh)
+    ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh, k_lo_off=band)
     if not dq_done:
         ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)

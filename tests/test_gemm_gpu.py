@@ -148,3 +148,24 @@ def test_lse_partial_and_ce_grad(dev, dtype):
     p = torch.softmax(z, dim=1)
     p[torch.arange(M), y] -= 1.0
     assert _rel(dz, p / M) < 1e-4
+
+
+@pytest.mark.parametrize("off", [-512, -300, 0, 200])
+def test_banded_a_skips_zero_k_blocks_bitwise(off):
+    """k_lo_off: op(A) row m is zero for k < m + off (the causal window of the
+    XL attention matrices); tiles skip those k-blocks -- the result is bitwise
+    the dense GEMM's (the skipped products are exact zeros)."""
+    from paper_1909_06695_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    HB, Kl, T, dh = 6, 1024, 512, 64
+    P = torch.rand(HB, T, Kl, device="cuda", generator=g).to(torch.bfloat16)
+    i = torch.arange(T, device="cuda")[:, None]
+    j = torch.arange(Kl, device="cuda")[None, :]
+    P = P.masked_fill(i < j + off, 0)  # A = P^T: row j is zero for k = i < j + off
+    G = (torch.randn(HB, T, dh, device="cuda", generator=g)).to(torch.bfloat16)
+    dense = ops.gemm(P, G, a_mn=True, b_mn=True, out_dtype=torch.float32)
+    band = ops.gemm(P, G, a_mn=True, b_mn=True, out_dtype=torch.float32, k_lo_off=off)
+    assert torch.equal(dense, band)
+    want = P.float().transpose(1, 2) @ G.float()
+    assert float((band - want).norm() / want.norm()) <= 1e-5
