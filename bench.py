@@ -62,10 +62,9 @@ CONFIGS = {
     # BASELINE.json configs[0] (the reference's CPU-runnable oracle case)
     "c1": dict(name="4L-d128-V1k", vocab=1000, d=128, f=512, blocks=4, seq=64, batch=16, p=0.1),
     # BASELINE.json configs[3]: Transformer-XL with the adaptive tied softmax over a
-    # WikiText-103-shaped vocabulary (cutoffs 20k / 40k / 200k, public XL scripts)
-    # The published d 410 / 10 heads x 41 break the 16-byte TMA row pitch; the
-    # nearest runnable shape is d 400 = 10 heads x 40, d_ff 2104 (= 2100 rounded to 8)
-    "c4": dict(name="XL-16L-d400(410)-H10x40-T150-M150-adaptive-WT103shape", vocab=267735, d=400, f=2104, blocks=16,
+    # WikiText-103-shaped vocabulary (cutoffs 20k / 40k / 200k, public XL scripts);
+    # the published d 410 = 10 heads x 41 and d_ff 2100: bf16 rows at 16-byte pitches
+    "c4": dict(name="XL-16L-d410-H10x41-T150-M150-adaptive-WT103shape", vocab=267735, d=410, f=2100, blocks=16,
                seq=150, batch=60, p=0.1, heads=10, mem=150, cutoffs=[20000, 40000, 200000]),
     # BASELINE.json configs[4]: Transformer-XL large, text8-shaped (27 symbols)
     "c5": dict(name="XL-24L-d1024-H8-T768-M768-text8shape", vocab=27, d=1024, f=3072, blocks=24, seq=768,

@@ -13,6 +13,10 @@
  *    for the duration of the (asynchronous) call and never frees caller memory.
  *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
  *    it.  Handles are thread-compatible, not thread-safe (one owner).
+ *  - Row pitches ("ld*", in elements; 0 = the row length): bf16 rows that are
+ *    operands of the TMA-fed GEMM need 16-byte pitches, so widths that are not
+ *    multiples of 8 (BASELINE configs[3]: d 410, heads of 41, d_ff 2100) live
+ *    in rows padded to the next multiple of 8.
  *  - Return value: rp_status.  On failure rp_last_error() gives the message.
  *    The Python host maps statuses onto the reference exception classes
  *    (tensor.py:20-25, model.py:28-33, engine.py:138-139).
@@ -123,13 +127,13 @@ int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t co
 /* y = (x-mu)*rstd*g + b over rows of d; saves mean/rstd (fp32). dtype: rp_dtype of x/y;
  * gain/bias are fp32. */
 int rp_layernorm_fwd(int32_t dtype, const void* x, const float* gain, const float* bias, void* y, float* mean,
-                     float* rstd, int64_t rows, int64_t d, int32_t* flag, void* stream);
+                     float* rstd, int64_t rows, int64_t d, int64_t ld_x, int64_t ld_y, int32_t* flag, void* stream);
 /* dx = LN-backward(dy) + resid_grad (fp32); dx_masked = dx*dropout-mask (dtype) if non-NULL;
  * writes rp_layernorm_bwd_blocks(rows) partial rows of dgain/dbias. */
 int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
                      const float* gain, const float* resid_grad, float* dx, void* dx_masked, uint64_t seed,
                      uint64_t threshold, float scale, int32_t drop_enabled, float* partial_gain,
-                     float* partial_bias, int64_t rows, int64_t d, void* stream);
+                     float* partial_bias, int64_t rows, int64_t d, int64_t ld_x, int64_t ld_masked, void* stream);
 int rp_layernorm_bwd_blocks(int64_t rows);
 
 /* ---- deterministic column sums (bias/gain gradients, layers.py:72-73,220,223) ---- */
@@ -144,7 +148,9 @@ int rp_colsum_finish_multi(const float* const* partials, const int32_t* nblocks,
  * (layers.py:209-220). */
 int rp_mask_grad_blocks(int64_t rows, int64_t d); /* partial rows rp_mask_grad writes */
 int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
-                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream);
+                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, int64_t ld_out, void* stream);
+/* partial rows rp_mask_grad writes when its output pitch ld_out differs from d */
+int rp_mask_grad_blocks_ld(int64_t rows, int64_t d, int64_t ld_out);
 
 /* ---- causal single-head attention softmax (layers.py:180-183, 237) ---------- */
 /* rows = B*T rows of length T, row stride ld (>= T) */
@@ -160,16 +166,18 @@ int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, vo
  * attention with segment memory.  xa rows: B*M memory rows, then B*T current
  * rows; head-major layouts qu/qv [H,B,T,dh], kh/vh [H,B,M+T,dh]. */
 int rp_xl_split_qkv(int32_t dtype, const void* qkv, const float* r_w_bias, const float* r_r_bias, void* qu, void* qv,
-                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream);
+                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
+                    int64_t ld_h, void* stream);
 /* dst[h, r, c] = src[r*ld + h*dh + c] */
 int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t dst_dtype, void* dst, int64_t rows,
-                      int32_t H, int32_t dh, void* stream);
+                      int32_t H, int32_t dh, int64_t ld_h, void* stream);
 /* dst[r*ld + h*dh + c] = src[h, r, c] */
 int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
-                      int32_t H, int32_t dh, void* stream);
+                      int32_t H, int32_t dh, int64_t ld_h, void* stream);
 /* g_qkv (xa row layout, [B*(M+T), 3d]) from fp32 head-major dQu, dQv, dK, dV */
 int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
-                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream);
+                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
+                      void* stream);
 /* P = softmax((AC + relshift(BD)) * scale) over keys M-mem_len <= j <= M+i; rows = H*B*T */
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream);
@@ -221,7 +229,7 @@ int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, floa
 /* ---- embedding (layers.py:114-136) ---------------------------------------- */
 int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
                  int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
-                 int32_t drop_enabled, int32_t* flag, void* stream);
+                 int32_t drop_enabled, int32_t* flag, int64_t ld, void* stream);
 /* grad_pos [Tmax,d] (fully written); emb[tok] += beta * sum of masked rows (deterministic
  * sorted, chunked scatter; replaces np.add.at, layers.py:135).  Ids outside [0, vocab)
  * are skipped (rp_embed_fwd already raised RP_FLAG_DIMENSION for them; the reference
@@ -229,7 +237,7 @@ int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const v
  * workspace: rp_embed_bwd_workspace_bytes(B*T, d) bytes. */
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
                  int64_t vocab, uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
-                 float* emb_grad, float beta, void* workspace, void* stream);
+                 float* emb_grad, float beta, void* workspace, int64_t ld_out, void* stream);
 int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
 
 /* ---- tied-head cross-entropy finish (layers.py:287-296, 310-316) ------------ */

@@ -184,19 +184,20 @@ def _declare(L):
         "rp_gemm_choose_splits": [i64, i64, i64, i64],
         "rp_splitk_reduce": [vp, i32, i64, i64, vp, i64, vp],
         "rp_tf32_split": [vp, vp, vp, i64, i64, i64, i64, vp],
-        "rp_layernorm_fwd": [i32, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp],
-        "rp_layernorm_bwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, u64, u64, f32, i32, vp, vp, i64, i64, vp],
+        "rp_layernorm_fwd": [i32, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp],
+        "rp_layernorm_bwd": [i32, vp, vp, vp, vp, vp, vp, vp, vp, u64, u64, f32, i32, vp, vp, i64, i64, i64, i64, vp],
         "rp_layernorm_bwd_blocks": [i64],
         "rp_colsum_blocks": [i64],
         "rp_mask_grad_blocks": [i64, i64],
         "rp_colsum_partial": [i32, vp, i64, i64, i64, vp, vp],
         "rp_colsum_finish": [vp, i32, i64, vp, vp],
         "rp_colsum_finish_multi": [vp, vp, vp, vp, i32, vp],
-        "rp_mask_grad": [i32, vp, vp, i64, i64, u64, u64, u64, f32, i32, vp, vp],
+        "rp_mask_grad": [i32, vp, vp, i64, i64, u64, u64, u64, f32, i32, vp, i64, vp],
+        "rp_mask_grad_blocks_ld": [i64, i64, i64],
         "rp_softmax_causal": [i32, vp, vp, i64, i64, i64, vp],
         "rp_softmax_bwd": [i32, vp, vp, vp, f32, i64, i64, i64, vp],
-        "rp_embed_fwd": [i32, vp, vp, vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp],
-        "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, vp],
+        "rp_embed_fwd": [i32, vp, vp, vp, vp, i64, i64, i64, i64, u64, u64, f32, i32, vp, i64, vp],
+        "rp_embed_bwd": [vp, vp, i64, i64, i64, i64, i64, u64, u64, f32, i32, vp, vp, f32, vp, i64, vp],
         "rp_embed_bwd_workspace_bytes": [i64, i64],
         "rp_ce_finish": [vp, i32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp],
         "rp_adam_step": [vp, vp, vp, vp, vp, i32, i64, f32, f32, f32, f32, f32, f32, vp, vp],
@@ -205,10 +206,10 @@ def _declare(L):
         "rp_cast": [vp, i32, vp, i32, i64, vp],
         "rp_embedding_gradient": [i64, i64, vp, vp, vp, i64, i32, vp],
         "rp_sq_norm": [vp, i64, vp, vp, i32, vp],
-        "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
-        "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, vp],
-        "rp_xl_merge_heads": [i32, vp, i32, vp, i64, i64, i32, i32, vp],
-        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, vp],
+        "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, vp],
+        "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, i64, vp],
+        "rp_xl_merge_heads": [i32, vp, i32, vp, i64, i64, i32, i32, i64, vp],
+        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, vp],
         "rp_xl_softmax_fwd": [i32, vp, vp, i64, vp, i64, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd": [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],

@@ -21,6 +21,7 @@ import torch
 from . import _native as N
 from . import ops
 from .errors import DimensionError
+from . import layers as LY
 from .layers import _pad8
 
 
@@ -37,8 +38,8 @@ class AdaptiveHead:
     def __init__(self, vocab, d, cutoffs, device, dtype=torch.bfloat16):
         if not cutoffs or cutoffs[0] <= 0 or any(b <= a for a, b in zip(cutoffs, cutoffs[1:])) or cutoffs[-1] > vocab:
             raise DimensionError(f"adaptive softmax: bad cutoffs {cutoffs} for vocab {vocab}")
-        if d % 8 or cutoffs[0] % 8:
-            raise DimensionError("adaptive softmax: d and the head size c_0 must be multiples of 8 (TMA 16-byte rows)")
+        if cutoffs[0] % 8:
+            raise DimensionError("adaptive softmax: the head size c_0 must be a multiple of 8 (TMA 16-byte rows)")
         self.vocab, self.d, self.cutoffs, self.device, self.dtype = vocab, d, list(cutoffs), device, dtype
         self.tails = clusters(cutoffs, vocab)
         self.n = len(self.tails)
@@ -105,7 +106,7 @@ class AdaptiveHead:
                 continue
             idx = torch.from_numpy(sel).to(dev, non_blocking=True)
             yk = torch.from_numpy(y[sel] - lo).to(dev, non_blocking=True)
-            hk = self._buf(f"h{k}", (sel.size, d), cdt)
+            hk = self._buf(f"h{k}", (sel.size, LY.pad_cols(d, cdt)), cdt)[:, :d]
             ops.rows_gather(h, idx, hk)
             lse_k, loss_k = self._lse(hk, tied_c[lo:hi], yk, hi - lo, f"t{k}", flag)
             total += loss_k * (sel.size / Nr)

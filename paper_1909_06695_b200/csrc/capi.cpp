@@ -60,19 +60,20 @@ int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t co
 #define RP_S(s) static_cast<cudaStream_t>(s)
 
 int rp_layernorm_fwd(int32_t dtype, const void* x, const float* gain, const float* bias, void* y, float* mean,
-                     float* rstd, int64_t rows, int64_t d, int32_t* flag, void* stream) {
-  return rp::layernorm_fwd(dtype, x, gain, bias, y, mean, rstd, rows, d, flag, RP_S(stream));
+                     float* rstd, int64_t rows, int64_t d, int64_t ld_x, int64_t ld_y, int32_t* flag, void* stream) {
+  return rp::layernorm_fwd(dtype, x, gain, bias, y, mean, rstd, rows, d, flag, RP_S(stream), ld_x, ld_y);
 }
 int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
                      const float* gain, const float* resid_grad, float* dx, void* dx_masked, uint64_t seed,
                      uint64_t threshold, float scale, int32_t drop_enabled, float* partial_gain,
-                     float* partial_bias, int64_t rows, int64_t d, void* stream) {
+                     float* partial_bias, int64_t rows, int64_t d, int64_t ld_x, int64_t ld_masked, void* stream) {
   return rp::layernorm_bwd(dtype, dy, x, mean, rstd, gain, resid_grad, dx, dx_masked, seed, threshold, scale,
-                           drop_enabled, partial_gain, partial_bias, rows, d, RP_S(stream));
+                           drop_enabled, partial_gain, partial_bias, rows, d, RP_S(stream), ld_x, ld_masked);
 }
 int rp_layernorm_bwd_blocks(int64_t rows) { return rp::ln_bwd_blocks(rows); }
 int rp_colsum_blocks(int64_t rows) { return rp::colsum_blocks(rows); }
 int rp_mask_grad_blocks(int64_t rows, int64_t d) { return rp::mask_grad_blocks(rows, d); }
+int rp_mask_grad_blocks_ld(int64_t rows, int64_t d, int64_t ld_out) { return rp::mask_grad_blocks_ld(rows, d, ld_out); }
 int rp_colsum_partial(int32_t dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* partial,
                       void* stream) {
   return rp::colsum_partial(dtype, x, rows, cols, ld, partial, RP_S(stream));
@@ -89,8 +90,9 @@ int rp_colsum_finish_multi(const float* const* partials, const int32_t* nblocks,
   return rp::colsum_finish_multi(jobs, n, RP_S(stream));
 }
 int rp_mask_grad(int32_t dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
-                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, void* stream) {
-  return rp::mask_grad(dtype, g, out, rows, d, seed, pos0, threshold, scale, drop_enabled, partial, RP_S(stream));
+                 uint64_t threshold, float scale, int32_t drop_enabled, float* partial, int64_t ld_out, void* stream) {
+  return rp::mask_grad(dtype, g, out, rows, d, seed, pos0, threshold, scale, drop_enabled, partial, RP_S(stream),
+                       ld_out);
 }
 int rp_softmax_causal(int32_t dtype, const float* scores, void* probs, int64_t rows, int64_t T, int64_t ld,
                       void* stream) {
@@ -102,15 +104,15 @@ int rp_softmax_bwd(int32_t dtype, const float* grad_probs, const void* probs, vo
 }
 int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,
                  int64_t T, int64_t d, int64_t vocab, uint64_t seed, uint64_t threshold, float scale,
-                 int32_t drop_enabled, int32_t* flag, void* stream) {
+                 int32_t drop_enabled, int32_t* flag, int64_t ld, void* stream) {
   return rp::embed_fwd(dtype, tokens, tied, pos, out, B, T, d, vocab, seed, threshold, scale, drop_enabled, flag,
-                       RP_S(stream));
+                       RP_S(stream), ld);
 }
 int rp_embed_bwd(const float* grad, const int64_t* tokens, int64_t B, int64_t T, int64_t Tmax, int64_t d,
                  int64_t vocab, uint64_t seed, uint64_t threshold, float scale, int32_t drop_enabled, float* grad_pos,
-                 float* emb_grad, float beta, void* work, void* stream) {
+                 float* emb_grad, float beta, void* work, int64_t ld_out, void* stream) {
   return rp::embed_bwd(grad, tokens, B, T, Tmax, d, vocab, seed, threshold, scale, drop_enabled, grad_pos, emb_grad, beta,
-                       work, RP_S(stream));
+                       work, RP_S(stream), ld_out);
 }
 int64_t rp_embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) { return rp::embed_bwd_workspace_bytes(n_tokens, d); }
 int rp_ce_finish(const float* partial, int32_t ntiles, const float* target_logit, const int64_t* targets,
@@ -150,20 +152,22 @@ int rp_sq_norm(const float* x, int64_t n, double* part, double* out, int32_t acc
 }
 
 int rp_xl_split_qkv(int32_t dtype, const void* qkv, const float* r_w_bias, const float* r_r_bias, void* qu, void* qv,
-                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream) {
-  return rp::xl_split_qkv(dtype, qkv, r_w_bias, r_r_bias, qu, qv, kh, vh, B, T, M, H, dh, RP_S(stream));
+                    void* kh, void* vh, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
+                    int64_t ld_h, void* stream) {
+  return rp::xl_split_qkv(dtype, qkv, r_w_bias, r_r_bias, qu, qv, kh, vh, B, T, M, H, dh, RP_S(stream), ld_qkv, ld_h);
 }
 int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t dst_dtype, void* dst, int64_t rows,
-                      int32_t H, int32_t dh, void* stream) {
-  return rp::xl_split_heads(src_dtype, src, ld, dst_dtype, dst, rows, H, dh, RP_S(stream));
+                      int32_t H, int32_t dh, int64_t ld_h, void* stream) {
+  return rp::xl_split_heads(src_dtype, src, ld, dst_dtype, dst, rows, H, dh, RP_S(stream), ld_h);
 }
 int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
-                      int32_t H, int32_t dh, void* stream) {
-  return rp::xl_merge_heads(src_dtype, src, dst_dtype, dst, ld, rows, H, dh, RP_S(stream));
+                      int32_t H, int32_t dh, int64_t ld_h, void* stream) {
+  return rp::xl_merge_heads(src_dtype, src, dst_dtype, dst, ld, rows, H, dh, RP_S(stream), ld_h);
 }
 int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
-                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, void* stream) {
-  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream));
+                      void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
+                      void* stream) {
+  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream), ld_qkv);
 }
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream) {

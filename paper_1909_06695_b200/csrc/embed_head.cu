@@ -19,7 +19,7 @@ namespace rp {
 template <typename T>
 __global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const T* __restrict__ V, const T* __restrict__ pos,
                                  T* __restrict__ out, int64_t rows, int Tn, int d, int64_t vocab, uint64_t seed,
-                                 uint64_t thr, float scale, int drop_on, int32_t* flag) {
+                                 uint64_t thr, float scale, int drop_on, int32_t* flag, int64_t ld) {
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
   const int64_t id = tok[r];
@@ -29,15 +29,15 @@ __global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, const T* __res
   }
   const int t = (int)(r % Tn);
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float v = (ok ? to_f(V[id * d + j]) : 0.f) + to_f(pos[(int64_t)t * d + j]);
+    float v = (ok ? to_f(V[id * ld + j]) : 0.f) + to_f(pos[(int64_t)t * ld + j]);
     if (drop_on) v = dropout_keep(seed, (uint64_t)r * d + j, thr) ? v * scale : 0.f;
-    out[r * d + j] = from_f<T>(v);
+    out[r * ld + j] = from_f<T>(v);
   }
 }
 
 // grad_pos[t, j] = sum_b g[b*T + t, j] * mask ; rows t >= T are zero.
 __global__ void embed_pos_grad_kernel(const float* __restrict__ g, float* __restrict__ gpos, int B, int Tn, int Tmax,
-                                      int d, uint64_t seed, uint64_t thr, float scale, int drop_on) {
+                                      int d, uint64_t seed, uint64_t thr, float scale, int drop_on, int64_t ldp) {
   const int t = blockIdx.x;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float s = 0.f;
@@ -49,7 +49,7 @@ __global__ void embed_pos_grad_kernel(const float* __restrict__ g, float* __rest
         s += v;
       }
     }
-    gpos[(int64_t)t * d + j] = s;
+    gpos[(int64_t)t * ldp + j] = s;
   }
 }
 
@@ -154,7 +154,7 @@ __global__ void embed_chunk_partial_kernel(const uint64_t* __restrict__ sorted, 
 }
 
 __global__ void embed_segment_kernel(const uint64_t* __restrict__ sorted, int n, const float* __restrict__ partial,
-                                     int d, float beta, float* __restrict__ emb) {
+                                     int d, float beta, float* __restrict__ emb, int64_t lde) {
   const int i = blockIdx.x;
   const uint32_t tokv = static_cast<uint32_t>(sorted[i] >> 32);
   if (tokv == kBadTok || (i > 0 && static_cast<uint32_t>(sorted[i - 1] >> 32) == tokv)) return;
@@ -171,7 +171,7 @@ __global__ void embed_segment_kernel(const uint64_t* __restrict__ sorted, int n,
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     float total = partial[(int64_t)i * d + j];
     for (int c = (i / kChunk + 1) * kChunk; c < end; c += kChunk) total += partial[(int64_t)c * d + j];
-    emb[(int64_t)tokv * d + j] += beta * total;
+    emb[(int64_t)tokv * lde + j] += beta * total;
   }
 }
 
@@ -237,13 +237,14 @@ __global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ x,
 
 int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, void* out, int64_t B, int64_t Tn,
               int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
-              cudaStream_t st) {
+              cudaStream_t st, int64_t ld) {
   const int64_t rows = B * Tn;
   if (rows == 0) return RP_OK;
+  if (ld <= 0) ld = d;
   const int threads = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
   RP_DT(dtype, embed_fwd_kernel<T><<<(unsigned)rows, threads, 0, st>>>(tok, (const T*)V, (const T*)pos, (T*)out,
                                                                        rows, (int)Tn, (int)d, vocab, seed, thr,
-                                                                       scale, drop_on, flag));
+                                                                       scale, drop_on, flag, ld));
   return check_launch("embed_fwd");
 }
 
@@ -257,14 +258,15 @@ int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d) {
 int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, int64_t vocab,
               uint64_t seed,
               uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
-              cudaStream_t st) {
+              cudaStream_t st, int64_t ld_out) {
+  if (ld_out <= 0) ld_out = d;
   uint64_t* work = static_cast<uint64_t*>(workspace);
   float* partial = reinterpret_cast<float*>(static_cast<char*>(workspace) + ((B * Tn * 8 + 255) / 256) * 256);
   const int64_t n = B * Tn;
   const int threads = (int)std::min<int64_t>(256, ((d + 31) / 32) * 32);
   if (gpos) {
     embed_pos_grad_kernel<<<(unsigned)Tmax, threads, 0, st>>>(g, gpos, (int)B, (int)Tn, (int)Tmax, (int)d, seed, thr,
-                                                              scale, drop_on);
+                                                              scale, drop_on, ld_out);
     if (int e = check_launch("embed_pos_grad")) return e;
   }
   if (!emb || n == 0) return RP_OK;
@@ -281,7 +283,7 @@ int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t
   dim3 grid(nchunk, (unsigned)std::max<int64_t>(1, (d + tpb - 1) / tpb));
   embed_chunk_partial_kernel<<<grid, tpb, 0, st>>>(work, (int)n, g, (int)d, seed, thr, scale, drop_on, partial);
   if (int e = check_launch("embed_chunk_partial")) return e;
-  embed_segment_kernel<<<(unsigned)n, tpb, 0, st>>>(work, (int)n, partial, (int)d, beta, emb);
+  embed_segment_kernel<<<(unsigned)n, tpb, 0, st>>>(work, (int)n, partial, (int)d, beta, emb, ld_out);
   return check_launch("embed_segment");
 }
 

@@ -824,7 +824,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int6
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= M * N) return;
   const int64_t m = i / N, n = i - m * N;
-  if ((N & 3) == 0 && (ldo & 3) == 0) {
+  if ((N & 3) == 0 && (ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     float4 acc = *reinterpret_cast<const float4*>(part + i);
     for (int s = 1; s < S; ++s) {
       const float4 v = *reinterpret_cast<const float4*>(part + s * sstride + i);

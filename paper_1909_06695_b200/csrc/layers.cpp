@@ -528,6 +528,10 @@ int check_xl(const rp_xl_block_desc& d) {
   if (d.H <= 0 || d.d % d.H || d.B <= 0 || d.T <= 0 || d.M < 0 || d.mem_len < 0 || d.mem_len > d.M)
     return set_error(RP_ERR_DIMENSION, "xl_block: bad shape");
   if (d.ldk < d.M + d.T || d.ldk % 8) return set_error(RP_ERR_DIMENSION, "xl_block: ldk must be pad8(M+T)");
+  if (d.dtype == RP_BF16 && (d.d % 8 || d.f % 8 || (d.d / d.H) % 8))
+    return set_error(RP_ERR_DIMENSION,
+                     "xl_block: the composite takes dense bf16 rows (d, d_ff, head dim multiples of 8); "
+                     "pitched rows go through the op-level entry points");
   if (d.dtype != RP_BF16 && (d.fused & 15)) return set_error(RP_ERR_INVALID, "xl_block: fused kernels are bf16 only");
   return RP_OK;
 }

@@ -74,6 +74,10 @@ int check_desc(const rp_module_desc& m) {
   if (m.drop_enabled && !m.layer_seeds) return set_error(RP_ERR_INVALID, "module: dropout needs layer_seeds");
   if (m.n_heads < 0 || (m.n_heads > 0 && (m.d % m.n_heads || m.M < 0 || m.mem_len < 0 || m.mem_len > m.M)))
     return set_error(RP_ERR_DIMENSION, "module: bad Transformer-XL shape");
+  if (m.dtype == RP_BF16 && (m.d % 8 || (m.n_blocks > 0 && m.f % 8) || (m.n_heads > 0 && (m.d / m.n_heads) % 8)))
+    return set_error(RP_ERR_DIMENSION,
+                     "module: the composite takes dense bf16 rows (d, d_ff, head dim multiples of 8); "
+                     "pitched rows go through the op-level entry points");
   return RP_OK;
 }
 

@@ -402,11 +402,12 @@ template <typename T, int NPL>
 __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict__ x, const float* __restrict__ g,
                                                               const float* __restrict__ b, T* __restrict__ y,
                                                               float* __restrict__ mean, float* __restrict__ rstd,
-                                                              int64_t rows, int d, int32_t* flag) {
+                                                              int64_t rows, int d, int32_t* flag, int64_t ldx,
+                                                              int64_t ldy) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
-  const T* xr = x + row * d;
+  const T* xr = x + row * ldx;
   float v[NPL];
   float s = 0.f;
   bool finite = true;
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const T* __restrict
   }
   q = warp_sum(q);
   const float rs = rsqrtf(q / d + kLnEps);
-  T* yr = y + row * d;
+  T* yr = y + row * ldy;
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int j = lane + 32 * i;
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
     const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
-    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d, int64_t ldx, int64_t ldm) {
   __shared__ float red[kRowWarps][2][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float acc_g[NPL], acc_b[NPL], gv[NPL];
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
     for (int i = 0; i < NPL; ++i) {
       const int j = lane + 32 * i;
       if (j < d) {
-        xh[i] = (to_f(x[row * d + j]) - mu) * rs;
+        xh[i] = (to_f(x[row * ldx + j]) - mu) * rs;
         dyv[i] = dy[row * d + j];
       } else {
         xh[i] = dyv[i] = 0.f;
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
         if (dx_masked) {
           float mo = o;
           if (drop_on) mo = dropout_keep(seed, (uint64_t)row * d + j, thr) ? o * scale : 0.f;
-          dx_masked[row * d + j] = from_f<T>(mo);
+          dx_masked[row * ldm + j] = from_f<T>(mo);
         }
       }
     }
@@ -580,7 +581,7 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, int64_t rows, int
 template <typename T>
 __global__ void mask_grad_kernel(const float* __restrict__ g, T* __restrict__ out, int64_t rows, int d,
                                  uint64_t seed, uint64_t pos0, uint64_t thr, float scale, int drop_on,
-                                 float* __restrict__ part) {
+                                 float* __restrict__ part, int64_t ldo) {
   const int64_t j = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (j >= d) return;
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
@@ -589,7 +590,7 @@ __global__ void mask_grad_kernel(const float* __restrict__ g, T* __restrict__ ou
   for (int64_t r = r0; r < r1; ++r) {
     float v = g[r * d + j];
     if (drop_on) v = dropout_keep(seed, pos0 + (uint64_t)r * d + j, thr) ? v * scale : 0.f;
-    out[r * d + j] = from_f<T>(v);
+    out[r * ldo + j] = from_f<T>(v);
     s += v;
   }
   if (part) part[(int64_t)blockIdx.x * d + j] = s;
@@ -744,9 +745,12 @@ inline int ng_for(int64_t d) {
 }
 
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
-                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st) {
+                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st, int64_t ldx, int64_t ldy) {
   if (rows == 0) return RP_OK;
-  if (const int ng = ng_for(d)) {
+  if (ldx <= 0) ldx = d;
+  if (ldy <= 0) ldy = d;
+  const bool pitched = ldx != d || ldy != d;  // row pitches wider than d: the scalar kernel
+  if (const int ng = pitched ? 0 : ng_for(d)) {
     RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_fwd_v4_kernel<T, NG>, row_blocks(rows), kRowThreads, 0, st, 
                                                     (const T*)x, g, b, (T*)y, mean, rstd, rows, (int)d, flag)));
     return check_launch("layernorm_fwd");
@@ -754,20 +758,24 @@ int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void
   const int npl = npl_for(d);
   RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, ln_fwd_kernel<T, NPL><<<row_blocks(rows), kRowThreads, 0, st>>>(
                                                     (const T*)x, g, b, (T*)y, mean, rstd,
-                                                    rows, (int)d, flag)));
+                                                    rows, (int)d, flag, ldx, ldy)));
   return check_launch("layernorm_fwd");
 }
 
 int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
                   const float* resid_grad, float* dx, void* dx_masked, uint64_t seed, uint64_t thr, float scale,
-                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st) {
+                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st, int64_t ldx,
+                  int64_t ldm) {
   if (rows == 0) return RP_OK;
+  if (ldx <= 0) ldx = d;
+  if (ldm <= 0) ldm = d;
+  const bool pitched = ldx != d || ldm != d;
   const int nb = ln_bwd_blocks(rows);
   // warps per row for d > 256 (RP_LN_SPLIT: 1 = one warp per row).  Measured
   // (tools/ln_bwd_bench.py): d 1024 two warps 106 -> 64 us (four: 70);
   // d 512 four warps 57 -> 47 us at 22528 rows, 29 -> 23 us at 8192; d 400 27 -> 23 us
   static const int split_env = getenv("RP_LN_SPLIT") ? atoi(getenv("RP_LN_SPLIT")) : -1;
-  const int ngd = ng_for(d);
+  const int ngd = pitched ? 0 : ng_for(d);
   int split = split_env >= 0 ? split_env : (ngd == 8 ? 2 : ngd == 4 ? 4 : 1);
   if (ngd < 4) split = 1;
 #define RP_LN_SPLIT_LAUNCH(NGV, PV)                                                                              \
@@ -780,7 +788,7 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
   if (ngd == 4 && split == 2) { RP_LN_SPLIT_LAUNCH(2, 2); }
   if (ngd == 4 && split == 4) { RP_LN_SPLIT_LAUNCH(1, 4); }
 #undef RP_LN_SPLIT_LAUNCH
-  if (const int ng = ng_for(d)) {
+  if (const int ng = ngd) {
     RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st,
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,
                                                     seed, thr, scale, drop_on, part_g, part_b, rows, (int)d)));
@@ -790,7 +798,7 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
   RP_DTYPE_DISPATCH(dtype, RP_NPL_DISPATCH(npl, ln_bwd_kernel<T, NPL><<<nb, kRowThreads, 0, st>>>(
                                                     dy, (const T*)x, mean, rstd, g, resid_grad, dx,
                                                     (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b,
-                                                    rows, (int)d)));
+                                                    rows, (int)d, ldx, ldm)));
   return check_launch("layernorm_bwd");
 }
 
@@ -818,6 +826,9 @@ int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st) {
 int mask_grad_blocks(int64_t rows, int64_t d) {
   return ng_for(d) ? ln_bwd_blocks(rows) : colsum_blocks(rows);
 }
+int mask_grad_blocks_ld(int64_t rows, int64_t d, int64_t ldo) {
+  return (ldo <= 0 || ldo == d) ? mask_grad_blocks(rows, d) : colsum_blocks(rows);
+}
 
 int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 128)); }
 
@@ -829,9 +840,10 @@ int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t
 }
 
 int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
-              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st) {
+              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st, int64_t ldo) {
   if (d == 0) return RP_OK;
-  if (const int ng = ng_for(d)) {
+  if (ldo <= 0) ldo = d;
+  if (const int ng = ldo == d ? ng_for(d) : 0) {
     RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(mask_grad_v4_kernel<T, NG>, ln_bwd_blocks(rows), kRowThreads, 0, st, 
                                                     g, (T*)out, rows, (int)d, seed, pos0, thr, scale, drop_on, part)));
     return check_launch("mask_grad");
@@ -840,7 +852,7 @@ int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uin
   // rp_mask_grad_blocks(rows, d) to the finish
   dim3 grid(colsum_blocks(rows), (unsigned)((d + 127) / 128));
   RP_DTYPE_DISPATCH(dtype, mask_grad_kernel<T><<<grid, 128, 0, st>>>(g, (T*)out, rows, (int)d, seed, pos0, thr,
-                                                                     scale, drop_on, part));
+                                                                     scale, drop_on, part, ldo));
   return check_launch("mask_grad");
 }
 

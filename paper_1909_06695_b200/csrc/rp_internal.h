@@ -42,11 +42,14 @@ int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, in
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);
 
+// ldx / ldy / ldm / ldo: row pitches in elements (0 = d); a pitch wider than d
+// (d not a multiple of 8: bf16 rows padded to 16 bytes) takes the scalar kernels
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
-                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st);
+                  int64_t rows, int64_t d, int32_t* flag, cudaStream_t st, int64_t ldx = 0, int64_t ldy = 0);
 int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
                   const float* resid_grad, float* dx, void* dx_masked, uint64_t seed, uint64_t thr, float scale,
-                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st);
+                  int drop_on, float* part_g, float* part_b, int64_t rows, int64_t d, cudaStream_t st,
+                  int64_t ldx = 0, int64_t ldm = 0);
 int ln_bwd_blocks(int64_t rows);
 int colsum_blocks(int64_t rows);
 int mask_grad_blocks(int64_t rows, int64_t d);
@@ -67,18 +70,20 @@ struct ColsumJobs {
 // up to kMaxColsumJobs colsum_finish operations in one launch (bitwise equal)
 int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st);
 int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uint64_t seed, uint64_t pos0,
-              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st);
+              uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st, int64_t ldo = 0);
+int mask_grad_blocks_ld(int64_t rows, int64_t d, int64_t ldo);
 int softmax_causal(int dtype, const float* s, void* p, int64_t rows, int64_t Tn, int64_t ld, cudaStream_t st);
 int softmax_bwd(int dtype, const float* gp, const void* p, void* gs, float scale, int64_t rows, int64_t Tn,
                 int64_t ld, cudaStream_t st);
+// ld: row pitch of V, pos and out (0 = d)
 int embed_fwd(int dtype, const int64_t* tok, const void* V, const void* pos, void* out, int64_t B, int64_t Tn,
               int64_t d, int64_t vocab, uint64_t seed, uint64_t thr, float scale, int drop_on, int32_t* flag,
-              cudaStream_t st);
+              cudaStream_t st, int64_t ld = 0);
 int64_t embed_bwd_workspace_bytes(int64_t n_tokens, int64_t d);
 int embed_bwd(const float* g, const int64_t* tok, int64_t B, int64_t Tn, int64_t Tmax, int64_t d, int64_t vocab,
               uint64_t seed,
               uint64_t thr, float scale, int drop_on, float* gpos, float* emb, float beta, void* workspace,
-              cudaStream_t st);
+              cudaStream_t st, int64_t ld_out = 0);  // ld_out: row pitch of gpos and emb
 int ce_finish(const float* partial, int ntiles, const float* zy, const int64_t* tgt, int64_t vocab, int64_t rows,
               float* lse, float* loss_rows, float* loss, double* loss64, int32_t* flag, cudaStream_t st);
 int adam_step(float* w, const float* g, float* m, float* v, void* copy, int copy_dtype, int64_t n, float lr, float b1,
@@ -93,14 +98,16 @@ int axpy(float* y, const float* x, float alpha, int64_t n, cudaStream_t st);
 int gelu_fwd(int dtype, const void* z, void* y, int64_t n, cudaStream_t st);
 int sq_norm(const float* x, int64_t n, double* part, double* out, int accumulate, cudaStream_t st);
 
+// ldq: row pitch of qkv / g_qkv (0 = 3*H*dh); ldh: row pitch of the
+// head-major [H, rows, dh] tensors (0 = dh)
 int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, void* qu, void* qv, void* kh, void* vh,
-                 int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st);
+                 int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq = 0, int64_t ldh = 0);
 int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, void* dst, int64_t rows, int H, int dh,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t ldh = 0);
 int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t ldh = 0);
 int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
-                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st);
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq = 0);
 int xl_softmax_fwd(int dtype, const float* ac, const float* bd, int64_t lds, void* p, int64_t ldp, int64_t rows,
                    int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st);
 int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64_t ldp, void* gac, void* gbd,

@@ -140,6 +140,92 @@ __global__ void merge_heads_kernel(const S* __restrict__ src, D* __restrict__ ds
   }
 }
 
+// Scalar forms of the head split / merge kernels for any head dim and row
+// pitches (d or the head dim not a multiple of 8, e.g. BASELINE configs[3]:
+// d 410 = 10 heads x 41; bf16 rows are padded to 16-byte pitches, so row r
+// starts at r * ld).  One thread per element.
+template <typename T>
+__global__ void split_qkv_scalar_kernel(const T* __restrict__ qkv, const float* __restrict__ u,
+                                        const float* __restrict__ v, T* __restrict__ qu, T* __restrict__ qv,
+                                        T* __restrict__ kh, T* __restrict__ vh, int B, int Tn, int M, int H, int dh,
+                                        int64_t ldq, int64_t ldh) {
+  const int Kl = M + Tn, d = H * dh;
+  XL_GRID_LOOP(e, (int64_t)H * B * Kl * dh) {
+    const int c = (int)(e % dh);
+    const int64_t hbj = e / dh;
+    const int j = (int)(hbj % Kl);
+    const int hb = (int)(hbj / Kl);
+    const int b = hb % B, h = hb / B;
+    const T* src = qkv + key_row(b, j, B, Tn, M) * ldq + h * dh + c;
+    kh[hbj * ldh + c] = src[d];
+    vh[hbj * ldh + c] = src[2 * d];
+    if (j >= M) {
+      const float x = to_f(src[0]);
+      const int64_t o = ((int64_t)hb * Tn + (j - M)) * ldh + c;
+      qu[o] = from_f<T>(x + u[h * dh + c]);
+      qv[o] = from_f<T>(x + v[h * dh + c]);
+    }
+  }
+}
+
+template <typename S, typename D>
+__global__ void split_heads_scalar_kernel(const S* __restrict__ src, int64_t ld, D* __restrict__ dst, int64_t rows,
+                                          int H, int dh, int64_t ldh) {
+  XL_GRID_LOOP(e, rows * H * dh) {
+    const int c = (int)(e % dh);
+    const int64_t hr = e / dh;
+    const int64_t r = hr % rows;
+    const int h = (int)(hr / rows);
+    dst[hr * ldh + c] = from_f<D>(to_f(src[r * ld + h * dh + c]));
+  }
+}
+
+template <typename S, typename D>
+__global__ void merge_heads_scalar_kernel(const S* __restrict__ src, D* __restrict__ dst, int64_t ld, int64_t rows,
+                                          int H, int dh, int64_t ldh) {
+  const int d = H * dh;
+  XL_GRID_LOOP(e, rows * d) {
+    const int64_t r = e / d;
+    const int col = (int)(e % d);
+    const int h = col / dh, c = col % dh;
+    dst[r * ld + col] = from_f<D>(to_f(src[((int64_t)h * rows + r) * ldh + c]));
+  }
+}
+
+template <typename T>
+__global__ void merge_grads_scalar_kernel(const float* __restrict__ gqu, const float* __restrict__ gqv,
+                                          const float* __restrict__ gkh, const float* __restrict__ gvh,
+                                          T* __restrict__ gqkv, int B, int Tn, int M, int H, int dh, int64_t ldq) {
+  const int Kl = M + Tn, d = H * dh;
+  const int64_t BM = (int64_t)B * M;
+  XL_GRID_LOOP(e, (int64_t)B * Kl * 3 * d) {
+    const int64_t row = e / (3 * d);
+    const int col = (int)(e % (3 * d));
+    const int part = col / d;
+    const int h = (col % d) / dh, c = col % dh;
+    int b, j;
+    if (row < BM) {
+      b = (int)(row / M);
+      j = (int)(row % M);
+    } else {
+      b = (int)((row - BM) / Tn);
+      j = M + (int)((row - BM) % Tn);
+    }
+    float g;
+    if (part == 0) {
+      if (j < M) {
+        g = 0.f;
+      } else {
+        const int64_t o = (((int64_t)h * B + b) * Tn + (j - M)) * dh + c;
+        g = gqu[o] + gqv[o];
+      }
+    } else {
+      g = (part == 1 ? gkh : gvh)[(((int64_t)h * B + b) * Kl + j) * dh + c];
+    }
+    gqkv[row * ldq + col] = from_f<T>(g);
+  }
+}
+
 // g_qkv rows in the xa layout: q columns = dQu + dQv (zero on memory rows),
 // k / v columns from the head-major key gradients.  unit = 8 columns of a row.
 template <typename T>
@@ -386,8 +472,16 @@ inline int npl_for(int64_t n) {
 inline int blocks8(int64_t units) { return blocks_for(units); }
 
 int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, void* qu, void* qv, void* kh, void* vh,
-                 int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st) {
-  if (dh % 8) return set_error(RP_ERR_DIMENSION, "xl_split_qkv: head dim must be a multiple of 8");
+                 int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq, int64_t ldh) {
+  if (ldq <= 0) ldq = 3 * (int64_t)H * dh;
+  if (ldh <= 0) ldh = dh;
+  if (dh % 8 || ldq != 3 * (int64_t)H * dh || ldh != dh) {
+    const int64_t ne = (int64_t)H * B * (M + Tn) * dh;
+    if (ne == 0) return RP_OK;
+    XL_DTYPE(dtype, split_qkv_scalar_kernel<T><<<blocks8(ne), kThreads, 0, st>>>(
+                        (const T*)qkv, u, v, (T*)qu, (T*)qv, (T*)kh, (T*)vh, (int)B, (int)Tn, (int)M, H, dh, ldq, ldh));
+    return check_launch("xl_split_qkv");
+  }
   const int64_t n = (int64_t)H * B * (M + Tn) * (dh / 8);
   if (n == 0) return RP_OK;
   XL_DTYPE(dtype, split_qkv_kernel<T><<<blocks8(n), kThreads, 0, st>>>(
@@ -415,8 +509,15 @@ int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, voi
   }
 
 int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, void* dst, int64_t rows, int H, int dh,
-                   cudaStream_t st) {
-  if (dh % 8 || ld % 8) return set_error(RP_ERR_DIMENSION, "xl_split_heads: head dim and ld must be multiples of 8");
+                   cudaStream_t st, int64_t ldh) {
+  if (ldh <= 0) ldh = dh;
+  if (dh % 8 || ld % 8 || ldh != dh) {
+    const int64_t ne = rows * H * dh;
+    if (ne == 0) return RP_OK;
+    XL_PAIR(src_dtype, dst_dtype, (split_heads_scalar_kernel<S, D><<<blocks8(ne), kThreads, 0, st>>>(
+                                      (const S*)src, ld, (D*)dst, rows, H, dh, ldh)));
+    return check_launch("xl_split_heads");
+  }
   const int64_t n = rows * H * (dh / 8);
   if (n == 0) return RP_OK;
   const int g = blocks8(n);
@@ -426,8 +527,15 @@ int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, vo
 }
 
 int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
-                   cudaStream_t st) {
-  if (dh % 8 || ld % 8) return set_error(RP_ERR_DIMENSION, "xl_merge_heads: head dim and ld must be multiples of 8");
+                   cudaStream_t st, int64_t ldh) {
+  if (ldh <= 0) ldh = dh;
+  if (dh % 8 || ld % 8 || ldh != dh) {
+    const int64_t ne = rows * H * dh;
+    if (ne == 0) return RP_OK;
+    XL_PAIR(src_dtype, dst_dtype, (merge_heads_scalar_kernel<S, D><<<blocks8(ne), kThreads, 0, st>>>(
+                                      (const S*)src, (D*)dst, ld, rows, H, dh, ldh)));
+    return check_launch("xl_merge_heads");
+  }
   const int64_t n = rows * H * (dh / 8);
   if (n == 0) return RP_OK;
   const int g = blocks8(n);
@@ -437,8 +545,15 @@ int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int
 }
 
 int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
-                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st) {
-  if (dh % 8) return set_error(RP_ERR_DIMENSION, "xl_merge_grads: head dim must be a multiple of 8");
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq) {
+  if (ldq <= 0) ldq = 3 * (int64_t)H * dh;
+  if (dh % 8 || ldq != 3 * (int64_t)H * dh) {
+    const int64_t ne = B * (M + Tn) * 3 * (int64_t)H * dh;
+    if (ne == 0) return RP_OK;
+    XL_DTYPE(dtype, merge_grads_scalar_kernel<T><<<blocks8(ne), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv,
+                                                                                  (int)B, (int)Tn, (int)M, H, dh, ldq));
+    return check_launch("xl_merge_grads");
+  }
   const int64_t n = B * (M + Tn) * 3 * (int64_t)H * dh / 8;
   if (n == 0) return RP_OK;
   XL_DTYPE(dtype, merge_grads_kernel<T><<<blocks8(n), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv, (int)B,

@@ -125,7 +125,7 @@ def packet_grad_sq_norm(packet):
         for key in sorted(grads):
             g = grads[key]
             ops.sq_norm(g.contiguous(), part, out, accumulate=True)
-    ops.sq_norm(packet.emb_grad, part, out, accumulate=True)
+    ops.sq_norm(packet.emb_grad.contiguous(), part, out, accumulate=True)
     return float(out.item())
 
 

@@ -60,6 +60,21 @@ class Dropout:
         return ((drop[0] + positions * _GOLDEN) & _MASK64,) + tuple(drop[1:])
 
 
+def pad_cols(cols, dtype):
+    """Row pitch of a [rows, cols] matrix: bf16 rows are padded to 16 bytes
+    (the TMA row-pitch rule) when cols is not a multiple of 8 -- BASELINE
+    configs[3]'s d 410, heads of 41 and d_ff 2100."""
+    return _pad8(cols) if dtype == torch.bfloat16 and cols % 8 else cols
+
+
+def empty_rows(*shape, dtype, device):
+    """torch.empty(shape) whose last-dim rows sit at pad_cols pitch (a view)."""
+    c = shape[-1]
+    cp = pad_cols(c, dtype)
+    t = torch.empty(*shape[:-1], cp, dtype=dtype, device=device)
+    return t if cp == c else t[..., :c]
+
+
 class Workspace:
     """Named scratch buffers reused across calls (one per module and role)."""
 
@@ -74,6 +89,13 @@ class Workspace:
             t = torch.empty(math.prod(shape), dtype=dtype, device=self.device)
             self._bufs[name] = t
         return t[: math.prod(shape)].view(shape)
+
+    def get_rows(self, name, shape, dtype):
+        """Like get, with the last-dim rows at pad_cols pitch."""
+        c = shape[-1]
+        cp = pad_cols(c, dtype)
+        t = self.get(name, tuple(shape[:-1]) + (cp,), dtype)
+        return t if cp == c else t[..., :c]
 
     def nbytes(self):
         return sum(t.numel() * t.element_size() for t in self._bufs.values())

@@ -125,16 +125,40 @@ def _dtype_of(name):
 
 
 class LayerParams:
-    """fp32 master + gradient + snapshot ring of one layer."""
+    """fp32 master + gradient + snapshot ring of one layer.
+
+    Flat buffers: the vectors, then the matrices row-major.  A matrix whose
+    compute-dtype rows would not be 16-byte multiples (bf16, cols % 8 != 0:
+    BASELINE configs[3]'s d 410, d_ff 2100) keeps its rows at LY.pad_cols
+    pitch in EVERY buffer (master, gradient, moments, ring), so the optimizer
+    and the casts stay one flat elementwise pass; the pad columns are zero
+    and stay zero (nothing writes them, and zero weight + zero gradient is a
+    fixed point of SGD and Adam).  Every vector and matrix starts on a
+    64-element boundary (256 bytes fp32), so each view is as aligned as a
+    fresh allocation whatever the widths (d 410 vectors would otherwise leave
+    the matrices 8-byte aligned)."""
+
+    ALIGN = 64
 
     def __init__(self, layer, device, cdtype):
         self.layer, self.device, self.cdtype = layer, device, cdtype
         vec, mat = layer.specs()
-        self.n_vec = sum(math.prod(s) for _, s in vec)
-        self.n_mat = sum(math.prod(s) for _, s in mat)
+        up = lambda n: -(-n // self.ALIGN) * self.ALIGN  # noqa: E731
+        self._mat_pitch = [LY.pad_cols(s[-1], cdtype) for _, s in mat]
+        self._vec_off, off = [], 0
+        for _, s in vec:
+            self._vec_off.append(off)
+            off = up(off + math.prod(s))
+        self.n_vec = off
+        self._mat_off, off = [], 0
+        for (_, s), pc in zip(mat, self._mat_pitch):
+            self._mat_off.append(off)
+            off = up(off + s[0] * pc)
+        self.n_mat = off
         n = self.n_vec + self.n_mat
         self.master = torch.zeros(n, dtype=torch.float32, device=device)
         self.grad = torch.zeros(n, dtype=torch.float32, device=device)
+        self.flat_master, self.flat_grad = self.master, self.grad
         self.m = self.v = None
         self._vec_specs, self._mat_specs = vec, mat
         self.P = self._carve(self.master, torch.float32, torch.float32)  # internal names
@@ -148,15 +172,16 @@ class LayerParams:
         out = {}
         if vec_flat is None:
             vec_flat, mat_flat = flat[: self.n_vec], flat[self.n_vec:]
-        off = 0
-        for name, shape in self._vec_specs:
+        for (name, shape), off in zip(self._vec_specs, self._vec_off):
             out[name] = vec_flat[off: off + math.prod(shape)].view(shape)
-            off += math.prod(shape)
-        off = 0
-        for name, shape in self._mat_specs:
-            out[name] = mat_flat[off: off + math.prod(shape)].view(shape)
-            off += math.prod(shape)
+        for name, off, r, c, pc in self.mat_blocks():
+            out[name] = mat_flat[off: off + r * pc].view(r, pc)[:, :c]
         return out
+
+    def mat_blocks(self):
+        """(name, offset in the matrix part, rows, cols, row pitch) per matrix."""
+        return [(name, off, r, c, pc) for (name, (r, c)), pc, off in zip(self._mat_specs, self._mat_pitch,
+                                                                          self._mat_off)]
 
     def _public(self, D):
         if self.layer.kind not in ("block", "xl_block"):
@@ -172,7 +197,7 @@ class LayerParams:
         self.ring = []
         for _ in range(capacity):
             vec = torch.empty(self.n_vec, dtype=torch.float32, device=self.device)
-            mat = torch.empty(self.n_mat, dtype=self.cdtype, device=self.device)
+            mat = torch.zeros(self.n_mat, dtype=self.cdtype, device=self.device)
             self.ring.append((vec, mat, self._carve(None, None, None, vec, mat)))
         self.ring_step = [None] * capacity
 
@@ -214,14 +239,23 @@ class TiedMatrix:
 
     def __init__(self, vocab, d, device, cdtype):
         self.vocab, self.d, self.device, self.cdtype = vocab, d, device, cdtype
-        self.master = torch.zeros(vocab, d, dtype=torch.float32, device=device)
-        self.grad = torch.zeros(vocab, d, dtype=torch.float32, device=device)
+        # rows at LY.pad_cols pitch in every buffer, as LayerParams
+        self.pitch = pd = LY.pad_cols(d, cdtype)
+        self.flat_master = torch.zeros(vocab * pd, dtype=torch.float32, device=device)
+        self.flat_grad = torch.zeros(vocab * pd, dtype=torch.float32, device=device)
+        self.flat_compute = (self.flat_master if cdtype == torch.float32
+                             else torch.zeros(vocab * pd, dtype=cdtype, device=device))
+        self.master, self.grad, self.compute = (self.rows(t) for t in (self.flat_master, self.flat_grad,
+                                                                        self.flat_compute))
         self.m = self.v = None
-        self.compute = self.master if cdtype == torch.float32 else torch.empty(vocab, d, dtype=cdtype, device=device)
+
+    def rows(self, flat):
+        """The logical [vocab, d] view of a flat buffer in this layout."""
+        return flat.view(self.vocab, self.pitch)[:, : self.d]
 
     def refresh(self):
-        if self.compute is not self.master:
-            ops.cast(self.master, self.compute)
+        if self.flat_compute is not self.flat_master:
+            ops.cast(self.flat_master, self.flat_compute)
 
 
 class LayerStack:
@@ -309,8 +343,12 @@ def build_xl_stack(vocab_size, model_dim, ffn_dim, n_blocks, seq_len, dropout_p,
                    dtype="bf16", device=None, cutoffs=None, activation="relu"):
     """The Transformer-XL language model: the reference embedding and tied
     head around `n_blocks` XL blocks with `mem_len` memory rows each."""
-    if model_dim % 8 or ffn_dim % 8 or (model_dim // n_heads) % 8:
-        raise DimensionError("model_dim, ffn_dim and the head dim must be multiples of 8 (TMA 16-byte rows)")
+    # widths that are not multiples of 8 (BASELINE configs[3]: d 410, 10 heads x 41,
+    # d_ff 2100) keep every bf16 row at a 16-byte pitch (LY.pad_cols) through the
+    # op-level path; the full-vocabulary head is a dense-row C-ABI composite, so
+    # such widths take the adaptive head (configs[3]'s own head)
+    if (model_dim % 8 or ffn_dim % 8 or (model_dim // n_heads) % 8) and not cutoffs:
+        raise DimensionError("widths that are not multiples of 8 need the adaptive head (cutoffs)")
     if not 0 <= mem_len <= seq_len:
         raise DimensionError("mem_len must be in [0, seq_len]")
     rt = Runtime.get(device)
@@ -458,8 +496,8 @@ def measure_layer_costs(stack, batch_x, dropout_seed=0, repeats=3):
     tied = stack.tied_store
     d, cdt = tied.d, stack.cdtype
     ws = LY.Workspace(dev)
-    act = torch.empty(Nt, d, dtype=cdt, device=dev)
-    out = torch.empty_like(act)
+    act = LY.empty_rows(Nt, d, dtype=cdt, device=dev)
+    out = LY.empty_rows(Nt, d, dtype=cdt, device=dev)
     g_out = torch.ones(Nt, d, dtype=torch.float32, device=dev)
     g_in = torch.empty_like(g_out)
     targets = torch.zeros(Nt, dtype=torch.int64, device=dev)
@@ -561,10 +599,10 @@ class _Arena:
                 self.acts.append(tp.x)  # the upstream writes straight into [memory; x]
             else:
                 tp = LY.BlockTape(B, T, d, layer.ffn_dim, cdt, dev, layer.activation)
-                self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
+                self.acts.append(LY.empty_rows(Nt, d, dtype=cdt, device=dev))
             self.tapes.append(tp)
         if module.has_projection:
-            self.acts.append(torch.empty(Nt, d, dtype=cdt, device=dev))
+            self.acts.append(LY.empty_rows(Nt, d, dtype=cdt, device=dev))
         self.head = LY.HeadState(Nt, dev) if module.has_projection else None
         last = module.layers[-1]
         self.adaptive = (AdaptiveHead(last.vocab_size, d, last.cutoffs, dev, cdt)
@@ -893,9 +931,9 @@ class ModuleState:
             emb_alpha, emb_beta = 1.0, 1.0
             vo_buf = vi_buf = None
             if self.has_projection:
-                vo_buf = torch.empty(self.vocab, d, dtype=torch.float32, device=self.device)
+                vo_buf = self._tied_buf()
             if self.has_embedding:
-                vi_buf = torch.zeros(self.vocab, d, dtype=torch.float32, device=self.device)
+                vi_buf = self._tied_buf()
             tied_out = {"Vi": vi_buf, "Vo": vo_buf}
         else:
             emb_alpha, emb_beta, emb_grad = emb
@@ -951,6 +989,10 @@ class ModuleState:
             return g_in, self.grad_views, tied_out, loss
         return g.clone().view(B, T, d), self.grad_views, tied_out, loss
 
+    def _tied_buf(self):
+        """A zeroed fp32 [vocab, d] gradient in the tied matrix's row layout."""
+        return self.tied.rows(torch.zeros_like(self.tied.flat_grad))
+
     def zero_grads(self):
         for st in self.storage:
             st.grad.zero_()
@@ -960,7 +1002,7 @@ class ModuleState:
         """A second gradient buffer of the layer (row blocks j > 0 write here,
         then it is added onto st.grad)."""
         if getattr(st, "_gscratch", None) is None or st._gscratch.numel() != st.grad.numel():
-            st._gscratch = torch.empty_like(st.grad)
+            st._gscratch = torch.zeros_like(st.grad)  # pad columns stay zero
             st._Gscratch = st._carve(st._gscratch, torch.float32, torch.float32)
         return st._Gscratch
 
@@ -993,10 +1035,8 @@ class ModuleState:
         tied_out = {"Vi": None, "Vo": None}
         if emb is None:
             emb_alpha, emb_beta = 1.0, 1.0
-            vo_buf = torch.empty(self.vocab, d, dtype=torch.float32, device=self.device) \
-                if self.has_projection else None
-            vi_buf = torch.zeros(self.vocab, d, dtype=torch.float32, device=self.device) \
-                if self.has_embedding else None
+            vo_buf = self._tied_buf() if self.has_projection else None
+            vi_buf = self._tied_buf() if self.has_embedding else None
             tied_out = {"Vi": vi_buf, "Vo": vo_buf}
         else:
             emb_alpha, emb_beta, emb_grad = emb

@@ -267,11 +267,32 @@ def _dtc(t):
     return _DT[t.dtype]
 
 
+def _pitch(t):
+    """Row pitch (elements) of a row-major matrix view whose rows may be padded
+    (d not a multiple of 8: 16-byte bf16 rows); checks the layout the kernels assume."""
+    if t is None:
+        return 0
+    if t.dim() >= 2 and t.stride(-1) == 1:
+        ld = t.stride(-2)
+        # leading dims must fold onto rows: stride(i) == size(i+1) * stride(i+1)
+        for i in range(t.dim() - 2):
+            if t.stride(i) != t.shape[i + 1] * t.stride(i + 1):
+                raise DimensionError("row-padded tensors must be dense above the row dimension")
+        return ld
+    if t.is_contiguous():
+        return t.shape[-1]
+    raise DimensionError("kernels take row-major tensors (unit column stride)")
+
+
+def _rows(t):
+    return t.numel() // t.shape[-1]
+
+
 def layernorm_fwd(x, gain, bias, y, mean, rstd, flag=None):
-    rows, d = x.numel() // x.shape[-1], x.shape[-1]
+    rows, d = _rows(x), x.shape[-1]
     _count(1)
     N.check(N.lib().rp_layernorm_fwd(_dtc(x), _ptr(x), _ptr(gain), _ptr(bias), _ptr(y), _ptr(mean), _ptr(rstd),
-                                     rows, d, _ptr(flag), _stream()), "layernorm_fwd")
+                                     rows, d, _pitch(x), _pitch(y), _ptr(flag), _stream()), "layernorm_fwd")
 
 
 def layernorm_bwd_blocks(rows):
@@ -279,12 +300,16 @@ def layernorm_bwd_blocks(rows):
 
 
 def layernorm_bwd(dy, x, mean, rstd, gain, dx, part_g, part_b, resid_grad=None, dx_masked=None, dropout=None):
-    rows, d = x.numel() // x.shape[-1], x.shape[-1]
+    rows, d = _rows(x), x.shape[-1]
+    for t in (dy, dx, resid_grad):
+        if t is not None and not t.is_contiguous():
+            raise DimensionError("layernorm_bwd: fp32 rows must be contiguous")
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
     _count(1)
     N.check(N.lib().rp_layernorm_bwd(_dtc(x), _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gain),
                                      _ptr(resid_grad), _ptr(dx), _ptr(dx_masked), seed, thr, scale,
-                                     int(dropout is not None), _ptr(part_g), _ptr(part_b), rows, d, _stream()),
+                                     int(dropout is not None), _ptr(part_g), _ptr(part_b), rows, d, _pitch(x),
+                                     _pitch(dx_masked), _stream()),
             "layernorm_bwd")
 
 
@@ -292,8 +317,8 @@ def colsum_blocks(rows):
     return N.lib().rp_colsum_blocks(rows)
 
 
-def mask_grad_blocks(rows, d):
-    return N.lib().rp_mask_grad_blocks(rows, d)
+def mask_grad_blocks(rows, d, ld_out=0):
+    return N.lib().rp_mask_grad_blocks_ld(rows, d, ld_out)
 
 
 def colsum_partial(x, part):
@@ -321,11 +346,11 @@ def colsum_finish(part, nblk, out):
 
 
 def mask_grad(g, out, pos0, dropout, part):
-    rows, d = g.numel() // g.shape[-1], g.shape[-1]
+    rows, d = _rows(g), g.shape[-1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
     _count(1)
     N.check(N.lib().rp_mask_grad(_dtc(out), _ptr(g), _ptr(out), rows, d, seed, pos0, thr, scale,
-                                 int(dropout is not None), _ptr(part), _stream()), "mask_grad")
+                                 int(dropout is not None), _ptr(part), _pitch(out), _stream()), "mask_grad")
 
 
 def softmax_causal(scores, probs):
@@ -351,9 +376,12 @@ def softmax_bwd(grad_probs, probs, grad_scores, scale):
 
 def xl_split_qkv(qkv, u, v, qu, qv, kh, vh, B, T, M, H, dh):
     _require_cuda(qkv, u, v, qu, qv, kh, vh)
+    ldh = _pitch(qu)
+    if any(_pitch(t) != ldh for t in (qv, kh, vh)):
+        raise DimensionError("xl_split_qkv: the head tensors share one row pitch")
     _count(1)
     N.check(N.lib().rp_xl_split_qkv(_dtc(qkv), _ptr(qkv), _ptr(u), _ptr(v), _ptr(qu), _ptr(qv), _ptr(kh), _ptr(vh),
-                                    B, T, M, H, dh, _stream()), "xl_split_qkv")
+                                    B, T, M, H, dh, _pitch(qkv), ldh, _stream()), "xl_split_qkv")
 
 
 def xl_split_heads(src, dst, H, dh):
@@ -361,7 +389,7 @@ def xl_split_heads(src, dst, H, dh):
     rows = src.shape[0]
     _count(1)
     N.check(N.lib().rp_xl_split_heads(_dtc(src), _ptr(src), src.stride(0), _dtc(dst), _ptr(dst), rows, H, dh,
-                                      _stream()), "xl_split_heads")
+                                      _pitch(dst), _stream()), "xl_split_heads")
 
 
 def xl_merge_heads(src, dst, H, dh):
@@ -369,13 +397,16 @@ def xl_merge_heads(src, dst, H, dh):
     rows = dst.shape[0]
     _count(1)
     N.check(N.lib().rp_xl_merge_heads(_dtc(src), _ptr(src), _dtc(dst), _ptr(dst), dst.stride(0), rows, H, dh,
-                                      _stream()), "xl_merge_heads")
+                                      _pitch(src), _stream()), "xl_merge_heads")
 
 
 def xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh):
     _count(1)
+    for t in (g_qu, g_qv, g_kh, g_vh):
+        if not t.is_contiguous():
+            raise DimensionError("xl_merge_grads: fp32 head gradients must be contiguous")
     N.check(N.lib().rp_xl_merge_grads(_dtc(g_qkv), _ptr(g_qu), _ptr(g_qv), _ptr(g_kh), _ptr(g_vh), _ptr(g_qkv), B, T,
-                                      M, H, dh, _stream()), "xl_merge_grads")
+                                      M, H, dh, _pitch(g_qkv), _stream()), "xl_merge_grads")
 
 
 def xl_softmax_fwd(ac, bd, probs, T, M, mem_len, scale):
@@ -465,10 +496,13 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
 def gelu(z, y):
     """y = GELU(z) = 0.5 z (1 + erf(z / sqrt 2)) (same dtype and size)."""
     _require_cuda(z, y)
-    if z.dtype != y.dtype or z.numel() != y.numel() or not (z.is_contiguous() and y.is_contiguous()):
-        raise DimensionError("gelu takes two contiguous tensors of one dtype and size")
+    if z.dtype != y.dtype or z.shape != y.shape or _pitch(z) != _pitch(y):
+        raise DimensionError("gelu takes two tensors of one dtype, shape and row pitch")
+    # pitched rows (pad_cols): the elementwise pass runs over the padded extent
+    # (pad columns are never read by the GEMMs)
+    n = _rows(z) * _pitch(z) if z.dim() >= 2 else z.numel()
     _count(1)
-    N.check(N.lib().rp_gelu_fwd(_dtc(z), _ptr(z), _ptr(y), z.numel(), _stream()), "gelu")
+    N.check(N.lib().rp_gelu_fwd(_dtc(z), _ptr(z), _ptr(y), n, _stream()), "gelu")
 
 
 def axpy(y, x, alpha=1.0):
@@ -525,8 +559,11 @@ def embed_fwd(tokens, tied, pos, out, vocab, dropout=None, flag=None):
     d = tied.shape[1]
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
     _count(1)
+    ld = _pitch(out)
+    if _pitch(tied) != ld or _pitch(pos) != ld:
+        raise DimensionError("embed_fwd: V, the position table and the output share one row pitch")
     N.check(N.lib().rp_embed_fwd(_dtc(out), _ptr(tokens), _ptr(tied), _ptr(pos), _ptr(out), B, T, d, vocab, seed,
-                                 thr, scale, int(dropout is not None), _ptr(flag), _stream()), "embed_fwd")
+                                 thr, scale, int(dropout is not None), _ptr(flag), ld, _stream()), "embed_fwd")
 
 
 def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None):
@@ -535,10 +572,15 @@ def embed_bwd(grad, tokens, t_max, grad_pos, emb_grad, beta, work, dropout=None)
     seed, thr, scale = dropout if dropout is not None else (0, 0, 1.0)
     # ids outside [0, vocab) are skipped by the scatter (the forward flagged them)
     vocab = emb_grad.shape[0] if emb_grad is not None else 1
+    if not grad.is_contiguous():
+        raise DimensionError("embed_bwd: the gradient rows must be contiguous")
+    ld = _pitch(grad_pos) if grad_pos is not None else _pitch(emb_grad)
+    if emb_grad is not None and grad_pos is not None and _pitch(emb_grad) != ld:
+        raise DimensionError("embed_bwd: the position and tied gradients share one row pitch")
     _count(4)
     N.check(N.lib().rp_embed_bwd(_ptr(grad), _ptr(tokens), B, T, t_max, d, vocab, seed, thr, scale,
                                  int(dropout is not None), _ptr(grad_pos), _ptr(emb_grad), beta, _ptr(work),
-                                 _stream()), "embed_bwd")
+                                 ld, _stream()), "embed_bwd")
 
 
 def ce_finish(partial, target_logit, targets, vocab, lse, loss_rows, loss, loss64=None, flag=None):

@@ -72,15 +72,15 @@ class _Base:
     def apply_module(self, t, module):
         flag = module.runtime.flag
         for st, (vec_dst, mat_dst) in zip(module.storage, _targets(module, t)):
-            n = st.master.numel()
+            n = st.flat_master.numel()
             if n == 0:
                 continue
             self._update(t, st, 0, st.n_vec, vec_dst, flag)
             self._update(t, st, st.n_vec, n, mat_dst, flag)
 
     def apply_tied(self, t, store, flag):
-        copy = None if store.compute is store.master else store.compute
-        self._update(t, store, 0, store.master.numel(), copy, flag)
+        copy = None if store.flat_compute is store.flat_master else store.flat_compute
+        self._update(t, store, 0, store.flat_master.numel(), copy, flag)
 
 
 class SgdOptimizer(_Base):
@@ -91,7 +91,7 @@ class SgdOptimizer(_Base):
 
     def _update(self, t, st, lo, hi, dst, flag):
         if hi > lo:
-            ops.sgd_step(st.master[lo:hi], st.grad[lo:hi], dst, hi - lo, self.schedule.at(t), flag)
+            ops.sgd_step(st.flat_master[lo:hi], st.flat_grad[lo:hi], dst, hi - lo, self.schedule.at(t), flag)
 
     def state_arrays(self):
         return {}
@@ -113,8 +113,8 @@ class AdamOptimizer(_Base):
     @staticmethod
     def _moments(obj):
         if obj.m is None:
-            obj.m = torch.zeros_like(obj.master)
-            obj.v = torch.zeros_like(obj.master)
+            obj.m = torch.zeros_like(obj.flat_master)
+            obj.v = torch.zeros_like(obj.flat_master)
         return obj.m, obj.v
 
     def prepare(self, modules):
@@ -127,7 +127,7 @@ class AdamOptimizer(_Base):
             c1 = 1.0 - self.beta1 ** (t + 1)
             c2 = 1.0 - self.beta2 ** (t + 1)
             m, v = self._moments(st)
-            ops.adam_step(st.master[lo:hi], st.grad[lo:hi], m[lo:hi], v[lo:hi], dst, hi - lo, lr, self.beta1,
+            ops.adam_step(st.flat_master[lo:hi], st.flat_grad[lo:hi], m[lo:hi], v[lo:hi], dst, hi - lo, lr, self.beta1,
                           self.beta2, self.eps, c1, c2, flag)
 
     def bind(self, modules):
@@ -156,7 +156,7 @@ class AdamOptimizer(_Base):
         store = _tied_store(self._mods)
         if store is not None:
             mb, vb = self._moments(store)
-            out.append(("tied", mb, vb))
+            out.append(("tied", store.rows(mb), store.rows(vb)))
         return out
 
     def state_arrays(self):

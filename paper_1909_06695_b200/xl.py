@@ -33,7 +33,9 @@ def sinusoid(Kl, d, dtype, device):
     inv = 1.0 / (10000.0 ** (np.arange(0, d, 2, dtype=np.float64) / d))
     ang = dist[:, None] * inv[None, :]
     R = np.concatenate([np.sin(ang), np.cos(ang)], axis=1)
-    return torch.from_numpy(R).to(device=device, dtype=dtype)
+    out = LY.empty_rows(Kl, d, dtype=dtype, device=device)  # a GEMM operand: 16-byte rows
+    out.copy_(torch.from_numpy(R))
+    return out
 
 
 class XLTape:
@@ -44,7 +46,8 @@ class XLTape:
         self.activation = activation
         dh = d // H
         ldk = _pad8(Kl)
-        e = lambda *s: torch.empty(s, dtype=dtype, device=device)  # noqa: E731
+        # rows at 16-byte pitches for bf16 (LY.pad_cols: d 410, head dim 41, d_ff 2100)
+        e = lambda *s: LY.empty_rows(*s, dtype=dtype, device=device)  # noqa: E731
         f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
         self.B, self.T, self.M, self.H, self.dh, self.Kl, self.ldk = B, T, M, H, dh, Kl, ldk
         self.xa = e(B * Kl, d)            # [memory rows; current rows]
@@ -54,7 +57,7 @@ class XLTape:
         self.qu, self.qv = e(H, B * T, dh), e(H, B * T, dh)
         self.kh, self.vh = e(H, B * Kl, dh), e(H, B * Kl, dh)
         self.rh = e(H, Kl, dh)
-        self.probs_buf = e(H * B, T, ldk)
+        self.probs_buf = torch.empty(H * B, T, ldk, dtype=dtype, device=device)
         self.probs = self.probs_buf[:, :, :Kl]
         self.ctx = e(B * T, d)
         self.x1 = e(B * T, d)
@@ -134,7 +137,7 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
     ops.layernorm_fwd(tp.xa, vecs["ln1_g"], vecs["ln1_b"], tp.a, tp.mean1, tp.rstd1, flag)
     _bg(tp.a, W["wqkv"], b_mn=True, out=tp.qkv)
     ops.xl_split_qkv(tp.qkv, vecs["r_w_bias"], vecs["r_r_bias"], tp.qu, tp.qv, tp.kh, tp.vh, B, T, M, H, dh)
-    r = ws.get("xl_r", (Kl, d), cdt)
+    r = ws.get_rows("xl_r", (Kl, d), cdt)
     _bg(R, W["wr"], b_mn=True, out=r)
     ops.xl_split_heads(r, tp.rh, H, dh)
     pv_done = False
@@ -156,7 +159,7 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
             ops.gemm(tp.qv, tp.rh, out=bd, tile_n=SCORE_TILE)
         ops.xl_softmax_fwd(ac, bd, tp.probs_buf, T, M, tp.mem_len, 1.0 / math.sqrt(dh))
     if not pv_done:
-        ctx_h = ws.get("xl_ctx_h", (H * B, T, dh), cdt)
+        ctx_h = ws.get_rows("xl_ctx_h", (H * B, T, dh), cdt)
         ops.gemm(tp.probs, tp.vh.view(H * B, Kl, dh), b_mn=True, out=ctx_h)
         ops.xl_merge_heads(ctx_h.view(H, B * T, dh), tp.ctx, H, dh)
     d0 = None if drop is None else (drop[0], drop[1], drop[2], 0)
@@ -181,13 +184,13 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     scale = 1.0 / math.sqrt(dh)
     # feed-forward + LN2 (as the reference block)
     nbc = ops.colsum_blocks(Nt)
-    nbm = ops.mask_grad_blocks(Nt, d)
+    g_h2 = ws.get_rows("g_h2", (Nt, d), cdt)
+    nbm = ops.mask_grad_blocks(Nt, d, ops._pitch(g_h2))
     part = ws.get("colsum_part", (max(nbc, nbm), max(f, 3 * d)), torch.float32)
-    g_h2 = ws.get("g_h2", (Nt, d), cdt)
     pm = ws.get("mask_part", (nbm, d), torch.float32)
     ops.mask_grad(g_out, g_h2, n, drop, pm)
     _bg(tp.h1, g_h2, a_mn=True, b_mn=True, out=G["w2"])
-    g_z1 = ws.get("g_z1", (Nt, f), cdt)
+    g_z1 = ws.get_rows("g_z1", (Nt, f), cdt)
     LY.ffn_act_grad(g_h2, W, tp, g_z1, probe="block_gemm")
     ops.colsum_partial(g_z1, part[:, :f])
     _bg(tp.m, g_z1, a_mn=True, b_mn=True, out=G["w1"])
@@ -198,16 +201,16 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     pg = ws.get("ln_pg", (nbl_cur + nbl_mem, d), torch.float32)
     pb = ws.get("ln_pb", (nbl_cur + nbl_mem, d), torch.float32)
     g_x1 = ws.get("g_x1", (Nt, d), torch.float32)
-    g_proj = ws.get("g_proj", (Nt, d), cdt)
+    g_proj = ws.get_rows("g_proj", (Nt, d), cdt)
     pg2 = ws.get("ln2_pg", (nbl_cur, d), torch.float32)
     pb2 = ws.get("ln2_pb", (nbl_cur, d), torch.float32)
     ops.layernorm_bwd(g_m, tp.x1, tp.mean2, tp.rstd2, vecs["ln2_g"], g_x1, pg2, pb2,
                       resid_grad=g_out, dx_masked=g_proj, dropout=drop)
     # relative-position attention
     _bg(tp.ctx, g_proj, a_mn=True, b_mn=True, out=G["wo"])
-    g_ctx = ws.get("g_ctx", (Nt, d), cdt)
+    g_ctx = ws.get_rows("g_ctx", (Nt, d), cdt)
     _bg(g_proj, W["wo"], out=g_ctx)
-    g_ctx_h = ws.get("xl_g_ctx_h", (H, Nt, dh), cdt)
+    g_ctx_h = ws.get_rows("xl_g_ctx_h", (H, Nt, dh), cdt)
     ops.xl_split_heads(g_ctx, g_ctx_h, H, dh)
     g3 = g_ctx_h.view(H * B, T, dh)
     g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
@@ -245,10 +248,10 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
     work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
     ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
-    g_r = ws.get("xl_g_r", (Kl, d), cdt)
+    g_r = ws.get_rows("xl_g_r", (Kl, d), cdt)
     ops.xl_merge_heads(g_rh, g_r, H, dh)
     _bg(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
-    g_qkv = ws.get("xl_g_qkv", (B * Kl, 3 * d), cdt)
+    g_qkv = ws.get_rows("xl_g_qkv", (B * Kl, 3 * d), cdt)
     ops.xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh)
     _bg(tp.a, g_qkv, a_mn=True, b_mn=True, out=G["wqkv"])
     g_a = ws.get("xl_g_a", (B * Kl, d), torch.float32)
