@@ -174,10 +174,11 @@ int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t ds
 /* dst[r*ld + h*dh + c] = src[h, r, c] */
 int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
                       int32_t H, int32_t dh, int64_t ld_h, void* stream);
-/* g_qkv (xa row layout, [B*(M+T), 3d]) from fp32 head-major dQu, dQv, dK, dV */
+/* g_qkv (xa row layout, [B*(M+T), 3d], row pitch ld_qkv) from fp32 head-major
+   dQu, dQv, dK, dV (row pitch ld_g; 0 = dh) */
 int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
                       void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
-                      void* stream);
+                      int64_t ld_g, void* stream);
 /* P = softmax((AC + relshift(BD)) * scale) over keys M-mem_len <= j <= M+i; rows = H*B*T */
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream);
@@ -223,8 +224,9 @@ int rp_rows_gather(int32_t dtype, const void* src, int64_t ld_src, const int64_t
                    void* dst, int64_t ld_dst, void* stream);
 int rp_rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, int64_t n, int64_t cols, float* dst,
                         int64_t ld_dst, void* stream);
+/* u / v gradients: column sums of dQu / dQv [H, R, dh] (row pitch ld_g; 0 = dh) */
 int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
-                    int32_t H, int64_t R, int32_t dh, void* stream);
+                    int32_t H, int64_t R, int32_t dh, int64_t ld_g, void* stream);
 
 /* ---- embedding (layers.py:114-136) ---------------------------------------- */
 int rp_embed_fwd(int32_t dtype, const int64_t* tokens, const void* tied, const void* pos, void* out, int64_t B,

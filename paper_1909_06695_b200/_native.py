@@ -209,7 +209,7 @@ def _declare(L):
         "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, vp],
         "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, i64, vp],
         "rp_xl_merge_heads": [i32, vp, i32, vp, i64, i64, i32, i32, i64, vp],
-        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, vp],
+        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, vp],
         "rp_xl_softmax_fwd": [i32, vp, vp, i64, vp, i64, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd": [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
@@ -220,7 +220,7 @@ def _declare(L):
         "rp_rows_copy": [i32, vp, i64, i64, i64, vp, f32, i32, i32, vp, i64, vp],
         "rp_rows_gather": [i32, vp, i64, vp, i64, i64, vp, i64, vp],
         "rp_rows_scatter_add": [vp, i64, vp, i64, i64, vp, i64, vp],
-        "rp_xl_bias_grad": [vp, vp, vp, vp, vp, i32, i64, i32, vp],
+        "rp_xl_bias_grad": [vp, vp, vp, vp, vp, i32, i64, i32, i64, vp],
         "rp_module_workspace_bytes": [ctypes.POINTER(ModuleDesc)],
         "rp_module_forward": [ctypes.POINTER(ModuleDesc), ctypes.POINTER(ModuleWeights), ctypes.POINTER(ModuleSlot),
                               vp, vp, i64, vp, vp],

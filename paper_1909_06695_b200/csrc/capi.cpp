@@ -166,8 +166,8 @@ int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, voi
 }
 int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
                       void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
-                      void* stream) {
-  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream), ld_qkv);
+                      int64_t ld_g, void* stream) {
+  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream), ld_qkv, ld_g);
 }
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream) {
@@ -215,8 +215,8 @@ int rp_rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, in
 }
 int64_t rp_xl_bias_grad_workspace_bytes(int32_t H, int32_t dh) { return rp::xl_bias_grad_workspace_bytes(H, dh); }
 int rp_xl_bias_grad(const float* g_qu, const float* g_qv, float* workspace, float* g_r_w_bias, float* g_r_r_bias,
-                    int32_t H, int64_t R, int32_t dh, void* stream) {
-  return rp::xl_bias_grad(g_qu, g_qv, workspace, g_r_w_bias, g_r_r_bias, H, R, dh, RP_S(stream));
+                    int32_t H, int64_t R, int32_t dh, int64_t ld_g, void* stream) {
+  return rp::xl_bias_grad(g_qu, g_qv, workspace, g_r_w_bias, g_r_r_bias, H, R, dh, RP_S(stream), ld_g);
 }
 
 int64_t rp_module_workspace_bytes(const rp_module_desc* desc) { return rp::module_workspace_bytes(*desc); }

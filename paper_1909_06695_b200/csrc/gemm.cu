@@ -72,6 +72,7 @@ struct GemmParams {
   float* target_logit;
   float ce_scale;
   int vec_ok;
+  int vec2_ok;  // fp32 C with 8-byte aligned rows (an even pitch: d 410): float2 stores
   int resid_vec;
   int ksplit;  // > 0: "batch" b covers K range [b*ksplit, (b+1)*ksplit) of one matrix
   int n_fast;  // raster: N tiles fastest
@@ -112,6 +113,10 @@ __device__ __forceinline__ void store_chunk(const GemmParams& p, int64_t m, int 
 #pragma unroll
       for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
+  } else if (p.vec2_ok && n0 + 32 <= p.N) {
+    float2* dst = reinterpret_cast<float2*>(reinterpret_cast<float*>(p.C) + base);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) dst[q] = make_float2(v[2 * q], v[2 * q + 1]);
   } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -1078,6 +1083,8 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
                 ((a.stride_residual * oe) % 16 == 0 || batch == 1);
   p.vec_ok = ((reinterpret_cast<uintptr_t>(a.C) & 15) == 0) && ((a.ldc * oe) % 16 == 0) &&
              ((a.stride_c * oe) % 16 == 0 || p.batch == 1);
+  p.vec2_ok = !p.out_bf16 && ((reinterpret_cast<uintptr_t>(a.C) & 7) == 0) && (a.ldc % 2 == 0) &&
+              (a.stride_c % 2 == 0 || p.batch == 1);
   if (p.num_tiles == 0) return RP_OK;
   int grid = std::min(p.num_tiles * kCta, num_sms() / kCta * kCta);
   if (a.max_ctas > 0) grid = std::min(grid, std::max(kCta, a.max_ctas / kCta * kCta));

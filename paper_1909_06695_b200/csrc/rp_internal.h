@@ -107,7 +107,8 @@ int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, vo
 int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
                    cudaStream_t st, int64_t ldh = 0);
 int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
-                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq = 0);
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq = 0,
+                   int64_t ldg = 0);
 int xl_softmax_fwd(int dtype, const float* ac, const float* bd, int64_t lds, void* p, int64_t ldp, int64_t rows,
                    int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st);
 int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64_t ldp, void* gac, void* gbd,
@@ -136,7 +137,7 @@ int rows_scatter_add(const float* src, int64_t ld_src, const int64_t* idx, int64
                      int64_t ld_dst, cudaStream_t st);
 int64_t xl_bias_grad_workspace_bytes(int H, int dh);
 int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
-                 cudaStream_t st);
+                 cudaStream_t st, int64_t ldg = 0);
 
 int64_t block_workspace_bytes(const rp_block_desc& d);
 int block_forward(const rp_block_desc& d, const rp_block_weights& w, const void* x, void* out, const rp_block_tape& tp,

@@ -140,89 +140,109 @@ __global__ void merge_heads_kernel(const S* __restrict__ src, D* __restrict__ ds
   }
 }
 
-// Scalar forms of the head split / merge kernels for any head dim and row
-// pitches (d or the head dim not a multiple of 8, e.g. BASELINE configs[3]:
-// d 410 = 10 heads x 41; bf16 rows are padded to 16-byte pitches, so row r
-// starts at r * ld).  One thread per element.
-template <typename T>
-__global__ void split_qkv_scalar_kernel(const T* __restrict__ qkv, const float* __restrict__ u,
-                                        const float* __restrict__ v, T* __restrict__ qu, T* __restrict__ qv,
-                                        T* __restrict__ kh, T* __restrict__ vh, int B, int Tn, int M, int H, int dh,
-                                        int64_t ldq, int64_t ldh) {
-  const int Kl = M + Tn, d = H * dh;
-  XL_GRID_LOOP(e, (int64_t)H * B * Kl * dh) {
-    const int c = (int)(e % dh);
-    const int64_t hbj = e / dh;
-    const int j = (int)(hbj % Kl);
-    const int hb = (int)(hbj / Kl);
-    const int b = hb % B, h = hb / B;
-    const T* src = qkv + key_row(b, j, B, Tn, M) * ldq + h * dh + c;
-    kh[hbj * ldh + c] = src[d];
-    vh[hbj * ldh + c] = src[2 * d];
-    if (j >= M) {
-      const float x = to_f(src[0]);
-      const int64_t o = ((int64_t)hb * Tn + (j - M)) * ldh + c;
-      qu[o] = from_f<T>(x + u[h * dh + c]);
-      qv[o] = from_f<T>(x + v[h * dh + c]);
-    }
-  }
-}
+// Row-block forms of the head split / merge kernels for any head dim and
+// row pitches (d or the head dim not a multiple of 8, e.g. BASELINE
+// configs[3]: d 410 = 10 heads x 41; bf16 rows are padded to 16-byte pitches,
+// so row r starts at r * ld).  One CTA per row (grid-stride over rows): the
+// row's coordinates are decoded once, the threads sweep its columns with
+// 32-bit index math, and the row-major side is read / written coalesced.
+constexpr int kRowBlk = 128;
 
-template <typename S, typename D>
-__global__ void split_heads_scalar_kernel(const S* __restrict__ src, int64_t ld, D* __restrict__ dst, int64_t rows,
-                                          int H, int dh, int64_t ldh) {
-  XL_GRID_LOOP(e, rows * H * dh) {
-    const int c = (int)(e % dh);
-    const int64_t hr = e / dh;
-    const int64_t r = hr % rows;
-    const int h = (int)(hr / rows);
-    dst[hr * ldh + c] = from_f<D>(to_f(src[r * ld + h * dh + c]));
-  }
-}
+inline int row_grid(int64_t rows) { return (int)std::min<int64_t>(rows, 148 * 32); }
 
-template <typename S, typename D>
-__global__ void merge_heads_scalar_kernel(const S* __restrict__ src, D* __restrict__ dst, int64_t ld, int64_t rows,
-                                          int H, int dh, int64_t ldh) {
-  const int d = H * dh;
-  XL_GRID_LOOP(e, rows * d) {
-    const int64_t r = e / d;
-    const int col = (int)(e % d);
-    const int h = col / dh, c = col % dh;
-    dst[r * ld + col] = from_f<D>(to_f(src[((int64_t)h * rows + r) * ldh + c]));
-  }
-}
-
-template <typename T>
-__global__ void merge_grads_scalar_kernel(const float* __restrict__ gqu, const float* __restrict__ gqv,
-                                          const float* __restrict__ gkh, const float* __restrict__ gvh,
-                                          T* __restrict__ gqkv, int B, int Tn, int M, int H, int dh, int64_t ldq) {
-  const int Kl = M + Tn, d = H * dh;
+__device__ __forceinline__ void key_coords(int64_t row, int B, int Tn, int M, int& b, int& j) {
   const int64_t BM = (int64_t)B * M;
-  XL_GRID_LOOP(e, (int64_t)B * Kl * 3 * d) {
-    const int64_t row = e / (3 * d);
-    const int col = (int)(e % (3 * d));
-    const int part = col / d;
-    const int h = (col % d) / dh, c = col % dh;
+  if (row < BM) {
+    b = (int)(row / M);
+    j = (int)(row - (int64_t)b * M);
+  } else {
+    const int64_t r = row - BM;
+    b = (int)(r / Tn);
+    j = M + (int)(r - (int64_t)b * Tn);
+  }
+}
+
+// qkv row (b, j) in the xa layout -> kh, vh [H, B, Kl, ldh]; current rows also
+// -> qu = q + u, qv = q + v [H, B, T, ldh]
+template <typename T>
+__global__ void __launch_bounds__(kRowBlk) split_qkv_rows_kernel(
+    const T* __restrict__ qkv, const float* __restrict__ u, const float* __restrict__ v, T* __restrict__ qu,
+    T* __restrict__ qv, T* __restrict__ kh, T* __restrict__ vh, int B, int Tn, int M, int H, int dh, int64_t ldq,
+    int64_t ldh) {
+  const int Kl = M + Tn, d = H * dh;
+  const int64_t rows = (int64_t)B * Kl;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
     int b, j;
-    if (row < BM) {
-      b = (int)(row / M);
-      j = (int)(row % M);
-    } else {
-      b = (int)((row - BM) / Tn);
-      j = M + (int)((row - BM) % Tn);
-    }
-    float g;
-    if (part == 0) {
-      if (j < M) {
-        g = 0.f;
-      } else {
-        const int64_t o = (((int64_t)h * B + b) * Tn + (j - M)) * dh + c;
-        g = gqu[o] + gqv[o];
+    key_coords(row, B, Tn, M, b, j);
+    const T* src = qkv + row * ldq;
+    for (int col = threadIdx.x; col < d; col += kRowBlk) {
+      const int h = col / dh, c = col - h * dh;
+      const int64_t hb = (int64_t)h * B + b;
+      kh[(hb * Kl + j) * ldh + c] = src[d + col];
+      vh[(hb * Kl + j) * ldh + c] = src[2 * d + col];
+      if (j >= M) {
+        const float x = to_f(src[col]);
+        const int64_t o = (hb * Tn + (j - M)) * ldh + c;
+        qu[o] = from_f<T>(x + u[col]);
+        qv[o] = from_f<T>(x + v[col]);
       }
-    } else {
-      g = (part == 1 ? gkh : gvh)[(((int64_t)h * B + b) * Kl + j) * dh + c];
     }
-    gqkv[row * ldq + col] = from_f<T>(g);
+  }
+}
+
+// dst[h, r, c] (pitch ldh) = src[r*ld + h*dh + c]
+template <typename S, typename D>
+__global__ void __launch_bounds__(kRowBlk) split_heads_rows_kernel(const S* __restrict__ src, int64_t ld,
+                                                                    D* __restrict__ dst, int64_t rows, int H, int dh,
+                                                                    int64_t ldh) {
+  const int d = H * dh;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int col = threadIdx.x; col < d; col += kRowBlk) {
+      const int h = col / dh, c = col - h * dh;
+      dst[((int64_t)h * rows + r) * ldh + c] = from_f<D>(to_f(src[r * ld + col]));
+    }
+  }
+}
+
+// dst[r*ld + h*dh + c] = src[h, r, c] (pitch ldh)
+template <typename S, typename D>
+__global__ void __launch_bounds__(kRowBlk) merge_heads_rows_kernel(const S* __restrict__ src, D* __restrict__ dst,
+                                                                    int64_t ld, int64_t rows, int H, int dh,
+                                                                    int64_t ldh) {
+  const int d = H * dh;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int col = threadIdx.x; col < d; col += kRowBlk) {
+      const int h = col / dh, c = col - h * dh;
+      dst[r * ld + col] = from_f<D>(to_f(src[((int64_t)h * rows + r) * ldh + c]));
+    }
+  }
+}
+
+// g_qkv row (b, j) (pitch ldq) from the head-major fp32 gradients (pitch ldg)
+template <typename T>
+__global__ void __launch_bounds__(kRowBlk) merge_grads_rows_kernel(
+    const float* __restrict__ gqu, const float* __restrict__ gqv, const float* __restrict__ gkh,
+    const float* __restrict__ gvh, T* __restrict__ gqkv, int B, int Tn, int M, int H, int dh, int64_t ldq,
+    int64_t ldg) {
+  const int Kl = M + Tn, d = H * dh;
+  const int64_t rows = (int64_t)B * Kl;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    int b, j;
+    key_coords(row, B, Tn, M, b, j);
+    T* dst = gqkv + row * ldq;
+    for (int col = threadIdx.x; col < d; col += kRowBlk) {
+      const int h = col / dh, c = col - h * dh;
+      const int64_t hb = (int64_t)h * B + b;
+      float q = 0.f;
+      if (j >= M) {
+        const int64_t o = (hb * Tn + (j - M)) * ldg + c;
+        q = gqu[o] + gqv[o];
+      }
+      const int64_t ok = (hb * Kl + j) * ldg + c;
+      dst[col] = from_f<T>(q);
+      dst[d + col] = from_f<T>(gkh[ok]);
+      dst[2 * d + col] = from_f<T>(gvh[ok]);
+    }
   }
 }
 
@@ -405,10 +425,10 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const float* __re
 constexpr int kBiasChunks = 64;
 
 __global__ void bias_partial_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ part,
-                                    int H, int64_t R, int dh) {
+                                    int H, int64_t R, int dh, int64_t ldg) {
   __shared__ float red[kThreads];
   const int chunk = blockIdx.x, h = blockIdx.y, which = blockIdx.z;
-  const float* src = (which ? b : a) + (int64_t)h * R * dh;
+  const float* src = (which ? b : a) + (int64_t)h * R * ldg;
   const int groups = kThreads / dh;
   const int c = threadIdx.x % dh, gi = threadIdx.x / dh;
   const int64_t per = (R + kBiasChunks - 1) / kBiasChunks;
@@ -416,7 +436,7 @@ __global__ void bias_partial_kernel(const float* __restrict__ a, const float* __
   const int64_t r1 = (r0 + per < R) ? r0 + per : R;
   float acc = 0.f;
   if (gi < groups)
-    for (int64_t r = r0 + gi; r < r1; r += groups) acc += src[r * dh + c];
+    for (int64_t r = r0 + gi; r < r1; r += groups) acc += src[r * ldg + c];
   red[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < dh) {
@@ -476,9 +496,9 @@ int xl_split_qkv(int dtype, const void* qkv, const float* u, const float* v, voi
   if (ldq <= 0) ldq = 3 * (int64_t)H * dh;
   if (ldh <= 0) ldh = dh;
   if (dh % 8 || ldq != 3 * (int64_t)H * dh || ldh != dh) {
-    const int64_t ne = (int64_t)H * B * (M + Tn) * dh;
-    if (ne == 0) return RP_OK;
-    XL_DTYPE(dtype, split_qkv_scalar_kernel<T><<<blocks8(ne), kThreads, 0, st>>>(
+    const int64_t rows = B * (M + Tn);
+    if (rows == 0) return RP_OK;
+    XL_DTYPE(dtype, split_qkv_rows_kernel<T><<<row_grid(rows), kRowBlk, 0, st>>>(
                         (const T*)qkv, u, v, (T*)qu, (T*)qv, (T*)kh, (T*)vh, (int)B, (int)Tn, (int)M, H, dh, ldq, ldh));
     return check_launch("xl_split_qkv");
   }
@@ -512,9 +532,8 @@ int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, vo
                    cudaStream_t st, int64_t ldh) {
   if (ldh <= 0) ldh = dh;
   if (dh % 8 || ld % 8 || ldh != dh) {
-    const int64_t ne = rows * H * dh;
-    if (ne == 0) return RP_OK;
-    XL_PAIR(src_dtype, dst_dtype, (split_heads_scalar_kernel<S, D><<<blocks8(ne), kThreads, 0, st>>>(
+    if (rows == 0) return RP_OK;
+    XL_PAIR(src_dtype, dst_dtype, (split_heads_rows_kernel<S, D><<<row_grid(rows), kRowBlk, 0, st>>>(
                                       (const S*)src, ld, (D*)dst, rows, H, dh, ldh)));
     return check_launch("xl_split_heads");
   }
@@ -530,9 +549,8 @@ int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int
                    cudaStream_t st, int64_t ldh) {
   if (ldh <= 0) ldh = dh;
   if (dh % 8 || ld % 8 || ldh != dh) {
-    const int64_t ne = rows * H * dh;
-    if (ne == 0) return RP_OK;
-    XL_PAIR(src_dtype, dst_dtype, (merge_heads_scalar_kernel<S, D><<<blocks8(ne), kThreads, 0, st>>>(
+    if (rows == 0) return RP_OK;
+    XL_PAIR(src_dtype, dst_dtype, (merge_heads_rows_kernel<S, D><<<row_grid(rows), kRowBlk, 0, st>>>(
                                       (const S*)src, (D*)dst, ld, rows, H, dh, ldh)));
     return check_launch("xl_merge_heads");
   }
@@ -545,13 +563,14 @@ int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int
 }
 
 int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
-                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq) {
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq, int64_t ldg) {
   if (ldq <= 0) ldq = 3 * (int64_t)H * dh;
-  if (dh % 8 || ldq != 3 * (int64_t)H * dh) {
-    const int64_t ne = B * (M + Tn) * 3 * (int64_t)H * dh;
-    if (ne == 0) return RP_OK;
-    XL_DTYPE(dtype, merge_grads_scalar_kernel<T><<<blocks8(ne), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv,
-                                                                                  (int)B, (int)Tn, (int)M, H, dh, ldq));
+  if (ldg <= 0) ldg = dh;
+  if (dh % 8 || ldq != 3 * (int64_t)H * dh || ldg != dh) {
+    const int64_t rows = B * (M + Tn);
+    if (rows == 0) return RP_OK;
+    XL_DTYPE(dtype, merge_grads_rows_kernel<T><<<row_grid(rows), kRowBlk, 0, st>>>(
+                        gqu, gqv, gkh, gvh, (T*)gqkv, (int)B, (int)Tn, (int)M, H, dh, ldq, ldg));
     return check_launch("xl_merge_grads");
   }
   const int64_t n = B * (M + Tn) * 3 * (int64_t)H * dh / 8;
@@ -611,9 +630,10 @@ int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64
 int64_t xl_bias_grad_workspace_bytes(int H, int dh) { return (int64_t)2 * H * kBiasChunks * dh * sizeof(float); }
 
 int xl_bias_grad(const float* gqu, const float* gqv, float* part, float* gu, float* gv, int H, int64_t R, int dh,
-                 cudaStream_t st) {
+                 cudaStream_t st, int64_t ldg) {
+  if (ldg <= 0) ldg = dh;
   if (dh > kThreads) return set_error(RP_ERR_DIMENSION, "xl_bias_grad: head dim must be <= 256");
-  bias_partial_kernel<<<dim3(kBiasChunks, H, 2), kThreads, 0, st>>>(gqu, gqv, part, H, R, dh);
+  bias_partial_kernel<<<dim3(kBiasChunks, H, 2), kThreads, 0, st>>>(gqu, gqv, part, H, R, dh, ldg);
   bias_finish_kernel<<<(2 * H * dh + kThreads - 1) / kThreads, kThreads, 0, st>>>(part, gu, gv, H, dh);
   return check_launch("xl_bias_grad");
 }

@@ -75,6 +75,19 @@ def empty_rows(*shape, dtype, device):
     return t if cp == c else t[..., :c]
 
 
+def copy_rows(dst, src):
+    """dst.copy_(src) for row-major [..., rows, cols] tensors; when both share
+    one padded row pitch the copy runs over the padded rows (one dense copy
+    instead of a strided one; pad columns carry no data)."""
+    ld = dst.stride(-2) if dst.dim() >= 2 else 0
+    if (dst.shape == src.shape and dst.dim() >= 2 and dst.stride(-1) == 1 and src.stride(-1) == 1
+            and ld != dst.shape[-1] and src.stride(-2) == ld and dst.dtype == src.dtype):
+        shp = tuple(dst.shape[:-1]) + (ld,)
+        dst.as_strided(shp, dst.stride()).copy_(src.as_strided(shp, src.stride()))
+    else:
+        dst.copy_(src)
+
+
 class Workspace:
     """Named scratch buffers reused across calls (one per module and role)."""
 

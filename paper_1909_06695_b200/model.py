@@ -811,15 +811,16 @@ class ModuleState:
         rows = tp.B * tp.M * m
         buf = self.mem.get(off)
         if buf is None or buf.shape[0] != rows:
-            buf = self.mem[off] = torch.zeros(rows, self.d, dtype=self.cdtype, device=self.device)
-        tp.mem.copy_(buf[j * tp.B * tp.M:(j + 1) * tp.B * tp.M])
+            buf = self.mem[off] = LY.empty_rows(rows, self.d, dtype=self.cdtype, device=self.device)
+            buf.zero_()
+        LY.copy_rows(tp.mem, buf[j * tp.B * tp.M:(j + 1) * tp.B * tp.M])
         tp.mem_len = self.mem_len
 
     def _store_memory(self, off, tp, part=(0, 1)):
         if tp.M:
             j = part[0]
             dst = self.mem[off][j * tp.B * tp.M:(j + 1) * tp.B * tp.M]
-            dst.view(tp.B, tp.M, self.d).copy_(tp.x.view(tp.B, tp.T, self.d)[:, tp.T - tp.M:])
+            LY.copy_rows(dst.view(tp.B, tp.M, self.d), tp.x.view(tp.B, tp.T, self.d)[:, tp.T - tp.M:])
 
     def reset_memory(self):
         self.mem_len = 0

@@ -401,12 +401,13 @@ def xl_merge_heads(src, dst, H, dh):
 
 
 def xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh):
+    """fp32 head-major gradients (one shared row pitch) -> g_qkv rows."""
+    ldg = _pitch(g_qu)
+    if any(_pitch(t) != ldg for t in (g_qv, g_kh, g_vh)):
+        raise DimensionError("xl_merge_grads: the head gradients share one row pitch")
     _count(1)
-    for t in (g_qu, g_qv, g_kh, g_vh):
-        if not t.is_contiguous():
-            raise DimensionError("xl_merge_grads: fp32 head gradients must be contiguous")
     N.check(N.lib().rp_xl_merge_grads(_dtc(g_qkv), _ptr(g_qu), _ptr(g_qv), _ptr(g_kh), _ptr(g_vh), _ptr(g_qkv), B, T,
-                                      M, H, dh, _pitch(g_qkv), _stream()), "xl_merge_grads")
+                                      M, H, dh, _pitch(g_qkv), ldg, _stream()), "xl_merge_grads")
 
 
 def xl_softmax_fwd(ac, bd, probs, T, M, mem_len, scale):
@@ -549,8 +550,11 @@ def xl_softmax_bwd(g_p, probs, g_ac, g_bd, T, M, mem_len, scale):
 
 
 def xl_bias_grad(g_qu, g_qv, work, g_u, g_v, H, rows, dh):
+    ldg = _pitch(g_qu)
+    if _pitch(g_qv) != ldg:
+        raise DimensionError("xl_bias_grad: dQu and dQv share one row pitch")
     _count(2)
-    N.check(N.lib().rp_xl_bias_grad(_ptr(g_qu), _ptr(g_qv), _ptr(work), _ptr(g_u), _ptr(g_v), H, rows, dh,
+    N.check(N.lib().rp_xl_bias_grad(_ptr(g_qu), _ptr(g_qv), _ptr(work), _ptr(g_u), _ptr(g_v), H, rows, dh, ldg,
                                     _stream()), "xl_bias_grad")
 
 

@@ -215,8 +215,11 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     g3 = g_ctx_h.view(H * B, T, dh)
     g_ac = ws.get("xl_g_ac", (H * B, T, tp.ldk), cdt)
     g_bd = ws.get("xl_g_bd", (H, Nt, tp.ldk), cdt)
-    g_qu = ws.get("xl_g_qu", (H, Nt, dh), torch.float32)
-    g_qv = ws.get("xl_g_qv", (H, Nt, dh), torch.float32)
+    # fp32 head-gradient rows at 16-byte pitches (head dim 41 -> 44): the GEMM
+    # epilogues store them with vector stores
+    f32r = lambda name, *s: ws.get(name, s[:-1] + (-(-s[-1] // 4) * 4,), torch.float32)[..., : s[-1]]  # noqa: E731
+    g_qu = f32r("xl_g_qu", H, Nt, dh)
+    g_qv = f32r("xl_g_qv", H, Nt, dh)
     dq_done = False
     if fused_dq_ok(tp):
         # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu)
@@ -232,14 +235,14 @@ def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
         g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
         ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p, tile_n=SCORE_TILE)
         ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
-    g_vh = ws.get("xl_g_vh", (H * B, Kl, dh), torch.float32)
+    g_vh = f32r("xl_g_vh", H * B, Kl, dh)
     # P^T and dAC^T are banded: key j sees queries i >= j - M (causal window),
     # so each key tile starts its K loop (over queries) at its first live block
     band = -M if BANDED else None
     ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
-    g_kh = ws.get("xl_g_kh", (H * B, Kl, dh), torch.float32)
-    g_rh = ws.get("xl_g_rh", (H, Kl, dh), torch.float32)
+    g_kh = f32r("xl_g_kh", H * B, Kl, dh)
+    g_rh = f32r("xl_g_rh", H, Kl, dh)
     if not dq_done:
         ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
     ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh, k_lo_off=band)
