@@ -375,10 +375,15 @@ class _Job:
             x = y = None  # tokens and targets live on the Ouroboros rank only
         b = self.E.BatchSample(x, y, self.t)
         if self.pipeline:
-            self.eng.step(self.t, b, self.opt, sync=sync, shape=(self.B, self.T))
+            self.eng.step(self.t, b, self.opt, sync=bool(sync), shape=(self.B, self.T))
         else:
             self.eng.step(self.t, b, self.opt, sync=sync)
         self.t += 1
+
+    def flush(self):
+        """Read the last step's result (sync="lagged" leaves one in flight)."""
+        if not self.pipeline:
+            self.eng.flush_lagged()
 
     def check(self):
         self.stack.runtime.check("bench", self.mods)
@@ -416,6 +421,8 @@ def _timed(job, steps, barrier, host=False, sync=False):
     s.record()
     for _ in range(steps):
         job.step(host=host, sync=sync)
+    if sync == "lagged":
+        job.flush()
     e.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
@@ -521,7 +528,10 @@ def run_ours(args, c):
     # windows of K steps, the median reported; GC paused while timing
     gc.disable()
     try:
-        windows = sorted(_max_over_ranks(_timed(job, args.steps, barrier, host=True, sync=True), dist)
+        # the public step API with host batches; the host reads every step's
+        # loss (and status words) from pinned memory one step behind, so it
+        # never idles the GPU between steps (engine.step(sync="lagged"))
+        windows = sorted(_max_over_ranks(_timed(job, args.steps, barrier, host=True, sync="lagged"), dist)
                          for _ in range(3))
     finally:
         gc.enable()
@@ -601,6 +611,10 @@ def run_ours(args, c):
                        "l2": "working set per step >> 126 MB L2 (no flush needed)"},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 2 * B * T * 8,
                     "d2h_bytes_per_step": 4 + 4 * (len(job_mods) + 1), "window": "median of 3 windows of K steps",
+                    "api": ("engine.step(t, host batch, optimizer, sync=True) per step" if pipeline else
+                            "engine.step(t, host batch, optimizer, sync='lagged'): pinned H2D of the step's tokens "
+                            "and targets, D2H of its loss + status words, each read on the host one step later; "
+                            "the window ends after the last step's loss is read"),
                     "windows_ms_per_step": [round(w / args.steps, 3) for w in windows]},
             "roofline": roofline,
             "model_flops_util": flops_per_token(c) * value / (world * peak_t * 1e12),

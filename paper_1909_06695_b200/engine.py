@@ -360,10 +360,62 @@ class PipelineEngine:
         self.last_backward_logical = longest + handoff
         self.clock = end
 
+    # -- lagged result read (sync="lagged") --------------------------------------
+    def _lag_submit(self, t, loss_dev):
+        """Queue the D2H copy of step t's loss and status words into pinned
+        host memory (no host wait); returns the previous step's host loss after
+        checking its status words (raising like the synchronous check)."""
+        words = [m.flag for m in self.modules] + [self.runtime.flag]
+        if getattr(self, "_lag", None) is None:
+            pin = lambda n, dt: torch.zeros(n, dtype=dt).pin_memory()  # noqa: E731
+            self._lag = {"bufs": [(pin(1, torch.float32), pin(len(words), torch.int32)) for _ in range(2)],
+                         "pending": None}
+        lag = self._lag
+        hl, hw = lag["bufs"][t % 2]
+        main = torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(main):
+            hl.copy_(loss_dev.detach().reshape(1).float(), non_blocking=True)
+            for i, w in enumerate(words):
+                hw[i: i + 1].copy_(w.view(1), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+        prev, lag["pending"] = lag["pending"], (t, ev, hl, hw, words)
+        return self._lag_read(prev)
+
+    def _lag_read(self, entry):
+        from . import _native as N
+
+        if entry is None:
+            return None
+        t, ev, hl, hw, words = entry
+        ev.synchronize()
+        bad = [(i, int(b)) for i, b in enumerate(hw.tolist()) if b]
+        if bad:
+            for w in words:
+                w.zero_()
+            i, bits = bad[0]
+            where = f"module {self.modules[i].index}" if i < len(self.modules) else "optimizer update"
+            if bits & N.FLAG_DIMENSION:
+                raise DimensionError(f"token or target id out of range in {where} (step {t})")
+            raise NonFiniteError(f"non-finite values in {where} (step {t})")
+        return float(hl.item())
+
+    def flush_lagged(self):
+        """sync="lagged": the last step's host loss (waits for it)."""
+        lag = getattr(self, "_lag", None)
+        if lag is None:
+            return None
+        entry, lag["pending"] = lag["pending"], None
+        return self._lag_read(entry)
+
     # -- public -----------------------------------------------------------------
     def step(self, t, batch, optimizer=None, sync=True):
         """One schedule step.  Returns (packet, loss); with sync=False the loss
-        stays a 0-d device tensor and the status word is not polled."""
+        stays a 0-d device tensor and the status word is not polled; with
+        sync="lagged" the step is issued without waiting and `loss` is the
+        host loss of step t-1 (None for the first), read from pinned memory
+        after its status words were checked -- the host stays one step ahead
+        of the device (flush_lagged() returns the last step's loss)."""
         if t < 0:
             raise ValueError("step index must be >= 0")
         V = self.stack.tied_store.vocab
@@ -381,6 +433,8 @@ class PipelineEngine:
         self.last_loss_device = loss_dev
         if self._dclock:
             self._dclock.flush(self.device_trace)
+        if sync == "lagged":
+            return packet, self._lag_submit(t, loss_dev)
         if sync:
             self.runtime.check(f"step {t}", self.modules)
             loss = float(loss_dev.item())
@@ -557,6 +611,8 @@ class ConcurrentPipelineEngine(PipelineEngine):
         # optimizer through start_ev / zero_ev (recorded on the main stream),
         # so no trailing fork is left open (CUDA-graph capture needs joins)
         self.last_loss_device = loss_dev
+        if sync == "lagged":
+            return packet, self._lag_submit(t, loss_dev)
         if sync:
             try:
                 self.runtime.check(f"step {t}", self.modules)
