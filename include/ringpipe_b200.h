@@ -110,8 +110,10 @@ int rp_last_error(char* buf, size_t len);
 int rp_gemm(const rp_gemm_args* args, void* stream);
 /* N tile the library picks for an (M, N, batch) GEMM (sizes RP_EPI_LSE_PARTIAL partials) */
 int rp_gemm_tile_n(int64_t M, int64_t N, int64_t batch);
-/* K splits the library uses for a batch-1 fp32 store GEMM with cap_bytes of partial scratch (1 = none) */
-int rp_gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes);
+/* K splits the library uses for an fp32 store GEMM of `batch` matrices with cap_bytes of partial scratch
+ * (1 = none).  Split-K partials are laid out [split][matrix][M][N]; a batched GEMM finishes with one
+ * rp_splitk_reduce over batch*M rows, so its output rows must be contiguous across the batch. */
+int rp_gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t batch, int64_t cap_bytes);
 /* out[m,n] = sum_s part[s][m,n] in fixed order (deterministic split-K finish) */
 int rp_splitk_reduce(const float* part, int32_t splits, int64_t M, int64_t N, float* out, int64_t ldo, void* stream);
 int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src,

@@ -181,7 +181,7 @@ def _declare(L):
         "rp_last_error": [ctypes.c_char_p, ctypes.c_size_t],
         "rp_gemm": [ctypes.POINTER(GemmArgs), vp],
         "rp_gemm_tile_n": [i64, i64, i64],
-        "rp_gemm_choose_splits": [i64, i64, i64, i64],
+        "rp_gemm_choose_splits": [i64, i64, i64, i64, i64],
         "rp_splitk_reduce": [vp, i32, i64, i64, vp, i64, vp],
         "rp_tf32_split": [vp, vp, vp, i64, i64, i64, i64, vp],
         "rp_layernorm_fwd": [i32, vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, vp, vp],

@@ -44,8 +44,8 @@ int rp_gemm(const rp_gemm_args* args, void* stream) {
 
 int rp_gemm_tile_n(int64_t M, int64_t N, int64_t batch) { return rp::gemm_tile_n(M, N, batch); }
 
-int rp_gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes) {
-  return rp::gemm_choose_splits(M, N, K, cap_bytes);
+int rp_gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t batch, int64_t cap_bytes) {
+  return rp::gemm_choose_splits(M, N, K, cap_bytes, batch);
 }
 
 int rp_splitk_reduce(const float* part, int32_t splits, int64_t M, int64_t N, float* out, int64_t ldo, void* stream) {

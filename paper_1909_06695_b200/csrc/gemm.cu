@@ -74,7 +74,8 @@ struct GemmParams {
   int vec_ok;
   int vec2_ok;  // fp32 C with 8-byte aligned rows (an even pitch: d 410): float2 stores
   int resid_vec;
-  int ksplit;  // > 0: "batch" b covers K range [b*ksplit, (b+1)*ksplit) of one matrix
+  int ksplit;  // > 0: unit b is split b / bsz of matrix b % bsz, K range [split*ksplit, (split+1)*ksplit)
+  int bsz;     // matrices in the batch (the split-K partials are laid out [split][matrix])
   int n_fast;  // raster: N tiles fastest
   int tma_store;  // bf16 C written by TMA bulk stores from a swizzled smem tile
   int tma_resid;  // bf16 residual / aux read by TMA bulk loads into a swizzled smem tile
@@ -342,8 +343,8 @@ __global__ void __launch_bounds__(384, 1)
         int mb, nb, b;
         decode_tile(p, tile, mb, nb, b);
         const int m0 = mb * Cfg::BM_TILE + crank * Cfg::BM, n0 = nb * BN + crank * Cfg::B_ROWS;
-        const int kbase = p.ksplit ? b * p.ksplit : 0;
-        const int bc = p.ksplit ? 0 : b;
+        const int kbase = p.ksplit ? (b / p.bsz) * p.ksplit : 0;
+        const int bc = p.ksplit ? b % p.bsz : b;
         const int kb_lo = tile_kb_lo<Cfg::BM_TILE, Cfg::BK>(p, mb);
         for (int pass = 0; pass < p.passes; ++pass) {
           const CUtensorMap* ma = (pass == 2) ? &mapA_lo : &mapA;
@@ -964,10 +965,9 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
                          Cfg::SMEM_BYTES);
   CUtensorMap ma, mal, mb, mbl;
   const int ks = a.k_splits > 1 ? a.k_splits : 1;
-  if (ks > 1 && (a.batch > 1 || a.epilogue != RP_EPI_STORE))
-    return set_error(RP_ERR_INVALID, "split-K needs batch 1 and the plain store epilogue");
+  if (ks > 1 && a.epilogue != RP_EPI_STORE) return set_error(RP_ERR_INVALID, "split-K needs the plain store epilogue");
   const int64_t kchunk = ks > 1 ? ((a.K + ks - 1) / ks + Cfg::BK - 1) / Cfg::BK * Cfg::BK : a.K;
-  const int64_t batch = ks > 1 ? 1 : std::max<int64_t>(a.batch, 1);
+  const int64_t batch = std::max<int64_t>(a.batch, 1);
   int st;
   // A: K-major -> inner K, rows M ; MN-major -> inner M, rows K
   if (!a.a_mn_major)
@@ -1048,8 +1048,9 @@ int launch(const rp_gemm_args& a, cudaStream_t stream) {
   p.M = (int)a.M;
   p.N = (int)a.N;
   p.K = (int)a.K;
-  p.batch = ks > 1 ? ks : (int)batch;
+  p.batch = ks > 1 ? ks * (int)batch : (int)batch;
   p.ksplit = ks > 1 ? (int)kchunk : 0;
+  p.bsz = (int)batch;
   p.a_mn = a.a_mn_major;
   p.b_mn = a.b_mn_major;
   p.passes = passes;
@@ -1170,7 +1171,7 @@ int gemm(const rp_gemm_args& a, cudaStream_t stream) {
   if (a.M < 0 || a.N < 0 || a.K <= 0) return set_error(RP_ERR_DIMENSION, "bad GEMM shape");
   if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return set_error(RP_ERR_DIMENSION, "GEMM dim too large");
   const bool tf32 = a.math != RP_MATH_BF16;
-  const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.M, a.N, a.k_splits > 1 ? a.k_splits : a.batch);
+  const int bn = a.tile_n > 0 ? a.tile_n : gemm_tile_n(a.M, a.N, a.k_splits > 1 ? a.k_splits * std::max<int64_t>(a.batch, 1) : a.batch);
   if (tf32) {
     if (bn == 256) return launch<true, 256, 1>(a, stream);
     if (bn == 128) return launch<true, 128, 1>(a, stream);

@@ -62,16 +62,17 @@ struct Ctx {
 
 // Deterministic split-K for weight-gradient shaped GEMMs (few output tiles,
 // long K): pick S minimising waves(S) * tile_time(K/S) + partial traffic.
-int choose_splits(int64_t M, int64_t N, int64_t K, int bn, int64_t cap_bytes) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+int choose_splits(int64_t M, int64_t N, int64_t K, int bn, int64_t cap_bytes, int64_t batch) {
+  batch = std::max<int64_t>(batch, 1);
+  const int64_t tiles = ((M + 127) / 128) * ((N + bn - 1) / bn) * batch;
   if (tiles >= 148 || K < 1024 || cap_bytes <= 0) return 1;
   const double R = 1.1e15 / 148.0, BW = 5.5e12;
   int best = 1;
   double best_t = 2.0 * 128 * bn * (double)K / R;
-  const int smax = (int)std::min<int64_t>({64, K / 512, cap_bytes / (M * N * 4)});
+  const int smax = (int)std::min<int64_t>({64, K / 512, cap_bytes / (M * N * 4 * batch)});
   for (int S = 2; S <= smax; ++S) {
     const double waves = std::ceil((double)(tiles * S) / 148.0);
-    const double t = waves * 2.0 * 128 * bn * ((double)K / S) / R + (double)S * M * N * 8.0 / BW;
+    const double t = waves * 2.0 * 128 * bn * ((double)K / S) / R + (double)S * M * N * batch * 8.0 / BW;
     if (t < best_t * 0.97) {
       best_t = t;
       best = S;
@@ -152,8 +153,10 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.ldc = C.ld;
   g.stride_c = C.bstride;
   int splits = 1;
-  if (out_dtype == RP_F32 && e.kind == RP_EPI_STORE && g.batch == 1 && c.splitk)
-    splits = choose_splits(g.M, g.N, g.K, 256, c.splitk_cap);
+  // batched split-K needs the batch's output rows contiguous (one [batch*M, N] reduce)
+  const bool rows_fold = g.batch == 1 || g.stride_c == g.M * g.ldc;
+  if (out_dtype == RP_F32 && e.kind == RP_EPI_STORE && rows_fold && g.k_lo_sign <= 0 && c.splitk)
+    splits = choose_splits(g.M, g.N, g.K, 256, c.splitk_cap, g.batch);
   if (splits > 1) {
     g.k_splits = splits;
     g.C = c.splitk;
@@ -178,7 +181,7 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.ce_scale = e.ce_scale;
   g.tile_n = e.tile_n;
   RP_TRY0(gemm(g, c.st));
-  if (splits > 1) return splitk_reduce(c.splitk, splits, g.M, g.N, static_cast<float*>(const_cast<void*>(C.p)), C.ld,
+  if (splits > 1) return splitk_reduce(c.splitk, splits, g.batch * g.M, g.N, static_cast<float*>(const_cast<void*>(C.p)), C.ld,
                                        c.st);
   return RP_OK;
 }
@@ -232,8 +235,8 @@ bool fork_enabled() {
 
 }  // namespace
 
-int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes) {
-  return choose_splits(M, N, K, 256, cap_bytes);
+int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes, int64_t batch) {
+  return choose_splits(M, N, K, 256, cap_bytes, batch);
 }
 
 // ---------------------------------------------------------------------------

@@ -36,8 +36,8 @@ int tma_map_bf16(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows,
 // 3-d bf16 map {inner, rows, batch} for 32 x 32 TMA store tiles staged with the 64B swizzle
 int tma_map_bf16_store32(CUtensorMap* map, const void* ptr, int64_t inner, int64_t rows, int64_t ld, int64_t batch);
 int gemm_tile_n(int64_t M, int64_t N, int64_t batch);
-// split count for a batch-1 fp32 GEMM (layers.cpp choose_splits); 1 = no split
-int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes);
+// split count for an fp32 store GEMM of `batch` matrices (layers.cpp choose_splits); 1 = no split
+int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int64_t cap_bytes, int64_t batch = 1);
 int splitk_reduce(const float* part, int S, int64_t M, int64_t N, float* out, int64_t ldo, cudaStream_t st);
 int tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t cols, int64_t ld_src, int64_t ld_dst,
                cudaStream_t stream);

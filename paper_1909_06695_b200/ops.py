@@ -223,10 +223,13 @@ def gemm(
         args.target_logit = target_logit.data_ptr()
     args.ce_scale = ce_scale
     splits = 1
-    if out is not None and out.dtype == torch.float32 and epilogue == N.EPI_STORE and batch == 1 and k_lo_off is None:
-        # deterministic split-K for weight-gradient shapes (few tiles, long K),
-        # the same rule and scratch size as the native composites (layers.cpp)
-        splits = N.lib().rp_gemm_choose_splits(M, Nn, K, SPLITK_CAP)
+    rows_fold = batch == 1 or (out is not None and args.stride_c == M * args.ldc)
+    if (out is not None and out.dtype == torch.float32 and epilogue == N.EPI_STORE and rows_fold
+            and k_lo_off is None):
+        # deterministic split-K for weight-gradient shapes (few tiles, long K;
+        # batched: the XL dR GEMM, 8 heads x 8 key tiles), the same rule and
+        # scratch size as the native composites (layers.cpp)
+        splits = N.lib().rp_gemm_choose_splits(M, Nn, K, batch, SPLITK_CAP)
     if splits > 1:
         part = _splitk_scratch(out.device)
         args.k_splits = splits
@@ -236,7 +239,7 @@ def gemm(
         N.check(N.lib().rp_gemm(ctypes.byref(args), _stream()), "gemm")
         if splits > 1:
             _count(1)
-            N.check(N.lib().rp_splitk_reduce(_ptr(part), splits, M, Nn, _ptr(out), out.stride(-2), _stream()),
+            N.check(N.lib().rp_splitk_reduce(_ptr(part), splits, batch * M, Nn, _ptr(out), out.stride(-2), _stream()),
                     "splitk_reduce")
     return out
 
