@@ -469,13 +469,25 @@ def run_ours(args, c):
     K, B, T = job.K, job.B, job.T
     pipeline = job.pipeline
     tokens_step = B * T * (1 if pipeline else world)
-    for _ in range(max(3, args.warmup) + K):
+    for _ in range(K):  # fill the stale slots, checking every step
         job.step(sync=True)
+    # the host issues each step while the device runs the previous one and
+    # reads that step's loss one step later (engine.step(sync="lagged")); it
+    # never queues further ahead: with several steps queued, a full launch
+    # queue on one stream blocks the host from feeding the others and the
+    # modules' streams lose their overlap (measured: sync=False windows
+    # 13.7-14.9 ms/step against 13.5 at C3)
+    step_sync = False if job.pipeline else "lagged"
+    for _ in range(max(3, args.warmup)):  # warm-up steps issued exactly like the timed ones
+        job.step(sync=step_sync)
+    if step_sync == "lagged":
+        job.flush()
     torch.cuda.synchronize()
+    job.check()
 
     clocks = ClockSampler(local).__enter__()
     # ---- 1. device-resident timed window (the headline `value`)
-    ms = _max_over_ranks(_timed(job, args.steps, barrier), dist)
+    ms = _max_over_ranks(_timed(job, args.steps, barrier, sync=step_sync), dist)
     job.check()
     ms_per_step = ms / args.steps
     value = tokens_step * args.steps / (ms / 1e3)
@@ -608,7 +620,9 @@ def run_ours(args, c):
                                        + (f", {args.micro} micro-batches" if args.micro > 1 else "")
                                        if pipeline else
                                        f"ouroboros K={K} per GPU" + (" (replicas)" if world > 1 else "")),
-                       "l2": "working set per step >> 126 MB L2 (no flush needed)"},
+                       "l2": "working set per step >> 126 MB L2 (no flush needed)",
+                       "issue": ("engine.step(sync=True)" if pipeline else
+                                 "engine.step(sync='lagged'): the host stays one step ahead of the device")},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 2 * B * T * 8,
                     "d2h_bytes_per_step": 4 + 4 * (len(job_mods) + 1), "window": "median of 3 windows of K steps",
                     "api": ("engine.step(t, host batch, optimizer, sync=True) per step" if pipeline else
@@ -654,9 +668,14 @@ def main():
     ap.add_argument("--no-fp32", dest="fp32", action="store_false", help="skip the fp32 check-mode line")
     ap.add_argument("--no-compare-k1", dest="compare_k1", action="store_false",
                     help="skip the K=1 backprop run that gives speedup_vs_k1 (BASELINE metric, second half)")
+    ap.add_argument("--dropout", type=float, default=None,
+                    help="override the config's dropout probability (A/B of the mask cost; not a bench line)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.dropout is not None:
+        c["p"] = args.dropout
+        c["name"] += f"-dropout{args.dropout:g}"
     if args.impl == "reference":
         run_reference(args, c)
     else:

@@ -361,6 +361,7 @@ int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, 
 #define RP_XL_FUSED_BWD 2 /* rp_xl_attn_bwd (bf16, dh 64 / 128, T % 8 == 0) */
 #define RP_XL_FUSED_PV 4  /* rp_xl_attn_fwd_pv (bf16, dh 64) */
 #define RP_XL_FUSED_DQ 8  /* rp_xl_attn_bwd_dq (bf16, dh 64, T % 128 == 0) */
+#define RP_XL_BANDED 16   /* dK / dV GEMMs skip the causal window's all-zero query blocks (bitwise the dense result) */
 typedef struct rp_xl_block_desc {
   int64_t B, T, M, d, f;
   int32_t H, dtype;

@@ -103,7 +103,7 @@ class ModuleDesc(ctypes.Structure):
                 ("M", ctypes.c_int64), ("xl_fused", ctypes.c_int32), ("score_tile", ctypes.c_int32)]
 
 
-XL_FUSED_FWD, XL_FUSED_BWD, XL_FUSED_PV, XL_FUSED_DQ = 1, 2, 4, 8
+XL_FUSED_FWD, XL_FUSED_BWD, XL_FUSED_PV, XL_FUSED_DQ, XL_BANDED = 1, 2, 4, 8, 16
 
 
 class XlBlockDesc(ctypes.Structure):

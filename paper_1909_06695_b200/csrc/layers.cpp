@@ -96,6 +96,8 @@ struct Epi {
   float* target_logit = nullptr;
   float ce_scale = 0.f;
   int tile_n = 0;  // N tile override (0: the library default)
+  int64_t k_lo_off = 0;  // banded A: row m of op(A) is zero for k < m + k_lo_off (with k_lo = 1)
+  int k_lo = 0;
 };
 
 int split_into(Ctx& c, Bump& b, const Mat& m, const void** hi, const void** lo, int64_t* ld, int64_t* bs) {
@@ -152,6 +154,8 @@ int mm(Ctx& c, const Mat& A, bool a_mn, const Mat& B, bool b_mn, const Mat& C, i
   g.C = const_cast<void*>(C.p);
   g.ldc = C.ld;
   g.stride_c = C.bstride;
+  g.k_lo_sign = e.k_lo;
+  g.k_lo_off = e.k_lo_off;
   int splits = 1;
   // batched split-K needs the batch's output rows contiguous (one [batch*M, N] reduce)
   const bool rows_fold = g.batch == 1 || g.stride_c == g.M * g.ldc;
@@ -565,7 +569,12 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
   bwd += al256(kBlockSplitK);
   b = std::max(fwd, bwd);
-  b += split_bytes(d.dtype, std::max({x.HB * x.T * x.ldk, x.B * x.Kl * 3 * x.D, x.N * x.F, x.D * x.F}));
+  // tf32x3 split scratch: the largest operand of any contraction of the block,
+  // rows padded to 4 floats (split_into)
+  auto pd = [](int64_t rows, int64_t cols) { return rows * ((cols + 3) / 4 * 4); };
+  b += split_bytes(d.dtype, std::max({pd(x.HB * x.T, x.ldk), pd(x.B * x.Kl, 3 * x.D), pd(x.N, x.F), pd(x.D, x.F),
+                                      pd(x.F, x.D), pd(x.D, 3 * x.D), pd(x.HB * x.Kl, x.dh), pd(x.H * x.N, x.dh),
+                                      pd(x.Kl, x.D), pd(x.B * x.Kl, x.D)}));
   return b + 4096;
 }
 
@@ -728,15 +737,20 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
               RP_F32, es));
     RP_TRY(xl_softmax_bwd(dt, g_p, x.ldk, tp.probs, x.ldk, g_ac, g_bd, x.HB * x.T, x.T, x.M, d.mem_len, scale, st));
   }
+  // P^T and dAC^T are banded (key j sees queries i >= j - M): with
+  // RP_XL_BANDED the key tiles start their query loop at the first live block
+  Epi eband;
+  eband.k_lo = (d.fused & RP_XL_BANDED) ? 1 : 0;
+  eband.k_lo_off = -x.M;
   RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true, bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh),
-            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32, eband));
   const Mat gac = bmat(g_ac, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk);
   const Mat gbd = bmat(g_bd, x.H, N, x.Kl, x.ldk, N * x.ldk);
   if (!dq_done)
     RP_TRY(mm(c, gac, false, bmat(tp.kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), RP_F32));
   RP_TRY(mm(c, gac, true, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true,
-            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32, eband));
   if (!dq_done)
     RP_TRY(mm(c, gbd, false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));

@@ -10,6 +10,7 @@
 // second pass sums partials in fixed order, so results are bitwise
 // reproducible for a given shape.
 #include <cstdlib>
+#include <initializer_list>
 #include <utility>
 #include <algorithm>
 
@@ -54,31 +55,62 @@ template <> struct V4<__nv_bfloat16> {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Vectorised variants (d % 128 == 0): lane owns 4 consecutive columns per
-// 128-column group, NG groups per row.
+// VW-wide vector load/store of T as fp32 (VW = 4: 16 B of fp32 / 8 B of
+// bf16; VW = 2: 8 B / 4 B -- even widths whose fp32 rows are only 8-byte
+// aligned, e.g. BASELINE configs[3]'s d 410).
+template <typename T, int VW> struct VecIO;
+template <typename T> struct VecIO<T, 4> {
+  static __device__ __forceinline__ void ld(const T* p, float (&v)[4]) { V4<T>::ld(p, v); }
+  static __device__ __forceinline__ void st(T* p, const float (&v)[4]) { V4<T>::st(p, v); }
+};
+template <> struct VecIO<float, 2> {
+  static __device__ __forceinline__ void ld(const float* p, float (&v)[2]) {
+    const float2 f = *reinterpret_cast<const float2*>(p);
+    v[0] = f.x; v[1] = f.y;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&v)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+template <> struct VecIO<__nv_bfloat16, 2> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float (&v)[2]) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    v[0] = a.x; v[1] = a.y;
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16* p, const float (&v)[2]) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v[0], v[1]);
+  }
+};
 
-template <typename T, int NG>
+// ---------------------------------------------------------------------------
+// Vectorised variants: lane owns VW consecutive columns per (32*VW)-column
+// group, NG groups per row (a ragged last group is masked).  Rows of the
+// compute-dtype tensors sit at their pitches (ldx / ldy / ldm: padded bf16
+// rows), fp32 rows at d.
+
+template <typename T, int NG, int VW = 4>
 __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restrict__ x, const float* __restrict__ g,
                                                                  const float* __restrict__ b, T* __restrict__ y,
                                                                  float* __restrict__ mean, float* __restrict__ rstd,
-                                                                 int64_t rows, int d, int32_t* flag) {
+                                                                 int64_t rows, int d, int32_t* flag, int64_t ldx,
+                                                                 int64_t ldy) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
-  float v[NG][4];
+  float v[NG][VW];
   float s = 0.f;
   bool finite = true;
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    if ((i * 32 + lane) * 4 < d) {
-      V4<T>::ld(x + row * d + (i * 32 + lane) * 4, v[i]);
+    if ((i * 32 + lane) * VW < d) {
+      VecIO<T, VW>::ld(x + row * ldx + (i * 32 + lane) * VW, v[i]);
     } else {
-      v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
+#pragma unroll
+      for (int q = 0; q < VW; ++q) v[i][q] = 0.f;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < VW; ++q) {
       finite &= isfinite(v[i][q]);
       s += v[i][q];
     }
@@ -87,20 +119,21 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restr
   float qv = 0.f;
 #pragma unroll
   for (int i = 0; i < NG; ++i)
-    if ((i * 32 + lane) * 4 < d) {
+    if ((i * 32 + lane) * VW < d) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) qv += (v[i][q] - mu) * (v[i][q] - mu);
+      for (int q = 0; q < VW; ++q) qv += (v[i][q] - mu) * (v[i][q] - mu);
     }
   const float rs = rsqrtf(warp_sum(qv) / d + kLnEps);
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const int j = (i * 32 + lane) * 4;
+    const int j = (i * 32 + lane) * VW;
     if (j >= d) continue;
-    const float4 gg = *reinterpret_cast<const float4*>(g + j);
-    const float4 bb = *reinterpret_cast<const float4*>(b + j);
-    float o[4] = {(v[i][0] - mu) * rs * gg.x + bb.x, (v[i][1] - mu) * rs * gg.y + bb.y,
-                  (v[i][2] - mu) * rs * gg.z + bb.z, (v[i][3] - mu) * rs * gg.w + bb.w};
-    V4<T>::st(y + row * d + j, o);
+    float gg[VW], bb[VW], o[VW];
+    VecIO<float, VW>::ld(g + j, gg);
+    VecIO<float, VW>::ld(b + j, bb);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) o[q] = (v[i][q] - mu) * rs * gg[q] + bb[q];
+    VecIO<T, VW>::st(y + row * ldy + j, o);
   }
   if (lane == 0) {
     mean[row] = mu;
@@ -109,71 +142,81 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_v4_kernel(const T* __restr
   if (!__all_sync(0xffffffffu, finite) && lane == 0) flag_set(flag, RP_FLAG_NONFINITE);
 }
 
-template <typename T, int NG>
+template <typename T, int NG, int VW = 4>
 __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
     const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
-    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d, int64_t ldx, int64_t ldm) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // wide rows (NG > 4, d >= 1024): the gain and the residual gradient are
-  // read where they are used instead of living in registers
-  constexpr bool kLean = NG > 4;
-  __shared__ float red[kRowWarps][2][128];
+  constexpr int GW = 32 * VW;  // columns per group
+  // wide rows (NG > 4 groups of 128, d >= 1024): the gain and the residual
+  // gradient are read where they are used instead of living in registers
+  constexpr bool kLean = NG * VW > 16;
+  __shared__ float red[kRowWarps][2][GW];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float acc_g[NG][4], acc_b[NG][4], gv[kLean ? 1 : NG][4];
+  float acc_g[NG][VW], acc_b[NG][VW], gv[kLean ? 1 : NG][VW];
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
     if constexpr (!kLean) {
-      const float4 gg = (i * 32 + lane) * 4 < d ? *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-      gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+      if ((i * 32 + lane) * VW < d) {
+        VecIO<float, VW>::ld(g + (i * 32 + lane) * VW, gv[i]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VW; ++q) gv[i][q] = 0.f;
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
+    for (int q = 0; q < VW; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
   }
-  auto gain = [&](int i, float (&o)[4]) {
+  auto gain = [&](int i, float (&o)[VW]) {
     if constexpr (kLean) {
-      const float4 gg = (i * 32 + lane) * 4 < d ? *reinterpret_cast<const float4*>(g + (i * 32 + lane) * 4)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-      o[0] = gg.x; o[1] = gg.y; o[2] = gg.z; o[3] = gg.w;
+      if ((i * 32 + lane) * VW < d) {
+        VecIO<float, VW>::ld(g + (i * 32 + lane) * VW, o);
+      } else {
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o[q] = 0.f;
+      }
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = gv[kLean ? 0 : i][q];
+      for (int q = 0; q < VW; ++q) o[q] = gv[kLean ? 0 : i][q];
     }
   };
   const int64_t stride = (int64_t)gridDim.x * kRowWarps;
   for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
     const float mu = mean[row], rs = rstd[row];
-    float xh[NG][4], dyv[NG][4], rv[kLean ? 1 : NG][4];
+    float xh[NG][VW], dyv[NG][VW], rv[kLean ? 1 : NG][VW];
     float s1 = 0.f, s2 = 0.f;
     // every load of the row is issued up front (the residual gradient too):
     // one DRAM round trip per row instead of two
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      const int j = (i * 32 + lane) * 4;
-      if (j >= d) {  // ragged width (d % 128 != 0): columns past d contribute nothing
+      const int j = (i * 32 + lane) * VW;
+      if (j >= d) {  // ragged width: columns past d contribute nothing
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xh[i][q] = dyv[i][q] = 0.f;
-        if constexpr (!kLean) rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+        for (int q = 0; q < VW; ++q) {
+          xh[i][q] = dyv[i][q] = 0.f;
+          if constexpr (!kLean) rv[i][q] = 0.f;
+        }
         continue;
       }
-      V4<T>::ld(x + row * d + j, xh[i]);
-      V4<float>::ld(dy + row * d + j, dyv[i]);
+      VecIO<T, VW>::ld(x + row * ldx + j, xh[i]);
+      VecIO<float, VW>::ld(dy + row * d + j, dyv[i]);
       if constexpr (!kLean) {
         if (resid_grad) {
-          V4<float>::ld(resid_grad + row * d + j, rv[i]);
+          VecIO<float, VW>::ld(resid_grad + row * d + j, rv[i]);
         } else {
-          rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+#pragma unroll
+          for (int q = 0; q < VW; ++q) rv[i][q] = 0.f;
         }
       }
     }
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      float gq[4];
+      float gq[VW];
       gain(i, gq);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < VW; ++q) {
         xh[i][q] = (xh[i][q] - mu) * rs;
         const float t = dyv[i][q] * gq[q];
         s1 += t;
@@ -186,107 +229,116 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
     s2 = warp_sum(s2) / d;
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      const int j = (i * 32 + lane) * 4;
+      const int j = (i * 32 + lane) * VW;
       if (j >= d) continue;
-      float gq[4], r4[4];
+      float gq[VW], r4[VW];
       gain(i, gq);
       if constexpr (kLean) {
         if (resid_grad) {
-          V4<float>::ld(resid_grad + row * d + j, r4);
+          VecIO<float, VW>::ld(resid_grad + row * d + j, r4);
         } else {
-          r4[0] = r4[1] = r4[2] = r4[3] = 0.f;
+#pragma unroll
+          for (int q = 0; q < VW; ++q) r4[q] = 0.f;
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) r4[q] = rv[kLean ? 0 : i][q];
+        for (int q = 0; q < VW; ++q) r4[q] = rv[kLean ? 0 : i][q];
       }
-      float o[4];
+      float o[VW];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gq[q] - s1 - xh[i][q] * s2) + r4[q];
-      V4<float>::st(dx + row * d + j, o);
+      for (int q = 0; q < VW; ++q) o[q] = rs * (dyv[i][q] * gq[q] - s1 - xh[i][q] * s2) + r4[q];
+      VecIO<float, VW>::st(dx + row * d + j, o);
       if (dx_masked) {
         if (drop_on) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < VW; ++q)
             o[q] = dropout_keep_z(dropout_z(seed, (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? o[q] * scale : 0.f;
         }
-        V4<T>::st(dx_masked + row * d + j, o);
+        VecIO<T, VW>::st(dx_masked + row * ldm + j, o);
       }
     }
   }
-  // per-CTA column partials, one 128-column group at a time (warp order fixed)
+  // per-CTA column partials, one group at a time (warp order fixed)
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
     if (i) __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      red[w][0][lane * 4 + q] = acc_g[i][q];
-      red[w][1][lane * 4 + q] = acc_b[i][q];
+    for (int q = 0; q < VW; ++q) {
+      red[w][0][lane * VW + q] = acc_g[i][q];
+      red[w][1][lane * VW + q] = acc_b[i][q];
     }
     __syncthreads();
-    const int which = threadIdx.x >> 7, c = threadIdx.x & 127;
-    float sacc = 0.f;
+    if (threadIdx.x < 2 * GW) {
+      const int which = threadIdx.x / GW, c = threadIdx.x % GW;
+      float sacc = 0.f;
 #pragma unroll
-    for (int q = 0; q < kRowWarps; ++q) sacc += red[q][which][c];
-    if (i * 128 + c < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + i * 128 + c] = sacc;
+      for (int q = 0; q < kRowWarps; ++q) sacc += red[q][which][c];
+      if (i * GW + c < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + i * GW + c] = sacc;
+    }
   }
 }
 
-// Split rows: P warps own one row, each NG 128-column groups (gain and
-// residual gradient in registers).  The one-warp-per-row kernel at d 1024
-// needs ~175 registers, so one CTA (8 warps) fits an SM and too few row loads
-// are in flight; NG 4 keeps 128 registers (two CTAs per SM), NG 2 ~80 (three).
-// The row sums s1, s2 combine the P parts through shared memory (part order,
-// the same in every warp of the row); column partials are summed over the
-// CTA's same-part warps in warp order.
-template <typename T, int NG, int P>
+// Split rows: P warps own one row, each NG groups (gain and residual
+// gradient in registers).  The one-warp-per-row kernel at d 1024 needs ~175
+// registers, so one CTA (8 warps) fits an SM and too few row loads are in
+// flight; NG 4 keeps 128 registers (two CTAs per SM), NG 2 ~80 (three).  The
+// row sums s1, s2 combine the P parts through shared memory (part order, the
+// same in every warp of the row); column partials are summed over the CTA's
+// same-part warps in warp order.
+template <typename T, int NG, int P, int VW = 4>
 __global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
     const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
-    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d) {
+    float* __restrict__ part_g, float* __restrict__ part_b, int64_t rows, int d, int64_t ldx, int64_t ldm) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int GW = 32 * VW;
   constexpr int kRows = kRowWarps / P;  // rows per CTA iteration
-  __shared__ float red[kRowWarps][2][128];
+  __shared__ float red[kRowWarps][2][GW];
   __shared__ float xs[2][kRowWarps][2];  // [iteration parity][warp][s1, s2]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int part = w % P, pair = w / P;
-  const int c0 = part * NG * 128;
-  float acc_g[NG][4], acc_b[NG][4], gv[NG][4];
+  const int c0 = part * NG * GW;
+  float acc_g[NG][VW], acc_b[NG][VW], gv[NG][VW];
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const int j = c0 + (i * 32 + lane) * 4;
-    const float4 gg = j < d ? *reinterpret_cast<const float4*>(g + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-    gv[i][0] = gg.x; gv[i][1] = gg.y; gv[i][2] = gg.z; gv[i][3] = gg.w;
+    const int j = c0 + (i * 32 + lane) * VW;
+    if (j < d) {
+      VecIO<float, VW>::ld(g + j, gv[i]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
+      for (int q = 0; q < VW; ++q) gv[i][q] = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < VW; ++q) acc_g[i][q] = acc_b[i][q] = 0.f;
   }
   const int64_t stride = (int64_t)gridDim.x * kRows;
   int it = 0;
   for (int64_t row = (int64_t)blockIdx.x * kRows + pair; row < rows; row += stride, ++it) {
     const float mu = mean[row], rs = rstd[row];
-    float xh[NG][4], dyv[NG][4], rv[NG][4];
+    float xh[NG][VW], dyv[NG][VW], rv[NG][VW];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      const int j = c0 + (i * 32 + lane) * 4;
+      const int j = c0 + (i * 32 + lane) * VW;
       if (j >= d) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xh[i][q] = dyv[i][q] = rv[i][q] = 0.f;
+        for (int q = 0; q < VW; ++q) xh[i][q] = dyv[i][q] = rv[i][q] = 0.f;
         continue;
       }
-      V4<T>::ld(x + row * d + j, xh[i]);
-      V4<float>::ld(dy + row * d + j, dyv[i]);
+      VecIO<T, VW>::ld(x + row * ldx + j, xh[i]);
+      VecIO<float, VW>::ld(dy + row * d + j, dyv[i]);
       if (resid_grad) {
-        V4<float>::ld(resid_grad + row * d + j, rv[i]);
+        VecIO<float, VW>::ld(resid_grad + row * d + j, rv[i]);
       } else {
-        rv[i][0] = rv[i][1] = rv[i][2] = rv[i][3] = 0.f;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) rv[i][q] = 0.f;
       }
     }
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < VW; ++q) {
         xh[i][q] = (xh[i][q] - mu) * rs;
         const float t = dyv[i][q] * gv[i][q];
         s1 += t;
@@ -313,19 +365,19 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
     s2 /= d;
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      const int j = c0 + (i * 32 + lane) * 4;
+      const int j = c0 + (i * 32 + lane) * VW;
       if (j >= d) continue;
-      float o[4];
+      float o[VW];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
-      V4<float>::st(dx + row * d + j, o);
+      for (int q = 0; q < VW; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
+      VecIO<float, VW>::st(dx + row * d + j, o);
       if (dx_masked) {
         if (drop_on) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < VW; ++q)
             o[q] = dropout_keep_z(dropout_z(seed, (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? o[q] * scale : 0.f;
         }
-        V4<T>::st(dx_masked + row * d + j, o);
+        VecIO<T, VW>::st(dx_masked + row * ldm + j, o);
       }
     }
   }
@@ -333,60 +385,62 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
   for (int i = 0; i < NG; ++i) {
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      red[w][0][lane * 4 + q] = acc_g[i][q];
-      red[w][1][lane * 4 + q] = acc_b[i][q];
+    for (int q = 0; q < VW; ++q) {
+      red[w][0][lane * VW + q] = acc_g[i][q];
+      red[w][1][lane * VW + q] = acc_b[i][q];
     }
     __syncthreads();
-    const int which = threadIdx.x >> 7, c = threadIdx.x & 127;
+    if (threadIdx.x < 2 * GW) {
+      const int which = threadIdx.x / GW, c = threadIdx.x % GW;
 #pragma unroll
-    for (int pp = 0; pp < P; ++pp) {
-      float sacc = 0.f;
+      for (int pp = 0; pp < P; ++pp) {
+        float sacc = 0.f;
 #pragma unroll
-      for (int q = 0; q < kRows; ++q) sacc += red[P * q + pp][which][c];
-      const int col = (pp * NG + i) * 128 + c;
-      if (col < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + col] = sacc;
+        for (int q = 0; q < kRows; ++q) sacc += red[P * q + pp][which][c];
+        const int col = (pp * NG + i) * GW + c;
+        if (col < d) (which ? part_b : part_g)[(int64_t)blockIdx.x * d + col] = sacc;
+      }
     }
   }
 }
 
 // out = g * mask (T) with per-CTA column partials of the masked fp32 values.
-template <typename T, int NG>
+template <typename T, int NG, int VW = 4>
 __global__ void __launch_bounds__(kRowThreads) mask_grad_v4_kernel(const float* __restrict__ g, T* __restrict__ out,
                                                                     int64_t rows, int d, uint64_t seed, uint64_t pos0,
                                                                     uint64_t thr, float scale, int drop_on,
-                                                                    float* __restrict__ part) {
+                                                                    float* __restrict__ part, int64_t ldo) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  __shared__ float red[kRowWarps][128 * NG];
+  __shared__ float red[kRowWarps][32 * VW * NG];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float acc[NG][4];
+  float acc[NG][VW];
 #pragma unroll
   for (int i = 0; i < NG; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+    for (int q = 0; q < VW; ++q) acc[i][q] = 0.f;
   const int64_t stride = (int64_t)gridDim.x * kRowWarps;
   for (int64_t row = (int64_t)blockIdx.x * kRowWarps + w; row < rows; row += stride) {
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      const int j = (i * 32 + lane) * 4;
+      const int j = (i * 32 + lane) * VW;
       if (j >= d) continue;
-      float v[4];
-      V4<float>::ld(g + row * d + j, v);
+      float v[VW];
+      VecIO<float, VW>::ld(g + row * d + j, v);
       if (drop_on) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < VW; ++q)
           v[q] = dropout_keep_z(dropout_z(seed, pos0 + (uint64_t)row * d + j) + (uint64_t)q * kGolden, thr) ? v[q] * scale : 0.f;
       }
-      V4<T>::st(out + row * d + j, v);
+      VecIO<T, VW>::st(out + row * ldo + j, v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[i][q] += v[q];
+      for (int q = 0; q < VW; ++q) acc[i][q] += v[q];
     }
   }
   if (!part) return;
 #pragma unroll
   for (int i = 0; i < NG; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) red[w][(i * 32 + lane) * 4 + q] = acc[i][q];
+    for (int q = 0; q < VW; ++q) red[w][(i * 32 + lane) * VW + q] = acc[i][q];
   __syncthreads();
   for (int j = threadIdx.x; j < d; j += kRowThreads) {
     float s = 0.f;
@@ -736,23 +790,49 @@ int ln_bwd_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
     default: break;                                 \
   }
 
-// 128-column groups per row for the vector kernels: any d % 4 == 0 up to
-// 1024 (a ragged last group is masked); 0 = use the scalar kernels
-inline int ng_for(int64_t d) {
-  if (d % 4 != 0 || d <= 0 || d > 1024) return 0;
-  const int64_t ng = (d + 127) / 128;
-  return ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
+// Vector width and (32*VW)-column groups per row for the vector kernels:
+// VW 4 for d % 4 == 0 up to 1024, VW 2 for even d up to 512 (fp32 rows of an
+// even width are 8-byte aligned: d 410); every compute-dtype pitch must be a
+// multiple of VW.  A ragged last group is masked.  ng 0 = the scalar kernels.
+struct VecShape {
+  int vw = 0, ng = 0;
+};
+inline VecShape vec_for(int64_t d, std::initializer_list<int64_t> pitches = {}) {
+  VecShape v;
+  if (d <= 0) return v;
+  for (int vw : {4, 2}) {
+    if (d % vw || d > 32 * vw * 8) continue;
+    bool ok = true;
+    for (int64_t ld : pitches) ok &= ld % vw == 0;
+    if (!ok) continue;
+    const int64_t ng = (d + 32 * vw - 1) / (32 * vw);
+    v.vw = vw;
+    v.ng = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;
+    return v;
+  }
+  return v;
 }
+inline int ng_for(int64_t d) { return vec_for(d).vw == 4 ? vec_for(d).ng : 0; }
+
+#define RP_VW_DISPATCH(VWV, ...)                              \
+  if ((VWV) == 4) {                                           \
+    constexpr int VW = 4;                                     \
+    __VA_ARGS__;                                              \
+  } else {                                                    \
+    constexpr int VW = 2;                                     \
+    __VA_ARGS__;                                              \
+  }
 
 int layernorm_fwd(int dtype, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
                   int64_t rows, int64_t d, int32_t* flag, cudaStream_t st, int64_t ldx, int64_t ldy) {
   if (rows == 0) return RP_OK;
   if (ldx <= 0) ldx = d;
   if (ldy <= 0) ldy = d;
-  const bool pitched = ldx != d || ldy != d;  // row pitches wider than d: the scalar kernel
-  if (const int ng = pitched ? 0 : ng_for(d)) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_fwd_v4_kernel<T, NG>, row_blocks(rows), kRowThreads, 0, st, 
-                                                    (const T*)x, g, b, (T*)y, mean, rstd, rows, (int)d, flag)));
+  const VecShape vs = vec_for(d, {ldx, ldy});
+  if (vs.ng) {
+    RP_DTYPE_DISPATCH(dtype, RP_VW_DISPATCH(vs.vw, RP_NG_DISPATCH(vs.ng, launch_pdl(
+                                 ln_fwd_v4_kernel<T, NG, VW>, row_blocks(rows), kRowThreads, 0, st, (const T*)x, g, b,
+                                 (T*)y, mean, rstd, rows, (int)d, flag, ldx, ldy))));
     return check_launch("layernorm_fwd");
   }
   const int npl = npl_for(d);
@@ -769,29 +849,32 @@ int layernorm_bwd(int dtype, const float* dy, const void* x, const float* mean, 
   if (rows == 0) return RP_OK;
   if (ldx <= 0) ldx = d;
   if (ldm <= 0) ldm = d;
-  const bool pitched = ldx != d || ldm != d;
   const int nb = ln_bwd_blocks(rows);
-  // warps per row for d > 256 (RP_LN_SPLIT: 1 = one warp per row).  Measured
-  // (tools/ln_bwd_bench.py): d 1024 two warps 106 -> 64 us (four: 70);
-  // d 512 four warps 57 -> 47 us at 22528 rows, 29 -> 23 us at 8192; d 400 27 -> 23 us
+  // warps per row once a lane holds >= 16 elements of the row (RP_LN_SPLIT:
+  // 1 = one warp per row).  Measured (tools/ln_bwd_bench.py): d 1024 two
+  // warps 106 -> 64 us (four: 70); d 512 four warps 57 -> 47 us at 22528
+  // rows, 29 -> 23 us at 8192; d 400 27 -> 23 us
   static const int split_env = getenv("RP_LN_SPLIT") ? atoi(getenv("RP_LN_SPLIT")) : -1;
-  const int ngd = pitched ? 0 : ng_for(d);
-  int split = split_env >= 0 ? split_env : (ngd == 8 ? 2 : ngd == 4 ? 4 : 1);
-  if (ngd < 4) split = 1;
+  const VecShape vs = vec_for(d, {ldx, ldm});
+  const int per_lane = vs.ng * vs.vw;  // row elements per lane with one warp per row
+  int split = split_env >= 0 ? split_env : (per_lane == 32 ? 2 : per_lane == 16 ? 4 : 1);
+  if (per_lane < 16) split = 1;
 #define RP_LN_SPLIT_LAUNCH(NGV, PV)                                                                              \
-  RP_DTYPE_DISPATCH(dtype, launch_pdl(ln_bwd_split_kernel<T, NGV, PV>, nb, kRowThreads, 0, st, dy, (const T*)x, mean, \
-                                      rstd, g, resid_grad, dx, (T*)dx_masked, seed, thr, scale, drop_on, part_g,     \
-                                      part_b, rows, (int)d));                                                        \
+  RP_DTYPE_DISPATCH(dtype, RP_VW_DISPATCH(vs.vw, launch_pdl(ln_bwd_split_kernel<T, NGV, PV, VW>, nb, kRowThreads, 0, \
+                                                            st, dy, (const T*)x, mean, rstd, g, resid_grad, dx,     \
+                                                            (T*)dx_masked, seed, thr, scale, drop_on, part_g,      \
+                                                            part_b, rows, (int)d, ldx, ldm)));                      \
   return check_launch("layernorm_bwd")
-  if (ngd == 8 && split == 2) { RP_LN_SPLIT_LAUNCH(4, 2); }
-  if (ngd == 8 && split == 4) { RP_LN_SPLIT_LAUNCH(2, 4); }
-  if (ngd == 4 && split == 2) { RP_LN_SPLIT_LAUNCH(2, 2); }
-  if (ngd == 4 && split == 4) { RP_LN_SPLIT_LAUNCH(1, 4); }
+  if (vs.ng == 8 && split == 2) { RP_LN_SPLIT_LAUNCH(4, 2); }
+  if (vs.ng == 8 && split == 4) { RP_LN_SPLIT_LAUNCH(2, 4); }
+  if (vs.ng == 4 && split == 2) { RP_LN_SPLIT_LAUNCH(2, 2); }
+  if (vs.ng == 4 && split == 4) { RP_LN_SPLIT_LAUNCH(1, 4); }
 #undef RP_LN_SPLIT_LAUNCH
-  if (const int ng = ngd) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(ln_bwd_v4_kernel<T, NG>, nb, kRowThreads, 0, st,
-                                                    dy, (const T*)x, mean, rstd, g, resid_grad, dx, (T*)dx_masked,
-                                                    seed, thr, scale, drop_on, part_g, part_b, rows, (int)d)));
+  if (vs.ng) {
+    RP_DTYPE_DISPATCH(dtype, RP_VW_DISPATCH(vs.vw, RP_NG_DISPATCH(vs.ng, launch_pdl(
+                                 ln_bwd_v4_kernel<T, NG, VW>, nb, kRowThreads, 0, st, dy, (const T*)x, mean, rstd, g,
+                                 resid_grad, dx, (T*)dx_masked, seed, thr, scale, drop_on, part_g, part_b, rows,
+                                 (int)d, ldx, ldm))));
     return check_launch("layernorm_bwd");
   }
   const int npl = npl_for(d);
@@ -823,12 +906,11 @@ int colsum_finish_multi(const ColsumJob* jobs, int n, cudaStream_t st) {
   return check_launch("colsum_finish_multi");
 }
 
-int mask_grad_blocks(int64_t rows, int64_t d) {
-  return ng_for(d) ? ln_bwd_blocks(rows) : colsum_blocks(rows);
-}
 int mask_grad_blocks_ld(int64_t rows, int64_t d, int64_t ldo) {
-  return (ldo <= 0 || ldo == d) ? mask_grad_blocks(rows, d) : colsum_blocks(rows);
+  if (ldo <= 0) ldo = d;
+  return vec_for(d, {ldo}).ng ? ln_bwd_blocks(rows) : colsum_blocks(rows);
 }
+int mask_grad_blocks(int64_t rows, int64_t d) { return mask_grad_blocks_ld(rows, d, d); }
 
 int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, 128)); }
 
@@ -843,9 +925,11 @@ int mask_grad(int dtype, const float* g, void* out, int64_t rows, int64_t d, uin
               uint64_t thr, float scale, int drop_on, float* part, cudaStream_t st, int64_t ldo) {
   if (d == 0) return RP_OK;
   if (ldo <= 0) ldo = d;
-  if (const int ng = ldo == d ? ng_for(d) : 0) {
-    RP_DTYPE_DISPATCH(dtype, RP_NG_DISPATCH(ng, launch_pdl(mask_grad_v4_kernel<T, NG>, ln_bwd_blocks(rows), kRowThreads, 0, st, 
-                                                    g, (T*)out, rows, (int)d, seed, pos0, thr, scale, drop_on, part)));
+  const VecShape vs = vec_for(d, {ldo});
+  if (vs.ng) {
+    RP_DTYPE_DISPATCH(dtype, RP_VW_DISPATCH(vs.vw, RP_NG_DISPATCH(vs.ng, launch_pdl(
+                                 mask_grad_v4_kernel<T, NG, VW>, ln_bwd_blocks(rows), kRowThreads, 0, st, g, (T*)out,
+                                 rows, (int)d, seed, pos0, thr, scale, drop_on, part, ldo))));
     return check_launch("mask_grad");
   }
   // scalar fallback writes colsum_blocks(rows) partial rows; callers pass

@@ -125,7 +125,40 @@ def fused_dq_ok(tp):
     return FUSED_DQ and fused_bwd_ok(tp) and tp.dh == 64 and tp.T % 128 == 0
 
 
+# The engines run each XL block as ONE C-ABI call (rp_xl_block_forward /
+# _backward: the same kernels in the same order, bitwise equal to the
+# op-by-op path below, tests/test_module_abi_gpu.py) -- ~25 launches per block
+# issued from C++ instead of Python, which keeps the host ahead of the GPU.
+# The op-by-op path runs under the bench's instrumented window (ops.PROBE:
+# per-launch events and FLOP tags), for widths the dense-row composite does
+# not take (bf16 rows of d 410 / head dim 41: pitched), and with RP_XL_NATIVE=0.
+NATIVE = os.environ.get("RP_XL_NATIVE", "1") != "0"
+
+
+def native_ok(tp):
+    if not NATIVE or ops.PROBE is not None:
+        return False
+    if tp.xa.dtype != torch.bfloat16:
+        return True
+    d, f = tp.H * tp.dh, tp.h1.shape[-1]
+    return d % 8 == 0 and f % 8 == 0 and tp.dh % 8 == 0
+
+
 def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
+    """One XL block forward (native composite when native_ok, else op by op)."""
+    if native_ok(tp):
+        return xl_block_forward_native(W, vecs, out, tp, R, drop, ws, flag, rows_total)
+    return xl_block_forward_ops(W, vecs, out, tp, R, drop, ws, flag, rows_total)
+
+
+def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
+    """One XL block backward (native composite when native_ok, else op by op)."""
+    if native_ok(tp):
+        return xl_block_backward_native(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total)
+    return xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total)
+
+
+def xl_block_forward_ops(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
     """tp.xa holds [memory; x]; writes out [B*T, d] and the tape.  rows_total:
     token rows of the whole batch when this is one row block of it (the
     second dropout mask starts at rows_total * d; `drop` is already shifted
@@ -172,7 +205,7 @@ def xl_block_forward(W, vecs, out, tp, R, drop, ws, flag, rows_total=0):
              residual=tp.x1, dropout=d1)
 
 
-def xl_block_backward(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
+def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0):
     """g_out, g_x: [B*T, d] fp32.  No gradient flows into the memory rows;
     their LayerNorm / K / V contributions to the weight gradients do."""
     B, T, M, H, dh, Kl = tp.B, tp.T, tp.M, tp.H, tp.dh, tp.Kl
@@ -290,6 +323,8 @@ def fused_flags(tp):
         f |= N.XL_FUSED_DQ
     elif fused_bwd_ok(tp):
         f |= N.XL_FUSED_BWD
+    if BANDED:
+        f |= N.XL_BANDED
     return f
 
 
