@@ -657,8 +657,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 // stored P (and the head merge of its output) disappear; O is written
 // straight into the merged ctx rows.  Pass 2 keeps one score buffer (TMEM
 // cols 0..255) so O fits beside it.
-constexpr int kFwdPvSmem = 1024 + 2 * 16384 /*Qu, Qv*/ + 3 * 32768 /*K + R band stages*/ + 8192 /*V*/ +
-                           16384 /*P tile*/ + kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 256;
+// NS: K + R band stages; NB: P tile / V tile buffers (NB = 2: the softmax
+// warps write step u+1's P while O += P V of step u still reads step u's)
+template <int NS, int NB>
+constexpr int fwd_pv_smem() {
+  return 1024 + 2 * 16384 /*Qu, Qv*/ + NS * 32768 /*K + R band stages*/ + NB * 8192 /*V*/ + NB * 16384 /*P tile*/ +
+         kSoftWarps * kRingWarp * 4 + 2 * kQT * 2 * 4 /*stats*/ + 256;
+}
 
 struct FwdPvParams {
   FwdParams f;
@@ -666,6 +671,7 @@ struct FwdPvParams {
   int d;
 };
 
+template <int NS, int NB>
 __global__ void __launch_bounds__(kThreadsFwd, 1)
     xl_attn_fwd_pv_kernel(const __grid_constant__ CUtensorMap mQu, const __grid_constant__ CUtensorMap mQv,
                           const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
@@ -678,22 +684,22 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   uint8_t* sQu = smem;
   uint8_t* sQv = smem + C::QBytes;
   uint8_t* stages = smem + 2 * C::QBytes;
-  uint8_t* sV = stages + 3 * C::StageBytes;  // 1024-aligned
-  uint8_t* sP = sV + 8192;
-  float* ring = reinterpret_cast<float*>(sP + 16384);
+  uint8_t* sV0 = stages + NS * C::StageBytes;  // 1024-aligned, NB x 8 KB
+  uint8_t* sP0 = sV0 + NB * 8192;              // NB x 16 KB
+  float* ring = reinterpret_cast<float*>(sP0 + NB * 16384);
   float* stats = ring + kSoftWarps * kRingWarp;  // [half][row][max, sum]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stats + 2 * kQT * 2);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [3]
-  uint64_t* kv_empty = bars + 4;  // [3]
-  uint64_t* s_full = bars + 7;    // [2]
-  uint64_t* s_empty = bars + 9;   // [2]
-  uint64_t* v_full = bars + 11;
-  uint64_t* v_empty = bars + 12;
-  uint64_t* p_full = bars + 13;
-  uint64_t* p_free = bars + 14;
-  uint64_t* o_full = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* kv_full = bars + 1;        // [NS]
+  uint64_t* kv_empty = kv_full + NS;   // [NS]
+  uint64_t* s_full = kv_empty + NS;    // [2]
+  uint64_t* s_empty = s_full + 2;      // [2]
+  uint64_t* v_full = s_empty + 2;      // [NB]
+  uint64_t* v_empty = v_full + NB;     // [NB]
+  uint64_t* p_full = v_empty + NB;     // [NB]
+  uint64_t* p_free = p_full + NB;      // [NB]
+  uint64_t* o_full = p_free + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int hb, qt;
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < 3; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
@@ -732,10 +738,12 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
       mbar_init(&s_full[bb], 1);
       mbar_init(&s_empty[bb], kSoftWarps * 32);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
-    mbar_init(p_full, kSoftWarps * 32);
-    mbar_init(p_free, 1);
+    for (int bb = 0; bb < NB; ++bb) {
+      mbar_init(&v_full[bb], 1);
+      mbar_init(&v_empty[bb], 1);
+      mbar_init(&p_full[bb], kSoftWarps * 32);
+      mbar_init(&p_free[bb], 1);
+    }
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
@@ -762,15 +770,16 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
         mbar_expect_tx(&kv_full[s], C::StageBytes);
         tma_atoms<1>(sk, &mK, &kv_full[s], kFKT, j0, hb);
         tma_atoms<1>(sk + C::KBytes, &mR, &kv_full[s], kFBand, p.T - kQT - i0 + j0, h);
-        if (++s == 3) {
+        if (++s == NS) {
           s = 0;
           ph ^= 1;
         }
         if (n >= per_pass) {
           const int u = n - per_pass;  // V of pass-2 step u, MN-major B of O += P V
-          mbar_wait(v_empty, (u & 1) ^ 1);
-          mbar_expect_tx(v_full, 8192);
-          tma_load_3d(sV, &mV, v_full, 0, j0, hb);
+          const int vb = u % NB;
+          mbar_wait(&v_empty[vb], ((u / NB) & 1) ^ 1);
+          mbar_expect_tx(&v_full[vb], 8192);
+          tma_load_3d(sV0 + vb * 8192, &mV, &v_full[vb], 0, j0, hb);
         }
       }
     }
@@ -780,18 +789,20 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
       const uint32_t id_ac = umma_idesc(false, false, false, kQT, kFKT);
       const uint32_t id_bd = umma_idesc(false, false, false, kQT, kFBand);
       const uint32_t id_pv = umma_idesc(false, false, true, kQT, 64);
-      const uint32_t qa = smem_u32(sQu), qb = smem_u32(sQv), pa = smem_u32(sP), va = smem_u32(sV);
+      const uint32_t qa = smem_u32(sQu), qb = smem_u32(sQv), pa0 = smem_u32(sP0), va0 = smem_u32(sV0);
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int u) {
-        mbar_wait(p_full, u & 1);
-        mbar_wait(v_full, u & 1);
+        const int pb = u % NB;
+        const uint32_t pa = pa0 + pb * 16384, va = va0 + pb * 8192;
+        mbar_wait(&p_full[pb], (u / NB) & 1);
+        mbar_wait(&v_full[pb], (u / NB) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           tc_mma<false>(t_o, umma_desc(pa + 32 * k, 16, 1024), umma_desc(va + k * 2048, 8192, 1024), id_pv,
                         (u | k) != 0);
-        tc_commit(p_free);
-        tc_commit(v_empty);
+        tc_commit(&p_free[pb]);
+        tc_commit(&v_empty[pb]);
       };
       int s = 0;
       uint32_t ph = 0;
@@ -810,7 +821,7 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
           tc_mma<false>(d + kFKT, atom_desc<1>(qb, kQT, k), atom_desc<1>(rb, kFBand, k), id_bd, k > 0);
         tc_commit(&kv_empty[s]);
         tc_commit(&s_full[buf]);
-        if (++s == 3) {
+        if (++s == NS) {
           s = 0;
           ph ^= 1;
         }
@@ -835,7 +846,6 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
     const int cb0 = 96 - 32 * q + 32 * half;
     const int off = 31 - lane;
     __nv_bfloat16* prow = p.p + ((int64_t)hb * p.T + i) * p.ldp;
-    uint8_t* prow_s = sP + r * 128;
     const int rsw = r & 7;
     float m = -INFINITY, l = 0.f, inv = 0.f;
     for (int n = 0; n < nsteps; ++n) {
@@ -908,22 +918,27 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
           __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2(sv[2 * t] - m) * inv, ex2(sv[2 * t + 1] - m) * inv);
           w[t] = row_ok ? *reinterpret_cast<uint32_t*>(&b2) : 0u;
         }
-        // the P tile is free once O += P V of the previous step and this
+        // P tile buffer u % NB is free once O += P V of step u - NB and this
         // quarter's TMA store of it have read it
-        if (u >= 1) mbar_wait(p_free, (u - 1) & 1);
-        if (half == 0 && lane == 0) tma_store_wait_read();
+        const int pb = u % NB;
+        uint8_t* sPb = sP0 + pb * 16384;
+        if (u >= NB) mbar_wait(&p_free[pb], ((u / NB) - 1) & 1);
+        if (half == 0 && lane == 0) {
+          if constexpr (NB == 1) tma_store_wait_read();
+          else bulk_wait_read_1();  // the newest store reads the other buffer
+        }
         named_sync(2 + q, 64);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          *reinterpret_cast<uint4*>(prow_s + (((4 * half + c) ^ rsw) << 4)) =
+          *reinterpret_cast<uint4*>(sPb + r * 128 + (((4 * half + c) ^ rsw) << 4)) =
               make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
         fence_proxy_async_smem();
-        mbar_arrive(p_full);
+        mbar_arrive(&p_full[pb]);
         named_sync(2 + q, 64);
         // this quarter's 32 rows x 64 keys of P (the map clips rows past T and columns past ldp)
         const int j0 = jb - 32 * half;
         if (half == 0 && lane == 0 && j0 < p.ldp && i0 + 32 * q < p.T)
-          tma_store_3d_p(&mP, sP + 32 * q * 128, j0, i0 + 32 * q, hb);
+          tma_store_3d_p(&mP, sPb + 32 * q * 128, j0, i0 + 32 * q, hb);
       }
     }
     // ---- O = P V: rows of this lane quarter, head columns [32 half, +32) -> merged ctx
@@ -1453,9 +1468,13 @@ int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* v
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kFBand));
   RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kFKT));
   RP_TRY0(tma_map_bf16(&mp, probs, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
+  // RP_XL_PV_BUF: 1 = one P / V tile and three K + R stages; 2 = double-buffered P / V, two stages
+  static const int pv_buf = getenv("RP_XL_PV_BUF") ? atoi(getenv("RP_XL_PV_BUF")) : 2;
   static uint64_t attr_done = 0;
-  if (first_on_device(attr_done))
-    cudaFuncSetAttribute(xl_attn_fwd_pv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdPvSmem);
+  if (first_on_device(attr_done)) {
+    cudaFuncSetAttribute(xl_attn_fwd_pv_kernel<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_pv_smem<3, 1>());
+    cudaFuncSetAttribute(xl_attn_fwd_pv_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_pv_smem<2, 2>());
+  }
   FwdPvParams pp{};
   FwdParams& p = pp.f;
   p.p = static_cast<__nv_bfloat16*>(probs);
@@ -1473,7 +1492,10 @@ int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* v
   pp.d = H * dh;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
-  xl_attn_fwd_pv_kernel<<<(unsigned)grid, kThreadsFwd, kFwdPvSmem, st>>>(mqu, mqv, mk, mr, mv, mp, pp);
+  if (pv_buf == 1)
+    xl_attn_fwd_pv_kernel<3, 1><<<(unsigned)grid, kThreadsFwd, fwd_pv_smem<3, 1>(), st>>>(mqu, mqv, mk, mr, mv, mp, pp);
+  else
+    xl_attn_fwd_pv_kernel<2, 2><<<(unsigned)grid, kThreadsFwd, fwd_pv_smem<2, 2>(), st>>>(mqu, mqv, mk, mr, mv, mp, pp);
   return check_launch("xl_attn_fwd_pv");
 }
 
