@@ -375,15 +375,14 @@ class _Job:
             x = y = None  # tokens and targets live on the Ouroboros rank only
         b = self.E.BatchSample(x, y, self.t)
         if self.pipeline:
-            self.eng.step(self.t, b, self.opt, sync=bool(sync), shape=(self.B, self.T))
+            self.eng.step(self.t, b, self.opt, sync=sync, shape=(self.B, self.T))
         else:
             self.eng.step(self.t, b, self.opt, sync=sync)
         self.t += 1
 
     def flush(self):
         """Read the last step's result (sync="lagged" leaves one in flight)."""
-        if not self.pipeline:
-            self.eng.flush_lagged()
+        self.eng.flush_lagged()
 
     def check(self):
         self.stack.runtime.check("bench", self.mods)
@@ -477,7 +476,7 @@ def run_ours(args, c):
     # queue on one stream blocks the host from feeding the others and the
     # modules' streams lose their overlap (measured: sync=False windows
     # 13.7-14.9 ms/step against 13.5 at C3)
-    step_sync = False if job.pipeline else "lagged"
+    step_sync = "lagged"
     for _ in range(max(3, args.warmup)):  # warm-up steps issued exactly like the timed ones
         job.step(sync=step_sync)
     if step_sync == "lagged":
@@ -621,12 +620,10 @@ def run_ours(args, c):
                                        if pipeline else
                                        f"ouroboros K={K} per GPU" + (" (replicas)" if world > 1 else "")),
                        "l2": "working set per step >> 126 MB L2 (no flush needed)",
-                       "issue": ("engine.step(sync=True)" if pipeline else
-                                 "engine.step(sync='lagged'): the host stays one step ahead of the device")},
+                       "issue": "engine.step(sync='lagged'): the host stays one step ahead of the device"},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 2 * B * T * 8,
                     "d2h_bytes_per_step": 4 + 4 * (len(job_mods) + 1), "window": "median of 3 windows of K steps",
-                    "api": ("engine.step(t, host batch, optimizer, sync=True) per step" if pipeline else
-                            "engine.step(t, host batch, optimizer, sync='lagged'): pinned H2D of the step's tokens "
+                    "api": ("engine.step(t, host batch, optimizer, sync='lagged'): pinned H2D of the step's tokens "
                             "and targets, D2H of its loss + status words, each read on the host one step later; "
                             "the window ends after the last step's loss is read"),
                     "windows_ms_per_step": [round(w / args.steps, 3) for w in windows]},

@@ -304,6 +304,12 @@ class DistributedPipelineEngine:
                 x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64))
                 y = torch.from_numpy(np.ascontiguousarray(y, dtype=np.int64))
             if S.gpu:
+                if not x.is_cuda:  # host batches: range-checked, staged through pinned memory
+                    V = getattr(self.tied, "vocab", None)
+                    for a, what in ((x, "token"), (y, "target")):
+                        if V is not None and a.numel() and (int(a.min()) < 0 or int(a.max()) >= V):
+                            raise DimensionError(f"{what} id out of range [0, {V})")
+                    x, y = x.pin_memory(), y.pin_memory()
                 x = x.to(self.device, non_blocking=True)
                 y = y.to(self.device, non_blocking=True)
             B, T = x.shape
@@ -387,6 +393,20 @@ class DistributedPipelineEngine:
         if optimizer is not None and not split:
             optimizer.apply(t, packet, mods, self.tied.master if self.tied is not None else None)
         self.last_loss_device = loss
+        if sync == "lagged" and S.gpu:
+            # the host stays one step ahead: step t-1's loss / status words
+            # are read (pinned D2H) after step t was issued
+            from .engine import LaggedReader
+
+            if getattr(self, "_lag", None) is None:
+                self._lag = LaggedReader(self.device)
+            rt = getattr(mods[0], "runtime", None)
+            try:
+                prev = self._lag.submit(t, loss, mods, rt.flag)
+            except (NonFiniteError, DimensionError) as exc:
+                raise WorkerFailure(f"distributed schedule aborted on rank {self.rank}: "
+                                    f"{type(exc).__name__}: {exc}") from exc
+            return packet, prev
         if sync and S.gpu:
             rt = getattr(mods[0], "runtime", None)
             if rt is not None:
@@ -399,6 +419,17 @@ class DistributedPipelineEngine:
                 loss = float(loss.item())
                 packet.loss = loss
         return packet, loss
+
+    def flush_lagged(self):
+        """sync="lagged": the last step's host loss on rank 0 (waits for it)."""
+        lag = getattr(self, "_lag", None)
+        if lag is None:
+            return None
+        try:
+            return lag.flush()
+        except (NonFiniteError, DimensionError) as exc:
+            raise WorkerFailure(f"distributed schedule aborted on rank {self.rank}: "
+                                f"{type(exc).__name__}: {exc}") from exc
 
     def _flag(self):
         m = next(iter(self.mods.values()))

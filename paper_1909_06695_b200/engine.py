@@ -202,6 +202,58 @@ def _to_device_tokens(a, device, vocab=None, what="token"):
     return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
 
 
+class LaggedReader:
+    """sync="lagged": queue the D2H copy of step t's loss and status words
+    into pinned host memory (no host wait) and hand back the previous step's
+    host loss after checking its status words -- the host stays one step
+    ahead of the device and still reads every step's result."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs = None
+        self.pending = None
+
+    def submit(self, t, loss_dev, modules, runtime_flag):
+        words = [m.flag for m in modules] + [runtime_flag]
+        if self.bufs is None or self.bufs[0][1].numel() != len(words):
+            pin = lambda n, dt: torch.zeros(n, dtype=dt).pin_memory()  # noqa: E731
+            self.bufs = [(pin(1, torch.float32), pin(len(words), torch.int32)) for _ in range(2)]
+        hl, hw = self.bufs[t % 2]
+        main = torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(main):
+            if loss_dev is not None:
+                hl.copy_(loss_dev.detach().reshape(1).float(), non_blocking=True)
+            for i, w in enumerate(words):
+                hw[i: i + 1].copy_(w.view(1), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(main)
+        prev, self.pending = self.pending, (t, ev, hl if loss_dev is not None else None, hw, words, modules)
+        return self._read(prev)
+
+    def flush(self):
+        entry, self.pending = self.pending, None
+        return self._read(entry)
+
+    @staticmethod
+    def _read(entry):
+        from . import _native as N
+
+        if entry is None:
+            return None
+        t, ev, hl, hw, words, modules = entry
+        ev.synchronize()
+        bad = [(i, int(b)) for i, b in enumerate(hw.tolist()) if b]
+        if bad:
+            for w in words:
+                w.zero_()
+            i, bits = bad[0]
+            where = f"module {modules[i].index}" if i < len(modules) else "optimizer update"
+            if bits & N.FLAG_DIMENSION:
+                raise DimensionError(f"token or target id out of range in {where} (step {t})")
+            raise NonFiniteError(f"non-finite values in {where} (step {t})")
+        return None if hl is None else float(hl.item())
+
+
 class _DeviceClock:
     """CUDA-event timing of (step, module, phase) spans for ScheduleTrace:
     events are recorded on the stream the work runs on and resolved to
@@ -362,51 +414,14 @@ class PipelineEngine:
 
     # -- lagged result read (sync="lagged") --------------------------------------
     def _lag_submit(self, t, loss_dev):
-        """Queue the D2H copy of step t's loss and status words into pinned
-        host memory (no host wait); returns the previous step's host loss after
-        checking its status words (raising like the synchronous check)."""
-        words = [m.flag for m in self.modules] + [self.runtime.flag]
         if getattr(self, "_lag", None) is None:
-            pin = lambda n, dt: torch.zeros(n, dtype=dt).pin_memory()  # noqa: E731
-            self._lag = {"bufs": [(pin(1, torch.float32), pin(len(words), torch.int32)) for _ in range(2)],
-                         "pending": None}
-        lag = self._lag
-        hl, hw = lag["bufs"][t % 2]
-        main = torch.cuda.current_stream(self.device)
-        with torch.cuda.stream(main):
-            hl.copy_(loss_dev.detach().reshape(1).float(), non_blocking=True)
-            for i, w in enumerate(words):
-                hw[i: i + 1].copy_(w.view(1), non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(main)
-        prev, lag["pending"] = lag["pending"], (t, ev, hl, hw, words)
-        return self._lag_read(prev)
-
-    def _lag_read(self, entry):
-        from . import _native as N
-
-        if entry is None:
-            return None
-        t, ev, hl, hw, words = entry
-        ev.synchronize()
-        bad = [(i, int(b)) for i, b in enumerate(hw.tolist()) if b]
-        if bad:
-            for w in words:
-                w.zero_()
-            i, bits = bad[0]
-            where = f"module {self.modules[i].index}" if i < len(self.modules) else "optimizer update"
-            if bits & N.FLAG_DIMENSION:
-                raise DimensionError(f"token or target id out of range in {where} (step {t})")
-            raise NonFiniteError(f"non-finite values in {where} (step {t})")
-        return float(hl.item())
+            self._lag = LaggedReader(self.device)
+        return self._lag.submit(t, loss_dev, self.modules, self.runtime.flag)
 
     def flush_lagged(self):
         """sync="lagged": the last step's host loss (waits for it)."""
         lag = getattr(self, "_lag", None)
-        if lag is None:
-            return None
-        entry, lag["pending"] = lag["pending"], None
-        return self._lag_read(entry)
+        return None if lag is None else lag.flush()
 
     # -- public -----------------------------------------------------------------
     def step(self, t, batch, optimizer=None, sync=True):
