@@ -1252,13 +1252,22 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const int c1 = cb + split;
         uint8_t* seg1 = ring + ((c1 >> 7) % kRing3) * kChunkBytes + ((c1 >> 6) & 1) * (128 * 128) + r * 128;
         const int e0 = cb & 63;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const uint32_t w = o[t >> 1];
-          const unsigned short hv = (unsigned short)((t & 1) ? (w >> 16) : (w & 0xffffu));
+        // run element t of this row in the ring (a 4-byte aligned pair never
+        // straddles the 64-column atom boundary: both start parities keep
+        // the pairs inside one atom)
+        auto at = [&](int t) -> uint8_t* {
           const bool lo = t < split;
           const int e = lo ? e0 + t : t - split;
-          *reinterpret_cast<unsigned short*>((lo ? seg0 : seg1) + ((((e >> 3) ^ rsw) << 4) | ((e & 7) << 1))) = hv;
+          return (lo ? seg0 : seg1) + ((((e >> 3) ^ rsw) << 4) | ((e & 7) << 1));
+        };
+        if ((cb & 1) == 0) {  // pairs land on 4-byte words: 16 word stores
+#pragma unroll
+          for (int m = 0; m < 16; ++m) *reinterpret_cast<uint32_t*>(at(2 * m)) = o[m];
+        } else {  // shifted by one element: an edge half-word each side, 15 re-paired words
+          *reinterpret_cast<unsigned short*>(at(0)) = (unsigned short)(o[0] & 0xffffu);
+#pragma unroll
+          for (int m = 0; m < 15; ++m) *reinterpret_cast<uint32_t*>(at(2 * m + 1)) = __byte_perm(o[m], o[m + 1], 0x5432);
+          *reinterpret_cast<unsigned short*>(at(31)) = (unsigned short)(o[15] >> 16);
         }
       }
       if (n == nt - 1 && half == 1) {
