@@ -1184,9 +1184,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       return reinterpret_cast<__nv_bfloat16*>(ring + (bc >> 7) % kRing3 * kChunkBytes + sw128_off(r, bc & 127));
     };
     const __nv_bfloat16 zb = __float2bfloat16_rn(0.f);
+    auto zero_ring = [&](int c0, int c1) {  // band columns [c0, c1) of row r: 16-byte chunks inside
+      int c = c0;
+      for (; c < c1 && (c & 7); ++c) *ring_at(c) = zb;
+      for (; c + 8 <= c1; c += 8) *reinterpret_cast<uint4*>(ring_at(c)) = make_uint4(0u, 0u, 0u, 0u);
+      for (; c < c1; ++c) *ring_at(c) = zb;
+    };
     // band columns before this row's first key (chunk 0)
-    if (half == 0)
-      for (int c = 0; c < 127 - r; ++c) *ring_at(c) = zb;
+    if (half == 0) zero_ring(0, 127 - r);
     for (int n = 0; n < nt; ++n) {
       const int s = n & 1;
       const int jt0 = (jt_lo + n) * kKT + 64 * half;
@@ -1223,6 +1228,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       for (int k = 0; k < 2; ++k) {
         const int jb = jt0 + 32 * k;
         uint32_t o[16];
+        // P is zero outside the window, but dP there is not: mask explicitly
+        // (runs wholly inside the window -- all but the diagonal and memory
+        // edge tiles -- skip the per-element test)
+        const bool inside = jb >= p.lo && jb + 31 <= jhi;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t w[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
@@ -1231,10 +1240,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
             const int t = 8 * c + 2 * e;
             const int j = jb + t;
-            // P is zero outside the window, but dP there is not: mask explicitly
-            const float a0 = (j >= p.lo && j <= jhi) ? pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale : 0.f;
-            const float a1 =
-                (j + 1 >= p.lo && j + 1 <= jhi) ? pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale : 0.f;
+            float a0 = pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale;
+            float a1 = pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale;
+            if (!inside) {
+              a0 = (j >= p.lo && j <= jhi) ? a0 : 0.f;
+              a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? a1 : 0.f;
+            }
             __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
             o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
           }
@@ -1270,10 +1281,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           *reinterpret_cast<unsigned short*>(at(31)) = (unsigned short)(o[15] >> 16);
         }
       }
-      if (n == nt - 1 && half == 1) {
-        // band columns after this row's last key (chunk nt)
-        for (int c = kKT * n + 255 - r; c < kKT * (nt + 1); ++c) *ring_at(c) = zb;
-      }
+      if (n == nt - 1 && half == 1) zero_ring(kKT * n + 255 - r, kKT * (nt + 1));  // after this row's last key
       fence_proxy_async_smem();
       __syncwarp();
       // this warp's 32 x 64 dAC block straight from the swizzled dS tile
