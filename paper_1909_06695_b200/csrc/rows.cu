@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
 // same in every warp of the row); column partials are summed over the CTA's
 // same-part warps in warp order.
 template <typename T, int NG, int P, int VW = 4>
-__global__ void __launch_bounds__(kRowThreads) ln_bwd_split_kernel(
+__global__ void __launch_bounds__(kRowThreads, NG == 1 ? 4 : NG == 2 ? 3 : 2) ln_bwd_split_kernel(
     const float* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const float* __restrict__ g, const float* __restrict__ resid_grad,
     float* __restrict__ dx, T* __restrict__ dx_masked, uint64_t seed, uint64_t thr, float scale, int drop_on,
