@@ -30,7 +30,8 @@ torch.cuda.synchronize()
 steps = 3
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA, torch.profiler.ProfilerActivity.CPU]) as prof:
     for t in range(4, 4 + steps):
-        eng.step(t, E.BatchSample(*dev[t % 2], t), opt, sync=False)
+        eng.step(t, E.BatchSample(*dev[t % 2], t), opt, sync="lagged")
+    eng.flush_lagged()
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 iv = sorted((e.time_range.start, e.time_range.end, e.name) for e in evs)
