@@ -176,11 +176,11 @@ int rp_xl_split_heads(int32_t src_dtype, const void* src, int64_t ld, int32_t ds
 /* dst[r*ld + h*dh + c] = src[h, r, c] */
 int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, void* dst, int64_t ld, int64_t rows,
                       int32_t H, int32_t dh, int64_t ld_h, void* stream);
-/* g_qkv (xa row layout, [B*(M+T), 3d], row pitch ld_qkv) from fp32 head-major
-   dQu, dQv, dK, dV (row pitch ld_g; 0 = dh) */
-int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
+/* g_qkv (xa row layout, [B*(M+T), 3d], row pitch ld_qkv, dtype) from head-major fp32 dQu, dQv
+   (row pitch ld_g; 0 = dh) and dK, dV in `dtype` (row pitch ld_kv) */
+int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const void* g_kh, const void* g_vh,
                       void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
-                      int64_t ld_g, void* stream);
+                      int64_t ld_g, int64_t ld_kv, void* stream);
 /* P = softmax((AC + relshift(BD)) * scale) over keys M-mem_len <= j <= M+i; rows = H*B*T */
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream);

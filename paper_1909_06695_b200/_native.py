@@ -209,7 +209,7 @@ def _declare(L):
         "rp_xl_split_qkv": [i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, vp],
         "rp_xl_split_heads": [i32, vp, i64, i32, vp, i64, i32, i32, i64, vp],
         "rp_xl_merge_heads": [i32, vp, i32, vp, i64, i64, i32, i32, i64, vp],
-        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, vp],
+        "rp_xl_merge_grads": [i32, vp, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, i64, i64, vp],
         "rp_xl_softmax_fwd": [i32, vp, vp, i64, vp, i64, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd": [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],

@@ -164,10 +164,10 @@ int rp_xl_merge_heads(int32_t src_dtype, const void* src, int32_t dst_dtype, voi
                       int32_t H, int32_t dh, int64_t ld_h, void* stream) {
   return rp::xl_merge_heads(src_dtype, src, dst_dtype, dst, ld, rows, H, dh, RP_S(stream), ld_h);
 }
-int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const float* g_kh, const float* g_vh,
+int rp_xl_merge_grads(int32_t dtype, const float* g_qu, const float* g_qv, const void* g_kh, const void* g_vh,
                       void* g_qkv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t ld_qkv,
-                      int64_t ld_g, void* stream) {
-  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream), ld_qkv, ld_g);
+                      int64_t ld_g, int64_t ld_kv, void* stream) {
+  return rp::xl_merge_grads(dtype, g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh, RP_S(stream), ld_qkv, ld_g, ld_kv);
 }
 int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t ld_scores, void* probs, int64_t ld_p,
                       int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale, void* stream) {

@@ -563,7 +563,7 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   bwd += 2 * al256(x.HB * x.T * x.ldk * e); // g_ac, g_bd
   bwd += al256(x.HB * x.T * x.ldk * 4);     // g_p (unfused)
   bwd += 2 * al256(x.H * x.N * x.dh * 4);   // g_qu, g_qv
-  bwd += 2 * al256(x.HB * x.Kl * x.dh * 4) + al256(x.H * x.Kl * x.dh * 4);  // g_vh, g_kh, g_rh
+  bwd += 2 * al256(x.HB * x.Kl * x.dh * e) + al256(x.H * x.Kl * x.dh * 4);  // g_vh, g_kh (compute dtype), g_rh
   bwd += al256(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh));
   bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
   bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
@@ -687,8 +687,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   float* g_p = static_cast<float*>(bp.take(x.HB * x.T * x.ldk * 4));
   float* g_qu = static_cast<float*>(bp.take(x.H * N * x.dh * 4));
   float* g_qv = static_cast<float*>(bp.take(x.H * N * x.dh * 4));
-  float* g_vh = static_cast<float*>(bp.take(x.HB * x.Kl * x.dh * 4));
-  float* g_kh = static_cast<float*>(bp.take(x.HB * x.Kl * x.dh * 4));
+  void* g_vh = bp.take(x.HB * x.Kl * x.dh * e);  // compute dtype: rounded as g_qkv holds them
+  void* g_kh = bp.take(x.HB * x.Kl * x.dh * e);
   float* g_rh = static_cast<float*>(bp.take(x.H * x.Kl * x.dh * 4));
   float* bias_ws = static_cast<float*>(bp.take(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh)));
   void* g_r = bp.take(x.Kl * D * e);
@@ -743,14 +743,14 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   eband.k_lo = (d.fused & RP_XL_BANDED) ? 1 : 0;
   eband.k_lo_off = -x.M;
   RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true, bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh),
-            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32, eband));
+            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt, eband));
   const Mat gac = bmat(g_ac, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk);
   const Mat gbd = bmat(g_bd, x.H, N, x.Kl, x.ldk, N * x.ldk);
   if (!dq_done)
     RP_TRY(mm(c, gac, false, bmat(tp.kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), RP_F32));
   RP_TRY(mm(c, gac, true, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true,
-            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32, eband));
+            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt, eband));
   if (!dq_done)
     RP_TRY(mm(c, gbd, false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));

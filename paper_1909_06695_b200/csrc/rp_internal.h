@@ -106,9 +106,10 @@ int xl_split_heads(int src_dtype, const void* src, int64_t ld, int dst_dtype, vo
                    cudaStream_t st, int64_t ldh = 0);
 int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t ld, int64_t rows, int H, int dh,
                    cudaStream_t st, int64_t ldh = 0);
-int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
+// gkh / gvh in the compute dtype (the dK / dV GEMMs store them rounded like g_qkv)
+int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const void* gkh, const void* gvh, void* gqkv,
                    int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq = 0,
-                   int64_t ldg = 0);
+                   int64_t ldg = 0, int64_t ldkv = 0);
 int xl_softmax_fwd(int dtype, const float* ac, const float* bd, int64_t lds, void* p, int64_t ldp, int64_t rows,
                    int64_t Tn, int64_t M, int64_t mem_len, float scale, cudaStream_t st);
 int xl_softmax_bwd(int dtype, const float* gp, int64_t lds, const void* p, int64_t ldp, void* gac, void* gbd,

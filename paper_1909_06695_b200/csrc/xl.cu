@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(kRowBlk) merge_heads_rows_kernel(const S* __re
 // g_qkv row (b, j) (pitch ldq) from the head-major fp32 gradients (pitch ldg)
 template <typename T>
 __global__ void __launch_bounds__(kRowBlk) merge_grads_rows_kernel(
-    const float* __restrict__ gqu, const float* __restrict__ gqv, const float* __restrict__ gkh,
-    const float* __restrict__ gvh, T* __restrict__ gqkv, int B, int Tn, int M, int H, int dh, int64_t ldq,
-    int64_t ldg) {
+    const float* __restrict__ gqu, const float* __restrict__ gqv, const T* __restrict__ gkh,
+    const T* __restrict__ gvh, T* __restrict__ gqkv, int B, int Tn, int M, int H, int dh, int64_t ldq,
+    int64_t ldg, int64_t ldkv) {
   const int Kl = M + Tn, d = H * dh;
   const int64_t rows = (int64_t)B * Kl;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -238,10 +238,10 @@ __global__ void __launch_bounds__(kRowBlk) merge_grads_rows_kernel(
         const int64_t o = (hb * Tn + (j - M)) * ldg + c;
         q = gqu[o] + gqv[o];
       }
-      const int64_t ok = (hb * Kl + j) * ldg + c;
+      const int64_t ok = (hb * Kl + j) * ldkv + c;
       dst[col] = from_f<T>(q);
-      dst[d + col] = from_f<T>(gkh[ok]);
-      dst[2 * d + col] = from_f<T>(gvh[ok]);
+      dst[d + col] = gkh[ok];
+      dst[2 * d + col] = gvh[ok];
     }
   }
 }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kRowBlk) merge_grads_rows_kernel(
 // k / v columns from the head-major key gradients.  unit = 8 columns of a row.
 template <typename T>
 __global__ void merge_grads_kernel(const float* __restrict__ gqu, const float* __restrict__ gqv,
-                                   const float* __restrict__ gkh, const float* __restrict__ gvh, T* __restrict__ gqkv,
+                                   const T* __restrict__ gkh, const T* __restrict__ gvh, T* __restrict__ gqkv,
                                    int B, int Tn, int M, int H, int dh) {
   const int Kl = M + Tn, d = H * dh, C3 = 3 * d / 8;
   const int64_t BM = (int64_t)B * M;
@@ -282,7 +282,7 @@ __global__ void merge_grads_kernel(const float* __restrict__ gqu, const float* _
       }
     } else {
       const int64_t o = (((int64_t)h * B + b) * Kl + j) * dh + c;
-      V8<float>::ld((part == 1 ? gkh : gvh) + o, g);
+      V8<T>::ld((part == 1 ? gkh : gvh) + o, g);
     }
     V8<T>::st(gqkv + row * 3 * d + col, g);
   }
@@ -562,21 +562,24 @@ int xl_merge_heads(int src_dtype, const void* src, int dst_dtype, void* dst, int
   return check_launch("xl_merge_heads");
 }
 
-int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const float* gkh, const float* gvh, void* gqkv,
-                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq, int64_t ldg) {
+int xl_merge_grads(int dtype, const float* gqu, const float* gqv, const void* gkh, const void* gvh, void* gqkv,
+                   int64_t B, int64_t Tn, int64_t M, int H, int dh, cudaStream_t st, int64_t ldq, int64_t ldg,
+                   int64_t ldkv) {
   if (ldq <= 0) ldq = 3 * (int64_t)H * dh;
   if (ldg <= 0) ldg = dh;
-  if (dh % 8 || ldq != 3 * (int64_t)H * dh || ldg != dh) {
+  if (ldkv <= 0) ldkv = dh;
+  if (dh % 8 || ldq != 3 * (int64_t)H * dh || ldg != dh || ldkv != dh) {
     const int64_t rows = B * (M + Tn);
     if (rows == 0) return RP_OK;
     XL_DTYPE(dtype, merge_grads_rows_kernel<T><<<row_grid(rows), kRowBlk, 0, st>>>(
-                        gqu, gqv, gkh, gvh, (T*)gqkv, (int)B, (int)Tn, (int)M, H, dh, ldq, ldg));
+                        gqu, gqv, (const T*)gkh, (const T*)gvh, (T*)gqkv, (int)B, (int)Tn, (int)M, H, dh, ldq, ldg,
+                        ldkv));
     return check_launch("xl_merge_grads");
   }
   const int64_t n = B * (M + Tn) * 3 * (int64_t)H * dh / 8;
   if (n == 0) return RP_OK;
-  XL_DTYPE(dtype, merge_grads_kernel<T><<<blocks8(n), kThreads, 0, st>>>(gqu, gqv, gkh, gvh, (T*)gqkv, (int)B,
-                                                                        (int)Tn, (int)M, H, dh));
+  XL_DTYPE(dtype, merge_grads_kernel<T><<<blocks8(n), kThreads, 0, st>>>(gqu, gqv, (const T*)gkh, (const T*)gvh,
+                                                                        (T*)gqkv, (int)B, (int)Tn, (int)M, H, dh));
   return check_launch("xl_merge_grads");
 }
 

@@ -404,13 +404,17 @@ def xl_merge_heads(src, dst, H, dh):
 
 
 def xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh):
-    """fp32 head-major gradients (one shared row pitch) -> g_qkv rows."""
-    ldg = _pitch(g_qu)
-    if any(_pitch(t) != ldg for t in (g_qv, g_kh, g_vh)):
-        raise DimensionError("xl_merge_grads: the head gradients share one row pitch")
+    """Head-major gradients -> g_qkv rows: dQu, dQv fp32 (one row pitch),
+    dK, dV in g_qkv's dtype (one row pitch)."""
+    ldg, ldkv = _pitch(g_qu), _pitch(g_kh)
+    if _pitch(g_qv) != ldg or _pitch(g_vh) != ldkv:
+        raise DimensionError("xl_merge_grads: dQu / dQv and dK / dV each share one row pitch")
+    if g_qu.dtype != torch.float32 or g_qv.dtype != torch.float32 or g_kh.dtype != g_qkv.dtype or \
+            g_vh.dtype != g_qkv.dtype:
+        raise DimensionError("xl_merge_grads: dQu / dQv fp32, dK / dV in the dtype of g_qkv")
     _count(1)
     N.check(N.lib().rp_xl_merge_grads(_dtc(g_qkv), _ptr(g_qu), _ptr(g_qv), _ptr(g_kh), _ptr(g_vh), _ptr(g_qkv), B, T,
-                                      M, H, dh, _pitch(g_qkv), ldg, _stream()), "xl_merge_grads")
+                                      M, H, dh, _pitch(g_qkv), ldg, ldkv, _stream()), "xl_merge_grads")
 
 
 def xl_softmax_fwd(ac, bd, probs, T, M, mem_len, scale):

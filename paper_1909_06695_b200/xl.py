@@ -268,13 +268,14 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
         g_p = ws.get("xl_ac", (H * B, T, tp.ldk), torch.float32)[:, :, :Kl]
         ops.gemm(g3, tp.vh.view(H * B, Kl, dh), out=g_p, tile_n=SCORE_TILE)
         ops.xl_softmax_bwd(g_p, tp.probs_buf, g_ac, g_bd, T, M, tp.mem_len, scale)
-    g_vh = f32r("xl_g_vh", H * B, Kl, dh)
+    # dK / dV leave their GEMMs rounded to the compute dtype, as g_qkv holds them
+    g_vh = ws.get_rows("xl_g_vh", (H * B, Kl, dh), cdt) if cdt == torch.bfloat16 else f32r("xl_g_vh", H * B, Kl, dh)
     # P^T and dAC^T are banded: key j sees queries i >= j - M (causal window),
     # so each key tile starts its K loop (over queries) at its first live block
     band = -M if BANDED else None
     ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
-    g_kh = f32r("xl_g_kh", H * B, Kl, dh)
+    g_kh = ws.get_rows("xl_g_kh", (H * B, Kl, dh), cdt) if cdt == torch.bfloat16 else f32r("xl_g_kh", H * B, Kl, dh)
     g_rh = f32r("xl_g_rh", H, Kl, dh)
     if not dq_done:
         ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
