@@ -106,9 +106,14 @@ int split_into(Ctx& c, Bump& b, const Mat& m, const void** hi, const void** lo, 
   float* h = static_cast<float*>(b.take(n * 4));
   float* l = static_cast<float*>(b.take(n * 4));
   if (b.off > b.cap) return set_error(RP_ERR_INVALID, "tf32x3 split scratch too small");
-  for (int64_t i = 0; i < m.batch; ++i) {
-    const float* src = static_cast<const float*>(m.p) + i * m.bstride;
-    if (int e = tf32_split(src, h + i * m.rows * ldd, l + i * m.rows * ldd, m.rows, m.cols, m.ld, ldd, c.st)) return e;
+  if (m.batch <= 1 || m.bstride == m.rows * m.ld) {  // batch rows evenly pitched: one launch
+    if (int e = tf32_split(static_cast<const float*>(m.p), h, l, m.batch * m.rows, m.cols, m.ld, ldd, c.st)) return e;
+  } else {
+    for (int64_t i = 0; i < m.batch; ++i) {
+      const float* src = static_cast<const float*>(m.p) + i * m.bstride;
+      if (int e = tf32_split(src, h + i * m.rows * ldd, l + i * m.rows * ldd, m.rows, m.cols, m.ld, ldd, c.st))
+        return e;
+    }
   }
   *hi = h;
   *lo = l;
