@@ -31,6 +31,34 @@ def clusters(cutoffs, vocab):
     return [(edges[k], edges[k + 1]) for k in range(len(cutoffs)) if edges[k] < edges[k + 1]]
 
 
+class HostCopy:
+    """A device int64 tensor copied to pinned host memory on a side stream,
+    ordered after the current stream's work so far: the adaptive head's row
+    bucketing waits for this copy only, not for the whole stream (device
+    batches; host batches are bucketed from the caller's array directly)."""
+
+    _streams = {}
+
+    def __init__(self, t):
+        dev = t.device
+        st = HostCopy._streams.get(dev)
+        if st is None:
+            st = HostCopy._streams[dev] = torch.cuda.Stream(device=dev)
+        self.host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(dev))
+        st.wait_event(ready)
+        with torch.cuda.stream(st):
+            self.host.copy_(t, non_blocking=True)
+            self.done = torch.cuda.Event()
+            self.done.record(st)
+        t.record_stream(st)
+
+    def numpy(self):
+        self.done.synchronize()
+        return self.host.numpy()
+
+
 class AdaptiveHead:
     """Forward (loss) and backward (grad of the input rows, of the tied
     matrix, of the cluster weights / biases) of the adaptive tied softmax."""
@@ -73,7 +101,10 @@ class AdaptiveHead:
         Nr, d = h.shape
         if d != self.d or tied_c.shape != (self.vocab, d) or w_c.shape != (self.n, d) or b_c.shape != (self.n,):
             raise DimensionError("adaptive softmax: shape mismatch")
-        y = targets.detach().cpu().numpy() if torch.is_tensor(targets) else np.asarray(targets)
+        if isinstance(targets, HostCopy):
+            y = targets.numpy()
+        else:
+            y = targets.detach().cpu().numpy() if torch.is_tensor(targets) else np.asarray(targets)
         y = y.reshape(-1).astype(np.int64)
         if y.size != Nr or (y.size and (y.min() < 0 or y.max() >= self.vocab)):
             raise DimensionError("adaptive softmax: targets out of range")

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import torch
 
-from .adaptive import AdaptiveHead, clusters
+from .adaptive import AdaptiveHead, HostCopy, clusters
 from . import layers as LY
 from . import ops
 from .errors import DimensionError, PartitionError, ScheduleViolation
@@ -731,7 +731,10 @@ class ModuleState:
                 raise ScheduleViolation("projection module slot lacks targets")
             tt = targets if torch.is_tensor(targets) else torch.as_tensor(targets)
             arena.targets.copy_(tt.reshape(-1), non_blocking=True)
-            arena.targets_host = targets
+            # the adaptive head buckets rows on the host: device targets leave
+            # by an early side-stream copy instead of a stream sync at the head
+            arena.targets_host = (HostCopy(tt) if arena.adaptive is not None and torch.is_tensor(tt) and tt.is_cuda
+                                  else targets)
         slot = StaleSlot(step, sample_id, arena.acts[0] if arena.acts else arena.tokens, targets, seeds, arena)
         self.slots.append(slot)
         if len(self.slots) > self.slot_capacity:
