@@ -630,6 +630,44 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, int64_t rows, int
   part[(int64_t)blockIdx.x * cols + j] = s;
 }
 
+// Two adjacent columns per thread (a warp reads 128 contiguous bytes of a
+// bf16 row), rows in groups of 4 loads in flight; the same row order per
+// column as colsum_partial_kernel (bitwise equal sums).
+template <typename T>
+__global__ void colsum_partial2_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                       float* __restrict__ part) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t j = 2 * ((int64_t)blockIdx.y * blockDim.x + threadIdx.x);
+  if (j >= cols) return;
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float s0 = 0.f, s1 = 0.f;
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    float a[4], b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float v[2];
+      VecIO<T, 2>::ld(x + (r + k) * ld + j, v);
+      a[k] = v[0];
+      b[k] = v[1];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      s0 += a[k];
+      s1 += b[k];
+    }
+  }
+  for (; r < r1; ++r) {
+    float v[2];
+    VecIO<T, 2>::ld(x + r * ld + j, v);
+    s0 += v[0];
+    s1 += v[1];
+  }
+  part[(int64_t)blockIdx.x * cols + j] = s0;
+  part[(int64_t)blockIdx.x * cols + j + 1] = s1;
+}
+
 // out = g * mask (T) with column partials of the masked fp32 values
 // (the b2 gradient, layers.py:215-220).
 template <typename T>
@@ -916,6 +954,13 @@ int colsum_blocks(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int6
 
 int colsum_partial(int dtype, const void* x, int64_t rows, int64_t cols, int64_t ld, float* part, cudaStream_t st) {
   if (cols == 0) return RP_OK;
+  const int esz = dtype == RP_BF16 ? 2 : 4;
+  if (cols % 2 == 0 && ld % 2 == 0 && (reinterpret_cast<uintptr_t>(x) % (2 * esz)) == 0) {
+    dim3 grid(colsum_blocks(rows), (unsigned)((cols / 2 + 127) / 128));
+    RP_DTYPE_DISPATCH(dtype, launch_pdl(colsum_partial2_kernel<T>, grid, 128, 0, st, (const T*)x, rows, cols, ld,
+                                        part));
+    return check_launch("colsum_partial");
+  }
   dim3 grid(colsum_blocks(rows), (unsigned)((cols + 127) / 128));
   RP_DTYPE_DISPATCH(dtype, launch_pdl(colsum_partial_kernel<T>, grid, 128, 0, st, (const T*)x, rows, cols, ld, part));
   return check_launch("colsum_partial");
