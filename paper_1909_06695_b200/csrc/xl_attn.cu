@@ -101,10 +101,15 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 
 // 32 TMEM columns of this thread's row -> staged ring slot (float2 stores:
 // conflict-free with the == 2 (mod 32) row stride)
-__device__ __forceinline__ void stage_band(float* ring_row, int slot, const uint32_t (&v)[32]) {
+// Only the pairs the lane's shifted read [31 - lane, 63 - lane) touches are
+// written (a predicated-off store moves no data): half the staging traffic.
+__device__ __forceinline__ void stage_band(float* ring_row, int slot, const uint32_t (&v)[32], int lane) {
   float2* dst = reinterpret_cast<float2*>(ring_row + 32 * slot);
 #pragma unroll
-  for (int t = 0; t < 16; ++t) dst[t] = make_float2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
+  for (int t = 0; t < 16; ++t) {
+    const bool used = slot == 0 ? (2 * t + 1 >= 31 - lane) : (2 * t <= 30 - lane);
+    if (used) dst[t] = make_float2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
+  }
 }
 
 __device__ __forceinline__ void tma_store_3d_p(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
@@ -292,8 +297,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
       tmem_wait_ld(a);
       tc_fence_before();
       mbar_arrive(&s_empty[buf]);  // this step's TMEM buffer is free for step n + 2
-      stage_band(myring, 0, v0);
-      stage_band(myring, 1, v1);
+      stage_band(myring, 0, v0, lane);
+      stage_band(myring, 1, v1, lane);
       __syncwarp();
       float s[32];
       float cm = -INFINITY;
@@ -880,8 +885,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
       tmem_wait_ld(a);
       tc_fence_before();
       mbar_arrive(&s_empty[buf]);
-      stage_band(myring, 0, v0);
-      stage_band(myring, 1, v1);
+      stage_band(myring, 0, v0, lane);
+      stage_band(myring, 1, v1, lane);
       __syncwarp();
       float sv[32];
       float cm = -INFINITY;
