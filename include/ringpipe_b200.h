@@ -189,12 +189,14 @@ int rp_xl_softmax_fwd(int32_t dtype, const float* ac, const float* bd, int64_t l
  * rp_xl_softmax_fwd over the AC / BD GEMM outputs, without materialising them */
 int rp_xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, void* probs, int64_t ld_p, int64_t B,
                    int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len, float scale, void* stream);
-/* rp_xl_attn_fwd with P.V folded in (dh = 64): also ctx = P v written as merged [B*T, H*dh] rows
- * (the normalised P tile stays in shared memory as the A operand of a second tcgen05 MMA into a
- * TMEM accumulator); P is still written for the backward */
+/* rp_xl_attn_fwd with P.V folded in (operand head dim dh = 64): also ctx = P v written as merged
+ * rows (the normalised P tile stays in shared memory as the A operand of a second tcgen05 MMA into a
+ * TMEM accumulator); P is still written for the backward.  A model head dim dh_out < 64 (e.g. 41)
+ * rides with its q / k / v / r rows zero-padded to 64: ctx then holds head h's dh_out columns at
+ * h * dh_out, rows at pitch ld_ctx (0, 0 = 64, H * 64) */
 int rp_xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,
                       int64_t ld_p, void* ctx, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, void* stream);
+                      float scale, int32_t dh_out, int64_t ld_ctx, void* stream);
 /* Fused backward of rp_xl_attn_fwd's softmax (bf16, dh = 64, tcgen05): dP = g_ctx_h v^T on the tensor
  * cores, D_i = <g_ctx_i, ctx_i> from the merged [B*T, H*dh] rows, dAC = P (dP - D) * scale and the
  * un-shifted dBD, both [H*B, T, ld_p]; replaces the dP GEMM + rp_xl_softmax_bwd */

@@ -214,7 +214,7 @@ def _declare(L):
         "rp_xl_attn_fwd": [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
-        "rp_xl_attn_fwd_pv": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, i32, i32, i64, f32, vp],
+        "rp_xl_attn_fwd_pv": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, i32, i32, i64, f32, i32, i64, vp],
         "rp_xl_attn_bwd_dq": [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],
         "rp_rows_copy": [i32, vp, i64, i64, i64, vp, f32, i32, i32, vp, i64, vp],

@@ -185,8 +185,9 @@ int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, vo
 }
 int rp_xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,
                       int64_t ld_p, void* ctx, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, void* stream) {
-  return rp::xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ld_p, ctx, B, T, M, H, dh, (int)mem_len, scale, RP_S(stream));
+                      float scale, int32_t dh_out, int64_t ld_ctx, void* stream) {
+  return rp::xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ld_p, ctx, B, T, M, H, dh, (int)mem_len, scale, RP_S(stream),
+                            dh_out, ld_ctx);
 }
 int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
                       void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,

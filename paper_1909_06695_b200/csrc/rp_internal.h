@@ -120,10 +120,11 @@ int xl_attn_fwd(const void* qu, const void* qv, const void* kh, const void* rh, 
 int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac, void* gbd, int64_t ldp,
                 const void* gctx, const void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
                 float scale, cudaStream_t st);
-// fused forward with P.V (dh = 64): also ctx (merged [B*T, H*dh]) = P v
+// fused forward with P.V (operands dh = 64; a smaller model head dim dh_out
+// rides zero-padded to 64): also ctx (merged rows, head h at h * dh_out, pitch ld_ctx) = P v
 int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,
                    int64_t ldp, void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale,
-                   cudaStream_t st);
+                   cudaStream_t st, int dh_out = 0, int64_t ld_ctx = 0);
 // fused backward with the query gradients on the tensor cores (dh = 64, T % 128 == 0):
 // also gqu = dAC K, gqv = dBD R as fp32 [H*B*T, 64]
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,

@@ -672,8 +672,10 @@ constexpr int fwd_pv_smem() {
 
 struct FwdPvParams {
   FwdParams f;
-  __nv_bfloat16* ctx;  // merged [B*T, H*64]
+  __nv_bfloat16* ctx;  // merged rows: head h's dh_out columns at h * dh_out, row pitch ld_ctx
   int d;
+  int dh_out;          // the model's head dim (<= 64: the operands' pads past it are zero)
+  int64_t ld_ctx;
 };
 
 template <int NS, int NB>
@@ -951,8 +953,8 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
     tc_fence_after();
     uint32_t o[32];
     tmem_ld32(tl + 256 + 32 * half, o);
-    if (row_ok) {
-      uint4* dst = reinterpret_cast<uint4*>(pp.ctx + ((int64_t)b * p.T + i) * pp.d + h * 64 + 32 * half);
+    if (row_ok && pp.dh_out == 64 && pp.ld_ctx % 8 == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(pp.ctx + ((int64_t)b * p.T + i) * pp.ld_ctx + h * 64 + 32 * half);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t ww[4];
@@ -962,6 +964,13 @@ __global__ void __launch_bounds__(kThreadsFwd, 1)
           ww[e] = *reinterpret_cast<uint32_t*>(&b2);
         }
         dst[c] = make_uint4(ww[0], ww[1], ww[2], ww[3]);
+      }
+    } else if (row_ok) {  // a head dim padded to 64: its real columns, at the merged rows' pitch
+      __nv_bfloat16* dst = pp.ctx + ((int64_t)b * p.T + i) * pp.ld_ctx + (int64_t)h * pp.dh_out;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int col = 32 * half + c;
+        if (col < pp.dh_out) dst[col] = __float2bfloat16_rn(__uint_as_float(o[c]));
       }
     }
     if (half == 0 && lane == 0) tma_store_wait_all();
@@ -1476,12 +1485,16 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
 
 int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,
                    int64_t ldp, void* ctx, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale,
-                   cudaStream_t st) {
+                   cudaStream_t st, int dh_out, int64_t ld_ctx) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: head dim must be 64 (got %d)", dh);
+  if (dh_out <= 0) dh_out = dh;
+  if (ld_ctx <= 0) ld_ctx = (int64_t)H * dh_out;
+  if (dh_out > 64 || ld_ctx < (int64_t)H * dh_out)
+    return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: output head dim <= 64, ctx pitch >= H * dh_out");
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
   if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: ldp must be >= M+T, multiple of 8");
   if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: mem_len out of range");
-  if (((reinterpret_cast<uintptr_t>(probs) | reinterpret_cast<uintptr_t>(ctx)) & 15) != 0)
+  if ((reinterpret_cast<uintptr_t>(probs) & 15) != 0 || (reinterpret_cast<uintptr_t>(ctx) & 1) != 0)
     return set_error(RP_ERR_DIMENSION, "xl_attn_fwd_pv: unaligned operand");
   CUtensorMap mqu, mqv, mk, mr, mv, mp;
   RP_TRY0(tma_map_bf16(&mqu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
@@ -1512,6 +1525,8 @@ int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* v
   p.dbg = 0;
   pp.ctx = static_cast<__nv_bfloat16*>(ctx);
   pp.d = H * dh;
+  pp.dh_out = dh_out;
+  pp.ld_ctx = ld_ctx;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   if (pv_buf == 1)

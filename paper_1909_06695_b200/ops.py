@@ -461,21 +461,31 @@ def xl_attn_bwd(g_ctx_h, vh, probs, g_ac, g_bd, g_ctx, ctx, B, T, M, mem_len, sc
                                    _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_bwd")
 
 
+def padded(t):
+    """The view of a row-pitched tensor over its full pitch (pad columns included)."""
+    ld = _pitch(t)
+    if ld == t.shape[-1]:
+        return t
+    return t.as_strided(tuple(t.shape[:-1]) + (ld,), t.stride())
+
+
 def xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ctx, B, T, M, mem_len, scale):
-    """xl_attn_fwd plus ctx = P v (dh = 64): qu / qv [H*B*T, dh], kh / vh
-    [H*B*(M+T), dh], rh [H, M+T, dh] head-major; probs [H*B, T, ldp]; ctx the
-    merged [B*T, H*dh] rows."""
+    """xl_attn_fwd plus ctx = P v: qu / qv [H*B*T, dh], kh / vh [H*B*(M+T),
+    dh], rh [H, M+T, dh] head-major; probs [H*B, T, ldp]; ctx the merged
+    [B*T, H*dh] rows.  The kernel's head dim is 64: a smaller model head dim
+    rides in rows pitched at 64 whose pad columns are zero (XLTape)."""
     _require_cuda(qu, qv, kh, vh, rh, probs, ctx)
     for t in (qu, qv, kh, vh, rh, probs, ctx):
         if t.dtype != torch.bfloat16:
             raise DimensionError("xl_attn_fwd_pv takes bf16 tensors")
-    for t in (qu, qv, kh, vh, rh, ctx):
-        if not t.is_contiguous():
-            raise DimensionError("xl_attn_fwd_pv operands must be contiguous")
     H, dh = rh.shape[0], rh.shape[-1]
+    ops_in = [padded(t) for t in (qu, qv, kh, vh, rh)]
+    for t in ops_in:
+        if not t.is_contiguous() or t.shape[-1] != 64:
+            raise DimensionError("xl_attn_fwd_pv operands: contiguous rows of 64 (head dims < 64 zero-padded)")
     _count(1)
-    N.check(N.lib().rp_xl_attn_fwd_pv(_ptr(qu), _ptr(qv), _ptr(kh), _ptr(vh), _ptr(rh), _ptr(probs), probs.stride(-2),
-                                      _ptr(ctx), B, T, M, H, dh, mem_len, scale, _stream()), "xl_attn_fwd_pv")
+    N.check(N.lib().rp_xl_attn_fwd_pv(*[_ptr(t) for t in ops_in], _ptr(probs), probs.stride(-2), _ptr(ctx), B, T, M, H,
+                                      64, mem_len, scale, dh, _pitch(ctx), _stream()), "xl_attn_fwd_pv")
 
 
 def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale):

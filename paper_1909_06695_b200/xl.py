@@ -50,13 +50,24 @@ class XLTape:
         e = lambda *s: LY.empty_rows(*s, dtype=dtype, device=device)  # noqa: E731
         f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
         self.B, self.T, self.M, self.H, self.dh, self.Kl, self.ldk = B, T, M, H, dh, Kl, ldk
+        # bf16 head dims below 64 that are not 16-byte rows (BASELINE
+        # configs[3]: 41) ride in rows zero-padded to 64: the fused forward
+        # (head dim 64) then takes them -- the pads add zero to every score
+        # and to P v (the split kernels write the real columns only)
+        self.dhp = 64 if (dtype == torch.bfloat16 and dh < 64 and dh % 8) else dh
+
+        def heads(*s):
+            if self.dhp == dh:
+                return e(*s)
+            return torch.zeros(*s[:-1], self.dhp, dtype=dtype, device=device)[..., :dh]
+
         self.xa = e(B * Kl, d)            # [memory rows; current rows]
         self.a = e(B * Kl, d)
         self.mean1, self.rstd1 = f32(B * Kl), f32(B * Kl)
         self.qkv = e(B * Kl, 3 * d)
-        self.qu, self.qv = e(H, B * T, dh), e(H, B * T, dh)
-        self.kh, self.vh = e(H, B * Kl, dh), e(H, B * Kl, dh)
-        self.rh = e(H, Kl, dh)
+        self.qu, self.qv = heads(H, B * T, dh), heads(H, B * T, dh)
+        self.kh, self.vh = heads(H, B * Kl, dh), heads(H, B * Kl, dh)
+        self.rh = heads(H, Kl, dh)
         self.probs_buf = torch.empty(H * B, T, ldk, dtype=dtype, device=device)
         self.probs = self.probs_buf[:, :, :Kl]
         self.ctx = e(B * T, d)
@@ -115,8 +126,11 @@ BANDED = os.environ.get("RP_XL_BANDED", "1") != "0"
 
 
 def fused_pv_ok(tp):
-    """The forward with P.V folded in (xl_attn_fwd_pv): head dim 64."""
-    return FUSED_PV and fused_ok(tp) and tp.dh == 64
+    """The forward with P.V folded in (xl_attn_fwd_pv): head dim 64, or a
+    smaller one zero-padded to 64 in the tape (XLTape.dhp)."""
+    if not FUSED_PV or tp.xa.dtype != torch.bfloat16:
+        return False
+    return (FUSED and tp.dh == 64) or (FUSED and getattr(tp, "dhp", tp.dh) == 64)
 
 
 def fused_dq_ok(tp):

@@ -222,3 +222,43 @@ def test_dense_row_composites_reject_pitched_widths():
                                    LY.Workspace(dev), stack.runtime.flag)
     with pytest.raises(DimensionError, match="adaptive head"):
         MD.build_xl_stack(64, d, f, 1, T, 0.1, 3, H, M, dtype="bf16")
+
+
+def test_fused_forward_takes_zero_padded_head_dims():
+    """Head dim 41 rides zero-padded to 64 through xl_attn_fwd_pv: P and
+    ctx = P v equal the unfused GEMM + softmax path within one bf16 rounding,
+    and the block output within the bf16 tolerance."""
+    from paper_1909_06695_b200 import layers as LY
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import xl as XD
+
+    B, T, M, H, d, f = 2, 150, 150, 10, 410, 2100
+    stack = MD.build_xl_stack(64, d, f, 1, T, 0.1, 3, H, M, dtype="bf16", cutoffs=[16, 40])
+    st = stack.storage[1]
+    st.configure_ring(1)
+    st.ensure(0)
+    W = st.weights(0)
+    dev = stack.runtime.device
+    g = torch.Generator(device=dev).manual_seed(4)
+    xa = (torch.rand(B * (M + T), d, device=dev, generator=g) * 2 - 1).bfloat16()
+    R = XD.sinusoid(M + T, d, torch.bfloat16, dev)
+    drop = LY.Dropout.make(99, 0.1, True)
+    res = []
+    saved = XD.FUSED_PV
+    try:
+        for fused in (False, True):
+            XD.FUSED_PV = fused
+            tp = XD.XLTape(B, T, M, d, f, H, torch.bfloat16, dev)
+            assert tp.dhp == 64 and XD.fused_pv_ok(tp) == fused
+            LY.copy_rows(tp.xa, xa)
+            tp.mem_len = M - 30
+            out = LY.empty_rows(B * T, d, dtype=torch.bfloat16, device=dev)
+            XD.xl_block_forward_ops(W, W, out, tp, R, drop, LY.Workspace(dev), stack.runtime.flag)
+            torch.cuda.synchronize()
+            res.append((tp.probs.float().clone(), tp.ctx.float().clone(), out.float().clone()))
+    finally:
+        XD.FUSED_PV = saved
+    (p0, c0, o0), (p1, c1, o1) = res
+    assert (p1 - p0).abs().max().item() <= 2 ** -8 * max(p0.abs().max().item(), 1e-3)
+    assert ((c1 - c0).norm() / c0.norm()).item() <= 1e-2
+    assert ((o1 - o0).norm() / o0.norm()).item() <= 1e-2
