@@ -574,14 +574,30 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
 
 // out[j] = sum_b partial[b, j]: 32 columns x 32 partial lanes per CTA, each
 // lane sums a fixed strided subset, then lane sums combine in fixed order.
+// s += part[b * cols + j] for b = b0, b0 + 32, ... < nblk, in that order,
+// four loads in flight (the additions keep their order: bitwise the plain loop)
+__device__ __forceinline__ float colsum_strided(const float* __restrict__ part, int b0, int nblk, int64_t cols,
+                                                int64_t j) {
+  float s = 0.f;
+  int b = b0;
+  for (; b + 96 < nblk; b += 128) {
+    const float v0 = part[(int64_t)b * cols + j], v1 = part[(int64_t)(b + 32) * cols + j];
+    const float v2 = part[(int64_t)(b + 64) * cols + j], v3 = part[(int64_t)(b + 96) * cols + j];
+    s += v0;
+    s += v1;
+    s += v2;
+    s += v3;
+  }
+  for (; b < nblk; b += 32) s += part[(int64_t)b * cols + j];
+  return s;
+}
+
 __global__ void __launch_bounds__(1024) colsum_finish_kernel(const float* __restrict__ part, int nblk, int64_t cols,
                                                              float* __restrict__ out) {
   __shared__ float red[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + tx;
-  float s = 0.f;
-  if (j < cols)
-    for (int b = ty; b < nblk; b += 32) s += part[(int64_t)b * cols + j];
+  const float s = j < cols ? colsum_strided(part, ty, nblk, cols, j) : 0.f;
   red[ty][tx] = s;
   __syncthreads();
   if (ty == 0 && j < cols) {
@@ -603,9 +619,7 @@ __global__ void __launch_bounds__(1024) colsum_finish_multi_kernel(ColsumJobs jo
   const ColsumJob& J = jobs.job[jb];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t j = (int64_t)(blockIdx.x - jobs.first_block[jb]) * 32 + tx;
-  float s = 0.f;
-  if (j < J.cols)
-    for (int b = ty; b < J.nblk; b += 32) s += J.part[(int64_t)b * J.cols + j];
+  const float s = j < J.cols ? colsum_strided(J.part, ty, J.nblk, J.cols, j) : 0.f;
   red[ty][tx] = s;
   __syncthreads();
   if (ty == 0 && j < J.cols) {
