@@ -209,7 +209,13 @@ int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, vo
 int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
                       void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,
                       float* grad_qv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, void* stream);
+                      float scale, float* bias_part, void* stream);
+/* bias_part of rp_xl_attn_bwd_dq (or NULL): per-CTA column sums of grad_qu / grad_qv, which
+ * rp_xl_dq_bias_finish turns into the r_w_bias / r_r_bias gradients ([H, 64] each) without
+ * re-reading the query gradients (the column sums of rp_xl_bias_grad) */
+int64_t rp_xl_dq_bias_part_bytes(int32_t H, int64_t B, int64_t T);
+int rp_xl_dq_bias_finish(const float* bias_part, float* g_r_w_bias, float* g_r_r_bias, int32_t H, int64_t B, int64_t T,
+                         void* stream);
 /* dAC = P (dP - <dP,P>) * scale; dBD = the same values un-shifted */
 int rp_xl_softmax_bwd(int32_t dtype, const float* grad_p, int64_t ld_scores, const void* probs, int64_t ld_p,
                       void* grad_ac, void* grad_bd, int64_t rows, int64_t T, int64_t M, int64_t mem_len, float scale,

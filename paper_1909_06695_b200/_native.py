@@ -215,7 +215,10 @@ def _declare(L):
         "rp_xl_attn_bwd": [vp, vp, vp, vp, vp, i64, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd_pv": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, i32, i32, i64, f32, i32, i64, vp],
-        "rp_xl_attn_bwd_dq": [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
+        "rp_xl_attn_bwd_dq": [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp,
+                              vp],
+        "rp_xl_dq_bias_part_bytes": [i32, i64, i64],
+        "rp_xl_dq_bias_finish": [vp, vp, vp, i32, i64, i64, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],
         "rp_rows_copy": [i32, vp, i64, i64, i64, vp, f32, i32, i32, vp, i64, vp],
         "rp_rows_gather": [i32, vp, i64, vp, i64, i64, vp, i64, vp],
@@ -261,6 +264,7 @@ def _declare(L):
         fn.restype = ctypes.c_int32
     L.rp_embed_bwd_workspace_bytes.restype = i64
     L.rp_xl_bias_grad_workspace_bytes.restype = i64
+    L.rp_xl_dq_bias_part_bytes.restype = i64
     L.rp_block_workspace_bytes.restype = i64
     L.rp_xl_block_workspace_bytes.restype = i64
     L.rp_module_workspace_bytes.restype = i64

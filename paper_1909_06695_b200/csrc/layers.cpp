@@ -570,6 +570,7 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   bwd += 2 * al256(x.H * x.N * x.dh * 4);   // g_qu, g_qv
   bwd += 2 * al256(x.HB * x.Kl * x.dh * e) + al256(x.H * x.Kl * x.dh * 4);  // g_vh, g_kh (compute dtype), g_rh
   bwd += al256(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh));
+  if (d.fused & RP_XL_FUSED_DQ) bwd += al256(xl_dq_bias_part_bytes((int)x.H, x.B, x.T));
   bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
   bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
   bwd += al256(kBlockSplitK);
@@ -696,6 +697,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   void* g_kh = bp.take(x.HB * x.Kl * x.dh * e);
   float* g_rh = static_cast<float*>(bp.take(x.H * x.Kl * x.dh * 4));
   float* bias_ws = static_cast<float*>(bp.take(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh)));
+  float* dq_bias = (d.fused & RP_XL_FUSED_DQ) ? static_cast<float*>(bp.take(xl_dq_bias_part_bytes((int)x.H, x.B, x.T)))
+                                              : nullptr;
   void* g_r = bp.take(x.Kl * D * e);
   void* g_qkv = bp.take(BK * 3 * D * e);
   float* g_a = static_cast<float*>(bp.take(BK * D * 4));
@@ -729,7 +732,7 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   bool dq_done = false;
   if (d.fused & RP_XL_FUSED_DQ) {
     RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, g_qu, g_qv, x.B,
-                          x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st));
+                          x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st, dq_bias));
     dq_done = true;
   } else if (d.fused & RP_XL_FUSED_BWD) {
     RP_TRY(xl_attn_bwd(g_ctx_h, tp.vh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, x.B, x.T, x.M, (int)x.H, (int)x.dh,
@@ -761,7 +764,10 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));
   RP_TRY(mm(c, gbd, true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh), true, bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh),
             RP_F32));
-  RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
+  if (dq_bias)
+    RP_TRY(xl_dq_bias_finish(dq_bias, G.r_w_bias, G.r_r_bias, (int)x.H, x.B, x.T, st));
+  else
+    RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
   RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
   RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
   RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));

@@ -127,9 +127,14 @@ int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* v
                    cudaStream_t st, int dh_out = 0, int64_t ld_ctx = 0);
 // fused backward with the query gradients on the tensor cores (dh = 64, T % 128 == 0):
 // also gqu = dAC K, gqv = dBD R as fp32 [H*B*T, 64]
+// bias_part (optional, xl_dq_bias_part_bytes): per-CTA column sums of gqu / gqv, finished
+// into the r_w_bias / r_r_bias gradients by xl_dq_bias_finish (no re-read of gqu / gqv)
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
                    void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
-                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st);
+                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st,
+                   float* bias_part = nullptr);
+int64_t xl_dq_bias_part_bytes(int H, int64_t B, int64_t Tn);
+int xl_dq_bias_finish(const float* part, float* gu, float* gv, int H, int64_t B, int64_t Tn, cudaStream_t st);
 // adaptive softmax row movers (adaptive.cu)
 int rows_copy(int src_dtype, const void* src, int64_t ld_src, int64_t rows, int64_t cols, const float* val,
               float val_const, int aug, int dst_dtype, void* dst, int64_t ld_dst, cudaStream_t st);

@@ -1010,7 +1010,24 @@ struct DqParams {
   BwdParams b;
   float* gqu;  // [H*B*T, 64] fp32 (rows hb*T + i)
   float* gqv;
+  float* bias_part;  // optional [2][H*B][nqt][64]: per-CTA column sums of dQu (u) and dQv (v)
 };
+
+// out[lane] = sum over the warp's 32 rows of column `lane` of v[0..31]
+// (butterfly transpose-reduce: 31 shuffles; a fixed summation tree)
+__device__ __forceinline__ float warp_colsum32(float (&a)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool upper = lane & s;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      const float send = upper ? a[k] : a[k + s];
+      const float keep = upper ? a[k + s] : a[k];
+      a[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return a[0];
+}
 
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     xl_attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
@@ -1325,12 +1342,39 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     for (int c = 0; c < 8; ++c)
       du[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
                           __uint_as_float(v[4 * c + 3]));
+    float colsum_u = 0.f, colsum_v = 0.f;
+    if (dq.bias_part) {  // rows past T are zero in TMEM (their dS is zero)
+      float a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = __uint_as_float(v[c]);
+      colsum_u = warp_colsum32(a, lane);
+    }
     tmem_ld32(tl + 320 + 32 * half, v);
     float4* dv = reinterpret_cast<float4*>(dq.gqv + orow);
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       dv[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]), __uint_as_float(v[4 * c + 2]),
                           __uint_as_float(v[4 * c + 3]));
+    if (dq.bias_part) {
+      float a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = __uint_as_float(v[c]);
+      colsum_v = warp_colsum32(a, lane);
+      // the four lane-quarter warps of this column half, summed in quarter
+      // order through the (now idle) dO tile
+      float* red = reinterpret_cast<float*>(sG);
+      red[((half * 2 + 0) * 4 + q) * 32 + lane] = colsum_u;
+      red[((half * 2 + 1) * 4 + q) * 32 + lane] = colsum_v;
+      named_sync(1, kSoftWarps * 32);
+      if (q == 0) {
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          const float* rr = red + (half * 2 + w) * 4 * 32 + lane;
+          const float s = ((rr[0] + rr[32]) + rr[64]) + rr[96];
+          dq.bias_part[(((int64_t)w * p.H * p.B + hb) * p.nqt + qt) * 64 + 32 * half + lane] = s;
+        }
+      }
+    }
     if (lane == 0) tma_store_wait_all();
   }
   tc_fence_before();
@@ -1339,6 +1383,35 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 }
 
 }  // namespace
+
+// u / v gradients from xl_attn_bwd_dq's per-CTA column sums: head h sums its
+// B * nqt partials in (b, query tile) order
+__global__ void dq_bias_finish_kernel(const float* __restrict__ part, float* __restrict__ gu, float* __restrict__ gv,
+                                      int H, int B, int nqt) {
+  const int h = blockIdx.x, w = blockIdx.y, c = threadIdx.x;  // 64 threads
+  const float* src = part + ((int64_t)w * H * B + (int64_t)h * B) * nqt * 64 + c;
+  float s = 0.f;
+  const int n = B * nqt;
+  int k = 0;
+  for (; k + 4 <= n; k += 4) {  // four loads in flight, additions in order
+    const float v0 = src[(int64_t)k * 64], v1 = src[(int64_t)(k + 1) * 64];
+    const float v2 = src[(int64_t)(k + 2) * 64], v3 = src[(int64_t)(k + 3) * 64];
+    s += v0;
+    s += v1;
+    s += v2;
+    s += v3;
+  }
+  for (; k < n; ++k) s += src[(int64_t)k * 64];
+  (w ? gv : gu)[h * 64 + c] = s;
+}
+
+int64_t xl_dq_bias_part_bytes(int H, int64_t B, int64_t Tn) { return 2 * (int64_t)H * B * (Tn / kQT) * 64 * 4; }
+
+int xl_dq_bias_finish(const float* part, float* gu, float* gv, int H, int64_t B, int64_t Tn, cudaStream_t st) {
+  if (H <= 0 || B <= 0 || Tn % kQT) return set_error(RP_ERR_DIMENSION, "xl_dq_bias_finish: bad shape");
+  dq_bias_finish_kernel<<<dim3(H, 2), 64, 0, st>>>(part, gu, gv, H, (int)B, (int)(Tn / kQT));
+  return check_launch("xl_dq_bias_finish");
+}
 
 // RP_XL_ORDER=0 restores the (head*batch)-major CTA order (A/B switch)
 static int xl_heavy_first() {
@@ -1438,7 +1511,7 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
 
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
                    void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
-                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st) {
+                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st, float* bias_part) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: head dim must be 64 (got %d)", dh);
   if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: T must be a multiple of 128");
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
@@ -1477,6 +1550,7 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   p.scale = scale;
   q.gqu = gqu;
   q.gqv = gqv;
+  q.bias_part = bias_part;
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);

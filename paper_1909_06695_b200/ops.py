@@ -488,7 +488,8 @@ def xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ctx, B, T, M, mem_len, scale):
                                       64, mem_len, scale, dh, _pitch(ctx), _stream()), "xl_attn_fwd_pv")
 
 
-def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale):
+def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale,
+                   bias_part=None):
     """xl_attn_bwd plus the query gradients on the tensor cores (dh = 64,
     T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh]."""
     _require_cuda(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv)
@@ -508,7 +509,17 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
     _count(1)
     N.check(N.lib().rp_xl_attn_bwd_dq(_ptr(g_ctx_h), _ptr(vh), _ptr(kh), _ptr(rh), _ptr(probs), _ptr(g_ac),
                                       _ptr(g_bd), ldp, _ptr(g_ctx), _ptr(ctx), _ptr(g_qu), _ptr(g_qv), B, T, M, H, dh,
-                                      mem_len, scale, _stream()), "xl_attn_bwd_dq")
+                                      mem_len, scale, _ptr(bias_part), _stream()), "xl_attn_bwd_dq")
+
+
+def xl_dq_bias_part_elems(H, B, T):
+    return N.lib().rp_xl_dq_bias_part_bytes(H, B, T) // 4
+
+
+def xl_dq_bias_finish(part, g_u, g_v, H, B, T):
+    """r_w_bias / r_r_bias gradients from xl_attn_bwd_dq's per-CTA column sums."""
+    _count(1)
+    N.check(N.lib().rp_xl_dq_bias_finish(_ptr(part), _ptr(g_u), _ptr(g_v), H, B, T, _stream()), "xl_dq_bias_finish")
 
 
 def gelu(z, y):

@@ -268,11 +268,14 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     g_qu = f32r("xl_g_qu", H, Nt, dh)
     g_qv = f32r("xl_g_qv", H, Nt, dh)
     dq_done = False
+    bias_part = None
     if fused_dq_ok(tp):
-        # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu)
+        # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu),
+        # plus the per-CTA column sums of dQu / dQv for the u / v gradients
+        bias_part = ws.get("xl_dq_bias", (ops.xl_dq_bias_part_elems(H, B, T),), torch.float32)
         with ops.span("xl_attn_bwd"):
             ops.xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, g_qu, g_qv, B,
-                               T, M, tp.mem_len, scale)
+                               T, M, tp.mem_len, scale, bias_part=bias_part)
         dq_done = True
     elif fused_bwd_ok(tp):
         # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
@@ -297,8 +300,11 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     if not dq_done:
         ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
-    work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
-    ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
+    if bias_part is not None:
+        ops.xl_dq_bias_finish(bias_part, G["r_w_bias"], G["r_r_bias"], H, B, T)
+    else:
+        work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
+        ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
     g_r = ws.get_rows("xl_g_r", (Kl, d), cdt)
     ops.xl_merge_heads(g_rh, g_r, H, dh)
     _bg(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
