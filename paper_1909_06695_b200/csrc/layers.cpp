@@ -764,9 +764,7 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));
   RP_TRY(mm(c, gbd, true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh), true, bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh),
             RP_F32));
-  if (dq_bias)
-    RP_TRY(xl_dq_bias_finish(dq_bias, G.r_w_bias, G.r_r_bias, (int)x.H, x.B, x.T, st));
-  else
+  if (!dq_bias)  // else: the fused backward's column sums, finished with the others below
     RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
   RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
   RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
@@ -779,10 +777,12 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
                          pg + (int64_t)nbl_cur * D, pb + (int64_t)nbl_cur * D, BM, D, st));
   RP_TRY(layernorm_bwd(dt, g_a + BM * D, static_cast<const char*>(tp.xa) + BM * D * e, tp.mean1 + BM, tp.rstd1 + BM,
                        w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
-  const ColsumJob jobs[6] = {{pm, nbm, D, G.b2}, {part, nbc, F, G.b1}, {pg2, nbl_cur, D, G.ln2_g},
+  const int nq = (int)(x.B * (x.T / 128));  // the fused backward's [B*nqt, H*64] bias partials
+  const ColsumJob jobs[8] = {{pm, nbm, D, G.b2}, {part, nbc, F, G.b1}, {pg2, nbl_cur, D, G.ln2_g},
                              {pb2, nbl_cur, D, G.ln2_b}, {pg, nbl_cur + nbl_mem, D, G.ln1_g},
-                             {pb, nbl_cur + nbl_mem, D, G.ln1_b}};
-  return colsum_finish_multi(jobs, 6, st);
+                             {pb, nbl_cur + nbl_mem, D, G.ln1_b},
+                             {dq_bias, nq, D, G.r_w_bias}, {dq_bias + (int64_t)nq * D, nq, D, G.r_r_bias}};
+  return colsum_finish_multi(jobs, dq_bias ? 8 : 6, st);
 }
 
 }  // namespace rp

@@ -1010,7 +1010,8 @@ struct DqParams {
   BwdParams b;
   float* gqu;  // [H*B*T, 64] fp32 (rows hb*T + i)
   float* gqv;
-  float* bias_part;  // optional [2][H*B][nqt][64]: per-CTA column sums of dQu (u) and dQv (v)
+  float* bias_part;  // optional [2][B*nqt][H*64]: per-CTA column sums of dQu (u) and dQv (v) -- a
+                     // [rows, cols] block per bias that a column-sum finish reduces
 };
 
 // out[lane] = sum over the warp's 32 rows of column `lane` of v[0..31]
@@ -1371,7 +1372,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         for (int w = 0; w < 2; ++w) {
           const float* rr = red + (half * 2 + w) * 4 * 32 + lane;
           const float s = ((rr[0] + rr[32]) + rr[64]) + rr[96];
-          dq.bias_part[(((int64_t)w * p.H * p.B + hb) * p.nqt + qt) * 64 + 32 * half + lane] = s;
+          const int hh = hb / p.B, bb = hb - hh * p.B;
+          dq.bias_part[(((int64_t)w * p.B + bb) * p.nqt + qt) * p.H * 64 + hh * 64 + 32 * half + lane] = s;
         }
       }
     }
@@ -1389,19 +1391,20 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 __global__ void dq_bias_finish_kernel(const float* __restrict__ part, float* __restrict__ gu, float* __restrict__ gv,
                                       int H, int B, int nqt) {
   const int h = blockIdx.x, w = blockIdx.y, c = threadIdx.x;  // 64 threads
-  const float* src = part + ((int64_t)w * H * B + (int64_t)h * B) * nqt * 64 + c;
+  const int64_t ld = (int64_t)H * 64;
+  const float* src = part + (int64_t)w * B * nqt * ld + h * 64 + c;
   float s = 0.f;
   const int n = B * nqt;
   int k = 0;
   for (; k + 4 <= n; k += 4) {  // four loads in flight, additions in order
-    const float v0 = src[(int64_t)k * 64], v1 = src[(int64_t)(k + 1) * 64];
-    const float v2 = src[(int64_t)(k + 2) * 64], v3 = src[(int64_t)(k + 3) * 64];
+    const float v0 = src[k * ld], v1 = src[(k + 1) * ld];
+    const float v2 = src[(k + 2) * ld], v3 = src[(k + 3) * ld];
     s += v0;
     s += v1;
     s += v2;
     s += v3;
   }
-  for (; k < n; ++k) s += src[(int64_t)k * 64];
+  for (; k < n; ++k) s += src[k * ld];
   (w ? gv : gu)[h * 64 + c] = s;
 }
 

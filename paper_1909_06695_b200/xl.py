@@ -300,8 +300,12 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     if not dq_done:
         ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
+    bias_jobs = []
     if bias_part is not None:
-        ops.xl_dq_bias_finish(bias_part, G["r_w_bias"], G["r_r_bias"], H, B, T)
+        # the fused backward's per-CTA dQu / dQv column sums: [B*nqt, H*64] per bias,
+        # finished with the block's other column sums below
+        pu, pv = bias_part.view(2, -1, H * dh)
+        bias_jobs = [(pu, pu.shape[0], G["r_w_bias"]), (pv, pv.shape[0], G["r_r_bias"])]
     else:
         work = ws.get("xl_bias_ws", (N.lib().rp_xl_bias_grad_workspace_bytes(H, dh) // 4,), torch.float32)
         ops.xl_bias_grad(g_qu, g_qv, work, G["r_w_bias"], G["r_r_bias"], H, Nt, dh)
@@ -324,7 +328,7 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     # every bias / gain column sum of the block finished in one launch
     ops.colsum_finish_multi([(pm, nbm, G["b2"]), (part[:, :f], nbc, G["b1"]), (pg2, nbl_cur, G["ln2_g"]),
                              (pb2, nbl_cur, G["ln2_b"]), (pg, nbl_cur + nbl_mem, G["ln1_g"]),
-                             (pb, nbl_cur + nbl_mem, G["ln1_b"])])
+                             (pb, nbl_cur + nbl_mem, G["ln1_b"])] + bias_jobs)
 
 
 # ---------------------------------------------------------------------------
