@@ -110,3 +110,31 @@ def test_xl_ouroboros_with_adaptive_head_matches_restatement(K):
                     assert rel(g, want) <= 2e-4, (t, k, key, rel(g, want))
         if np.any(opk["emb_grad"]):
             assert rel(got.emb_grad, opk["emb_grad"]) <= 2e-4
+
+
+def test_device_batches_equal_host_batches_with_the_adaptive_head():
+    """Device-resident targets reach the adaptive head's host bucketing
+    through an early side-stream copy (adaptive.HostCopy), not a stream sync:
+    the same losses and tied gradient as host batches, bitwise."""
+    from paper_1909_06695_b200 import engine as E
+    from paper_1909_06695_b200 import model as MD
+    from paper_1909_06695_b200 import optim as O
+    from oracle.rng import Stream
+
+    vocab, d, f, blocks, T, M, H, B, cut = 96, 64, 128, 2, 16, 16, 2, 2, [24, 56]
+    toks = [((Stream(s).uniform((B, T)) * vocab).astype(np.int64), (Stream(s + 50).uniform((B, T)) * vocab).astype(np.int64))
+            for s in range(4)]
+    runs = []
+    for device_batches in (False, True):
+        stack = MD.build_xl_stack(vocab, d, f, blocks, T, 0.1, 5, H, M, dtype="bf16", cutoffs=cut)
+        eng = E.ConcurrentPipelineEngine(stack, MD.partition(stack.num_layers, 2), 9)
+        opt = O.make_optimizer("adam", O.LrSchedule(1e-3, "fixed"))
+        losses = []
+        for t, (x, y) in enumerate(toks):
+            if device_batches:
+                x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+            packet, loss = eng.step(t, E.BatchSample(x, y, t), opt)
+            losses.append(loss)
+        runs.append((losses, packet.cpu().emb_grad))
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
