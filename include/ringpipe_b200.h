@@ -205,11 +205,21 @@ int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, vo
                    int64_t mem_len, float scale, void* stream);
 /* rp_xl_attn_bwd plus the query gradients on the tensor cores (dh = 64, T % 128 == 0):
  * grad_qu = dAC kh and grad_qv = dBD r_h, fp32 [H*B*T, dh] -- the two head-dim-wide GEMMs
- * over the dAC / dBD matrices are folded into the kernel (dS stays in shared memory) */
+ * over the dAC / dBD matrices are folded into the kernel (dS stays in shared memory).
+ * grad_ac NULL: dAC is not written (rp_xl_attn_bwd_kv forms the key gradient itself);
+ * d_rows (or NULL): D_i = <g_ctx_i, ctx_i> per query row, fp32 [H*B*T], for rp_xl_attn_bwd_kv */
 int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
                       void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,
                       float* grad_qv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, float* bias_part, void* stream);
+                      float scale, float* bias_part, float* d_rows, void* stream);
+/* Key-major key / value gradients (bf16, dh = 64, T % 128 == 0; after rp_xl_attn_bwd_dq with
+ * d_rows): one CTA per (head*batch, 128-key tile) recomputes dP = g_ctx_h v^T and dS on the
+ * tensor cores and accumulates grad_vh = P^T g_ctx_h and grad_kh = dS^T qu in TMEM, written as
+ * bf16 [H*B, M+T, dh] -- bitwise the banded GEMMs over P and dAC it replaces (kernels.bmm,
+ * kernels.py:68-81, on the XL score matrices), without the dAC matrix */
+int rp_xl_attn_bwd_kv(const void* grad_ctx_h, const void* vh, const void* qu, const void* probs, int64_t ld_p,
+                      const float* d_rows, void* grad_kh, void* grad_vh, int64_t B, int64_t T, int64_t M, int32_t H,
+                      int32_t dh, int64_t mem_len, float scale, void* stream);
 /* bias_part of rp_xl_attn_bwd_dq (or NULL): per-CTA column sums of grad_qu / grad_qv, which
  * rp_xl_dq_bias_finish turns into the r_w_bias / r_r_bias gradients ([H, 64] each) without
  * re-reading the query gradients (the column sums of rp_xl_bias_grad) */
@@ -370,6 +380,7 @@ int rp_head_backward(const rp_head_desc* desc, const void* x, const void* tied, 
 #define RP_XL_FUSED_PV 4  /* rp_xl_attn_fwd_pv (bf16, dh 64) */
 #define RP_XL_FUSED_DQ 8  /* rp_xl_attn_bwd_dq (bf16, dh 64, T % 128 == 0) */
 #define RP_XL_BANDED 16   /* dK / dV GEMMs skip the causal window's all-zero query blocks (bitwise the dense result) */
+#define RP_XL_FUSED_KV 32 /* rp_xl_attn_bwd_kv after rp_xl_attn_bwd_dq (no dAC; needs RP_XL_FUSED_DQ) */
 typedef struct rp_xl_block_desc {
   int64_t B, T, M, d, f;
   int32_t H, dtype;

@@ -103,7 +103,7 @@ class ModuleDesc(ctypes.Structure):
                 ("M", ctypes.c_int64), ("xl_fused", ctypes.c_int32), ("score_tile", ctypes.c_int32)]
 
 
-XL_FUSED_FWD, XL_FUSED_BWD, XL_FUSED_PV, XL_FUSED_DQ, XL_BANDED = 1, 2, 4, 8, 16
+XL_FUSED_FWD, XL_FUSED_BWD, XL_FUSED_PV, XL_FUSED_DQ, XL_BANDED, XL_FUSED_KV = 1, 2, 4, 8, 16, 32
 
 
 class XlBlockDesc(ctypes.Structure):
@@ -216,7 +216,8 @@ def _declare(L):
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd_pv": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, i32, i32, i64, f32, i32, i64, vp],
         "rp_xl_attn_bwd_dq": [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp,
-                              vp],
+                              vp, vp],
+        "rp_xl_attn_bwd_kv": [vp, vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
         "rp_xl_dq_bias_part_bytes": [i32, i64, i64],
         "rp_xl_dq_bias_finish": [vp, vp, vp, i32, i64, i64, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],

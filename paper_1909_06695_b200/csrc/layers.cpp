@@ -544,7 +544,10 @@ int check_xl(const rp_xl_block_desc& d) {
     return set_error(RP_ERR_DIMENSION,
                      "xl_block: the composite takes dense bf16 rows (d, d_ff, head dim multiples of 8); "
                      "pitched rows go through the op-level entry points");
-  if (d.dtype != RP_BF16 && (d.fused & 15)) return set_error(RP_ERR_INVALID, "xl_block: fused kernels are bf16 only");
+  if (d.dtype != RP_BF16 && (d.fused & (15 | RP_XL_FUSED_KV)))
+    return set_error(RP_ERR_INVALID, "xl_block: fused kernels are bf16 only");
+  if ((d.fused & RP_XL_FUSED_KV) && !(d.fused & RP_XL_FUSED_DQ))
+    return set_error(RP_ERR_INVALID, "xl_block: RP_XL_FUSED_KV needs RP_XL_FUSED_DQ");
   return RP_OK;
 }
 
@@ -571,6 +574,7 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   bwd += 2 * al256(x.HB * x.Kl * x.dh * e) + al256(x.H * x.Kl * x.dh * 4);  // g_vh, g_kh (compute dtype), g_rh
   bwd += al256(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh));
   if (d.fused & RP_XL_FUSED_DQ) bwd += al256(xl_dq_bias_part_bytes((int)x.H, x.B, x.T));
+  if (d.fused & RP_XL_FUSED_KV) bwd += al256(x.HB * x.T * 4);  // D rows
   bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
   bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
   bwd += al256(kBlockSplitK);
@@ -699,6 +703,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   float* bias_ws = static_cast<float*>(bp.take(xl_bias_grad_workspace_bytes((int)x.H, (int)x.dh)));
   float* dq_bias = (d.fused & RP_XL_FUSED_DQ) ? static_cast<float*>(bp.take(xl_dq_bias_part_bytes((int)x.H, x.B, x.T)))
                                               : nullptr;
+  const bool kv = (d.fused & RP_XL_FUSED_KV) != 0;
+  float* d_rows = kv ? static_cast<float*>(bp.take(x.HB * x.T * 4)) : nullptr;
   void* g_r = bp.take(x.Kl * D * e);
   void* g_qkv = bp.take(BK * 3 * D * e);
   float* g_a = static_cast<float*>(bp.take(BK * D * 4));
@@ -731,8 +737,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   RP_TRY(xl_split_heads(dt, g_ctx, D, dt, g_ctx_h, N, (int)x.H, (int)x.dh, st));
   bool dq_done = false;
   if (d.fused & RP_XL_FUSED_DQ) {
-    RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, g_qu, g_qv, x.B,
-                          x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st, dq_bias));
+    RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, kv ? nullptr : g_ac, g_bd, x.ldk, g_ctx, tp.ctx,
+                          g_qu, g_qv, x.B, x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st, dq_bias, d_rows));
     dq_done = true;
   } else if (d.fused & RP_XL_FUSED_BWD) {
     RP_TRY(xl_attn_bwd(g_ctx_h, tp.vh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, x.B, x.T, x.M, (int)x.H, (int)x.dh,
@@ -750,15 +756,21 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   Epi eband;
   eband.k_lo = (d.fused & RP_XL_BANDED) ? 1 : 0;
   eband.k_lo_off = -x.M;
-  RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true, bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh),
-            true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt, eband));
+  if (kv)  // dV = P^T dO and dK = dS^T (q+u) in one key-major kernel (no dAC)
+    RP_TRY(xl_attn_bwd_kv(g_ctx_h, tp.vh, tp.qu, tp.probs, x.ldk, d_rows, g_kh, g_vh, x.B, x.T, x.M, (int)x.H,
+                          (int)x.dh, d.mem_len, scale, st));
+  else
+    RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true,
+              bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt,
+              eband));
   const Mat gac = bmat(g_ac, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk);
   const Mat gbd = bmat(g_bd, x.H, N, x.Kl, x.ldk, N * x.ldk);
   if (!dq_done)
     RP_TRY(mm(c, gac, false, bmat(tp.kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), RP_F32));
-  RP_TRY(mm(c, gac, true, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true,
-            bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt, eband));
+  if (!kv)
+    RP_TRY(mm(c, gac, true, bmat(tp.qu, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true,
+              bmat(g_kh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt, eband));
   if (!dq_done)
     RP_TRY(mm(c, gbd, false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));

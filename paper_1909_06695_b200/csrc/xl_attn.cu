@@ -1012,6 +1012,8 @@ struct DqParams {
   float* gqv;
   float* bias_part;  // optional [2][B*nqt][H*64]: per-CTA column sums of dQu (u) and dQv (v) -- a
                      // [rows, cols] block per bias that a column-sum finish reduces
+  float* d_rows;     // optional [HB*T]: D_i = dO_i . O_i for xl_attn_bwd_kv
+  int no_dac;        // dAC is not written (xl_attn_bwd_kv computes dK from dS itself)
 };
 
 // out[lane] = sum over the warp's 32 rows of column `lane` of v[0..31]
@@ -1202,13 +1204,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           D = fmaf(gf.y, cf.y, D);
         }
       }
+      if (dq.d_rows && half == 0) dq.d_rows[(int64_t)hb * p.T + i] = D;
       // columns outside the key tiles this query tile sees: dAC = 0, and the
       // dBD margins outside the stored band chunks
       if (half == 0) {
-        zero_row(arow, 0, (int64_t)jt_lo * kKT);
+        if (!dq.no_dac) zero_row(arow, 0, (int64_t)jt_lo * kKT);
         zero_row(brow, 0, lmin(lmax(P0, 0), p.ldp));
       } else {
-        zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
+        if (!dq.no_dac) zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
         zero_row(brow, lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp), p.ldp);
       }
     }
@@ -1317,7 +1320,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       fence_proxy_async_smem();
       __syncwarp();
       // this warp's 32 x 64 dAC block straight from the swizzled dS tile
-      if (lane == 0 && jt0 < p.ldp) tma_store_3d(&mAC, sA + half * (128 * 128) + 32 * q * 128, jt0, i0 + 32 * q, hb);
+      if (!dq.no_dac && lane == 0 && jt0 < p.ldp) tma_store_3d(&mAC, sA + half * (128 * 128) + 32 * q * 128, jt0, i0 + 32 * q, hb);
       // earlier dBD chunk stores have read the ring (all but the newest bulk
       // group: this tile's dAC store, which nobody waits for here)
       if (warp == 4 && lane == 0) bulk_wait_read_1();
@@ -1378,6 +1381,254 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
     }
     if (lane == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+// Key-major backward of the key-side gradients (head dim 64, bf16; after
+// xl_attn_bwd_dq, which leaves D_i = dO_i . O_i per query row): one CTA per
+// (head*batch, 128-key tile), over the query tiles that see the tile
+//     dP   = dO_q V^T            TMEM cols 0..255 (two buffers), lanes = queries
+//     dS   = P (dP - D) scale    bwd_dq's dAC arithmetic, bf16 into a swizzled [128 x 128] tile
+//     dV  += P_q^T dO_q          TMEM cols 256..319, lanes = keys (A = the TMA'd P tile, MN-major)
+//     dK  += dS_q^T Qu_q         TMEM cols 320..383            (A = the dS tile, MN-major)
+// This is the K = 16 MMA sequence of the banded dV / dK GEMMs over P and dAC
+// (the same operands in the same order), so the result is bitwise theirs --
+// without the dAC matrix (185 MB written and read per block at C3) or the
+// GEMMs' second read of P.
+constexpr int kKvSmem = 1024 + 16384 /*V*/ + 2 * 16384 /*dO*/ + 2 * 16384 /*Qu*/ + 2 * kChunkBytes /*P*/ +
+                        kChunkBytes /*dS*/ + 256 /*barriers*/;
+
+struct KvParams {
+  const float* D;     // [HB*T]
+  __nv_bfloat16* gk;  // [HB, Kl, 64]
+  __nv_bfloat16* gv;
+  int T, M, Kl, lo, nkt;
+  float scale;
+};
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    xl_attn_bwd_kv_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
+                          const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mP,
+                          const KvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sV = smem;
+  uint8_t* sG = sV + 16384;      // [2]
+  uint8_t* sU = sG + 2 * 16384;  // [2]
+  uint8_t* sP = sU + 2 * 16384;  // [2] x two 64-key atoms
+  uint8_t* sA = sP + 2 * kChunkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kChunkBytes);
+  uint64_t* v_full = bars;
+  uint64_t* g_full = bars + 1;      // [2]
+  uint64_t* g_empty = bars + 3;     // [2]
+  uint64_t* u_full = bars + 5;      // [2]
+  uint64_t* u_empty = bars + 7;     // [2]
+  uint64_t* p_full = bars + 9;      // [2]
+  uint64_t* p_empty = bars + 11;    // [2]: the softmax warps' reads + the dV MMA
+  uint64_t* acc_full = bars + 13;   // [2]
+  uint64_t* acc_empty = bars + 15;  // [2]
+  uint64_t* ds_ready = bars + 17;
+  uint64_t* a_free = bars + 18;
+  uint64_t* done = bars + 19;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // key tile major: the memory-side tiles, seen by every query tile, first
+  const int HB = (int)gridDim.x / p.nkt;
+  const int kt = (int)blockIdx.x / HB, hb = (int)blockIdx.x % HB;
+  const int j0 = kt * kKT;
+  // query i sees key j <= M + i: the first query tile with a query at or past j0 - M
+  const int qt_lo = max(j0 - p.M, 0) / kQT;
+  const int nq = p.T / kQT - qt_lo;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mG);
+    tma_prefetch(&mV);
+    tma_prefetch(&mU);
+    tma_prefetch(&mP);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(v_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&g_full[s], 1);
+      mbar_init(&g_empty[s], 1);
+      mbar_init(&u_full[s], 1);
+      mbar_init(&u_empty[s], 1);
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], kSoftWarps * 32 + 1);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kSoftWarps * 32);
+    }
+    mbar_init(ds_ready, 1);
+    mbar_init(a_free, 1);
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t t_dv = tmem_base + 256, t_dk = tmem_base + 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_expect_tx(v_full, 16384);
+      tma_load_3d(sV, &mV, v_full, 0, j0, hb);
+      for (int n = 0; n < nq; ++n) {
+        const int s = n & 1;
+        const uint32_t ph = ((n >> 1) & 1) ^ 1;
+        const int i0 = (qt_lo + n) * kQT;
+        mbar_wait(&g_empty[s], ph);
+        mbar_expect_tx(&g_full[s], 16384);
+        tma_load_3d(sG + s * 16384, &mG, &g_full[s], 0, i0, hb);
+        mbar_wait(&p_empty[s], ph);
+        mbar_expect_tx(&p_full[s], kChunkBytes);
+        tma_load_3d(sP + s * kChunkBytes, &mP, &p_full[s], j0, i0, hb);
+        tma_load_3d(sP + s * kChunkBytes + 128 * 128, &mP, &p_full[s], j0 + 64, i0, hb);
+        mbar_wait(&u_empty[s], ph);
+        mbar_expect_tx(&u_full[s], 16384);
+        tma_load_3d(sU + s * 16384, &mU, &u_full[s], 0, i0, hb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
+      const uint32_t id_kv = umma_idesc(false, true, true, kKT, 64);
+      const uint32_t vb = smem_u32(sV), aa = smem_u32(sA);
+      mbar_wait(v_full, 0);
+      auto issue_dk = [&](int m) {
+        const int s = m & 1;
+        mbar_wait(ds_ready, m & 1);
+        mbar_wait(&u_full[s], (m >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ua = smem_u32(sU + s * 16384);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma<false>(t_dk, umma_desc(aa + k * 2048, 16384, 1024), umma_desc(ua + k * 2048, 16384, 1024), id_kv,
+                        (m | k) != 0);
+        tc_commit(a_free);
+        tc_commit(&u_empty[s]);
+      };
+      for (int n = 0; n < nq; ++n) {
+        const int s = n & 1;
+        const uint32_t ph = (n >> 1) & 1;
+        mbar_wait(&acc_empty[s], ph ^ 1);
+        mbar_wait(&g_full[s], ph);
+        tc_fence_after();
+        const uint32_t ga = smem_u32(sG + s * 16384);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vb, kKT, k), id_dp, k > 0);
+        tc_commit(&acc_full[s]);
+        mbar_wait(&p_full[s], ph);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sP + s * kChunkBytes);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma<false>(t_dv, umma_desc(pa + k * 2048, 16384, 1024), umma_desc(ga + k * 2048, 16384, 1024), id_kv,
+                        (n | k) != 0);
+        tc_commit(&p_empty[s]);
+        tc_commit(&g_empty[s]);
+        if (n >= 1) issue_dk(n - 1);
+      }
+      issue_dk(nq - 1);
+      tc_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const int rsw = r & 7;
+    const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    float D = p.D[(int64_t)hb * p.T + qt_lo * kQT + r];
+    for (int n = 0; n < nq; ++n) {
+      const int s = n & 1;
+      const uint32_t ph = (n >> 1) & 1;
+      const int i = (qt_lo + n) * kQT + r;
+      const int jhi = p.M + i;
+      const float Dn = (n + 1 < nq) ? p.D[(int64_t)hb * p.T + i + kQT] : 0.f;  // the next tile's, in flight
+      uint4 pr[2][4];
+      mbar_wait(&p_full[s], ph);
+      {
+        const uint8_t* prow_s = sP + s * kChunkBytes + half * (128 * 128) + r * 128;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            pr[k][c] = *reinterpret_cast<const uint4*>(prow_s + (((4 * k + c) ^ rsw) << 4));
+      }
+      mbar_arrive(&p_empty[s]);
+      mbar_wait(&acc_full[s], ph);
+      tc_fence_after();
+      uint32_t dp[2][32];
+      tmem_ld32(tl + s * kKT + 64 * half, dp[0]);
+      tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[s]);
+      if (n >= 1) mbar_wait(a_free, (n - 1) & 1);  // the previous tile's dK MMA has read the dS tile
+      uint8_t* arow_s = sA + half * (128 * 128) + r * 128;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int jb = j0 + 64 * half + 32 * k;
+        const bool inside = jb >= p.lo && jb + 31 <= jhi;
+        uint32_t o[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t w[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+            const int t = 8 * c + 2 * e;
+            const int j = jb + t;
+            float a0 = pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale;
+            float a1 = pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale;
+            if (!inside) {
+              a0 = (j >= p.lo && j <= jhi) ? a0 : 0.f;
+              a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? a1 : 0.f;
+            }
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+            o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(arow_s + (((4 * k + c) ^ rsw) << 4)) =
+              make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+      }
+      D = Dn;
+      fence_proxy_async_smem();
+      named_sync(1, kSoftWarps * 32);
+      if (warp == 4 && lane == 0) mbar_arrive(ds_ready);
+    }
+    // ---- dV / dK epilogue: key rows of this lane quarter, columns [32 half, +32)
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int j = j0 + r;
+    const int64_t orow = ((int64_t)hb * p.Kl + j) * 64 + 32 * half;
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      uint32_t v[32];
+      tmem_ld32(tl + 256 + 64 * w + 32 * half, v);
+      if (j < p.Kl) {
+        uint4* dst = reinterpret_cast<uint4*>((w == 0 ? p.gv : p.gk) + orow);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 b2 =
+                __floats2bfloat162_rn(__uint_as_float(v[8 * c + 2 * e]), __uint_as_float(v[8 * c + 2 * e + 1]));
+            o[e] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1514,7 +1765,8 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
 
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
                    void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
-                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st, float* bias_part) {
+                   int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st, float* bias_part,
+                   float* d_rows) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: head dim must be 64 (got %d)", dh);
   if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: T must be a multiple of 128");
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
@@ -1529,7 +1781,8 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   RP_TRY0(tma_map_bf16(&mk, kh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
   RP_TRY0(tma_map_bf16(&mr, rh, dh, Kl, dh, H, Kl * dh, 64, kKT));
   RP_TRY0(tma_map_bf16(&mbd, gbd, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
-  RP_TRY0(tma_map_bf16(&mac, gac, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
+  // gac NULL: no dAC (xl_attn_bwd_kv forms dK from dS itself); the map is then never used
+  RP_TRY0(tma_map_bf16(&mac, gac ? gac : gbd, ldp, Tn, ldp, HB, Tn * ldp, 64, 32));
   static uint64_t attr_done = 0;
   if (first_on_device(attr_done))
     cudaFuncSetAttribute(xl_attn_bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
@@ -1554,10 +1807,48 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   q.gqu = gqu;
   q.gqv = gqv;
   q.bias_part = bias_part;
+  q.d_rows = d_rows;
+  q.no_dac = gac == nullptr;
+  if ((reinterpret_cast<uintptr_t>(d_rows) & 3) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned D rows");
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
   xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);
   return check_launch("xl_attn_bwd_dq");
+}
+
+int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const void* probs, int64_t ldp,
+                   const float* d_rows, void* gk, void* gv, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
+                   float scale, cudaStream_t st) {
+  if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: head dim must be 64 (got %d)", dh);
+  if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: T must be a multiple of 128");
+  const int64_t Kl = M + Tn, HB = (int64_t)H * B;
+  if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: ldp must be >= M+T, multiple of 8");
+  if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: mem_len out of range");
+  if (!d_rows || !gk || !gv) return set_error(RP_ERR_INVALID, "xl_attn_bwd_kv: null output or D rows");
+  for (const void* q : {probs, gctx_h, vh, qu, (const void*)gk, (const void*)gv})
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: unaligned operand");
+  CUtensorMap mg, mv, mu, mp;
+  RP_TRY0(tma_map_bf16(&mp, probs, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mg, gctx_h, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  RP_TRY0(tma_map_bf16(&mv, vh, dh, Kl, dh, HB, Kl * dh, 64, kKT));
+  RP_TRY0(tma_map_bf16(&mu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
+  static uint64_t attr_done = 0;
+  if (first_on_device(attr_done))
+    cudaFuncSetAttribute(xl_attn_bwd_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem);
+  KvParams p{};
+  p.D = d_rows;
+  p.gk = static_cast<__nv_bfloat16*>(gk);
+  p.gv = static_cast<__nv_bfloat16*>(gv);
+  p.T = (int)Tn;
+  p.M = (int)M;
+  p.Kl = (int)Kl;
+  p.lo = (int)(M - mem_len);
+  p.nkt = (int)((Kl + kKT - 1) / kKT);
+  p.scale = scale;
+  const int64_t grid = HB * p.nkt;
+  if (grid <= 0) return RP_OK;
+  xl_attn_bwd_kv_kernel<<<(unsigned)grid, kThreadsBwd, kKvSmem, st>>>(mg, mv, mu, mp, p);
+  return check_launch("xl_attn_bwd_kv");
 }
 
 int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* vh, const void* rh, void* probs,

@@ -489,11 +489,16 @@ def xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ctx, B, T, M, mem_len, scale):
 
 
 def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale,
-                   bias_part=None):
+                   bias_part=None, d_rows=None):
     """xl_attn_bwd plus the query gradients on the tensor cores (dh = 64,
-    T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh]."""
-    _require_cuda(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv)
-    for t in (g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx):
+    T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh].
+    g_ac None: dAC is not written (xl_attn_bwd_kv forms dK itself); d_rows:
+    fp32 [H*B*T] receives D_i = <g_ctx_i, ctx_i> for xl_attn_bwd_kv."""
+    _require_cuda(g_ctx_h, vh, kh, rh, probs, g_bd, g_ctx, ctx, g_qu, g_qv)
+    if d_rows is not None and (d_rows.dtype != torch.float32 or d_rows.numel() < g_qu.shape[0] * g_qu.shape[1]
+                               or not d_rows.is_contiguous()):
+        raise DimensionError("xl_attn_bwd_dq: d_rows is a contiguous fp32 [H*B*T] buffer")
+    for t in (g_ctx_h, vh, kh, rh, probs, g_bd, g_ctx, ctx) + ((g_ac,) if g_ac is not None else ()):
         if t.dtype != torch.bfloat16:
             raise DimensionError("xl_attn_bwd_dq takes bf16 operands")
     for t in (g_qu, g_qv):
@@ -503,13 +508,34 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
         if not t.is_contiguous():
             raise DimensionError("xl_attn_bwd_dq operands must be contiguous")
     ldp = probs.stride(-2)
-    if g_ac.stride(-2) != ldp or g_bd.stride(-2) != ldp:
+    if (g_ac is not None and g_ac.stride(-2) != ldp) or g_bd.stride(-2) != ldp:
         raise DimensionError("xl_attn_bwd_dq: P, dAC and dBD must share the row pitch")
     H, dh = g_ctx.shape[-1] // vh.shape[-1], vh.shape[-1]
     _count(1)
     N.check(N.lib().rp_xl_attn_bwd_dq(_ptr(g_ctx_h), _ptr(vh), _ptr(kh), _ptr(rh), _ptr(probs), _ptr(g_ac),
                                       _ptr(g_bd), ldp, _ptr(g_ctx), _ptr(ctx), _ptr(g_qu), _ptr(g_qv), B, T, M, H, dh,
-                                      mem_len, scale, _ptr(bias_part), _stream()), "xl_attn_bwd_dq")
+                                      mem_len, scale, _ptr(bias_part), _ptr(d_rows), _stream()), "xl_attn_bwd_dq")
+
+
+def xl_attn_bwd_kv(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh, B, T, M, mem_len, scale):
+    """Key-major dK / dV (dh = 64, T % 128 == 0; after xl_attn_bwd_dq with
+    d_rows): g_vh = P^T g_ctx_h and g_kh = dS^T qu as bf16 [H*B, M+T, dh],
+    bitwise the banded GEMMs over P and dAC."""
+    _require_cuda(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh)
+    for t in (g_ctx_h, vh, qu, probs, g_kh, g_vh):
+        if t.dtype != torch.bfloat16:
+            raise DimensionError("xl_attn_bwd_kv takes bf16 operands")
+    for t in (g_ctx_h, vh, qu, g_kh, g_vh, d_rows):
+        if not t.is_contiguous():
+            raise DimensionError("xl_attn_bwd_kv operands must be contiguous")
+    if d_rows.dtype != torch.float32:
+        raise DimensionError("xl_attn_bwd_kv: d_rows is fp32")
+    dh = vh.shape[-1]
+    H = vh.numel() // (B * (M + T) * dh)
+    _count(1)
+    N.check(N.lib().rp_xl_attn_bwd_kv(_ptr(g_ctx_h), _ptr(vh), _ptr(qu), _ptr(probs), probs.stride(-2), _ptr(d_rows),
+                                      _ptr(g_kh), _ptr(g_vh), B, T, M, H, dh, mem_len, scale, _stream()),
+            "xl_attn_bwd_kv")
 
 
 def xl_dq_bias_part_elems(H, B, T):

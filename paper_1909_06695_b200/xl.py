@@ -123,6 +123,7 @@ def fused_bwd_ok(tp):
 FUSED_DQ = os.environ.get("RP_XL_FUSED_DQ", "1") != "0"
 FUSED_PV = os.environ.get("RP_XL_FUSED_PV", "1") != "0"
 BANDED = os.environ.get("RP_XL_BANDED", "1") != "0"
+FUSED_KV = os.environ.get("RP_XL_FUSED_KV", "1") != "0"
 
 
 def fused_pv_ok(tp):
@@ -137,6 +138,12 @@ def fused_dq_ok(tp):
     """The backward with the query-gradient MMAs folded in (xl_attn_bwd_dq):
     head dim 64 and whole 128-query tiles."""
     return FUSED_DQ and fused_bwd_ok(tp) and tp.dh == 64 and tp.T % 128 == 0
+
+
+def fused_kv_ok(tp):
+    """dK / dV from the key-major kernel (xl_attn_bwd_kv) after xl_attn_bwd_dq,
+    which then skips the dAC matrix."""
+    return FUSED_KV and fused_dq_ok(tp)
 
 
 # The engines run each XL block as ONE C-ABI call (rp_xl_block_forward /
@@ -269,13 +276,16 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     g_qv = f32r("xl_g_qv", H, Nt, dh)
     dq_done = False
     bias_part = None
+    kv = fused_kv_ok(tp)
+    d_rows = ws.get("xl_d_rows", (H * B * T,), torch.float32) if kv else None
     if fused_dq_ok(tp):
         # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu),
-        # plus the per-CTA column sums of dQu / dQv for the u / v gradients
+        # plus the per-CTA column sums of dQu / dQv for the u / v gradients; with
+        # the key-major kernel below it leaves D per query row instead of dAC
         bias_part = ws.get("xl_dq_bias", (ops.xl_dq_bias_part_elems(H, B, T),), torch.float32)
         with ops.span("xl_attn_bwd"):
-            ops.xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs_buf, g_ac, g_bd, g_ctx, tp.ctx, g_qu, g_qv, B,
-                               T, M, tp.mem_len, scale, bias_part=bias_part)
+            ops.xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs_buf, None if kv else g_ac, g_bd, g_ctx, tp.ctx,
+                               g_qu, g_qv, B, T, M, tp.mem_len, scale, bias_part=bias_part, d_rows=d_rows)
         dq_done = True
     elif fused_bwd_ok(tp):
         # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
@@ -290,13 +300,21 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     # P^T and dAC^T are banded: key j sees queries i >= j - M (causal window),
     # so each key tile starts its K loop (over queries) at its first live block
     band = -M if BANDED else None
-    ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
-    g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
     g_kh = ws.get_rows("xl_g_kh", (H * B, Kl, dh), cdt) if cdt == torch.bfloat16 else f32r("xl_g_kh", H * B, Kl, dh)
+    if kv:
+        # dV = P^T dO and dK = dS^T (q+u) in one key-major kernel: bitwise the two
+        # banded GEMMs below, without the dAC matrix
+        with ops.span("xl_attn_bwd"):
+            ops.xl_attn_bwd_kv(g3, tp.vh.view(H * B, Kl, dh), tp.qu.view(H * B, T, dh), tp.probs_buf, d_rows, g_kh,
+                               g_vh, B, T, M, tp.mem_len, scale)
+    else:
+        ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
+    g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
     g_rh = f32r("xl_g_rh", H, Kl, dh)
     if not dq_done:
         ops.gemm(g_ac, tp.kh.view(H * B, Kl, dh), b_mn=True, out=g_qu.view(H * B, T, dh))
-    ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh, k_lo_off=band)
+    if not kv:
+        ops.gemm(g_ac, tp.qu.view(H * B, T, dh), a_mn=True, b_mn=True, out=g_kh, k_lo_off=band)
     if not dq_done:
         ops.gemm(g_bd, tp.rh, b_mn=True, out=g_qv)
     ops.gemm(g_bd, tp.qv, a_mn=True, b_mn=True, out=g_rh)
@@ -346,6 +364,8 @@ def fused_flags(tp):
         f |= N.XL_FUSED_FWD
     if fused_dq_ok(tp):
         f |= N.XL_FUSED_DQ
+        if fused_kv_ok(tp):
+            f |= N.XL_FUSED_KV
     elif fused_bwd_ok(tp):
         f |= N.XL_FUSED_BWD
     if BANDED:

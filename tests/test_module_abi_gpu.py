@@ -173,6 +173,7 @@ def test_xl_block_abi_bitwise_equals_host_loop(dtype, act):
         assert torch.equal(u, v)
     if dtype == "bf16":
         assert XD.fused_flags(tp) & 15 == 12  # the P.V-fused forward and the dQ-fused backward ran
+        assert XD.fused_flags(tp) & XD.N.XL_FUSED_KV  # and the key-major dK / dV kernel
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])

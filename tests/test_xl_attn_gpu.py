@@ -331,3 +331,68 @@ def test_fused_pv_forward_equals_fused_forward_plus_gemm(B, H, T, M, mem_len):
     want = want_h.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh)
     assert torch.isfinite(ctx.float()).all()
     assert rel(ctx.float().cpu(), want.cpu()) <= 4e-3
+
+
+@pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 2, 256, 256, 100), (2, 1, 128, 0, 0),
+                                             (1, 3, 384, 128, 60), (2, 8, 512, 512, 512), (1, 2, 256, 200, 150)])
+def test_fused_kv_backward_equals_banded_gemms(B, H, T, M, mem_len):
+    """xl_attn_bwd_kv: dV = P^T dO and dK = dS^T (q+u), key-major with dS
+    recomputed from P, dP and xl_attn_bwd_dq's D rows, bitwise equal to the
+    banded dV / dK GEMMs over P and dAC (the same K = 16 MMA sequence); and
+    xl_attn_bwd_dq without dAC leaves dBD / dQu / dQv bitwise unchanged."""
+    from paper_1909_06695_b200 import ops
+
+    dev, dh = "cuda", 64
+    g = torch.Generator(device=dev).manual_seed(7 * T + M + mem_len)
+    Kl = M + T
+    ldp = _pad8(Kl)
+    mk = lambda *s: (torch.randn(*s, device=dev, generator=g) * 0.6).to(torch.bfloat16)  # noqa: E731
+    qu, qv = mk(H, B * T, dh), mk(H, B * T, dh)
+    kh, rh, vh = mk(H, B * Kl, dh), mk(H, Kl, dh), mk(H, B * Kl, dh)
+    scale = 1.0 / math.sqrt(dh)
+    probs = torch.empty(H * B, T, ldp, device=dev, dtype=torch.bfloat16)
+    ops.xl_attn_fwd(qu, qv, kh, rh, probs, B, T, M, mem_len, scale)
+    g3 = mk(H, B * T, dh)
+    gctx = g3.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    ctx_h = (probs[:, :, :Kl].float() @ vh.float().view(H * B, Kl, dh)).to(torch.bfloat16)
+    ctx = ctx_h.view(H, B * T, dh).permute(1, 0, 2).reshape(B * T, H * dh).contiguous()
+    nan = lambda *s: torch.full(s, float("nan"), device=dev, dtype=torch.bfloat16)  # noqa: E731
+    nanf = lambda *s: torch.full(s, float("nan"), device=dev)  # noqa: E731
+    gac1, gbd1, gbd2 = nan(H * B, T, ldp), nan(H, B * T, ldp), nan(H, B * T, ldp)
+    gqu1, gqv1, gqu2, gqv2 = (nanf(H, B * T, dh) for _ in range(4))
+    d_rows = nanf(H * B * T)
+    ops.xl_attn_bwd_dq(g3, vh, kh, rh, probs, gac1, gbd1, gctx, ctx, gqu1, gqv1, B, T, M, mem_len, scale)
+    ops.xl_attn_bwd_dq(g3, vh, kh, rh, probs, None, gbd2, gctx, ctx, gqu2, gqv2, B, T, M, mem_len, scale,
+                       d_rows=d_rows)
+    gk, gv = nan(H * B, Kl, dh), nan(H * B, Kl, dh)
+    g3h, quh = g3.view(H * B, T, dh), qu.view(H * B, T, dh)
+    ops.xl_attn_bwd_kv(g3h, vh.view(H * B, Kl, dh), quh, probs, d_rows, gk, gv, B, T, M, mem_len, scale)
+    want_v, want_k = nan(H * B, Kl, dh), nan(H * B, Kl, dh)
+    ops.gemm(probs[:, :, :Kl], g3h, a_mn=True, b_mn=True, out=want_v, k_lo_off=-M)
+    ops.gemm(gac1[:, :, :Kl], quh, a_mn=True, b_mn=True, out=want_k, k_lo_off=-M)
+    torch.cuda.synchronize()
+    assert torch.equal(gbd1, gbd2)
+    assert torch.equal(gqu1, gqu2) and torch.equal(gqv1, gqv2)
+    want_d = (gctx.float() * ctx.float()).view(B, T, H, dh).sum(-1).permute(2, 0, 1).reshape(-1)
+    assert rel(d_rows.cpu(), want_d.cpu()) <= 1e-5
+    assert torch.equal(gv, want_v), (gv.float() - want_v.float()).abs().max().item()
+    assert torch.equal(gk, want_k), (gk.float() - want_k.float()).abs().max().item()
+    # and against fp32 torch products of the same bf16 matrices (one bf16 rounding)
+    fv = probs[:, :, :Kl].float().transpose(1, 2) @ g3h.float()
+    fk = gac1[:, :, :Kl].float().transpose(1, 2) @ quh.float()
+    assert rel(gv.float().cpu(), fv.cpu()) <= 4e-3
+    assert rel(gk.float().cpu(), fk.cpu()) <= 4e-3
+
+
+@pytest.mark.parametrize("H,T,M,mem_len", [(2, 128, 128, 128), (2, 256, 128, 100)])
+def test_fused_kv_block_bitwise_equals_gemm_path(H, T, M, mem_len, monkeypatch):
+    """A bf16 XL block with the key-major dK / dV kernel (RP_XL_FUSED_KV) is
+    bitwise the block with the banded GEMMs over P and dAC."""
+    from paper_1909_06695_b200 import xl as XD
+
+    monkeypatch.setattr(XD, "FUSED_KV", True)
+    a, _ = _block(H, T, M, mem_len, True, monkeypatch)
+    monkeypatch.setattr(XD, "FUSED_KV", False)
+    b, _ = _block(H, T, M, mem_len, True, monkeypatch)
+    for k in b:
+        assert np.array_equal(a[k], b[k]), (k, rel(a[k], b[k]))
