@@ -20,6 +20,7 @@
 // thread), warp 2 TMEM allocator, warps 4..11 softmax (warp w owns TMEM lane
 // quarter w % 4 and half of each key tile's columns).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1388,61 +1389,97 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 }
 
 // Key-major backward of the key-side gradients (head dim 64, bf16; after
-// xl_attn_bwd_dq, which leaves D_i = dO_i . O_i per query row): one CTA per
-// (head*batch, 128-key tile), over the query tiles that see the tile
+// xl_attn_bwd_dq, which leaves D_i = dO_i . O_i per query row).  Work item =
+// (head*batch, 128-key tile); per query tile that sees the key tile
 //     dP   = dO_q V^T            TMEM cols 0..255 (two buffers), lanes = queries
 //     dS   = P (dP - D) scale    bwd_dq's dAC arithmetic, bf16 into a swizzled [128 x 128] tile
-//     dV  += P_q^T dO_q          TMEM cols 256..319, lanes = keys (A = the TMA'd P tile, MN-major)
-//     dK  += dS_q^T Qu_q         TMEM cols 320..383            (A = the dS tile, MN-major)
+//     dV  += P_q^T dO_q          lanes = keys (A = the TMA'd P tile, MN-major)
+//     dK  += dS_q^T Qu_q                      (A = the dS tile, MN-major)
+// with dV / dK double-buffered per item (TMEM cols 256 + 128 b: dV, +64: dK).
+// Persistent: one CTA per SM walks the items (memory-side key tiles, which
+// every query tile sees, first) and the pipelines run on across item
+// boundaries -- an item has only 1..4 query tiles.  P is the one DRAM stream
+// (dO, q+u and v tiles are re-read across key tiles from L2): it has its own
+// producer thread and kKvP stages against the ~3 us load latency of a
+// saturated memory system; dO / q+u are double-buffered (a single dO buffer
+// chains each step's dP behind the previous step's dV and a load).
+// Sixteen softmax warps (four per TMEM lane quarter, 32 key columns each):
+// with eight the dS arithmetic of a step ran at ~1/3 issue efficiency, every
+// warp waiting on its own TMEM loads and dependent chains.
 // This is the K = 16 MMA sequence of the banded dV / dK GEMMs over P and dAC
 // (the same operands in the same order), so the result is bitwise theirs --
 // without the dAC matrix (185 MB written and read per block at C3) or the
 // GEMMs' second read of P.
-constexpr int kKvSmem = 1024 + 16384 /*V*/ + 2 * 16384 /*dO*/ + 2 * 16384 /*Qu*/ + 2 * kChunkBytes /*P*/ +
-                        kChunkBytes /*dS*/ + 256 /*barriers*/;
+constexpr int kKvP = 3;
+constexpr int kKvSoft = 16;                       // softmax warps
+constexpr int kKvThreads = 128 + 32 * kKvSoft;    // + TMA (P), MMA, TMEM, TMA (dO / q+u / v)
+// NP P stages, NDS dS tiles (shared memory: 96 KB of v / dO / q+u tiles + 32 KB per P stage or dS
+// tile).  Measured at C3 (tools/prof_xl_fused.py): 3 P stages + 1 dS tile and 2 + 2 run alike
+// (78 us); so do P from L2 instead of DRAM, no dV / dK MMAs, or no dS arithmetic (71-77 us) --
+// the kernel is bound by the per-step handoff latency between its roles, not by one resource.
+template <int NP, int NDS>
+constexpr int kv_smem() {
+  return 1024 + 2 * 16384 /*V*/ + 2 * 16384 /*dO*/ + 2 * 16384 /*Qu*/ + NP * kChunkBytes /*P*/ +
+         NDS * kChunkBytes /*dS*/ + 512 /*barriers*/;
+}
 
 struct KvParams {
   const float* D;     // [HB*T]
   __nv_bfloat16* gk;  // [HB, Kl, 64]
   __nv_bfloat16* gv;
-  int T, M, Kl, lo, nkt;
+  int T, M, Kl, lo, nkt, HB;
   float scale;
+  unsigned long long* trace;  // RP_XL_KV_TRACE: CTA 0's event times (diagnostics)
 };
 
-__global__ void __launch_bounds__(kThreadsBwd, 1)
+__device__ __forceinline__ void kv_trace(const KvParams& p, int ev, int idx) {
+  if (p.trace && blockIdx.x == 0 && idx < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[ev * 64 + idx] = t;
+  }
+}
+
+// item -> (key tile, head*batch, first query tile, query tiles)
+__device__ __forceinline__ void kv_item(const KvParams& p, int it, int& kt, int& hb, int& qt_lo, int& nq) {
+  kt = it / p.HB;
+  hb = it - kt * p.HB;
+  // query i sees key j <= M + i: the first query tile with a query at or past j0 - M
+  qt_lo = max(kt * kKT - p.M, 0) / kQT;
+  nq = p.T / kQT - qt_lo;
+}
+
+template <int NP, int NDS>
+__global__ void __launch_bounds__(kKvThreads, 1)
     xl_attn_bwd_kv_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
                           const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mP,
                           const KvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sV = smem;
-  uint8_t* sG = sV + 16384;      // [2]
+  uint8_t* sV = smem;            // [2] per item
+  uint8_t* sG = sV + 2 * 16384;  // [2] per step
   uint8_t* sU = sG + 2 * 16384;  // [2]
-  uint8_t* sP = sU + 2 * 16384;  // [2] x two 64-key atoms
-  uint8_t* sA = sP + 2 * kChunkBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kChunkBytes);
-  uint64_t* v_full = bars;
-  uint64_t* g_full = bars + 1;      // [2]
-  uint64_t* g_empty = bars + 3;     // [2]
-  uint64_t* u_full = bars + 5;      // [2]
-  uint64_t* u_empty = bars + 7;     // [2]
-  uint64_t* p_full = bars + 9;      // [2]
-  uint64_t* p_empty = bars + 11;    // [2]: the softmax warps' reads + the dV MMA
-  uint64_t* acc_full = bars + 13;   // [2]
-  uint64_t* acc_empty = bars + 15;  // [2]
-  uint64_t* ds_ready = bars + 17;
-  uint64_t* a_free = bars + 18;
-  uint64_t* done = bars + 19;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint8_t* sP = sU + 2 * 16384;  // [NP] x two 64-key atoms
+  uint8_t* sA = sP + NP * kChunkBytes;  // [NDS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + NDS * kChunkBytes);
+  uint64_t* v_full = bars;          // [2]
+  uint64_t* v_empty = bars + 2;     // [2]
+  uint64_t* g_full = bars + 4;      // [2]
+  uint64_t* g_empty = bars + 6;     // [2]
+  uint64_t* u_full = bars + 8;      // [2]
+  uint64_t* u_empty = bars + 10;    // [2]
+  uint64_t* acc_full = bars + 12;   // [2]
+  uint64_t* acc_empty = bars + 14;  // [2]
+  uint64_t* kv_full = bars + 16;    // [2]: an item's dV / dK complete
+  uint64_t* kv_empty = bars + 18;   // [2]: and read out
+  uint64_t* ds_ready = bars + 20;         // [NDS]
+  uint64_t* a_free = bars + 20 + NDS;     // [NDS]
+  uint64_t* p_full = bars + 20 + 2 * NDS;  // [NP]
+  uint64_t* p_empty = p_full + NP;        // [NP]: the softmax warps' reads + the dV MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NP);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // key tile major: the memory-side tiles, seen by every query tile, first
-  const int HB = (int)gridDim.x / p.nkt;
-  const int kt = (int)blockIdx.x / HB, hb = (int)blockIdx.x % HB;
-  const int j0 = kt * kKT;
-  // query i sees key j <= M + i: the first query tile with a query at or past j0 - M
-  const int qt_lo = max(j0 - p.M, 0) / kQT;
-  const int nq = p.T / kQT - qt_lo;
+  const int n_items = p.HB * p.nkt;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mG);
@@ -1451,20 +1488,26 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     tma_prefetch(&mP);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(v_full, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kKvSoft * 32);
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], kKvSoft * 32);
       mbar_init(&g_full[s], 1);
       mbar_init(&g_empty[s], 1);
       mbar_init(&u_full[s], 1);
       mbar_init(&u_empty[s], 1);
-      mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], kSoftWarps * 32 + 1);
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], kSoftWarps * 32);
     }
-    mbar_init(ds_ready, 1);
-    mbar_init(a_free, 1);
-    mbar_init(done, 1);
+    for (int s = 0; s < NP; ++s) {
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], kKvSoft * 32 + 1);
+    }
+    for (int s = 0; s < NDS; ++s) {
+      mbar_init(&ds_ready[s], kKvSoft * 32);  // every softmax thread, after its own proxy fence
+      mbar_init(&a_free[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -1472,27 +1515,49 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t t_dv = tmem_base + 256, t_dk = tmem_base + 320;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      mbar_expect_tx(v_full, 16384);
-      tma_load_3d(sV, &mV, v_full, 0, j0, hb);
-      for (int n = 0; n < nq; ++n) {
-        const int s = n & 1;
-        const uint32_t ph = ((n >> 1) & 1) ^ 1;
-        const int i0 = (qt_lo + n) * kQT;
-        mbar_wait(&g_empty[s], ph);
-        mbar_expect_tx(&g_full[s], 16384);
-        tma_load_3d(sG + s * 16384, &mG, &g_full[s], 0, i0, hb);
-        mbar_wait(&p_empty[s], ph);
-        mbar_expect_tx(&p_full[s], kChunkBytes);
-        tma_load_3d(sP + s * kChunkBytes, &mP, &p_full[s], j0, i0, hb);
-        tma_load_3d(sP + s * kChunkBytes + 128 * 128, &mP, &p_full[s], j0 + 64, i0, hb);
-        mbar_wait(&u_empty[s], ph);
-        mbar_expect_tx(&u_full[s], 16384);
-        tma_load_3d(sU + s * 16384, &mU, &u_full[s], 0, i0, hb);
+      // ---------------- TMA producer: the P stream ----------------
+      int gs = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int kt, hb, qt_lo, nq;
+        kv_item(p, it, kt, hb, qt_lo, nq);
+        const int j0 = kt * kKT;
+        for (int n = 0; n < nq; ++n, ++gs) {
+          const int ps = gs % NP;
+          mbar_wait(&p_empty[ps], ((gs / NP) & 1) ^ 1);
+          kv_trace(p, 1, gs);
+          mbar_expect_tx(&p_full[ps], kChunkBytes);
+          const int i0 = (qt_lo + n) * kQT;
+          tma_load_3d(sP + ps * kChunkBytes, &mP, &p_full[ps], j0, i0, hb);
+          tma_load_3d(sP + ps * kChunkBytes + 128 * 128, &mP, &p_full[ps], j0 + 64, i0, hb);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ---------------- TMA producer: v per item, dO / q+u per step (L2-resident) ----------------
+      int gs = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        int kt, hb, qt_lo, nq;
+        kv_item(p, it, kt, hb, qt_lo, nq);
+        const int vb = li & 1;
+        mbar_wait(&v_empty[vb], ((li >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[vb], 16384);
+        tma_load_3d(sV + vb * 16384, &mV, &v_full[vb], 0, kt * kKT, hb);
+        for (int n = 0; n < nq; ++n, ++gs) {
+          const int i0 = (qt_lo + n) * kQT, s = gs & 1;
+          const uint32_t ph = ((gs >> 1) & 1) ^ 1;
+          mbar_wait(&g_empty[s], ph);
+          kv_trace(p, 0, gs);
+          mbar_expect_tx(&g_full[s], 16384);
+          tma_load_3d(sG + s * 16384, &mG, &g_full[s], 0, i0, hb);
+          mbar_wait(&u_empty[s], ph);
+          kv_trace(p, 2, gs);
+          mbar_expect_tx(&u_full[s], 16384);
+          tma_load_3d(sU + s * 16384, &mU, &u_full[s], 0, i0, hb);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1500,134 +1565,168 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       // ---------------- MMA issuer ----------------
       const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
       const uint32_t id_kv = umma_idesc(false, true, true, kKT, 64);
-      const uint32_t vb = smem_u32(sV), aa = smem_u32(sA);
-      mbar_wait(v_full, 0);
-      auto issue_dk = [&](int m) {
-        const int s = m & 1;
-        mbar_wait(ds_ready, m & 1);
-        mbar_wait(&u_full[s], (m >> 1) & 1);
+      // per step: dP(n), dV(n) (frees the dO tile for step n + 1), then dK(n - 1),
+      // which waits for that step's dS; an item's last dK goes out as soon as
+      // its dS is ready (the item's dV / dK read-out waits on it)
+      int pend_gs = -1, pend_kb = 0, pend_first = 0, pend_last = 0;
+      auto issue_dk = [&]() {
+        const int ds = pend_gs % NDS;
+        const uint32_t aa = smem_u32(sA + ds * kChunkBytes);
+        mbar_wait(&ds_ready[ds], (pend_gs / NDS) & 1);
+        kv_trace(p, 3, pend_gs);
+        const int us = pend_gs & 1;
+        mbar_wait(&u_full[us], (pend_gs >> 1) & 1);
+        kv_trace(p, 4, pend_gs);
         tc_fence_after();
-        const uint32_t ua = smem_u32(sU + s * 16384);
+        const uint32_t ua = smem_u32(sU + us * 16384);
+        const uint32_t t_dk = tmem_base + 256 + 128 * pend_kb + 64;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           tc_mma<false>(t_dk, umma_desc(aa + k * 2048, 16384, 1024), umma_desc(ua + k * 2048, 16384, 1024), id_kv,
-                        (m | k) != 0);
-        tc_commit(a_free);
-        tc_commit(&u_empty[s]);
+                        (pend_first == 0 || k != 0) ? 1u : 0u);
+        tc_commit(&a_free[ds]);
+        tc_commit(&u_empty[us]);
+        if (pend_last) tc_commit(&kv_full[pend_kb]);
+        pend_gs = -1;
       };
-      for (int n = 0; n < nq; ++n) {
-        const int s = n & 1;
-        const uint32_t ph = (n >> 1) & 1;
-        mbar_wait(&acc_empty[s], ph ^ 1);
-        mbar_wait(&g_full[s], ph);
-        tc_fence_after();
-        const uint32_t ga = smem_u32(sG + s * 16384);
+      int gs = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        int kt, hb, qt_lo, nq;
+        kv_item(p, it, kt, hb, qt_lo, nq);
+        const int kb = li & 1;
+        const uint32_t t_dv = tmem_base + 256 + 128 * kb;
+        const uint32_t vaddr = smem_u32(sV + kb * 16384);
+        mbar_wait(&v_full[kb], (li >> 1) & 1);
+        mbar_wait(&kv_empty[kb], ((li >> 1) & 1) ^ 1);  // item li - 2's dV / dK read out
+        for (int n = 0; n < nq; ++n, ++gs) {
+          const int s = gs & 1;
+          mbar_wait(&acc_empty[s], ((gs >> 1) & 1) ^ 1);
+          kv_trace(p, 5, gs);
+          mbar_wait(&g_full[s], (gs >> 1) & 1);
+          kv_trace(p, 6, gs);
+          tc_fence_after();
+          const uint32_t ga = smem_u32(sG + s * 16384);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vb, kKT, k), id_dp, k > 0);
-        tc_commit(&acc_full[s]);
-        mbar_wait(&p_full[s], ph);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(sP + s * kChunkBytes);
+          for (int k = 0; k < 4; ++k)
+            tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vaddr, kKT, k), id_dp, k > 0);
+          tc_commit(&acc_full[s]);
+          if (n == nq - 1) tc_commit(&v_empty[kb]);
+          const int ps = gs % NP;
+          mbar_wait(&p_full[ps], (gs / NP) & 1);
+          kv_trace(p, 7, gs);
+          tc_fence_after();
+          const uint32_t pa = smem_u32(sP + ps * kChunkBytes);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc_mma<false>(t_dv, umma_desc(pa + k * 2048, 16384, 1024), umma_desc(ga + k * 2048, 16384, 1024), id_kv,
-                        (n | k) != 0);
-        tc_commit(&p_empty[s]);
-        tc_commit(&g_empty[s]);
-        if (n >= 1) issue_dk(n - 1);
+          for (int k = 0; k < 8; ++k)
+            tc_mma<false>(t_dv, umma_desc(pa + k * 2048, 16384, 1024), umma_desc(ga + k * 2048, 16384, 1024), id_kv,
+                          (n | k) != 0);
+          tc_commit(&p_empty[ps]);
+          tc_commit(&g_empty[s]);
+          if (pend_gs >= 0) issue_dk();
+          pend_gs = gs;
+          pend_kb = kb;
+          pend_first = n == 0;
+          pend_last = n == nq - 1;
+        }
+        issue_dk();
       }
-      issue_dk(nq - 1);
-      tc_commit(done);
     }
   } else if (warp >= 4) {
-    const int q = warp & 3, half = (warp - 4) >> 2;
+    // lane quarter q (TMEM lanes 32q..: query rows, then key rows), key columns [32 part, +32)
+    const int q = warp & 3, part = (warp - 4) >> 2;
     const int r = 32 * q + lane;
     const int rsw = r & 7;
+    const int atom = part >> 1, cb = (part & 1) * 4;  // 64-key swizzle atom and 16-byte chunk base
     const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
-    float D = p.D[(int64_t)hb * p.T + qt_lo * kQT + r];
-    for (int n = 0; n < nq; ++n) {
-      const int s = n & 1;
-      const uint32_t ph = (n >> 1) & 1;
-      const int i = (qt_lo + n) * kQT + r;
-      const int jhi = p.M + i;
-      const float Dn = (n + 1 < nq) ? p.D[(int64_t)hb * p.T + i + kQT] : 0.f;  // the next tile's, in flight
-      uint4 pr[2][4];
-      mbar_wait(&p_full[s], ph);
-      {
-        const uint8_t* prow_s = sP + s * kChunkBytes + half * (128 * 128) + r * 128;
+    int gs = 0, li = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+      int kt, hb, qt_lo, nq;
+      kv_item(p, it, kt, hb, qt_lo, nq);
+      const int j0 = kt * kKT, kb = li & 1;
+      for (int n = 0; n < nq; ++n, ++gs) {
+        const int s = gs & 1, ps = gs % NP, ds = gs % NDS;
+        const int i = (qt_lo + n) * kQT + r;
+        const int jhi = p.M + i;
+        const float D = p.D[(int64_t)hb * p.T + i];
+        uint4 pr[4];
+        mbar_wait(&p_full[ps], (gs / NP) & 1);
+        if (r == 0 && part == 0) kv_trace(p, 8, gs);
+        {
+          const uint8_t* prow_s = sP + ps * kChunkBytes + atom * (128 * 128) + r * 128;
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            pr[k][c] = *reinterpret_cast<const uint4*>(prow_s + (((4 * k + c) ^ rsw) << 4));
-      }
-      mbar_arrive(&p_empty[s]);
-      mbar_wait(&acc_full[s], ph);
-      tc_fence_after();
-      uint32_t dp[2][32];
-      tmem_ld32(tl + s * kKT + 64 * half, dp[0]);
-      tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
-      tc_fence_before();
-      mbar_arrive(&acc_empty[s]);
-      if (n >= 1) mbar_wait(a_free, (n - 1) & 1);  // the previous tile's dK MMA has read the dS tile
-      uint8_t* arow_s = sA + half * (128 * 128) + r * 128;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int jb = j0 + 64 * half + 32 * k;
-        const bool inside = jb >= p.lo && jb + 31 <= jhi;
+          for (int c = 0; c < 4; ++c) pr[c] = *reinterpret_cast<const uint4*>(prow_s + (((cb + c) ^ rsw) << 4));
+        }
+        mbar_arrive(&p_empty[ps]);
+        mbar_wait(&acc_full[s], (gs >> 1) & 1);
+        if (r == 0 && part == 0) kv_trace(p, 9, gs);
+        tc_fence_after();
+        uint32_t dp[32];
+        tmem_ld32(tl + s * kKT + 32 * part, dp);
+        tc_fence_before();
+        mbar_arrive(&acc_empty[s]);
         uint32_t o[16];
+        {
+          const int jb = j0 + 32 * part;
+          const bool inside = jb >= p.lo && jb + 31 <= jhi;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t w[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t w[4] = {pr[c].x, pr[c].y, pr[c].z, pr[c].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-            const int t = 8 * c + 2 * e;
-            const int j = jb + t;
-            float a0 = pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale;
-            float a1 = pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale;
-            if (!inside) {
-              a0 = (j >= p.lo && j <= jhi) ? a0 : 0.f;
-              a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? a1 : 0.f;
+            for (int e = 0; e < 4; ++e) {
+              const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+              const int t = 8 * c + 2 * e;
+              const int j = jb + t;
+              float a0 = pf.x * (__uint_as_float(dp[t]) - D) * p.scale;
+              float a1 = pf.y * (__uint_as_float(dp[t + 1]) - D) * p.scale;
+              if (!inside) {
+                a0 = (j >= p.lo && j <= jhi) ? a0 : 0.f;
+                a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? a1 : 0.f;
+              }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+              o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
             }
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
-            o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
           }
         }
+        // the dS tile is free once the dK MMA NDS steps back has read it
+        if (gs >= NDS) mbar_wait(&a_free[ds], ((gs / NDS) & 1) ^ 1);
+        if (r == 0 && part == 0) kv_trace(p, 10, gs);
+        {
+          uint8_t* arow_s = sA + ds * kChunkBytes + atom * (128 * 128) + r * 128;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          *reinterpret_cast<uint4*>(arow_s + (((4 * k + c) ^ rsw) << 4)) =
-              make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(arow_s + (((cb + c) ^ rsw) << 4)) =
+                make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&ds_ready[ds]);
+        if (r == 0 && part == 0) kv_trace(p, 11, gs);
       }
-      D = Dn;
-      fence_proxy_async_smem();
-      named_sync(1, kSoftWarps * 32);
-      if (warp == 4 && lane == 0) mbar_arrive(ds_ready);
-    }
-    // ---- dV / dK epilogue: key rows of this lane quarter, columns [32 half, +32)
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int j = j0 + r;
-    const int64_t orow = ((int64_t)hb * p.Kl + j) * 64 + 32 * half;
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
+      // ---- this item's dV (parts 0, 1) / dK (parts 2, 3): key rows of this lane quarter
+      if (r == 0 && part == 0) kv_trace(p, 12, li);
+      mbar_wait(&kv_full[kb], (li >> 1) & 1);
+      if (r == 0 && part == 0) kv_trace(p, 13, li);
+      tc_fence_after();
+      const int j = j0 + r;
       uint32_t v[32];
-      tmem_ld32(tl + 256 + 64 * w + 32 * half, v);
+      tmem_ld32(tl + 256 + 128 * kb + 32 * part, v);
+      tc_fence_before();
+      mbar_arrive(&kv_empty[kb]);
       if (j < p.Kl) {
-        uint4* dst = reinterpret_cast<uint4*>((w == 0 ? p.gv : p.gk) + orow);
+        uint4* dst =
+            reinterpret_cast<uint4*>((part < 2 ? p.gv : p.gk) + ((int64_t)hb * p.Kl + j) * 64 + 32 * (part & 1));
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t o[4];
+          uint32_t ob[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             __nv_bfloat162 b2 =
                 __floats2bfloat162_rn(__uint_as_float(v[8 * c + 2 * e]), __uint_as_float(v[8 * c + 2 * e + 1]));
-            o[e] = *reinterpret_cast<uint32_t*>(&b2);
+            ob[e] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+          dst[c] = make_uint4(ob[0], ob[1], ob[2], ob[3]);
         }
       }
+      if (r == 0 && part == 0) kv_trace(p, 14, li);
     }
   }
   tc_fence_before();
@@ -1834,7 +1933,8 @@ int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const voi
   RP_TRY0(tma_map_bf16(&mu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
   static uint64_t attr_done = 0;
   if (first_on_device(attr_done))
-    cudaFuncSetAttribute(xl_attn_bwd_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem);
+    cudaFuncSetAttribute(xl_attn_bwd_kv_kernel<kKvP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kv_smem<kKvP, 1>());
   KvParams p{};
   p.D = d_rows;
   p.gk = static_cast<__nv_bfloat16*>(gk);
@@ -1844,10 +1944,45 @@ int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const voi
   p.Kl = (int)Kl;
   p.lo = (int)(M - mem_len);
   p.nkt = (int)((Kl + kKT - 1) / kKT);
+  p.HB = (int)HB;
   p.scale = scale;
-  const int64_t grid = HB * p.nkt;
-  if (grid <= 0) return RP_OK;
-  xl_attn_bwd_kv_kernel<<<(unsigned)grid, kThreadsBwd, kKvSmem, st>>>(mg, mv, mu, mp, p);
+  const int64_t items = HB * p.nkt;
+  if (items <= 0) return RP_OK;
+  if (items >= (1LL << 31)) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: too many key tiles");
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sms[dev & 63] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev & 63] = v > 0 ? v : 148;
+  }
+  int64_t grid = std::min<int64_t>(items, sms[dev & 63]);  // persistent: one CTA per SM
+  if (const char* e = getenv("RP_XL_KV_CTAS"))  // tests: fewer CTAs, several items each
+    if (atoi(e) > 0) grid = std::min<int64_t>(grid, atoi(e));
+  static unsigned long long* trace = nullptr;
+  const bool tr = getenv("RP_XL_KV_TRACE") != nullptr;
+  if (tr) {
+    if (!trace) cudaMalloc(&trace, 15 * 64 * 8);
+    cudaMemsetAsync(trace, 0, 15 * 64 * 8, st);
+    p.trace = trace;
+  }
+  xl_attn_bwd_kv_kernel<kKvP, 1><<<(unsigned)grid, kKvThreads, kv_smem<kKvP, 1>(), st>>>(mg, mv, mu, mp, p);
+  if (tr) {
+    unsigned long long h[15 * 64];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < 15 * 64; ++i)
+      if (h[i] && h[i] < t0) t0 = h[i];
+    static const char* names[15] = {"P:G", "P:P", "P:U", "M:dsrdy", "M:ufull", "M:accE", "M:gfull", "M:pfull",
+                                    "S:pfull", "S:acc", "S:afree", "S:ds", "S:epiW", "S:epiGo", "S:epiDone"};
+    for (int ev = 0; ev < 15; ++ev) {
+      fprintf(stderr, "%-9s", names[ev]);
+      for (int i = 0; i < 40; ++i) fprintf(stderr, " %6.2f", h[ev * 64 + i] ? (h[ev * 64 + i] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   return check_launch("xl_attn_bwd_kv");
 }
 

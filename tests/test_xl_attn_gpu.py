@@ -333,14 +333,20 @@ def test_fused_pv_forward_equals_fused_forward_plus_gemm(B, H, T, M, mem_len):
     assert rel(ctx.float().cpu(), want.cpu()) <= 4e-3
 
 
+@pytest.mark.parametrize("ctas", [0, 3])
 @pytest.mark.parametrize("B,H,T,M,mem_len", [(2, 2, 128, 128, 128), (1, 2, 256, 256, 100), (2, 1, 128, 0, 0),
                                              (1, 3, 384, 128, 60), (2, 8, 512, 512, 512), (1, 2, 256, 200, 150)])
-def test_fused_kv_backward_equals_banded_gemms(B, H, T, M, mem_len):
+def test_fused_kv_backward_equals_banded_gemms(B, H, T, M, mem_len, ctas, monkeypatch):
     """xl_attn_bwd_kv: dV = P^T dO and dK = dS^T (q+u), key-major with dS
     recomputed from P, dP and xl_attn_bwd_dq's D rows, bitwise equal to the
     banded dV / dK GEMMs over P and dAC (the same K = 16 MMA sequence); and
-    xl_attn_bwd_dq without dAC leaves dBD / dQu / dQv bitwise unchanged."""
+    xl_attn_bwd_dq without dAC leaves dBD / dQu / dQv bitwise unchanged.
+    ctas = 3: the persistent kernel on 3 CTAs, each walking many (key tile,
+    head*batch) items with its pipelines running across item boundaries."""
     from paper_1909_06695_b200 import ops
+
+    if ctas:
+        monkeypatch.setenv("RP_XL_KV_CTAS", str(ctas))
 
     dev, dh = "cuda", 64
     g = torch.Generator(device=dev).manual_seed(7 * T + M + mem_len)
