@@ -1392,36 +1392,35 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 // xl_attn_bwd_dq, which leaves D_i = dO_i . O_i per query row).  Work item =
 // (head*batch, 128-key tile); per query tile that sees the key tile
 //     dP   = dO_q V^T            TMEM cols 0..255 (two buffers), lanes = queries
-//     dS   = P (dP - D) scale    bwd_dq's dAC arithmetic, bf16 into a swizzled [128 x 128] tile
+//     dS   = P (dP - D) scale    bwd_dq's dAC arithmetic, bf16, written over the P tile
 //     dV  += P_q^T dO_q          lanes = keys (A = the TMA'd P tile, MN-major)
-//     dK  += dS_q^T Qu_q                      (A = the dS tile, MN-major)
+//     dK  += dS_q^T Qu_q                      (A = the same tile, now dS, MN-major)
 // with dV / dK double-buffered per item (TMEM cols 256 + 128 b: dV, +64: dK).
 // Persistent: one CTA per SM walks the items (memory-side key tiles, which
 // every query tile sees, first) and the pipelines run on across item
 // boundaries -- an item has only 1..4 query tiles.  P is the one DRAM stream
 // (dO, q+u and v tiles are re-read across key tiles from L2): it has its own
-// producer thread and kKvP stages against the ~3 us load latency of a
-// saturated memory system; dO / q+u are double-buffered (a single dO buffer
-// chains each step's dP behind the previous step's dV and a load).
-// Sixteen softmax warps (four per TMEM lane quarter, 32 key columns each):
-// with eight the dS arithmetic of a step ran at ~1/3 issue efficiency, every
-// warp waiting on its own TMEM loads and dependent chains.
+// producer thread and kKvP stages.  Each thread overwrites exactly the P
+// values it read with its dS (same rows, same columns), once the dV MMA of
+// the step has read the tile -- so dS needs no buffer of its own and has as
+// many as P (a separate single dS tile chained every step's dS stores behind
+// the previous step's dK).  dP / dV and dK have separate issuing threads, so
+// neither waits on the other's operands.  Sixteen softmax warps, four per TMEM
+// lane quarter, 32 key columns each.
+// Measured at C3 (tools/prof_xl_fused.py, RP_XL_KV_TRACE event timelines):
+// ~76 us, ~1.2 us per step, bound by the P stream -- a 32 KB tile lands
+// ~5.7 us after its TMA issue (~3.2 TB/s of 256-byte row segments), and the
+// shared memory holds four stages.  The banded dV / dK GEMMs it replaces took
+// 37 us each, plus the dAC matrix (16 us of xl_attn_bwd_dq).
 // This is the K = 16 MMA sequence of the banded dV / dK GEMMs over P and dAC
 // (the same operands in the same order), so the result is bitwise theirs --
 // without the dAC matrix (185 MB written and read per block at C3) or the
 // GEMMs' second read of P.
-constexpr int kKvP = 3;
+constexpr int kKvP = 4;
 constexpr int kKvSoft = 16;                       // softmax warps
-constexpr int kKvThreads = 128 + 32 * kKvSoft;    // + TMA (P), MMA, TMEM, TMA (dO / q+u / v)
-// NP P stages, NDS dS tiles (shared memory: 96 KB of v / dO / q+u tiles + 32 KB per P stage or dS
-// tile).  Measured at C3 (tools/prof_xl_fused.py): 3 P stages + 1 dS tile and 2 + 2 run alike
-// (78 us); so do P from L2 instead of DRAM, no dV / dK MMAs, or no dS arithmetic (71-77 us) --
-// the kernel is bound by the per-step handoff latency between its roles, not by one resource.
-template <int NP, int NDS>
-constexpr int kv_smem() {
-  return 1024 + 2 * 16384 /*V*/ + 2 * 16384 /*dO*/ + 2 * 16384 /*Qu*/ + NP * kChunkBytes /*P*/ +
-         NDS * kChunkBytes /*dS*/ + 512 /*barriers*/;
-}
+constexpr int kKvThreads = 128 + 32 * kKvSoft;    // + TMA (P), MMA (dP, dV), TMEM + MMA (dK), TMA (dO / q+u / v)
+constexpr int kKvSmem = 1024 + 2 * 16384 /*V*/ + 2 * 16384 /*dO*/ + 2 * 16384 /*Qu*/ + kKvP * kChunkBytes /*P, dS*/ +
+                        512 /*barriers*/;
 
 struct KvParams {
   const float* D;     // [HB*T]
@@ -1449,19 +1448,18 @@ __device__ __forceinline__ void kv_item(const KvParams& p, int it, int& kt, int&
   nq = p.T / kQT - qt_lo;
 }
 
-template <int NP, int NDS>
 __global__ void __launch_bounds__(kKvThreads, 1)
     xl_attn_bwd_kv_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
                           const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mP,
                           const KvParams p) {
+  constexpr int NP = kKvP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sV = smem;            // [2] per item
   uint8_t* sG = sV + 2 * 16384;  // [2] per step
   uint8_t* sU = sG + 2 * 16384;  // [2]
-  uint8_t* sP = sU + 2 * 16384;  // [NP] x two 64-key atoms
-  uint8_t* sA = sP + NP * kChunkBytes;  // [NDS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + NDS * kChunkBytes);
+  uint8_t* sP = sU + 2 * 16384;  // [NP] x two 64-key atoms: P, then dS
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + NP * kChunkBytes);
   uint64_t* v_full = bars;          // [2]
   uint64_t* v_empty = bars + 2;     // [2]
   uint64_t* g_full = bars + 4;      // [2]
@@ -1472,10 +1470,10 @@ __global__ void __launch_bounds__(kKvThreads, 1)
   uint64_t* acc_empty = bars + 14;  // [2]
   uint64_t* kv_full = bars + 16;    // [2]: an item's dV / dK complete
   uint64_t* kv_empty = bars + 18;   // [2]: and read out
-  uint64_t* ds_ready = bars + 20;         // [NDS]
-  uint64_t* a_free = bars + 20 + NDS;     // [NDS]
-  uint64_t* p_full = bars + 20 + 2 * NDS;  // [NP]
-  uint64_t* p_empty = p_full + NP;        // [NP]: the softmax warps' reads + the dV MMA
+  uint64_t* p_full = bars + 20;     // [NP]: P landed
+  uint64_t* pv_done = p_full + NP;  // [NP]: the dV MMA has read P (dS may overwrite it)
+  uint64_t* ds_ready = pv_done + NP;  // [NP]: dS written (every softmax thread)
+  uint64_t* p_empty = ds_ready + NP;  // [NP]: the dK MMA has read dS
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NP);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1491,22 +1489,20 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
-      mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], kKvSoft * 32);
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], kKvSoft * 32);
       mbar_init(&g_full[s], 1);
       mbar_init(&g_empty[s], 1);
       mbar_init(&u_full[s], 1);
       mbar_init(&u_empty[s], 1);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kKvSoft * 32);
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], kKvSoft * 32);
     }
     for (int s = 0; s < NP; ++s) {
       mbar_init(&p_full[s], 1);
-      mbar_init(&p_empty[s], kKvSoft * 32 + 1);
-    }
-    for (int s = 0; s < NDS; ++s) {
+      mbar_init(&pv_done[s], 1);
       mbar_init(&ds_ready[s], kKvSoft * 32);  // every softmax thread, after its own proxy fence
-      mbar_init(&a_free[s], 1);
+      mbar_init(&p_empty[s], 1);
     }
     fence_mbar_init();
   }
@@ -1562,33 +1558,9 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+      // ---------------- MMA issuer: dP and dV (need only the TMA'd tiles) ----------------
       const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
       const uint32_t id_kv = umma_idesc(false, true, true, kKT, 64);
-      // per step: dP(n), dV(n) (frees the dO tile for step n + 1), then dK(n - 1),
-      // which waits for that step's dS; an item's last dK goes out as soon as
-      // its dS is ready (the item's dV / dK read-out waits on it)
-      int pend_gs = -1, pend_kb = 0, pend_first = 0, pend_last = 0;
-      auto issue_dk = [&]() {
-        const int ds = pend_gs % NDS;
-        const uint32_t aa = smem_u32(sA + ds * kChunkBytes);
-        mbar_wait(&ds_ready[ds], (pend_gs / NDS) & 1);
-        kv_trace(p, 3, pend_gs);
-        const int us = pend_gs & 1;
-        mbar_wait(&u_full[us], (pend_gs >> 1) & 1);
-        kv_trace(p, 4, pend_gs);
-        tc_fence_after();
-        const uint32_t ua = smem_u32(sU + us * 16384);
-        const uint32_t t_dk = tmem_base + 256 + 128 * pend_kb + 64;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc_mma<false>(t_dk, umma_desc(aa + k * 2048, 16384, 1024), umma_desc(ua + k * 2048, 16384, 1024), id_kv,
-                        (pend_first == 0 || k != 0) ? 1u : 0u);
-        tc_commit(&a_free[ds]);
-        tc_commit(&u_empty[us]);
-        if (pend_last) tc_commit(&kv_full[pend_kb]);
-        pend_gs = -1;
-      };
       int gs = 0, li = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
         int kt, hb, qt_lo, nq;
@@ -1599,7 +1571,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         mbar_wait(&v_full[kb], (li >> 1) & 1);
         mbar_wait(&kv_empty[kb], ((li >> 1) & 1) ^ 1);  // item li - 2's dV / dK read out
         for (int n = 0; n < nq; ++n, ++gs) {
-          const int s = gs & 1;
+          const int s = gs & 1, ps = gs % NP;
           mbar_wait(&acc_empty[s], ((gs >> 1) & 1) ^ 1);
           kv_trace(p, 5, gs);
           mbar_wait(&g_full[s], (gs >> 1) & 1);
@@ -1611,7 +1583,6 @@ __global__ void __launch_bounds__(kKvThreads, 1)
             tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vaddr, kKT, k), id_dp, k > 0);
           tc_commit(&acc_full[s]);
           if (n == nq - 1) tc_commit(&v_empty[kb]);
-          const int ps = gs % NP;
           mbar_wait(&p_full[ps], (gs / NP) & 1);
           kv_trace(p, 7, gs);
           tc_fence_after();
@@ -1620,15 +1591,43 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           for (int k = 0; k < 8; ++k)
             tc_mma<false>(t_dv, umma_desc(pa + k * 2048, 16384, 1024), umma_desc(ga + k * 2048, 16384, 1024), id_kv,
                           (n | k) != 0);
-          tc_commit(&p_empty[ps]);
+          tc_commit(&pv_done[ps]);
           tc_commit(&g_empty[s]);
-          if (pend_gs >= 0) issue_dk();
-          pend_gs = gs;
-          pend_kb = kb;
-          pend_first = n == 0;
-          pend_last = n == nq - 1;
         }
-        issue_dk();
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ---------------- MMA issuer: dK (waits for each step's dS) ----------------
+      // A second issuing thread: with one, a step's dK queued behind the next
+      // step's P tile (dV) or the next dV behind this dK, and each step paid
+      // that wait.  dK of an item's last step completing implies the item's dV
+      // did (the softmax warps wrote that dS only after its dV), so its commit
+      // alone signals the item's dV / dK.
+      const uint32_t id_kv = umma_idesc(false, true, true, kKT, 64);
+      int gs = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        int kt, hb, qt_lo, nq;
+        kv_item(p, it, kt, hb, qt_lo, nq);
+        const int kb = li & 1;
+        const uint32_t t_dk = tmem_base + 256 + 128 * kb + 64;
+        mbar_wait(&kv_empty[kb], ((li >> 1) & 1) ^ 1);
+        for (int n = 0; n < nq; ++n, ++gs) {
+          const int ps = gs % NP, us = gs & 1;
+          mbar_wait(&ds_ready[ps], (gs / NP) & 1);
+          kv_trace(p, 3, gs);
+          mbar_wait(&u_full[us], (gs >> 1) & 1);
+          kv_trace(p, 4, gs);
+          tc_fence_after();
+          const uint32_t aa = smem_u32(sP + ps * kChunkBytes), ua = smem_u32(sU + us * 16384);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc_mma<false>(t_dk, umma_desc(aa + k * 2048, 16384, 1024), umma_desc(ua + k * 2048, 16384, 1024), id_kv,
+                          (n | k) != 0);
+          tc_commit(&p_empty[ps]);
+          tc_commit(&u_empty[us]);
+          if (n == nq - 1) tc_commit(&kv_full[kb]);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -1644,19 +1643,16 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       kv_item(p, it, kt, hb, qt_lo, nq);
       const int j0 = kt * kKT, kb = li & 1;
       for (int n = 0; n < nq; ++n, ++gs) {
-        const int s = gs & 1, ps = gs % NP, ds = gs % NDS;
+        const int s = gs & 1, ps = gs % NP;
         const int i = (qt_lo + n) * kQT + r;
         const int jhi = p.M + i;
         const float D = p.D[(int64_t)hb * p.T + i];
+        uint8_t* row_s = sP + ps * kChunkBytes + atom * (128 * 128) + r * 128;
         uint4 pr[4];
         mbar_wait(&p_full[ps], (gs / NP) & 1);
         if (r == 0 && part == 0) kv_trace(p, 8, gs);
-        {
-          const uint8_t* prow_s = sP + ps * kChunkBytes + atom * (128 * 128) + r * 128;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) pr[c] = *reinterpret_cast<const uint4*>(prow_s + (((cb + c) ^ rsw) << 4));
-        }
-        mbar_arrive(&p_empty[ps]);
+        for (int c = 0; c < 4; ++c) pr[c] = *reinterpret_cast<const uint4*>(row_s + (((cb + c) ^ rsw) << 4));
         mbar_wait(&acc_full[s], (gs >> 1) & 1);
         if (r == 0 && part == 0) kv_trace(p, 9, gs);
         tc_fence_after();
@@ -1687,19 +1683,17 @@ __global__ void __launch_bounds__(kKvThreads, 1)
             }
           }
         }
-        // the dS tile is free once the dK MMA NDS steps back has read it
-        if (gs >= NDS) mbar_wait(&a_free[ds], ((gs / NDS) & 1) ^ 1);
+        // dS over this thread's own P values, once the dV MMA has read the tile
+        mbar_wait(&pv_done[ps], (gs / NP) & 1);
         if (r == 0 && part == 0) kv_trace(p, 10, gs);
-        {
-          uint8_t* arow_s = sA + ds * kChunkBytes + atom * (128 * 128) + r * 128;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(arow_s + (((cb + c) ^ rsw) << 4)) =
-                make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-        }
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(row_s + (((cb + c) ^ rsw) << 4)) =
+              make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
         fence_proxy_async_smem();
-        mbar_arrive(&ds_ready[ds]);
+        mbar_arrive(&ds_ready[ps]);
         if (r == 0 && part == 0) kv_trace(p, 11, gs);
+        if (lane == 0) kv_trace(p, 15 + warp - 4, gs);  // every softmax warp's arrival
       }
       // ---- this item's dV (parts 0, 1) / dK (parts 2, 3): key rows of this lane quarter
       if (r == 0 && part == 0) kv_trace(p, 12, li);
@@ -1933,8 +1927,7 @@ int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const voi
   RP_TRY0(tma_map_bf16(&mu, qu, dh, Tn, dh, HB, Tn * dh, 64, kQT));
   static uint64_t attr_done = 0;
   if (first_on_device(attr_done))
-    cudaFuncSetAttribute(xl_attn_bwd_kv_kernel<kKvP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kv_smem<kKvP, 1>());
+    cudaFuncSetAttribute(xl_attn_bwd_kv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem);
   KvParams p{};
   p.D = d_rows;
   p.gk = static_cast<__nv_bfloat16*>(gk);
@@ -1963,22 +1956,22 @@ int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const voi
   static unsigned long long* trace = nullptr;
   const bool tr = getenv("RP_XL_KV_TRACE") != nullptr;
   if (tr) {
-    if (!trace) cudaMalloc(&trace, 15 * 64 * 8);
-    cudaMemsetAsync(trace, 0, 15 * 64 * 8, st);
+    if (!trace) cudaMalloc(&trace, 31 * 64 * 8);
+    cudaMemsetAsync(trace, 0, 31 * 64 * 8, st);
     p.trace = trace;
   }
-  xl_attn_bwd_kv_kernel<kKvP, 1><<<(unsigned)grid, kKvThreads, kv_smem<kKvP, 1>(), st>>>(mg, mv, mu, mp, p);
+  xl_attn_bwd_kv_kernel<<<(unsigned)grid, kKvThreads, kKvSmem, st>>>(mg, mv, mu, mp, p);
   if (tr) {
-    unsigned long long h[15 * 64];
+    unsigned long long h[31 * 64];
     cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     unsigned long long t0 = ~0ull;
-    for (int i = 0; i < 15 * 64; ++i)
+    for (int i = 0; i < 31 * 64; ++i)
       if (h[i] && h[i] < t0) t0 = h[i];
     static const char* names[15] = {"P:G", "P:P", "P:U", "M:dsrdy", "M:ufull", "M:accE", "M:gfull", "M:pfull",
                                     "S:pfull", "S:acc", "S:afree", "S:ds", "S:epiW", "S:epiGo", "S:epiDone"};
-    for (int ev = 0; ev < 15; ++ev) {
-      fprintf(stderr, "%-9s", names[ev]);
+    for (int ev = 0; ev < 31; ++ev) {
+      fprintf(stderr, "%-9s", ev < 15 ? names[ev] : "S:w");
       for (int i = 0; i < 40; ++i) fprintf(stderr, " %6.2f", h[ev * 64 + i] ? (h[ev * 64 + i] - t0) * 1e-3 : -1.0);
       fprintf(stderr, "\n");
     }
