@@ -1015,6 +1015,9 @@ struct DqParams {
                      // [rows, cols] block per bias that a column-sum finish reduces
   float* d_rows;     // optional [HB*T]: D_i = dO_i . O_i for xl_attn_bwd_kv
   int no_dac;        // dAC is not written (xl_attn_bwd_kv computes dK from dS itself)
+  unsigned long long* trace;  // RP_XL_DQ_TRACE: CTA 0's event times (diagnostics)
+  int zero_rows;              // margins zeroed by the softmax warps, a row per thread: with dAC (twice the
+                              // margins; two warps are then the tail), or RP_XL_DQ_ZERO_ROWS=1 (A/B)
 };
 
 // out[lane] = sum over the warp's 32 rows of column `lane` of v[0..31]
@@ -1031,6 +1034,14 @@ __device__ __forceinline__ float warp_colsum32(float (&a)[32], int lane) {
     }
   }
   return a[0];
+}
+
+__device__ __forceinline__ void dq_trace(unsigned long long* tr, int ev, int idx) {
+  if (tr && blockIdx.x == tr[11 * 32] && idx < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[ev * 32 + idx] = t;
+  }
 }
 
 __global__ void __launch_bounds__(kThreadsBwd, 1)
@@ -1052,19 +1063,24 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   uint64_t* g_full = bars;
   uint64_t* v_full = bars + 1;
   uint64_t* v_empty = bars + 2;
-  uint64_t* p_full = bars + 3;
-  uint64_t* p_empty = bars + 4;
+  uint64_t* p_full = bars + 17;   // [2]
+  uint64_t* p_empty = bars + 19;  // [2]: the dQu MMA has read the tile's dS (written over its P)
   uint64_t* acc_full = bars + 5;   // [2]
   uint64_t* acc_empty = bars + 7;  // [2]
   uint64_t* kr_full = bars + 9;
   uint64_t* kr_empty = bars + 10;
   uint64_t* ds_ready = bars + 11;
-  uint64_t* a_free = bars + 12;
   uint64_t* ring_free = bars + 13;  // [3]
   uint64_t* dq_full = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  // P tile n in buffer n & 1 (the former dS tile is the second buffer): each
+  // thread writes its dS over the P values it read, and the dQu MMA reads it
+  // there -- no dS tile, so a tile's dS stores no longer wait for the
+  // previous tile's dQu MMA
+  auto pbuf = [&](int n) -> uint8_t* { return (n & 1) ? sA : sP; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) dq_trace(dq.trace, 0, 0);
   int hb, qt;
   cta_tile(p.nqt, p.heavy_first, hb, qt);
   const int h = hb / p.B, b = hb % p.B;
@@ -1087,8 +1103,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     mbar_init(g_full, 1);
     mbar_init(v_full, 1);
     mbar_init(v_empty, 1);
-    mbar_init(p_full, 1);
-    mbar_init(p_empty, kSoftWarps * 32);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], kSoftWarps * 32);
@@ -1096,7 +1114,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     mbar_init(kr_full, 1);
     mbar_init(kr_empty, 1);
     mbar_init(ds_ready, 1);
-    mbar_init(a_free, 1);
     for (int c = 0; c < kRing3; ++c) mbar_init(&ring_free[c], 1);
     mbar_init(dq_full, 1);
     fence_mbar_init();
@@ -1118,10 +1135,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           mbar_wait(v_empty, (n & 1) ^ 1);
           mbar_expect_tx(v_full, 16384);
           tma_atoms<1>(sV, &mV, v_full, kKT, (jt_lo + n) * kKT, hb);
-          mbar_wait(p_empty, (n & 1) ^ 1);
-          mbar_expect_tx(p_full, kChunkBytes);
-          tma_load_3d(sP, &mP, p_full, (jt_lo + n) * kKT, i0, hb);
-          tma_load_3d(sP + 128 * 128, &mP, p_full, (jt_lo + n) * kKT + 64, i0, hb);
+          const int pb = n & 1;
+          mbar_wait(&p_empty[pb], ((n >> 1) & 1) ^ 1);
+          dq_trace(dq.trace, 1, n);
+          mbar_expect_tx(&p_full[pb], kChunkBytes);
+          tma_load_3d(pbuf(n), &mP, &p_full[pb], (jt_lo + n) * kKT, i0, hb);
+          tma_load_3d(pbuf(n) + 128 * 128, &mP, &p_full[pb], (jt_lo + n) * kKT + 64, i0, hb);
         }
         // K tile n (MN-major B of dQu) and relative-encoding rows of band chunk n
         // (MN-major B of dQv); after the last tile only the rows of chunk nt
@@ -1136,21 +1155,22 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       // ---------------- MMA issuer ----------------
       const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
       const uint32_t id_dq = umma_idesc(false, false, true, kQT, 64);
-      const uint32_t ga = smem_u32(sG), ka = smem_u32(sK), ra = smem_u32(sR), aa = smem_u32(sA);
+      const uint32_t ga = smem_u32(sG), ka = smem_u32(sK), ra = smem_u32(sR);
       const uint32_t rg = smem_u32(ring);
       mbar_wait(g_full, 0);
       auto issue_dq = [&](int n) {
         mbar_wait(ds_ready, n & 1);
+        dq_trace(dq.trace, 2, n);
         mbar_wait(kr_full, n & 1);
         tc_fence_after();
-        const uint32_t ch = rg + (uint32_t)((n % kRing3) * kChunkBytes);
+        const uint32_t ch = rg + (uint32_t)((n % kRing3) * kChunkBytes), aa = smem_u32(pbuf(n));
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           tc_mma<false>(t_dqu, atom_desc<1>(aa, kQT, k), umma_desc(ka + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
-        tc_commit(a_free);
+        tc_commit(&p_empty[n & 1]);
         tc_commit(&ring_free[n % kRing3]);
         tc_commit(kr_empty);
       };
@@ -1158,6 +1178,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const int s = n & 1;
         mbar_wait(&acc_empty[s], ((n >> 1) & 1) ^ 1);
         mbar_wait(v_full, n & 1);
+        dq_trace(dq.trace, 3, n);
         tc_fence_after();
         const uint32_t vb = smem_u32(sV);
 #pragma unroll
@@ -1206,16 +1227,17 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         }
       }
       if (dq.d_rows && half == 0) dq.d_rows[(int64_t)hb * p.T + i] = D;
-      // columns outside the key tiles this query tile sees: dAC = 0, and the
-      // dBD margins outside the stored band chunks
-      if (half == 0) {
-        if (!dq.no_dac) zero_row(arow, 0, (int64_t)jt_lo * kKT);
-        zero_row(brow, 0, lmin(lmax(P0, 0), p.ldp));
-      } else {
-        if (!dq.no_dac) zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
-        zero_row(brow, lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp), p.ldp);
+      if (dq.zero_rows) {
+        if (half == 0) {
+          if (!dq.no_dac) zero_row(arow, 0, (int64_t)jt_lo * kKT);
+          zero_row(brow, 0, lmin(lmax(P0, 0), p.ldp));
+        } else {
+          if (!dq.no_dac) zero_row(arow, lmin((int64_t)(jt_hi + 1) * kKT, p.ldp), p.ldp);
+          zero_row(brow, lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp), p.ldp);
+        }
       }
     }
+    if (r == 0 && half == 0) dq_trace(dq.trace, 4, 0);  // prologue (D, zero margins) done
     auto ring_at = [&](int bc) -> __nv_bfloat16* {  // band column bc of row r
       return reinterpret_cast<__nv_bfloat16*>(ring + (bc >> 7) % kRing3 * kChunkBytes + sw128_off(r, bc & 127));
     };
@@ -1233,16 +1255,17 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       const int jt0 = (jt_lo + n) * kKT + 64 * half;
       // this row's 64 P values of the tile from the swizzled smem tile (zero past ldp: TMA fill)
       uint4 pr[2][4];
-      mbar_wait(p_full, n & 1);
+      mbar_wait(&p_full[n & 1], (n >> 1) & 1);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 5, n);
+      uint8_t* const tile = pbuf(n);
       {
-        const uint8_t* prow_s = sP + half * (128 * 128) + r * 128;
+        const uint8_t* prow_s = tile + half * (128 * 128) + r * 128;
 #pragma unroll
         for (int k = 0; k < 2; ++k)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             pr[k][c] = *reinterpret_cast<const uint4*>(prow_s + (((4 * k + c) ^ (r & 7)) << 4));
       }
-      mbar_arrive(p_empty);
       mbar_wait(&acc_full[s], (n >> 1) & 1);
       tc_fence_after();
       uint32_t dp[2][32];
@@ -1250,16 +1273,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
       tc_fence_before();
       mbar_arrive(&acc_empty[s]);
-      // the dS tile is free once the previous tile's dQu MMA and this warp's
-      // dAC store from it are done; the upper band chunk of this tile is
-      // reused from tile n - 2, whose dQv MMA must be done (its TMA store was
-      // retired before barrier n - 1)
-      if (n >= 1) mbar_wait(a_free, (n - 1) & 1);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 6, n);
+      // dS goes over this thread's own P values (no wait); the upper band
+      // chunk of this tile is reused from tile n - 2, whose dQv MMA must be
+      // done (its TMA store was retired before barrier n - 1)
       if (n >= 2) mbar_wait(&ring_free[(n + 1) % kRing3], ((n - 2) / kRing3) & 1);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 7, n);
       if (lane == 0) tma_store_wait_read();
       __syncwarp();
       const int rsw = r & 7;
-      uint8_t* arow_s = sA + half * (128 * 128) + r * 128;
+      uint8_t* arow_s = tile + half * (128 * 128) + r * 128;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int jb = jt0 + 32 * k;
@@ -1321,12 +1344,19 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       fence_proxy_async_smem();
       __syncwarp();
       // this warp's 32 x 64 dAC block straight from the swizzled dS tile
-      if (!dq.no_dac && lane == 0 && jt0 < p.ldp) tma_store_3d(&mAC, sA + half * (128 * 128) + 32 * q * 128, jt0, i0 + 32 * q, hb);
+      if (!dq.no_dac && lane == 0 && jt0 < p.ldp) {
+        tma_store_3d(&mAC, tile + half * (128 * 128) + 32 * q * 128, jt0, i0 + 32 * q, hb);
+        // the tile is reloaded (P of tile n + 2) once the dQu MMA released it:
+        // this store must have read it before ds_ready
+        tma_store_wait_read();
+      }
       // earlier dBD chunk stores have read the ring (all but the newest bulk
       // group: this tile's dAC store, which nobody waits for here)
       if (warp == 4 && lane == 0) bulk_wait_read_1();
+      if (r == 0 && half == 0) dq_trace(dq.trace, 8, n);
       named_sync(1, kSoftWarps * 32);
       if (warp == 4 && lane == 0) {
+        dq_trace(dq.trace, 9, n);
         mbar_arrive(ds_ready);
         for (int m = n; m <= (n == nt - 1 ? n + 1 : n); ++m) {
           const uint8_t* ch = ring + (m % kRing3) * kChunkBytes;
@@ -1337,7 +1367,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
     }
     // ---- dQu / dQv epilogue: rows of this lane quarter, columns [32 half, +32)
+    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 0);
     mbar_wait(dq_full, 0);
+    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 1);
     tc_fence_after();
     uint32_t v[32];
     const int64_t orow = ((int64_t)hb * p.T + i) * 64 + 32 * half;
@@ -1382,9 +1414,30 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
     }
     if (lane == 0) tma_store_wait_all();
+  } else if (!dq.zero_rows) {
+    // warps 2 and 3 (otherwise idle): the columns outside the key tiles this
+    // query tile sees (dAC = 0) and the dBD margins outside the stored band
+    // chunks, as coalesced 16-byte stores (all bounds are multiples of 128
+    // columns: T % 128 == 0) -- in the softmax warps, one row per thread,
+    // these stores held the prologue up for several microseconds
+    const int64_t bl = lmin(lmax(P0, 0), p.ldp), br = lmin(lmax((int64_t)P0 + kKT * (nt + 1), 0), p.ldp);
+    const int64_t al = lmin((int64_t)jt_lo * kKT, p.ldp), ar = lmin((int64_t)(jt_hi + 1) * kKT, p.ldp);
+    auto zero = [&](__nv_bfloat16* row, int64_t a, int64_t e) {
+      for (int64_t c = a + 8 * lane; c < e; c += 256) *reinterpret_cast<uint4*>(row + c) = make_uint4(0u, 0u, 0u, 0u);
+    };
+    for (int rr = warp - 2; rr < kQT; rr += 2) {
+      const int64_t rowoff = ((int64_t)hb * p.T + i0 + rr) * p.ldp;
+      zero(p.gbd + rowoff, 0, bl);
+      zero(p.gbd + rowoff, br, p.ldp);
+      if (!dq.no_dac) {
+        zero(p.gac + rowoff, 0, al);
+        zero(p.gac + rowoff, ar, p.ldp);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) dq_trace(dq.trace, 10, 2);
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
@@ -1902,10 +1955,35 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   q.bias_part = bias_part;
   q.d_rows = d_rows;
   q.no_dac = gac == nullptr;
+  // C3 A/B: without dAC, warps 2-3 zeroing the dBD margins 182 -> 176 us; with dAC 202 -> 208 us
+  q.zero_rows = gac != nullptr;
+  if (const char* e = getenv("RP_XL_DQ_ZERO_ROWS")) q.zero_rows = atoi(e);
   if ((reinterpret_cast<uintptr_t>(d_rows) & 3) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned D rows");
   const int64_t grid = HB * p.nqt;
   if (grid <= 0) return RP_OK;
+  static unsigned long long* trace = nullptr;
+  const bool tr = getenv("RP_XL_DQ_TRACE") != nullptr;
+  if (tr) {
+    if (!trace) cudaMalloc(&trace, 12 * 32 * 8);
+    cudaMemsetAsync(trace, 0, 11 * 32 * 8, st);
+    const unsigned long long cta = (unsigned long long)atoi(getenv("RP_XL_DQ_TRACE"));
+    cudaMemcpyAsync(trace + 11 * 32, &cta, 8, cudaMemcpyHostToDevice, st);
+    q.trace = trace;
+  }
   xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);
+  if (tr) {
+    unsigned long long h[11 * 32];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const unsigned long long t0 = h[0];
+    static const char* names[11] = {"start", "P:P", "M:dsrdy", "M:vfull", "S:prolog", "S:pfull", "S:acc",
+                                    "S:ring", "S:stored", "S:ds", "S:epi"};
+    for (int ev = 0; ev < 11; ++ev) {
+      fprintf(stderr, "%-9s", names[ev]);
+      for (int i = 0; i < 12; ++i) fprintf(stderr, " %6.2f", h[ev * 32 + i] ? (h[ev * 32 + i] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   return check_launch("xl_attn_bwd_dq");
 }
 
