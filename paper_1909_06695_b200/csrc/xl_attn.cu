@@ -1015,7 +1015,8 @@ struct DqParams {
                      // [rows, cols] block per bias that a column-sum finish reduces
   float* d_rows;     // optional [HB*T]: D_i = dO_i . O_i for xl_attn_bwd_kv
   int no_dac;        // dAC is not written (xl_attn_bwd_kv computes dK from dS itself)
-  unsigned long long* trace;  // RP_XL_DQ_TRACE: CTA 0's event times (diagnostics)
+  unsigned long long* trace;  // RP_XL_DQ_TRACE=<cta>: that CTA's event times (diagnostics)
+  int trace_cta;
   int zero_rows;              // margins zeroed by the softmax warps, a row per thread: with dAC (twice the
                               // margins; two warps are then the tail), or RP_XL_DQ_ZERO_ROWS=1 (A/B)
 };
@@ -1036,8 +1037,10 @@ __device__ __forceinline__ float warp_colsum32(float (&a)[32], int lane) {
   return a[0];
 }
 
-__device__ __forceinline__ void dq_trace(unsigned long long* tr, int ev, int idx) {
-  if (tr && blockIdx.x == tr[11 * 32] && idx < 32) {
+// (the traced CTA comes as a kernel parameter: a global load in the probe
+// itself stalled the producer thread for microseconds and faked TMA stalls)
+__device__ __forceinline__ void dq_trace(unsigned long long* tr, int ev, int idx, int cta) {
+  if (tr && (int)blockIdx.x == cta && idx < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     tr[ev * 32 + idx] = t;
@@ -1080,7 +1083,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   auto pbuf = [&](int n) -> uint8_t* { return (n & 1) ? sA : sP; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) dq_trace(dq.trace, 0, 0);
+  if (threadIdx.x == 0) dq_trace(dq.trace, 0, 0, dq.trace_cta);
   int hb, qt;
   cta_tile(p.nqt, p.heavy_first, hb, qt);
   const int h = hb / p.B, b = hb % p.B;
@@ -1137,7 +1140,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           tma_atoms<1>(sV, &mV, v_full, kKT, (jt_lo + n) * kKT, hb);
           const int pb = n & 1;
           mbar_wait(&p_empty[pb], ((n >> 1) & 1) ^ 1);
-          dq_trace(dq.trace, 1, n);
+          dq_trace(dq.trace, 1, n, dq.trace_cta);
           mbar_expect_tx(&p_full[pb], kChunkBytes);
           tma_load_3d(pbuf(n), &mP, &p_full[pb], (jt_lo + n) * kKT, i0, hb);
           tma_load_3d(pbuf(n) + 128 * 128, &mP, &p_full[pb], (jt_lo + n) * kKT + 64, i0, hb);
@@ -1160,7 +1163,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       mbar_wait(g_full, 0);
       auto issue_dq = [&](int n) {
         mbar_wait(ds_ready, n & 1);
-        dq_trace(dq.trace, 2, n);
+        dq_trace(dq.trace, 2, n, dq.trace_cta);
         mbar_wait(kr_full, n & 1);
         tc_fence_after();
         const uint32_t ch = rg + (uint32_t)((n % kRing3) * kChunkBytes), aa = smem_u32(pbuf(n));
@@ -1178,7 +1181,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const int s = n & 1;
         mbar_wait(&acc_empty[s], ((n >> 1) & 1) ^ 1);
         mbar_wait(v_full, n & 1);
-        dq_trace(dq.trace, 3, n);
+        dq_trace(dq.trace, 3, n, dq.trace_cta);
         tc_fence_after();
         const uint32_t vb = smem_u32(sV);
 #pragma unroll
@@ -1237,7 +1240,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         }
       }
     }
-    if (r == 0 && half == 0) dq_trace(dq.trace, 4, 0);  // prologue (D, zero margins) done
+    if (r == 0 && half == 0) dq_trace(dq.trace, 4, 0, dq.trace_cta);  // prologue (D, zero margins) done
     auto ring_at = [&](int bc) -> __nv_bfloat16* {  // band column bc of row r
       return reinterpret_cast<__nv_bfloat16*>(ring + (bc >> 7) % kRing3 * kChunkBytes + sw128_off(r, bc & 127));
     };
@@ -1256,7 +1259,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       // this row's 64 P values of the tile from the swizzled smem tile (zero past ldp: TMA fill)
       uint4 pr[2][4];
       mbar_wait(&p_full[n & 1], (n >> 1) & 1);
-      if (r == 0 && half == 0) dq_trace(dq.trace, 5, n);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 5, n, dq.trace_cta);
       uint8_t* const tile = pbuf(n);
       {
         const uint8_t* prow_s = tile + half * (128 * 128) + r * 128;
@@ -1273,12 +1276,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
       tc_fence_before();
       mbar_arrive(&acc_empty[s]);
-      if (r == 0 && half == 0) dq_trace(dq.trace, 6, n);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 6, n, dq.trace_cta);
       // dS goes over this thread's own P values (no wait); the upper band
       // chunk of this tile is reused from tile n - 2, whose dQv MMA must be
       // done (its TMA store was retired before barrier n - 1)
       if (n >= 2) mbar_wait(&ring_free[(n + 1) % kRing3], ((n - 2) / kRing3) & 1);
-      if (r == 0 && half == 0) dq_trace(dq.trace, 7, n);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 7, n, dq.trace_cta);
       if (lane == 0) tma_store_wait_read();
       __syncwarp();
       const int rsw = r & 7;
@@ -1353,10 +1356,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       // earlier dBD chunk stores have read the ring (all but the newest bulk
       // group: this tile's dAC store, which nobody waits for here)
       if (warp == 4 && lane == 0) bulk_wait_read_1();
-      if (r == 0 && half == 0) dq_trace(dq.trace, 8, n);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 8, n, dq.trace_cta);
       named_sync(1, kSoftWarps * 32);
       if (warp == 4 && lane == 0) {
-        dq_trace(dq.trace, 9, n);
+        dq_trace(dq.trace, 9, n, dq.trace_cta);
         mbar_arrive(ds_ready);
         for (int m = n; m <= (n == nt - 1 ? n + 1 : n); ++m) {
           const uint8_t* ch = ring + (m % kRing3) * kChunkBytes;
@@ -1367,9 +1370,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
     }
     // ---- dQu / dQv epilogue: rows of this lane quarter, columns [32 half, +32)
-    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 0);
+    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 0, dq.trace_cta);
     mbar_wait(dq_full, 0);
-    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 1);
+    if (r == 0 && half == 0) dq_trace(dq.trace, 10, 1, dq.trace_cta);
     tc_fence_after();
     uint32_t v[32];
     const int64_t orow = ((int64_t)hb * p.T + i) * 64 + 32 * half;
@@ -1437,7 +1440,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) dq_trace(dq.trace, 10, 2);
+  if (threadIdx.x == 0) dq_trace(dq.trace, 10, 2, dq.trace_cta);
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
@@ -1964,10 +1967,9 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   static unsigned long long* trace = nullptr;
   const bool tr = getenv("RP_XL_DQ_TRACE") != nullptr;
   if (tr) {
-    if (!trace) cudaMalloc(&trace, 12 * 32 * 8);
+    if (!trace) cudaMalloc(&trace, 11 * 32 * 8);
     cudaMemsetAsync(trace, 0, 11 * 32 * 8, st);
-    const unsigned long long cta = (unsigned long long)atoi(getenv("RP_XL_DQ_TRACE"));
-    cudaMemcpyAsync(trace + 11 * 32, &cta, 8, cudaMemcpyHostToDevice, st);
+    q.trace_cta = atoi(getenv("RP_XL_DQ_TRACE"));
     q.trace = trace;
   }
   xl_attn_bwd_dq_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mac, mp, q);
