@@ -1444,6 +1444,411 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
+// Persistent form of xl_attn_bwd_dq for the production path (no dAC; D rows
+// from xl_d_rows): one CTA per SM walks the (head*batch, query tile) items in
+// the heavy-first order, with the TMA / MMA / softmax pipelines running on
+// across items.  The per-CTA overhead of the one-item kernel -- ~5 us from
+// CTA start to the first tile (first TMA on each descriptor, D-row loads under
+// full-GPU traffic) and ~4-6 us of epilogue -- was a third of each ~30 us CTA
+// (RP_XL_DQ_TRACE); here the producer fetches the next item's dO / v / P
+// tiles while the softmax warps finish the current item.  The arithmetic and
+// every store are those of xl_attn_bwd_dq_kernel (bitwise equal outputs).
+__global__ void d_rows_kernel(const __nv_bfloat16* __restrict__ gctx, const __nv_bfloat16* __restrict__ ctx,
+                              float* __restrict__ d_rows, int B, int T, int H, int d) {
+  // D[(h*B + b)*T + i] = g_ctx[b*T + i, h*64 : +64] . ctx[same], in bwd_dq's order
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)H * B * T) return;
+  const int hb = (int)(idx / T), i = (int)(idx - (int64_t)hb * T), h = hb / B, b = hb - h * B;
+  const int64_t mo = ((int64_t)b * T + i) * d + h * 64;
+  const uint4* g4 = reinterpret_cast<const uint4*>(gctx + mo);
+  const uint4* c4 = reinterpret_cast<const uint4*>(ctx + mo);
+  float D = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 gu = g4[c], cu = c4[c];
+    const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, cw[4] = {cu.x, cu.y, cu.z, cu.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[e]));
+      const float2 cf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cw[e]));
+      D = fmaf(gf.x, cf.x, D);
+      D = fmaf(gf.y, cf.y, D);
+    }
+  }
+  d_rows[idx] = D;
+}
+
+struct DqItem {
+  int hb, qt, h, b, i0, jt_lo, jt_hi, nt, P0;
+};
+
+__device__ __forceinline__ DqItem dq_item(const BwdParams& p, int it) {
+  DqItem w;
+  const int nhb = p.H * p.B;
+  w.qt = p.heavy_first ? p.nqt - 1 - it / nhb : it % p.nqt;
+  w.hb = p.heavy_first ? it % nhb : it / p.nqt;
+  w.h = w.hb / p.B;
+  w.b = w.hb % p.B;
+  w.i0 = w.qt * kQT;
+  const int imax = min(w.i0 + kQT, p.T) - 1;
+  w.jt_lo = p.lo / kKT;
+  w.jt_hi = min(p.M + imax, p.Kl - 1) / kKT;
+  w.nt = w.jt_hi - w.jt_lo + 1;
+  w.P0 = p.T - kQT - w.i0 + w.jt_lo * kKT;
+  return w;
+}
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    xl_attn_bwd_dq_persist_kernel(const __grid_constant__ CUtensorMap mG, const __grid_constant__ CUtensorMap mV,
+                                  const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mR,
+                                  const __grid_constant__ CUtensorMap mBD, const __grid_constant__ CUtensorMap mP,
+                                  const DqParams dq) {
+  const BwdParams& p = dq.b;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sG = smem;
+  uint8_t* sV = smem + 16384;
+  uint8_t* sK = smem + 2 * 16384;
+  uint8_t* sR = smem + 3 * 16384;
+  uint8_t* sP = smem + 4 * 16384;
+  uint8_t* ring = sP + kChunkBytes;
+  uint8_t* sA = ring + kRing3 * kChunkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kChunkBytes);
+  uint64_t* g_full = bars;
+  uint64_t* g_empty = bars + 1;
+  uint64_t* v_full = bars + 2;
+  uint64_t* v_empty = bars + 3;
+  uint64_t* acc_full = bars + 4;   // [2]
+  uint64_t* acc_empty = bars + 6;  // [2]
+  uint64_t* kr_full = bars + 8;
+  uint64_t* kr_empty = bars + 9;
+  uint64_t* ds_ready = bars + 10;
+  uint64_t* ring_free = bars + 11;  // [3]
+  uint64_t* dq_full = bars + 14;
+  uint64_t* dq_empty = bars + 15;
+  uint64_t* p_full = bars + 16;   // [2]
+  uint64_t* p_empty = bars + 18;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  auto pbuf = [&](int g) -> uint8_t* { return (g & 1) ? sA : sP; };
+  const int n_items = p.H * p.B * p.nqt;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mG);
+    tma_prefetch(&mV);
+    tma_prefetch(&mK);
+    tma_prefetch(&mR);
+    tma_prefetch(&mBD);
+    tma_prefetch(&mP);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(g_full, 1);
+    mbar_init(g_empty, 1);
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kSoftWarps * 32);
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], 1);
+    }
+    mbar_init(kr_full, 1);
+    mbar_init(kr_empty, 1);
+    mbar_init(ds_ready, 1);
+    for (int c = 0; c < kRing3; ++c) mbar_init(&ring_free[c], 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, kSoftWarps * 32);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t t_dqu = tmem_base + 256, t_dqv = tmem_base + 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (runs ahead across items) ----------------
+      int gt = 0, gk = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        const DqItem w = dq_item(p, it);
+        mbar_wait(g_empty, (li & 1) ^ 1);  // the previous item's last dP has read dO
+        mbar_expect_tx(g_full, 16384);
+        tma_atoms<1>(sG, &mG, g_full, kQT, w.i0, w.hb);
+        for (int n = 0; n <= w.nt; ++n) {
+          if (n < w.nt) {
+            mbar_wait(v_empty, (gt & 1) ^ 1);
+            mbar_expect_tx(v_full, 16384);
+            tma_atoms<1>(sV, &mV, v_full, kKT, (w.jt_lo + n) * kKT, w.hb);
+            const int pb = gt & 1;
+            mbar_wait(&p_empty[pb], ((gt >> 1) & 1) ^ 1);
+            dq_trace(dq.trace, 1, gt, dq.trace_cta);
+            mbar_expect_tx(&p_full[pb], kChunkBytes);
+            tma_load_3d(pbuf(gt), &mP, &p_full[pb], (w.jt_lo + n) * kKT, w.i0, w.hb);
+            tma_load_3d(pbuf(gt) + 128 * 128, &mP, &p_full[pb], (w.jt_lo + n) * kKT + 64, w.i0, w.hb);
+            ++gt;
+          }
+          // K tile n and the relative-encoding rows of band chunk n; after the
+          // item's last tile only the rows of chunk nt
+          mbar_wait(kr_empty, (gk & 1) ^ 1);
+          mbar_expect_tx(kr_full, n < w.nt ? 32768 : 16384);
+          if (n < w.nt) tma_load_3d(sK, &mK, kr_full, 0, (w.jt_lo + n) * kKT, w.hb);
+          tma_load_3d(sR, &mR, kr_full, 0, w.P0 + kKT * n, w.h);
+          ++gk;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t id_dp = umma_idesc(false, false, false, kQT, kKT);
+      const uint32_t id_dq = umma_idesc(false, false, true, kQT, 64);
+      const uint32_t ga = smem_u32(sG), ka = smem_u32(sK), ra = smem_u32(sR), vb = smem_u32(sV);
+      const uint32_t rg = smem_u32(ring);
+      int gt = 0, gk = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        const DqItem w = dq_item(p, it);
+        const int gt0 = gt;  // the item's first tile
+        auto issue_dq = [&](int n) {
+          const int g = gt0 + n;
+          if (n == 0) mbar_wait(dq_empty, (li & 1) ^ 1);  // the previous item's dQ read out
+          mbar_wait(ds_ready, g & 1);
+          dq_trace(dq.trace, 2, g, dq.trace_cta);
+          mbar_wait(kr_full, gk & 1);
+          tc_fence_after();
+          const uint32_t ch = rg + (uint32_t)((n % kRing3) * kChunkBytes), aa = smem_u32(pbuf(g));
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc_mma<false>(t_dqu, atom_desc<1>(aa, kQT, k), umma_desc(ka + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, (n | k) != 0);
+          tc_commit(&p_empty[g & 1]);
+          tc_commit(&ring_free[n % kRing3]);
+          tc_commit(kr_empty);
+          ++gk;
+        };
+        mbar_wait(g_full, li & 1);
+        for (int n = 0; n < w.nt; ++n, ++gt) {
+          const int s = gt & 1;
+          mbar_wait(&acc_empty[s], ((gt >> 1) & 1) ^ 1);
+          mbar_wait(v_full, gt & 1);
+          dq_trace(dq.trace, 3, gt, dq.trace_cta);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vb, kKT, k), id_dp, k > 0);
+          tc_commit(v_empty);
+          tc_commit(&acc_full[s]);
+          if (n == w.nt - 1) tc_commit(g_empty);
+          if (n >= 1) issue_dq(n - 1);
+        }
+        issue_dq(w.nt - 1);
+        // band chunk nt (the columns right of the last key tile) is complete with tile nt-1
+        mbar_wait(kr_full, gk & 1);
+        tc_fence_after();
+        const uint32_t ch = rg + (uint32_t)((w.nt % kRing3) * kChunkBytes);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, 1u);
+        tc_commit(kr_empty);
+        ++gk;
+        tc_commit(dq_full);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = 32 * q + lane;
+    const uint32_t tl = tmem_base + (static_cast<uint32_t>(32 * q) << 16);
+    const int rsw = r & 7;
+    int ring_uses[kRing3] = {0, 0, 0};  // dQv commits to each ring slot so far (the MMA issuer's count)
+    int gt = 0, li = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+      const DqItem w = dq_item(p, it);
+      const int i = w.i0 + r;
+      const int jhi = p.M + i;
+      const float D = dq.d_rows[(int64_t)w.hb * p.T + i];
+      // the previous item's band chunk stores have read the ring and its
+      // dQv MMAs are done (dq_full, waited in its epilogue): chunk 0 restarts
+      if (warp == 4 && lane == 0) tma_store_wait_read();
+      named_sync(1, kSoftWarps * 32);
+      auto ring_at = [&](int bc) -> __nv_bfloat16* {  // band column bc of row r
+        return reinterpret_cast<__nv_bfloat16*>(ring + (bc >> 7) % kRing3 * kChunkBytes + sw128_off(r, bc & 127));
+      };
+      const __nv_bfloat16 zb = __float2bfloat16_rn(0.f);
+      auto zero_ring = [&](int c0, int c1) {  // band columns [c0, c1) of row r: 16-byte chunks inside
+        int c = c0;
+        for (; c < c1 && (c & 7); ++c) *ring_at(c) = zb;
+        for (; c + 8 <= c1; c += 8) *reinterpret_cast<uint4*>(ring_at(c)) = make_uint4(0u, 0u, 0u, 0u);
+        for (; c < c1; ++c) *ring_at(c) = zb;
+      };
+      if (half == 0) zero_ring(0, 127 - r);  // band columns before this row's first key (chunk 0)
+      if (r == 0 && half == 0) dq_trace(dq.trace, 4, li, dq.trace_cta);
+      for (int n = 0; n < w.nt; ++n, ++gt) {
+        const int s = gt & 1;
+        const int jt0 = (w.jt_lo + n) * kKT + 64 * half;
+        uint4 pr[2][4];
+        mbar_wait(&p_full[gt & 1], (gt >> 1) & 1);
+        if (r == 0 && half == 0) dq_trace(dq.trace, 5, gt, dq.trace_cta);
+        uint8_t* const tile = pbuf(gt);
+        {
+          const uint8_t* prow_s = tile + half * (128 * 128) + r * 128;
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) pr[k][c] = *reinterpret_cast<const uint4*>(prow_s + (((4 * k + c) ^ rsw) << 4));
+        }
+        mbar_wait(&acc_full[s], (gt >> 1) & 1);
+        tc_fence_after();
+        uint32_t dp[2][32];
+        tmem_ld32(tl + s * kKT + 64 * half, dp[0]);
+        tmem_ld32(tl + s * kKT + 64 * half + 32, dp[1]);
+        tc_fence_before();
+        mbar_arrive(&acc_empty[s]);
+        if (r == 0 && half == 0) dq_trace(dq.trace, 6, gt, dq.trace_cta);
+        // the upper band chunk of this tile is reused from tile n - 2 of this
+        // item, whose dQv MMA must be done
+        if (n >= 2) {
+          const int slot = (n + 1) % kRing3;
+          mbar_wait(&ring_free[slot], (ring_uses[slot] - 1) & 1);
+        }
+        if (r == 0 && half == 0) dq_trace(dq.trace, 7, gt, dq.trace_cta);
+        if (lane == 0) tma_store_wait_read();
+        __syncwarp();
+        uint8_t* arow_s = tile + half * (128 * 128) + r * 128;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int jb = jt0 + 32 * k;
+          uint32_t o[16];
+          const bool inside = jb >= p.lo && jb + 31 <= jhi;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t wv[4] = {pr[k][c].x, pr[k][c].y, pr[k][c].z, pr[k][c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+              const int t = 8 * c + 2 * e;
+              const int j = jb + t;
+              float a0 = pf.x * (__uint_as_float(dp[k][t]) - D) * p.scale;
+              float a1 = pf.y * (__uint_as_float(dp[k][t + 1]) - D) * p.scale;
+              if (!inside) {
+                a0 = (j >= p.lo && j <= jhi) ? a0 : 0.f;
+                a1 = (j + 1 >= p.lo && j + 1 <= jhi) ? a1 : 0.f;
+              }
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+              o[t >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(arow_s + (((4 * k + c) ^ rsw) << 4)) =
+                make_uint4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+          const int cb = kKT * n + 127 - r + 64 * half + 32 * k;
+          const int split = 64 - (cb & 63);
+          uint8_t* seg0 = ring + ((cb >> 7) % kRing3) * kChunkBytes + ((cb >> 6) & 1) * (128 * 128) + r * 128;
+          const int c1 = cb + split;
+          uint8_t* seg1 = ring + ((c1 >> 7) % kRing3) * kChunkBytes + ((c1 >> 6) & 1) * (128 * 128) + r * 128;
+          const int e0 = cb & 63;
+          auto at = [&](int t) -> uint8_t* {
+            const bool lo = t < split;
+            const int e = lo ? e0 + t : t - split;
+            return (lo ? seg0 : seg1) + ((((e >> 3) ^ rsw) << 4) | ((e & 7) << 1));
+          };
+          if ((cb & 1) == 0) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) *reinterpret_cast<uint32_t*>(at(2 * m)) = o[m];
+          } else {
+            *reinterpret_cast<unsigned short*>(at(0)) = (unsigned short)(o[0] & 0xffffu);
+#pragma unroll
+            for (int m = 0; m < 15; ++m) *reinterpret_cast<uint32_t*>(at(2 * m + 1)) = __byte_perm(o[m], o[m + 1], 0x5432);
+            *reinterpret_cast<unsigned short*>(at(31)) = (unsigned short)(o[15] >> 16);
+          }
+        }
+        if (n == w.nt - 1 && half == 1) zero_ring(kKT * n + 255 - r, kKT * (w.nt + 1));  // after this row's last key
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (warp == 4 && lane == 0) tma_store_wait_read();
+        if (r == 0 && half == 0) dq_trace(dq.trace, 8, gt, dq.trace_cta);
+        named_sync(1, kSoftWarps * 32);
+        if (r == 0 && half == 0) dq_trace(dq.trace, 9, gt, dq.trace_cta);
+        ++ring_uses[n % kRing3];  // the dQv MMA of this tile commits ring_free[n % 3]
+        if (warp == 4 && lane == 0) {
+          mbar_arrive(ds_ready);
+          for (int m = n; m <= (n == w.nt - 1 ? n + 1 : n); ++m) {
+            const uint8_t* ch = ring + (m % kRing3) * kChunkBytes;
+            const int c0 = w.P0 + kKT * m;
+            if (c0 < p.ldp) tma_store_3d(&mBD, ch, c0, w.i0, w.hb);
+            if (c0 + 64 < p.ldp) tma_store_3d(&mBD, ch + 128 * 128, c0 + 64, w.i0, w.hb);
+          }
+        }
+      }
+      // ---- dQu / dQv epilogue: rows of this lane quarter, columns [32 half, +32)
+      mbar_wait(dq_full, li & 1);
+      if (r == 0 && half == 0) dq_trace(dq.trace, 10, li, dq.trace_cta);
+      tc_fence_after();
+      uint32_t vu[32], vv[32];
+      tmem_ld32(tl + 256 + 32 * half, vu);
+      tmem_ld32(tl + 320 + 32 * half, vv);
+      tc_fence_before();
+      mbar_arrive(dq_empty);  // the next item's dQ MMAs may overwrite the accumulators
+      const int64_t orow = ((int64_t)w.hb * p.T + i) * 64 + 32 * half;
+      float4* du = reinterpret_cast<float4*>(dq.gqu + orow);
+      float4* dv = reinterpret_cast<float4*>(dq.gqv + orow);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        du[c] = make_float4(__uint_as_float(vu[4 * c]), __uint_as_float(vu[4 * c + 1]), __uint_as_float(vu[4 * c + 2]),
+                            __uint_as_float(vu[4 * c + 3]));
+        dv[c] = make_float4(__uint_as_float(vv[4 * c]), __uint_as_float(vv[4 * c + 1]), __uint_as_float(vv[4 * c + 2]),
+                            __uint_as_float(vv[4 * c + 3]));
+      }
+      if (dq.bias_part) {
+        float a[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) a[c] = __uint_as_float(vu[c]);
+        const float colsum_u = warp_colsum32(a, lane);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) a[c] = __uint_as_float(vv[c]);
+        const float colsum_v = warp_colsum32(a, lane);
+        // the four lane-quarter warps of this column half, summed in quarter
+        // order through ring chunk 2 (its last reader -- a dBD store or a dQv
+        // MMA of this item -- is done: dq_full, and the stores are waited below)
+        if (warp == 4 && lane == 0) tma_store_wait_read();
+        named_sync(1, kSoftWarps * 32);
+        float* red = reinterpret_cast<float*>(ring + 2 * kChunkBytes);
+        red[((half * 2 + 0) * 4 + q) * 32 + lane] = colsum_u;
+        red[((half * 2 + 1) * 4 + q) * 32 + lane] = colsum_v;
+        named_sync(1, kSoftWarps * 32);
+        if (q == 0) {
+#pragma unroll
+          for (int wq = 0; wq < 2; ++wq) {
+            const float* rr = red + (half * 2 + wq) * 4 * 32 + lane;
+            const float sum = ((rr[0] + rr[32]) + rr[64]) + rr[96];
+            dq.bias_part[(((int64_t)wq * p.B + w.b) * p.nqt + w.qt) * p.H * 64 + w.h * 64 + 32 * half + lane] = sum;
+          }
+        }
+        named_sync(1, kSoftWarps * 32);  // the scratch is read before the next item zeroes the ring
+      }
+    }
+    if (lane == 0) tma_store_wait_all();
+  } else {
+    // warps 2 and 3: the dBD margins outside each item's band chunks (coalesced)
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const DqItem w = dq_item(p, it);
+      const int64_t bl = lmin(lmax(w.P0, 0), p.ldp), br = lmin(lmax((int64_t)w.P0 + kKT * (w.nt + 1), 0), p.ldp);
+      for (int rr = warp - 2; rr < kQT; rr += 2) {
+        __nv_bfloat16* row = p.gbd + ((int64_t)w.hb * p.T + w.i0 + rr) * p.ldp;
+        for (int64_t c = 8 * lane; c < bl; c += 256) *reinterpret_cast<uint4*>(row + c) = make_uint4(0u, 0u, 0u, 0u);
+        for (int64_t c = br + 8 * lane; c < p.ldp; c += 256)
+          *reinterpret_cast<uint4*>(row + c) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
 // Key-major backward of the key-side gradients (head dim 64, bf16; after
 // xl_attn_bwd_dq, which leaves D_i = dO_i . O_i per query row).  Work item =
 // (head*batch, 128-key tile); per query tile that sees the key tile
@@ -1958,6 +2363,78 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   q.bias_part = bias_part;
   q.d_rows = d_rows;
   q.no_dac = gac == nullptr;
+  static int persist = -1;
+  if (persist < 0) {
+    const char* e = getenv("RP_XL_DQ_PERSIST");
+    persist = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (persist && q.no_dac && d_rows) {
+    // the production path: D rows first (one pass over g_ctx / ctx), then the
+    // persistent kernel (one CTA per SM over the (head*batch, query tile) items)
+    if ((reinterpret_cast<uintptr_t>(d_rows) & 3) != 0)
+      return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned D rows");
+    const int64_t rows = HB * Tn;
+    if (rows > 0)
+      d_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(gctx),
+                                                                    static_cast<const __nv_bfloat16*>(ctx), d_rows,
+                                                                    (int)B, (int)Tn, H, H * dh);
+    p.ldp = ldp;
+    p.B = (int)B;
+    p.T = (int)Tn;
+    p.M = (int)M;
+    p.Kl = (int)Kl;
+    p.lo = (int)(M - mem_len);
+    p.nqt = (int)(Tn / kQT);
+    p.heavy_first = xl_heavy_first();
+    p.H = H;
+    p.d = H * dh;
+    p.scale = scale;
+    p.p = static_cast<const __nv_bfloat16*>(probs);
+    p.gbd = static_cast<__nv_bfloat16*>(gbd);
+    q.gqu = gqu;
+    q.gqv = gqv;
+    const int64_t items = HB * p.nqt;
+    if (items <= 0) return RP_OK;
+    static uint64_t attr_p = 0;
+    if (first_on_device(attr_p))
+      cudaFuncSetAttribute(xl_attn_bwd_dq_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
+    static int sms[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (sms[dev & 63] == 0) {
+      int v = 0;
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      sms[dev & 63] = v > 0 ? v : 148;
+    }
+    int64_t grid = std::min<int64_t>(items, sms[dev & 63]);
+    if (const char* e = getenv("RP_XL_DQ_CTAS"))  // tests: fewer CTAs, several items each
+      if (atoi(e) > 0) grid = std::min<int64_t>(grid, atoi(e));
+    static unsigned long long* ptrace = nullptr;
+    const bool tr = getenv("RP_XL_DQ_TRACE") != nullptr;
+    if (tr) {
+      if (!ptrace) cudaMalloc(&ptrace, 11 * 32 * 8);
+      cudaMemsetAsync(ptrace, 0, 11 * 32 * 8, st);
+      q.trace_cta = atoi(getenv("RP_XL_DQ_TRACE"));
+      q.trace = ptrace;
+    }
+    xl_attn_bwd_dq_persist_kernel<<<(unsigned)grid, kThreadsBwd, kDqSmem, st>>>(mg, mv, mk, mr, mbd, mp, q);
+    if (tr) {
+      unsigned long long h[11 * 32];
+      cudaMemcpyAsync(h, ptrace, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      unsigned long long t0 = ~0ull;
+      for (int i = 0; i < 11 * 32; ++i)
+        if (h[i] && h[i] < t0) t0 = h[i];
+      static const char* names[11] = {"-", "P:P", "M:dsrdy", "M:vfull", "S:item", "S:pfull", "S:acc",
+                                      "S:ring", "S:stored", "S:ds", "S:dqfull"};
+      for (int ev = 1; ev < 11; ++ev) {
+        fprintf(stderr, "%-9s", names[ev]);
+        for (int i = 0; i < 32; ++i) fprintf(stderr, " %6.2f", h[ev * 32 + i] ? (h[ev * 32 + i] - t0) * 1e-3 : -1.0);
+        fprintf(stderr, "\n");
+      }
+    }
+    return check_launch("xl_attn_bwd_dq (persistent)");
+  }
   // C3 A/B: without dAC, warps 2-3 zeroing the dBD margins 182 -> 176 us; with dAC 202 -> 208 us
   q.zero_rows = gac != nullptr;
   if (const char* e = getenv("RP_XL_DQ_ZERO_ROWS")) q.zero_rows = atoi(e);

@@ -341,12 +341,15 @@ def test_fused_kv_backward_equals_banded_gemms(B, H, T, M, mem_len, ctas, monkey
     recomputed from P, dP and xl_attn_bwd_dq's D rows, bitwise equal to the
     banded dV / dK GEMMs over P and dAC (the same K = 16 MMA sequence); and
     xl_attn_bwd_dq without dAC leaves dBD / dQu / dQv bitwise unchanged.
-    ctas = 3: the persistent kernel on 3 CTAs, each walking many (key tile,
-    head*batch) items with its pipelines running across item boundaries."""
+    ctas = 3: the persistent kernels (xl_attn_bwd_kv, and xl_attn_bwd_dq
+    without dAC) on 3 CTAs, each walking many items with its pipelines
+    running across item boundaries -- the no-dAC dq outputs are then those of
+    the persistent dq kernel against the one-item kernel's."""
     from paper_1909_06695_b200 import ops
 
     if ctas:
         monkeypatch.setenv("RP_XL_KV_CTAS", str(ctas))
+        monkeypatch.setenv("RP_XL_DQ_CTAS", str(ctas))
 
     dev, dh = "cuda", 64
     g = torch.Generator(device=dev).manual_seed(7 * T + M + mem_len)
