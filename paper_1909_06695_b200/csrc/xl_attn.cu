@@ -1811,11 +1811,11 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         for (int c = 0; c < 32; ++c) a[c] = __uint_as_float(vv[c]);
         const float colsum_v = warp_colsum32(a, lane);
         // the four lane-quarter warps of this column half, summed in quarter
-        // order through ring chunk 2 (its last reader -- a dBD store or a dQv
-        // MMA of this item -- is done: dq_full, and the stores are waited below)
-        if (warp == 4 && lane == 0) tma_store_wait_read();
-        named_sync(1, kSoftWarps * 32);
-        float* red = reinterpret_cast<float*>(ring + 2 * kChunkBytes);
+        // order through ring slot (nt + 1) % 3: it held chunk nt - 2, whose
+        // dBD stores were read before tile nt - 1's barrier and whose dQv MMA
+        // is done (dq_full).  The next item's start barrier orders these reads
+        // before its ring writes.
+        float* red = reinterpret_cast<float*>(ring + ((w.nt + 1) % kRing3) * kChunkBytes);
         red[((half * 2 + 0) * 4 + q) * 32 + lane] = colsum_u;
         red[((half * 2 + 1) * 4 + q) * 32 + lane] = colsum_v;
         named_sync(1, kSoftWarps * 32);
@@ -1827,7 +1827,6 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             dq.bias_part[(((int64_t)wq * p.B + w.b) * p.nqt + w.qt) * p.H * 64 + w.h * 64 + 32 * half + lane] = sum;
           }
         }
-        named_sync(1, kSoftWarps * 32);  // the scratch is read before the next item zeroes the ring
       }
     }
     if (lane == 0) tma_store_wait_all();
