@@ -207,19 +207,28 @@ int rp_xl_attn_bwd(const void* grad_ctx_h, const void* vh, const void* probs, vo
  * grad_qu = dAC kh and grad_qv = dBD r_h, fp32 [H*B*T, dh] -- the two head-dim-wide GEMMs
  * over the dAC / dBD matrices are folded into the kernel (dS stays in shared memory).
  * grad_ac NULL: dAC is not written (rp_xl_attn_bwd_kv forms the key gradient itself);
- * d_rows (or NULL): D_i = <g_ctx_i, ctx_i> per query row, fp32 [H*B*T], for rp_xl_attn_bwd_kv */
+ * d_rows (or NULL): D_i = <g_ctx_i, ctx_i> per query row, fp32 [H*B*T], for rp_xl_attn_bwd_kv.
+ * grad_qkv (or NULL; with grad_ac NULL and d_rows): bf16(grad_qu + grad_qv) goes straight into the
+ * query columns of the merged bf16 g_qkv rows ([B*M memory rows; B*T current rows] x 3*H*dh, the
+ * layout rp_xl_merge_grads writes) instead of grad_qu / grad_qv, which may then be NULL */
 int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
                       void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,
                       float* grad_qv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, float* bias_part, float* d_rows, void* stream);
+                      float scale, float* bias_part, float* d_rows, void* grad_qkv, void* stream);
 /* Key-major key / value gradients (bf16, dh = 64, T % 128 == 0; after rp_xl_attn_bwd_dq with
  * d_rows): one CTA per (head*batch, 128-key tile) recomputes dP = g_ctx_h v^T and dS on the
  * tensor cores and accumulates grad_vh = P^T g_ctx_h and grad_kh = dS^T qu in TMEM, written as
  * bf16 [H*B, M+T, dh] -- bitwise the banded GEMMs over P and dAC it replaces (kernels.bmm,
- * kernels.py:68-81, on the XL score matrices), without the dAC matrix */
+ * kernels.py:68-81, on the XL score matrices), without the dAC matrix.  grad_qkv (or NULL): dK and
+ * dV go straight into the key / value columns of the merged g_qkv rows (as rp_xl_attn_bwd_dq), and
+ * the memory rows' query columns are zeroed -- with rp_xl_attn_bwd_dq's grad_qkv this replaces
+ * rp_xl_merge_grads; grad_kh / grad_vh may then be NULL */
+/* 1 when rp_xl_attn_bwd_dq runs its persistent kernel for the no-dAC path (RP_XL_DQ_PERSIST != 0),
+ * the one that takes grad_qkv */
+int rp_xl_dq_persistent(void);
 int rp_xl_attn_bwd_kv(const void* grad_ctx_h, const void* vh, const void* qu, const void* probs, int64_t ld_p,
                       const float* d_rows, void* grad_kh, void* grad_vh, int64_t B, int64_t T, int64_t M, int32_t H,
-                      int32_t dh, int64_t mem_len, float scale, void* stream);
+                      int32_t dh, int64_t mem_len, float scale, void* grad_qkv, void* stream);
 /* bias_part of rp_xl_attn_bwd_dq (or NULL): per-CTA column sums of grad_qu / grad_qv, which
  * rp_xl_dq_bias_finish turns into the r_w_bias / r_r_bias gradients ([H, 64] each) without
  * re-reading the query gradients (the column sums of rp_xl_bias_grad) */

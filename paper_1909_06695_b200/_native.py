@@ -216,8 +216,9 @@ def _declare(L):
         "rp_xl_softmax_bwd": [i32, vp, i64, vp, i64, vp, vp, i64, i64, i64, i64, f32, vp],
         "rp_xl_attn_fwd_pv": [vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, i64, i32, i32, i64, f32, i32, i64, vp],
         "rp_xl_attn_bwd_dq": [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp,
-                              vp, vp],
-        "rp_xl_attn_bwd_kv": [vp, vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp],
+                              vp, vp, vp],
+        "rp_xl_attn_bwd_kv": [vp, vp, vp, vp, i64, vp, vp, vp, i64, i64, i64, i32, i32, i64, f32, vp, vp],
+        "rp_xl_dq_persistent": [],
         "rp_xl_dq_bias_part_bytes": [i32, i64, i64],
         "rp_xl_dq_bias_finish": [vp, vp, vp, i32, i64, i64, vp],
         "rp_xl_bias_grad_workspace_bytes": [i32, i32],

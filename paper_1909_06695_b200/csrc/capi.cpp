@@ -192,15 +192,16 @@ int rp_xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void
 int rp_xl_attn_bwd_dq(const void* grad_ctx_h, const void* vh, const void* kh, const void* rh, const void* probs,
                       void* grad_ac, void* grad_bd, int64_t ld_p, const void* grad_ctx, const void* ctx, float* grad_qu,
                       float* grad_qv, int64_t B, int64_t T, int64_t M, int32_t H, int32_t dh, int64_t mem_len,
-                      float scale, float* bias_part, float* d_rows, void* stream) {
+                      float scale, float* bias_part, float* d_rows, void* grad_qkv, void* stream) {
   return rp::xl_attn_bwd_dq(grad_ctx_h, vh, kh, rh, probs, grad_ac, grad_bd, ld_p, grad_ctx, ctx, grad_qu, grad_qv, B,
-                            T, M, H, dh, (int)mem_len, scale, RP_S(stream), bias_part, d_rows);
+                            T, M, H, dh, (int)mem_len, scale, RP_S(stream), bias_part, d_rows, grad_qkv);
 }
+int rp_xl_dq_persistent(void) { return rp::xl_dq_persistent() ? 1 : 0; }
 int rp_xl_attn_bwd_kv(const void* grad_ctx_h, const void* vh, const void* qu, const void* probs, int64_t ld_p,
                       const float* d_rows, void* grad_kh, void* grad_vh, int64_t B, int64_t T, int64_t M, int32_t H,
-                      int32_t dh, int64_t mem_len, float scale, void* stream) {
+                      int32_t dh, int64_t mem_len, float scale, void* grad_qkv, void* stream) {
   return rp::xl_attn_bwd_kv(grad_ctx_h, vh, qu, probs, ld_p, d_rows, grad_kh, grad_vh, B, T, M, H, dh, (int)mem_len,
-                            scale, RP_S(stream));
+                            scale, RP_S(stream), grad_qkv);
 }
 int64_t rp_xl_dq_bias_part_bytes(int32_t H, int64_t B, int64_t T) { return rp::xl_dq_bias_part_bytes(H, B, T); }
 int rp_xl_dq_bias_finish(const float* bias_part, float* g_r_w_bias, float* g_r_r_bias, int32_t H, int64_t B, int64_t T,

@@ -704,6 +704,9 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   float* dq_bias = (d.fused & RP_XL_FUSED_DQ) ? static_cast<float*>(bp.take(xl_dq_bias_part_bytes((int)x.H, x.B, x.T)))
                                               : nullptr;
   const bool kv = (d.fused & RP_XL_FUSED_KV) != 0;
+  // the persistent bwd_dq and bwd_kv write straight into the merged g_qkv
+  // rows (no fp32 dQu / dQv, no xl_merge_grads pass)
+  const bool merged = kv && xl_dq_persistent();
   float* d_rows = kv ? static_cast<float*>(bp.take(x.HB * x.T * 4)) : nullptr;
   void* g_r = bp.take(x.Kl * D * e);
   void* g_qkv = bp.take(BK * 3 * D * e);
@@ -738,7 +741,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   bool dq_done = false;
   if (d.fused & RP_XL_FUSED_DQ) {
     RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, kv ? nullptr : g_ac, g_bd, x.ldk, g_ctx, tp.ctx,
-                          g_qu, g_qv, x.B, x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st, dq_bias, d_rows));
+                          g_qu, g_qv, x.B, x.T, x.M, (int)x.H, (int)x.dh, d.mem_len, scale, st, dq_bias, d_rows,
+                          merged ? g_qkv : nullptr));
     dq_done = true;
   } else if (d.fused & RP_XL_FUSED_BWD) {
     RP_TRY(xl_attn_bwd(g_ctx_h, tp.vh, tp.probs, g_ac, g_bd, x.ldk, g_ctx, tp.ctx, x.B, x.T, x.M, (int)x.H, (int)x.dh,
@@ -758,7 +762,7 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   eband.k_lo_off = -x.M;
   if (kv)  // dV = P^T dO and dK = dS^T (q+u) in one key-major kernel (no dAC)
     RP_TRY(xl_attn_bwd_kv(g_ctx_h, tp.vh, tp.qu, tp.probs, x.ldk, d_rows, g_kh, g_vh, x.B, x.T, x.M, (int)x.H,
-                          (int)x.dh, d.mem_len, scale, st));
+                          (int)x.dh, d.mem_len, scale, st, merged ? g_qkv : nullptr));
   else
     RP_TRY(mm(c, bmat(tp.probs, x.HB, x.T, x.Kl, x.ldk, x.T * x.ldk), true,
               bmat(g_ctx_h, x.HB, x.T, x.dh, x.dh, x.T * x.dh), true, bmat(g_vh, x.HB, x.Kl, x.dh, x.dh, x.Kl * x.dh), dt,
@@ -780,7 +784,7 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
     RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
   RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
   RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
-  RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));
+  if (!merged) RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));
   RP_TRY(mm(c, mat(tp.a, BK, D, D), true, mat(g_qkv, BK, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32));
   RP_TRY(mm(c, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32));
   // LN1 over both row blocks: memory rows add to the gain / bias sums only

@@ -132,13 +132,14 @@ int xl_attn_fwd_pv(const void* qu, const void* qv, const void* kh, const void* v
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
                    void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
                    int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st,
-                   float* bias_part = nullptr, float* d_rows = nullptr);
+                   float* bias_part = nullptr, float* d_rows = nullptr, void* gqkv = nullptr);
+bool xl_dq_persistent();  // RP_XL_DQ_PERSIST (default on): the no-dAC bwd_dq runs the persistent kernel
 // key-major dK / dV (dh = 64, T % 128 == 0) from P, g_ctx_h, v, q+u and xl_attn_bwd_dq's D
 // rows: gk = dS^T (q+u), gv = P^T g_ctx_h as bf16 [H*B, Kl, 64] -- bitwise the banded GEMMs
 // over dAC and P, so xl_attn_bwd_dq can skip dAC (gac = NULL)
 int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const void* probs, int64_t ldp,
                    const float* d_rows, void* gk, void* gv, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
-                   float scale, cudaStream_t st);
+                   float scale, cudaStream_t st, void* gqkv = nullptr);
 int64_t xl_dq_bias_part_bytes(int H, int64_t B, int64_t Tn);
 int xl_dq_bias_finish(const float* part, float* gu, float* gv, int H, int64_t B, int64_t Tn, cudaStream_t st);
 // adaptive softmax row movers (adaptive.cu)

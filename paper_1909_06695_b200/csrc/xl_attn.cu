@@ -1011,6 +1011,8 @@ struct DqParams {
   BwdParams b;
   float* gqu;  // [H*B*T, 64] fp32 (rows hb*T + i)
   float* gqv;
+  __nv_bfloat16* gqkv;  // optional (persistent kernel): bf16(dQu + dQv) straight into the merged g_qkv rows
+                        // [B*M memory rows; B*T current rows] x 3d, query columns (xl_merge_grads' arithmetic)
   float* bias_part;  // optional [2][B*nqt][H*64]: per-CTA column sums of dQu (u) and dQv (v) -- a
                      // [rows, cols] block per bias that a column-sum finish reduces
   float* d_rows;     // optional [HB*T]: D_i = dO_i . O_i for xl_attn_bwd_kv
@@ -1792,15 +1794,33 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       tmem_ld32(tl + 320 + 32 * half, vv);
       tc_fence_before();
       mbar_arrive(dq_empty);  // the next item's dQ MMAs may overwrite the accumulators
-      const int64_t orow = ((int64_t)w.hb * p.T + i) * 64 + 32 * half;
-      float4* du = reinterpret_cast<float4*>(dq.gqu + orow);
-      float4* dv = reinterpret_cast<float4*>(dq.gqv + orow);
+      if (dq.gqkv) {
+        // the merged query gradient: bf16(dQu + dQv) in the current row's query columns
+        uint4* dst = reinterpret_cast<uint4*>(
+            dq.gqkv + ((int64_t)p.B * p.M + (int64_t)w.b * p.T + i) * (3 * p.d) + w.h * 64 + 32 * half);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        du[c] = make_float4(__uint_as_float(vu[4 * c]), __uint_as_float(vu[4 * c + 1]), __uint_as_float(vu[4 * c + 2]),
-                            __uint_as_float(vu[4 * c + 3]));
-        dv[c] = make_float4(__uint_as_float(vv[4 * c]), __uint_as_float(vv[4 * c + 1]), __uint_as_float(vv[4 * c + 2]),
-                            __uint_as_float(vv[4 * c + 3]));
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int t = 8 * c + 2 * e;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(vu[t]) + __uint_as_float(vv[t]),
+                                                      __uint_as_float(vu[t + 1]) + __uint_as_float(vv[t + 1]));
+            o4[e] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          dst[c] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        }
+      } else {
+        const int64_t orow = ((int64_t)w.hb * p.T + i) * 64 + 32 * half;
+        float4* du = reinterpret_cast<float4*>(dq.gqu + orow);
+        float4* dv = reinterpret_cast<float4*>(dq.gqv + orow);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          du[c] = make_float4(__uint_as_float(vu[4 * c]), __uint_as_float(vu[4 * c + 1]), __uint_as_float(vu[4 * c + 2]),
+                              __uint_as_float(vu[4 * c + 3]));
+          dv[c] = make_float4(__uint_as_float(vv[4 * c]), __uint_as_float(vv[4 * c + 1]), __uint_as_float(vv[4 * c + 2]),
+                              __uint_as_float(vv[4 * c + 3]));
+        }
       }
       if (dq.bias_part) {
         float a[32];
@@ -1889,6 +1909,8 @@ struct KvParams {
   int T, M, Kl, lo, nkt, HB;
   float scale;
   unsigned long long* trace;  // RP_XL_KV_TRACE: CTA 0's event times (diagnostics)
+  __nv_bfloat16* gqkv;  // optional: dK / dV straight into the merged g_qkv rows (key / value columns)
+  int B, d;
 };
 
 __device__ __forceinline__ void kv_trace(const KvParams& p, int ev, int idx) {
@@ -2166,8 +2188,14 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       tc_fence_before();
       mbar_arrive(&kv_empty[kb]);
       if (j < p.Kl) {
-        uint4* dst =
-            reinterpret_cast<uint4*>((part < 2 ? p.gv : p.gk) + ((int64_t)hb * p.Kl + j) * 64 + 32 * (part & 1));
+        uint4* dst;
+        if (p.gqkv) {  // merged rows: memory rows b*M + j, then current rows B*M + b*T + (j - M)
+          const int h = hb / p.B, b = hb - h * p.B;
+          const int64_t row = j < p.M ? (int64_t)b * p.M + j : (int64_t)p.B * p.M + (int64_t)b * p.T + (j - p.M);
+          dst = reinterpret_cast<uint4*>(p.gqkv + row * (3 * p.d) + (part < 2 ? 2 : 1) * p.d + h * 64 + 32 * (part & 1));
+        } else {
+          dst = reinterpret_cast<uint4*>((part < 2 ? p.gv : p.gk) + ((int64_t)hb * p.Kl + j) * 64 + 32 * (part & 1));
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t ob[4];
@@ -2316,10 +2344,19 @@ int xl_attn_bwd(const void* gctx_h, const void* vh, const void* probs, void* gac
   return check_launch("xl_attn_bwd");
 }
 
+bool xl_dq_persistent() {
+  static int persist = -1;
+  if (persist < 0) {
+    const char* e = getenv("RP_XL_DQ_PERSIST");
+    persist = (e && e[0] == '0') ? 0 : 1;
+  }
+  return persist == 1;
+}
+
 int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const void* rh, const void* probs, void* gac,
                    void* gbd, int64_t ldp, const void* gctx, const void* ctx, float* gqu, float* gqv, int64_t B,
                    int64_t Tn, int64_t M, int H, int dh, int mem_len, float scale, cudaStream_t st, float* bias_part,
-                   float* d_rows) {
+                   float* d_rows, void* gqkv) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: head dim must be 64 (got %d)", dh);
   if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: T must be a multiple of 128");
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
@@ -2362,11 +2399,13 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
   q.bias_part = bias_part;
   q.d_rows = d_rows;
   q.no_dac = gac == nullptr;
-  static int persist = -1;
-  if (persist < 0) {
-    const char* e = getenv("RP_XL_DQ_PERSIST");
-    persist = (e && e[0] == '0') ? 0 : 1;
-  }
+  const bool persist = xl_dq_persistent();
+  q.gqkv = static_cast<__nv_bfloat16*>(gqkv);
+  if (gqkv && !(persist && q.no_dac && d_rows))
+    return set_error(RP_ERR_INVALID, "xl_attn_bwd_dq: merged query-gradient rows need the persistent kernel "
+                                     "(no dAC, D rows, RP_XL_DQ_PERSIST != 0)");
+  if (gqkv && (reinterpret_cast<uintptr_t>(gqkv) & 15) != 0)
+    return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned merged rows");
   if (persist && q.no_dac && d_rows) {
     // the production path: D rows first (one pass over g_ctx / ctx), then the
     // persistent kernel (one CTA per SM over the (head*batch, query tile) items)
@@ -2467,14 +2506,14 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
 
 int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const void* probs, int64_t ldp,
                    const float* d_rows, void* gk, void* gv, int64_t B, int64_t Tn, int64_t M, int H, int dh, int mem_len,
-                   float scale, cudaStream_t st) {
+                   float scale, cudaStream_t st, void* gqkv) {
   if (dh != 64) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: head dim must be 64 (got %d)", dh);
   if (Tn % 128 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: T must be a multiple of 128");
   const int64_t Kl = M + Tn, HB = (int64_t)H * B;
   if (ldp < Kl || ldp % 8 != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: ldp must be >= M+T, multiple of 8");
   if (mem_len < 0 || mem_len > M) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: mem_len out of range");
-  if (!d_rows || !gk || !gv) return set_error(RP_ERR_INVALID, "xl_attn_bwd_kv: null output or D rows");
-  for (const void* q : {probs, gctx_h, vh, qu, (const void*)gk, (const void*)gv})
+  if (!d_rows || (!gqkv && (!gk || !gv))) return set_error(RP_ERR_INVALID, "xl_attn_bwd_kv: null output or D rows");
+  for (const void* q : {probs, gctx_h, vh, qu, gqkv ? gqkv : (const void*)gk, gqkv ? gqkv : (const void*)gv})
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: unaligned operand");
   CUtensorMap mg, mv, mu, mp;
   RP_TRY0(tma_map_bf16(&mp, probs, ldp, Tn, ldp, HB, Tn * ldp, 64, kQT));
@@ -2495,6 +2534,14 @@ int xl_attn_bwd_kv(const void* gctx_h, const void* vh, const void* qu, const voi
   p.nkt = (int)((Kl + kKT - 1) / kKT);
   p.HB = (int)HB;
   p.scale = scale;
+  p.gqkv = static_cast<__nv_bfloat16*>(gqkv);
+  p.B = (int)B;
+  p.d = H * dh;
+  if (gqkv && B * M > 0) {
+    // the memory rows carry no query gradient: zero their query columns
+    if (cudaMemset2DAsync(gqkv, (size_t)3 * p.d * 2, 0, (size_t)p.d * 2, (size_t)(B * M), st) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "xl_attn_bwd_kv: memset of the memory rows' query gradient");
+  }
   const int64_t items = HB * p.nkt;
   if (items <= 0) return RP_OK;
   if (items >= (1LL << 31)) return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_kv: too many key tiles");

@@ -489,20 +489,28 @@ def xl_attn_fwd_pv(qu, qv, kh, vh, rh, probs, ctx, B, T, M, mem_len, scale):
 
 
 def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_qv, B, T, M, mem_len, scale,
-                   bias_part=None, d_rows=None):
+                   bias_part=None, d_rows=None, g_qkv=None):
     """xl_attn_bwd plus the query gradients on the tensor cores (dh = 64,
     T % 128 == 0): g_qu = dAC kh, g_qv = dBD r_h written as fp32 [H*B*T, dh].
     g_ac None: dAC is not written (xl_attn_bwd_kv forms dK itself); d_rows:
-    fp32 [H*B*T] receives D_i = <g_ctx_i, ctx_i> for xl_attn_bwd_kv."""
-    _require_cuda(g_ctx_h, vh, kh, rh, probs, g_bd, g_ctx, ctx, g_qu, g_qv)
-    if d_rows is not None and (d_rows.dtype != torch.float32 or d_rows.numel() < g_qu.shape[0] * g_qu.shape[1]
+    fp32 [H*B*T] receives D_i = <g_ctx_i, ctx_i> for xl_attn_bwd_kv.  g_qkv
+    (with g_ac None and d_rows): bf16(dQu + dQv) straight into the merged
+    [B*(M+T), 3d] query-gradient columns instead of g_qu / g_qv (then None)."""
+    _require_cuda(g_ctx_h, vh, kh, rh, probs, g_bd, g_ctx, ctx)
+    if g_qkv is not None:
+        _require_cuda(g_qkv)
+        if g_qkv.dtype != torch.bfloat16 or not g_qkv.is_contiguous():
+            raise DimensionError("xl_attn_bwd_dq: g_qkv is contiguous bf16 [B*(M+T), 3d]")
+    else:
+        _require_cuda(g_qu, g_qv)
+    if d_rows is not None and (d_rows.dtype != torch.float32 or d_rows.numel() < g_ctx_h.shape[0] * g_ctx_h.shape[1]
                                or not d_rows.is_contiguous()):
         raise DimensionError("xl_attn_bwd_dq: d_rows is a contiguous fp32 [H*B*T] buffer")
     for t in (g_ctx_h, vh, kh, rh, probs, g_bd, g_ctx, ctx) + ((g_ac,) if g_ac is not None else ()):
         if t.dtype != torch.bfloat16:
             raise DimensionError("xl_attn_bwd_dq takes bf16 operands")
     for t in (g_qu, g_qv):
-        if t.dtype != torch.float32 or not t.is_contiguous():
+        if t is not None and (t.dtype != torch.float32 or not t.is_contiguous()):
             raise DimensionError("xl_attn_bwd_dq writes contiguous fp32 query gradients")
     for t in (g_ctx_h, vh, kh, rh, g_ctx, ctx):
         if not t.is_contiguous():
@@ -511,21 +519,25 @@ def xl_attn_bwd_dq(g_ctx_h, vh, kh, rh, probs, g_ac, g_bd, g_ctx, ctx, g_qu, g_q
     if (g_ac is not None and g_ac.stride(-2) != ldp) or g_bd.stride(-2) != ldp:
         raise DimensionError("xl_attn_bwd_dq: P, dAC and dBD must share the row pitch")
     H, dh = g_ctx.shape[-1] // vh.shape[-1], vh.shape[-1]
-    _count(1)
+    _count(2 if d_rows is not None and g_ac is None and N.lib().rp_xl_dq_persistent() else 1)  # + the D-rows kernel
     N.check(N.lib().rp_xl_attn_bwd_dq(_ptr(g_ctx_h), _ptr(vh), _ptr(kh), _ptr(rh), _ptr(probs), _ptr(g_ac),
                                       _ptr(g_bd), ldp, _ptr(g_ctx), _ptr(ctx), _ptr(g_qu), _ptr(g_qv), B, T, M, H, dh,
-                                      mem_len, scale, _ptr(bias_part), _ptr(d_rows), _stream()), "xl_attn_bwd_dq")
+                                      mem_len, scale, _ptr(bias_part), _ptr(d_rows), _ptr(g_qkv), _stream()),
+            "xl_attn_bwd_dq")
 
 
-def xl_attn_bwd_kv(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh, B, T, M, mem_len, scale):
+def xl_attn_bwd_kv(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh, B, T, M, mem_len, scale, g_qkv=None):
     """Key-major dK / dV (dh = 64, T % 128 == 0; after xl_attn_bwd_dq with
     d_rows): g_vh = P^T g_ctx_h and g_kh = dS^T qu as bf16 [H*B, M+T, dh],
-    bitwise the banded GEMMs over P and dAC."""
-    _require_cuda(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh)
-    for t in (g_ctx_h, vh, qu, probs, g_kh, g_vh):
+    bitwise the banded GEMMs over P and dAC.  g_qkv: into the merged
+    [B*(M+T), 3d] key / value columns instead (g_kh / g_vh None), the memory
+    rows' query columns zeroed."""
+    outs = (g_qkv,) if g_qkv is not None else (g_kh, g_vh)
+    _require_cuda(g_ctx_h, vh, qu, probs, d_rows, *outs)
+    for t in (g_ctx_h, vh, qu, probs) + outs:
         if t.dtype != torch.bfloat16:
             raise DimensionError("xl_attn_bwd_kv takes bf16 operands")
-    for t in (g_ctx_h, vh, qu, g_kh, g_vh, d_rows):
+    for t in (g_ctx_h, vh, qu, d_rows) + outs:
         if not t.is_contiguous():
             raise DimensionError("xl_attn_bwd_kv operands must be contiguous")
     if d_rows.dtype != torch.float32:
@@ -534,7 +546,7 @@ def xl_attn_bwd_kv(g_ctx_h, vh, qu, probs, d_rows, g_kh, g_vh, B, T, M, mem_len,
     H = vh.numel() // (B * (M + T) * dh)
     _count(1)
     N.check(N.lib().rp_xl_attn_bwd_kv(_ptr(g_ctx_h), _ptr(vh), _ptr(qu), _ptr(probs), probs.stride(-2), _ptr(d_rows),
-                                      _ptr(g_kh), _ptr(g_vh), B, T, M, H, dh, mem_len, scale, _stream()),
+                                      _ptr(g_kh), _ptr(g_vh), B, T, M, H, dh, mem_len, scale, _ptr(g_qkv), _stream()),
             "xl_attn_bwd_kv")
 
 

@@ -278,6 +278,10 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     bias_part = None
     kv = fused_kv_ok(tp)
     d_rows = ws.get("xl_d_rows", (H * B * T,), torch.float32) if kv else None
+    # the persistent bwd_dq and bwd_kv write straight into the merged g_qkv rows
+    # (no fp32 dQu / dQv, no merge pass)
+    merged = kv and bool(N.lib().rp_xl_dq_persistent())
+    g_qkv = ws.get_rows("xl_g_qkv", (B * Kl, 3 * d), cdt)
     if fused_dq_ok(tp):
         # dP, dS, dAC / dBD and dQu = dAC k, dQv = dBD r in one kernel (csrc/xl_attn.cu),
         # plus the per-CTA column sums of dQu / dQv for the u / v gradients; with
@@ -285,7 +289,8 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
         bias_part = ws.get("xl_dq_bias", (ops.xl_dq_bias_part_elems(H, B, T),), torch.float32)
         with ops.span("xl_attn_bwd"):
             ops.xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs_buf, None if kv else g_ac, g_bd, g_ctx, tp.ctx,
-                               g_qu, g_qv, B, T, M, tp.mem_len, scale, bias_part=bias_part, d_rows=d_rows)
+                               None if merged else g_qu, None if merged else g_qv, B, T, M, tp.mem_len, scale,
+                               bias_part=bias_part, d_rows=d_rows, g_qkv=g_qkv if merged else None)
         dq_done = True
     elif fused_bwd_ok(tp):
         # dP on the tensor cores, dS, dAC and the un-shifted dBD in one kernel (csrc/xl_attn.cu)
@@ -305,8 +310,9 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
         # dV = P^T dO and dK = dS^T (q+u) in one key-major kernel: bitwise the two
         # banded GEMMs below, without the dAC matrix
         with ops.span("xl_attn_bwd"):
-            ops.xl_attn_bwd_kv(g3, tp.vh.view(H * B, Kl, dh), tp.qu.view(H * B, T, dh), tp.probs_buf, d_rows, g_kh,
-                               g_vh, B, T, M, tp.mem_len, scale)
+            ops.xl_attn_bwd_kv(g3, tp.vh.view(H * B, Kl, dh), tp.qu.view(H * B, T, dh), tp.probs_buf, d_rows,
+                               None if merged else g_kh, None if merged else g_vh, B, T, M, tp.mem_len, scale,
+                               g_qkv=g_qkv if merged else None)
     else:
         ops.gemm(tp.probs, g3, a_mn=True, b_mn=True, out=g_vh, k_lo_off=band)
     g_ac, g_bd = g_ac[:, :, :Kl], g_bd[:, :, :Kl]
@@ -330,8 +336,8 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     g_r = ws.get_rows("xl_g_r", (Kl, d), cdt)
     ops.xl_merge_heads(g_rh, g_r, H, dh)
     _bg(R, g_r, a_mn=True, b_mn=True, out=G["wr"])
-    g_qkv = ws.get_rows("xl_g_qkv", (B * Kl, 3 * d), cdt)
-    ops.xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh)
+    if not merged:
+        ops.xl_merge_grads(g_qu, g_qv, g_kh, g_vh, g_qkv, B, T, M, H, dh)
     _bg(tp.a, g_qkv, a_mn=True, b_mn=True, out=G["wqkv"])
     g_a = ws.get("xl_g_a", (B * Kl, d), torch.float32)
     _bg(g_qkv, W["wqkv"], out=g_a)
