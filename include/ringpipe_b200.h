@@ -130,8 +130,9 @@ int rp_tf32_split(const float* x, float* hi, float* lo, int64_t rows, int64_t co
  * gain/bias are fp32. */
 int rp_layernorm_fwd(int32_t dtype, const void* x, const float* gain, const float* bias, void* y, float* mean,
                      float* rstd, int64_t rows, int64_t d, int64_t ld_x, int64_t ld_y, int32_t* flag, void* stream);
-/* dx = LN-backward(dy) + resid_grad (fp32); dx_masked = dx*dropout-mask (dtype) if non-NULL;
- * writes rp_layernorm_bwd_blocks(rows) partial rows of dgain/dbias. */
+/* dx = LN-backward(dy) + resid_grad (fp32), or not written when dx is NULL (rows that only add to
+ * the gain / bias sums, as XL's stop-gradient memory rows); dx_masked = dx*dropout-mask (dtype) if
+ * non-NULL; writes rp_layernorm_bwd_blocks(rows) partial rows of dgain/dbias. */
 int rp_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
                      const float* gain, const float* resid_grad, float* dx, void* dx_masked, uint64_t seed,
                      uint64_t threshold, float scale, int32_t drop_enabled, float* partial_gain,

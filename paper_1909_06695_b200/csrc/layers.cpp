@@ -576,7 +576,7 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   if (d.fused & RP_XL_FUSED_DQ) bwd += al256(xl_dq_bias_part_bytes((int)x.H, x.B, x.T));
   if (d.fused & RP_XL_FUSED_KV) bwd += al256(x.HB * x.T * 4);  // D rows
   bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
-  bwd += al256(x.B * x.Kl * x.D * 4) + al256(x.B * x.M * x.D * 4);  // g_a, g_mem
+  bwd += al256(x.B * x.Kl * x.D * 4);  // g_a
   bwd += al256(kBlockSplitK);
   b = std::max(fwd, bwd);
   // tf32x3 split scratch: the largest operand of any contraction of the block,
@@ -711,7 +711,6 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   void* g_r = bp.take(x.Kl * D * e);
   void* g_qkv = bp.take(BK * 3 * D * e);
   float* g_a = static_cast<float*>(bp.take(BK * D * 4));
-  float* g_mem = static_cast<float*>(bp.take(BM * D * 4 + 4));
   Ctx c{dt, st};
   c.max_ctas = d.max_ctas;
   c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
@@ -789,7 +788,8 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   RP_TRY(mm(c, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32));
   // LN1 over both row blocks: memory rows add to the gain / bias sums only
   if (x.M)
-    RP_TRY(layernorm_bwd(dt, g_a, tp.xa, tp.mean1, tp.rstd1, w.ln1_g, nullptr, g_mem, nullptr, 0, 0, 1.f, 0,
+    // the memory rows take no gradient (stop-gradient): only their gain / bias sums, no dx
+    RP_TRY(layernorm_bwd(dt, g_a, tp.xa, tp.mean1, tp.rstd1, w.ln1_g, nullptr, nullptr, nullptr, 0, 0, 1.f, 0,
                          pg + (int64_t)nbl_cur * D, pb + (int64_t)nbl_cur * D, BM, D, st));
   RP_TRY(layernorm_bwd(dt, g_a + BM * D, static_cast<const char*>(tp.xa) + BM * D * e, tp.mean1 + BM, tp.rstd1 + BM,
                        w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));

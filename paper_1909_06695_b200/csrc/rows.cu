@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_v4_kernel(
       float o[VW];
 #pragma unroll
       for (int q = 0; q < VW; ++q) o[q] = rs * (dyv[i][q] * gq[q] - s1 - xh[i][q] * s2) + r4[q];
-      VecIO<float, VW>::st(dx + row * d + j, o);
+      if (dx) VecIO<float, VW>::st(dx + row * d + j, o);  // NULL: only the gain / bias sums (XL memory rows)
       if (dx_masked) {
         if (drop_on) {
 #pragma unroll
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kRowThreads, NG == 1 ? 4 : NG == 2 ? 3 : 2) ln
       float o[VW];
 #pragma unroll
       for (int q = 0; q < VW; ++q) o[q] = rs * (dyv[i][q] * gv[i][q] - s1 - xh[i][q] * s2) + rv[i][q];
-      VecIO<float, VW>::st(dx + row * d + j, o);
+      if (dx) VecIO<float, VW>::st(dx + row * d + j, o);  // NULL: only the gain / bias sums (XL memory rows)
       if (dx_masked) {
         if (drop_on) {
 #pragma unroll
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
       if (j < d) {
         float o = rs * (dyv[i] * gv[i] - s1 - xh[i] * s2);
         if (resid_grad) o += resid_grad[row * d + j];
-        dx[row * d + j] = o;
+        if (dx) dx[row * d + j] = o;
         if (dx_masked) {
           float mo = o;
           if (drop_on) mo = dropout_keep(seed, (uint64_t)row * d + j, thr) ? o * scale : 0.f;

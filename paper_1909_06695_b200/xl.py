@@ -342,10 +342,10 @@ def xl_block_backward_ops(W, vecs, tp, R, g_out, g_x, G, drop, ws, rows_total=0)
     g_a = ws.get("xl_g_a", (B * Kl, d), torch.float32)
     _bg(g_qkv, W["wqkv"], out=g_a)
     # LN1 over both row blocks: memory rows add to the gain / bias sums only
+    # (stop-gradient: no dx is written for them)
     BM = B * M
     if M:
-        g_mem = ws.get("xl_g_mem", (BM, d), torch.float32)
-        ops.layernorm_bwd(g_a[:BM], tp.xa[:BM], tp.mean1[:BM], tp.rstd1[:BM], vecs["ln1_g"], g_mem,
+        ops.layernorm_bwd(g_a[:BM], tp.xa[:BM], tp.mean1[:BM], tp.rstd1[:BM], vecs["ln1_g"], None,
                           pg[nbl_cur:], pb[nbl_cur:])
     ops.layernorm_bwd(g_a[BM:], tp.xa[BM:], tp.mean1[BM:], tp.rstd1[BM:], vecs["ln1_g"], g_x, pg[:nbl_cur],
                       pb[:nbl_cur], resid_grad=g_x1)
