@@ -1011,6 +1011,7 @@ struct DqParams {
   BwdParams b;
   float* gqu;  // [H*B*T, 64] fp32 (rows hb*T + i)
   float* gqv;
+  int d_in_kernel;      // persistent kernel: warps 2-3 compute the D rows (no separate D pass)
   __nv_bfloat16* gqkv;  // optional (persistent kernel): bf16(dQu + dQv) straight into the merged g_qkv rows
                         // [B*M memory rows; B*T current rows] x 3d, query columns (xl_merge_grads' arithmetic)
   float* bias_part;  // optional [2][B*nqt][H*64]: per-CTA column sums of dQu (u) and dQv (v) -- a
@@ -1530,7 +1531,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   uint64_t* dq_empty = bars + 15;
   uint64_t* p_full = bars + 16;   // [2]
   uint64_t* p_empty = bars + 18;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* d_ready = bars + 20;  // [2]: an item's D rows written (warps 2-3)
+  uint64_t* d_taken = bars + 22;  // [2]: and read by the softmax warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   auto pbuf = [&](int g) -> uint8_t* { return (g & 1) ? sA : sP; };
   const int n_items = p.H * p.B * p.nqt;
 
@@ -1560,6 +1563,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     for (int c = 0; c < kRing3; ++c) mbar_init(&ring_free[c], 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, kSoftWarps * 32);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&d_ready[s], 64);
+      mbar_init(&d_taken[s], kSoftWarps * 32);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -1670,7 +1677,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       const DqItem w = dq_item(p, it);
       const int i = w.i0 + r;
       const int jhi = p.M + i;
-      const float D = dq.d_rows[(int64_t)w.hb * p.T + i];
+      float D;
+      if (dq.d_in_kernel) {  // written by warps 2-3 (one item ahead), read here
+        mbar_wait(&d_ready[li & 1], (li >> 1) & 1);
+        D = *reinterpret_cast<volatile const float*>(dq.d_rows + (int64_t)w.hb * p.T + i);
+        mbar_arrive(&d_taken[li & 1]);
+      } else {
+        D = dq.d_rows[(int64_t)w.hb * p.T + i];
+      }
       // the previous item's band chunk stores have read the ring and its
       // dQv MMAs are done (dq_full, waited in its epilogue): chunk 0 restarts
       if (warp == 4 && lane == 0) tma_store_wait_read();
@@ -1851,9 +1865,37 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     }
     if (lane == 0) tma_store_wait_all();
   } else {
-    // warps 2 and 3: the dBD margins outside each item's band chunks (coalesced)
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    // warps 2 and 3: each item's D rows (one item ahead of the softmax warps:
+    // D_i = g_ctx_i . ctx_i, bwd_dq's arithmetic, into d_rows for bwd_kv as
+    // well), then the dBD margins outside its band chunks (coalesced)
+    int li = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
       const DqItem w = dq_item(p, it);
+      if (dq.d_in_kernel) {
+        if (li >= 2) mbar_wait(&d_taken[li & 1], ((li >> 1) - 1) & 1);  // bounded lookahead: the barrier's phase
+        for (int rr = (warp - 2) * 32 + lane; rr < kQT; rr += 64) {
+          const int i = w.i0 + rr;
+          const int64_t mo = ((int64_t)w.b * p.T + i) * p.d + w.h * 64;
+          const uint4* g4 = reinterpret_cast<const uint4*>(p.gctx + mo);
+          const uint4* c4 = reinterpret_cast<const uint4*>(p.ctx + mo);
+          float D = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 gu = g4[c], cu = c4[c];
+            const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, cw[4] = {cu.x, cu.y, cu.z, cu.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[e]));
+              const float2 cf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cw[e]));
+              D = fmaf(gf.x, cf.x, D);
+              D = fmaf(gf.y, cf.y, D);
+            }
+          }
+          dq.d_rows[(int64_t)w.hb * p.T + i] = D;
+        }
+        __threadfence_block();
+        mbar_arrive(&d_ready[li & 1]);
+      }
       const int64_t bl = lmin(lmax(w.P0, 0), p.ldp), br = lmin(lmax((int64_t)w.P0 + kKT * (w.nt + 1), 0), p.ldp);
       for (int rr = warp - 2; rr < kQT; rr += 2) {
         __nv_bfloat16* row = p.gbd + ((int64_t)w.hb * p.T + w.i0 + rr) * p.ldp;
@@ -2412,7 +2454,9 @@ int xl_attn_bwd_dq(const void* gctx_h, const void* vh, const void* kh, const voi
     if ((reinterpret_cast<uintptr_t>(d_rows) & 3) != 0)
       return set_error(RP_ERR_DIMENSION, "xl_attn_bwd_dq: unaligned D rows");
     const int64_t rows = HB * Tn;
-    if (rows > 0)
+    static const int d_sep = getenv("RP_XL_DQ_DPASS") ? atoi(getenv("RP_XL_DQ_DPASS")) : 0;  // 1: separate D pass
+    q.d_in_kernel = d_sep ? 0 : 1;
+    if (rows > 0 && d_sep)
       d_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(gctx),
                                                                     static_cast<const __nv_bfloat16*>(ctx), d_rows,
                                                                     (int)B, (int)Tn, H, H * dh);
