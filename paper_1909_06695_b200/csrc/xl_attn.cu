@@ -1579,7 +1579,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (runs ahead across items) ----------------
-      int gt = 0, gk = 0, li = 0;
+      int gt = 0, gk = 0, gv = 0, li = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
         const DqItem w = dq_item(p, it);
         mbar_wait(g_empty, (li & 1) ^ 1);  // the previous item's last dP has read dO
@@ -1587,9 +1587,10 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tma_atoms<1>(sG, &mG, g_full, kQT, w.i0, w.hb);
         for (int n = 0; n <= w.nt; ++n) {
           if (n < w.nt) {
-            mbar_wait(v_empty, (gt & 1) ^ 1);
+            mbar_wait(v_empty, (gv & 1) ^ 1);
             mbar_expect_tx(v_full, 16384);
             tma_atoms<1>(sV, &mV, v_full, kKT, (w.jt_lo + n) * kKT, w.hb);
+            ++gv;
             const int pb = gt & 1;
             mbar_wait(&p_empty[pb], ((gt >> 1) & 1) ^ 1);
             dq_trace(dq.trace, 1, gt, dq.trace_cta);
@@ -1598,13 +1599,23 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             tma_load_3d(pbuf(gt) + 128 * 128, &mP, &p_full[pb], (w.jt_lo + n) * kKT + 64, w.i0, w.hb);
             ++gt;
           }
-          // K tile n and the relative-encoding rows of band chunk n; after the
-          // item's last tile only the rows of chunk nt
-          mbar_wait(kr_empty, (gk & 1) ^ 1);
-          mbar_expect_tx(kr_full, n < w.nt ? 32768 : 16384);
-          if (n < w.nt) tma_load_3d(sK, &mK, kr_full, 0, (w.jt_lo + n) * kKT, w.hb);
-          tma_load_3d(sR, &mR, kr_full, 0, w.P0 + kKT * n, w.h);
-          ++gk;
+          if (n < w.nt) {
+            // K tile n and the relative-encoding rows of band chunk n
+            mbar_wait(kr_empty, (gk & 1) ^ 1);
+            mbar_expect_tx(kr_full, 32768);
+            tma_load_3d(sK, &mK, kr_full, 0, (w.jt_lo + n) * kKT, w.hb);
+            tma_load_3d(sR, &mR, kr_full, 0, w.P0 + kKT * n, w.h);
+            ++gk;
+          } else {
+            // the rows of the last band chunk nt go into the v tile, free once
+            // the item's last dP has read it: they no longer queue behind the
+            // last tile's dQ MMAs on the single K / R buffer (the item's dQ
+            // read-out waited ~2 us for them)
+            mbar_wait(v_empty, (gv & 1) ^ 1);
+            mbar_expect_tx(v_full, 16384);
+            tma_load_3d(sV, &mR, v_full, 0, w.P0 + kKT * n, w.h);
+            ++gv;
+          }
         }
       }
     }
@@ -1615,7 +1626,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       const uint32_t id_dq = umma_idesc(false, false, true, kQT, 64);
       const uint32_t ga = smem_u32(sG), ka = smem_u32(sK), ra = smem_u32(sR), vb = smem_u32(sV);
       const uint32_t rg = smem_u32(ring);
-      int gt = 0, gk = 0, li = 0;
+      int gt = 0, gk = 0, gv = 0, li = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
         const DqItem w = dq_item(p, it);
         const int gt0 = gt;  // the item's first tile
@@ -1642,27 +1653,29 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         for (int n = 0; n < w.nt; ++n, ++gt) {
           const int s = gt & 1;
           mbar_wait(&acc_empty[s], ((gt >> 1) & 1) ^ 1);
-          mbar_wait(v_full, gt & 1);
+          mbar_wait(v_full, gv & 1);
           dq_trace(dq.trace, 3, gt, dq.trace_cta);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             tc_mma<false>(tmem_base + s * kKT, atom_desc<1>(ga, kQT, k), atom_desc<1>(vb, kKT, k), id_dp, k > 0);
           tc_commit(v_empty);
+          ++gv;
           tc_commit(&acc_full[s]);
           if (n == w.nt - 1) tc_commit(g_empty);
           if (n >= 1) issue_dq(n - 1);
         }
         issue_dq(w.nt - 1);
-        // band chunk nt (the columns right of the last key tile) is complete with tile nt-1
-        mbar_wait(kr_full, gk & 1);
+        // band chunk nt (the columns right of the last key tile) is complete with
+        // tile nt-1; its relative-encoding rows are in the v tile
+        mbar_wait(v_full, gv & 1);
         tc_fence_after();
         const uint32_t ch = rg + (uint32_t)((w.nt % kRing3) * kChunkBytes);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(ra + k * 2048, 16384, 1024), id_dq, 1u);
-        tc_commit(kr_empty);
-        ++gk;
+          tc_mma<false>(t_dqv, atom_desc<1>(ch, kQT, k), umma_desc(vb + k * 2048, 16384, 1024), id_dq, 1u);
+        tc_commit(v_empty);
+        ++gv;
         tc_commit(dq_full);
       }
     }
