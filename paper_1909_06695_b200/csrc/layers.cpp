@@ -577,7 +577,7 @@ int64_t xl_block_workspace_bytes(const rp_xl_block_desc& d) {
   if (d.fused & RP_XL_FUSED_KV) bwd += al256(x.HB * x.T * 4);  // D rows
   bwd += al256(x.Kl * x.D * e) + al256(x.B * x.Kl * 3 * x.D * e);  // g_r, g_qkv
   bwd += al256(x.B * x.Kl * x.D * 4);  // g_a
-  bwd += al256(kBlockSplitK);
+  bwd += al256(kBlockSplitK) * 2;  // main + side stream partials
   b = std::max(fwd, bwd);
   // tf32x3 split scratch: the largest operand of any contraction of the block,
   // rows padded to 4 floats (split_into)
@@ -715,27 +715,53 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   c.max_ctas = d.max_ctas;
   c.splitk = static_cast<float*>(bp.take(kBlockSplitK));
   c.splitk_cap = kBlockSplitK;
+  float* splitk_side = static_cast<float*>(bp.take(kBlockSplitK));
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
   const int64_t ld_part = std::max(F, 3 * D);
+  // weight-gradient GEMMs on a side stream beside their input-gradient twins
+  // (bf16; the block backward's pairing, bitwise the serial order)
+  const bool fork = dt == RP_BF16 && fork_enabled();
+  SideStream* ss = fork ? &side_for(st) : nullptr;
+  Ctx cs = c;
+  if (fork) {
+    cs.st = ss->s;
+    cs.splitk = splitk_side;
+  }
+  auto pair = [&](auto&& first, auto&& second) -> int {
+    if (!fork) {
+      RP_TRY(first(c));
+      return second(c);
+    }
+    if (cudaEventRecord(ss->fork, st) != cudaSuccess || cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "xl_block_backward: fork failed");
+    RP_TRY(second(cs));
+    RP_TRY(first(c));
+    if (cudaEventRecord(ss->join, ss->s) != cudaSuccess || cudaStreamWaitEvent(st, ss->join, 0) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "xl_block_backward: join failed");
+    return RP_OK;
+  };
   // feed-forward + LN2 (as the reference block)
   RP_TRY(mask_grad(dt, g_out, g_h2, N, D, d.drop_seed, static_cast<uint64_t>(n), d.drop_threshold, d.drop_scale,
                    d.drop_enabled, pm, st));
-  RP_TRY(mm(c, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32));
   Epi er;
   er.kind = d.activation == 1 ? RP_EPI_GELU_GRAD : RP_EPI_RELU_GRAD;
   er.resid = d.activation == 1 ? tp.z1 : tp.h1;
   er.ld_resid = F;
-  RP_TRY(mm(c, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er));
-  RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, st));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_h2, N, D, D), false, mat(w.w2, F, D, D), false, mat(g_z1, N, F, F), dt, er); },
+              [&](Ctx& x) { return mm(x, mat(tp.h1, N, F, F), true, mat(g_h2, N, D, D), true, mat(G.w2, F, D, D), RP_F32); }));
   (void)ld_part;
-  RP_TRY(mm(c, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32));
-  RP_TRY(mm(c, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32));
+  // b1 partial sums ride with dW1 on the side stream (both only read g_z1)
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_z1, N, F, F), false, mat(w.w1, D, F, F), false, mat(g_m, N, D, D), RP_F32); },
+              [&](Ctx& x) {
+                RP_TRY(colsum_partial(dt, g_z1, N, F, F, part, x.st));
+                return mm(x, mat(tp.m, N, D, D), true, mat(g_z1, N, F, F), true, mat(G.w1, D, F, F), RP_F32);
+              }));
   RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
                        d.drop_threshold, d.drop_scale, d.drop_enabled, pg2, pb2, N, D, st));
   // relative-position attention
-  RP_TRY(mm(c, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32));
-  RP_TRY(mm(c, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt));
+  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt); },
+              [&](Ctx& x) { return mm(x, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32); }));
   RP_TRY(xl_split_heads(dt, g_ctx, D, dt, g_ctx_h, N, (int)x.H, (int)x.dh, st));
   bool dq_done = false;
   if (d.fused & RP_XL_FUSED_DQ) {
@@ -784,8 +810,9 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
   RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
   if (!merged) RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));
-  RP_TRY(mm(c, mat(tp.a, BK, D, D), true, mat(g_qkv, BK, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32));
-  RP_TRY(mm(c, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32));
+  RP_TRY(pair(
+      [&](Ctx& x) { return mm(x, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32); },
+      [&](Ctx& x) { return mm(x, mat(tp.a, BK, D, D), true, mat(g_qkv, BK, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32); }));
   // LN1 over both row blocks: memory rows add to the gain / bias sums only
   if (x.M)
     // the memory rows take no gradient (stop-gradient): only their gain / bias sums, no dx
