@@ -814,12 +814,18 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
       [&](Ctx& x) { return mm(x, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32); },
       [&](Ctx& x) { return mm(x, mat(tp.a, BK, D, D), true, mat(g_qkv, BK, 3 * D, 3 * D), true, mat(G.wqkv, D, 3 * D, 3 * D), RP_F32); }));
   // LN1 over both row blocks: memory rows add to the gain / bias sums only
-  if (x.M)
-    // the memory rows take no gradient (stop-gradient): only their gain / bias sums, no dx
-    RP_TRY(layernorm_bwd(dt, g_a, tp.xa, tp.mean1, tp.rstd1, w.ln1_g, nullptr, nullptr, nullptr, 0, 0, 1.f, 0,
-                         pg + (int64_t)nbl_cur * D, pb + (int64_t)nbl_cur * D, BM, D, st));
-  RP_TRY(layernorm_bwd(dt, g_a + BM * D, static_cast<const char*>(tp.xa) + BM * D * e, tp.mean1 + BM, tp.rstd1 + BM,
-                       w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, st));
+  // the memory rows take no gradient (stop-gradient): only their gain / bias
+  // sums, no dx -- on the side stream beside the current rows' LN1 backward
+  RP_TRY(pair(
+      [&](Ctx& x) {
+        return layernorm_bwd(dt, g_a + BM * D, static_cast<const char*>(tp.xa) + BM * D * e, tp.mean1 + BM,
+                             tp.rstd1 + BM, w.ln1_g, g_x1, g_x, nullptr, 0, 0, 1.f, 0, pg, pb, N, D, x.st);
+      },
+      [&](Ctx& x) {
+        return BM ? layernorm_bwd(dt, g_a, tp.xa, tp.mean1, tp.rstd1, w.ln1_g, nullptr, nullptr, nullptr, 0, 0, 1.f,
+                                  0, pg + (int64_t)nbl_cur * D, pb + (int64_t)nbl_cur * D, BM, D, x.st)
+                  : (int)RP_OK;
+      }));
   const int nq = (int)(x.B * (x.T / 128));  // the fused backward's [B*nqt, H*64] bias partials
   const ColsumJob jobs[8] = {{pm, nbm, D, G.b2}, {part, nbc, F, G.b1}, {pg2, nbl_cur, D, G.ln2_g},
                              {pb2, nbl_cur, D, G.ln2_b}, {pg, nbl_cur + nbl_mem, D, G.ln1_g},
