@@ -605,13 +605,25 @@ int xl_block_forward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, co
   c.split_base = bp.base + bp.off;
   c.split_cap = ws_bytes - bp.off;
   const int64_t BK = x.B * x.Kl;
+  // the relative-encoding projection (independent of the block input) on the
+  // side stream beside LN1 and the QKV projection (bf16; joined before the scores)
+  const bool fork = dt == RP_BF16 && fork_enabled();
+  SideStream* ss = fork ? &side_for(st) : nullptr;
+  Ctx cs = c;
+  if (fork) {
+    cs.st = ss->s;
+    if (cudaEventRecord(ss->fork, st) != cudaSuccess || cudaStreamWaitEvent(ss->s, ss->fork, 0) != cudaSuccess)
+      return set_error(RP_ERR_CUDA, "xl_block_forward: fork failed");
+  }
+  RP_TRY(mm(cs, mat(R, x.Kl, x.D, x.D), false, mat(w.wr, x.D, x.D, x.D), true, mat(r, x.Kl, x.D, x.D), dt));
+  RP_TRY(xl_split_heads(dt, r, x.D, dt, tp.rh, x.Kl, (int)x.H, (int)x.dh, cs.st));
   RP_TRY(layernorm_fwd(dt, tp.xa, w.ln1_g, w.ln1_b, tp.a, tp.mean1, tp.rstd1, BK, x.D, flag, st));
   RP_TRY(mm(c, mat(tp.a, BK, x.D, x.D), false, mat(w.wqkv, x.D, 3 * x.D, 3 * x.D), true,
             mat(tp.qkv, BK, 3 * x.D, 3 * x.D), dt));
   RP_TRY(xl_split_qkv(dt, tp.qkv, w.r_w_bias, w.r_r_bias, tp.qu, tp.qv, tp.kh, tp.vh, x.B, x.T, x.M, (int)x.H,
                       (int)x.dh, st));
-  RP_TRY(mm(c, mat(R, x.Kl, x.D, x.D), false, mat(w.wr, x.D, x.D, x.D), true, mat(r, x.Kl, x.D, x.D), dt));
-  RP_TRY(xl_split_heads(dt, r, x.D, dt, tp.rh, x.Kl, (int)x.H, (int)x.dh, st));
+  if (fork && (cudaEventRecord(ss->join, ss->s) != cudaSuccess || cudaStreamWaitEvent(st, ss->join, 0) != cudaSuccess))
+    return set_error(RP_ERR_CUDA, "xl_block_forward: join failed");
   bool pv_done = false;
   if (d.fused & RP_XL_FUSED_PV) {
     RP_TRY(xl_attn_fwd_pv(tp.qu, tp.qv, tp.kh, tp.vh, tp.rh, tp.probs, x.ldk, tp.ctx, x.B, x.T, x.M, (int)x.H,
