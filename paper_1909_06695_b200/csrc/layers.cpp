@@ -797,7 +797,23 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   Epi eband;
   eband.k_lo = (d.fused & RP_XL_BANDED) ? 1 : 0;
   eband.k_lo_off = -x.M;
-  if (kv)  // dV = P^T dO and dK = dS^T (q+u) in one key-major kernel (no dAC)
+  // the production path: the key-major dK / dV kernel on this stream, the
+  // relative-encoding chain (dR GEMM over dBD, head merge, dWr) on the side
+  // stream -- they share no operand
+  const bool rel_side = kv && dq_done && dq_bias;
+  if (rel_side) {
+    RP_TRY(pair(
+        [&](Ctx& cx) {
+          return xl_attn_bwd_kv(g_ctx_h, tp.vh, tp.qu, tp.probs, x.ldk, d_rows, g_kh, g_vh, x.B, x.T, x.M, (int)x.H,
+                                (int)x.dh, d.mem_len, scale, cx.st, merged ? g_qkv : nullptr);
+        },
+        [&](Ctx& cx) {
+          RP_TRY(mm(cx, bmat(g_bd, x.H, N, x.Kl, x.ldk, N * x.ldk), true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh),
+                    true, bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+          RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, cx.st));
+          return mm(cx, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32);
+        }));
+  } else if (kv)  // dV = P^T dO and dK = dS^T (q+u) in one key-major kernel (no dAC)
     RP_TRY(xl_attn_bwd_kv(g_ctx_h, tp.vh, tp.qu, tp.probs, x.ldk, d_rows, g_kh, g_vh, x.B, x.T, x.M, (int)x.H,
                           (int)x.dh, d.mem_len, scale, st, merged ? g_qkv : nullptr));
   else
@@ -815,12 +831,14 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   if (!dq_done)
     RP_TRY(mm(c, gbd, false, bmat(tp.rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), true,
               bmat(g_qv, x.H, N, x.dh, x.dh, N * x.dh), RP_F32));
-  RP_TRY(mm(c, gbd, true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh), true, bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh),
-            RP_F32));
-  if (!dq_bias)  // else: the fused backward's column sums, finished with the others below
-    RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
-  RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
-  RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
+  if (!rel_side) {
+    RP_TRY(mm(c, gbd, true, bmat(tp.qv, x.H, N, x.dh, x.dh, N * x.dh), true,
+              bmat(g_rh, x.H, x.Kl, x.dh, x.dh, x.Kl * x.dh), RP_F32));
+    if (!dq_bias)  // else: the fused backward's column sums, finished with the others below
+      RP_TRY(xl_bias_grad(g_qu, g_qv, bias_ws, G.r_w_bias, G.r_r_bias, (int)x.H, N, (int)x.dh, st));
+    RP_TRY(xl_merge_heads(RP_F32, g_rh, dt, g_r, D, x.Kl, (int)x.H, (int)x.dh, st));
+    RP_TRY(mm(c, mat(R, x.Kl, D, D), true, mat(g_r, x.Kl, D, D), true, mat(G.wr, D, D, D), RP_F32));
+  }
   if (!merged) RP_TRY(xl_merge_grads(dt, g_qu, g_qv, g_kh, g_vh, g_qkv, x.B, x.T, x.M, (int)x.H, (int)x.dh, st));
   RP_TRY(pair(
       [&](Ctx& x) { return mm(x, mat(g_qkv, BK, 3 * D, 3 * D), false, mat(w.wqkv, D, 3 * D, 3 * D), false, mat(g_a, BK, D, D), RP_F32); },
