@@ -772,9 +772,12 @@ int xl_block_backward(const rp_xl_block_desc& d, const rp_xl_block_weights& w, c
   RP_TRY(layernorm_bwd(dt, g_m, tp.x1, tp.mean2, tp.rstd2, w.ln2_g, g_out, g_x1, g_proj, d.drop_seed,
                        d.drop_threshold, d.drop_scale, d.drop_enabled, pg2, pb2, N, D, st));
   // relative-position attention
-  RP_TRY(pair([&](Ctx& x) { return mm(x, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt); },
-              [&](Ctx& x) { return mm(x, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32); }));
-  RP_TRY(xl_split_heads(dt, g_ctx, D, dt, g_ctx_h, N, (int)x.H, (int)x.dh, st));
+  RP_TRY(pair(
+      [&](Ctx& cx) {
+        RP_TRY(mm(cx, mat(g_proj, N, D, D), false, mat(w.wo, D, D, D), false, mat(g_ctx, N, D, D), dt));
+        return xl_split_heads(dt, g_ctx, D, dt, g_ctx_h, N, (int)x.H, (int)x.dh, cx.st);  // beside dWo too
+      },
+      [&](Ctx& cx) { return mm(cx, mat(tp.ctx, N, D, D), true, mat(g_proj, N, D, D), true, mat(G.wo, D, D, D), RP_F32); }));
   bool dq_done = false;
   if (d.fused & RP_XL_FUSED_DQ) {
     RP_TRY(xl_attn_bwd_dq(g_ctx_h, tp.vh, tp.kh, tp.rh, tp.probs, kv ? nullptr : g_ac, g_bd, x.ldk, g_ctx, tp.ctx,
